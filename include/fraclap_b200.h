@@ -1,0 +1,196 @@
+/*
+ * fraclap_b200 — C ABI of the B200 (sm_100a) implementation of the dense hot path of
+ * Ainsworth & Glusa's FEM for the integral fractional Laplacian (reference package
+ * `fraclap`, /root/reference/pkg/src/fraclap).
+ *
+ * The path:  assemble_dense (assembly.py:1059-1104)  ->  pcg with the dense matvec
+ *            `lambda x: Ad @ x` (solve.py:27-32, 52-109).
+ *
+ * Conventions
+ *   - Plain pointers + int64 sizes, row-major, no torch types.  Host arrays are BORROWED
+ *     for the duration of a call.  `fl_dense` OWNS its device matrix and workspaces.
+ *   - Every entry point returns 0 (FL_OK) or a negative FL_E_* code; `fl_last_error()`
+ *     returns a thread-local message for the last failure.  No partial outputs on error.
+ *   - The mapping of codes onto the reference's exceptions is 1:1:
+ *       FL_E_ARG      -> ValueError      (assembly.py:59-60, mesh.py:208-209)
+ *       FL_E_ASSEMBLY -> AssemblyError   (assembly.py:1062-1063, :871)
+ *       FL_E_QUAD     -> QuadratureError (quadrature.py:157-158, :405-406)
+ *       FL_E_SOLVER   -> SolverError     (solve.py:67-68, :87-88)
+ *       FL_E_CUDA / FL_E_OOM -> RuntimeError
+ */
+#ifndef FRACLAP_B200_H
+#define FRACLAP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FL_ABI_VERSION 1
+
+#define FL_OK 0
+#define FL_E_ARG (-1)
+#define FL_E_ASSEMBLY (-2)
+#define FL_E_QUAD (-3)
+#define FL_E_SOLVER (-4)
+#define FL_E_CUDA (-5)
+#define FL_E_OOM (-6)
+
+/* kernel variants (assembly.py:47-50) */
+#define FL_VARIANT_INTEGRAL 0
+#define FL_VARIANT_REGIONAL 1
+#define FL_VARIANT_SYMMETRIZED 2 /* refused with FL_E_ASSEMBLY: out of scope */
+
+/* rule-table topologies (quadrature.py:38-46) plus the two per-cell rules */
+#define FL_TOPO_IDENTICAL 0
+#define FL_TOPO_COMMON_EDGE 1
+#define FL_TOPO_COMMON_VERTEX 2
+#define FL_TOPO_DISJOINT 3      /* ONE-cell simplex_rule(d,k) (quadrature.py:81-85) */
+#define FL_TOPO_EDGE_OF_CELL 4
+#define FL_TOPO_TOUCHING_EDGE 5
+#define FL_TOPO_CELL 6          /* cell rule XQ_ORDER[d] (assembly.py:282-298, :635) */
+#define FL_TOPO_EDGE_GL 7       /* GL rule of order EDGE_GL_ORDER on [0,1] (assembly.py:43) */
+#define FL_NTOPO 8
+#define FL_KDIR 33              /* k = 0..32 (K_MAX = 32, quadrature.py:35) */
+#define FL_NODE_STRIDE 8        /* doubles per packed node record */
+
+/* Mesh input contract (mesh.py:24-197).  `boundary_normals` are OUTWARD unit normals. */
+typedef struct fl_mesh {
+  int32_t d;                        /* 1 or 2 */
+  int32_t pad_;
+  int64_t nv, nc, nb;
+  const double* vertices;           /* (nv, d) */
+  const int64_t* cells;             /* (nc, d+1); in 2D CCW with the refinement edge first */
+  const int64_t* boundary_edges;    /* (nb, d) */
+  const double* boundary_normals;   /* (nb, d) outward */
+} fl_mesh;
+
+/* DofMap (mesh.py:200-240): vertex -> dof, -1 for a non-DoF vertex. */
+typedef struct fl_dofmap {
+  int64_t n;
+  const int64_t* vertex_to_dof;     /* (nv,) */
+} fl_dofmap;
+
+/* FractionalKernel (assembly.py:66-94).  C_ds = normalisation(d, s) (assembly.py:57-63). */
+typedef struct fl_kernel {
+  int32_t d;
+  int32_t variant;
+  double s;
+  double C_ds;
+} fl_kernel;
+
+/* OrderParams (quadrature.py:115-131) with alpha already resolved by target_alpha(d, s). */
+typedef struct fl_order_params {
+  double rho1, rho2, rho3, rho4;
+  double C_offset;
+  double alpha;
+} fl_order_params;
+
+/* Packed quadrature tables, built host-side from the same Gauss-Legendre / Gauss-Jacobi
+ * node sets the reference uses (quadrature.py:53-420).  `dir` has FL_NTOPO*FL_KDIR*2 int64:
+ * dir[2*(topo*FL_KDIR+k)+0] = first node, dir[...+1] = node count (0: rule absent).  Node
+ * records are FL_NODE_STRIDE doubles in `data`:
+ *   IDENTICAL / COMMON_EDGE / COMMON_VERTEX : x0 x1 y0 y1 w           (1D: x y in slots 0/2)
+ *   EDGE_OF_CELL / TOUCHING_EDGE            : x0 x1 a w               (1D: x in slot 0)
+ *   DISJOINT (one cell, order k)            : u0 u1 w lw0 lw1 lw2     (lw_a = lambda_a(u) w)
+ *   CELL                                    : u0 u1 w lam0 lam1 lam2
+ *   EDGE_GL                                 : t w
+ * IDENTICAL 1D and EDGE_OF_CELL 1D ignore k and are stored at k = 0. */
+typedef struct fl_tables {
+  const int64_t* dir;
+  const double* data;
+  int64_t ndata;                    /* doubles in data */
+} fl_tables;
+
+typedef struct fl_dense fl_dense;   /* opaque: device rows [row_begin,row_end) x n of A */
+
+typedef struct fl_solve_report {
+  int64_t iterations;
+  double residual;                  /* sqrt|r.z| / sqrt|r0.z0| (solve.py:104) */
+  double seconds;
+  int32_t converged;
+  int32_t pad_;
+  double true_residual;             /* ||b - A x|| / ||b||, reported beside the reference's */
+} fl_solve_report;
+
+typedef struct fl_assembly_stats {
+  /* element-pair quadratures, counted as the reference does */
+  int64_t pairs_identical, pairs_touching, pairs_cross, pairs_tail;
+  int64_t pairs_boundary_singular, pairs_boundary_flux;
+  /* kernel evaluations (quadrature node pairs) actually performed */
+  double evals_cross, evals_tail, evals_singular, evals_boundary;
+  /* device milliseconds per phase (CUDA events on the assembly stream) */
+  double ms_prep, ms_singular, ms_tail, ms_cross, ms_local, ms_total;
+  int64_t cross_tile_pairs;
+  int32_t ncolors, ntiles;
+} fl_assembly_stats;
+
+/* ---------------------------------------------------------------- library */
+int32_t fl_abi_version(void);
+const char* fl_last_error(void);
+int32_t fl_device_count(void);
+
+/* ------------------------------------------------------------- assembly
+ * Replaces assembly.assemble_dense (assembly.py:1059-1104) for the rows
+ * [row_begin, row_end) of the (n x n) matrix; (0, n) = the whole matrix.
+ * n_limit reproduces the refusal at assembly.py:1062-1063 (pass <0 to disable).
+ * stream: a cudaStream_t (NULL = the library's own stream). */
+int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap,
+                          const fl_kernel* kernel, const fl_order_params* params,
+                          const fl_tables* tables, int64_t n_limit,
+                          int64_t row_begin, int64_t row_end,
+                          int32_t device, void* stream, fl_dense** out);
+
+/* Wrap an existing dense host matrix (n x n, row-major) as a device operator — the
+ * `Ad = np.asarray(A)` branch of LinearOperatorHandle.from_matrix (solve.py:31-32). */
+int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out);
+
+void fl_dense_free(fl_dense* A);
+int32_t fl_dense_info(const fl_dense* A, int64_t* n, int64_t* row_begin, int64_t* row_end,
+                      double** device_ptr);
+int32_t fl_dense_stats(const fl_dense* A, fl_assembly_stats* stats);
+/* copy the owned rows (row-major, (row_end-row_begin) x n) to host memory */
+int32_t fl_dense_to_host(const fl_dense* A, double* host_rows);
+/* diagonal entries of the owned rows (host) */
+int32_t fl_dense_diag(const fl_dense* A, double* host_diag);
+
+/* ------------------------------------------------------------- matvec
+ * y[rows] = A[rows, :] @ x  (solve.py:31-32).  ptr_kind 0: host pointers, 1: device. */
+int32_t fl_matvec(const fl_dense* A, const double* x, double* y, int32_t ptr_kind);
+/* device-pointer matvec on an explicit stream (used by the sharded CG) */
+int32_t fl_matvec_async(const fl_dense* A, const double* x_dev, double* y_dev, void* stream);
+
+/* ------------------------------------------------------------- solve
+ * Jacobi-preconditioned CG of solve.pcg (solve.py:52-109) on a whole-matrix fl_dense.
+ * precond: 0 none, 1 jacobi.  x0 may be NULL.  b, x0, x are host arrays of length n. */
+int32_t fl_pcg(const fl_dense* A, const double* b, const double* x0, double tol,
+               int64_t max_iter, int32_t precond, double* x, fl_solve_report* report);
+
+/* Fused CG vector step on device pointers for the sharded solver (rows of one shard):
+ *   x += alpha p; r -= alpha Ap; z = minv * r; partial[0] = r.z   (deterministic)    */
+int32_t fl_cg_update_async(int64_t m, double alpha, double* x, double* r, double* z,
+                           const double* p, const double* Ap, const double* minv,
+                           double* partial_dev, void* stream);
+/* partial_dev[0] = a.b over m entries (deterministic fixed-order reduction) */
+int32_t fl_dot_async(int64_t m, const double* a, const double* b, double* out_dev, void* stream);
+/* p = z + beta p */
+int32_t fl_xpby_async(int64_t m, const double* z, double beta, double* p, void* stream);
+
+/* ------------------------------------------------------------- parity / diagnostics
+ * Per-pair Gauss orders exactly as select_order computes them (quadrature.py:138-179):
+ *   cross_k[a*nc+b] (a<b disjoint, assembly.py:705-706), tail_k[t*nc+s] (C_offset-4,
+ *   assembly.py:997, :1010-1012); 0 elsewhere.  Host int8 arrays of nc*nc. */
+int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                        const fl_order_params* params, int32_t device,
+                        int8_t* cross_k, int8_t* tail_k);
+/* Touching pairs as classify/canonicalize produce them (assembly.py:412-473):
+ * host outputs sized by *npairs (call with pairs==NULL first to get the count). */
+int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                          const fl_order_params* params, int32_t device, int64_t* npairs,
+                          int64_t* pairs, int32_t* topo, int32_t* k, int32_t* ident_k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FRACLAP_B200_H */

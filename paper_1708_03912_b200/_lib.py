@@ -1,0 +1,160 @@
+"""ctypes binding of libfraclap_b200.so (include/fraclap_b200.h).
+
+There is no CPU fallback: if the shared library is missing or cannot be loaded, every
+entry point raises.  Error codes map 1:1 onto the reference's exceptions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libfraclap_b200.so")
+
+FL_OK, FL_E_ARG, FL_E_ASSEMBLY, FL_E_QUAD, FL_E_SOLVER, FL_E_CUDA, FL_E_OOM = 0, -1, -2, -3, -4, -5, -6
+VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
+
+EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_assemble_dense", "fl_dense_from_host",
+           "fl_dense_free",
+           "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_diag", "fl_matvec",
+           "fl_matvec_async", "fl_pcg", "fl_cg_update_async", "fl_dot_async", "fl_xpby_async",
+           "fl_debug_orders", "fl_debug_touching"]
+
+
+class fl_mesh(C.Structure):
+    _fields_ = [("d", C.c_int32), ("pad_", C.c_int32), ("nv", C.c_int64), ("nc", C.c_int64),
+                ("nb", C.c_int64), ("vertices", C.c_void_p), ("cells", C.c_void_p),
+                ("boundary_edges", C.c_void_p), ("boundary_normals", C.c_void_p)]
+
+
+class fl_dofmap(C.Structure):
+    _fields_ = [("n", C.c_int64), ("vertex_to_dof", C.c_void_p)]
+
+
+class fl_kernel(C.Structure):
+    _fields_ = [("d", C.c_int32), ("variant", C.c_int32), ("s", C.c_double), ("C_ds", C.c_double)]
+
+
+class fl_order_params(C.Structure):
+    _fields_ = [("rho1", C.c_double), ("rho2", C.c_double), ("rho3", C.c_double), ("rho4", C.c_double),
+                ("C_offset", C.c_double), ("alpha", C.c_double)]
+
+
+class fl_tables(C.Structure):
+    _fields_ = [("dir", C.c_void_p), ("data", C.c_void_p), ("ndata", C.c_int64)]
+
+
+class fl_solve_report(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("residual", C.c_double), ("seconds", C.c_double),
+                ("converged", C.c_int32), ("pad_", C.c_int32), ("true_residual", C.c_double)]
+
+
+class fl_assembly_stats(C.Structure):
+    _fields_ = [("pairs_identical", C.c_int64), ("pairs_touching", C.c_int64), ("pairs_cross", C.c_int64),
+                ("pairs_tail", C.c_int64), ("pairs_boundary_singular", C.c_int64),
+                ("pairs_boundary_flux", C.c_int64), ("evals_cross", C.c_double), ("evals_tail", C.c_double),
+                ("evals_singular", C.c_double), ("evals_boundary", C.c_double), ("ms_prep", C.c_double),
+                ("ms_singular", C.c_double), ("ms_tail", C.c_double), ("ms_cross", C.c_double),
+                ("ms_local", C.c_double), ("ms_total", C.c_double), ("cross_tile_pairs", C.c_int64),
+                ("ncolors", C.c_int32), ("ntiles", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load():
+    """Load the extension; raises (never falls back) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError("fraclap_b200 CUDA library not built: %s (run __graft_entry__.build())" % LIB_PATH)
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp = C.c_void_p
+    sig = {
+        "fl_abi_version": (C.c_int32, []),
+        "fl_last_error": (C.c_char_p, []),
+        "fl_device_count": (C.c_int32, []),
+        "fl_assemble_dense": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),
+                                          P(fl_tables), C.c_int64, C.c_int64, C.c_int64, C.c_int32, vp,
+                                          P(vp)]),
+        "fl_dense_from_host": (C.c_int32, [vp, C.c_int64, C.c_int32, P(vp)]),
+        "fl_dense_free": (None, [vp]),
+        "fl_dense_info": (C.c_int32, [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(vp)]),
+        "fl_dense_stats": (C.c_int32, [vp, P(fl_assembly_stats)]),
+        "fl_dense_to_host": (C.c_int32, [vp, vp]),
+        "fl_dense_diag": (C.c_int32, [vp, vp]),
+        "fl_matvec": (C.c_int32, [vp, vp, vp, C.c_int32]),
+        "fl_matvec_async": (C.c_int32, [vp, vp, vp, vp]),
+        "fl_pcg": (C.c_int32, [vp, vp, vp, C.c_double, C.c_int64, C.c_int32, vp, P(fl_solve_report)]),
+        "fl_cg_update_async": (C.c_int32, [C.c_int64, C.c_double, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "fl_dot_async": (C.c_int32, [C.c_int64, vp, vp, vp, vp]),
+        "fl_xpby_async": (C.c_int32, [C.c_int64, vp, C.c_double, vp, vp]),
+        "fl_debug_orders": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), C.c_int32,
+                                        vp, vp]),
+        "fl_debug_touching": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), C.c_int32,
+                                          P(C.c_int64), vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(code):
+    """Raise the reference's exception for a negative FL_E_* code."""
+    if code == FL_OK:
+        return
+    msg = load().fl_last_error().decode(errors="replace")
+    if code == FL_E_ARG:
+        raise ValueError(msg)
+    if code == FL_E_ASSEMBLY:
+        from .assembly import AssemblyError
+        raise AssemblyError(msg)
+    if code == FL_E_QUAD:
+        from .quadrature import QuadratureError
+        raise QuadratureError(msg)
+    if code == FL_E_SOLVER:
+        from .solve import SolverError
+        raise SolverError(msg)
+    if code == FL_E_OOM:
+        raise MemoryError(msg)
+    raise RuntimeError("fraclap_b200 CUDA error: %s" % msg)
+
+
+def ptr(a):
+    return a.ctypes.data if a is not None else None
+
+
+class Marshal:
+    """Keeps the contiguous host arrays alive for the duration of one C call."""
+
+    def __init__(self, mesh, dofmap, kernel, params):
+        from .quadrature import OrderParams
+        d = int(mesh.vertices.shape[1])
+        self.vertices = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        self.cells = np.ascontiguousarray(mesh.cells, dtype=np.int64)
+        be = np.asarray(mesh.boundary_edges, dtype=np.int64).reshape(-1, d)
+        bn = np.asarray(mesh.boundary_normals, dtype=np.float64).reshape(-1, d)
+        self.bedges = np.ascontiguousarray(be)
+        self.bnormals = np.ascontiguousarray(bn)
+        self.v2d = np.ascontiguousarray(dofmap.vertex_to_dof, dtype=np.int64)
+        self.mesh = fl_mesh(d, 0, len(self.vertices), len(self.cells), len(self.bedges), ptr(self.vertices),
+                            ptr(self.cells), ptr(self.bedges) if len(self.bedges) else None,
+                            ptr(self.bnormals) if len(self.bnormals) else None)
+        self.dofmap = fl_dofmap(int(dofmap.n), ptr(self.v2d))
+        variant = getattr(kernel, "variant", "integral")
+        variant = getattr(variant, "value", variant)
+        self.kernel = fl_kernel(int(kernel.d), VARIANT_ID[str(variant)], float(kernel.s), float(kernel.C_ds))
+        params = params if params is not None else OrderParams()
+        self.params = fl_order_params(params.rho1, params.rho2, params.rho3, params.rho4, params.C_offset,
+                                      float(params.target_alpha(d, float(kernel.s))))
+        self.d = d

@@ -1,0 +1,128 @@
+"""Dense P1 stiffness assembly of the integral fractional Laplacian on a B200.
+
+Drop-in for `fraclap.assembly.assemble_dense` (reference assembly.py:1059-1104): same
+signature, same refusal beyond `n_limit`, same (n, n) float64 result.  The work runs in
+libfraclap_b200.so (csrc/): classification, singular pairs, tail, boundary flux, cross
+tiles and the deterministic accumulation; Python only marshals arrays.
+
+`assemble_dense_device` returns the matrix left in HBM as a `DenseDeviceOperator`, which
+`solve.pcg` — and the reference's own pcg through LinearOperatorHandle.from_matrix
+(solve.py:29-30) — accept directly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+from scipy.special import gammaln
+
+from . import _lib
+from .quadrature import OrderParams, XQ_ORDER, EDGE_GL_ORDER, pack_tables, simplex_rule
+
+DENSE_LIMIT = 4000            # assembly.py:44
+
+
+class Variant(Enum):
+    """assembly.py:47-50."""
+    INTEGRAL = "integral"
+    REGIONAL = "regional"
+    SYMMETRIZED = "symmetrized"
+
+
+class AssemblyError(RuntimeError):
+    """assembly.py:53."""
+
+
+def normalisation(d: int, s: float) -> float:
+    """C(d,s) = 2^{2s} s Gamma(s+d/2) / (pi^{d/2} Gamma(1-s))  (assembly.py:57-63)."""
+    if not 0.0 < s < 1.0:
+        raise ValueError("s must lie in (0,1)")
+    return float(2.0 ** (2 * s) * s * math.exp(gammaln(s + d / 2) - gammaln(1.0 - s)) / math.pi ** (d / 2))
+
+
+@dataclass
+class FractionalKernel:
+    """assembly.py:66-94 (the symmetrized variant is outside the dense device path)."""
+    d: int
+    s: float
+    variant: Variant = Variant.INTEGRAL
+
+    def __post_init__(self):
+        self.C_ds = normalisation(self.d, self.s)
+
+    @property
+    def exponent(self):
+        return -(self.d / 2.0 + self.s)
+
+
+def _device_index(device):
+    if device is None:
+        try:
+            import torch
+            return torch.cuda.current_device() if torch.cuda.is_available() else 0
+        except Exception:
+            return 0
+    return int(getattr(device, "index", device) or 0)
+
+
+def _tables(d, s):
+    dir_, data = pack_tables(d, float(s))
+    return dir_, data, _lib.fl_tables(dir_.ctypes.data, data.ctypes.data, len(data))
+
+
+def assemble_dense_device(mesh, dofmap, kernel, params: OrderParams | None = None, n_limit=None,
+                          rows=None, device=None, stream=None):
+    """Assemble rows [r0, r1) (default: all) of A on the GPU; returns a DenseDeviceOperator."""
+    from .operator import DenseDeviceOperator
+    lib = _lib.load()
+    variant = getattr(getattr(kernel, "variant", Variant.INTEGRAL), "value", "integral")
+    if variant == "symmetrized":
+        raise AssemblyError("symmetrized kernels are not supported by the dense device path")
+    m = _lib.Marshal(mesh, dofmap, kernel, params)
+    dir_, data, tb = _tables(m.d, float(kernel.s))
+    n = int(dofmap.n)
+    r0, r1 = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
+    handle = C.c_void_p()
+    code = lib.fl_assemble_dense(C.byref(m.mesh), C.byref(m.dofmap), C.byref(m.kernel), C.byref(m.params),
+                                 C.byref(tb), -1 if n_limit is None else int(n_limit), r0, r1,
+                                 _device_index(device), C.c_void_p(stream) if stream else None,
+                                 C.byref(handle))
+    _lib.check(code)
+    return DenseDeviceOperator(handle, n, r0, r1)
+
+
+def assemble_dense(mesh, dofmap, kernel, params: OrderParams | None = None, n_limit=DENSE_LIMIT):
+    """Dense stiffness matrix, all cell pairs (assembly.py:1059-1104) -> np.ndarray (n, n)."""
+    if dofmap.n > n_limit:
+        raise AssemblyError("dense assembly refused beyond %d dofs" % n_limit)
+    op = assemble_dense_device(mesh, dofmap, kernel, params, n_limit=n_limit)
+    try:
+        return op.to_host()
+    finally:
+        op.free()
+
+
+def load_vector(mesh, dofmap, f, order=4):
+    """b_i = int f phi_i by the per-cell rule of `order` (assembly.py:550-570).  Host O(n)
+    work outside the accelerated path; no discontinuity splitting."""
+    d = mesh.vertices.shape[1]
+    pts, w = simplex_rule(d, order)
+    lam = np.stack([1 - pts[:, 0], pts[:, 0]], axis=1) if d == 1 else \
+        np.stack([1 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], axis=1)
+    P = mesh.vertices[mesh.cells]
+    E = P[:, 1:] - P[:, 0:1]
+    X = P[:, 0:1, :] + pts @ E
+    if d == 1:
+        J = np.abs(P[:, 1, 0] - P[:, 0, 0])
+    else:
+        a, b_ = P[:, 1] - P[:, 0], P[:, 2] - P[:, 0]
+        J = np.abs(a[:, 0] * b_[:, 1] - a[:, 1] * b_[:, 0])
+    fv = np.asarray(f(X.reshape(-1, d))).reshape(len(P), -1)
+    loc = np.einsum("cq,qa->ca", np.outer(J, w) * fv, lam)
+    b = np.zeros(dofmap.n)
+    gd = np.asarray(dofmap.cell_dofs)
+    np.add.at(b, gd[gd >= 0], loc[gd >= 0])
+    return b

@@ -1,0 +1,573 @@
+// C ABI of fraclap_b200 (include/fraclap_b200.h): argument checks with the reference's error
+// semantics, host->device upload of the borrowed mesh arrays, and the orchestration of the
+// assembly phases of assemble_dense (assembly.py:1059-1104) on one stream.
+#include <algorithm>
+#include <chrono>
+#include <memory>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/fraclap_b200.h"
+#include "fl_internal.h"
+
+using namespace fl;
+
+struct fl_dense {
+  int device = 0;
+  int64_t n = 0, row0 = 0, row1 = 0, lda = 0;
+  DBuf<double> A;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  fl_assembly_stats stats{};
+  ~fl_dense() {
+    A.free();
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+static thread_local std::string g_err;
+
+static int32_t fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define FL_API_BEGIN try {
+#define FL_API_END                                              \
+  }                                                             \
+  catch (const Error& e) { return fail(e.code, e.what()); }     \
+  catch (const std::bad_alloc&) { return fail(FL_E_OOM, "host allocation failed"); } \
+  catch (const std::exception& e) { return fail(FL_E_CUDA, e.what()); }
+
+extern "C" {
+
+int32_t fl_abi_version(void) { return FL_ABI_VERSION; }
+const char* fl_last_error(void) { return g_err.c_str(); }
+int32_t fl_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+}  // extern "C"
+
+namespace {
+
+int e4_of(int d, double s) {
+  // e = d + 2s; specialised for s in {1/4, 1/2, 3/4}
+  const double e = d + 2.0 * s;
+  const double e4 = 4.0 * e;
+  if (std::fabs(e4 - std::round(e4)) == 0.0 && (s == 0.25 || s == 0.5 || s == 0.75)) return (int)std::lround(e4);
+  return 0;
+}
+
+OrderConsts make_order_consts(const fl_order_params& p, int d, double s, int64_t n) {
+  OrderConsts oc{};
+  const double ln_n = std::log(std::max((double)n, 2.0));          // quadrature.py:145
+  oc.lead_lnn = (p.alpha / 2 + 0.5) * ln_n;                         // :149
+  oc.lead_lnn_b = (p.alpha / 2 + 0.25) * ln_n;
+  oc.s = s;
+  oc.sm1 = s - 1;
+  oc.ln_rho1 = std::log(p.rho1);
+  oc.ln_rho2 = std::log(p.rho2);
+  oc.ln_rho3 = std::log(p.rho3);
+  oc.coff = p.C_offset;
+  oc.coff_tail = p.C_offset - 4;                                    // assembly.py:985, :997
+  oc.cap_disjoint = (d == 2) ? 9 : KMAX;                            // quadrature.py:171-175
+  return oc;
+}
+
+void check_inputs(const fl_mesh* mesh, const fl_dofmap* dm, const fl_kernel* k, const fl_order_params* p,
+                  const fl_tables* t) {
+  if (!mesh || !dm || !k || !p || !t) throw Error(FL_E_ARG, "null argument");
+  if (mesh->d != 1 && mesh->d != 2) throw Error(FL_E_ARG, "mesh dimension must be 1 or 2");
+  if (k->d != mesh->d) throw Error(FL_E_ARG, "kernel dimension does not match the mesh");
+  if (!(k->s > 0.0 && k->s < 1.0)) throw Error(FL_E_ARG, "s must lie in (0,1)");   // assembly.py:59-60
+  if (std::min(std::min(p->rho1, p->rho2), std::min(p->rho3, p->rho4)) <= 1)
+    throw Error(FL_E_ARG, "all rho parameters must exceed 1");                      // quadrature.py:125-126
+  if (mesh->nv <= 0 || mesh->nc <= 0 || mesh->nv >= (1LL << 31) || mesh->nc >= (1LL << 28))
+    throw Error(FL_E_ARG, "mesh size out of range");
+  if (!mesh->vertices || !mesh->cells || (mesh->nb > 0 && (!mesh->boundary_edges || !mesh->boundary_normals)))
+    throw Error(FL_E_ARG, "missing mesh arrays");
+  if (!dm->vertex_to_dof || dm->n < 0) throw Error(FL_E_ARG, "bad dofmap");
+  if (!t->dir || !t->data || t->ndata <= 0) throw Error(FL_E_ARG, "missing quadrature tables");
+}
+
+struct Uploaded {
+  DBuf<double> vert, bnorm, tab, X, W;
+  DBuf<int> cells, v2d, bedges, patch_off, patch_cells;
+  DBuf<CellGeo> geo;
+  DevMesh m;
+  DevTables t;
+};
+
+void upload(const fl_mesh* mesh, const fl_dofmap* dm, const fl_tables* tb, Uploaded& U, cudaStream_t st) {
+  const int d = mesh->d;
+  const int64_t nv = mesh->nv, nc = mesh->nc, nb = mesh->nb;
+  std::vector<int> hc((size_t)nc * (d + 1)), hv2d(nv), hbe((size_t)std::max<int64_t>(nb, 1) * d);
+  for (size_t i = 0; i < hc.size(); ++i) {
+    const int64_t c = mesh->cells[i];
+    if (c < 0 || c >= nv) throw Error(FL_E_ARG, "cell vertex index out of range");
+    hc[i] = (int)c;
+  }
+  int64_t maxdof = -1;
+  for (int64_t v = 0; v < nv; ++v) {
+    hv2d[v] = (int)dm->vertex_to_dof[v];
+    maxdof = std::max<int64_t>(maxdof, dm->vertex_to_dof[v]);
+  }
+  if (maxdof + 1 != dm->n) throw Error(FL_E_ARG, "dofmap.n does not match vertex_to_dof");
+  for (int64_t i = 0; i < nb * d; ++i) hbe[i] = (int)mesh->boundary_edges[i];
+  U.vert.alloc(nv * d);
+  U.cells.alloc(hc.size());
+  U.v2d.alloc(nv);
+  U.bedges.alloc(hbe.size());
+  U.bnorm.alloc(std::max<int64_t>(nb, 1) * d);
+  FL_CUDA(cudaMemcpyAsync(U.vert.p, mesh->vertices, nv * d * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(U.cells.p, hc.data(), hc.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(U.v2d.p, hv2d.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
+  if (nb > 0) {
+    FL_CUDA(cudaMemcpyAsync(U.bedges.p, hbe.data(), nb * d * sizeof(int), cudaMemcpyHostToDevice, st));
+    FL_CUDA(cudaMemcpyAsync(U.bnorm.p, mesh->boundary_normals, nb * d * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  U.tab.alloc(tb->ndata);
+  FL_CUDA(cudaMemcpyAsync(U.tab.p, tb->data, tb->ndata * sizeof(double), cudaMemcpyHostToDevice, st));
+  for (int i = 0; i < NTOPO * KDIR; ++i) {
+    const int64_t off = tb->dir[2 * i], cnt = tb->dir[2 * i + 1];
+    if (cnt < 0 || off < 0 || (off + cnt) * NODE > tb->ndata) throw Error(FL_E_ARG, "corrupt quadrature table");
+    U.t.dir[i] = RuleRef{(int)off, (int)cnt};
+  }
+  U.t.data = U.tab.p;
+  if (U.t.rule(T_CELL, 0).cnt <= 0) throw Error(FL_E_ARG, "missing cell rule");
+  DevMesh& m = U.m;
+  m.d = d; m.nv = (int)nv; m.nc = (int)nc; m.nb = (int)nb; m.n = (int)dm->n;
+  m.q = U.t.rule(T_CELL, 0).cnt;
+  if (m.q != (d == 1 ? 6 : 16)) throw Error(FL_E_ARG, "cell rule must have 6 (1D) / 16 (2D) nodes (XQ_ORDER)");
+  m.vert = U.vert.p; m.cells = U.cells.p; m.v2d = U.v2d.p; m.bedges = U.bedges.p; m.bnorm = U.bnorm.p;
+  build_patches((int)nv, (int)nc, d, U.cells.p, U.patch_off, U.patch_cells, st);
+  m.patch_off = U.patch_off.p;
+  m.patch_cells = U.patch_cells.p;
+  U.geo.alloc(nc);
+  launch_prep_cells(m, U.geo.p, st);
+  m.geo = U.geo.p;
+  U.X.alloc((size_t)nc * m.q * d);
+  U.W.alloc((size_t)nc * m.q);
+  launch_cell_nodes(m, U.t, U.X.p, U.W.p, st);
+  m.X = U.X.p;
+  m.W = U.W.p;
+}
+
+__global__ void flag_target_cells(DevMesh m, int r0, int r1, int* flags) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m.nc) return;
+  int f = 0;
+  for (int i = 0; i <= m.d; ++i) {
+    const int dof = m.v2d[m.cells[c * (m.d + 1) + i]];
+    f |= (dof >= r0 && dof < r1);
+  }
+  flags[c] = f;
+}
+__global__ void iota2(int* a, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+__global__ void dof_vertex2(DevMesh m, int* dv) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < m.nv && m.v2d[v] >= 0) dv[m.v2d[v]] = v;
+}
+
+struct Timer {
+  cudaEvent_t e[8];
+  int k = 0;
+  cudaStream_t st;
+  explicit Timer(cudaStream_t s) : st(s) {
+    for (auto& x : e) cudaEventCreate(&x);
+  }
+  ~Timer() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+  void mark() { cudaEventRecord(e[k++], st); }
+  double ms(int a, int b) {
+    float f = 0;
+    cudaEventElapsedTime(&f, e[a], e[b]);
+    return f;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                          const fl_order_params* params, const fl_tables* tables, int64_t n_limit,
+                          int64_t row_begin, int64_t row_end, int32_t device, void* stream, fl_dense** out) {
+  FL_API_BEGIN
+  if (!out) return fail(FL_E_ARG, "null output handle");
+  *out = nullptr;
+  check_inputs(mesh, dofmap, kernel, params, tables);
+  if (kernel->variant == FL_VARIANT_SYMMETRIZED)
+    return fail(FL_E_ASSEMBLY, "symmetrized kernels are out of scope of the dense device path");
+  if (n_limit >= 0 && dofmap->n > n_limit)
+    return fail(FL_E_ASSEMBLY, "dense assembly refused beyond " + std::to_string(n_limit) + " dofs");
+  const int64_t n = dofmap->n;
+  if (row_begin < 0 || row_end > n || row_begin > row_end) return fail(FL_E_ARG, "row range out of bounds");
+  FL_CUDA(cudaSetDevice(device));
+  std::unique_ptr<fl_dense> D(new fl_dense());
+  D->device = device;
+  D->n = n;
+  D->row0 = row_begin;
+  D->row1 = row_end;
+  D->lda = ((n + 31) / 32) * 32;
+  if (stream) {
+    D->stream = (cudaStream_t)stream;
+  } else {
+    FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
+    D->own_stream = true;
+  }
+  cudaStream_t st = D->stream;
+  const int d = mesh->d;
+  const double s = kernel->s, C = kernel->C_ds;
+  const double ex = -(d / 2.0 + s);
+  const int e4 = e4_of(d, s);
+  const bool integral = kernel->variant == FL_VARIANT_INTEGRAL;
+  const int64_t rows = row_end - row_begin;
+
+  Timer tm(st);
+  tm.mark();  // 0
+  Uploaded U;
+  upload(mesh, dofmap, tables, U, st);
+  DevMesh& m = U.m;
+  const int ncolors = color_cells(m, U.geo.p, st);
+  const OrderConsts oc = make_order_consts(*params, d, s, n);
+
+  // target cells: cells with a vertex DoF in the owned rows
+  DBuf<int> flags(m.nc), all(m.nc), targets(m.nc), nsel(1);
+  flag_target_cells<<<(m.nc + 255) / 256, 256, 0, st>>>(m, (int)row_begin, (int)row_end, flags.p);
+  iota2<<<(m.nc + 255) / 256, 256, 0, st>>>(all.p, m.nc);
+  {
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, all.p, flags.p, targets.p, nsel.p, m.nc, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, all.p, flags.p, targets.p, nsel.p, m.nc, st));
+    FL_CHECK_LAUNCH();
+  }
+  int ntargets = 0;
+  FL_CUDA(cudaMemcpyAsync(&ntargets, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  DBuf<int> row_vertex(n > 0 ? n : 1);
+  dof_vertex2<<<(m.nv + 255) / 256, 256, 0, st>>>(m, row_vertex.p);
+
+  // classification (quadrature.py:90-110, assembly.py:412-473, :784-841)
+  DBuf<TouchPair> tpairs;
+  DBuf<int> ident_k;
+  int64_t npairs = 0, nitems = 0;
+  classify_touching(m, oc, tpairs, npairs, ident_k, st);
+  DBuf<BndPair> bitems;
+  const bool do_bnd = integral && m.nb > 0;
+  if (do_bnd) classify_boundary(m, oc, bitems, nitems, st);
+  else bitems.alloc(1);
+  tm.mark();  // 1
+
+  // singular pairs
+  DBuf<double> ident((size_t)m.nc * 9), tloc((size_t)std::max<int64_t>(npairs, 1) * 25),
+      bloc((size_t)std::max<int64_t>(nitems, 1) * 9);
+  launch_singular_identical(m, U.t, ex, e4, ident_k.p, ident.p, st);
+  launch_singular_touching(m, U.t, ex, e4, tpairs.p, npairs, tloc.p, st);
+  if (do_bnd) launch_singular_boundary(m, U.t, ex, e4, bitems.p, nitems, bloc.p, st);
+  tm.mark();  // 2
+
+  // tail + flux at the nodes of the target cells
+  DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
+  FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
+  launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, st);
+  if (do_bnd) launch_flux(m, U.t, ex, e4, targets.p, ntargets, win.p, st);
+  tm.mark();  // 3
+
+  // dense rows: cross term tiles, then the local/sparse pull
+  D->A.alloc((size_t)std::max<int64_t>(rows, 1) * D->lda);
+  if (D->lda > n && rows > 0)
+    FL_CUDA(cudaMemset2DAsync(D->A.p + n, D->lda * sizeof(double), 0, (D->lda - n) * sizeof(double), rows, st));
+  Tiles trow, tcol;
+  const bool full = (row_begin == 0 && row_end == n);
+  build_tiles(m, (int)row_begin, (int)row_end, trow, st);
+  if (!full) build_tiles(m, 0, (int)n, tcol, st);
+  int64_t ntp = 0;
+  launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
+                     D->lda, ncolors, ntp, st);
+  tm.mark();  // 4
+  DBuf<double> Lc((size_t)m.nc * 9);
+  launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
+  SparseIndex si;
+  build_sparse_index(m, tpairs.p, npairs, bitems.p, nitems, si, st);
+  launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
+                     (int)row_begin, (int)row_end, D->A.p, D->lda, st);
+  tm.mark();  // 5
+  FL_CUDA(cudaStreamSynchronize(st));
+
+  fl_assembly_stats& S = D->stats;
+  const int64_t nc = m.nc;
+  S.pairs_identical = nc;
+  S.pairs_touching = npairs;
+  S.pairs_cross = nc * (nc - 1) / 2 - npairs;
+  S.pairs_tail = nc * (nc - 1) - 2 * npairs;
+  S.pairs_boundary_singular = nitems;
+  S.pairs_boundary_flux = integral ? nc * m.nb : 0;
+  S.ms_prep = tm.ms(0, 1);
+  S.ms_singular = tm.ms(1, 2);
+  S.ms_tail = tm.ms(2, 3);
+  S.ms_cross = tm.ms(3, 4);
+  S.ms_local = tm.ms(4, 5);
+  S.ms_total = tm.ms(0, 5);
+  S.cross_tile_pairs = ntp;
+  S.ncolors = ncolors;
+  S.ntiles = trow.ntiles;
+  *out = D.release();
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out) {
+  FL_API_BEGIN
+  if (!A || !out || n <= 0) return fail(FL_E_ARG, "bad argument");
+  *out = nullptr;
+  FL_CUDA(cudaSetDevice(device));
+  std::unique_ptr<fl_dense> D(new fl_dense());
+  D->device = device;
+  D->n = n;
+  D->row0 = 0;
+  D->row1 = n;
+  D->lda = ((n + 31) / 32) * 32;
+  FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
+  D->own_stream = true;
+  D->A.alloc((size_t)n * D->lda);
+  FL_CUDA(cudaMemsetAsync(D->A.p, 0, (size_t)n * D->lda * sizeof(double), D->stream));
+  FL_CUDA(cudaMemcpy2DAsync(D->A.p, D->lda * sizeof(double), A, n * sizeof(double), n * sizeof(double), n,
+                            cudaMemcpyHostToDevice, D->stream));
+  FL_CUDA(cudaStreamSynchronize(D->stream));
+  *out = D.release();
+  return FL_OK;
+  FL_API_END
+}
+
+void fl_dense_free(fl_dense* A) { delete A; }
+
+int32_t fl_dense_info(const fl_dense* A, int64_t* n, int64_t* r0, int64_t* r1, double** ptr) {
+  if (!A) return fail(FL_E_ARG, "null handle");
+  if (n) *n = A->n;
+  if (r0) *r0 = A->row0;
+  if (r1) *r1 = A->row1;
+  if (ptr) *ptr = A->A.p;
+  return FL_OK;
+}
+
+int32_t fl_dense_stats(const fl_dense* A, fl_assembly_stats* s) {
+  if (!A || !s) return fail(FL_E_ARG, "null argument");
+  *s = A->stats;
+  return FL_OK;
+}
+
+int32_t fl_dense_to_host(const fl_dense* A, double* host) {
+  FL_API_BEGIN
+  if (!A || !host) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(A->device));
+  const int64_t rows = A->row1 - A->row0;
+  if (rows == 0 || A->n == 0) return FL_OK;
+  FL_CUDA(cudaMemcpy2DAsync(host, A->n * sizeof(double), A->A.p, A->lda * sizeof(double), A->n * sizeof(double),
+                            rows, cudaMemcpyDeviceToHost, A->stream));
+  FL_CUDA(cudaStreamSynchronize(A->stream));
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_dense_diag(const fl_dense* A, double* host_diag) {
+  FL_API_BEGIN
+  if (!A || !host_diag) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(A->device));
+  const int64_t rows = A->row1 - A->row0;
+  if (rows == 0) return FL_OK;
+  DBuf<double> d(rows);
+  launch_diag(A->A.p, rows, A->row0, A->lda, d.p, A->stream);
+  FL_CUDA(cudaMemcpyAsync(host_diag, d.p, rows * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+  FL_CUDA(cudaStreamSynchronize(A->stream));
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_matvec_async(const fl_dense* A, const double* x_dev, double* y_dev, void* stream) {
+  FL_API_BEGIN
+  if (!A || !x_dev || !y_dev) return fail(FL_E_ARG, "null argument");
+  cudaStream_t st = stream ? (cudaStream_t)stream : A->stream;
+  launch_matvec(A->A.p, A->row1 - A->row0, A->n, A->lda, x_dev, y_dev, st);
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_matvec(const fl_dense* A, const double* x, double* y, int32_t ptr_kind) {
+  FL_API_BEGIN
+  if (!A || !x || !y) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(A->device));
+  const int64_t rows = A->row1 - A->row0;
+  if (ptr_kind == 1) {
+    launch_matvec(A->A.p, rows, A->n, A->lda, x, y, A->stream);
+    FL_CUDA(cudaStreamSynchronize(A->stream));
+    return FL_OK;
+  }
+  DBuf<double> xd(A->lda), yd(std::max<int64_t>(rows, 1));
+  FL_CUDA(cudaMemsetAsync(xd.p, 0, A->lda * sizeof(double), A->stream));
+  FL_CUDA(cudaMemcpyAsync(xd.p, x, A->n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
+  launch_matvec(A->A.p, rows, A->n, A->lda, xd.p, yd.p, A->stream);
+  FL_CUDA(cudaMemcpyAsync(y, yd.p, rows * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+  FL_CUDA(cudaStreamSynchronize(A->stream));
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_pcg(const fl_dense* A, const double* b, const double* x0, double tol, int64_t max_iter, int32_t precond,
+               double* x, fl_solve_report* rep) {
+  FL_API_BEGIN
+  if (!A || !b || !x || !rep) return fail(FL_E_ARG, "null argument");
+  if (A->row0 != 0 || A->row1 != A->n) return fail(FL_E_ARG, "fl_pcg needs the whole matrix on one device");
+  FL_CUDA(cudaSetDevice(A->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = A->n, L = A->lda;
+  cudaStream_t st = A->stream;
+  std::vector<double> diag(n), minv(n);
+  if (precond == 1) {
+    DBuf<double> d(std::max<int64_t>(n, 1));
+    launch_diag(A->A.p, n, 0, L, d.p, st);
+    FL_CUDA(cudaMemcpyAsync(diag.data(), d.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < n; ++i) {
+      if (!(diag[i] > 0)) return fail(FL_E_SOLVER, "nonpositive diagonal; operator not SPD");   // solve.py:67-68
+      minv[i] = 1.0 / diag[i];
+    }
+  } else {
+    for (int64_t i = 0; i < n; ++i) minv[i] = 1.0;
+  }
+  DBuf<double> dminv(L), dx(L), dr(L), dz(L), dp(L), dAp(L), db(L);
+  for (auto* buf : {&dminv, &dx, &dr, &dz, &dp, &dAp, &db}) FL_CUDA(cudaMemsetAsync(buf->p, 0, L * sizeof(double), st));
+  FL_CUDA(cudaMemcpyAsync(dminv.p, minv.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dr.p, b, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(db.p, b, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (x0) FL_CUDA(cudaMemcpyAsync(dx.p, x0, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  const long long mi = max_iter;
+  PcgResult r = run_pcg(A->A.p, n, L, dminv.p, dx.p, dr.p, dz.p, dp.p, dAp.p, tol, mi, x0 != nullptr, st);
+  if (r.error) return fail(FL_E_SOLVER, "p^T A p <= 0: operator not SPD");                  // solve.py:87-88
+  FL_CUDA(cudaMemcpyAsync(x, dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // true residual ||b - A x|| / ||b|| reported beside the reference's preconditioned one
+  launch_matvec(A->A.p, n, n, L, dx.p, dAp.p, st);
+  std::vector<double> ax(n);
+  FL_CUDA(cudaMemcpyAsync(ax.data(), dAp.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  double nr = 0, nb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    nr += (b[i] - ax[i]) * (b[i] - ax[i]);
+    nb += b[i] * b[i];
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  rep->iterations = r.it;
+  rep->residual = (r.norm0 == 0.0) ? 0.0 : std::sqrt(std::fabs(r.rz)) / r.norm0;
+  rep->seconds = std::chrono::duration<double>(t1 - t0).count();
+  rep->converged = (r.norm0 == 0.0) ? 1 : r.converged;
+  rep->true_residual = nb > 0 ? std::sqrt(nr / nb) : 0.0;
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_cg_update_async(int64_t m, double alpha, double* x, double* r, double* z, const double* p,
+                           const double* Ap, const double* minv, double* partial_dev, void* stream) {
+  FL_API_BEGIN
+  DBuf<double> scratch(DOT_BLOCKS);
+  launch_cg_update(m, alpha, nullptr, x, r, z, p, Ap, minv, partial_dev, scratch.p, (cudaStream_t)stream);
+  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_dot_async(int64_t m, const double* a, const double* b, double* out_dev, void* stream) {
+  FL_API_BEGIN
+  DBuf<double> scratch(DOT_BLOCKS);
+  launch_dot(m, a, b, out_dev, scratch.p, (cudaStream_t)stream);
+  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_xpby_async(int64_t m, const double* z, double beta, double* p, void* stream) {
+  FL_API_BEGIN
+  launch_xpby(m, z, beta, nullptr, p, (cudaStream_t)stream);
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                        const fl_order_params* params, int32_t device, int8_t* cross_k, int8_t* tail_k) {
+  FL_API_BEGIN
+  if (!mesh || !dofmap || !kernel || !params || !cross_k || !tail_k) return fail(FL_E_ARG, "null argument");
+  if (kernel->d != mesh->d || !(kernel->s > 0 && kernel->s < 1)) return fail(FL_E_ARG, "bad kernel");
+  FL_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // minimal table: the cell rule is needed by upload(); fake a 1-node rule of the right size
+  std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
+  const int q = mesh->d == 1 ? 6 : 16;
+  std::vector<double> data((size_t)q * NODE, 0.0);
+  dir[2 * (T_CELL * KDIR + 0) + 1] = q;
+  fl_tables t{dir.data(), data.data(), (int64_t)data.size()};
+  Uploaded U;
+  upload(mesh, dofmap, &t, U, st);
+  const OrderConsts oc = make_order_consts(*params, mesh->d, kernel->s, dofmap->n);
+  const int64_t tot = mesh->nc * mesh->nc;
+  DBuf<int8_t> ck(tot), tk(tot);
+  launch_debug_orders(U.m, oc, ck.p, tk.p, st);
+  FL_CUDA(cudaMemcpyAsync(cross_k, ck.p, tot, cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(tail_k, tk.p, tot, cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  cudaStreamDestroy(st);
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                          const fl_order_params* params, int32_t device, int64_t* npairs, int64_t* pairs,
+                          int32_t* topo, int32_t* k, int32_t* ident_k) {
+  FL_API_BEGIN
+  if (!mesh || !dofmap || !kernel || !params || !npairs) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
+  const int q = mesh->d == 1 ? 6 : 16;
+  std::vector<double> data((size_t)q * NODE, 0.0);
+  dir[2 * (T_CELL * KDIR + 0) + 1] = q;
+  fl_tables t{dir.data(), data.data(), (int64_t)data.size()};
+  Uploaded U;
+  upload(mesh, dofmap, &t, U, st);
+  const OrderConsts oc = make_order_consts(*params, mesh->d, kernel->s, dofmap->n);
+  DBuf<TouchPair> tp;
+  DBuf<int> ik;
+  int64_t np = 0;
+  classify_touching(U.m, oc, tp, np, ik, st);
+  FL_CUDA(cudaStreamSynchronize(st));
+  const int64_t cap = *npairs;
+  *npairs = np;
+  if (pairs && topo && k && cap >= np) {
+    std::vector<TouchPair> h(np);
+    if (np) FL_CUDA(cudaMemcpy(h.data(), tp.p, np * sizeof(TouchPair), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < np; ++i) {
+      pairs[2 * i] = h[i].c0;
+      pairs[2 * i + 1] = h[i].c1;
+      topo[i] = h[i].topo;
+      k[i] = h[i].k;
+    }
+    if (ident_k) FL_CUDA(cudaMemcpy(ident_k, ik.p, mesh->nc * sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  cudaStreamDestroy(st);
+  return FL_OK;
+  FL_API_END
+}
+
+}  // extern "C"

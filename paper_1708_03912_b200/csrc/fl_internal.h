@@ -1,0 +1,183 @@
+// Internal host-side declarations shared by the fraclap_b200 translation units.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "fl_device.cuh"
+
+namespace fl {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FL_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::fl::Error(e_ == cudaErrorMemoryAllocation ? -6 : -5,                     \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+
+#define FL_CHECK_LAUNCH() FL_CUDA(cudaGetLastError())
+
+// Device buffer with RAII.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t cnt) { alloc(cnt); }
+  void alloc(size_t cnt) {
+    free();
+    n = cnt;
+    if (cnt) FL_CUDA(cudaMalloc(&p, cnt * sizeof(T)));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    free();
+    p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+    return *this;
+  }
+};
+
+// Device view of the mesh + derived per-cell data (all int32 indices; nv, nc < 2^31).
+struct DevMesh {
+  int d = 0, nv = 0, nc = 0, nb = 0, n = 0, q = 0;
+  const double* vert = nullptr;    // nv*d
+  const int* cells = nullptr;      // nc*(d+1)
+  const int* v2d = nullptr;        // nv
+  const int* bedges = nullptr;     // nb*d
+  const double* bnorm = nullptr;   // nb*d (outward)
+  const CellGeo* geo = nullptr;    // nc
+  const int* patch_off = nullptr;  // nv+1
+  const int* patch_cells = nullptr;// nc*(d+1), ascending cell id per vertex (mesh.py:114-125)
+  const double* X = nullptr;       // nc*q*d  cell quadrature nodes (assembly.py:292-298)
+  const double* W = nullptr;       // nc*q
+};
+
+struct DevTables {
+  const double* data = nullptr;
+  RuleRef dir[NTOPO * KDIR];
+  __host__ __device__ RuleRef rule(int topo, int k) const { return dir[topo * KDIR + k]; }
+};
+
+// Touching pair record (assembly.py:412-473 + the order of :680).
+struct TouchPair {
+  int c0, c1;       // c0 < c1  (sorted unordered pair)
+  int topo;         // T_CE / T_CV
+  int k;
+  int vK[3], vK2[3];// canonical vertex orders
+  int locs[5];      // global vertex behind each local basis slot
+  int nloc;
+};
+
+// Boundary (cell, edge) singular pair (assembly.py:796-841).
+struct BndPair {
+  int cell, edge, topo, k;
+  int locs[3];      // canonical cell vertex order
+  int nloc;
+  double pe[2][2];  // canonical edge points (1D: pe[0][0])
+  double ne[2];     // INWARD normal (assembly.py:792)
+};
+
+// ------------------------------------------------------------ launchers (by file)
+// fl_prep.cu
+void launch_prep_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st);
+void launch_cell_nodes(const DevMesh& m, const DevTables& t, double* X, double* W, cudaStream_t st);
+void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf<int>& data,
+                   cudaStream_t st);
+int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st);  // returns #colours
+void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>& pairs,
+                       int64_t& npairs, DBuf<int>& ident_k, cudaStream_t st);
+void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& items,
+                       int64_t& nitems, cudaStream_t st);
+// DoF tiles of TILE dofs in Morton order; per tile the sorted (colour, id) list of cells that
+// touch one of its DoFs, with the tile-local slot of each cell vertex.
+constexpr int TILE = 64;
+constexpr int TILE_MAXC = 256;
+struct Tiles {
+  int ntiles = 0;
+  DBuf<int> dofs;     // ntiles*TILE (-1 pad)
+  DBuf<int> ncell;    // ntiles
+  DBuf<int> cells;    // ntiles*TILE_MAXC
+  DBuf<int> slots;    // ntiles*TILE_MAXC*3 (-1: vertex not a DoF of this tile)
+  DBuf<int> cstart;   // ntiles*(maxcolors+1): colour class ranges in the cell list
+};
+constexpr int MAXCOLORS = 32;
+void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& t, cudaStream_t st);
+
+// fl_singular.cu
+void launch_singular_touching(const DevMesh& m, const DevTables& t, double ex, int e4,
+                              const TouchPair* pairs, int64_t npairs, double* out /*npairs*25*/,
+                              cudaStream_t st);
+void launch_singular_identical(const DevMesh& m, const DevTables& t, double ex, int e4,
+                               const int* ident_k, double* out /*nc*9*/, cudaStream_t st);
+void launch_singular_boundary(const DevMesh& m, const DevTables& t, double ex, int e4,
+                              const BndPair* items, int64_t nitems, double* out /*nitems*9*/,
+                              cudaStream_t st);
+
+// fl_far.cu
+void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                 const int* targets, int ntargets, double* psi /*nc*q*/, cudaStream_t st);
+void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const int* targets,
+                 int ntargets, double* win /*nc*q*/, cudaStream_t st);
+void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,
+                        int e4, double Cds, const Tiles& rows, const Tiles& cols, bool symmetric,
+                        int row_begin, int row_end, double* A, int64_t lda, int ncolors,
+                        int64_t& ntilepairs, cudaStream_t st);
+void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
+                         cudaStream_t st);
+
+// fl_local.cu
+void launch_cell_local(const DevMesh& m, const DevTables& t, double Cds, double s, bool integral,
+                       const int* targets, int ntargets, const double* ident, const double* psi,
+                       const double* win, double* Lc /*nc*9*/, cudaStream_t st);
+struct SparseIndex {
+  DBuf<int> tp_first_off, tp_second_off, tp_second;   // touching pairs by first / second cell
+  DBuf<int> bp_off, bp_idx;                           // boundary items by cell
+};
+void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs,
+                        const BndPair* items, int64_t nitems, SparseIndex& si, cudaStream_t st);
+void launch_sparse_pull(const DevMesh& m, double Cds, double s, const double* Lc,
+                        const TouchPair* pairs, const double* tloc, const BndPair* items,
+                        const double* bloc, const SparseIndex& si, const int* row_vertex,
+                        int row_begin, int row_end, double* A, int64_t lda, cudaStream_t st);
+
+// fl_solve.cu
+void launch_matvec(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
+                   cudaStream_t st);
+void launch_diag(const double* A, int64_t rows, int64_t row0, int64_t lda, double* d, cudaStream_t st);
+void launch_dot(int64_t m, const double* a, const double* b, double* out, double* scratch,
+                cudaStream_t st);
+void launch_cg_update(int64_t m, double alpha, const double* alpha_dev, double* x, double* r,
+                      double* z, const double* p, const double* Ap, const double* minv,
+                      double* out, double* scratch, cudaStream_t st);
+void launch_xpby(int64_t m, const double* z, double beta, const double* beta_dev, double* p,
+                 cudaStream_t st);
+void launch_matvec_flag(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
+                        const int* done, cudaStream_t st);
+struct PcgResult {
+  long long it;
+  double rz, norm0;
+  int converged, error;
+};
+PcgResult run_pcg(const double* A, int64_t n, int64_t lda, const double* minv, double* x, double* r, double* z,
+                  double* p, double* Ap, double tol, long long max_iter, bool have_x0, cudaStream_t st);
+constexpr int DOT_BLOCKS = 296;   // 2 x 148 SMs; fixed => deterministic reduction tree
+
+}  // namespace fl

@@ -1,0 +1,580 @@
+// Mesh preparation on the device: per-cell geometry, cell quadrature nodes, vertex patches,
+// vertex-disjoint colouring, touching-pair / boundary-pair classification and the DoF tiles
+// of the cross kernel.
+//
+// Reference: mesh.py:76-130 (diameters, patches), assembly.py:282-298 (cell rule),
+// assembly.py:412-473 (enumerate/canonicalize touching pairs), assembly.py:784-841
+// (boundary pairs), quadrature.py:90-110 (classification), :138-179 (orders).
+#include <cub/cub.cuh>
+
+#include "fl_internal.h"
+
+namespace fl {
+
+// ---------------------------------------------------------------- per-cell geometry
+template <int D>
+__global__ void prep_cells_kernel(DevMesh m, CellGeo* geo) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m.nc) return;
+  CellGeo g;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    g.v[i] = -1; g.dof[i] = -1; g.p[i][0] = 0.0; g.p[i][1] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i <= D; ++i) {
+    const int v = m.cells[c * (D + 1) + i];
+    g.v[i] = v;
+    g.dof[i] = m.v2d[v];
+#pragma unroll
+    for (int j = 0; j < D; ++j) g.p[i][j] = m.vert[v * D + j];
+  }
+  if constexpr (D == 1) {
+    g.diam = fabs(__dsub_rn(g.p[1][0], g.p[0][0]));           // mesh.py:80
+    g.J = g.diam;                                              // assembly.py:137
+    g.cx = __dmul_rn(0.5, __dadd_rn(g.p[0][0], g.p[1][0]));
+    g.cy = 0.0;
+    g.rad = __dmul_rn(0.5, g.diam);
+  } else {
+    const double e0 = norm2d(__dsub_rn(g.p[1][0], g.p[0][0]), __dsub_rn(g.p[1][1], g.p[0][1]));
+    const double e1 = norm2d(__dsub_rn(g.p[2][0], g.p[1][0]), __dsub_rn(g.p[2][1], g.p[1][1]));
+    const double e2 = norm2d(__dsub_rn(g.p[0][0], g.p[2][0]), __dsub_rn(g.p[0][1], g.p[2][1]));
+    g.diam = fmax(e0, fmax(e1, e2));                           // mesh.py:82-85
+    const double ax = __dsub_rn(g.p[1][0], g.p[0][0]), ay = __dsub_rn(g.p[1][1], g.p[0][1]);
+    const double bx = __dsub_rn(g.p[2][0], g.p[0][0]), by = __dsub_rn(g.p[2][1], g.p[0][1]);
+    g.J = fabs(__dsub_rn(__dmul_rn(ax, by), __dmul_rn(ay, bx)));   // assembly.py:138-140
+    g.cx = __ddiv_rn(__dadd_rn(__dadd_rn(g.p[0][0], g.p[1][0]), g.p[2][0]), 3.0);   // :771
+    g.cy = __ddiv_rn(__dadd_rn(__dadd_rn(g.p[0][1], g.p[1][1]), g.p[2][1]), 3.0);
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r = fmax(r, norm2d(__dsub_rn(g.p[i][0], g.cx), __dsub_rn(g.p[i][1], g.cy)));
+    g.rad = r;                                                 // :773
+  }
+  g.ldiam = fabs(log(g.diam));
+  g.color = -1;
+  g.pad = 0;
+  geo[c] = g;
+}
+
+void launch_prep_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st) {
+  const int tb = 128, nb = (m.nc + tb - 1) / tb;
+  if (m.d == 1) prep_cells_kernel<1><<<nb, tb, 0, st>>>(m, geo);
+  else prep_cells_kernel<2><<<nb, tb, 0, st>>>(m, geo);
+  FL_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- cell quadrature nodes
+template <int D>
+__global__ void cell_nodes_kernel(DevMesh m, const double* __restrict__ tab, RuleRef r,
+                                  double* X, double* W) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.nc * r.cnt) return;
+  const int c = i / r.cnt, q = i % r.cnt;
+  const CellGeo g = m.geo[c];
+  const double* nd = tab + (size_t)(r.off + q) * NODE;
+  if constexpr (D == 1) {
+    const double e = __dsub_rn(g.p[1][0], g.p[0][0]);
+    X[i] = g.p[0][0] + nd[0] * e;
+  } else {
+    const double e00 = __dsub_rn(g.p[1][0], g.p[0][0]), e01 = __dsub_rn(g.p[1][1], g.p[0][1]);
+    const double e10 = __dsub_rn(g.p[2][0], g.p[0][0]), e11 = __dsub_rn(g.p[2][1], g.p[0][1]);
+    X[2 * i + 0] = g.p[0][0] + (nd[0] * e00 + nd[1] * e10);
+    X[2 * i + 1] = g.p[0][1] + (nd[0] * e01 + nd[1] * e11);
+  }
+  W[i] = __dmul_rn(g.J, nd[2]);                                 // np.outer(J, w)
+}
+
+void launch_cell_nodes(const DevMesh& m, const DevTables& t, double* X, double* W, cudaStream_t st) {
+  const RuleRef r = t.rule(T_CELL, 0);
+  const int tot = m.nc * r.cnt, tb = 256;
+  if (m.d == 1) cell_nodes_kernel<1><<<(tot + tb - 1) / tb, tb, 0, st>>>(m, t.data, r, X, W);
+  else cell_nodes_kernel<2><<<(tot + tb - 1) / tb, tb, 0, st>>>(m, t.data, r, X, W);
+  FL_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- vertex patches (CSR)
+__global__ void iota_kernel(int* a, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+__global__ void patch_offsets_kernel(const int* keys, int m, int nv, int* off) {
+  // off[v] = #entries with key < v: position i starts vertices prev+1 .. cur
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > m) return;
+  const int prev = (i == 0) ? -1 : keys[i - 1];
+  const int cur = (i == m) ? nv : keys[i];
+  for (int v = prev + 1; v <= cur; ++v) off[v] = i;
+}
+__global__ void flat_to_cell_kernel(const int* flat, int m, int dp1, int* cellv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) cellv[i] = flat[i] / dp1;
+}
+
+// mesh.py:114-125: argsort(cells.ravel(), kind="stable") -> per vertex, ascending cell ids.
+void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf<int>& data,
+                   cudaStream_t st) {
+  const int m = nc * (d + 1);
+  DBuf<int> idx(m), keys_out(m), idx_out(m);
+  iota_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx.p, m);
+  size_t tmp = 0;
+  int bits = 1;
+  while ((1 << bits) < nv + 1) ++bits;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, cells, keys_out.p, idx.p, idx_out.p, m, 0, bits, st);
+  DBuf<unsigned char> t(tmp);
+  FL_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, cells, keys_out.p, idx.p, idx_out.p, m, 0, bits, st));
+  off.alloc(nv + 1);
+  data.alloc(m);
+  patch_offsets_kernel<<<(m + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p);
+  flat_to_cell_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx_out.p, m, d + 1, data.p);
+  FL_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- colouring
+// Jones-Plassmann with a fixed hash priority and double-buffered colours: deterministic.
+__device__ __forceinline__ uint32_t prio(uint32_t c) {
+  uint32_t h = c * 0x9E3779B1u;
+  h ^= h >> 15; h *= 0x85EBCA77u; h ^= h >> 13; h *= 0xC2B2AE3Du; h ^= h >> 16;
+  return h;
+}
+template <int D>
+__global__ void jp_round_kernel(DevMesh m, const int* col_in, int* col_out, int* remaining, int* overflow) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m.nc) return;
+  const int cur = col_in[c];
+  col_out[c] = cur;
+  if (cur >= 0) return;
+  const uint32_t pc = prio(c);
+  uint32_t used = 0;
+  bool is_max = true;
+  for (int i = 0; i <= D && is_max; ++i) {
+    const int v = m.cells[c * (D + 1) + i];
+    for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
+      const int o = m.patch_cells[p];
+      if (o == c) continue;
+      const int co = col_in[o];
+      if (co >= 0) {
+        if (co < 32) used |= 1u << co;
+      } else {
+        const uint32_t po = prio(o);
+        if (po > pc || (po == pc && o > c)) { is_max = false; break; }
+      }
+    }
+  }
+  if (!is_max) { atomicAdd(remaining, 1); return; }
+  const int color = __ffs(~used) - 1;
+  if (color < 0 || color >= MAXCOLORS) { atomicAdd(overflow, 1); return; }
+  col_out[c] = color;
+}
+__global__ void fill_kernel(int* a, int n, int v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+__global__ void store_colors_kernel(CellGeo* geo, const int* col, int nc, int* maxc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  geo[c].color = col[c];
+  atomicMax(maxc, col[c]);
+}
+
+int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st) {
+  DBuf<int> a(m.nc), b(m.nc), cnt(3);
+  const int tb = 256, nb = (m.nc + tb - 1) / tb;
+  fill_kernel<<<nb, tb, 0, st>>>(a.p, m.nc, -1);
+  int h[3];
+  for (int round = 0; round < 10000; ++round) {
+    FL_CUDA(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(int), st));
+    if (m.d == 1) jp_round_kernel<1><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1);
+    else jp_round_kernel<2><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1);
+    FL_CHECK_LAUNCH();
+    FL_CUDA(cudaMemcpyAsync(h, cnt.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    std::swap(a.p, b.p);
+    if (h[1]) throw Error(-2, "cell colouring needs more than 32 colours (vertex valence too high)");
+    if (h[0] == 0) break;
+  }
+  FL_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
+  store_colors_kernel<<<nb, tb, 0, st>>>(geo, a.p, m.nc, cnt.p);
+  FL_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  return h[0] + 1;
+}
+
+// ---------------------------------------------------------------- touching pairs
+constexpr int MAXNB = 96;   // distinct neighbours of one cell
+
+template <int D>
+__device__ int neighbours_above(const DevMesh& m, int K, int* out) {
+  int cnt = 0;
+  for (int i = 0; i <= D; ++i) {
+    const int v = m.cells[K * (D + 1) + i];
+    for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
+      const int o = m.patch_cells[p];
+      if (o <= K) continue;
+      bool seen = false;
+      for (int j = 0; j < cnt; ++j) seen |= (out[j] == o);
+      if (!seen && cnt < MAXNB) out[cnt++] = o;
+    }
+  }
+  // insertion sort: pairs sorted by (min, max) as sorted(set) in assembly.py:423
+  for (int i = 1; i < cnt; ++i) {
+    const int x = out[i];
+    int j = i - 1;
+    while (j >= 0 && out[j] > x) { out[j + 1] = out[j]; --j; }
+    out[j + 1] = x;
+  }
+  return cnt;
+}
+
+template <int D>
+__global__ void touch_count_kernel(DevMesh m, int* counts) {
+  const int K = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K >= m.nc) return;
+  int nb[MAXNB];
+  counts[K] = neighbours_above<D>(m, K, nb);
+}
+
+template <int D>
+__global__ void touch_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, TouchPair* pairs, int* ident_k) {
+  const int K = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K >= m.nc) return;
+  const CellGeo A = m.geo[K];
+  ident_k[K] = order_touching(oc, A.ldiam, false);   // assembly.py:658
+  int nb[MAXNB];
+  const int cnt = neighbours_above<D>(m, K, nb);
+  int o = offs[K];
+  for (int t = 0; t < cnt; ++t) {
+    const int K2 = nb[t];
+    const CellGeo B = m.geo[K2];
+    TouchPair tp;
+    tp.c0 = K; tp.c1 = K2;
+    for (int i = 0; i < 5; ++i) tp.locs[i] = -1;
+    for (int i = 0; i < 3; ++i) { tp.vK[i] = -1; tp.vK2[i] = -1; }
+    // hmin = np.minimum(h_K, h_K2) -> |log hmin| (quadrature.py:154-155)
+    const double lmin = (A.diam <= B.diam) ? A.ldiam : B.ldiam;
+    tp.k = order_touching(oc, lmin, false);
+    if constexpr (D == 1) {
+      // assembly.py:435-446: shared vertex first in both cells
+      int sh = -1;
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j)
+          if (A.v[i] == B.v[j]) sh = max(sh, A.v[i]);
+      tp.topo = T_CV;
+      tp.vK[0] = sh; tp.vK[1] = (A.v[0] == sh) ? A.v[1] : A.v[0];
+      tp.vK2[0] = sh; tp.vK2[1] = (B.v[0] == sh) ? B.v[1] : B.v[0];
+      tp.locs[0] = sh; tp.locs[1] = tp.vK[1]; tp.locs[2] = tp.vK2[1];
+      tp.nloc = 3;
+    } else {
+      // assembly.py:452-472: common = sorted(shared); vK = common + restA; vK2 = common + restB
+      int common[3], nc_ = 0;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+          if (A.v[i] == B.v[j]) common[nc_++] = A.v[i];
+      if (nc_ == 2 && common[0] > common[1]) { const int x = common[0]; common[0] = common[1]; common[1] = x; }
+      int ka = 0, kb = 0;
+      for (int i = 0; i < nc_; ++i) { tp.vK[ka++] = common[i]; tp.vK2[kb++] = common[i]; }
+      for (int i = 0; i < 3; ++i) {
+        bool inA = false, inB = false;
+        for (int j = 0; j < nc_; ++j) { inA |= (A.v[i] == common[j]); inB |= (B.v[i] == common[j]); }
+        if (!inA) tp.vK[ka++] = A.v[i];
+        if (!inB) tp.vK2[kb++] = B.v[i];
+      }
+      if (nc_ == 2) {                                  // COMMON_EDGE, 4 locals (:469)
+        tp.topo = T_CE;
+        tp.locs[0] = tp.vK[0]; tp.locs[1] = tp.vK[1]; tp.locs[2] = tp.vK[2]; tp.locs[3] = tp.vK2[2];
+        tp.nloc = 4;
+      } else {                                         // COMMON_VERTEX, 5 locals (:471)
+        tp.topo = T_CV;
+        tp.locs[0] = tp.vK[0]; tp.locs[1] = tp.vK[1]; tp.locs[2] = tp.vK[2];
+        tp.locs[3] = tp.vK2[1]; tp.locs[4] = tp.vK2[2];
+        tp.nloc = 5;
+      }
+    }
+    pairs[o + t] = tp;
+  }
+}
+
+void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>& pairs,
+                       int64_t& npairs, DBuf<int>& ident_k, cudaStream_t st) {
+  const int tb = 128, nb = (m.nc + tb - 1) / tb;
+  DBuf<int> counts(m.nc + 1), offs(m.nc + 1);
+  FL_CUDA(cudaMemsetAsync(counts.p, 0, (m.nc + 1) * sizeof(int), st));
+  if (m.d == 1) touch_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p);
+  else touch_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p);
+  FL_CHECK_LAUNCH();
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offs.p, m.nc + 1, st);
+  DBuf<unsigned char> t(tmp);
+  FL_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, counts.p, offs.p, m.nc + 1, st));
+  int total = 0;
+  FL_CUDA(cudaMemcpyAsync(&total, offs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  npairs = total;
+  pairs.alloc(total > 0 ? total : 1);
+  ident_k.alloc(m.nc);
+  if (m.d == 1) touch_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p);
+  else touch_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p);
+  FL_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- boundary pairs
+template <int D>
+__device__ int edge_cells(const DevMesh& m, int e, int* out) {
+  int cnt = 0;
+  for (int i = 0; i < D; ++i) {
+    const int v = m.bedges[e * D + i];
+    for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
+      const int o = m.patch_cells[p];
+      bool seen = false;
+      for (int j = 0; j < cnt; ++j) seen |= (out[j] == o);
+      if (!seen && cnt < MAXNB) out[cnt++] = o;
+    }
+  }
+  for (int i = 1; i < cnt; ++i) {   // np.unique -> ascending (assembly.py:799)
+    const int x = out[i];
+    int j = i - 1;
+    while (j >= 0 && out[j] > x) { out[j + 1] = out[j]; --j; }
+    out[j + 1] = x;
+  }
+  return cnt;
+}
+
+template <int D>
+__global__ void bnd_count_kernel(DevMesh m, int* counts) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m.nb) return;
+  int cs[MAXNB];
+  counts[e] = edge_cells<D>(m, e, cs);    // every patch cell shares >= 1 vertex
+}
+
+template <int D>
+__global__ void bnd_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, BndPair* items) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m.nb) return;
+  int cs[MAXNB];
+  const int cnt = edge_cells<D>(m, e, cs);
+  int ev[2] = {m.bedges[e * D + 0], D == 2 ? m.bedges[e * D + 1] : -1};
+  for (int t = 0; t < cnt; ++t) {
+    const int c = cs[t];
+    const CellGeo g = m.geo[c];
+    BndPair it;
+    it.cell = c; it.edge = e;
+    int shared[2], ns = 0;
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j <= D; ++j)
+        if (ev[i] == g.v[j]) shared[ns++] = ev[i];
+    if (ns == 2 && shared[0] > shared[1]) { const int x = shared[0]; shared[0] = shared[1]; shared[1] = x; }
+    int order[3] = {-1, -1, -1};
+    int pe[2] = {-1, -1};
+    if (D == 1) {                                  // 1D: boundary point first (:832-835)
+      it.topo = T_EOC;
+      order[0] = ev[0];
+      order[1] = (g.v[0] == ev[0]) ? g.v[1] : g.v[0];
+      pe[0] = ev[0];
+      it.nloc = 2;
+    } else if (ns == 2) {                          // EDGE_OF_CELL (:824-826)
+      it.topo = T_EOC;
+      order[0] = ev[0]; order[1] = ev[1];
+      for (int j = 0; j < 3; ++j)
+        if (g.v[j] != ev[0] && g.v[j] != ev[1]) order[2] = g.v[j];
+      pe[0] = ev[0]; pe[1] = ev[1];
+      it.nloc = 3;
+    } else {                                       // TOUCHING_EDGE (:827-831)
+      it.topo = T_TE;
+      const int sv = shared[0];
+      order[0] = sv;
+      int k = 1;
+      for (int j = 0; j < 3; ++j)
+        if (g.v[j] != sv) order[k++] = g.v[j];
+      pe[0] = sv;
+      pe[1] = (ev[0] == sv) ? ev[1] : ev[0];
+      it.nloc = 3;
+    }
+    for (int j = 0; j < 3; ++j) it.locs[j] = order[j];
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j)
+        it.pe[i][j] = (pe[i] >= 0 && j < D) ? m.vert[pe[i] * D + j] : 0.0;
+    it.ne[0] = -m.bnorm[e * D + 0];
+    it.ne[1] = (D == 2) ? -m.bnorm[e * D + 1] : 0.0;
+    it.k = order_touching(oc, g.ldiam, true);      // select_order(..., boundary=True) :815
+    items[offs[e] + t] = it;
+  }
+}
+
+void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& items,
+                       int64_t& nitems, cudaStream_t st) {
+  nitems = 0;
+  if (m.nb == 0) { items.alloc(1); return; }
+  const int tb = 64, nb = (m.nb + tb - 1) / tb;
+  DBuf<int> counts(m.nb + 1), offs(m.nb + 1);
+  FL_CUDA(cudaMemsetAsync(counts.p, 0, (m.nb + 1) * sizeof(int), st));
+  if (m.d == 1) bnd_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p);
+  else bnd_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p);
+  FL_CHECK_LAUNCH();
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offs.p, m.nb + 1, st);
+  DBuf<unsigned char> t(tmp);
+  FL_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, counts.p, offs.p, m.nb + 1, st));
+  int total = 0;
+  FL_CUDA(cudaMemcpyAsync(&total, offs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  nitems = total;
+  items.alloc(total > 0 ? total : 1);
+  if (m.d == 1) bnd_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p);
+  else bnd_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p);
+  FL_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- DoF tiles
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+__global__ void dof_vertex_kernel(DevMesh m, int* dof_vertex) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= m.nv) return;
+  const int d = m.v2d[v];
+  if (d >= 0) dof_vertex[d] = v;
+}
+__global__ void morton_kernel(DevMesh m, const int* dof_vertex, int r0, int r1, double x0, double y0,
+                              double sx, double sy, uint32_t* keys, int* vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= r1 - r0) return;
+  const int dof = r0 + i;
+  const int v = dof_vertex[dof];
+  uint32_t key;
+  if (m.d == 1) {
+    key = (uint32_t)i;
+  } else {
+    const double fx = (m.vert[2 * v] - x0) * sx, fy = (m.vert[2 * v + 1] - y0) * sy;
+    const uint32_t qx = (uint32_t)fmin(fmax(fx, 0.0), 65535.0);
+    const uint32_t qy = (uint32_t)fmin(fmax(fy, 0.0), 65535.0);
+    key = spread16(qx) | (spread16(qy) << 1);
+  }
+  keys[i] = key;
+  vals[i] = dof;
+}
+
+constexpr int CAND = 1024;
+__global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* sorted_dofs, int nrows,
+                                                         const int* dof_vertex, int* tdofs, int* tncell,
+                                                         int* tcells, int* tslots, int* tcstart, int* err) {
+  const int t = blockIdx.x;
+  __shared__ int sd[TILE];
+  __shared__ unsigned long long key[CAND];
+  __shared__ int ncand;
+  const int tid = threadIdx.x;
+  if (tid < TILE) {
+    const int i = t * TILE + tid;
+    sd[tid] = (i < nrows) ? sorted_dofs[i] : -1;
+    tdofs[t * TILE + tid] = sd[tid];
+  }
+  if (tid == 0) ncand = 0;
+  __syncthreads();
+  if (tid < TILE && sd[tid] >= 0) {
+    const int v = dof_vertex[sd[tid]];
+    for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
+      const int c = m.patch_cells[p];
+      const int slot = atomicAdd(&ncand, 1);
+      if (slot < CAND) key[slot] = ((unsigned long long)(unsigned)m.geo[c].color << 32) | (unsigned)c;
+    }
+  }
+  __syncthreads();
+  const int nc_ = ncand;
+  if (nc_ > CAND) { if (tid == 0) atomicAdd(err, 1); return; }
+  for (int i = nc_ + tid; i < CAND; i += blockDim.x) key[i] = ~0ull;
+  __syncthreads();
+  // bitonic sort of CAND keys (colour, cell id)
+  for (int k = 2; k <= CAND; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < CAND; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = ((i & k) == 0);
+          const unsigned long long a = key[i], b = key[ixj];
+          if ((a > b) == up) { key[i] = b; key[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // unique (serial; <= CAND entries, once per tile)
+  __shared__ int nuniq;
+  if (tid == 0) {
+    int u = 0;
+    for (int i = 0; i < nc_; ++i)
+      if (i == 0 || key[i] != key[i - 1]) key[u++] = key[i];
+    nuniq = u;
+  }
+  __syncthreads();
+  const int nu = nuniq;
+  if (nu > TILE_MAXC) { if (tid == 0) atomicAdd(err, 1); return; }
+  if (tid == 0) tncell[t] = nu;
+  for (int i = tid; i < nu; i += blockDim.x) {
+    const int c = (int)(key[i] & 0xffffffffu);
+    tcells[t * TILE_MAXC + i] = c;
+    for (int a = 0; a < 3; ++a) {
+      int slot = -1;
+      if (a <= m.d) {
+        const int dof = m.v2d[m.cells[c * (m.d + 1) + a]];
+        if (dof >= 0)
+          for (int r = 0; r < TILE; ++r)
+            if (sd[r] == dof) slot = r;
+      }
+      tslots[(t * TILE_MAXC + i) * 3 + a] = slot;
+    }
+  }
+  // colour class starts
+  for (int col = tid; col <= MAXCOLORS; col += blockDim.x) {
+    int lo = 0;
+    while (lo < nu && (int)(key[lo] >> 32) < col) ++lo;
+    tcstart[t * (MAXCOLORS + 1) + col] = lo;
+  }
+}
+
+void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStream_t st) {
+  const int nrows = row_end - row_begin;
+  T.ntiles = (nrows + TILE - 1) / TILE;
+  DBuf<int> dof_vertex(m.n > 0 ? m.n : 1);
+  dof_vertex_kernel<<<(m.nv + 255) / 256, 256, 0, st>>>(m, dof_vertex.p);
+  // bounding box of the vertices (host copy is not available here; reduce on device)
+  double bb[4] = {0, 1, 0, 1};
+  if (m.d == 2) {
+    std::vector<double> hv((size_t)m.nv * 2);
+    FL_CUDA(cudaMemcpyAsync(hv.data(), m.vert, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    bb[0] = bb[1] = hv[0]; bb[2] = bb[3] = hv[1];
+    for (int v = 0; v < m.nv; ++v) {
+      bb[0] = std::min(bb[0], hv[2 * v]); bb[1] = std::max(bb[1], hv[2 * v]);
+      bb[2] = std::min(bb[2], hv[2 * v + 1]); bb[3] = std::max(bb[3], hv[2 * v + 1]);
+    }
+  }
+  const double sx = 65535.0 / std::max(bb[1] - bb[0], 1e-300), sy = 65535.0 / std::max(bb[3] - bb[2], 1e-300);
+  DBuf<uint32_t> keys(nrows), keys2(nrows);
+  DBuf<int> vals(nrows), vals2(nrows);
+  morton_kernel<<<(nrows + 255) / 256, 256, 0, st>>>(m, dof_vertex.p, row_begin, row_end, bb[0], bb[2],
+                                                    sx, sy, keys.p, vals.p);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.p, keys2.p, vals.p, vals2.p, nrows, 0, 32, st);
+  DBuf<unsigned char> tb(tmp);
+  FL_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, keys.p, keys2.p, vals.p, vals2.p, nrows, 0, 32, st));
+  T.dofs.alloc((size_t)T.ntiles * TILE);
+  T.ncell.alloc(T.ntiles);
+  T.cells.alloc((size_t)T.ntiles * TILE_MAXC);
+  T.slots.alloc((size_t)T.ntiles * TILE_MAXC * 3);
+  T.cstart.alloc((size_t)T.ntiles * (MAXCOLORS + 1));
+  DBuf<int> err(1);
+  FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
+  tile_cells_kernel<<<T.ntiles, 256, 0, st>>>(m, vals2.p, nrows, dof_vertex.p, T.dofs.p, T.ncell.p,
+                                              T.cells.p, T.slots.p, T.cstart.p, err.p);
+  FL_CHECK_LAUNCH();
+  int herr = 0;
+  FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  if (herr) throw Error(-2, "DoF tile touches more than 256 cells (vertex valence too high)");
+}
+
+}  // namespace fl

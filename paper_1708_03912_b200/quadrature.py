@@ -1,0 +1,451 @@
+"""Quadrature rules, pair classification and Gauss-order selection — host side.
+
+Mirrors `fraclap.quadrature` (reference quadrature.py): the same public names and
+argument meaning.  The node sets are produced by the same third-party generators the
+reference calls (numpy `leggauss`, scipy `roots_jacobi`), and the Sauter–Schwab/Duffy
+payload transforms are restated here (quadrature.py:188-398) so the device tables are
+bitwise the reference's payloads (pinned by tests/test_tables.py).
+
+`pack_tables(d, s)` flattens every rule the device kernels can ask for into the
+`fl_tables` blob of include/fraclap_b200.h.
+"""
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass
+from enum import Enum
+from functools import lru_cache
+
+import numpy as np
+from numpy.polynomial.legendre import leggauss
+from scipy.special import roots_jacobi
+
+log = logging.getLogger(__name__)
+
+K_MAX = 32                    # quadrature.py:35
+XQ_ORDER = {1: 6, 2: 4}       # assembly.py:635
+EDGE_GL_ORDER = 8             # assembly.py:43
+
+
+class PairTopology(Enum):
+    """quadrature.py:38-46."""
+    IDENTICAL = "identical"
+    COMMON_EDGE = "common_edge"
+    COMMON_VERTEX = "common_vertex"
+    DISJOINT = "disjoint"
+    EDGE_OF_CELL = "edge_of_cell"
+    TOUCHING_EDGE = "touching_edge"
+    DISJOINT_EDGE = "disjoint_edge"
+
+
+class QuadratureError(RuntimeError):
+    """quadrature.py:49."""
+
+
+# ids of the device table directory (include/fraclap_b200.h FL_TOPO_*)
+TOPO_ID = {PairTopology.IDENTICAL: 0, PairTopology.COMMON_EDGE: 1, PairTopology.COMMON_VERTEX: 2,
+           PairTopology.DISJOINT: 3, PairTopology.EDGE_OF_CELL: 4, PairTopology.TOUCHING_EDGE: 5}
+TOPO_CELL, TOPO_EDGE_GL, NTOPO, KDIR, NODE = 6, 7, 8, 33, 8
+
+
+# ------------------------------------------------------------------ 1-D rules
+@lru_cache(maxsize=None)
+def gauss_legendre(k: int):
+    """k-point Gauss–Legendre on [0,1] (quadrature.py:53-59)."""
+    if k < 1:
+        raise ValueError("order must be >= 1")
+    t, w = leggauss(k)
+    return 0.5 * (t + 1.0), 0.5 * w
+
+
+@lru_cache(maxsize=None)
+def gauss_jacobi(k: int, alpha: float):
+    """k-point Gauss rule on [0,1] for the weight t^alpha (quadrature.py:62-68)."""
+    if alpha <= -1:
+        raise ValueError("weight exponent must be > -1")
+    t, w = roots_jacobi(k, alpha, 0.0)
+    return 0.5 * (1.0 - t), w * 2.0 ** (-alpha - 1.0)
+
+
+@lru_cache(maxsize=None)
+def triangle_rule(k: int):
+    """Collapsed (Duffy) tensor rule on the unit triangle (quadrature.py:71-78)."""
+    t, wt = gauss_legendre(k)
+    a, b = np.meshgrid(t, t, indexing="ij")
+    w = np.outer(wt, wt) * (1 - a)
+    return np.stack([a, b * (1 - a)], axis=-1).reshape(-1, 2), w.ravel()
+
+
+def simplex_rule(d: int, k: int):
+    """quadrature.py:81-85."""
+    if d == 1:
+        t, w = gauss_legendre(k)
+        return t[:, None], w
+    return triangle_rule(k)
+
+
+# ------------------------------------------------------------------ classification
+def classify_pair(cell_a, cell_b=None, edge=None) -> PairTopology:
+    """By shared-vertex count (quadrature.py:90-110)."""
+    a = set(cell_a)
+    if edge is not None:
+        e = list(edge)
+        shared = len(a & set(e))
+        if shared == len(e):
+            return PairTopology.EDGE_OF_CELL
+        return PairTopology.TOUCHING_EDGE if shared else PairTopology.DISJOINT_EDGE
+    b = set(cell_b)
+    d = len(list(cell_a)) - 1
+    shared = len(a & b)
+    if shared == d + 1:
+        return PairTopology.IDENTICAL
+    if d == 2 and shared == 2:
+        return PairTopology.COMMON_EDGE
+    return PairTopology.COMMON_VERTEX if shared else PairTopology.DISJOINT
+
+
+# ------------------------------------------------------------------ order selection
+@dataclass
+class OrderParams:
+    """quadrature.py:115-131."""
+    rho1: float = 2.0
+    rho2: float = 2.0
+    rho3: float = 2.0
+    rho4: float = 2.0
+    C_offset: float = 1.0
+    alpha: float | None = None
+
+    def __post_init__(self):
+        if min(self.rho1, self.rho2, self.rho3, self.rho4) <= 1:
+            raise ValueError("all rho parameters must exceed 1")
+
+    def target_alpha(self, d, s):
+        if self.alpha is not None:
+            return self.alpha
+        return 2.0 - s if d == 1 else 1.0
+
+
+_TOUCHING = (PairTopology.IDENTICAL, PairTopology.COMMON_EDGE, PairTopology.COMMON_VERTEX,
+             PairTopology.EDGE_OF_CELL, PairTopology.TOUCHING_EDGE)
+
+
+def select_order(pair, h_K, h_K2, dist, n, s, params: OrderParams, boundary=False, d=2):
+    """Gauss points per direction (quadrature.py:138-179).  Host restatement; the device
+    evaluates the same expression per pair (csrc/fl_device.cuh order_*)."""
+    h_K = np.asarray(h_K, float)
+    h_K2 = np.asarray(h_K2, float)
+    dist = np.asarray(dist, float)
+    lead = params.target_alpha(d, s) / 2 + (0.25 if boundary else 0.5)
+    lnn = np.log(max(float(n), 2.0))
+    if pair in _TOUCHING:
+        rho = params.rho3 if boundary else params.rho1
+        k = (lead * lnn + s * np.abs(np.log(np.minimum(h_K, h_K2)))) / np.log(rho) - params.C_offset
+    else:
+        if np.any(dist <= 0):
+            raise QuadratureError("disjoint pair classified with zero distance")
+        rho = params.rho4 if boundary else params.rho2
+        lK, lK2 = np.abs(np.log(h_K)), np.abs(np.log(h_K2))
+        mx = np.maximum(lK, lK2)
+
+        def one(ha, hb, lhb):
+            num = lead * lnn + (s - 1) * lhb + mx - s * np.log(dist / hb) - params.C_offset
+            return num / (np.maximum(np.log(np.maximum(dist / ha, 1e-300)), 0.0) + np.log(rho))
+
+        k = np.maximum(one(h_K, h_K2, lK2), one(h_K2, h_K, lK))
+    k = np.ceil(k)
+    cap = 9 if (pair not in _TOUCHING and d == 2) else K_MAX
+    if np.any(k > cap):
+        log.info("quadrature order clamped to %d for %d pair(s)", cap, int(np.sum(k > cap)))
+    return np.clip(k, 2, cap).astype(np.int64)
+
+
+# ------------------------------------------------------------------ singular payloads
+# Each returns dict(x=..., y=... | a=..., w=...) in the reference's node order.
+_HEX = np.array([(1, 0), (0, 1), (-1, 1), (-1, 0), (0, -1), (1, -1)], float)
+
+
+def _hex_area(w):
+    """Area of the identical-pair sub-domain at offset w (quadrature.py:191-198)."""
+    w1, w2 = w[..., 0], w[..., 1]
+    t = w1 + w2
+    out = np.where(w1 > 0, np.where(t >= 0, (1 - w1) ** 2, (1 + w2) ** 2),
+                   np.where(t >= 0, (1 - w2) ** 2, (1 + w1) ** 2))
+    out = np.where((w1 <= 0) & (w2 <= 0), (1 + t) ** 2, out)
+    out = np.where((w1 >= 0) & (w2 >= 0), (1 - t) ** 2, out)
+    return 0.5 * out
+
+
+def _hex_rep(w):
+    """Representative point x of the identical-pair sub-domain (quadrature.py:201-218)."""
+    w1, w2 = w[..., 0], w[..., 1]
+    t = w1 + w2
+    cx, cy = np.empty_like(w1), np.empty_like(w2)
+    quad = (w1 >= 0) & (w2 >= 0)
+    cases = [
+        (quad, w1 + (1 - t) / 3, w2 + (1 - t) / 3),
+        ((w1 <= 0) & (w2 <= 0) & ~quad, (1 + t) / 3, (1 + t) / 3),
+        ((w1 > 0) & (w2 < 0) & (t >= 0), (1 + 2 * w1) / 3, (1 - w1) / 3),
+        ((w1 > 0) & (w2 < 0) & (t < 0), w1 + (1 + w2) / 3, (1 + w2) / 3),
+        ((w1 < 0) & (w2 > 0) & (t >= 0), (1 - w2) / 3, (1 + 2 * w2) / 3),
+        ((w1 < 0) & (w2 > 0) & (t < 0), (1 + w1) / 3, w2 + (1 + w1) / 3),
+    ]
+    for m, vx, vy in cases:
+        cx[m] = vx[m]
+        cy[m] = vy[m]
+    return np.stack([cx, cy], axis=-1)
+
+
+@lru_cache(maxsize=None)
+def rule_identical_1d(s):
+    """quadrature.py:221-230."""
+    z, wz = gauss_jacobi(3, 1 - 2 * s)
+    w = wz * (1 - z) * z ** (2 * s - 1)
+    xp, xm = (1 + z) / 2, (1 - z) / 2
+    return dict(x=np.concatenate([xp, xm]), y=np.concatenate([xp - z, xm + z]),
+                w=np.concatenate([w, w]))
+
+
+@lru_cache(maxsize=None)
+def rule_vertex_1d(k, s):
+    """Both cells parametrised away from the shared vertex (quadrature.py:233-243)."""
+    tq, tw = gauss_jacobi(3, 2 - 2 * s)
+    vq, vw = gauss_legendre(k)
+    T, V = np.meshgrid(tq, vq, indexing="ij")
+    W = np.outer(tw * tq ** (2 * s - 1), vw).ravel()
+    TV = (T * V).ravel()
+    return dict(x=np.concatenate([T.ravel(), TV]), y=np.concatenate([TV, T.ravel()]),
+                w=np.concatenate([W, W]))
+
+
+@lru_cache(maxsize=None)
+def rule_identical_2d(k, s):
+    """Six radial sectors of the hexagon of offsets (quadrature.py:246-260)."""
+    t, wt = gauss_legendre(k)
+    rq, rw = gauss_jacobi(3, 1 - 2 * s)
+    xs, ys, ws = [], [], []
+    for sector in range(6):
+        edge = (1 - t)[:, None] * _HEX[sector] + t[:, None] * _HEX[(sector + 1) % 6]
+        for r, wr in zip(rq, rw):
+            off = r * edge
+            x = _hex_rep(off)
+            xs.append(x)
+            ys.append(x - off)
+            ws.append(wt * wr * _hex_area(off) * r ** (2 * s))
+    return dict(x=np.concatenate(xs), y=np.concatenate(ys), w=np.concatenate(ws))
+
+
+@lru_cache(maxsize=None)
+def rule_common_edge_2d(k, s):
+    """Shared edge = local (0,1) of both cells (quadrature.py:263-294)."""
+    k = min(k, 16)
+    z, wz = gauss_legendre(k)
+    v, wv = gauss_legendre(k)
+    rq, rw = gauss_jacobi(3, 2 - 2 * s)
+    Z, V = np.meshgrid(z, v, indexing="ij")
+    WZV = np.outer(wz, wv)
+    X, Y, W = [], [], []
+    for swap in (False, True):
+        for second in (False, True):
+            for r, wr in zip(rq, rw):
+                if second:
+                    zz, bb, bp, jac = r * V * Z, r * V * (1 - Z), np.full_like(Z, r), V
+                else:
+                    zz, bb, bp, jac = r * Z, r * (1 - Z), r * V, np.ones_like(Z)
+                al = zz + 0.5 * (1 - r)
+                u = np.stack([al, bb], -1).reshape(-1, 2)
+                uu = np.stack([al - zz, bp], -1).reshape(-1, 2)
+                wts = (WZV * jac).reshape(-1) * wr * (1 - r) * r ** (2 * s)
+                X.append(uu if swap else u)
+                Y.append(u if swap else uu)
+                W.append(wts)
+    return dict(x=np.concatenate(X), y=np.concatenate(Y), w=np.concatenate(W))
+
+
+def _cv_order(k):
+    return max(2, min(8, (k + 1) // 2 + 1))
+
+
+@lru_cache(maxsize=None)
+def _rule_common_vertex_2d(kk, s):
+    su, wsu = gauss_legendre(kk)
+    wr_, wwr = gauss_legendre(kk)
+    rq, rw = gauss_jacobi(3, 3 - 2 * s)
+    SU, SV, WW = np.meshgrid(su, su, wr_, indexing="ij")
+    WT = wsu[:, None, None] * wsu[None, :, None] * wwr[None, None, :]
+    X, Y, W = [], [], []
+    for second in (False, True):
+        for r, wr in zip(rq, rw):
+            rx = (r * WW) if second else np.full_like(WW, r)
+            ry = np.full_like(WW, r) if second else (r * WW)
+            X.append(np.stack([rx * (1 - SU), rx * SU], -1).reshape(-1, 2))
+            Y.append(np.stack([ry * (1 - SV), ry * SV], -1).reshape(-1, 2))
+            W.append((WT * WW).reshape(-1) * wr * r ** (2 * s))
+    return dict(x=np.concatenate(X), y=np.concatenate(Y), w=np.concatenate(W))
+
+
+def rule_common_vertex_2d(k, s):
+    """Shared vertex = local 0 of both cells (quadrature.py:297-315)."""
+    return _rule_common_vertex_2d(_cv_order(k), s)
+
+
+@lru_cache(maxsize=None)
+def rule_edge_of_cell_1d(s, vanishing):
+    """quadrature.py:332-335."""
+    rq, rw = gauss_jacobi(3, vanishing - 2 * s)
+    return dict(x=rq, a=np.zeros_like(rq), w=rw * rq ** (2 * s - vanishing))
+
+
+@lru_cache(maxsize=None)
+def rule_edge_of_cell_2d(k, s, vanishing):
+    """Cell (e0, e1, p) and its boundary edge (e0, e1) (quadrature.py:338-360)."""
+    zq, zw = gauss_legendre(k)
+    tq, tw = gauss_legendre(max(3, k // 2))
+    rq, rw = gauss_jacobi(4, vanishing - 2 * s)
+    Z, T = np.meshgrid(zq, tq, indexing="ij")
+    WZT = np.outer(zw, tw)
+    X, A, W = [], [], []
+    for piece in (1, 2, 3):
+        for r, wr in zip(rq, rw):
+            if piece == 1:
+                zrel, beta = r * Z, r * (1 - Z)
+                al = zrel + T * (1 - r)
+            elif piece == 2:
+                beta, zrel, al = r * Z, np.full_like(Z, -r), T * (1 - r)
+            else:
+                beta, zrel, al = np.full_like(Z, r), -r * Z, T * (1 - r)
+            X.append(np.stack([al, beta], -1).reshape(-1, 2))
+            A.append((al - zrel).reshape(-1))
+            W.append((WZT * (1 - r)).reshape(-1) * wr * r ** (1 + 2 * s - vanishing))
+    return dict(x=np.concatenate(X), a=np.concatenate(A), w=np.concatenate(W))
+
+
+@lru_cache(maxsize=None)
+def rule_touching_edge_2d(k, s):
+    """Cell (c, A, B), edge leaving the shared vertex c (quadrature.py:363-384)."""
+    kk = max(2, (k + 1) // 2 + 1)
+    sq, sw = gauss_legendre(kk)
+    wq, ww = gauss_legendre(kk)
+    rq, rw = gauss_jacobi(4, 1 - 2 * s)
+    S, Wg = np.meshgrid(sq, wq, indexing="ij")
+    WW = np.outer(sw, ww)
+    X, A, W = [], [], []
+    for second in (False, True):
+        for xi, wr in zip(rq, rw):
+            if second:
+                ru, ap, jac = xi * Wg, np.full_like(Wg, xi), Wg
+            else:
+                ru, ap, jac = np.full_like(Wg, xi), xi * Wg, np.ones_like(Wg)
+            X.append(np.stack([ru * (1 - S), ru * S], -1).reshape(-1, 2))
+            A.append(ap.reshape(-1))
+            W.append((WW * jac).reshape(-1) * wr * xi ** (1 + 2 * s))
+    return dict(x=np.concatenate(X), a=np.concatenate(A), w=np.concatenate(W))
+
+
+def payload(topology: PairTopology, k: int, s: float, d: int, vanishing=0):
+    """Same contract as reference_payload (quadrature.py:401-420)."""
+    T = PairTopology
+    if topology is T.IDENTICAL:
+        return rule_identical_1d(s) if d == 1 else rule_identical_2d(min(k, 24), s)
+    if topology is T.COMMON_EDGE:
+        if d != 2:
+            raise QuadratureError("common-edge pairs exist in 2D only")
+        return rule_common_edge_2d(k, s)
+    if topology is T.COMMON_VERTEX:
+        return rule_vertex_1d(k, s) if d == 1 else rule_common_vertex_2d(k, s)
+    if topology is T.DISJOINT:
+        px, wx = simplex_rule(d, k)
+        nx = len(wx)
+        x = np.repeat(px, nx, axis=0)
+        y = np.tile(px, (nx, 1))
+        w = np.outer(wx, wx).ravel()
+        return dict(x=x.ravel(), y=y.ravel(), w=w) if d == 1 else dict(x=x, y=y, w=w)
+    if topology is T.EDGE_OF_CELL:
+        return rule_edge_of_cell_1d(s, vanishing) if d == 1 else rule_edge_of_cell_2d(k, s, vanishing)
+    if topology is T.TOUCHING_EDGE:
+        if d != 2:
+            raise QuadratureError("1D boundary points touching a cell are EDGE_OF_CELL")
+        return rule_touching_edge_2d(k, s)
+    if topology is T.DISJOINT_EDGE:
+        px, wx = simplex_rule(d, k)
+        if d == 1:
+            return dict(x=px.ravel(), a=np.zeros(len(wx)), w=wx)
+        aq, aw = gauss_legendre(k)
+        return dict(x=np.repeat(px, k, axis=0), a=np.tile(aq, len(wx)), w=np.outer(wx, aw).ravel())
+    raise QuadratureError("unsupported topology %r" % topology)
+
+
+# ------------------------------------------------------------------ device tables
+def _lam(d, pts):
+    if d == 1:
+        return np.stack([1 - pts[:, 0], pts[:, 0]], axis=1)
+    return np.stack([1 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], axis=1)
+
+
+@lru_cache(maxsize=16)
+def pack_tables(d: int, s: float):
+    """All rules of one (d, s) in the fl_tables layout: (dir int64[8*33*2], data float64)."""
+    if not 0.0 < s < 1.0:
+        raise ValueError("s must lie in (0,1)")
+    recs = []          # (topo_id, k, records[N, 8])
+    T = PairTopology
+    vanish = 0 if s < 0.5 else 2          # assembly.py:794
+
+    def pair_rec(p):
+        N = len(p["w"])
+        r = np.zeros((N, NODE))
+        x = np.asarray(p["x"], float).reshape(N, -1)
+        y = np.asarray(p["y"], float).reshape(N, -1)
+        r[:, 0:x.shape[1]] = x
+        r[:, 2:2 + y.shape[1]] = y
+        r[:, 4] = p["w"]
+        return r
+
+    def edge_rec(p):
+        N = len(p["w"])
+        r = np.zeros((N, NODE))
+        x = np.asarray(p["x"], float).reshape(N, -1)
+        r[:, 0:x.shape[1]] = x
+        r[:, 2] = p["a"]
+        r[:, 3] = p["w"]
+        return r
+
+    def cell_rec(pts, w, weighted):
+        N = len(w)
+        r = np.zeros((N, NODE))
+        r[:, 0:pts.shape[1]] = pts
+        r[:, 2] = w
+        lam = _lam(d, pts)
+        r[:, 3:3 + lam.shape[1]] = lam * w[:, None] if weighted else lam
+        return r
+
+    if d == 1:
+        recs.append((0, 0, pair_rec(rule_identical_1d(s))))
+        for k in range(2, K_MAX + 1):
+            recs.append((2, k, pair_rec(rule_vertex_1d(k, s))))
+        recs.append((4, 0, edge_rec(rule_edge_of_cell_1d(s, vanish))))
+    else:
+        for k in range(2, K_MAX + 1):
+            recs.append((0, k, pair_rec(rule_identical_2d(min(k, 24), s))))
+            recs.append((1, k, pair_rec(rule_common_edge_2d(k, s))))
+            recs.append((2, k, pair_rec(rule_common_vertex_2d(k, s))))
+            recs.append((4, k, edge_rec(rule_edge_of_cell_2d(k, s, vanish))))
+            recs.append((5, k, edge_rec(rule_touching_edge_2d(k, s))))
+    for k in range(2, (K_MAX if d == 1 else 9) + 1):
+        pts, w = simplex_rule(d, k)
+        recs.append((3, k, cell_rec(pts, w, True)))
+    pts, w = simplex_rule(d, XQ_ORDER[d])
+    recs.append((TOPO_CELL, 0, cell_rec(pts, w, False)))
+    t, w = gauss_legendre(EDGE_GL_ORDER)
+    er = np.zeros((len(w), NODE))
+    er[:, 0], er[:, 1] = t, w
+    recs.append((TOPO_EDGE_GL, 0, er))
+    dir_ = np.zeros((NTOPO * KDIR, 2), np.int64)
+    off = 0
+    for topo, k, r in recs:
+        dir_[topo * KDIR + k] = (off, len(r))
+        off += len(r)
+    data = np.ascontiguousarray(np.concatenate([r for _, _, r in recs]).ravel())
+    dir_ = np.ascontiguousarray(dir_.ravel())
+    dir_.setflags(write=False)
+    data.setflags(write=False)
+    return dir_, data

@@ -1,0 +1,54 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+    config.addinivalue_line("markers", "slow: long CPU test (oracle at full BASELINE size)")
+
+
+def golden(name):
+    path = os.path.join(GOLDEN, name + ".npz")
+    if not os.path.exists(path):
+        pytest.skip("golden fixture %s.npz not generated" % name)
+    return np.load(path, allow_pickle=False)
+
+
+def make_mesh(kind, N):
+    from paper_1708_03912_b200 import mesh as M
+    if kind == "uniform1d":
+        return M.build_interval_mesh(-1.0, 1.0, N)
+    if kind == "graded1d":
+        return M.build_graded_interval_mesh(N)
+    if kind == "square2d":
+        return M.build_unit_square_mesh(N)
+    raise ValueError(kind)
+
+
+def small_cases():
+    path = os.path.join(GOLDEN, "small.npz")
+    if not os.path.exists(path):
+        return []
+    keys = sorted({k.split("/")[0] for k in np.load(path).files})
+    out = []
+    for key in keys:
+        kind, N, s = key.rsplit("_", 2)
+        out.append((key, kind, int(N), float(s)))
+    return out
+
+
+@pytest.fixture(scope="session")
+def cuda_lib():
+    from paper_1708_03912_b200 import _lib
+    lib = _lib.load()
+    if lib.fl_device_count() < 1:
+        pytest.fail("GPU test collected but no CUDA device visible")
+    return lib
