@@ -121,7 +121,7 @@ typedef struct fl_assembly_stats {
   /* kernel evaluations (quadrature node pairs) actually performed */
   double evals_cross, evals_tail, evals_singular, evals_boundary;
   /* device milliseconds per phase (CUDA events on the assembly stream) */
-  double ms_prep, ms_singular, ms_tail, ms_cross, ms_local, ms_total;
+  double ms_prep, ms_singular, ms_tail, ms_flux, ms_tiles, ms_cross, ms_local, ms_total;
   int64_t cross_tile_pairs;
   int32_t ncolors, ntiles;
 } fl_assembly_stats;
@@ -130,6 +130,8 @@ typedef struct fl_assembly_stats {
 int32_t fl_abi_version(void);
 const char* fl_last_error(void);
 int32_t fl_device_count(void);
+/* number of CUDA kernel launches this library has issued so far (graph replays included) */
+int64_t fl_launch_count(void);
 
 /* ------------------------------------------------------------- assembly
  * Replaces assembly.assemble_dense (assembly.py:1059-1104) for the rows
@@ -184,6 +186,13 @@ int32_t fl_xpby_async(int64_t m, const double* z, double beta, double* p, void* 
 int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
                         const fl_order_params* params, int32_t device,
                         int8_t* cross_k, int8_t* tail_k);
+/* Exact histograms (index = k, 33 bins) of the same orders, accumulated on the device —
+ * usable at every BASELINE size (no nc*nc host arrays). */
+int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                            const fl_order_params* params, int32_t device, int64_t* cross_hist,
+                            int64_t* tail_hist);
+/* Measured FP64 FMA peak of the device (TFLOP/s), the roofline denominator of assembly. */
+int32_t fl_probe_fp64_peak(int32_t device, double* tflops);
 /* Touching pairs as classify/canonicalize produce them (assembly.py:412-473):
  * host outputs sized by *npairs (call with pairs==NULL first to get the count). */
 int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,

@@ -16,11 +16,12 @@ LIB_PATH = os.path.join(_HERE, "lib", "libfraclap_b200.so")
 FL_OK, FL_E_ARG, FL_E_ASSEMBLY, FL_E_QUAD, FL_E_SOLVER, FL_E_CUDA, FL_E_OOM = 0, -1, -2, -3, -4, -5, -6
 VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
 
-EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_assemble_dense", "fl_dense_from_host",
+EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_count", "fl_assemble_dense",
+           "fl_dense_from_host",
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_diag", "fl_matvec",
            "fl_matvec_async", "fl_pcg", "fl_cg_update_async", "fl_dot_async", "fl_xpby_async",
-           "fl_debug_orders", "fl_debug_touching"]
+           "fl_debug_orders", "fl_debug_order_hist", "fl_probe_fp64_peak", "fl_debug_touching"]
 
 
 class fl_mesh(C.Structure):
@@ -56,7 +57,8 @@ class fl_assembly_stats(C.Structure):
                 ("pairs_tail", C.c_int64), ("pairs_boundary_singular", C.c_int64),
                 ("pairs_boundary_flux", C.c_int64), ("evals_cross", C.c_double), ("evals_tail", C.c_double),
                 ("evals_singular", C.c_double), ("evals_boundary", C.c_double), ("ms_prep", C.c_double),
-                ("ms_singular", C.c_double), ("ms_tail", C.c_double), ("ms_cross", C.c_double),
+                ("ms_singular", C.c_double), ("ms_tail", C.c_double), ("ms_flux", C.c_double),
+                ("ms_tiles", C.c_double), ("ms_cross", C.c_double),
                 ("ms_local", C.c_double), ("ms_total", C.c_double), ("cross_tile_pairs", C.c_int64),
                 ("ncolors", C.c_int32), ("ntiles", C.c_int32)]
 
@@ -81,6 +83,7 @@ def load():
         "fl_abi_version": (C.c_int32, []),
         "fl_last_error": (C.c_char_p, []),
         "fl_device_count": (C.c_int32, []),
+        "fl_launch_count": (C.c_int64, []),
         "fl_assemble_dense": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),
                                           P(fl_tables), C.c_int64, C.c_int64, C.c_int64, C.c_int32, vp,
                                           P(vp)]),
@@ -98,6 +101,9 @@ def load():
         "fl_xpby_async": (C.c_int32, [C.c_int64, vp, C.c_double, vp, vp]),
         "fl_debug_orders": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), C.c_int32,
                                         vp, vp]),
+        "fl_debug_order_hist": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),
+                                            C.c_int32, vp, vp]),
+        "fl_probe_fp64_peak": (C.c_int32, [C.c_int32, P(C.c_double)]),
         "fl_debug_touching": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), C.c_int32,
                                           P(C.c_int64), vp, vp, vp, vp]),
     }

@@ -94,13 +94,15 @@ def assemble_dense_device(mesh, dofmap, kernel, params: OrderParams | None = Non
     return DenseDeviceOperator(handle, n, r0, r1)
 
 
-def assemble_dense(mesh, dofmap, kernel, params: OrderParams | None = None, n_limit=DENSE_LIMIT):
-    """Dense stiffness matrix, all cell pairs (assembly.py:1059-1104) -> np.ndarray (n, n)."""
+def assemble_dense(mesh, dofmap, kernel, params: OrderParams | None = None, n_limit=DENSE_LIMIT, *,
+                   out=None):
+    """Dense stiffness matrix, all cell pairs (assembly.py:1059-1104) -> np.ndarray (n, n).
+    `out` (keyword only): a preallocated C-contiguous (n, n) float64 array, e.g. pinned."""
     if dofmap.n > n_limit:
         raise AssemblyError("dense assembly refused beyond %d dofs" % n_limit)
     op = assemble_dense_device(mesh, dofmap, kernel, params, n_limit=n_limit)
     try:
-        return op.to_host()
+        return op.to_host(out)
     finally:
         op.free()
 

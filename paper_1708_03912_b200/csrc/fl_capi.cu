@@ -17,6 +17,13 @@
 
 using namespace fl;
 
+namespace fl {
+long long& launch_counter() {
+  static long long c = 0;
+  return c;
+}
+}  // namespace fl
+
 struct fl_dense {
   int device = 0;
   int64_t n = 0, row0 = 0, row1 = 0, lda = 0;
@@ -47,6 +54,7 @@ static int32_t fail(int code, const std::string& msg) {
 extern "C" {
 
 int32_t fl_abi_version(void) { return FL_ABI_VERSION; }
+int64_t fl_launch_count(void) { return launch_counter(); }
 const char* fl_last_error(void) { return g_err.c_str(); }
 int32_t fl_device_count(void) {
   int c = 0;
@@ -246,8 +254,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
 
   // target cells: cells with a vertex DoF in the owned rows
   DBuf<int> flags(m.nc), all(m.nc), targets(m.nc), nsel(1);
-  flag_target_cells<<<(m.nc + 255) / 256, 256, 0, st>>>(m, (int)row_begin, (int)row_end, flags.p);
-  iota2<<<(m.nc + 255) / 256, 256, 0, st>>>(all.p, m.nc);
+  flag_target_cells<<<(m.nc + 255) / 256, 256, 0, st>>>(m, (int)row_begin, (int)row_end, flags.p), ::fl::note_launch();
+  iota2<<<(m.nc + 255) / 256, 256, 0, st>>>(all.p, m.nc), ::fl::note_launch();
   {
     size_t tmp = 0;
     cub::DeviceSelect::Flagged(nullptr, tmp, all.p, flags.p, targets.p, nsel.p, m.nc, st);
@@ -258,7 +266,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   int ntargets = 0;
   FL_CUDA(cudaMemcpyAsync(&ntargets, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   DBuf<int> row_vertex(n > 0 ? n : 1);
-  dof_vertex2<<<(m.nv + 255) / 256, 256, 0, st>>>(m, row_vertex.p);
+  dof_vertex2<<<(m.nv + 255) / 256, 256, 0, st>>>(m, row_vertex.p), ::fl::note_launch();
 
   // classification (quadrature.py:90-110, assembly.py:412-473, :784-841)
   DBuf<TouchPair> tpairs;
@@ -280,11 +288,14 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   tm.mark();  // 2
 
   // tail + flux at the nodes of the target cells
+  DBuf<unsigned long long> evc(2);
+  FL_CUDA(cudaMemsetAsync(evc.p, 0, 2 * sizeof(unsigned long long), st));
   DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
   FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
-  launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, st);
-  if (do_bnd) launch_flux(m, U.t, ex, e4, targets.p, ntargets, win.p, st);
+  launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
   tm.mark();  // 3
+  if (do_bnd) launch_flux(m, U.t, ex, e4, targets.p, ntargets, win.p, st);
+  tm.mark();  // 4
 
   // dense rows: cross term tiles, then the local/sparse pull
   D->A.alloc((size_t)std::max<int64_t>(rows, 1) * D->lda);
@@ -295,16 +306,19 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   build_tiles(m, (int)row_begin, (int)row_end, trow, st);
   if (!full) build_tiles(m, 0, (int)n, tcol, st);
   int64_t ntp = 0;
+  tm.mark();  // 5
   launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
-                     D->lda, ncolors, ntp, st);
-  tm.mark();  // 4
+                     D->lda, ncolors, ntp, evc.p + 1, st);
+  tm.mark();  // 6
   DBuf<double> Lc((size_t)m.nc * 9);
   launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
   SparseIndex si;
   build_sparse_index(m, tpairs.p, npairs, bitems.p, nitems, si, st);
   launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
                      (int)row_begin, (int)row_end, D->A.p, D->lda, st);
-  tm.mark();  // 5
+  tm.mark();  // 7
+  unsigned long long hev[2] = {0, 0};
+  FL_CUDA(cudaMemcpyAsync(hev, evc.p, sizeof(hev), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
 
   fl_assembly_stats& S = D->stats;
@@ -315,12 +329,16 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   S.pairs_tail = nc * (nc - 1) - 2 * npairs;
   S.pairs_boundary_singular = nitems;
   S.pairs_boundary_flux = integral ? nc * m.nb : 0;
+  S.evals_tail = (double)hev[0];
+  S.evals_cross = (double)hev[1];
   S.ms_prep = tm.ms(0, 1);
   S.ms_singular = tm.ms(1, 2);
   S.ms_tail = tm.ms(2, 3);
-  S.ms_cross = tm.ms(3, 4);
-  S.ms_local = tm.ms(4, 5);
-  S.ms_total = tm.ms(0, 5);
+  S.ms_flux = tm.ms(3, 4);
+  S.ms_tiles = tm.ms(4, 5);
+  S.ms_cross = tm.ms(5, 6);
+  S.ms_local = tm.ms(6, 7);
+  S.ms_total = tm.ms(0, 7);
   S.cross_tile_pairs = ntp;
   S.ncolors = ncolors;
   S.ntiles = trow.ntiles;
@@ -526,6 +544,48 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
   FL_CUDA(cudaMemcpyAsync(cross_k, ck.p, tot, cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(tail_k, tk.p, tot, cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  cudaStreamDestroy(st);
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                            const fl_order_params* params, int32_t device, int64_t* cross_hist, int64_t* tail_hist) {
+  FL_API_BEGIN
+  if (!mesh || !dofmap || !kernel || !params || !cross_hist || !tail_hist) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
+  const int q = mesh->d == 1 ? 6 : 16;
+  std::vector<double> data((size_t)q * NODE, 0.0);
+  dir[2 * (T_CELL * KDIR + 0) + 1] = q;
+  fl_tables t{dir.data(), data.data(), (int64_t)data.size()};
+  Uploaded U;
+  upload(mesh, dofmap, &t, U, st);
+  const OrderConsts oc = make_order_consts(*params, mesh->d, kernel->s, dofmap->n);
+  DBuf<unsigned long long> h(2 * KDIR);
+  FL_CUDA(cudaMemsetAsync(h.p, 0, 2 * KDIR * sizeof(unsigned long long), st));
+  launch_order_hist(U.m, oc, h.p, h.p + KDIR, st);
+  std::vector<unsigned long long> hh(2 * KDIR);
+  FL_CUDA(cudaMemcpyAsync(hh.data(), h.p, hh.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  for (int i = 0; i < KDIR; ++i) {
+    cross_hist[i] = (int64_t)hh[i];
+    tail_hist[i] = (int64_t)hh[KDIR + i];
+  }
+  cudaStreamDestroy(st);
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_probe_fp64_peak(int32_t device, double* tflops) {
+  FL_API_BEGIN
+  if (!tflops) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *tflops = probe_fp64_tflops(st);
   cudaStreamDestroy(st);
   return FL_OK;
   FL_API_END

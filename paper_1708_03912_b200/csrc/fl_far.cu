@@ -25,7 +25,8 @@ template <int D, int E4>
 __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const double* __restrict__ tab,
                                                                DevTables dir, OrderConsts oc, double ex,
                                                                const int* __restrict__ targets, int ntargets,
-                                                               double* __restrict__ psi) {
+                                                               double* __restrict__ psi,
+                                                               unsigned long long* __restrict__ evals) {
   constexpr int Q = (D == 1) ? 6 : 16;
   constexpr int G = 32 / Q;
   __shared__ double2 s_y[TAIL_WARPS][TAIL_WIN];
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
     if (D == 2) xq1 = m.X[((size_t)K * Q + q) * D + 1];
   }
   double acc = 0.0;
+  unsigned long long nodes = 0;
   for (int s0 = 0; s0 < m.nc; s0 += 32) {
     const int src = s0 + lane;
     int k = 0, nn = 0;
@@ -76,6 +78,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
     s_off[w][lane] = incl - nn;
     s_k[w][lane] = k;
     if (lane == 31) s_off[w][32] = total;
+    nodes += (unsigned long long)total;
     __syncwarp();
     for (int base = 0; base < total; base += TAIL_WIN) {
       const int cnt = min(TAIL_WIN, total - base);
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
 #pragma unroll
   for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, acc, (lane + gg * Q) & 31);
   if (lane < Q) psi[(size_t)K * Q + q] = tot;
+  if (lane == 0 && evals) atomicAdd(evals, nodes * Q);
 }
 
 // ====================================================================== boundary flux
@@ -236,7 +240,9 @@ __global__ void __launch_bounds__(XW * 32) cross_tile_kernel(DevMesh m, const do
                                                              double negC, TileView R, TileView Cv,
                                                              const int2* __restrict__ tpairs, int ncolors,
                                                              int symmetric, int row_begin, int row_end,
-                                                             double* __restrict__ Aout, int64_t lda) {
+                                                             double* __restrict__ Aout, int64_t lda,
+                                                             unsigned long long* __restrict__ evals) {
+  unsigned long long my_evals = 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double (*At)[TILE + 1] = reinterpret_cast<double (*)[TILE + 1]>(smem_raw);
   CellGeo* sR = reinterpret_cast<CellGeo*>(smem_raw + sizeof(double) * TILE * (TILE + 1));
@@ -285,6 +291,7 @@ __global__ void __launch_bounds__(XW * 32) cross_tile_kernel(DevMesh m, const do
             const double dist = dist_estimate<D>(P, Qc);
             const int k = order_disjoint(oc, oc.coff, P, Qc, dist);
             cross_block<D, E4>(tab, dir.rule(T_DISJ, k), K, L, ex, Gm);
+            my_evals += (D == 1) ? (unsigned long long)(k * k) : (unsigned long long)(k * k * k * k);
             have = true;
           }
         }
@@ -311,6 +318,11 @@ __global__ void __launch_bounds__(XW * 32) cross_tile_kernel(DevMesh m, const do
       }
     }
     __syncthreads();
+  }
+  if (evals) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_evals += __shfl_xor_sync(0xffffffffu, my_evals, o);
+    if (lane == 0) atomicAdd(evals, my_evals);
   }
   // write the tile (and its mirror) once
   for (int idx = tid; idx < TILE * TILE; idx += blockDim.x) {
@@ -363,13 +375,13 @@ __global__ void orders_kernel(DevMesh m, OrderConsts oc, int8_t* cross_k, int8_t
   }
 
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
-                 const int* targets, int ntargets, double* psi, cudaStream_t st) {
+                 const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st) {
   if (ntargets <= 0) return;
   const int grid = (ntargets + TAIL_WARPS - 1) / TAIL_WARPS;
   if (m.d == 1) {
-    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi)));
+    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi)));
+    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }
@@ -380,9 +392,9 @@ void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const 
   const int Q = m.q, tot = ntargets * Q, grid = (tot + 127) / 128;
   const RuleRef gl = t.rule(T_EGL, 0);
   if (m.d == 1) {
-    FL_E4_SWITCH(e4, (flux_kernel<1, E4><<<grid, 128, 0, st>>>(m, t.data, gl, ex, targets, ntargets, win)));
+    FL_E4_SWITCH(e4, (flux_kernel<1, E4><<<grid, 128, 0, st>>>(m, t.data, gl, ex, targets, ntargets, win), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCH(e4, (flux_kernel<2, E4><<<grid, 128, 0, st>>>(m, t.data, gl, ex, targets, ntargets, win)));
+    FL_E4_SWITCH(e4, (flux_kernel<2, E4><<<grid, 128, 0, st>>>(m, t.data, gl, ex, targets, ntargets, win), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }
@@ -390,7 +402,7 @@ void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const 
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                         double Cds, const Tiles& rows, const Tiles& cols, bool symmetric, int row_begin,
                         int row_end, double* A, int64_t lda, int ncolors, int64_t& ntilepairs,
-                        cudaStream_t st) {
+                        unsigned long long* evals, cudaStream_t st) {
   std::vector<int2> hp;
   for (int r = 0; r < rows.ntiles; ++r)
     for (int c = symmetric ? r : 0; c < cols.ntiles; ++c) hp.push_back(make_int2(r, c));
@@ -409,13 +421,13 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
       FL_E4_SWITCH(e4, {
         FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<1, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cross_tile_kernel<1, E4><<<grid, XW * 32, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, ncolors,
-                                                            symmetric ? 1 : 0, row_begin, row_end, A, lda);
+                                                            symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
       });
     } else {
       FL_E4_SWITCH(e4, {
         FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<2, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cross_tile_kernel<2, E4><<<grid, XW * 32, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, ncolors,
-                                                            symmetric ? 1 : 0, row_begin, row_end, A, lda);
+                                                            symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
       });
     }
     FL_CHECK_LAUNCH();
@@ -423,12 +435,85 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
   FL_CUDA(cudaStreamSynchronize(st));   // dp is freed on return
 }
 
+// Exact per-order histograms of the disjoint pairs: cross (unordered, normal orders) and
+// tail (ordered, C_offset-4); integer atomics => exact totals at any mesh size.
+template <int D>
+__global__ void order_hist_kernel(DevMesh m, OrderConsts oc, unsigned long long* hc, unsigned long long* ht) {
+  __shared__ unsigned long long sc[KDIR], stl[KDIR];
+  for (int i = threadIdx.x; i < KDIR; i += blockDim.x) { sc[i] = 0; stl[i] = 0; }
+  __syncthreads();
+  const int a = blockIdx.x;
+  const CellGeo A = m.geo[a];
+  for (int b = threadIdx.x; b < m.nc; b += blockDim.x) {
+    if (b == a) continue;
+    const CellGeo B = m.geo[b];
+    if (touching<D>(A, B)) continue;
+    const double dt = dist_estimate<D>(A, B);
+    atomicAdd(&stl[order_disjoint(oc, oc.coff_tail, A, B, dt)], 1ull);
+    if (a < b) atomicAdd(&sc[order_disjoint(oc, oc.coff, A, B, dt)], 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < KDIR; i += blockDim.x) {
+    if (sc[i]) atomicAdd(&hc[i], sc[i]);
+    if (stl[i]) atomicAdd(&ht[i], stl[i]);
+  }
+}
+
+void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,
+                       cudaStream_t st) {
+  if (m.d == 1) order_hist_kernel<1><<<m.nc, 256, 0, st>>>(m, oc, hc, ht), ::fl::note_launch();
+  else order_hist_kernel<2><<<m.nc, 256, 0, st>>>(m, oc, hc, ht), ::fl::note_launch();
+  FL_CHECK_LAUNCH();
+}
+
+// FP64 peak probe: 8 independent DFMA chains per thread, 148*8 CTAs of 256 threads.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1.2345) out[0] = s;
+}
+
+double probe_fp64_tflops(cudaStream_t st) {
+  DBuf<double> out(1);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = sms * 8, iters = 4096;
+  dfma_probe_kernel<<<grid, 256, 0, st>>>(out.p, 64, 0.999999, 1e-7), ::fl::note_launch();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, st);
+    dfma_probe_kernel<<<grid, 256, 0, st>>>(out.p, iters, 0.999999, 1e-7), ::fl::note_launch();
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  FL_CHECK_LAUNCH();
+  const double flops = 2.0 * 8.0 * iters * 256.0 * grid;
+  return flops / (best * 1e-3) / 1e12;
+}
+
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st) {
   const int64_t tot = (int64_t)m.nc * m.nc;
   const int grid = (int)((tot + 255) / 256);
-  if (m.d == 1) orders_kernel<1><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k);
-  else orders_kernel<2><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k);
+  if (m.d == 1) orders_kernel<1><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k), ::fl::note_launch();
+  else orders_kernel<2><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 

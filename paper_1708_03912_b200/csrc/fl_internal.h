@@ -27,6 +27,10 @@ struct Error : std::runtime_error {
 
 #define FL_CHECK_LAUNCH() FL_CUDA(cudaGetLastError())
 
+// Host-side count of kernel launches issued by this library (fl_launch_count()).
+long long& launch_counter();
+inline void note_launch(long long k = 1) { launch_counter() += k; }
+
 // Device buffer with RAII.
 template <class T>
 struct DBuf {
@@ -133,15 +137,19 @@ void launch_singular_boundary(const DevMesh& m, const DevTables& t, double ex, i
 
 // fl_far.cu
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
-                 const int* targets, int ntargets, double* psi /*nc*q*/, cudaStream_t st);
+                 const int* targets, int ntargets, double* psi /*nc*q*/, unsigned long long* evals,
+                 cudaStream_t st);
 void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const int* targets,
                  int ntargets, double* win /*nc*q*/, cudaStream_t st);
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,
                         int e4, double Cds, const Tiles& rows, const Tiles& cols, bool symmetric,
                         int row_begin, int row_end, double* A, int64_t lda, int ncolors,
-                        int64_t& ntilepairs, cudaStream_t st);
+                        int64_t& ntilepairs, unsigned long long* evals, cudaStream_t st);
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
+void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,
+                       cudaStream_t st);
+double probe_fp64_tflops(cudaStream_t st);
 
 // fl_local.cu
 void launch_cell_local(const DevMesh& m, const DevTables& t, double Cds, double s, bool integral,

@@ -52,10 +52,10 @@ void launch_cell_local(const DevMesh& m, const DevTables& t, double Cds, double 
   const int grid = (ntargets + 127) / 128;
   if (m.d == 1)
     cell_local_kernel<1><<<grid, 128, 0, st>>>(m, t.data, cr, Cds, s, integral ? 1 : 0, targets, ntargets, ident,
-                                               psi, win, Lc);
+                                               psi, win, Lc), ::fl::note_launch();
   else
     cell_local_kernel<2><<<grid, 128, 0, st>>>(m, t.data, cr, Cds, s, integral ? 1 : 0, targets, ntargets, ident,
-                                               psi, win, Lc);
+                                               psi, win, Lc), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -103,10 +103,10 @@ void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs
   if (np > 0) {
     DBuf<int> k0(np), k1(np), idx(np), k1s(np);
     si.tp_second.alloc(np);
-    pair_keys_kernel<<<(np + 255) / 256, 256, 0, st>>>(pairs, np, k0.p, k1.p, idx.p);
-    offsets_kernel<<<(np + 1 + 255) / 256, 256, 0, st>>>(k0.p, np, nc, si.tp_first_off.p);  // already sorted by c0
+    pair_keys_kernel<<<(np + 255) / 256, 256, 0, st>>>(pairs, np, k0.p, k1.p, idx.p), ::fl::note_launch();
+    offsets_kernel<<<(np + 1 + 255) / 256, 256, 0, st>>>(k0.p, np, nc, si.tp_first_off.p), ::fl::note_launch();  // already sorted by c0
     sort_by_key(k1.p, idx.p, k1s.p, si.tp_second.p, np, nc, st);                           // stable
-    offsets_kernel<<<(np + 1 + 255) / 256, 256, 0, st>>>(k1s.p, np, nc, si.tp_second_off.p);
+    offsets_kernel<<<(np + 1 + 255) / 256, 256, 0, st>>>(k1s.p, np, nc, si.tp_second_off.p), ::fl::note_launch();
   } else {
     si.tp_second.alloc(1);
     FL_CUDA(cudaMemsetAsync(si.tp_first_off.p, 0, (nc + 1) * sizeof(int), st));
@@ -116,9 +116,9 @@ void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs
   if (ni > 0) {
     DBuf<int> k(ni), idx(ni), ks(ni);
     si.bp_idx.alloc(ni);
-    item_keys_kernel<<<(ni + 255) / 256, 256, 0, st>>>(items, ni, k.p, idx.p);
+    item_keys_kernel<<<(ni + 255) / 256, 256, 0, st>>>(items, ni, k.p, idx.p), ::fl::note_launch();
     sort_by_key(k.p, idx.p, ks.p, si.bp_idx.p, ni, nc, st);
-    offsets_kernel<<<(ni + 1 + 255) / 256, 256, 0, st>>>(ks.p, ni, nc, si.bp_off.p);
+    offsets_kernel<<<(ni + 1 + 255) / 256, 256, 0, st>>>(ks.p, ni, nc, si.bp_off.p), ::fl::note_launch();
   } else {
     si.bp_idx.alloc(1);
     FL_CUDA(cudaMemsetAsync(si.bp_off.p, 0, (nc + 1) * sizeof(int), st));
@@ -210,11 +210,11 @@ void launch_sparse_pull(const DevMesh& m, double Cds, double s, const double* Lc
   if (m.d == 1)
     sparse_pull_kernel<1><<<grid, 128, 0, st>>>(m, Cds, cb, Lc, pairs, tloc, items, bloc, si.tp_first_off.p,
                                                 si.tp_second_off.p, si.tp_second.p, si.bp_off.p, si.bp_idx.p,
-                                                row_vertex, row_begin, row_end, A, lda);
+                                                row_vertex, row_begin, row_end, A, lda), ::fl::note_launch();
   else
     sparse_pull_kernel<2><<<grid, 128, 0, st>>>(m, Cds, cb, Lc, pairs, tloc, items, bloc, si.tp_first_off.p,
                                                 si.tp_second_off.p, si.tp_second.p, si.bp_off.p, si.bp_idx.p,
-                                                row_vertex, row_begin, row_end, A, lda);
+                                                row_vertex, row_begin, row_end, A, lda), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 

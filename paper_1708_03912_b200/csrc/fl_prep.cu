@@ -58,8 +58,8 @@ __global__ void prep_cells_kernel(DevMesh m, CellGeo* geo) {
 
 void launch_prep_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st) {
   const int tb = 128, nb = (m.nc + tb - 1) / tb;
-  if (m.d == 1) prep_cells_kernel<1><<<nb, tb, 0, st>>>(m, geo);
-  else prep_cells_kernel<2><<<nb, tb, 0, st>>>(m, geo);
+  if (m.d == 1) prep_cells_kernel<1><<<nb, tb, 0, st>>>(m, geo), ::fl::note_launch();
+  else prep_cells_kernel<2><<<nb, tb, 0, st>>>(m, geo), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -87,8 +87,8 @@ __global__ void cell_nodes_kernel(DevMesh m, const double* __restrict__ tab, Rul
 void launch_cell_nodes(const DevMesh& m, const DevTables& t, double* X, double* W, cudaStream_t st) {
   const RuleRef r = t.rule(T_CELL, 0);
   const int tot = m.nc * r.cnt, tb = 256;
-  if (m.d == 1) cell_nodes_kernel<1><<<(tot + tb - 1) / tb, tb, 0, st>>>(m, t.data, r, X, W);
-  else cell_nodes_kernel<2><<<(tot + tb - 1) / tb, tb, 0, st>>>(m, t.data, r, X, W);
+  if (m.d == 1) cell_nodes_kernel<1><<<(tot + tb - 1) / tb, tb, 0, st>>>(m, t.data, r, X, W), ::fl::note_launch();
+  else cell_nodes_kernel<2><<<(tot + tb - 1) / tb, tb, 0, st>>>(m, t.data, r, X, W), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -115,7 +115,7 @@ void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf
                    cudaStream_t st) {
   const int m = nc * (d + 1);
   DBuf<int> idx(m), keys_out(m), idx_out(m);
-  iota_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx.p, m);
+  iota_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx.p, m), ::fl::note_launch();
   size_t tmp = 0;
   int bits = 1;
   while ((1 << bits) < nv + 1) ++bits;
@@ -124,8 +124,8 @@ void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf
   FL_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, cells, keys_out.p, idx.p, idx_out.p, m, 0, bits, st));
   off.alloc(nv + 1);
   data.alloc(m);
-  patch_offsets_kernel<<<(m + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p);
-  flat_to_cell_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx_out.p, m, d + 1, data.p);
+  patch_offsets_kernel<<<(m + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p), ::fl::note_launch();
+  flat_to_cell_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx_out.p, m, d + 1, data.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -179,12 +179,12 @@ __global__ void store_colors_kernel(CellGeo* geo, const int* col, int nc, int* m
 int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st) {
   DBuf<int> a(m.nc), b(m.nc), cnt(3);
   const int tb = 256, nb = (m.nc + tb - 1) / tb;
-  fill_kernel<<<nb, tb, 0, st>>>(a.p, m.nc, -1);
+  fill_kernel<<<nb, tb, 0, st>>>(a.p, m.nc, -1), ::fl::note_launch();
   int h[3];
   for (int round = 0; round < 10000; ++round) {
     FL_CUDA(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(int), st));
-    if (m.d == 1) jp_round_kernel<1><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1);
-    else jp_round_kernel<2><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1);
+    if (m.d == 1) jp_round_kernel<1><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1), ::fl::note_launch();
+    else jp_round_kernel<2><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1), ::fl::note_launch();
     FL_CHECK_LAUNCH();
     FL_CUDA(cudaMemcpyAsync(h, cnt.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
     FL_CUDA(cudaStreamSynchronize(st));
@@ -193,7 +193,7 @@ int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st) {
     if (h[0] == 0) break;
   }
   FL_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
-  store_colors_kernel<<<nb, tb, 0, st>>>(geo, a.p, m.nc, cnt.p);
+  store_colors_kernel<<<nb, tb, 0, st>>>(geo, a.p, m.nc, cnt.p), ::fl::note_launch();
   FL_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   return h[0] + 1;
@@ -298,8 +298,8 @@ void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>&
   const int tb = 128, nb = (m.nc + tb - 1) / tb;
   DBuf<int> counts(m.nc + 1), offs(m.nc + 1);
   FL_CUDA(cudaMemsetAsync(counts.p, 0, (m.nc + 1) * sizeof(int), st));
-  if (m.d == 1) touch_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p);
-  else touch_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p);
+  if (m.d == 1) touch_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
+  else touch_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offs.p, m.nc + 1, st);
@@ -311,8 +311,8 @@ void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>&
   npairs = total;
   pairs.alloc(total > 0 ? total : 1);
   ident_k.alloc(m.nc);
-  if (m.d == 1) touch_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p);
-  else touch_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p);
+  if (m.d == 1) touch_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p), ::fl::note_launch();
+  else touch_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -407,8 +407,8 @@ void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& i
   const int tb = 64, nb = (m.nb + tb - 1) / tb;
   DBuf<int> counts(m.nb + 1), offs(m.nb + 1);
   FL_CUDA(cudaMemsetAsync(counts.p, 0, (m.nb + 1) * sizeof(int), st));
-  if (m.d == 1) bnd_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p);
-  else bnd_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p);
+  if (m.d == 1) bnd_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
+  else bnd_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offs.p, m.nb + 1, st);
@@ -419,8 +419,8 @@ void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& i
   FL_CUDA(cudaStreamSynchronize(st));
   nitems = total;
   items.alloc(total > 0 ? total : 1);
-  if (m.d == 1) bnd_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p);
-  else bnd_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p);
+  if (m.d == 1) bnd_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p), ::fl::note_launch();
+  else bnd_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -539,7 +539,7 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   const int nrows = row_end - row_begin;
   T.ntiles = (nrows + TILE - 1) / TILE;
   DBuf<int> dof_vertex(m.n > 0 ? m.n : 1);
-  dof_vertex_kernel<<<(m.nv + 255) / 256, 256, 0, st>>>(m, dof_vertex.p);
+  dof_vertex_kernel<<<(m.nv + 255) / 256, 256, 0, st>>>(m, dof_vertex.p), ::fl::note_launch();
   // bounding box of the vertices (host copy is not available here; reduce on device)
   double bb[4] = {0, 1, 0, 1};
   if (m.d == 2) {
@@ -556,7 +556,7 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   DBuf<uint32_t> keys(nrows), keys2(nrows);
   DBuf<int> vals(nrows), vals2(nrows);
   morton_kernel<<<(nrows + 255) / 256, 256, 0, st>>>(m, dof_vertex.p, row_begin, row_end, bb[0], bb[2],
-                                                    sx, sy, keys.p, vals.p);
+                                                    sx, sy, keys.p, vals.p), ::fl::note_launch();
   size_t tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.p, keys2.p, vals.p, vals2.p, nrows, 0, 32, st);
   DBuf<unsigned char> tb(tmp);
@@ -569,7 +569,7 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   DBuf<int> err(1);
   FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
   tile_cells_kernel<<<T.ntiles, 256, 0, st>>>(m, vals2.p, nrows, dof_vertex.p, T.dofs.p, T.ncell.p,
-                                              T.cells.p, T.slots.p, T.cstart.p, err.p);
+                                              T.cells.p, T.slots.p, T.cstart.p, err.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
   int herr = 0;
   FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));

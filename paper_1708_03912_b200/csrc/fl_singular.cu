@@ -220,12 +220,12 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, const double* 
 
 #define FL_E4_DISPATCH(e4, D, KERNEL, GRID, BLOCK, ST, ...)                           \
   switch (e4) {                                                                        \
-    case 6: KERNEL<D, 6><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__); break;                  \
-    case 8: KERNEL<D, 8><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__); break;                  \
-    case 10: KERNEL<D, 10><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__); break;                \
-    case 12: KERNEL<D, 12><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__); break;                \
-    case 14: KERNEL<D, 14><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__); break;                \
-    default: KERNEL<D, 0><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__); break;                 \
+    case 6: KERNEL<D, 6><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__), ::fl::note_launch(); break;                  \
+    case 8: KERNEL<D, 8><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__), ::fl::note_launch(); break;                  \
+    case 10: KERNEL<D, 10><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__), ::fl::note_launch(); break;                \
+    case 12: KERNEL<D, 12><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__), ::fl::note_launch(); break;                \
+    case 14: KERNEL<D, 14><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__), ::fl::note_launch(); break;                \
+    default: KERNEL<D, 0><<<GRID, BLOCK, 0, ST>>>(__VA_ARGS__), ::fl::note_launch(); break;                 \
   }
 
 void launch_singular_touching(const DevMesh& m, const DevTables& t, double ex, int e4,

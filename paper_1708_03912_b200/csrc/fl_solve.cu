@@ -63,11 +63,11 @@ void launch_matvec_flag(const double* A, int64_t rows, int64_t n, int64_t lda, c
   if (rows >= 148LL * 64 * 4) {
     const int64_t warps = (rows + 3) / 4;
     const int grid = (int)((warps * 32 + 255) / 256);
-    matvec_kernel<4><<<grid, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done);
+    matvec_kernel<4><<<grid, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done), ::fl::note_launch();
   } else {
     const int64_t warps = rows;
     const int grid = (int)((warps * 32 + 255) / 256);
-    matvec_kernel<1><<<grid, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done);
+    matvec_kernel<1><<<grid, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done), ::fl::note_launch();
   }
   FL_CHECK_LAUNCH();
 }
@@ -83,7 +83,7 @@ __global__ void diag_kernel(const double* A, int64_t rows, int64_t row0, int64_t
 }
 void launch_diag(const double* A, int64_t rows, int64_t row0, int64_t lda, double* d, cudaStream_t st) {
   if (rows <= 0) return;
-  diag_kernel<<<(int)((rows + 255) / 256), 256, 0, st>>>(A, rows, row0, lda, d);
+  diag_kernel<<<(int)((rows + 255) / 256), 256, 0, st>>>(A, rows, row0, lda, d), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(256) sum_final_kernel(const double* part, int 
 
 void launch_dot_flag(int64_t m, const double* a, const double* b, double* out, double* scratch, const int* done,
                      cudaStream_t st) {
-  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, st>>>(m, a, b, scratch, done);
-  sum_final_kernel<<<1, 256, 0, st>>>(scratch, DOT_BLOCKS, out, done);
+  dot_partial_kernel<<<DOT_BLOCKS, 256, 0, st>>>(m, a, b, scratch, done), ::fl::note_launch();
+  sum_final_kernel<<<1, 256, 0, st>>>(scratch, DOT_BLOCKS, out, done), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 void launch_dot(int64_t m, const double* a, const double* b, double* out, double* scratch, cudaStream_t st) {
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int64_t m, double alpha_
 void launch_cg_update_flag(int64_t m, double alpha, const double* alpha_dev, double* x, double* r, double* z,
                            const double* p, const double* Ap, const double* minv, double* out, double* scratch,
                            const int* done, cudaStream_t st) {
-  cg_update_kernel<<<DOT_BLOCKS, 256, 0, st>>>(m, alpha, alpha_dev, x, r, z, p, Ap, minv, scratch, done);
-  sum_final_kernel<<<1, 256, 0, st>>>(scratch, DOT_BLOCKS, out, done);
+  cg_update_kernel<<<DOT_BLOCKS, 256, 0, st>>>(m, alpha, alpha_dev, x, r, z, p, Ap, minv, scratch, done), ::fl::note_launch();
+  sum_final_kernel<<<1, 256, 0, st>>>(scratch, DOT_BLOCKS, out, done), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 void launch_cg_update(int64_t m, double alpha, const double* alpha_dev, double* x, double* r, double* z,
@@ -177,7 +177,7 @@ __global__ void xpby_kernel(int64_t m, const double* __restrict__ z, double beta
 }
 void launch_xpby_flag(int64_t m, const double* z, double beta, const double* beta_dev, double* p, const int* done,
                       cudaStream_t st) {
-  xpby_kernel<<<DOT_BLOCKS, 256, 0, st>>>(m, z, beta, beta_dev, p, done);
+  xpby_kernel<<<DOT_BLOCKS, 256, 0, st>>>(m, z, beta, beta_dev, p, done), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 void launch_xpby(int64_t m, const double* z, double beta, const double* beta_dev, double* p, cudaStream_t st) {
@@ -249,10 +249,10 @@ PcgResult run_pcg(const double* A, int64_t n, int64_t lda, const double* minv, d
   // r = b - A x0 (b is passed in r) (solve.py:74), z = minv r, p = z, rz = r.z (:75-77)
   if (have_x0) {
     launch_matvec(A, n, n, lda, x, Ap, st);
-    sub_kernel<<<DOT_BLOCKS, 256, 0, st>>>(n, r, Ap);
+    sub_kernel<<<DOT_BLOCKS, 256, 0, st>>>(n, r, Ap), ::fl::note_launch();
   }
-  precond_kernel<<<DOT_BLOCKS, 256, 0, st>>>(n, r, minv, z, p, scratch.p);
-  sum_final_kernel<<<1, 256, 0, st>>>(scratch.p, DOT_BLOCKS, &sc.p->rz, nullptr);
+  precond_kernel<<<DOT_BLOCKS, 256, 0, st>>>(n, r, minv, z, p, scratch.p), ::fl::note_launch();
+  sum_final_kernel<<<1, 256, 0, st>>>(scratch.p, DOT_BLOCKS, &sc.p->rz, nullptr), ::fl::note_launch();
   FL_CHECK_LAUNCH();
   double rz0 = 0.0;
   FL_CUDA(cudaMemcpyAsync(&rz0, &sc.p->rz, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -270,19 +270,23 @@ PcgResult run_pcg(const double* A, int64_t n, int64_t lda, const double* minv, d
   cudaStream_t cs;
   FL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   FL_CUDA(cudaStreamSynchronize(st));
+  const long long before = launch_counter();
   FL_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   for (int k = 0; k < CHK; ++k) {
     launch_matvec_flag(A, n, n, lda, p, Ap, done.p, cs);
     launch_dot_flag(n, p, Ap, &sc.p->pAp, scratch.p, done.p, cs);
-    cg_alpha_kernel<<<1, 1, 0, cs>>>(sc.p, done.p);
+    cg_alpha_kernel<<<1, 1, 0, cs>>>(sc.p, done.p), ::fl::note_launch();
     launch_cg_update_flag(n, 0.0, &sc.p->alpha, x, r, z, p, Ap, minv, &sc.p->rz_new, scratch.p, done.p, cs);
-    cg_beta_kernel<<<1, 1, 0, cs>>>(sc.p, done.p);
+    cg_beta_kernel<<<1, 1, 0, cs>>>(sc.p, done.p), ::fl::note_launch();
     launch_xpby_flag(n, z, 0.0, &sc.p->beta, p, done.p, cs);
   }
   FL_CUDA(cudaStreamEndCapture(cs, &graph));
   FL_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  const long long per_graph = launch_counter() - before;   // kernels per replay
+  launch_counter() = before;
   for (long long launched = 0;; launched += CHK) {
     FL_CUDA(cudaGraphLaunch(exec, cs));
+    note_launch(per_graph);
     FL_CUDA(cudaMemcpyAsync(&h, sc.p, sizeof(CgScalars), cudaMemcpyDeviceToHost, cs));
     FL_CUDA(cudaStreamSynchronize(cs));
     if (h.done) break;

@@ -74,8 +74,12 @@ class DenseDeviceOperator:
         _lib.check(_lib.load().fl_dense_stats(self.handle, C.byref(s)))
         return s.as_dict()
 
-    def to_host(self):
-        out = np.empty((self.row_end - self.row_begin, self.n))
+    def to_host(self, out=None):
+        shape = (self.row_end - self.row_begin, self.n)
+        if out is None:
+            out = np.empty(shape)
+        elif out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array of shape %r" % (shape,))
         _lib.check(_lib.load().fl_dense_to_host(self.handle, out.ctypes.data))
         return out
 
