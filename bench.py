@@ -43,7 +43,7 @@ CONFIG_TEXT = {
 # per-evaluation algorithmic fp64 FLOPs excluding the power and the
 # executed FLOPs of the specialised power r2^ex (ncu-measured)
 ALG_FLOPS = {(1, "tail"): 4, (1, "cross"): 6, (2, "tail"): 7, (2, "cross"): 11}
-POW_FLOPS = {6: 17, 8: 12, 10: 18, 12: 13, 14: 19, 0: 60}
+POW_FLOPS = {6: 18, 8: 9, 10: 19, 12: 10, 14: 20, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh
 
 
 def peaks():
@@ -186,7 +186,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
 
     mesh, s = M.baseline_mesh(args.config)
@@ -295,8 +296,9 @@ def main():
     e2e = None
     if world == 1:
         Mh = A._lib.Marshal(mesh, dm, ker, None)
+        tdir, tdata, _ = A._tables(mesh, dm, s, None)
         h2d = (Mh.vertices.nbytes + Mh.cells.nbytes + Mh.bedges.nbytes + Mh.bnormals.nbytes + Mh.v2d.nbytes
-               + A.pack_tables(mesh.d, s)[1].nbytes + A.pack_tables(mesh.d, s)[0].nbytes)
+               + tdir.nbytes + tdata.nbytes)
         out = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
         et = []
         for i in range(max(2, args.steps)):

@@ -136,6 +136,18 @@ def check(code):
     raise RuntimeError("fraclap_b200 CUDA error: %s" % msg)
 
 
+CUDA_STREAM_LEGACY = 0x1
+
+
+def stream_arg(stream):
+    """None -> the library's own stream; 0 (torch's default stream) -> cudaStreamLegacy;
+    a torch.cuda.Stream or a raw handle -> that stream."""
+    if stream is None:
+        return None
+    stream = getattr(stream, "cuda_stream", stream)
+    return C.c_void_p(CUDA_STREAM_LEGACY if int(stream) == 0 else int(stream))
+
+
 def ptr(a):
     return a.ctypes.data if a is not None else None
 

@@ -68,8 +68,10 @@ def _device_index(device):
     return int(getattr(device, "index", device) or 0)
 
 
-def _tables(d, s):
-    dir_, data = pack_tables(d, float(s))
+def _tables(mesh, dofmap, s, params):
+    from .quadrature import needed_orders
+    kt, kb = needed_orders(mesh, dofmap, float(s), params)
+    dir_, data = pack_tables(mesh.vertices.shape[1], float(s), kt, kb)
     return dir_, data, _lib.fl_tables(dir_.ctypes.data, data.ctypes.data, len(data))
 
 
@@ -82,13 +84,13 @@ def assemble_dense_device(mesh, dofmap, kernel, params: OrderParams | None = Non
     if variant == "symmetrized":
         raise AssemblyError("symmetrized kernels are not supported by the dense device path")
     m = _lib.Marshal(mesh, dofmap, kernel, params)
-    dir_, data, tb = _tables(m.d, float(kernel.s))
+    dir_, data, tb = _tables(mesh, dofmap, float(kernel.s), params)
     n = int(dofmap.n)
     r0, r1 = (0, n) if rows is None else (int(rows[0]), int(rows[1]))
     handle = C.c_void_p()
     code = lib.fl_assemble_dense(C.byref(m.mesh), C.byref(m.dofmap), C.byref(m.kernel), C.byref(m.params),
                                  C.byref(tb), -1 if n_limit is None else int(n_limit), r0, r1,
-                                 _device_index(device), C.c_void_p(stream) if stream else None,
+                                 _device_index(device), _lib.stream_arg(stream),
                                  C.byref(handle))
     _lib.check(code)
     return DenseDeviceOperator(handle, n, r0, r1)

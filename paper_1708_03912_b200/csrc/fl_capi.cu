@@ -22,6 +22,20 @@ long long& launch_counter() {
   static long long c = 0;
   return c;
 }
+cudaStream_t& cur_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+void init_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;   // keep freed blocks cached: repeated assemblies reuse them
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
 }  // namespace fl
 
 struct fl_dense {
@@ -108,7 +122,7 @@ void check_inputs(const fl_mesh* mesh, const fl_dofmap* dm, const fl_kernel* k, 
 
 struct Uploaded {
   DBuf<double> vert, bnorm, tab, X, W;
-  DBuf<int> cells, v2d, bedges, patch_off, patch_cells;
+  DBuf<int> cells, v2d, bedges, patch_off, patch_cells, err;
   DBuf<CellGeo> geo;
   DevMesh m;
   DevTables t;
@@ -156,9 +170,21 @@ void upload(const fl_mesh* mesh, const fl_dofmap* dm, const fl_tables* tb, Uploa
   m.q = U.t.rule(T_CELL, 0).cnt;
   if (m.q != (d == 1 ? 6 : 16)) throw Error(FL_E_ARG, "cell rule must have 6 (1D) / 16 (2D) nodes (XQ_ORDER)");
   m.vert = U.vert.p; m.cells = U.cells.p; m.v2d = U.v2d.p; m.bedges = U.bedges.p; m.bnorm = U.bnorm.p;
+  U.err.alloc(1);
+  FL_CUDA(cudaMemsetAsync(U.err.p, 0, sizeof(int), st));
+  m.err = U.err.p;
   build_patches((int)nv, (int)nc, d, U.cells.p, U.patch_off, U.patch_cells, st);
   m.patch_off = U.patch_off.p;
   m.patch_cells = U.patch_cells.p;
+  {
+    std::vector<int> po(nv + 1);
+    FL_CUDA(cudaMemcpyAsync(po.data(), U.patch_off.p, (nv + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    int mv = 0;
+    for (int64_t v = 0; v < nv; ++v) mv = std::max(mv, po[v + 1] - po[v]);
+    if (mv > MAX_VALENCE)
+      throw Error(FL_E_ASSEMBLY, "vertex valence " + std::to_string(mv) + " exceeds " + std::to_string(MAX_VALENCE));
+  }
   U.geo.alloc(nc);
   launch_prep_cells(m, U.geo.p, st);
   m.geo = U.geo.p;
@@ -230,13 +256,11 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   D->row0 = row_begin;
   D->row1 = row_end;
   D->lda = ((n + 31) / 32) * 32;
-  if (stream) {
-    D->stream = (cudaStream_t)stream;
-  } else {
-    FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
-    D->own_stream = true;
-  }
-  cudaStream_t st = D->stream;
+  init_pool(device);
+  FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));   // the operator's own stream
+  D->own_stream = true;
+  cudaStream_t st = stream ? (cudaStream_t)stream : D->stream;             // the assembly's stream
+  StreamScope scope(st);
   const int d = mesh->d;
   const double s = kernel->s, C = kernel->C_ds;
   const double ex = -(d / 2.0 + s);
@@ -299,6 +323,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
 
   // dense rows: cross term tiles, then the local/sparse pull
   D->A.alloc((size_t)std::max<int64_t>(rows, 1) * D->lda);
+  D->A.st = D->stream;
   if (D->lda > n && rows > 0)
     FL_CUDA(cudaMemset2DAsync(D->A.p + n, D->lda * sizeof(double), 0, (D->lda - n) * sizeof(double), rows, st));
   Tiles trow, tcol;
@@ -318,8 +343,11 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
                      (int)row_begin, (int)row_end, D->A.p, D->lda, st);
   tm.mark();  // 7
   unsigned long long hev[2] = {0, 0};
+  int herr = 0;
   FL_CUDA(cudaMemcpyAsync(hev, evc.p, sizeof(hev), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&herr, m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  if (herr) throw Error(FL_E_QUAD, "a quadrature rule for a selected order is missing from the tables");
 
   fl_assembly_stats& S = D->stats;
   const int64_t nc = m.nc;
@@ -358,8 +386,10 @@ int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense*
   D->row0 = 0;
   D->row1 = n;
   D->lda = ((n + 31) / 32) * 32;
+  init_pool(device);
   FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
   D->own_stream = true;
+  StreamScope scope(D->stream);
   D->A.alloc((size_t)n * D->lda);
   FL_CUDA(cudaMemsetAsync(D->A.p, 0, (size_t)n * D->lda * sizeof(double), D->stream));
   FL_CUDA(cudaMemcpy2DAsync(D->A.p, D->lda * sizeof(double), A, n * sizeof(double), n * sizeof(double), n,
@@ -391,6 +421,7 @@ int32_t fl_dense_to_host(const fl_dense* A, double* host) {
   FL_API_BEGIN
   if (!A || !host) return fail(FL_E_ARG, "null argument");
   FL_CUDA(cudaSetDevice(A->device));
+  StreamScope scope(A->stream);
   const int64_t rows = A->row1 - A->row0;
   if (rows == 0 || A->n == 0) return FL_OK;
   FL_CUDA(cudaMemcpy2DAsync(host, A->n * sizeof(double), A->A.p, A->lda * sizeof(double), A->n * sizeof(double),
@@ -404,6 +435,7 @@ int32_t fl_dense_diag(const fl_dense* A, double* host_diag) {
   FL_API_BEGIN
   if (!A || !host_diag) return fail(FL_E_ARG, "null argument");
   FL_CUDA(cudaSetDevice(A->device));
+  StreamScope scope(A->stream);
   const int64_t rows = A->row1 - A->row0;
   if (rows == 0) return FL_OK;
   DBuf<double> d(rows);
@@ -427,6 +459,7 @@ int32_t fl_matvec(const fl_dense* A, const double* x, double* y, int32_t ptr_kin
   FL_API_BEGIN
   if (!A || !x || !y) return fail(FL_E_ARG, "null argument");
   FL_CUDA(cudaSetDevice(A->device));
+  StreamScope scope(A->stream);
   const int64_t rows = A->row1 - A->row0;
   if (ptr_kind == 1) {
     launch_matvec(A->A.p, rows, A->n, A->lda, x, y, A->stream);
@@ -449,6 +482,7 @@ int32_t fl_pcg(const fl_dense* A, const double* b, const double* x0, double tol,
   if (!A || !b || !x || !rep) return fail(FL_E_ARG, "null argument");
   if (A->row0 != 0 || A->row1 != A->n) return fail(FL_E_ARG, "fl_pcg needs the whole matrix on one device");
   FL_CUDA(cudaSetDevice(A->device));
+  StreamScope scope(A->stream);
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t n = A->n, L = A->lda;
   cudaStream_t st = A->stream;
@@ -529,6 +563,7 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
   FL_CUDA(cudaSetDevice(device));
   cudaStream_t st;
   FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  StreamScope scope(st);
   // minimal table: the cell rule is needed by upload(); fake a 1-node rule of the right size
   std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
   const int q = mesh->d == 1 ? 6 : 16;
@@ -556,6 +591,7 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
   FL_CUDA(cudaSetDevice(device));
   cudaStream_t st;
   FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  StreamScope scope(st);
   std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
   const int q = mesh->d == 1 ? 6 : 16;
   std::vector<double> data((size_t)q * NODE, 0.0);
@@ -585,6 +621,7 @@ int32_t fl_probe_fp64_peak(int32_t device, double* tflops) {
   FL_CUDA(cudaSetDevice(device));
   cudaStream_t st;
   FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  StreamScope scope(st);
   *tflops = probe_fp64_tflops(st);
   cudaStreamDestroy(st);
   return FL_OK;
@@ -599,6 +636,7 @@ int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   FL_CUDA(cudaSetDevice(device));
   cudaStream_t st;
   FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  StreamScope scope(st);
   std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
   const int q = mesh->d == 1 ? 6 : 16;
   std::vector<double> data((size_t)q * NODE, 0.0);

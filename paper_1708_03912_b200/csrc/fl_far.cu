@@ -5,14 +5,17 @@
 //
 // Tail:  one warp per target cell K.  Lanes own target nodes x_q (16 in 2D, 6 in 1D); the
 //        32 sources of a chunk get their order k (select_order with C_offset-4) in parallel,
-//        their k^d mapped nodes are staged in shared memory and the half-warps (2D) / lane
-//        groups (1D) sweep that node list: uniform work, no divergence on k.
-// Cross: one CTA per (row tile, column tile) of 64 DoFs.  Cells touching the row tile are
-//        processed colour class by colour class (vertex-disjoint => their rows are disjoint);
-//        a warp owns one row cell, lanes own column cells, and the column-cell updates are
-//        applied colour by colour inside the warp.  Every A entry therefore receives its <=36
-//        contributions in the fixed (row colour, column colour) order: deterministic and free
-//        of atomics; the tile is written to HBM once (and mirrored when symmetric).
+//        their k^d mapped nodes are staged in shared memory (padded to the unroll width) and
+//        the half-warps (2D) / lane groups (1D) sweep that node list 4 nodes at a time:
+//        uniform work, no divergence on k, independent evaluations in flight.
+// Cross: one CTA per (row tile, column tile) of 64 DoFs.  The cells touching the two tiles
+//        are taken 16 x 32 at a time: (A) every pair gets its order k, (B) the pairs are
+//        sorted by k and their 3x3 blocks M^{K,K~} computed into shared memory — a whole
+//        warp per pair for large k (lanes over the x nodes), one thread per pair otherwise —
+//        (C) each tile row is owned by 4 threads (disjoint column classes) that add the
+//        blocks of its cells in a fixed order.  No atomics on values: every A entry receives
+//        its contributions in the same order on every run; the tile is written to HBM once
+//        (and mirrored when the assembly is symmetric).
 #include "fl_internal.h"
 
 namespace fl {
@@ -20,25 +23,31 @@ namespace fl {
 // ====================================================================== tail Psi_K
 constexpr int TAIL_WARPS = 4;
 constexpr int TAIL_WIN = 256;
+constexpr int TAIL_U = 4;
 
 template <int D, int E4>
-__global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const double* __restrict__ tab,
-                                                               DevTables dir, OrderConsts oc, double ex,
-                                                               const int* __restrict__ targets, int ntargets,
-                                                               double* __restrict__ psi,
-                                                               unsigned long long* __restrict__ evals) {
+__global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, const double* __restrict__ tab,
+                                                                  DevTables dir, OrderConsts oc, double ex,
+                                                                  const int* __restrict__ targets, int ntargets,
+                                                                  double* __restrict__ psi,
+                                                                  unsigned long long* __restrict__ evals) {
   constexpr int Q = (D == 1) ? 6 : 16;
   constexpr int G = 32 / Q;
-  __shared__ double2 s_y[TAIL_WARPS][TAIL_WIN];
-  __shared__ double s_jw[TAIL_WARPS][TAIL_WIN];
+  constexpr int PADW = TAIL_WIN + TAIL_U * 8;
+  __shared__ double2 s_y[TAIL_WARPS][PADW];
+  __shared__ double s_jw[TAIL_WARPS][PADW];
   __shared__ double s_src[TAIL_WARPS][32][8];   // P0 (2), E (4), J, pad
+  __shared__ CellGeo s_tgt[TAIL_WARPS];
   __shared__ int s_off[TAIL_WARPS][33];
   __shared__ int s_k[TAIL_WARPS][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = blockIdx.x * TAIL_WARPS + w;
   if (ti >= ntargets) return;
   const int K = targets[ti];
-  const CellGeo A = m.geo[K];
+  if (lane < (int)(sizeof(CellGeo) / 8))
+    reinterpret_cast<double*>(&s_tgt[w])[lane] = reinterpret_cast<const double*>(&m.geo[K])[lane];
+  __syncwarp();
+  const CellGeo& A = s_tgt[w];
   const int q = lane % Q, g = lane / Q;
   const bool active = lane < G * Q;
   double xq0 = 0.0, xq1 = 0.0;
@@ -46,13 +55,13 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
     xq0 = m.X[((size_t)K * Q + q) * D + 0];
     if (D == 2) xq1 = m.X[((size_t)K * Q + q) * D + 1];
   }
-  double acc = 0.0;
+  double acc0 = 0.0, acc1 = 0.0;
   unsigned long long nodes = 0;
   for (int s0 = 0; s0 < m.nc; s0 += 32) {
     const int src = s0 + lane;
     int k = 0, nn = 0;
     if (src < m.nc && src != K) {
-      const CellGeo B = m.geo[src];
+      const CellGeo& B = m.geo[src];
       if (!touching<D>(A, B)) {
         const double dist = dist_estimate<D>(A, B);            // (target, source) orientation
         k = order_disjoint(oc, oc.coff_tail, A, B, dist);      // boosted orders (:997)
@@ -67,7 +76,6 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
         sg[6] = B.J;
       }
     }
-    // warp exclusive scan of node counts
     int incl = nn;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -82,13 +90,18 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
     __syncwarp();
     for (int base = 0; base < total; base += TAIL_WIN) {
       const int cnt = min(TAIL_WIN, total - base);
-      for (int idx = lane; idx < cnt; idx += 32) {
+      const int cntp = (cnt + TAIL_U * G - 1) / (TAIL_U * G) * (TAIL_U * G);
+      for (int idx = lane; idx < cntp; idx += 32) {
+        if (idx >= cnt) {                                      // padding: far away, zero weight
+          s_y[w][idx] = make_double2(1e100, 1e100);
+          s_jw[w][idx] = 0.0;
+          continue;
+        }
         const int gi = base + idx;
         int lo = 0;                                            // owner: last j with off[j] <= gi
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1)
           if (lo + step < 32 && s_off[w][lo + step] <= gi) lo += step;
-        while (s_k[w][lo] == 0 || s_off[w][lo + 1] <= gi) ++lo;   // skip empty sources
         const int r = gi - s_off[w][lo];
         const RuleRef rr = dir.rule(T_DISJ, s_k[w][lo]);
         const double* nd = tab + (size_t)(rr.off + r) * NODE;
@@ -105,28 +118,342 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32) tail_kernel(DevMesh m, const 
       }
       __syncwarp();
       if (active) {
-        for (int p = g; p < cnt; p += G) {
-          const double2 y = s_y[w][p];
-          const double d0 = xq0 - y.x;
-          double r2;
-          if (D == 1) {
-            r2 = d0 * d0;
-          } else {
-            const double d1 = xq1 - y.y;
-            r2 = fma(d1, d1, d0 * d0);
+#pragma unroll 1
+        for (int p = g; p < cntp; p += TAIL_U * G) {
+          double v[TAIL_U];
+#pragma unroll
+          for (int u = 0; u < TAIL_U; ++u) {
+            const double2 y = s_y[w][p + u * G];
+            const double d0 = xq0 - y.x;
+            double r2;
+            if (D == 1) {
+              r2 = d0 * d0;
+            } else {
+              const double d1 = xq1 - y.y;
+              r2 = fma(d1, d1, d0 * d0);
+            }
+            v[u] = kpow<E4>(r2, ex);
           }
-          acc = fma(s_jw[w][p], kpow<E4>(r2, ex), acc);
+          acc0 = fma(s_jw[w][p], v[0], acc0);
+          acc1 = fma(s_jw[w][p + G], v[1], acc1);
+          acc0 = fma(s_jw[w][p + 2 * G], v[2], acc0);
+          acc1 = fma(s_jw[w][p + 3 * G], v[3], acc1);
         }
       }
       __syncwarp();
     }
   }
-  // combine the G groups of each target node in a fixed order
+  // combine the accumulators and the G groups of each target node in a fixed order
+  const double acc = acc0 + acc1;
   double tot = acc;
 #pragma unroll
   for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, acc, (lane + gg * Q) & 31);
   if (lane < Q) psi[(size_t)K * Q + q] = tot;
   if (lane == 0 && evals) atomicAdd(evals, nodes * Q);
+}
+
+// ====================================================================== cross tiles
+constexpr int XT = 256;                 // threads per cross CTA
+constexpr int XWARPS = XT / 32;
+constexpr int SBR = 16, SBC = 32, SBP = SBR * SBC;
+constexpr int ROWL = MAX_VALENCE;  // max (cell, slot) entries of one tile row
+
+struct TileView {
+  const int* dofs; const int* ncell; const int* cells; const int* slots; const int* cstart;
+};
+
+struct CrossShared {
+  double At[TILE][TILE + 1];
+  double Gs[SBP][9];
+  int rowc[TILE_MAXC], colc[TILE_MAXC];
+  signed char rslot[TILE_MAXC][3], cslot[TILE_MAXC][3];
+  short rowl[TILE][ROWL];
+  unsigned char rown[TILE];
+  short plist[SBP];
+  unsigned char pk[SBP];
+  int hist[KDIR + 1], cursor[KDIR + 1];
+  int qlarge, qsmall, nlarge, nsmall;
+  int rdof[TILE], cdof[TILE];
+  int kofs[KDIR], kcnt[KDIR];
+  // followed by the packed disjoint rules: per node u0 u1 lw0 lw1 lw2 (5 doubles)
+};
+
+template <int D, int E4>
+__device__ __forceinline__ void cross_pair_thread(const double* __restrict__ rt, int nn, const CellGeo& K,
+                                                  const CellGeo& L, double ex, double* __restrict__ out) {
+  double Gm[3][3] = {};
+  const double ke00 = K.p[1][0] - K.p[0][0], ke01 = K.p[1][1] - K.p[0][1];
+  const double ke10 = K.p[2][0] - K.p[0][0], ke11 = K.p[2][1] - K.p[0][1];
+  const double le00 = L.p[1][0] - L.p[0][0], le01 = L.p[1][1] - L.p[0][1];
+  const double le10 = L.p[2][0] - L.p[0][0], le11 = L.p[2][1] - L.p[0][1];
+  for (int x = 0; x < nn; ++x) {
+    const double* nx = rt + 5 * x;
+    double X0, X1 = 0.0;
+    if (D == 1) {
+      X0 = (K.p[0][0] + nx[0] * ke00) - L.p[0][0];
+    } else {
+      X0 = (K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10)) - L.p[0][0];
+      X1 = (K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11)) - L.p[0][1];
+    }
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 2
+    for (int y = 0; y < nn; ++y) {
+      const double* ny = rt + 5 * y;
+      double r2;
+      if (D == 1) {
+        const double d0 = fma(-ny[0], le00, X0);
+        r2 = d0 * d0;
+      } else {
+        const double d0 = fma(-ny[1], le10, fma(-ny[0], le00, X0));
+        const double d1 = fma(-ny[1], le11, fma(-ny[0], le01, X1));
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+      t0 = fma(v, ny[2], t0);
+      t1 = fma(v, ny[3], t1);
+      if (D == 2) t2 = fma(v, ny[4], t2);
+    }
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      const double lx = nx[2 + a];
+      Gm[a][0] = fma(lx, t0, Gm[a][0]);
+      Gm[a][1] = fma(lx, t1, Gm[a][1]);
+      if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
+    }
+  }
+  const double JJ = K.J * L.J;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) out[a * 3 + b] = Gm[a][b] * JJ;
+}
+
+template <int D, int E4>
+__device__ __forceinline__ void cross_pair_warp(const double* __restrict__ rt, int nn, const CellGeo& K,
+                                                const CellGeo& L, double ex, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  double Gm[3][3] = {};
+  const double ke00 = K.p[1][0] - K.p[0][0], ke01 = K.p[1][1] - K.p[0][1];
+  const double ke10 = K.p[2][0] - K.p[0][0], ke11 = K.p[2][1] - K.p[0][1];
+  const double le00 = L.p[1][0] - L.p[0][0], le01 = L.p[1][1] - L.p[0][1];
+  const double le10 = L.p[2][0] - L.p[0][0], le11 = L.p[2][1] - L.p[0][1];
+  for (int x = lane; x < nn; x += 32) {
+    const double* nx = rt + 5 * x;
+    double X0, X1 = 0.0;
+    if (D == 1) {
+      X0 = (K.p[0][0] + nx[0] * ke00) - L.p[0][0];
+    } else {
+      X0 = (K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10)) - L.p[0][0];
+      X1 = (K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11)) - L.p[0][1];
+    }
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 2
+    for (int y = 0; y < nn; ++y) {
+      const double* ny = rt + 5 * y;
+      double r2;
+      if (D == 1) {
+        const double d0 = fma(-ny[0], le00, X0);
+        r2 = d0 * d0;
+      } else {
+        const double d0 = fma(-ny[1], le10, fma(-ny[0], le00, X0));
+        const double d1 = fma(-ny[1], le11, fma(-ny[0], le01, X1));
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+      t0 = fma(v, ny[2], t0);
+      t1 = fma(v, ny[3], t1);
+      if (D == 2) t2 = fma(v, ny[4], t2);
+    }
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      const double lx = nx[2 + a];
+      Gm[a][0] = fma(lx, t0, Gm[a][0]);
+      Gm[a][1] = fma(lx, t1, Gm[a][1]);
+      if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
+    }
+  }
+  const double JJ = K.J * L.J;
+#pragma unroll
+  for (int a = 0; a <= D; ++a)
+#pragma unroll
+    for (int b = 0; b <= D; ++b) {
+      const double s = warp_sum(Gm[a][b]);
+      if (lane == 0) out[a * 3 + b] = s * JJ;
+    }
+}
+
+template <int D, int E4>
+__global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const double* __restrict__ tab,
+                                                           DevTables dir, OrderConsts oc, double ex,
+                                                           double negC, TileView R, TileView Cv,
+                                                           const int2* __restrict__ tpairs, int kmax,
+                                                           int symmetric, int row_begin, int row_end,
+                                                           double* __restrict__ Aout, int64_t lda,
+                                                           unsigned long long* __restrict__ evals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CrossShared& S = *reinterpret_cast<CrossShared*>(smem_raw);
+  double* rtab = reinterpret_cast<double*>(smem_raw + ((sizeof(CrossShared) + 15) / 16) * 16);
+  const int KW = (D == 1) ? 12 : 5;       // warp-cooperative from k^d >= 144 (1D) / 25 (2D) x nodes
+  const int2 tp = tpairs[blockIdx.x];
+  const int tr = tp.x, tc = tp.y;
+  const int nR = R.ncell[tr], nC = Cv.ncell[tc];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned long long my_evals = 0;
+
+  // ---- stage the tile metadata and the disjoint rules
+  for (int i = tid; i < nR; i += XT) {
+    S.rowc[i] = R.cells[tr * TILE_MAXC + i];
+    for (int a = 0; a < 3; ++a) S.rslot[i][a] = (signed char)R.slots[(tr * TILE_MAXC + i) * 3 + a];
+  }
+  for (int i = tid; i < nC; i += XT) {
+    S.colc[i] = Cv.cells[tc * TILE_MAXC + i];
+    for (int a = 0; a < 3; ++a) S.cslot[i][a] = (signed char)Cv.slots[(tc * TILE_MAXC + i) * 3 + a];
+  }
+  for (int i = tid; i < TILE; i += XT) {
+    S.rdof[i] = R.dofs[tr * TILE + i];
+    S.cdof[i] = Cv.dofs[tc * TILE + i];
+  }
+  if (tid == 0) {
+    int off = 0;
+    for (int k = 0; k < KDIR; ++k) {
+      const int c = (k >= 2 && k <= kmax) ? dir.rule(T_DISJ, k).cnt : 0;
+      S.kofs[k] = off;
+      S.kcnt[k] = c;
+      off += c;
+    }
+  }
+  for (int i = tid; i < TILE * (TILE + 1); i += XT) (&S.At[0][0])[i] = 0.0;
+  __syncthreads();
+  for (int k = 2; k <= kmax; ++k) {
+    const RuleRef rr = dir.rule(T_DISJ, k);
+    for (int i = tid; i < rr.cnt; i += XT) {
+      const double* nd = tab + (size_t)(rr.off + i) * NODE;
+      double* o = rtab + 5 * (S.kofs[k] + i);
+      o[0] = nd[0]; o[1] = nd[1]; o[2] = nd[3]; o[3] = nd[4]; o[4] = nd[5];
+    }
+  }
+  // tile row r -> its (row cell, slot) entries, in cell-list order
+  if (tid < TILE) {
+    int c = 0;
+    for (int i = 0; i < nR; ++i)
+      for (int a = 0; a <= D; ++a)
+        if (S.rslot[i][a] == tid && c < ROWL) S.rowl[tid][c++] = (short)(i * 4 + a);
+    S.rown[tid] = (unsigned char)c;
+  }
+  __syncthreads();
+
+  for (int rs0 = 0; rs0 < nR; rs0 += SBR) {
+    for (int cs0 = 0; cs0 < nC; cs0 += SBC) {
+      // ---- (A) orders of the 512 pairs of this sub-block
+      if (tid <= KDIR) S.hist[tid] = 0;
+      __syncthreads();
+      for (int p = tid; p < SBP; p += XT) {
+        const int rc = rs0 + p / SBC, cc = cs0 + p % SBC;
+        int k = 0;
+        if (rc < nR && cc < nC) {
+          const int idK = S.rowc[rc], idL = S.colc[cc];
+          const CellGeo& Kg = m.geo[idK];
+          const CellGeo& Lg = m.geo[idL];
+          if (!touching<D>(Kg, Lg)) {
+            // the reference orders a disjoint pair as (min id, max id) (assembly.py:973-982, :705)
+            const CellGeo& P = (idK < idL) ? Kg : Lg;
+            const CellGeo& Qg = (idK < idL) ? Lg : Kg;
+            k = order_disjoint(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
+          }
+        }
+        S.pk[p] = (unsigned char)k;
+        atomicAdd(&S.hist[k], 1);
+      }
+      __syncthreads();
+      if (tid == 0) {                    // descending k: large (warp) pairs first
+        int off = 0;
+        for (int k = KDIR - 1; k >= 1; --k) { S.cursor[k] = off; off += S.hist[k]; }
+        int nl = 0;
+        for (int k = KDIR - 1; k >= KW; --k) nl += S.hist[k];
+        S.nlarge = nl;
+        S.nsmall = off - nl;
+        S.qlarge = 0;
+        S.qsmall = 0;
+      }
+      __syncthreads();
+      for (int p = tid; p < SBP; p += XT) {
+        const int k = S.pk[p];
+        if (k > 0) S.plist[atomicAdd(&S.cursor[k], 1)] = (short)p;
+      }
+      __syncthreads();
+      // ---- (B) the 3x3 blocks, pairs sorted by k
+      const int nl = S.nlarge, ns = S.nsmall;
+      for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&S.qlarge, 1);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= nl) break;
+        const int p = S.plist[i];
+        const int k = S.pk[p];
+        const int nn = (D == 1) ? k : k * k;
+        cross_pair_warp<D, E4>(rtab + 5 * S.kofs[k], nn, m.geo[S.rowc[rs0 + p / SBC]],
+                               m.geo[S.colc[cs0 + p % SBC]], ex, S.Gs[p]);
+        if (lane == 0) my_evals += (unsigned long long)nn * nn;
+      }
+      for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&S.qsmall, 32);
+        i = __shfl_sync(0xffffffffu, i, 0) + lane;
+        if (i - lane >= ns) break;
+        if (i < ns) {
+          const int p = S.plist[nl + i];
+          const int k = S.pk[p];
+          const int nn = (D == 1) ? k : k * k;
+          cross_pair_thread<D, E4>(rtab + 5 * S.kofs[k], nn, m.geo[S.rowc[rs0 + p / SBC]],
+                                   m.geo[S.colc[cs0 + p % SBC]], ex, S.Gs[p]);
+          my_evals += (unsigned long long)nn * nn;
+        }
+      }
+      __syncthreads();
+      // ---- (C) row-owner scatter: 4 threads per tile row, column classes c % 4
+      {
+        const int r = tid >> 2, cg = tid & 3;
+        for (int e = 0; e < S.rown[r]; ++e) {
+          const int rc = S.rowl[r][e] >> 2, a = S.rowl[r][e] & 3;
+          if (rc < rs0 || rc >= rs0 + SBR) continue;
+          const int pr = (rc - rs0) * SBC;
+          for (int cc = 0; cc < SBC && cs0 + cc < nC; ++cc) {
+            const int p = pr + cc;
+            if (S.pk[p] == 0) continue;
+#pragma unroll
+            for (int b = 0; b <= D; ++b) {
+              const int cs = S.cslot[cs0 + cc][b];
+              if (cs >= 0 && (cs & 3) == cg) S.At[r][cs] += negC * S.Gs[p][a * 3 + b];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (evals) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_evals += __shfl_xor_sync(0xffffffffu, my_evals, o);
+    if (lane == 0) atomicAdd(evals, my_evals);
+  }
+  // ---- write the tile (and its mirror) once
+  for (int idx = tid; idx < TILE * TILE; idx += XT) {
+    const int r = idx / TILE, c = idx % TILE;
+    const int i = S.rdof[r], j = S.cdof[c];
+    if (i >= row_begin && i < row_end && j >= 0) Aout[(int64_t)(i - row_begin) * lda + j] = S.At[r][c];
+  }
+  if (symmetric && tr != tc) {
+    for (int idx = tid; idx < TILE * TILE; idx += XT) {
+      const int c = idx / TILE, r = idx % TILE;
+      const int i = S.rdof[r], j = S.cdof[c];
+      if (i >= 0 && j >= row_begin && j < row_end) Aout[(int64_t)(j - row_begin) * lda + i] = S.At[r][c];
+    }
+  }
+}
+
+size_t cross_smem_bytes(int d) {
+  const int nodes = (d == 1) ? (32 * 33 / 2 - 1) : (9 * 10 * 19 / 6 - 1);   // sum_{k=2}^{kmax} k^d
+  return ((sizeof(CrossShared) + 15) / 16) * 16 + sizeof(double) * 5 * nodes;
 }
 
 // ====================================================================== boundary flux
@@ -171,177 +498,6 @@ __global__ void __launch_bounds__(128) flux_kernel(DevMesh m, const double* __re
     }
   }
   win[(size_t)K * Q + q] = -acc;
-}
-
-// ====================================================================== cross tiles
-constexpr int XW = 4;   // warps per cross CTA
-
-struct TileView {
-  const int* dofs; const int* ncell; const int* cells; const int* slots; const int* cstart;
-};
-
-template <int D, int E4>
-__device__ __forceinline__ void cross_block(const double* __restrict__ tab, RuleRef rr, const CellGeo& K,
-                                            const CellGeo& L, double ex, double (&Gm)[3][3]) {
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) Gm[a][b] = 0.0;
-  const double ke00 = K.p[1][0] - K.p[0][0], ke01 = K.p[1][1] - K.p[0][1];
-  const double ke10 = K.p[2][0] - K.p[0][0], ke11 = K.p[2][1] - K.p[0][1];
-  const double le00 = L.p[1][0] - L.p[0][0], le01 = L.p[1][1] - L.p[0][1];
-  const double le10 = L.p[2][0] - L.p[0][0], le11 = L.p[2][1] - L.p[0][1];
-  for (int x = 0; x < rr.cnt; ++x) {
-    const double* nx = tab + (size_t)(rr.off + x) * NODE;
-    double X0, X1 = 0.0;
-    if (D == 1) {
-      X0 = K.p[0][0] + nx[0] * ke00;
-    } else {
-      X0 = K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10);
-      X1 = K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11);
-    }
-    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    for (int y = 0; y < rr.cnt; ++y) {
-      const double* ny = tab + (size_t)(rr.off + y) * NODE;
-      double r2;
-      if (D == 1) {
-        const double Y0 = L.p[0][0] + ny[0] * le00;
-        const double d0 = X0 - Y0;
-        r2 = d0 * d0;
-      } else {
-        const double Y0 = L.p[0][0] + (ny[0] * le00 + ny[1] * le10);
-        const double Y1 = L.p[0][1] + (ny[0] * le01 + ny[1] * le11);
-        const double d0 = X0 - Y0, d1 = X1 - Y1;
-        r2 = fma(d1, d1, d0 * d0);
-      }
-      const double v = kpow<E4>(r2, ex);
-      t0 = fma(v, ny[3], t0);
-      t1 = fma(v, ny[4], t1);
-      if (D == 2) t2 = fma(v, ny[5], t2);
-    }
-#pragma unroll
-    for (int a = 0; a <= D; ++a) {
-      const double lx = nx[3 + a];
-      Gm[a][0] = fma(lx, t0, Gm[a][0]);
-      Gm[a][1] = fma(lx, t1, Gm[a][1]);
-      if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
-    }
-  }
-  const double JJ = K.J * L.J;
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) Gm[a][b] *= JJ;
-}
-
-template <int D, int E4>
-__global__ void __launch_bounds__(XW * 32) cross_tile_kernel(DevMesh m, const double* __restrict__ tab,
-                                                             DevTables dir, OrderConsts oc, double ex,
-                                                             double negC, TileView R, TileView Cv,
-                                                             const int2* __restrict__ tpairs, int ncolors,
-                                                             int symmetric, int row_begin, int row_end,
-                                                             double* __restrict__ Aout, int64_t lda,
-                                                             unsigned long long* __restrict__ evals) {
-  unsigned long long my_evals = 0;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double (*At)[TILE + 1] = reinterpret_cast<double (*)[TILE + 1]>(smem_raw);
-  CellGeo* sR = reinterpret_cast<CellGeo*>(smem_raw + sizeof(double) * TILE * (TILE + 1));
-  CellGeo* sC = sR + TILE_MAXC;
-  int* sRs = reinterpret_cast<int*>(sC + TILE_MAXC);      // TILE_MAXC*3
-  int* sCs = sRs + TILE_MAXC * 3;
-  int* sRd = sCs + TILE_MAXC * 3;                           // TILE dofs
-  int* sCd = sRd + TILE;
-  const int2 tp = tpairs[blockIdx.x];
-  const int tr = tp.x, tc = tp.y;
-  const int nR = R.ncell[tr], nC = Cv.ncell[tc];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int i = tid; i < nR; i += blockDim.x) {
-    sR[i] = m.geo[R.cells[tr * TILE_MAXC + i]];
-    for (int a = 0; a < 3; ++a) sRs[i * 3 + a] = R.slots[(tr * TILE_MAXC + i) * 3 + a];
-  }
-  for (int i = tid; i < nC; i += blockDim.x) {
-    sC[i] = m.geo[Cv.cells[tc * TILE_MAXC + i]];
-    for (int a = 0; a < 3; ++a) sCs[i * 3 + a] = Cv.slots[(tc * TILE_MAXC + i) * 3 + a];
-  }
-  for (int i = tid; i < TILE; i += blockDim.x) {
-    sRd[i] = R.dofs[tr * TILE + i];
-    sCd[i] = Cv.dofs[tc * TILE + i];
-  }
-  for (int i = tid; i < TILE * (TILE + 1); i += blockDim.x) (&At[0][0])[i] = 0.0;
-  __syncthreads();
-
-  for (int cr = 0; cr < ncolors; ++cr) {
-    const int a0 = R.cstart[tr * (MAXCOLORS + 1) + cr], a1 = R.cstart[tr * (MAXCOLORS + 1) + cr + 1];
-    for (int ri = a0 + wid; ri < a1; ri += XW) {
-      const CellGeo& K = sR[ri];
-      const int lr0 = sRs[ri * 3 + 0], lr1 = sRs[ri * 3 + 1], lr2 = sRs[ri * 3 + 2];
-      for (int cj0 = 0; cj0 < nC; cj0 += 32) {
-        const int cj = cj0 + lane;
-        double Gm[3][3];
-        bool have = false;
-        int mycol = MAXCOLORS;
-        if (cj < nC) {
-          const CellGeo& L = sC[cj];
-          mycol = L.color;
-          if (!touching<D>(K, L)) {
-            // reference orientation of the order: (min id, max id) (assembly.py:973-982, :705)
-            const int idK = R.cells[tr * TILE_MAXC + ri], idL = Cv.cells[tc * TILE_MAXC + cj];
-            const CellGeo& P = (idK < idL) ? K : L;
-            const CellGeo& Qc = (idK < idL) ? L : K;
-            const double dist = dist_estimate<D>(P, Qc);
-            const int k = order_disjoint(oc, oc.coff, P, Qc, dist);
-            cross_block<D, E4>(tab, dir.rule(T_DISJ, k), K, L, ex, Gm);
-            my_evals += (D == 1) ? (unsigned long long)(k * k) : (unsigned long long)(k * k * k * k);
-            have = true;
-          }
-        }
-        // apply column colour classes one after another (vertex-disjoint within a class)
-        unsigned pending = __ballot_sync(0xffffffffu, have);
-        while (pending) {
-          const int cmin = __reduce_min_sync(0xffffffffu, have ? mycol : MAXCOLORS);
-          const bool mine = have && mycol == cmin;
-          if (mine) {
-            const int lc0 = sCs[cj * 3 + 0], lc1 = sCs[cj * 3 + 1], lc2 = sCs[cj * 3 + 2];
-            const int lr[3] = {lr0, lr1, lr2}, lc[3] = {lc0, lc1, lc2};
-#pragma unroll
-            for (int a = 0; a <= D; ++a) {
-              if (lr[a] < 0) continue;
-#pragma unroll
-              for (int b = 0; b <= D; ++b)
-                if (lc[b] >= 0) At[lr[a]][lc[b]] += negC * Gm[a][b];
-            }
-            have = false;
-          }
-          __syncwarp();
-          pending = __ballot_sync(0xffffffffu, have);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (evals) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my_evals += __shfl_xor_sync(0xffffffffu, my_evals, o);
-    if (lane == 0) atomicAdd(evals, my_evals);
-  }
-  // write the tile (and its mirror) once
-  for (int idx = tid; idx < TILE * TILE; idx += blockDim.x) {
-    const int r = idx / TILE, c = idx % TILE;
-    const int i = sRd[r], j = sCd[c];
-    if (i >= row_begin && i < row_end && j >= 0) Aout[(int64_t)(i - row_begin) * lda + j] = At[r][c];
-  }
-  if (symmetric && tr != tc) {
-    for (int idx = tid; idx < TILE * TILE; idx += blockDim.x) {
-      const int c = idx / TILE, r = idx % TILE;
-      const int i = sRd[r], j = sCd[c];
-      if (i >= 0 && j >= row_begin && j < row_end) Aout[(int64_t)(j - row_begin) * lda + i] = At[r][c];
-    }
-  }
-}
-
-size_t cross_smem_bytes() {
-  return sizeof(double) * TILE * (TILE + 1) + sizeof(CellGeo) * 2 * TILE_MAXC + sizeof(int) * TILE_MAXC * 6 +
-         sizeof(int) * TILE * 2;
 }
 
 // ====================================================================== debug: orders
@@ -403,6 +559,7 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
                         double Cds, const Tiles& rows, const Tiles& cols, bool symmetric, int row_begin,
                         int row_end, double* A, int64_t lda, int ncolors, int64_t& ntilepairs,
                         unsigned long long* evals, cudaStream_t st) {
+  (void)ncolors;
   std::vector<int2> hp;
   for (int r = 0; r < rows.ntiles; ++r)
     for (int c = symmetric ? r : 0; c < cols.ntiles; ++c) hp.push_back(make_int2(r, c));
@@ -412,27 +569,37 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
   FL_CUDA(cudaMemcpyAsync(dp.p, hp.data(), hp.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
   TileView R{rows.dofs.p, rows.ncell.p, rows.cells.p, rows.slots.p, rows.cstart.p};
   TileView C{cols.dofs.p, cols.ncell.p, cols.cells.p, cols.slots.p, cols.cstart.p};
-  const size_t smem = cross_smem_bytes();
+  const size_t smem = cross_smem_bytes(m.d);
   const double negC = -Cds;   // (C/2) * (-2)  (assembly.py:723, :1100)
+  const int kmax = oc.cap_disjoint;
   const int64_t np_ = (int64_t)hp.size();
   for (int64_t base = 0; base < np_; base += 2147483647LL) {
     const int grid = (int)std::min<int64_t>(np_ - base, 2147483647LL);
     if (m.d == 1) {
       FL_E4_SWITCH(e4, {
         FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<1, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cross_tile_kernel<1, E4><<<grid, XW * 32, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, ncolors,
-                                                            symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
+        cross_tile_kernel<1, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, kmax,
+                                                       symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
       });
     } else {
       FL_E4_SWITCH(e4, {
         FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<2, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cross_tile_kernel<2, E4><<<grid, XW * 32, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, ncolors,
-                                                            symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
+        cross_tile_kernel<2, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, kmax,
+                                                       symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
       });
     }
     FL_CHECK_LAUNCH();
   }
   FL_CUDA(cudaStreamSynchronize(st));   // dp is freed on return
+}
+
+void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
+                         cudaStream_t st) {
+  const int64_t tot = (int64_t)m.nc * m.nc;
+  const int grid = (int)((tot + 255) / 256);
+  if (m.d == 1) orders_kernel<1><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k), ::fl::note_launch();
+  else orders_kernel<2><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k), ::fl::note_launch();
+  FL_CHECK_LAUNCH();
 }
 
 // Exact per-order histograms of the disjoint pairs: cross (unordered, normal orders) and
@@ -506,15 +673,6 @@ double probe_fp64_tflops(cudaStream_t st) {
   FL_CHECK_LAUNCH();
   const double flops = 2.0 * 8.0 * iters * 256.0 * grid;
   return flops / (best * 1e-3) / 1e12;
-}
-
-void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
-                         cudaStream_t st) {
-  const int64_t tot = (int64_t)m.nc * m.nc;
-  const int grid = (int)((tot + 255) / 256);
-  if (m.d == 1) orders_kernel<1><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k), ::fl::note_launch();
-  else orders_kernel<2><<<grid, 256, 0, st>>>(m, oc, cross_k, tail_k), ::fl::note_launch();
-  FL_CHECK_LAUNCH();
 }
 
 }  // namespace fl

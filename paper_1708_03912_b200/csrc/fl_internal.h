@@ -31,30 +31,43 @@ struct Error : std::runtime_error {
 long long& launch_counter();
 inline void note_launch(long long k = 1) { launch_counter() += k; }
 
+// The stream the current API call works on; device buffers are allocated and released
+// stream-ordered from the device's memory pool (no device-wide sync on free).
+cudaStream_t& cur_stream();
+void init_pool(int device);
+
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(cur_stream()) { cur_stream() = s; }
+  ~StreamScope() { cur_stream() = prev; }
+};
+
 // Device buffer with RAII.
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;
   DBuf() = default;
   explicit DBuf(size_t cnt) { alloc(cnt); }
   void alloc(size_t cnt) {
     free();
     n = cnt;
-    if (cnt) FL_CUDA(cudaMalloc(&p, cnt * sizeof(T)));
+    st = cur_stream();
+    if (cnt) FL_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), st));
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     n = 0;
   }
   ~DBuf() { free(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), st(o.st) { o.p = nullptr; o.n = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     free();
-    p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+    p = o.p; n = o.n; st = o.st; o.p = nullptr; o.n = 0;
     return *this;
   }
 };
@@ -72,6 +85,7 @@ struct DevMesh {
   const int* patch_cells = nullptr;// nc*(d+1), ascending cell id per vertex (mesh.py:114-125)
   const double* X = nullptr;       // nc*q*d  cell quadrature nodes (assembly.py:292-298)
   const double* W = nullptr;       // nc*q
+  int* err = nullptr;              // device error word (bit 0: a quadrature rule was missing)
 };
 
 struct DevTables {
@@ -114,6 +128,7 @@ void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& i
 // touch one of its DoFs, with the tile-local slot of each cell vertex.
 constexpr int TILE = 64;
 constexpr int TILE_MAXC = 256;
+constexpr int MAX_VALENCE = 12;   // cells around one vertex (cross-tile row lists)
 struct Tiles {
   int ntiles = 0;
   DBuf<int> dofs;     // ntiles*TILE (-1 pad)

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(128) touching_kernel(DevMesh m, const double* 
     }
   const double scale = jac<D>(PK) * jac<D>(PK2);
   const RuleRef r = dir.rule(tp.topo, tp.k);
+  if (r.cnt == 0) { if ((threadIdx.x & 31) == 0) atomicOr(m.err, 1); return; }
   double* o = out + p * 25;
   if (tp.topo == T_CE) {
     if constexpr (D == 2) pair_quad<D, E4, T_CE>(tab, r, PK, PK2, ex, scale, o);
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(128) identical_kernel(DevMesh m, const double*
   for (int i = 0; i < 3; ++i) { PK[i][0] = g.p[i][0]; PK[i][1] = g.p[i][1]; }
   const double J = jac<D>(PK);
   const RuleRef r = dir.rule(T_IDENT, D == 1 ? 0 : ident_k[c]);
+  if (r.cnt == 0) { if ((threadIdx.x & 31) == 0) atomicOr(m.err, 1); return; }
   double tmp[25];
   __shared__ double sh[4][25];
   double* o = sh[threadIdx.x >> 5];
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(128) boundary_kernel(DevMesh m, const double* 
   for (int i = 0; i <= D; ++i)
     for (int j = 0; j < D; ++j) PK[i][j] = m.vert[it.locs[i] * D + j];
   const RuleRef r = dir.rule(it.topo, D == 1 ? 0 : it.k);
+  if (r.cnt == 0) { if ((threadIdx.x & 31) == 0) atomicOr(m.err, 1); return; }
   double acc[15];
 #pragma unroll
   for (int i = 0; i < 15; ++i) acc[i] = 0.0;

@@ -29,7 +29,7 @@ def shard_rows(n: int, world: int, weights=None):
     else:
         w = np.cumsum(np.asarray(weights, float))
         tot = w[-1] if len(w) else 0.0
-        cuts = [0] + [int(np.searchsorted(w, tot * g / world)) for g in range(1, world)] + [n]
+        cuts = [0] + [min(n, int(np.searchsorted(w, tot * g / world)) + 1) for g in range(1, world)] + [n]
     return [(cuts[g], cuts[g + 1]) for g in range(world)]
 
 

@@ -99,7 +99,7 @@ class DenseDeviceOperator:
     def matvec_device(self, x_ptr, y_ptr, stream=None):
         """y[rows] = A[rows, :] x on device pointers (x padded to a multiple of 32 entries)."""
         _lib.check(_lib.load().fl_matvec_async(self.handle, C.c_void_p(x_ptr), C.c_void_p(y_ptr),
-                                               C.c_void_p(stream) if stream else None))
+                                               _lib.stream_arg(stream)))
 
     def __matmul__(self, x):
         return self.matvec(x)

@@ -381,9 +381,33 @@ def _lam(d, pts):
     return np.stack([1 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], axis=1)
 
 
-@lru_cache(maxsize=16)
-def pack_tables(d: int, s: float):
-    """All rules of one (d, s) in the fl_tables layout: (dir int64[8*33*2], data float64)."""
+def needed_orders(mesh, dofmap, s, params: OrderParams | None = None):
+    """Sets of touching / boundary orders the device can ask for on this mesh: every touching
+    pair's order is the touching formula at one of its cells' diameters (quadrature.py:150-155,
+    hmin = min(h_K, h_K2)), so evaluating it per cell bounds them; +-1 guards a last-ulp log
+    difference.  Returns two sorted tuples."""
+    params = params or OrderParams()
+    d = mesh.vertices.shape[1]
+    h = np.asarray(mesh.cell_diameters(), float) if hasattr(mesh, "cell_diameters") else None
+    if h is None:
+        P = mesh.vertices[mesh.cells]
+        h = np.abs(P[:, 1, 0] - P[:, 0, 0]) if d == 1 else np.max(
+            [np.linalg.norm(P[:, (i + 1) % 3] - P[:, i], axis=1) for i in range(3)], axis=0)
+    out = []
+    for bnd in (False, True):
+        k = np.unique(select_order(PairTopology.IDENTICAL, h, h, 0.0, dofmap.n, s, params, boundary=bnd, d=d))
+        ks = set()
+        for v in k.tolist():
+            ks.update((v - 1, v, v + 1))
+        out.append(tuple(sorted(x for x in ks if 2 <= x <= K_MAX)))
+    return out[0], out[1]
+
+
+@lru_cache(maxsize=32)
+def pack_tables(d: int, s: float, korders=None, borders=None):
+    """Rules of one (d, s) in the fl_tables layout: (dir int64[8*33*2], data float64).
+    korders / borders restrict the touching / boundary singular rules to those orders
+    (default: every order 2..32)."""
     if not 0.0 < s < 1.0:
         raise ValueError("s must lie in (0,1)")
     recs = []          # (topo_id, k, records[N, 8])
@@ -418,16 +442,19 @@ def pack_tables(d: int, s: float):
         r[:, 3:3 + lam.shape[1]] = lam * w[:, None] if weighted else lam
         return r
 
+    kt = range(2, K_MAX + 1) if korders is None else korders
+    kb = range(2, K_MAX + 1) if borders is None else borders
     if d == 1:
         recs.append((0, 0, pair_rec(rule_identical_1d(s))))
-        for k in range(2, K_MAX + 1):
+        for k in kt:
             recs.append((2, k, pair_rec(rule_vertex_1d(k, s))))
         recs.append((4, 0, edge_rec(rule_edge_of_cell_1d(s, vanish))))
     else:
-        for k in range(2, K_MAX + 1):
+        for k in kt:
             recs.append((0, k, pair_rec(rule_identical_2d(min(k, 24), s))))
             recs.append((1, k, pair_rec(rule_common_edge_2d(k, s))))
             recs.append((2, k, pair_rec(rule_common_vertex_2d(k, s))))
+        for k in kb:
             recs.append((4, k, edge_rec(rule_edge_of_cell_2d(k, s, vanish))))
             recs.append((5, k, edge_rec(rule_touching_edge_2d(k, s))))
     for k in range(2, (K_MAX if d == 1 else 9) + 1):
