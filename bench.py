@@ -294,7 +294,7 @@ def main():
 
     # e2e through the public API with host buffers: assemble_dense -> (n, n) ndarray
     e2e = None
-    if world == 1:
+    if world == 1 and 8.0 * n * n <= 4e9:     # host copy of A must fit comfortably in pinned RAM
         Mh = A._lib.Marshal(mesh, dm, ker, None)
         tdir, tdata, _ = A._tables(mesh, dm, s, None)
         h2d = (Mh.vertices.nbytes + Mh.cells.nbytes + Mh.bedges.nbytes + Mh.bnormals.nbytes + Mh.v2d.nbytes

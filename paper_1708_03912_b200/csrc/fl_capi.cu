@@ -214,6 +214,17 @@ __global__ void dof_vertex2(DevMesh m, int* dv) {
   if (v < m.nv && m.v2d[v] >= 0) dv[m.v2d[v]] = v;
 }
 
+struct OwnedStream {          // destroyed after every buffer declared later in the scope
+  cudaStream_t s = nullptr;
+  OwnedStream() { FL_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~OwnedStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
 struct Timer {
   cudaEvent_t e[8];
   int k = 0;
@@ -400,7 +411,11 @@ int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense*
   FL_API_END
 }
 
-void fl_dense_free(fl_dense* A) { delete A; }
+void fl_dense_free(fl_dense* A) {
+  if (!A) return;
+  cudaSetDevice(A->device);
+  delete A;
+}
 
 int32_t fl_dense_info(const fl_dense* A, int64_t* n, int64_t* r0, int64_t* r1, double** ptr) {
   if (!A) return fail(FL_E_ARG, "null handle");
@@ -561,8 +576,8 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
   if (!mesh || !dofmap || !kernel || !params || !cross_k || !tail_k) return fail(FL_E_ARG, "null argument");
   if (kernel->d != mesh->d || !(kernel->s > 0 && kernel->s < 1)) return fail(FL_E_ARG, "bad kernel");
   FL_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  OwnedStream os_;
+  cudaStream_t st = os_.s;
   StreamScope scope(st);
   // minimal table: the cell rule is needed by upload(); fake a 1-node rule of the right size
   std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
@@ -579,7 +594,6 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
   FL_CUDA(cudaMemcpyAsync(cross_k, ck.p, tot, cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(tail_k, tk.p, tot, cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
-  cudaStreamDestroy(st);
   return FL_OK;
   FL_API_END
 }
@@ -589,8 +603,8 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
   FL_API_BEGIN
   if (!mesh || !dofmap || !kernel || !params || !cross_hist || !tail_hist) return fail(FL_E_ARG, "null argument");
   FL_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  OwnedStream os_;
+  cudaStream_t st = os_.s;
   StreamScope scope(st);
   std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
   const int q = mesh->d == 1 ? 6 : 16;
@@ -610,7 +624,6 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
     cross_hist[i] = (int64_t)hh[i];
     tail_hist[i] = (int64_t)hh[KDIR + i];
   }
-  cudaStreamDestroy(st);
   return FL_OK;
   FL_API_END
 }
@@ -619,11 +632,10 @@ int32_t fl_probe_fp64_peak(int32_t device, double* tflops) {
   FL_API_BEGIN
   if (!tflops) return fail(FL_E_ARG, "null argument");
   FL_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  OwnedStream os_;
+  cudaStream_t st = os_.s;
   StreamScope scope(st);
   *tflops = probe_fp64_tflops(st);
-  cudaStreamDestroy(st);
   return FL_OK;
   FL_API_END
 }
@@ -634,8 +646,8 @@ int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   FL_API_BEGIN
   if (!mesh || !dofmap || !kernel || !params || !npairs) return fail(FL_E_ARG, "null argument");
   FL_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  FL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  OwnedStream os_;
+  cudaStream_t st = os_.s;
   StreamScope scope(st);
   std::vector<int64_t> dir(NTOPO * KDIR * 2, 0);
   const int q = mesh->d == 1 ? 6 : 16;
@@ -663,7 +675,6 @@ int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     }
     if (ident_k) FL_CUDA(cudaMemcpy(ident_k, ik.p, mesh->nc * sizeof(int), cudaMemcpyDeviceToHost));
   }
-  cudaStreamDestroy(st);
   return FL_OK;
   FL_API_END
 }

@@ -23,7 +23,8 @@ namespace fl {
 // ====================================================================== tail Psi_K
 constexpr int TAIL_WARPS = 4;
 constexpr int TAIL_WIN = 256;
-constexpr int TAIL_U = 4;
+constexpr int TAIL_U = 4;   // source nodes per lane per step
+constexpr int TAIL_T = 2;   // target nodes per lane
 
 template <int D, int E4>
 __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, const double* __restrict__ tab,
@@ -31,12 +32,14 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
                                                                   const int* __restrict__ targets, int ntargets,
                                                                   double* __restrict__ psi,
                                                                   unsigned long long* __restrict__ evals) {
-  constexpr int Q = (D == 1) ? 6 : 16;
-  constexpr int G = 32 / Q;
-  constexpr int PADW = TAIL_WIN + TAIL_U * 8;
+  constexpr int Q = (D == 1) ? 6 : 16;     // cell quadrature nodes (XQ_ORDER)
+  constexpr int L = Q / TAIL_T;            // lanes per group (8 in 2D, 3 in 1D)
+  constexpr int G = 32 / L;                // groups sweeping disjoint source nodes (4 / 10)
+  constexpr int STEP = TAIL_U * G;
+  constexpr int PADW = TAIL_WIN + STEP;
   __shared__ double2 s_y[TAIL_WARPS][PADW];
   __shared__ double s_jw[TAIL_WARPS][PADW];
-  __shared__ double s_src[TAIL_WARPS][32][8];   // P0 (2), E (4), J, pad
+  __shared__ double s_src[TAIL_WARPS][7][32];    // SoA: P0x P0y E00 E01 E10 E11 J of the chunk
   __shared__ CellGeo s_tgt[TAIL_WARPS];
   __shared__ int s_off[TAIL_WARPS][33];
   __shared__ int s_k[TAIL_WARPS][32];
@@ -48,14 +51,16 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
     reinterpret_cast<double*>(&s_tgt[w])[lane] = reinterpret_cast<const double*>(&m.geo[K])[lane];
   __syncwarp();
   const CellGeo& A = s_tgt[w];
-  const int q = lane % Q, g = lane / Q;
-  const bool active = lane < G * Q;
-  double xq0 = 0.0, xq1 = 0.0;
-  if (active) {
-    xq0 = m.X[((size_t)K * Q + q) * D + 0];
-    if (D == 2) xq1 = m.X[((size_t)K * Q + q) * D + 1];
+  const int j = lane % L, g = lane / L;
+  const bool active = lane < G * L;
+  double x0[TAIL_T], x1[TAIL_T];
+#pragma unroll
+  for (int t = 0; t < TAIL_T; ++t) {
+    const int q = j + t * L;
+    x0[t] = active ? m.X[((size_t)K * Q + q) * D + 0] : 0.0;
+    x1[t] = (active && D == 2) ? m.X[((size_t)K * Q + q) * D + 1] : 0.0;
   }
-  double acc0 = 0.0, acc1 = 0.0;
+  double acc[TAIL_T][2] = {};
   unsigned long long nodes = 0;
   for (int s0 = 0; s0 < m.nc; s0 += 32) {
     const int src = s0 + lane;
@@ -66,14 +71,13 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
         const double dist = dist_estimate<D>(A, B);            // (target, source) orientation
         k = order_disjoint(oc, oc.coff_tail, A, B, dist);      // boosted orders (:997)
         nn = (D == 1) ? k : k * k;
-        double* sg = s_src[w][lane];
-        sg[0] = B.p[0][0];
-        sg[1] = B.p[0][1];
-        sg[2] = B.p[1][0] - B.p[0][0];
-        sg[3] = B.p[1][1] - B.p[0][1];
-        sg[4] = B.p[2][0] - B.p[0][0];
-        sg[5] = B.p[2][1] - B.p[0][1];
-        sg[6] = B.J;
+        s_src[w][0][lane] = B.p[0][0];
+        s_src[w][1][lane] = B.p[0][1];
+        s_src[w][2][lane] = B.p[1][0] - B.p[0][0];
+        s_src[w][3][lane] = B.p[1][1] - B.p[0][1];
+        s_src[w][4][lane] = B.p[2][0] - B.p[0][0];
+        s_src[w][5][lane] = B.p[2][1] - B.p[0][1];
+        s_src[w][6][lane] = B.J;
       }
     }
     int incl = nn;
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
     __syncwarp();
     for (int base = 0; base < total; base += TAIL_WIN) {
       const int cnt = min(TAIL_WIN, total - base);
-      const int cntp = (cnt + TAIL_U * G - 1) / (TAIL_U * G) * (TAIL_U * G);
+      const int cntp = (cnt + STEP - 1) / STEP * STEP;
       for (int idx = lane; idx < cntp; idx += 32) {
         if (idx >= cnt) {                                      // padding: far away, zero weight
           s_y[w][idx] = make_double2(1e100, 1e100);
@@ -105,50 +109,56 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
         const int r = gi - s_off[w][lo];
         const RuleRef rr = dir.rule(T_DISJ, s_k[w][lo]);
         const double* nd = tab + (size_t)(rr.off + r) * NODE;
-        const double* sg = s_src[w][lo];
         double y0, y1 = 0.0;
         if (D == 1) {
-          y0 = sg[0] + nd[0] * sg[2];
+          y0 = s_src[w][0][lo] + nd[0] * s_src[w][2][lo];
         } else {
-          y0 = sg[0] + (nd[0] * sg[2] + nd[1] * sg[4]);
-          y1 = sg[1] + (nd[0] * sg[3] + nd[1] * sg[5]);
+          y0 = s_src[w][0][lo] + (nd[0] * s_src[w][2][lo] + nd[1] * s_src[w][4][lo]);
+          y1 = s_src[w][1][lo] + (nd[0] * s_src[w][3][lo] + nd[1] * s_src[w][5][lo]);
         }
         s_y[w][idx] = make_double2(y0, y1);
-        s_jw[w][idx] = sg[6] * nd[2];
+        s_jw[w][idx] = s_src[w][6][lo] * nd[2];
       }
       __syncwarp();
       if (active) {
 #pragma unroll 1
-        for (int p = g; p < cntp; p += TAIL_U * G) {
-          double v[TAIL_U];
+        for (int p = g; p < cntp; p += STEP) {
+          double2 y[TAIL_U];
+          double jw[TAIL_U];
 #pragma unroll
           for (int u = 0; u < TAIL_U; ++u) {
-            const double2 y = s_y[w][p + u * G];
-            const double d0 = xq0 - y.x;
-            double r2;
-            if (D == 1) {
-              r2 = d0 * d0;
-            } else {
-              const double d1 = xq1 - y.y;
-              r2 = fma(d1, d1, d0 * d0);
-            }
-            v[u] = kpow<E4>(r2, ex);
+            y[u] = s_y[w][p + u * G];
+            jw[u] = s_jw[w][p + u * G];
           }
-          acc0 = fma(s_jw[w][p], v[0], acc0);
-          acc1 = fma(s_jw[w][p + G], v[1], acc1);
-          acc0 = fma(s_jw[w][p + 2 * G], v[2], acc0);
-          acc1 = fma(s_jw[w][p + 3 * G], v[3], acc1);
+#pragma unroll
+          for (int t = 0; t < TAIL_T; ++t) {
+#pragma unroll
+            for (int u = 0; u < TAIL_U; ++u) {
+              const double d0 = x0[t] - y[u].x;
+              double r2;
+              if (D == 1) {
+                r2 = d0 * d0;
+              } else {
+                const double d1 = x1[t] - y[u].y;
+                r2 = fma(d1, d1, d0 * d0);
+              }
+              acc[t][u & 1] = fma(jw[u], kpow<E4>(r2, ex), acc[t][u & 1]);
+            }
+          }
         }
       }
       __syncwarp();
     }
   }
-  // combine the accumulators and the G groups of each target node in a fixed order
-  const double acc = acc0 + acc1;
-  double tot = acc;
+  // combine the two accumulators and the G groups of each target node in a fixed order
 #pragma unroll
-  for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, acc, (lane + gg * Q) & 31);
-  if (lane < Q) psi[(size_t)K * Q + q] = tot;
+  for (int t = 0; t < TAIL_T; ++t) {
+    const double a = acc[t][0] + acc[t][1];
+    double tot = a;
+#pragma unroll
+    for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, a, (lane + gg * L) & 31);
+    if (lane < L) psi[(size_t)K * Q + j + t * L] = tot;
+  }
   if (lane == 0 && evals) atomicAdd(evals, nodes * Q);
 }
 
@@ -564,6 +574,26 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
   for (int r = 0; r < rows.ntiles; ++r)
     for (int c = symmetric ? r : 0; c < cols.ntiles; ++c) hp.push_back(make_int2(r, c));
   ntilepairs = (int64_t)hp.size();
+  {
+    // heavy (near) tile pairs first: higher orders live there; sorting by tile distance keeps the
+    // expensive CTAs out of the tail of the grid
+    std::vector<double> gr((size_t)rows.ntiles * 3), gc((size_t)cols.ntiles * 3);
+    FL_CUDA(cudaMemcpyAsync(gr.data(), rows.geo3.p, gr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaMemcpyAsync(gc.data(), cols.geo3.p, gc.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> key(hp.size());
+    for (size_t i = 0; i < hp.size(); ++i) {
+      const double* a = &gr[3 * hp[i].x];
+      const double* b = &gc[3 * hp[i].y];
+      key[i] = std::hypot(a[0] - b[0], a[1] - b[1]) - a[2] - b[2];
+    }
+    std::vector<size_t> idx(hp.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return key[a] < key[b]; });
+    std::vector<int2> sorted(hp.size());
+    for (size_t i = 0; i < idx.size(); ++i) sorted[i] = hp[idx[i]];
+    hp.swap(sorted);
+  }
   if (hp.empty()) return;
   DBuf<int2> dp(hp.size());
   FL_CUDA(cudaMemcpyAsync(dp.p, hp.data(), hp.size() * sizeof(int2), cudaMemcpyHostToDevice, st));

@@ -136,6 +136,7 @@ struct Tiles {
   DBuf<int> cells;    // ntiles*TILE_MAXC
   DBuf<int> slots;    // ntiles*TILE_MAXC*3 (-1: vertex not a DoF of this tile)
   DBuf<int> cstart;   // ntiles*(maxcolors+1): colour class ranges in the cell list
+  DBuf<double> geo3;  // ntiles*3: centre (x, y) and radius of the tile's DoF vertices
 };
 constexpr int MAXCOLORS = 32;
 void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& t, cudaStream_t st);

@@ -461,7 +461,8 @@ __global__ void morton_kernel(DevMesh m, const int* dof_vertex, int r0, int r1, 
 constexpr int CAND = 1024;
 __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* sorted_dofs, int nrows,
                                                          const int* dof_vertex, int* tdofs, int* tncell,
-                                                         int* tcells, int* tslots, int* tcstart, int* err) {
+                                                         int* tcells, int* tslots, int* tcstart, double* tgeo,
+                                                         int* err) {
   const int t = blockIdx.x;
   __shared__ int sd[TILE];
   __shared__ unsigned long long key[CAND];
@@ -472,7 +473,29 @@ __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* s
     sd[tid] = (i < nrows) ? sorted_dofs[i] : -1;
     tdofs[t * TILE + tid] = sd[tid];
   }
-  if (tid == 0) ncand = 0;
+  if (tid == 0) {
+    ncand = 0;
+    double cx = 0, cy = 0, r = 0;
+    int c = 0;
+    for (int i = 0; i < TILE; ++i)
+      if (sd[i] >= 0) {
+        const int v = dof_vertex[sd[i]];
+        cx += m.vert[v * m.d];
+        cy += (m.d == 2) ? m.vert[v * m.d + 1] : 0.0;
+        ++c;
+      }
+    cx /= max(c, 1);
+    cy /= max(c, 1);
+    for (int i = 0; i < TILE; ++i)
+      if (sd[i] >= 0) {
+        const int v = dof_vertex[sd[i]];
+        const double dx = m.vert[v * m.d] - cx, dy = (m.d == 2) ? m.vert[v * m.d + 1] - cy : 0.0;
+        r = fmax(r, sqrt(dx * dx + dy * dy));
+      }
+    tgeo[3 * t] = cx;
+    tgeo[3 * t + 1] = cy;
+    tgeo[3 * t + 2] = r;
+  }
   __syncthreads();
   if (tid < TILE && sd[tid] >= 0) {
     const int v = dof_vertex[sd[tid]];
@@ -566,10 +589,11 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   T.cells.alloc((size_t)T.ntiles * TILE_MAXC);
   T.slots.alloc((size_t)T.ntiles * TILE_MAXC * 3);
   T.cstart.alloc((size_t)T.ntiles * (MAXCOLORS + 1));
+  T.geo3.alloc((size_t)T.ntiles * 3);
   DBuf<int> err(1);
   FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
   tile_cells_kernel<<<T.ntiles, 256, 0, st>>>(m, vals2.p, nrows, dof_vertex.p, T.dofs.p, T.ncell.p,
-                                              T.cells.p, T.slots.p, T.cstart.p, err.p), ::fl::note_launch();
+                                              T.cells.p, T.slots.p, T.cstart.p, T.geo3.p, err.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
   int herr = 0;
   FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));

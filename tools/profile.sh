@@ -9,4 +9,4 @@ $CMD > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_l_$TAG.log 2>&1
 $CMD > gpurun_out/plain2_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"$KRE" -c 2 -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
-tail -2 gpurun_out/ncu_l_$TAG.log gpurun_out/ncu_full_$TAG.log
+tail -n 2 gpurun_out/ncu_l_$TAG.log gpurun_out/ncu_full_$TAG.log
