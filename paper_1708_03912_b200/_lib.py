@@ -21,7 +21,7 @@ EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_coun
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_diag", "fl_matvec",
            "fl_matvec_async", "fl_pcg", "fl_cg_update_async", "fl_dot_async", "fl_xpby_async",
-           "fl_debug_orders", "fl_debug_order_hist", "fl_probe_fp64_peak", "fl_debug_touching"]
+           "fl_debug_orders", "fl_debug_order_hist", "fl_debug_kpow", "fl_probe_fp64_peak", "fl_debug_touching"]
 
 
 class fl_mesh(C.Structure):
@@ -104,6 +104,7 @@ def load():
         "fl_debug_order_hist": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),
                                             C.c_int32, vp, vp]),
         "fl_probe_fp64_peak": (C.c_int32, [C.c_int32, P(C.c_double)]),
+        "fl_debug_kpow": (C.c_int32, [C.c_int32, C.c_double, vp, C.c_int64, vp, C.c_int32]),
         "fl_debug_touching": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), C.c_int32,
                                           P(C.c_int64), vp, vp, vp, vp]),
     }

@@ -593,7 +593,10 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
   launch_debug_orders(U.m, oc, ck.p, tk.p, st);
   FL_CUDA(cudaMemcpyAsync(cross_k, ck.p, tot, cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(tail_k, tk.p, tot, cudaMemcpyDeviceToHost, st));
+  int herr = 0;
+  FL_CUDA(cudaMemcpyAsync(&herr, U.m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  if (herr & 2) return fail(FL_E_QUAD, "fast order path disagrees with the exact select_order arithmetic");
   return FL_OK;
   FL_API_END
 }
@@ -619,11 +622,30 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
   launch_order_hist(U.m, oc, h.p, h.p + KDIR, st);
   std::vector<unsigned long long> hh(2 * KDIR);
   FL_CUDA(cudaMemcpyAsync(hh.data(), h.p, hh.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  int herr = 0;
+  FL_CUDA(cudaMemcpyAsync(&herr, U.m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  if (herr & 2) return fail(FL_E_QUAD, "fast order path disagrees with the exact select_order arithmetic");
   for (int i = 0; i < KDIR; ++i) {
     cross_hist[i] = (int64_t)hh[i];
     tail_hist[i] = (int64_t)hh[KDIR + i];
   }
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_debug_kpow(int32_t d, double s, const double* r2, int64_t n, double* out, int32_t device) {
+  FL_API_BEGIN
+  if (!r2 || !out || n < 0) return fail(FL_E_ARG, "bad argument");
+  FL_CUDA(cudaSetDevice(device));
+  OwnedStream os_;
+  cudaStream_t st = os_.s;
+  StreamScope scope(st);
+  DBuf<double> a(std::max<int64_t>(n, 1)), b(std::max<int64_t>(n, 1));
+  FL_CUDA(cudaMemcpyAsync(a.p, r2, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  launch_kpow_probe(e4_of(d, s), a.p, n, -(d / 2.0 + s), b.p, st);
+  FL_CUDA(cudaMemcpyAsync(out, b.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
   return FL_OK;
   FL_API_END
 }

@@ -41,8 +41,6 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
   __shared__ double s_jw[TAIL_WARPS][PADW];
   __shared__ double s_src[TAIL_WARPS][7][32];    // SoA: P0x P0y E00 E01 E10 E11 J of the chunk
   __shared__ CellGeo s_tgt[TAIL_WARPS];
-  __shared__ int s_off[TAIL_WARPS][33];
-  __shared__ int s_k[TAIL_WARPS][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = blockIdx.x * TAIL_WARPS + w;
   if (ti >= ntargets) return;
@@ -69,7 +67,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
       const CellGeo& B = m.geo[src];
       if (!touching<D>(A, B)) {
         const double dist = dist_estimate<D>(A, B);            // (target, source) orientation
-        k = order_disjoint(oc, oc.coff_tail, A, B, dist);      // boosted orders (:997)
+        k = order_disjoint_fast(oc, oc.coff_tail, A, B, dist);      // boosted orders (:997)
         nn = (D == 1) ? k : k * k;
         s_src[w][0][lane] = B.p[0][0];
         s_src[w][1][lane] = B.p[0][1];
@@ -87,37 +85,37 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
       if (lane >= o) incl += v;
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
-    s_off[w][lane] = incl - nn;
-    s_k[w][lane] = k;
-    if (lane == 31) s_off[w][32] = total;
     nodes += (unsigned long long)total;
     __syncwarp();
     for (int base = 0; base < total; base += TAIL_WIN) {
       const int cnt = min(TAIL_WIN, total - base);
       const int cntp = (cnt + STEP - 1) / STEP * STEP;
-      for (int idx = lane; idx < cntp; idx += 32) {
-        if (idx >= cnt) {                                      // padding: far away, zero weight
-          s_y[w][idx] = make_double2(1e100, 1e100);
-          s_jw[w][idx] = 0.0;
-          continue;
+      // every lane maps its own source's nodes that fall into this window
+      if (nn > 0) {
+        const int my0 = incl - nn - base;
+        const int r0 = max(0, -my0), r1 = min(nn, cnt - my0);
+        if (r0 < r1) {
+          const RuleRef rr = dir.rule(T_DISJ, k);
+          const double p0x = s_src[w][0][lane], p0y = s_src[w][1][lane];
+          const double e00 = s_src[w][2][lane], e01 = s_src[w][3][lane];
+          const double e10 = s_src[w][4][lane], e11 = s_src[w][5][lane], J = s_src[w][6][lane];
+          for (int r = r0; r < r1; ++r) {
+            const double* nd = tab + (size_t)(rr.off + r) * NODE;
+            double y0, y1 = 0.0;
+            if (D == 1) {
+              y0 = p0x + nd[0] * e00;
+            } else {
+              y0 = p0x + (nd[0] * e00 + nd[1] * e10);
+              y1 = p0y + (nd[0] * e01 + nd[1] * e11);
+            }
+            s_y[w][my0 + r] = make_double2(y0, y1);
+            s_jw[w][my0 + r] = J * nd[2];
+          }
         }
-        const int gi = base + idx;
-        int lo = 0;                                            // owner: last j with off[j] <= gi
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1)
-          if (lo + step < 32 && s_off[w][lo + step] <= gi) lo += step;
-        const int r = gi - s_off[w][lo];
-        const RuleRef rr = dir.rule(T_DISJ, s_k[w][lo]);
-        const double* nd = tab + (size_t)(rr.off + r) * NODE;
-        double y0, y1 = 0.0;
-        if (D == 1) {
-          y0 = s_src[w][0][lo] + nd[0] * s_src[w][2][lo];
-        } else {
-          y0 = s_src[w][0][lo] + (nd[0] * s_src[w][2][lo] + nd[1] * s_src[w][4][lo]);
-          y1 = s_src[w][1][lo] + (nd[0] * s_src[w][3][lo] + nd[1] * s_src[w][5][lo]);
-        }
-        s_y[w][idx] = make_double2(y0, y1);
-        s_jw[w][idx] = s_src[w][6][lo] * nd[2];
+      }
+      for (int idx = cnt + lane; idx < cntp; idx += 32) {      // padding: far away, zero weight
+        s_y[w][idx] = make_double2(1e100, 1e100);
+        s_jw[w][idx] = 0.0;
       }
       __syncwarp();
       if (active) {
@@ -185,6 +183,9 @@ struct CrossShared {
   int qlarge, qsmall, nlarge, nsmall;
   int rdof[TILE], cdof[TILE];
   int kofs[KDIR], kcnt[KDIR];
+  short cgl[4][SBC * 3];        // column-class lists of the current column sub-block: cc*4 + b
+  unsigned char cgs[4][SBC * 3];//   ... and the tile column slot
+  int cgn[4];
   // followed by the packed disjoint rules: per node u0 u1 lw0 lw1 lw2 (5 doubles)
 };
 
@@ -352,8 +353,22 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
   }
   __syncthreads();
 
-  for (int rs0 = 0; rs0 < nR; rs0 += SBR) {
-    for (int cs0 = 0; cs0 < nC; cs0 += SBC) {
+  for (int cs0 = 0; cs0 < nC; cs0 += SBC) {
+    // column class c % 4 -> (column cell, slot) entries of this column sub-block
+    if (tid < 4) {
+      int c = 0;
+      for (int cc = 0; cc < SBC && cs0 + cc < nC; ++cc)
+        for (int b = 0; b <= D; ++b) {
+          const int cs = S.cslot[cs0 + cc][b];
+          if (cs >= 0 && (cs & 3) == tid) {
+            S.cgl[tid][c] = (short)(cc * 4 + b);
+            S.cgs[tid][c] = (unsigned char)cs;
+            ++c;
+          }
+        }
+      S.cgn[tid] = c;
+    }
+    for (int rs0 = 0; rs0 < nR; rs0 += SBR) {
       // ---- (A) orders of the 512 pairs of this sub-block
       if (tid <= KDIR) S.hist[tid] = 0;
       __syncthreads();
@@ -368,7 +383,7 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
             // the reference orders a disjoint pair as (min id, max id) (assembly.py:973-982, :705)
             const CellGeo& P = (idK < idL) ? Kg : Lg;
             const CellGeo& Qg = (idK < idL) ? Lg : Kg;
-            k = order_disjoint(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
+            k = order_disjoint_fast(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
           }
         }
         S.pk[p] = (unsigned char)k;
@@ -423,18 +438,16 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
       // ---- (C) row-owner scatter: 4 threads per tile row, column classes c % 4
       {
         const int r = tid >> 2, cg = tid & 3;
+        const int ng = S.cgn[cg];
         for (int e = 0; e < S.rown[r]; ++e) {
           const int rc = S.rowl[r][e] >> 2, a = S.rowl[r][e] & 3;
           if (rc < rs0 || rc >= rs0 + SBR) continue;
           const int pr = (rc - rs0) * SBC;
-          for (int cc = 0; cc < SBC && cs0 + cc < nC; ++cc) {
-            const int p = pr + cc;
+          for (int u = 0; u < ng; ++u) {
+            const int it = S.cgl[cg][u];
+            const int p = pr + (it >> 2);
             if (S.pk[p] == 0) continue;
-#pragma unroll
-            for (int b = 0; b <= D; ++b) {
-              const int cs = S.cslot[cs0 + cc][b];
-              if (cs >= 0 && (cs & 3) == cg) S.At[r][cs] += negC * S.Gs[p][a * 3 + b];
-            }
+            S.At[r][S.cgs[cg][u]] += negC * S.Gs[p][a * 3 + (it & 3)];
           }
         }
       }
@@ -520,9 +533,14 @@ __global__ void orders_kernel(DevMesh m, OrderConsts oc, int8_t* cross_k, int8_t
   if (a != b) {
     const CellGeo A = m.geo[a], B = m.geo[b];
     if (!touching<D>(A, B)) {
+      // the kernels use the fast path; it must agree with the exact reference arithmetic
       const double dt = dist_estimate<D>(A, B);
-      kt = (int8_t)order_disjoint(oc, oc.coff_tail, A, B, dt);
-      if (a < b) kc = (int8_t)order_disjoint(oc, oc.coff, A, B, dt);
+      kt = (int8_t)order_disjoint_fast(oc, oc.coff_tail, A, B, dt);
+      if (kt != order_disjoint(oc, oc.coff_tail, A, B, dt)) atomicOr(m.err, 2);
+      if (a < b) {
+        kc = (int8_t)order_disjoint_fast(oc, oc.coff, A, B, dt);
+        if (kc != order_disjoint(oc, oc.coff, A, B, dt)) atomicOr(m.err, 2);
+      }
     }
   }
   cross_k[idx] = kc;
@@ -646,8 +664,14 @@ __global__ void order_hist_kernel(DevMesh m, OrderConsts oc, unsigned long long*
     const CellGeo B = m.geo[b];
     if (touching<D>(A, B)) continue;
     const double dt = dist_estimate<D>(A, B);
-    atomicAdd(&stl[order_disjoint(oc, oc.coff_tail, A, B, dt)], 1ull);
-    if (a < b) atomicAdd(&sc[order_disjoint(oc, oc.coff, A, B, dt)], 1ull);
+    const int kt = order_disjoint_fast(oc, oc.coff_tail, A, B, dt);
+    if (kt != order_disjoint(oc, oc.coff_tail, A, B, dt)) atomicOr(m.err, 2);
+    atomicAdd(&stl[kt], 1ull);
+    if (a < b) {
+      const int kc = order_disjoint_fast(oc, oc.coff, A, B, dt);
+      if (kc != order_disjoint(oc, oc.coff, A, B, dt)) atomicOr(m.err, 2);
+      atomicAdd(&sc[kc], 1ull);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < KDIR; i += blockDim.x) {
@@ -705,4 +729,17 @@ double probe_fp64_tflops(cudaStream_t st) {
   return flops / (best * 1e-3) / 1e12;
 }
 
+}  // namespace fl
+
+namespace fl {
+template <int E4>
+__global__ void kpow_probe_kernel(const double* r2, int64_t n, double ex, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = kpow<E4>(r2[i], ex);
+}
+void launch_kpow_probe(int e4, const double* r2, int64_t n, double ex, double* out, cudaStream_t st) {
+  const int grid = (int)((n + 255) / 256);
+  FL_E4_SWITCH(e4, (kpow_probe_kernel<E4><<<grid, 256, 0, st>>>(r2, n, ex, out), ::fl::note_launch()));
+  FL_CHECK_LAUNCH();
+}
 }  // namespace fl
