@@ -327,7 +327,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   FL_CUDA(cudaMemsetAsync(evc.p, 0, 2 * sizeof(unsigned long long), st));
   DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
   FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
-  launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+  if (d == 1) launch_tail1d(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+  else launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
   tm.mark();  // 3
   if (do_bnd) launch_flux(m, U.t, ex, e4, targets.p, ntargets, win.p, st);
   tm.mark();  // 4
@@ -337,14 +338,22 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   D->A.st = D->stream;
   if (D->lda > n && rows > 0)
     FL_CUDA(cudaMemset2DAsync(D->A.p + n, D->lda * sizeof(double), 0, (D->lda - n) * sizeof(double), rows, st));
-  Tiles trow, tcol;
   const bool full = (row_begin == 0 && row_end == n);
-  build_tiles(m, (int)row_begin, (int)row_end, trow, st);
-  if (!full) build_tiles(m, 0, (int)n, tcol, st);
   int64_t ntp = 0;
-  tm.mark();  // 5
-  launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
-                     D->lda, ncolors, ntp, evc.p + 1, st);
+  int ntiles = 0;
+  if (d == 1 && cross1d_fits(m, ntargets, full)) {
+    tm.mark();  // 5
+    launch_cross1d(m, U.t, oc, ex, e4, C, targets.p, ntargets, row_vertex.p, full, (int)row_begin, (int)row_end,
+                   D->A.p, D->lda, evc.p + 1, st);
+  } else {
+    Tiles trow, tcol;
+    build_tiles(m, (int)row_begin, (int)row_end, trow, st);
+    if (!full) build_tiles(m, 0, (int)n, tcol, st);
+    ntiles = trow.ntiles;
+    tm.mark();  // 5
+    launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
+                       D->lda, ncolors, ntp, evc.p + 1, st);
+  }
   tm.mark();  // 6
   DBuf<double> Lc((size_t)m.nc * 9);
   launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
@@ -380,7 +389,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   S.ms_total = tm.ms(0, 7);
   S.cross_tile_pairs = ntp;
   S.ncolors = ncolors;
-  S.ntiles = trow.ntiles;
+  S.ntiles = ntiles;
   *out = D.release();
   return FL_OK;
   FL_API_END

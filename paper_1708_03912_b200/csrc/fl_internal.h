@@ -163,6 +163,13 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
                         int64_t& ntilepairs, unsigned long long* evals, cudaStream_t st);
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
+// fl_far1d.cu (1D: lean tail, packed pair-block cross + gather)
+void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                   const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st);
+bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric);
+void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+                    const int* targets, int ntargets, const int* dof_vertex, bool symmetric, int row_begin,
+                    int row_end, double* A, int64_t lda, unsigned long long* evals, cudaStream_t st);
 void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,
                        cudaStream_t st);
 double probe_fp64_tflops(cudaStream_t st);
