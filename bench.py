@@ -325,7 +325,10 @@ def main():
                            "cells": mesh.num_cells, "pairs_per_step": pairs,
                            "parallelism": "rows%d" % world, "l2": "flushed (256 MB write) between steps",
                            "phases_ms": {k: stats[k] for k in ("ms_prep", "ms_singular", "ms_tail", "ms_flux",
-                                                               "ms_tiles", "ms_cross", "ms_local", "ms_total")}},
+                                                               "ms_tiles", "ms_cross", "ms_discover", "ms_near",
+                                                               "ms_cross_compute", "ms_local", "ms_total")},
+                           "near_pairs": stats["near_pairs"], "evals_tail": stats["evals_tail"],
+                           "evals_cross": stats["evals_cross"]},
                 "roofline": roofline, "matvec": matvec, "cg": cg, "e2e": e2e, "cpu_baseline": cpu,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)

@@ -124,6 +124,9 @@ typedef struct fl_assembly_stats {
   double ms_prep, ms_singular, ms_tail, ms_flux, ms_tiles, ms_cross, ms_local, ms_total;
   int64_t cross_tile_pairs;
   int32_t ncolors, ntiles;
+  /* cross term split: discovery pass (orders only), near blocks, compute pass; near pair count */
+  double ms_discover, ms_near, ms_cross_compute;
+  int64_t near_pairs;
 } fl_assembly_stats;
 
 /* ---------------------------------------------------------------- library */
@@ -154,6 +157,8 @@ int32_t fl_dense_info(const fl_dense* A, int64_t* n, int64_t* row_begin, int64_t
 int32_t fl_dense_stats(const fl_dense* A, fl_assembly_stats* stats);
 /* copy the owned rows (row-major, (row_end-row_begin) x n) to host memory */
 int32_t fl_dense_to_host(const fl_dense* A, double* host_rows);
+/* copy selected global rows (each within [row_begin, row_end)) to host, nrows x n */
+int32_t fl_dense_rows(const fl_dense* A, int64_t nrows, const int64_t* rows, double* host_out);
 /* diagonal entries of the owned rows (host) */
 int32_t fl_dense_diag(const fl_dense* A, double* host_diag);
 

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfraclap_b200.so")
+LIB_PATH = os.environ.get("FRACLAP_B200_LIB") or os.path.join(_HERE, "lib", "libfraclap_b200.so")
 
 FL_OK, FL_E_ARG, FL_E_ASSEMBLY, FL_E_QUAD, FL_E_SOLVER, FL_E_CUDA, FL_E_OOM = 0, -1, -2, -3, -4, -5, -6
 VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
@@ -19,7 +19,7 @@ VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
 EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_count", "fl_assemble_dense",
            "fl_dense_from_host",
            "fl_dense_free",
-           "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_diag", "fl_matvec",
+           "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_rows", "fl_dense_diag", "fl_matvec",
            "fl_matvec_async", "fl_pcg", "fl_cg_update_async", "fl_dot_async", "fl_xpby_async",
            "fl_debug_orders", "fl_debug_order_hist", "fl_debug_kpow", "fl_probe_fp64_peak", "fl_debug_touching"]
 
@@ -60,7 +60,8 @@ class fl_assembly_stats(C.Structure):
                 ("ms_singular", C.c_double), ("ms_tail", C.c_double), ("ms_flux", C.c_double),
                 ("ms_tiles", C.c_double), ("ms_cross", C.c_double),
                 ("ms_local", C.c_double), ("ms_total", C.c_double), ("cross_tile_pairs", C.c_int64),
-                ("ncolors", C.c_int32), ("ntiles", C.c_int32)]
+                ("ncolors", C.c_int32), ("ntiles", C.c_int32), ("ms_discover", C.c_double),
+                ("ms_near", C.c_double), ("ms_cross_compute", C.c_double), ("near_pairs", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -93,6 +94,7 @@ def load():
         "fl_dense_stats": (C.c_int32, [vp, P(fl_assembly_stats)]),
         "fl_dense_to_host": (C.c_int32, [vp, vp]),
         "fl_dense_diag": (C.c_int32, [vp, vp]),
+        "fl_dense_rows": (C.c_int32, [vp, C.c_int64, vp, vp]),
         "fl_matvec": (C.c_int32, [vp, vp, vp, C.c_int32]),
         "fl_matvec_async": (C.c_int32, [vp, vp, vp, vp]),
         "fl_pcg": (C.c_int32, [vp, vp, vp, C.c_double, C.c_int64, C.c_int32, vp, P(fl_solve_report)]),

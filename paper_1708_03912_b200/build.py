@@ -32,14 +32,17 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force=False, verbose=False, ptxas_v=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, ptxas_v=False, defines=(), out=None):
+    """Compile csrc/*.cu into the in-tree library (or `out`, with extra -D `defines`)."""
+    lib_path = out or LIB
+    if not force and not defines and out is None and up_to_date():
         return LIB
-    os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
-    extra = ["-Xptxas", "-v"] if ptxas_v else []
+    objdir = os.path.join(OUT_DIR, "obj" if not defines else "obj_" + "_".join(d.replace("=", "") for d in defines))
+    os.makedirs(objdir, exist_ok=True)
+    extra = (["-Xptxas", "-v"] if ptxas_v else []) + ["-D" + d for d in defines]
 
     def one(src):
-        obj = os.path.join(OUT_DIR, "obj", os.path.basename(src) + ".o")
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC] + FLAGS + extra + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -50,13 +53,13 @@ def build(force=False, verbose=False, ptxas_v=False):
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(one, _sources()))
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s" % r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":

@@ -226,7 +226,7 @@ struct OwnedStream {          // destroyed after every buffer declared later in 
 };
 
 struct Timer {
-  cudaEvent_t e[8];
+  cudaEvent_t e[12];
   int k = 0;
   cudaStream_t st;
   explicit Timer(cudaStream_t s) : st(s) {
@@ -284,7 +284,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   Uploaded U;
   upload(mesh, dofmap, tables, U, st);
   DevMesh& m = U.m;
-  const int ncolors = color_cells(m, U.geo.p, st);
+  const int ncolors = 0;   // (the cross tiles no longer need a cell colouring)
   const OrderConsts oc = make_order_consts(*params, d, s, n);
 
   // target cells: cells with a vertex DoF in the owned rows
@@ -339,8 +339,14 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   if (D->lda > n && rows > 0)
     FL_CUDA(cudaMemset2DAsync(D->A.p + n, D->lda * sizeof(double), 0, (D->lda - n) * sizeof(double), rows, st));
   const bool full = (row_begin == 0 && row_end == n);
-  int64_t ntp = 0;
+  int64_t ntp = 0, nkeys = 0;
   int ntiles = 0;
+  DBuf<unsigned long long> near_keys;
+  DBuf<unsigned int> near_cnt(1);
+  NearPairs near;
+  cudaEvent_t xev[2];
+  cudaEventCreate(&xev[0]);
+  cudaEventCreate(&xev[1]);
   if (d == 1 && cross1d_fits(m, ntargets, full)) {
     tm.mark();  // 5
     launch_cross1d(m, U.t, oc, ex, e4, C, targets.p, ntargets, row_vertex.p, full, (int)row_begin, (int)row_end,
@@ -351,8 +357,27 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     if (!full) build_tiles(m, 0, (int)n, tcol, st);
     ntiles = trow.ntiles;
     tm.mark();  // 5
+    // pass 1 (discovery): the orders of every pair; near pairs (order >= KW) are recorded
+    unsigned int cap = (unsigned int)std::min<int64_t>((int64_t)m.nc * 1024, (int64_t)1 << 31);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      near_keys.alloc(cap);
+      FL_CUDA(cudaMemsetAsync(near_cnt.p, 0, sizeof(unsigned int), st));
+      launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
+                         D->lda, ncolors, ntp, evc.p + 1, near_keys.p, near_cnt.p, cap, 1, nullptr, 0, nullptr, st);
+      unsigned int cnt = 0;
+      FL_CUDA(cudaMemcpyAsync(&cnt, near_cnt.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+      FL_CUDA(cudaStreamSynchronize(st));
+      nkeys = cnt;
+      if (cnt <= cap) break;
+      cap = cnt;                                 // rare: grow the list and rediscover
+    }
+    cudaEventRecord(xev[0], st);
+    // each near block once (warp per pair), then pass 2 computes the rest and scatters all
+    near_pairs_build(m, U.t, oc, ex, e4, near_keys.p, nkeys, near, evc.p + 1, st);
+    near_keys.free();
+    cudaEventRecord(xev[1], st);
     launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
-                       D->lda, ncolors, ntp, evc.p + 1, st);
+                       D->lda, ncolors, ntp, evc.p + 1, nullptr, nullptr, 0, 0, near.U.p, near.n, near.G.p, st);
   }
   tm.mark();  // 6
   DBuf<double> Lc((size_t)m.nc * 9);
@@ -367,7 +392,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   FL_CUDA(cudaMemcpyAsync(hev, evc.p, sizeof(hev), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&herr, m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
-  if (herr) throw Error(FL_E_QUAD, "a quadrature rule for a selected order is missing from the tables");
+  if (herr & 1) throw Error(FL_E_QUAD, "a quadrature rule for a selected order is missing from the tables");
+  if (herr & 4) throw Error(FL_E_CUDA, "internal: a near pair missing from the discovery pass");
 
   fl_assembly_stats& S = D->stats;
   const int64_t nc = m.nc;
@@ -388,6 +414,16 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   S.ms_local = tm.ms(6, 7);
   S.ms_total = tm.ms(0, 7);
   S.cross_tile_pairs = ntp;
+  S.near_pairs = near.n;
+  if (ntiles > 0) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, tm.e[5], xev[0]);
+    cudaEventElapsedTime(&b, xev[0], xev[1]);
+    cudaEventElapsedTime(&c, xev[1], tm.e[6]);
+    S.ms_discover = a; S.ms_near = b; S.ms_cross_compute = c;
+  }
+  cudaEventDestroy(xev[0]);
+  cudaEventDestroy(xev[1]);
   S.ncolors = ncolors;
   S.ntiles = ntiles;
   *out = D.release();
@@ -450,6 +486,21 @@ int32_t fl_dense_to_host(const fl_dense* A, double* host) {
   if (rows == 0 || A->n == 0) return FL_OK;
   FL_CUDA(cudaMemcpy2DAsync(host, A->n * sizeof(double), A->A.p, A->lda * sizeof(double), A->n * sizeof(double),
                             rows, cudaMemcpyDeviceToHost, A->stream));
+  FL_CUDA(cudaStreamSynchronize(A->stream));
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_dense_rows(const fl_dense* A, int64_t nrows, const int64_t* rows, double* host_out) {
+  FL_API_BEGIN
+  if (!A || (nrows > 0 && (!rows || !host_out))) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(A->device));
+  StreamScope scope(A->stream);
+  for (int64_t r = 0; r < nrows; ++r)
+    if (rows[r] < A->row0 || rows[r] >= A->row1) return fail(FL_E_ARG, "row outside the operator's rows");
+  for (int64_t r = 0; r < nrows; ++r)
+    FL_CUDA(cudaMemcpyAsync(host_out + r * A->n, A->A.p + (rows[r] - A->row0) * A->lda, A->n * sizeof(double),
+                            cudaMemcpyDeviceToHost, A->stream));
   FL_CUDA(cudaStreamSynchronize(A->stream));
   return FL_OK;
   FL_API_END

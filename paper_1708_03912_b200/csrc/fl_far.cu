@@ -161,10 +161,18 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, con
 }
 
 // ====================================================================== cross tiles
+#ifndef FL_FIXED3
+#define FL_FIXED3 0
+#endif
+#ifndef FL_PERSISTENT
+#define FL_PERSISTENT 1
+#endif
 constexpr int XT = 256;                 // threads per cross CTA
-constexpr int XWARPS = XT / 32;
+constexpr int NEAR_MARK = 255;          // pk of a near pair whose block came from fl_near.cu
 constexpr int SBR = 16, SBC = 32, SBP = SBR * SBC;
-constexpr int ROWL = MAX_VALENCE;  // max (cell, slot) entries of one tile row
+constexpr int ROWL = MAX_VALENCE;       // max (cell, slot) entries of one tile row
+constexpr int KPRE = 3;                 // node coordinates precomputed per sub-block for k <= KPRE
+constexpr int NPRE = 4 + 9;             // sum_{k=2}^{KPRE} k^2 (2D; 1D uses the first 5)
 
 struct TileView {
   const int* dofs; const int* ncell; const int* cells; const int* slots; const int* cstart;
@@ -173,6 +181,7 @@ struct TileView {
 struct CrossShared {
   double At[TILE][TILE + 1];
   double Gs[SBP][9];
+  double2 nodes[SBR + SBC][NPRE];       // mapped nodes (k <= KPRE) of the sub-block's row / column cells
   int rowc[TILE_MAXC], colc[TILE_MAXC];
   signed char rslot[TILE_MAXC][3], cslot[TILE_MAXC][3];
   short rowl[TILE][ROWL];
@@ -180,31 +189,124 @@ struct CrossShared {
   short plist[SBP];
   unsigned char pk[SBP];
   int hist[KDIR + 1], cursor[KDIR + 1];
-  int qlarge, qsmall, nlarge, nsmall;
+  int qlarge, qsmall, nlarge, nsmall, tile;
   int rdof[TILE], cdof[TILE];
-  int kofs[KDIR], kcnt[KDIR];
-  short cgl[4][SBC * 3];        // column-class lists of the current column sub-block: cc*4 + b
-  unsigned char cgs[4][SBC * 3];//   ... and the tile column slot
+  int kofs[KDIR];
+  short cgl[4][SBC * 3];                // column-class lists of the current column sub-block: cc*4 + b
+  unsigned char cgs[4][SBC * 3];        //   ... and the tile column slot
   int cgn[4];
   // followed by the packed disjoint rules: per node u0 u1 lw0 lw1 lw2 (5 doubles)
 };
 
+template <int D>
+__device__ __forceinline__ int pre_off(int k) {   // offset of order k in CrossShared::nodes
+  return D == 1 ? (k == 2 ? 0 : k == 3 ? 2 : 5) : (k == 2 ? 0 : k == 3 ? 4 : 13);
+}
+
+// fully unrolled block for small fixed k: column-cell nodes and weights held in registers
+template <int D, int E4, int KK>
+__device__ __forceinline__ void cross_fixed(const double2* __restrict__ Xn, const double2* __restrict__ Yn,
+                                            const double* __restrict__ rt, double JJ, double ex,
+                                            double* __restrict__ out) {
+  constexpr int NN = (D == 1) ? KK : KK * KK;
+  double2 y[NN];
+  double ly[NN][D + 1];
+#pragma unroll
+  for (int j = 0; j < NN; ++j) {
+    y[j] = Yn[j];
+#pragma unroll
+    for (int b = 0; b <= D; ++b) ly[j][b] = rt[5 * j + 2 + b];
+  }
+  double Gm[D + 1][D + 1] = {};
+#pragma unroll
+  for (int i = 0; i < NN; ++i) {
+    const double2 X = Xn[i];
+    double t[D + 1] = {};
+#pragma unroll
+    for (int j = 0; j < NN; ++j) {
+      const double d0 = X.x - y[j].x;
+      double r2;
+      if (D == 1) {
+        r2 = d0 * d0;
+      } else {
+        const double d1 = X.y - y[j].y;
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+#pragma unroll
+      for (int b = 0; b <= D; ++b) t[b] = fma(v, ly[j][b], t[b]);
+    }
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      const double lx = rt[5 * i + 2 + a];
+#pragma unroll
+      for (int b = 0; b <= D; ++b) Gm[a][b] = fma(lx, t[b], Gm[a][b]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) out[a * 3 + b] = (a <= D && b <= D) ? Gm[a < D + 1 ? a : 0][b < D + 1 ? b : 0] * JJ : 0.0;
+}
+
+// precomputed nodes, runtime k (k <= KPRE)
 template <int D, int E4>
-__device__ __forceinline__ void cross_pair_thread(const double* __restrict__ rt, int nn, const CellGeo& K,
-                                                  const CellGeo& L, double ex, double* __restrict__ out) {
+__device__ __forceinline__ void cross_pre(const double2* __restrict__ Xn, const double2* __restrict__ Yn,
+                                          const double* __restrict__ rt, int nn, double JJ, double ex,
+                                          double* __restrict__ out) {
+  double Gm[3][3] = {};
+  for (int i = 0; i < nn; ++i) {
+    const double2 X = Xn[i];
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 2
+    for (int j = 0; j < nn; ++j) {
+      const double2 Y = Yn[j];
+      const double d0 = X.x - Y.x;
+      double r2;
+      if (D == 1) {
+        r2 = d0 * d0;
+      } else {
+        const double d1 = X.y - Y.y;
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+      const double* ny = rt + 5 * j;
+      t0 = fma(v, ny[2], t0);
+      t1 = fma(v, ny[3], t1);
+      if (D == 2) t2 = fma(v, ny[4], t2);
+    }
+    const double* nx = rt + 5 * i;
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      Gm[a][0] = fma(nx[2 + a], t0, Gm[a][0]);
+      Gm[a][1] = fma(nx[2 + a], t1, Gm[a][1]);
+      if (D == 2) Gm[a][2] = fma(nx[2 + a], t2, Gm[a][2]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) out[a * 3 + b] = Gm[a][b] * JJ;
+}
+
+// on-the-fly mapping (any k); `lanes` = 32 (warp-cooperative over x nodes) or 1 (one thread)
+template <int D, int E4>
+__device__ __forceinline__ void cross_gen(const double* __restrict__ rt, int nn, const CellGeo& K, const CellGeo& L,
+                                          double ex, double* __restrict__ out, bool warp) {
+  const int lane = threadIdx.x & 31;
   double Gm[3][3] = {};
   const double ke00 = K.p[1][0] - K.p[0][0], ke01 = K.p[1][1] - K.p[0][1];
   const double ke10 = K.p[2][0] - K.p[0][0], ke11 = K.p[2][1] - K.p[0][1];
   const double le00 = L.p[1][0] - L.p[0][0], le01 = L.p[1][1] - L.p[0][1];
   const double le10 = L.p[2][0] - L.p[0][0], le11 = L.p[2][1] - L.p[0][1];
-  for (int x = 0; x < nn; ++x) {
+  for (int x = warp ? lane : 0; x < nn; x += warp ? 32 : 1) {
     const double* nx = rt + 5 * x;
     double X0, X1 = 0.0;
     if (D == 1) {
-      X0 = (K.p[0][0] + nx[0] * ke00) - L.p[0][0];
+      X0 = K.p[0][0] + nx[0] * ke00;
     } else {
-      X0 = (K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10)) - L.p[0][0];
-      X1 = (K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11)) - L.p[0][1];
+      X0 = K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10);
+      X1 = K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11);
     }
     double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll 2
@@ -212,11 +314,11 @@ __device__ __forceinline__ void cross_pair_thread(const double* __restrict__ rt,
       const double* ny = rt + 5 * y;
       double r2;
       if (D == 1) {
-        const double d0 = fma(-ny[0], le00, X0);
+        const double d0 = X0 - (L.p[0][0] + ny[0] * le00);
         r2 = d0 * d0;
       } else {
-        const double d0 = fma(-ny[1], le10, fma(-ny[0], le00, X0));
-        const double d1 = fma(-ny[1], le11, fma(-ny[0], le01, X1));
+        const double d0 = X0 - (L.p[0][0] + (ny[0] * le00 + ny[1] * le10));
+        const double d1 = X1 - (L.p[0][1] + (ny[0] * le01 + ny[1] * le11));
         r2 = fma(d1, d1, d0 * d0);
       }
       const double v = kpow<E4>(r2, ex);
@@ -236,60 +338,9 @@ __device__ __forceinline__ void cross_pair_thread(const double* __restrict__ rt,
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
-    for (int b = 0; b < 3; ++b) out[a * 3 + b] = Gm[a][b] * JJ;
-}
-
-template <int D, int E4>
-__device__ __forceinline__ void cross_pair_warp(const double* __restrict__ rt, int nn, const CellGeo& K,
-                                                const CellGeo& L, double ex, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  double Gm[3][3] = {};
-  const double ke00 = K.p[1][0] - K.p[0][0], ke01 = K.p[1][1] - K.p[0][1];
-  const double ke10 = K.p[2][0] - K.p[0][0], ke11 = K.p[2][1] - K.p[0][1];
-  const double le00 = L.p[1][0] - L.p[0][0], le01 = L.p[1][1] - L.p[0][1];
-  const double le10 = L.p[2][0] - L.p[0][0], le11 = L.p[2][1] - L.p[0][1];
-  for (int x = lane; x < nn; x += 32) {
-    const double* nx = rt + 5 * x;
-    double X0, X1 = 0.0;
-    if (D == 1) {
-      X0 = (K.p[0][0] + nx[0] * ke00) - L.p[0][0];
-    } else {
-      X0 = (K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10)) - L.p[0][0];
-      X1 = (K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11)) - L.p[0][1];
-    }
-    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-#pragma unroll 2
-    for (int y = 0; y < nn; ++y) {
-      const double* ny = rt + 5 * y;
-      double r2;
-      if (D == 1) {
-        const double d0 = fma(-ny[0], le00, X0);
-        r2 = d0 * d0;
-      } else {
-        const double d0 = fma(-ny[1], le10, fma(-ny[0], le00, X0));
-        const double d1 = fma(-ny[1], le11, fma(-ny[0], le01, X1));
-        r2 = fma(d1, d1, d0 * d0);
-      }
-      const double v = kpow<E4>(r2, ex);
-      t0 = fma(v, ny[2], t0);
-      t1 = fma(v, ny[3], t1);
-      if (D == 2) t2 = fma(v, ny[4], t2);
-    }
-#pragma unroll
-    for (int a = 0; a <= D; ++a) {
-      const double lx = nx[2 + a];
-      Gm[a][0] = fma(lx, t0, Gm[a][0]);
-      Gm[a][1] = fma(lx, t1, Gm[a][1]);
-      if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
-    }
-  }
-  const double JJ = K.J * L.J;
-#pragma unroll
-  for (int a = 0; a <= D; ++a)
-#pragma unroll
-    for (int b = 0; b <= D; ++b) {
-      const double s = warp_sum(Gm[a][b]);
-      if (lane == 0) out[a * 3 + b] = s * JJ;
+    for (int b = 0; b < 3; ++b) {
+      const double s = warp ? warp_sum(Gm[a][b]) : Gm[a][b];
+      if (!warp || lane == 0) out[a * 3 + b] = s * JJ;
     }
 }
 
@@ -297,43 +348,31 @@ template <int D, int E4>
 __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const double* __restrict__ tab,
                                                            DevTables dir, OrderConsts oc, double ex,
                                                            double negC, TileView R, TileView Cv,
-                                                           const int2* __restrict__ tpairs, int kmax,
-                                                           int symmetric, int row_begin, int row_end,
+                                                           const int2* __restrict__ tpairs, int ntp,
+                                                           int* __restrict__ queue, int kmax, int symmetric,
+                                                           int row_begin, int row_end,
                                                            double* __restrict__ Aout, int64_t lda,
-                                                           unsigned long long* __restrict__ evals) {
+                                                           unsigned long long* __restrict__ evals,
+                                                           unsigned long long* __restrict__ near_keys,
+                                                           unsigned int* __restrict__ near_count,
+                                                           unsigned int near_cap, int discover,
+                                                           const unsigned long long* __restrict__ nearU,
+                                                           int64_t nU, const double* __restrict__ nearG) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CrossShared& S = *reinterpret_cast<CrossShared*>(smem_raw);
   double* rtab = reinterpret_cast<double*>(smem_raw + ((sizeof(CrossShared) + 15) / 16) * 16);
-  const int KW = (D == 1) ? 12 : 5;       // warp-cooperative from k^d >= 144 (1D) / 25 (2D) x nodes
-  const int2 tp = tpairs[blockIdx.x];
-  const int tr = tp.x, tc = tp.y;
-  const int nR = R.ncell[tr], nC = Cv.ncell[tc];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int KW = (D == 1) ? KW1D : KW2D;   // near pairs (k >= KW) go to fl_near.cu when a list is given
+  const int tid = threadIdx.x, lane = tid & 31;
   unsigned long long my_evals = 0;
 
-  // ---- stage the tile metadata and the disjoint rules
-  for (int i = tid; i < nR; i += XT) {
-    S.rowc[i] = R.cells[tr * TILE_MAXC + i];
-    for (int a = 0; a < 3; ++a) S.rslot[i][a] = (signed char)R.slots[(tr * TILE_MAXC + i) * 3 + a];
-  }
-  for (int i = tid; i < nC; i += XT) {
-    S.colc[i] = Cv.cells[tc * TILE_MAXC + i];
-    for (int a = 0; a < 3; ++a) S.cslot[i][a] = (signed char)Cv.slots[(tc * TILE_MAXC + i) * 3 + a];
-  }
-  for (int i = tid; i < TILE; i += XT) {
-    S.rdof[i] = R.dofs[tr * TILE + i];
-    S.cdof[i] = Cv.dofs[tc * TILE + i];
-  }
+  // ---- the disjoint rules, once per CTA
   if (tid == 0) {
     int off = 0;
     for (int k = 0; k < KDIR; ++k) {
-      const int c = (k >= 2 && k <= kmax) ? dir.rule(T_DISJ, k).cnt : 0;
       S.kofs[k] = off;
-      S.kcnt[k] = c;
-      off += c;
+      off += (k >= 2 && k <= kmax) ? dir.rule(T_DISJ, k).cnt : 0;
     }
   }
-  for (int i = tid; i < TILE * (TILE + 1); i += XT) (&S.At[0][0])[i] = 0.0;
   __syncthreads();
   for (int k = 2; k <= kmax; ++k) {
     const RuleRef rr = dir.rule(T_DISJ, k);
@@ -343,134 +382,215 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
       o[0] = nd[0]; o[1] = nd[1]; o[2] = nd[3]; o[3] = nd[4]; o[4] = nd[5];
     }
   }
-  // tile row r -> its (row cell, slot) entries, in cell-list order
-  if (tid < TILE) {
-    int c = 0;
-    for (int i = 0; i < nR; ++i)
-      for (int a = 0; a <= D; ++a)
-        if (S.rslot[i][a] == tid && c < ROWL) S.rowl[tid][c++] = (short)(i * 4 + a);
-    S.rown[tid] = (unsigned char)c;
-  }
-  __syncthreads();
 
-  for (int cs0 = 0; cs0 < nC; cs0 += SBC) {
-    // column class c % 4 -> (column cell, slot) entries of this column sub-block
-    if (tid < 4) {
-      int c = 0;
-      for (int cc = 0; cc < SBC && cs0 + cc < nC; ++cc)
-        for (int b = 0; b <= D; ++b) {
-          const int cs = S.cslot[cs0 + cc][b];
-          if (cs >= 0 && (cs & 3) == tid) {
-            S.cgl[tid][c] = (short)(cc * 4 + b);
-            S.cgs[tid][c] = (unsigned char)cs;
-            ++c;
-          }
-        }
-      S.cgn[tid] = c;
+  for (;;) {
+    if (tid == 0) S.tile = atomicAdd(queue, 1);       // tile pairs come heavy (near) first
+    __syncthreads();
+    const int ti = S.tile;
+    if (ti >= ntp) break;
+    const int2 tp = tpairs[ti];
+    const int tr = tp.x, tc = tp.y;
+    const int nR = R.ncell[tr], nC = Cv.ncell[tc];
+
+    // ---- stage the tile metadata
+    for (int i = tid; i < nR; i += XT) {
+      S.rowc[i] = R.cells[tr * TILE_MAXC + i];
+      for (int a = 0; a < 3; ++a) S.rslot[i][a] = (signed char)R.slots[(tr * TILE_MAXC + i) * 3 + a];
     }
-    for (int rs0 = 0; rs0 < nR; rs0 += SBR) {
-      // ---- (A) orders of the 512 pairs of this sub-block
-      if (tid <= KDIR) S.hist[tid] = 0;
-      __syncthreads();
-      for (int p = tid; p < SBP; p += XT) {
-        const int rc = rs0 + p / SBC, cc = cs0 + p % SBC;
-        int k = 0;
-        if (rc < nR && cc < nC) {
-          const int idK = S.rowc[rc], idL = S.colc[cc];
-          const CellGeo& Kg = m.geo[idK];
-          const CellGeo& Lg = m.geo[idL];
-          if (!touching<D>(Kg, Lg)) {
-            // the reference orders a disjoint pair as (min id, max id) (assembly.py:973-982, :705)
-            const CellGeo& P = (idK < idL) ? Kg : Lg;
-            const CellGeo& Qg = (idK < idL) ? Lg : Kg;
-            k = order_disjoint_fast(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
+    for (int i = tid; i < nC; i += XT) {
+      S.colc[i] = Cv.cells[tc * TILE_MAXC + i];
+      for (int a = 0; a < 3; ++a) S.cslot[i][a] = (signed char)Cv.slots[(tc * TILE_MAXC + i) * 3 + a];
+    }
+    for (int i = tid; i < TILE; i += XT) {
+      S.rdof[i] = R.dofs[tr * TILE + i];
+      S.cdof[i] = Cv.dofs[tc * TILE + i];
+    }
+    for (int i = tid; i < TILE * (TILE + 1); i += XT) (&S.At[0][0])[i] = 0.0;
+    __syncthreads();
+    if (tid < TILE) {                    // tile row r -> its (row cell, slot) entries, in cell-list order
+      int c = 0;
+      for (int i = 0; i < nR; ++i)
+        for (int a = 0; a <= D; ++a)
+          if (S.rslot[i][a] == tid && c < ROWL) S.rowl[tid][c++] = (short)(i * 4 + a);
+      S.rown[tid] = (unsigned char)c;
+    }
+
+    for (int cs0 = 0; cs0 < nC; cs0 += SBC) {
+      if (tid < 4) {                     // column class c % 4 -> (column cell, slot) entries
+        int c = 0;
+        for (int cc = 0; cc < SBC && cs0 + cc < nC; ++cc)
+          for (int b = 0; b <= D; ++b) {
+            const int cs = S.cslot[cs0 + cc][b];
+            if (cs >= 0 && (cs & 3) == tid) {
+              S.cgl[tid][c] = (short)(cc * 4 + b);
+              S.cgs[tid][c] = (unsigned char)cs;
+              ++c;
+            }
+          }
+        S.cgn[tid] = c;
+      }
+      for (int rs0 = 0; rs0 < nR; rs0 += SBR) {
+        // ---- (A) orders of the 512 pairs of this sub-block
+        if (tid <= KDIR) S.hist[tid] = 0;
+        __syncthreads();
+        for (int p = tid; p < SBP; p += XT) {
+          const int rc = rs0 + p / SBC, cc = cs0 + p % SBC;
+          int k = 0;
+          if (rc < nR && cc < nC) {
+            const int idK = S.rowc[rc], idL = S.colc[cc];
+            const CellGeo& Kg = m.geo[idK];
+            const CellGeo& Lg = m.geo[idL];
+            if (!touching<D>(Kg, Lg)) {
+              // the reference orders a disjoint pair as (min id, max id) (assembly.py:973-982, :705)
+              const CellGeo& P = (idK < idL) ? Kg : Lg;
+              const CellGeo& Qg = (idK < idL) ? Lg : Kg;
+              k = order_disjoint_fast(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
+              if (k >= KW && (discover || nearG != nullptr)) {
+                // near pair: its block is computed once by the near-pair kernel (fl_near.cu)
+                const unsigned long long key = ((unsigned long long)min(idK, idL) << 32) | (unsigned)max(idK, idL);
+                if (discover) {
+                  const unsigned int slot = atomicAdd(near_count, 1u);
+                  if (slot < near_cap) near_keys[slot] = key;
+                  k = 0;
+                } else {
+                  int64_t lo = 0, hi = nU - 1;                 // binary search in the sorted unique keys
+                  while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (nearU[mid] < key) lo = mid + 1; else hi = mid;
+                  }
+                  if (nearU[lo] != key) atomicOr(m.err, 4);       // cannot happen: same orders as discovery
+                  const double* g = nearG + lo * 9;
+                  const bool tr = idK > idL;                     // M^{min,max}: transpose when K is the max
+#pragma unroll
+                  for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) S.Gs[p][a * 3 + b] = tr ? g[b * 3 + a] : g[a * 3 + b];
+                  k = NEAR_MARK;
+                }
+              }
+            }
+          }
+          S.pk[p] = (unsigned char)k;
+          if (k != NEAR_MARK) atomicAdd(&S.hist[k], 1);
+        }
+        __syncthreads();
+        if (discover) continue;
+        if (tid == 0) {                  // descending k: large (warp) pairs first
+          int off = 0;
+          for (int k = KDIR - 1; k >= 1; --k) { S.cursor[k] = off; off += S.hist[k]; }
+          int nl = 0;
+          for (int k = KDIR - 1; k >= KW; --k) nl += S.hist[k];
+          S.nlarge = nl;
+          S.nsmall = off - nl;
+          S.qlarge = 0;
+          S.qsmall = 0;
+        }
+        // ---- (A2) node coordinates of the sub-block's cells for the small orders present
+        for (int k = 2; k <= KPRE; ++k) {
+          if (S.hist[k] == 0) continue;
+          const int nn = (D == 1) ? k : k * k;
+          const double* rt = rtab + 5 * S.kofs[k];
+          for (int idx = tid; idx < (SBR + SBC) * nn; idx += XT) {
+            const int c = idx / nn, x = idx % nn;
+            const int cl = (c < SBR) ? rs0 + c : cs0 + (c - SBR);
+            if ((c < SBR && cl >= nR) || (c >= SBR && cl >= nC)) continue;
+            const CellGeo& g = m.geo[(c < SBR) ? S.rowc[cl] : S.colc[cl]];
+            double X0, X1 = 0.0;
+            if (D == 1) {
+              X0 = g.p[0][0] + rt[5 * x] * (g.p[1][0] - g.p[0][0]);
+            } else {
+              X0 = g.p[0][0] + (rt[5 * x] * (g.p[1][0] - g.p[0][0]) + rt[5 * x + 1] * (g.p[2][0] - g.p[0][0]));
+              X1 = g.p[0][1] + (rt[5 * x] * (g.p[1][1] - g.p[0][1]) + rt[5 * x + 1] * (g.p[2][1] - g.p[0][1]));
+            }
+            S.nodes[c][pre_off<D>(k) + x] = make_double2(X0, X1);
           }
         }
-        S.pk[p] = (unsigned char)k;
-        atomicAdd(&S.hist[k], 1);
-      }
-      __syncthreads();
-      if (tid == 0) {                    // descending k: large (warp) pairs first
-        int off = 0;
-        for (int k = KDIR - 1; k >= 1; --k) { S.cursor[k] = off; off += S.hist[k]; }
-        int nl = 0;
-        for (int k = KDIR - 1; k >= KW; --k) nl += S.hist[k];
-        S.nlarge = nl;
-        S.nsmall = off - nl;
-        S.qlarge = 0;
-        S.qsmall = 0;
-      }
-      __syncthreads();
-      for (int p = tid; p < SBP; p += XT) {
-        const int k = S.pk[p];
-        if (k > 0) S.plist[atomicAdd(&S.cursor[k], 1)] = (short)p;
-      }
-      __syncthreads();
-      // ---- (B) the 3x3 blocks, pairs sorted by k
-      const int nl = S.nlarge, ns = S.nsmall;
-      for (;;) {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(&S.qlarge, 1);
-        i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= nl) break;
-        const int p = S.plist[i];
-        const int k = S.pk[p];
-        const int nn = (D == 1) ? k : k * k;
-        cross_pair_warp<D, E4>(rtab + 5 * S.kofs[k], nn, m.geo[S.rowc[rs0 + p / SBC]],
-                               m.geo[S.colc[cs0 + p % SBC]], ex, S.Gs[p]);
-        if (lane == 0) my_evals += (unsigned long long)nn * nn;
-      }
-      for (;;) {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(&S.qsmall, 32);
-        i = __shfl_sync(0xffffffffu, i, 0) + lane;
-        if (i - lane >= ns) break;
-        if (i < ns) {
-          const int p = S.plist[nl + i];
+        __syncthreads();
+        for (int p = tid; p < SBP; p += XT) {
+          const int k = S.pk[p];
+          if (k > 0 && k != NEAR_MARK) S.plist[atomicAdd(&S.cursor[k], 1)] = (short)p;
+        }
+        __syncthreads();
+        // ---- (B) the 3x3 blocks, pairs sorted by k
+        const int nl = S.nlarge, ns = S.nsmall;
+        for (;;) {
+          int i = 0;
+          if (lane == 0) i = atomicAdd(&S.qlarge, 1);
+          i = __shfl_sync(0xffffffffu, i, 0);
+          if (i >= nl) break;
+          const int p = S.plist[i];
           const int k = S.pk[p];
           const int nn = (D == 1) ? k : k * k;
-          cross_pair_thread<D, E4>(rtab + 5 * S.kofs[k], nn, m.geo[S.rowc[rs0 + p / SBC]],
-                                   m.geo[S.colc[cs0 + p % SBC]], ex, S.Gs[p]);
-          my_evals += (unsigned long long)nn * nn;
+          cross_gen<D, E4>(rtab + 5 * S.kofs[k], nn, m.geo[S.rowc[rs0 + p / SBC]], m.geo[S.colc[cs0 + p % SBC]],
+                           ex, S.Gs[p], true);
+          if (lane == 0) my_evals += (unsigned long long)nn * nn;
         }
-      }
-      __syncthreads();
-      // ---- (C) row-owner scatter: 4 threads per tile row, column classes c % 4
-      {
-        const int r = tid >> 2, cg = tid & 3;
-        const int ng = S.cgn[cg];
-        for (int e = 0; e < S.rown[r]; ++e) {
-          const int rc = S.rowl[r][e] >> 2, a = S.rowl[r][e] & 3;
-          if (rc < rs0 || rc >= rs0 + SBR) continue;
-          const int pr = (rc - rs0) * SBC;
-          for (int u = 0; u < ng; ++u) {
-            const int it = S.cgl[cg][u];
-            const int p = pr + (it >> 2);
-            if (S.pk[p] == 0) continue;
-            S.At[r][S.cgs[cg][u]] += negC * S.Gs[p][a * 3 + (it & 3)];
+        for (;;) {
+          int i = 0;
+          if (lane == 0) i = atomicAdd(&S.qsmall, 32);
+          i = __shfl_sync(0xffffffffu, i, 0) + lane;
+          if (i - lane >= ns) break;
+          if (i < ns) {
+            const int p = S.plist[nl + i];
+            const int k = S.pk[p];
+            const int nn = (D == 1) ? k : k * k;
+            const int r = p / SBC, c = p % SBC;
+            const double* rt = rtab + 5 * S.kofs[k];
+            if (k <= KPRE) {
+              const double JJ = m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
+              const double2* Xn = &S.nodes[r][pre_off<D>(k)];
+              const double2* Yn = &S.nodes[SBR + c][pre_off<D>(k)];
+              if (k == 2) cross_fixed<D, E4, 2>(Xn, Yn, rt, JJ, ex, S.Gs[p]);
+#if FL_FIXED3
+              else if (k == 3) cross_fixed<D, E4, 3>(Xn, Yn, rt, JJ, ex, S.Gs[p]);
+#endif
+              else cross_pre<D, E4>(Xn, Yn, rt, nn, JJ, ex, S.Gs[p]);
+            } else {
+              cross_gen<D, E4>(rt, nn, m.geo[S.rowc[rs0 + r]], m.geo[S.colc[cs0 + c]], ex, S.Gs[p], false);
+            }
+            my_evals += (unsigned long long)nn * nn;
           }
         }
+        __syncthreads();
+        // ---- (C) row-owner scatter: 4 threads per tile row, column classes c % 4
+        {
+          const int r = tid >> 2, cg = tid & 3;
+          const int ng = S.cgn[cg];
+          for (int e = 0; e < S.rown[r]; ++e) {
+            const int rc = S.rowl[r][e] >> 2, a = S.rowl[r][e] & 3;
+            if (rc < rs0 || rc >= rs0 + SBR) continue;
+            const int pr = (rc - rs0) * SBC;
+            for (int u = 0; u < ng; ++u) {
+              const int it = S.cgl[cg][u];
+              const int p = pr + (it >> 2);
+              if (S.pk[p] == 0) continue;
+              S.At[r][S.cgs[cg][u]] += negC * S.Gs[p][a * 3 + (it & 3)];
+            }
+          }
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
+    // ---- write the tile (and its mirror) once
+    if (discover) { __syncthreads(); continue; }
+    for (int idx = tid; idx < TILE * TILE; idx += XT) {
+      const int r = idx / TILE, c = idx % TILE;
+      const int i = S.rdof[r], j = S.cdof[c];
+      if (i >= row_begin && i < row_end && j >= 0) Aout[(int64_t)(i - row_begin) * lda + j] = S.At[r][c];
+    }
+    if (symmetric && tr != tc) {
+      for (int idx = tid; idx < TILE * TILE; idx += XT) {
+        const int c = idx / TILE, r = idx % TILE;
+        const int i = S.rdof[r], j = S.cdof[c];
+        if (i >= 0 && j >= row_begin && j < row_end) Aout[(int64_t)(j - row_begin) * lda + i] = S.At[r][c];
+      }
+    }
+    __syncthreads();
   }
   if (evals) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_evals += __shfl_xor_sync(0xffffffffu, my_evals, o);
     if (lane == 0) atomicAdd(evals, my_evals);
-  }
-  // ---- write the tile (and its mirror) once
-  for (int idx = tid; idx < TILE * TILE; idx += XT) {
-    const int r = idx / TILE, c = idx % TILE;
-    const int i = S.rdof[r], j = S.cdof[c];
-    if (i >= row_begin && i < row_end && j >= 0) Aout[(int64_t)(i - row_begin) * lda + j] = S.At[r][c];
-  }
-  if (symmetric && tr != tc) {
-    for (int idx = tid; idx < TILE * TILE; idx += XT) {
-      const int c = idx / TILE, r = idx % TILE;
-      const int i = S.rdof[r], j = S.cdof[c];
-      if (i >= 0 && j >= row_begin && j < row_end) Aout[(int64_t)(j - row_begin) * lda + i] = S.At[r][c];
-    }
   }
 }
 
@@ -586,7 +706,9 @@ void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const 
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                         double Cds, const Tiles& rows, const Tiles& cols, bool symmetric, int row_begin,
                         int row_end, double* A, int64_t lda, int ncolors, int64_t& ntilepairs,
-                        unsigned long long* evals, cudaStream_t st) {
+                        unsigned long long* evals, unsigned long long* near_keys, unsigned int* near_count,
+                        unsigned int near_cap, int discover, const unsigned long long* nearU, int64_t nU,
+                        const double* nearG, cudaStream_t st) {
   (void)ncolors;
   std::vector<int2> hp;
   for (int r = 0; r < rows.ntiles; ++r)
@@ -620,24 +742,29 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
   const size_t smem = cross_smem_bytes(m.d);
   const double negC = -Cds;   // (C/2) * (-2)  (assembly.py:723, :1100)
   const int kmax = oc.cap_disjoint;
-  const int64_t np_ = (int64_t)hp.size();
-  for (int64_t base = 0; base < np_; base += 2147483647LL) {
-    const int grid = (int)std::min<int64_t>(np_ - base, 2147483647LL);
-    if (m.d == 1) {
-      FL_E4_SWITCH(e4, {
-        FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<1, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cross_tile_kernel<1, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, kmax,
-                                                       symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
-      });
-    } else {
-      FL_E4_SWITCH(e4, {
-        FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<2, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        cross_tile_kernel<2, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p + base, kmax,
-                                                       symmetric ? 1 : 0, row_begin, row_end, A, lda, evals), ::fl::note_launch();
-      });
-    }
-    FL_CHECK_LAUNCH();
+  const int ntp = (int)hp.size();
+  DBuf<int> queue(1);
+  FL_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = FL_PERSISTENT ? std::min(ntp, 2 * sms) : ntp;   // persistent: 2 CTAs per SM
+  if (m.d == 1) {
+    FL_E4_SWITCH(e4, {
+      FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<1, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cross_tile_kernel<1, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p, ntp, queue.p, kmax,
+                                                     symmetric ? 1 : 0, row_begin, row_end, A, lda, evals, near_keys,
+                                                     near_count, near_cap, discover, nearU, nU, nearG), ::fl::note_launch();
+    });
+  } else {
+    FL_E4_SWITCH(e4, {
+      FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<2, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cross_tile_kernel<2, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p, ntp, queue.p, kmax,
+                                                     symmetric ? 1 : 0, row_begin, row_end, A, lda, evals, near_keys,
+                                                     near_count, near_cap, discover, nearU, nU, nearG), ::fl::note_launch();
+    });
   }
+  FL_CHECK_LAUNCH();
   FL_CUDA(cudaStreamSynchronize(st));   // dp is freed on return
 }
 

@@ -160,7 +160,20 @@ void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const 
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,
                         int e4, double Cds, const Tiles& rows, const Tiles& cols, bool symmetric,
                         int row_begin, int row_end, double* A, int64_t lda, int ncolors,
-                        int64_t& ntilepairs, unsigned long long* evals, cudaStream_t st);
+                        int64_t& ntilepairs, unsigned long long* evals, unsigned long long* near_keys,
+                        unsigned int* near_count, unsigned int near_cap, int discover,
+                        const unsigned long long* nearU, int64_t nU, const double* nearG, cudaStream_t st);
+// fl_near.cu: near disjoint pairs (order >= KW) collected by the cross tiles, one block each
+constexpr int KW2D = 5, KW1D = 12;
+struct NearPairs {
+  int64_t n = 0;
+  DBuf<unsigned long long> U;           // sorted unique keys (min << 32 | max)
+  DBuf<int> P, Q;                       // the two cells of each key
+  DBuf<double> G;                       // n*9: M^{P,Q} (cross_matrices orientation)
+};
+void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                      unsigned long long* keys, int64_t nkeys, NearPairs& np, unsigned long long* evals,
+                      cudaStream_t st);
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
 // fl_far1d.cu (1D: lean tail, packed pair-block cross + gather)

@@ -1,0 +1,171 @@
+// Near disjoint pairs: the few cell pairs whose Gauss order k >= KW (k^(2d) >= 625 nodes in 2D)
+// carry most of the cross-term work (cross_matrices, assembly.py:172-229) but are rare.  The
+// cross tiles only record them; here they are de-duplicated (sort + unique of the (min, max)
+// key — the reference's own orientation, assembly.py:973-982), each block is computed ONCE by a
+// warp with the column cell's mapped nodes staged in shared memory (no barriers, no halo
+// redundancy), and CSR indexes let the row-owner pull (fl_local.cu) add -C*M to every entry
+// in a fixed order.
+#include <cub/cub.cuh>
+
+#include "fl_internal.h"
+
+namespace fl {
+
+constexpr int NW = 8;          // warps per CTA
+constexpr int NMAXN = 81;      // max k^d nodes (2D cap 9; 1D k <= 32)
+
+template <int D, int E4>
+__global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const double* __restrict__ tab,
+                                                             DevTables dir, OrderConsts oc, double ex,
+                                                             const int* __restrict__ P, const int* __restrict__ Q,
+                                                             int64_t n, double* __restrict__ G,
+                                                             unsigned long long* __restrict__ evals) {
+  __shared__ double2 sy[NW][NMAXN];
+  __shared__ double slw[NW][NMAXN][3];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long my = 0;
+  for (int64_t pi = (int64_t)blockIdx.x * NW + w; pi < n; pi += (int64_t)gridDim.x * NW) {
+    const CellGeo& A = m.geo[P[pi]];
+    const CellGeo& B = m.geo[Q[pi]];
+    const int k = order_disjoint_fast(oc, oc.coff, A, B, dist_estimate<D>(A, B));   // (min, max) orientation
+    const RuleRef rr = dir.rule(T_DISJ, k);
+    const int nn = rr.cnt;
+    // stage the y (column cell) nodes, absolute coordinates as _map_points forms them
+    for (int y = lane; y < nn; y += 32) {
+      const double* nd = tab + (size_t)(rr.off + y) * NODE;
+      double Y0, Y1 = 0.0;
+      if (D == 1) {
+        Y0 = B.p[0][0] + nd[0] * (B.p[1][0] - B.p[0][0]);
+      } else {
+        Y0 = B.p[0][0] + (nd[0] * (B.p[1][0] - B.p[0][0]) + nd[1] * (B.p[2][0] - B.p[0][0]));
+        Y1 = B.p[0][1] + (nd[0] * (B.p[1][1] - B.p[0][1]) + nd[1] * (B.p[2][1] - B.p[0][1]));
+      }
+      sy[w][y] = make_double2(Y0, Y1);
+      slw[w][y][0] = nd[3];
+      slw[w][y][1] = nd[4];
+      slw[w][y][2] = nd[5];
+    }
+    __syncwarp();
+    // work items (x node, y chunk): split the y range so that k^d * S fills the warp well
+    int S = 1;
+    {
+      float best = 0.f;
+      for (int s = 1; s <= 4; ++s) {
+        const int items = nn * s;
+        const float u = (float)items / (32.f * (float)((items + 31) / 32));
+        if (u > best + 1e-3f) { best = u; S = s; }
+      }
+    }
+    const int chunk = (nn + S - 1) / S;
+    double Gm[3][3] = {};
+    for (int it = lane; it < nn * S; it += 32) {
+      const int x = it / S, c = it % S;
+      const double* nx = tab + (size_t)(rr.off + x) * NODE;
+      double X0, X1 = 0.0;
+      if (D == 1) {
+        X0 = A.p[0][0] + nx[0] * (A.p[1][0] - A.p[0][0]);
+      } else {
+        X0 = A.p[0][0] + (nx[0] * (A.p[1][0] - A.p[0][0]) + nx[1] * (A.p[2][0] - A.p[0][0]));
+        X1 = A.p[0][1] + (nx[0] * (A.p[1][1] - A.p[0][1]) + nx[1] * (A.p[2][1] - A.p[0][1]));
+      }
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      const int y1 = min(nn, (c + 1) * chunk);
+#pragma unroll 2
+      for (int y = c * chunk; y < y1; ++y) {
+        const double2 Y = sy[w][y];
+        const double d0 = X0 - Y.x;
+        double r2;
+        if (D == 1) {
+          r2 = d0 * d0;
+        } else {
+          const double d1 = X1 - Y.y;
+          r2 = fma(d1, d1, d0 * d0);
+        }
+        const double v = kpow<E4>(r2, ex);
+        t0 = fma(v, slw[w][y][0], t0);
+        t1 = fma(v, slw[w][y][1], t1);
+        if (D == 2) t2 = fma(v, slw[w][y][2], t2);
+      }
+#pragma unroll
+      for (int a = 0; a <= D; ++a) {
+        const double lx = nx[3 + a];
+        Gm[a][0] = fma(lx, t0, Gm[a][0]);
+        Gm[a][1] = fma(lx, t1, Gm[a][1]);
+        if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
+      }
+    }
+    const double JJ = A.J * B.J;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const double s = warp_sum(Gm[a][b]);
+        if (lane == 0) G[pi * 9 + a * 3 + b] = s * JJ;
+      }
+    if (lane == 0) my += (unsigned long long)nn * nn;
+    __syncwarp();
+  }
+  if (lane == 0 && evals && my) atomicAdd(evals, my);
+}
+
+__global__ void split_keys_kernel(const unsigned long long* keys, int64_t n, int* P, int* Q, int* idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  P[i] = (int)(keys[i] >> 32);
+  Q[i] = (int)(keys[i] & 0xffffffffu);
+  idx[i] = (int)i;
+}
+#define FL_E4_SWITCHN(e4, ...)                                \
+  switch (e4) {                                               \
+    case 6: { constexpr int E4 = 6; __VA_ARGS__; } break;     \
+    case 8: { constexpr int E4 = 8; __VA_ARGS__; } break;     \
+    case 10: { constexpr int E4 = 10; __VA_ARGS__; } break;   \
+    case 12: { constexpr int E4 = 12; __VA_ARGS__; } break;   \
+    case 14: { constexpr int E4 = 14; __VA_ARGS__; } break;   \
+    default: { constexpr int E4 = 0; __VA_ARGS__; } break;    \
+  }
+
+void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                      unsigned long long* keys, int64_t nkeys, NearPairs& np, unsigned long long* evals,
+                      cudaStream_t st) {
+  np.n = 0;
+  if (nkeys <= 0) {
+    np.U.alloc(1); np.P.alloc(1); np.Q.alloc(1); np.G.alloc(1);
+    return;
+  }
+  // sort + unique of the (min, max) keys: deterministic order of the pairs
+  DBuf<unsigned long long> sorted(nkeys);
+  np.U.alloc(nkeys);
+  DBuf<int> nsel(1);
+  {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, sorted.p, (int)nkeys, 0, 64, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceRadixSort::SortKeys(tb.p, tmp, keys, sorted.p, (int)nkeys, 0, 64, st));
+    size_t tmp2 = 0;
+    cub::DeviceSelect::Unique(nullptr, tmp2, sorted.p, np.U.p, nsel.p, (int)nkeys, st);
+    DBuf<unsigned char> tb2(tmp2);
+    FL_CUDA(cub::DeviceSelect::Unique(tb2.p, tmp2, sorted.p, np.U.p, nsel.p, (int)nkeys, st));
+  }
+  int nu = 0;
+  FL_CUDA(cudaMemcpyAsync(&nu, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  np.n = nu;
+  np.P.alloc(nu); np.Q.alloc(nu); np.G.alloc((size_t)nu * 9);
+  DBuf<int> idx(nu);
+  split_keys_kernel<<<(nu + 255) / 256, 256, 0, st>>>(np.U.p, nu, np.P.p, np.Q.p, idx.p), ::fl::note_launch();
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((nu + NW - 1) / NW, (int64_t)sms * 8);
+  if (m.d == 1) {
+    FL_E4_SWITCHN(e4, (near_block_kernel<1, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, np.P.p, np.Q.p, nu,
+                                                                         np.G.p, evals), ::fl::note_launch()));
+  } else {
+    FL_E4_SWITCHN(e4, (near_block_kernel<2, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, np.P.p, np.Q.p, nu,
+                                                                         np.G.p, evals), ::fl::note_launch()));
+  }
+  FL_CHECK_LAUNCH();
+}
+
+}  // namespace fl

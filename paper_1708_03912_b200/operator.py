@@ -83,6 +83,13 @@ class DenseDeviceOperator:
         _lib.check(_lib.load().fl_dense_to_host(self.handle, out.ctypes.data))
         return out
 
+    def rows(self, idx):
+        """Copy the global rows `idx` (inside this operator's row range) to the host."""
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.empty((len(idx), self.n))
+        _lib.check(_lib.load().fl_dense_rows(self.handle, len(idx), idx.ctypes.data, out.ctypes.data))
+        return out
+
     def diag(self):
         out = np.empty(self.row_end - self.row_begin)
         _lib.check(_lib.load().fl_dense_diag(self.handle, out.ctypes.data))
