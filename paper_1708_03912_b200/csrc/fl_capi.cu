@@ -101,6 +101,12 @@ OrderConsts make_order_consts(const fl_order_params& p, int d, double s, int64_t
   oc.coff = p.C_offset;
   oc.coff_tail = p.C_offset - 4;                                    // assembly.py:985, :997
   oc.cap_disjoint = (d == 2) ? 9 : KMAX;                            // quadrature.py:171-175
+  oc.lead_f = (float)oc.lead_lnn;
+  oc.s_f = (float)oc.s;
+  oc.sm1_f = (float)oc.sm1;
+  oc.lr2_f = (float)oc.ln_rho2;
+  oc.coff_f = (float)oc.coff;
+  oc.coff_tail_f = (float)oc.coff_tail;
   return oc;
 }
 

@@ -5,25 +5,33 @@
 //  * tail1d:  one warp per target cell, one LANE per source cell, six per-lane accumulators
 //             (the six cell-rule nodes), a single warp reduction at the end.  Source data is
 //             read from structure-of-arrays (coalesced, no 128-B record loads).
-//  * cross1d: every unordered disjoint pair (K < L) gets its 2x2 block M^{K,L} once
-//             (cross_matrices, assembly.py:172-229, orders in the reference's (min, max)
-//             orientation) into a packed triangular buffer; a tiled gather then forms
-//             A[i][j] = -C sum_{K∋i, L∋j} M[a][b] (assembly.py:723-725) with the sum taken in
-//             one canonical order for (i, j) and (j, i): the cross part is exactly symmetric
-//             and no halo pair is ever evaluated twice.
+//  * cross1d (fused, default): a CTA owns a 32 x 32 tile of DoFs (upper triangle, mirrored),
+//             computes the 2x2 blocks M^{K,L} (cross_matrices, assembly.py:172-229, orders in
+//             the reference's (min, max) orientation) of the <= 40 x 40 cell pairs behind it
+//             into shared memory, bucketed by order so each warp runs one fixed-k unrolled
+//             block, and forms A[i][j] = -C sum_{K∋i, L∋j} M[a][b] (assembly.py:723-725) with
+//             the sum in one canonical order for (i, j) and (j, i): exactly symmetric.
+//  * cross1d (pairs, fallback when a tile has > 40 cells, or FRACLAP_CROSS1D=pairs): every
+//             unordered pair's block once into a packed triangular buffer, then a tiled gather
+//             with the same canonical order; bitwise identical results.
 // Row-block (multi-GPU) mode computes the ordered pairs (K in the owned rows' cells, all L)
 // into a rectangular buffer instead.
 #include "fl_internal.h"
+
+#include <climits>
+#include <cstdlib>
+#include <string>
 
 namespace fl {
 
 struct Src1D {
   const double *x0, *x1, *lo, *hi, *h, *lh;
   const int *v0, *v1;
+  const float *lnhf, *lhf;      // __logf((float)h), (float)|ln h| for the fp32 order estimate
 };
 
 __global__ void build_src1d_kernel(DevMesh m, double* x0, double* x1, double* lo, double* hi, double* h,
-                                   double* lh, int* v0, int* v1) {
+                                   double* lh, int* v0, int* v1, float* lnhf, float* lhf) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= m.nc) return;
   const CellGeo& g = m.geo[c];
@@ -35,6 +43,15 @@ __global__ void build_src1d_kernel(DevMesh m, double* x0, double* x1, double* lo
   lh[c] = g.ldiam;
   v0[c] = g.v[0];
   v1[c] = g.v[1];
+  lnhf[c] = __logf((float)g.diam);
+  lhf[c] = (float)g.ldiam;
+}
+
+// the exact fp64 order (rare: the fp32 estimate is within ORDER_DELTA of an integer), kept out
+// of line so its registers do not count against the hot loops
+static __device__ __noinline__ int order_exact1d(const OrderConsts& oc, double coff, double hA, double lA, double hB,
+                                                 double lB, double dist) {
+  return order_disjoint_s(oc, coff, hA, lA, hB, lB, dist);
 }
 
 // ------------------------------------------------------------------ tail
@@ -50,6 +67,7 @@ __global__ void __launch_bounds__(128, 4) tail1d_kernel(DevMesh m, const double*
   if (ti >= ntargets) return;
   const int K = targets[ti];
   const double alo = S.lo[K], ahi = S.hi[K], ah = S.h[K], alh = S.lh[K];
+  const float alnf = S.lnhf[K], alhf = S.lhf[K];
   const int av0 = S.v0[K], av1 = S.v1[K];
   double xq[Q], acc[Q];
 #pragma unroll
@@ -63,9 +81,14 @@ __global__ void __launch_bounds__(128, 4) tail1d_kernel(DevMesh m, const double*
     if (s == K || bv0 == av0 || bv0 == av1 || bv1 == av0 || bv1 == av1) continue;   // N(K) (:999-1009)
     const double blo = S.lo[s], bhi = S.hi[s];
     const double dist = fmax(fmax(__dsub_rn(blo, ahi), __dsub_rn(alo, bhi)), 0.0);   // (:750-752)
-    const int k = order_disjoint_fast_s(oc, oc.coff_tail, ah, alh, S.h[s], S.lh[s], dist);
+    const double J = S.h[s];
+    int k = 0;
+    if (dist > 1e-30)
+      k = order_from_estimate(order_estimate_f(oc, oc.coff_tail_f, alnf, alhf, S.lnhf[s], S.lhf[s],
+                                               __logf((float)dist)), oc.cap_disjoint);
+    if (!k) k = order_exact1d(oc, oc.coff_tail, ah, alh, J, S.lh[s], dist);
     const RuleRef rr = dir.rule(T_DISJ, k);
-    const double x0 = S.x0[s], e = S.x1[s] - x0, J = S.h[s];
+    const double x0 = S.x0[s], e = S.x1[s] - x0;
     nodes += (unsigned long long)k;
     for (int r = 0; r < k; ++r) {
       const double* nd = tab + (size_t)(rr.off + r) * NODE;
@@ -185,6 +208,383 @@ __device__ __forceinline__ double comp(const double4& g, int a, int b) {
   return a == 0 ? (b == 0 ? g.x : g.y) : (b == 0 ? g.z : g.w);
 }
 
+// ------------------------------------------------------------------ cross: fused DoF tiles
+// The fused path never materialises the pair blocks: a CTA owns a T1 x T1 tile of DoFs
+// (bi <= bj, mirrored), computes the blocks M^{K,L} of the <= T1C x T1C cell pairs behind it
+// into shared memory and sums them into the tile in the same canonical order as gather1d.
+// Cell pairs are bucketed by order inside the CTA so every warp evaluates 32 pairs of one
+// order with the rule nodes in registers (no divergence, fully unrolled for k <= 6).
+constexpr int T1 = 32;       // DoFs per tile side
+constexpr int T1C = 40;      // max cells behind one DoF tile on the fused path
+constexpr int T1K = 33;      // order buckets (KDIR)
+
+// one warp per DoF tile: sorted unique cells of the patches of its DoFs; per DoF the
+// (slot << 1 | basis) of each patch cell (-1 = none); the owning tile of every cell
+__global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_vertex, int n, int nt,
+                                    int* __restrict__ tcnt, int* __restrict__ tcell, int* __restrict__ dslot,
+                                    int* __restrict__ owner, int* __restrict__ maxcnt) {
+  __shared__ int cand[4][2 * T1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 4 + w;
+  if (t >= nt) return;
+  const int i = t * T1 + lane;
+  int c0 = INT_MAX, c1 = INT_MAX, vi = -1, np = 0;
+  if (i < n) {
+    vi = dof_vertex[i];
+    const int b = m.patch_off[vi];
+    np = m.patch_off[vi + 1] - b;
+    if (np > 0) c0 = m.patch_cells[b];
+    if (np > 1) c1 = m.patch_cells[b + 1];
+  }
+  if (__any_sync(0xffffffffu, np > 2)) {        // not an interval mesh patch: no fused path
+    if (lane == 0) atomicMax(maxcnt, 1 << 20);
+    return;
+  }
+  cand[w][lane] = c0;
+  cand[w][32 + lane] = c1;
+  __syncwarp();
+  // first occurrence flags, then unique rank = number of distinct values below
+  int first[2], rk[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int v = h ? c1 : c0, me = h * 32 + lane;
+    int f = 1;
+    for (int q = 0; q < me; ++q) f &= (cand[w][q] != v);
+    first[h] = f;
+  }
+  const unsigned f0 = __ballot_sync(0xffffffffu, first[0]), f1 = __ballot_sync(0xffffffffu, first[1]);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int v = h ? c1 : c0;
+    int r = 0;
+    for (int q = 0; q < 2 * T1; ++q) {
+      const bool fq = q < 32 ? ((f0 >> q) & 1u) : ((f1 >> (q - 32)) & 1u);
+      r += (fq && cand[w][q] < v);
+    }
+    rk[h] = r;
+  }
+  const int ncand_unique = __reduce_add_sync(0xffffffffu, (c0 != INT_MAX && first[0]) + (c1 != INT_MAX && first[1]));
+  if (lane == 0) {
+    tcnt[t] = ncand_unique;
+    atomicMax(maxcnt, ncand_unique);
+  }
+  if (ncand_unique > T1C) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = h ? c1 : c0;
+    if (c != INT_MAX && first[h]) {
+      tcell[(size_t)t * T1C + rk[h]] = c;
+      atomicMin(&owner[c], t);
+    }
+  }
+  if (i < n) {
+    dslot[2 * i] = c0 != INT_MAX ? (rk[0] << 1 | (m.cells[2 * c0] == vi ? 0 : 1)) : -1;
+    dslot[2 * i + 1] = c1 != INT_MAX ? (rk[1] << 1 | (m.cells[2 * c1] == vi ? 0 : 1)) : -1;
+  }
+}
+
+template <int KK, int E4>
+__device__ __forceinline__ double4 block1d_k(const double* __restrict__ nd, double kx0, double ke, double lx0,
+                                             double le, double JJ, double ex) {
+  double tq[KK], w0[KK], w1[KK], Y[KK];
+#pragma unroll
+  for (int r = 0; r < KK; ++r) {
+    tq[r] = nd[r * NODE];
+    w0[r] = nd[r * NODE + 3];
+    w1[r] = nd[r * NODE + 4];
+    Y[r] = lx0 + tq[r] * le;
+  }
+  double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
+#pragma unroll
+  for (int x = 0; x < KK; ++x) {
+    const double X = kx0 + tq[x] * ke;
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int y = 0; y < KK; ++y) {
+      const double d = X - Y[y];
+      const double v = kpow<E4>(d * d, ex);
+      t0 = fma(v, w0[y], t0);
+      t1 = fma(v, w1[y], t1);
+    }
+    m00 = fma(w0[x], t0, m00);
+    m01 = fma(w0[x], t1, m01);
+    m10 = fma(w1[x], t0, m10);
+    m11 = fma(w1[x], t1, m11);
+  }
+  return make_double4(m00 * JJ, m01 * JJ, m10 * JJ, m11 * JJ);
+}
+
+struct Cell1S {   // shared-memory copy of a tile's cells
+  double x0[T1C], x1[T1C], lo[T1C], hi[T1C], h[T1C], lh[T1C];
+  float lnhf[T1C], lhf[T1C];
+  int id[T1C], v0[T1C], v1[T1C], own[T1C];
+};
+
+// fp32 order estimate of the disjoint pair (P, Q) = (min, max) of two tile cells (reference
+// orientation); 0 = ambiguous (resolved by order_exact1d outside the hot loop)
+__device__ __forceinline__ int order_est1d(const OrderConsts& oc, const Cell1S& P, int ip, const Cell1S& Q, int iq,
+                                           double& dist) {
+  const double d1 = __dsub_rn(Q.lo[iq], P.hi[ip]), d2 = __dsub_rn(P.lo[ip], Q.hi[iq]);
+  dist = fmax(fmax(d1, d2), 0.0);
+  if (!(dist > 1e-30)) return 0;
+  return order_from_estimate(order_estimate_f(oc, oc.coff_f, P.lnhf[ip], P.lhf[ip], Q.lnhf[iq], Q.lhf[iq],
+                                              __logf((float)dist)), oc.cap_disjoint);
+}
+
+struct PairGeo1D {
+  double px0, pe, qx0, qe, JJ;
+  bool kl;
+};
+__device__ __forceinline__ PairGeo1D pair_geo1d(const Cell1S& cr, int a, const Cell1S& cc, int b) {
+  PairGeo1D g;
+  g.kl = cr.id[a] < cc.id[b];
+  const Cell1S& P = g.kl ? cr : cc;
+  const Cell1S& Q = g.kl ? cc : cr;
+  const int ip = g.kl ? a : b, iq = g.kl ? b : a;
+  g.px0 = P.x0[ip];
+  g.pe = P.x1[ip] - g.px0;
+  g.qx0 = Q.x0[iq];
+  g.qe = Q.x1[iq] - g.qx0;
+  g.JJ = P.h[ip] * Q.h[iq];
+  return g;
+}
+// stored row cell first: Mp[aK * 2 + bL]
+__device__ __forceinline__ void store_block1d(double* __restrict__ Mp, const double4& g, bool kl) {
+  Mp[0] = g.x;
+  Mp[1] = kl ? g.y : g.z;
+  Mp[2] = kl ? g.z : g.y;
+  Mp[3] = g.w;
+}
+
+template <int E4>
+__device__ __forceinline__ double4 block1d_small(const double* __restrict__ tab, const DevTables& dir, double ex,
+                                                 const PairGeo1D& q, int k) {
+  const RuleRef rr = dir.rule(T_DISJ, k);
+  const double* nd = tab + (size_t)rr.off * NODE;
+  switch (k) {
+    case 2: return block1d_k<2, E4>(nd, q.px0, q.pe, q.qx0, q.qe, q.JJ, ex);
+    case 3: return block1d_k<3, E4>(nd, q.px0, q.pe, q.qx0, q.qe, q.JJ, ex);
+    case 4: return block1d_k<4, E4>(nd, q.px0, q.pe, q.qx0, q.qe, q.JJ, ex);
+    case 5: return block1d_k<5, E4>(nd, q.px0, q.pe, q.qx0, q.qe, q.JJ, ex);
+    default: return block1d<E4>(tab, rr, q.px0, q.pe, q.qx0, q.qe, q.JJ, ex);
+  }
+}
+
+// One pair, one warp (large k, up to 32^2 evaluations): lane x owns the x-node row of block1d,
+// then every lane folds the rows in x order — the same operations in the same order as
+// block1d, so the result is bitwise identical to the thread-per-pair path.
+template <int E4>
+__device__ __forceinline__ double4 block1d_warp(const double* __restrict__ tab, RuleRef rr, double kx0, double ke,
+                                                double lx0, double le, double JJ, double ex, int lane) {
+  double t0 = 0.0, t1 = 0.0;
+  if (lane < rr.cnt) {
+    const double* nx = tab + (size_t)(rr.off + lane) * NODE;
+    const double X = kx0 + nx[0] * ke;
+    for (int y = 0; y < rr.cnt; ++y) {
+      const double* ny = tab + (size_t)(rr.off + y) * NODE;
+      const double d = X - (lx0 + ny[0] * le);
+      const double v = kpow<E4>(d * d, ex);
+      t0 = fma(v, ny[3], t0);
+      t1 = fma(v, ny[4], t1);
+    }
+  }
+  double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
+  for (int x = 0; x < rr.cnt; ++x) {
+    const double* nx = tab + (size_t)(rr.off + x) * NODE;
+    const double a0 = __shfl_sync(0xffffffffu, t0, x), a1 = __shfl_sync(0xffffffffu, t1, x);
+    m00 = fma(nx[3], a0, m00);
+    m01 = fma(nx[3], a1, m01);
+    m10 = fma(nx[4], a0, m10);
+    m11 = fma(nx[4], a1, m11);
+  }
+  return make_double4(m00 * JJ, m01 * JJ, m10 * JJ, m11 * JJ);
+}
+
+constexpr int T1WARP = 6;    // orders >= this get a warp per pair
+
+template <int E4>
+__global__ void __launch_bounds__(256, 3) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
+                                                           OrderConsts oc, double ex, Src1D S, int nt,
+                                                           const int* __restrict__ tcnt, const int* __restrict__ tcell,
+                                                           const int* __restrict__ dslot, const int* __restrict__ owner,
+                                                           int mc, int n, double negC, double* __restrict__ A,
+                                                           int64_t lda, unsigned long long* __restrict__ evals) {
+  extern __shared__ __align__(16) unsigned char smem1d[];
+  __shared__ Cell1S cr, cc;
+  __shared__ int bcnt[T1K], boff[T1K + 1], ndefer;
+  __shared__ int rA[T1][2], rB[T1][2], cA[T1][2], cB[T1][2];
+  __shared__ double tt[T1][T1 + 1];
+  // diagonal-major tile order (near-diagonal tiles hold the high orders: heavy first)
+  const int64_t bx = blockIdx.x;
+  const double q2 = 2.0 * nt + 1.0;
+  int dg = (int)((q2 - sqrt(q2 * q2 - 8.0 * (double)bx)) * 0.5);
+  auto cum = [&](int64_t e) { return e * nt - e * (e - 1) / 2; };
+  while (dg > 0 && cum(dg) > bx) --dg;
+  while (cum(dg + 1) <= bx) ++dg;
+  const int bi = (int)(bx - cum(dg)), bj = bi + dg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nr = tcnt[bi], ncl = tcnt[bj];
+  const int np = nr * ncl;
+  const unsigned inv = ((1u << 20) + ncl - 1) / ncl;                 // p / ncl for p < 1600
+  double* M = reinterpret_cast<double*>(smem1d);                      // [np][2][2]
+  int* defer = reinterpret_cast<int*>(smem1d + sizeof(double) * 4 * (size_t)mc * mc);
+  int* sorted = defer + mc * mc;
+
+  for (int q = tid; q < 2 * T1C; q += blockDim.x) {
+    Cell1S& C = q < T1C ? cr : cc;
+    const int a = q < T1C ? q : q - T1C;
+    const int cnt = q < T1C ? nr : ncl;
+    if (a < cnt) {
+      const int c = tcell[(size_t)(q < T1C ? bi : bj) * T1C + a];
+      C.id[a] = c; C.x0[a] = S.x0[c]; C.x1[a] = S.x1[c]; C.lo[a] = S.lo[c]; C.hi[a] = S.hi[c];
+      C.h[a] = S.h[c]; C.lh[a] = S.lh[c]; C.v0[a] = S.v0[c]; C.v1[a] = S.v1[c];
+      C.lnhf[a] = S.lnhf[c]; C.lhf[a] = S.lhf[c]; C.own[a] = owner[c];
+    }
+  }
+  if (tid < T1K) bcnt[tid] = 0;
+  if (tid == 0) ndefer = 0;
+  if (tid < 2 * T1) {
+    // per DoF and patch cell: offsets into M as the outer (row) and inner (column) factor
+    const int h = tid >> 5, a = tid & 31;
+    const int i = bi * T1 + a, j = bj * T1 + a;
+    const int si = i < n ? dslot[2 * i + h] : -1, sj = j < n ? dslot[2 * j + h] : -1;
+    rA[a][h] = si < 0 ? -1 : 4 * (si >> 1) * ncl + 2 * (si & 1);
+    rB[a][h] = si < 0 ? -1 : 4 * (si >> 1) + (si & 1);
+    cA[a][h] = sj < 0 ? -1 : 4 * (sj >> 1) * ncl + 2 * (sj & 1);
+    cB[a][h] = sj < 0 ? -1 : 4 * (sj >> 1) + (sj & 1);
+  }
+  __syncthreads();
+
+  // phase 1: every cell pair's order; k = 2 pairs (~95%) get their block right away
+  unsigned my = 0;
+  for (int p = tid; p < np; p += blockDim.x) {
+    const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
+    const int K = cr.id[a], L = cc.id[b];
+    const int kv0 = cr.v0[a], kv1 = cr.v1[a], lv0 = cc.v0[b], lv1 = cc.v1[b];
+    double* Mp = M + 4 * p;
+    if (K == L || lv0 == kv0 || lv0 == kv1 || lv1 == kv0 || lv1 == kv1) {
+      Mp[0] = 0.0; Mp[1] = 0.0; Mp[2] = 0.0; Mp[3] = 0.0;
+      continue;
+    }
+    double dist;
+    const int k = K < L ? order_est1d(oc, cr, a, cc, b, dist) : order_est1d(oc, cc, b, cr, a, dist);
+    // algorithmic count: each unordered pair once, in the tile of its cells' owners
+    const int oK = cr.own[a], oL = cc.own[b];
+    const bool owned = K < L && min(oK, oL) == bi && max(oK, oL) == bj;
+    if (k == 2) {
+      const PairGeo1D g = pair_geo1d(cr, a, cc, b);
+      store_block1d(Mp, block1d_k<2, E4>(tab + (size_t)dir.rule(T_DISJ, 2).off * NODE, g.px0, g.pe, g.qx0, g.qe,
+                                         g.JJ, ex), g.kl);
+      my += owned ? 4u : 0u;
+    } else {
+      if (k) {
+        atomicAdd(&bcnt[k], 1);
+        my += owned ? (unsigned)(k * k) : 0u;
+      }
+      defer[atomicAdd(&ndefer, 1)] = p | (k << 16);
+    }
+  }
+  __syncthreads();
+  const int nd = ndefer;
+  if (nd > 0) {
+    // ambiguous estimates: the exact fp64 order
+    for (int it = tid; it < nd; it += blockDim.x) {
+      const int e = defer[it];
+      if (e >> 16) continue;
+      const int p = e & 0xffff;
+      const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
+      const bool kl = cr.id[a] < cc.id[b];
+      const Cell1S& P = kl ? cr : cc;
+      const Cell1S& Q = kl ? cc : cr;
+      const int ip = kl ? a : b, iq = kl ? b : a;
+      const double dist = fmax(fmax(__dsub_rn(Q.lo[iq], P.hi[ip]), __dsub_rn(P.lo[ip], Q.hi[iq])), 0.0);
+      const int k = order_exact1d(oc, oc.coff, P.h[ip], P.lh[ip], Q.h[iq], Q.lh[iq], dist);
+      defer[it] = p | (k << 16);
+      atomicAdd(&bcnt[k], 1);
+      const int oK = cr.own[a], oL = cc.own[b];
+      if (kl && min(oK, oL) == bi && max(oK, oL) == bj) my += (unsigned)(k * k);
+    }
+    __syncthreads();
+    // sort by order: ascending k, so [0, nsmall) are thread-per-pair and the rest warp-per-pair
+    if (tid < 32) {
+      const int c = bcnt[tid];
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      boff[tid] = x - c;
+      if (tid == 31) boff[32] = x;
+    }
+    __syncthreads();
+    const int nsmall = boff[T1WARP];
+    __syncthreads();
+    for (int it = tid; it < nd; it += blockDim.x) {
+      const int e = defer[it];
+      sorted[atomicAdd(&boff[e >> 16], 1)] = e;
+    }
+    __syncthreads();
+    for (int it = nsmall + warp; it < nd; it += blockDim.x >> 5) {
+      const int e = sorted[it];
+      const int p = e & 0xffff, k = e >> 16;
+      const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
+      const PairGeo1D g = pair_geo1d(cr, a, cc, b);
+      const double4 v = block1d_warp<E4>(tab, dir.rule(T_DISJ, k), g.px0, g.pe, g.qx0, g.qe, g.JJ, ex, lane);
+      if (lane == 0) store_block1d(M + 4 * p, v, g.kl);
+    }
+    for (int it = tid; it < nsmall; it += blockDim.x) {
+      const int e = sorted[it];
+      const int p = e & 0xffff, k = e >> 16;
+      const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
+      const PairGeo1D g = pair_geo1d(cr, a, cc, b);
+      store_block1d(M + 4 * p, block1d_small<E4>(tab, dir, ex, g, k), g.kl);
+    }
+  }
+  __syncthreads();
+
+  // phase 3: A[i][j] = -C sum_{K in P(i)} sum_{L in P(j)} M  (gather1d's canonical order: the
+  // cells of min(i, j) outer; touching / identical pairs hold zeros, which add nothing)
+  const int tx = lane;
+  constexpr int RPT = T1 / 8;
+  double v[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int rr_ = warp + 8 * q;
+    const int i = bi * T1 + rr_, j = bj * T1 + tx;
+    const bool sw = i > j;                     // only in diagonal tiles (one cell list)
+    const int* po = sw ? cA[tx] : rA[rr_];
+    const int* pi = sw ? rB[rr_] : cB[tx];
+    const int o0 = po[0], o1 = po[1], i0 = pi[0], i1 = pi[1];
+    double x = 0.0;
+    if (o0 >= 0 && i0 >= 0) x += negC * M[o0 + i0];
+    if (o0 >= 0 && i1 >= 0) x += negC * M[o0 + i1];
+    if (o1 >= 0 && i0 >= 0) x += negC * M[o1 + i0];
+    if (o1 >= 0 && i1 >= 0) x += negC * M[o1 + i1];
+    v[q] = x;
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int rr_ = warp + 8 * q;
+    const int i = bi * T1 + rr_, j = bj * T1 + tx;
+    tt[rr_][tx] = v[q];
+    if (i < n && j < n) A[(int64_t)i * lda + j] = v[q];
+  }
+  if (evals) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+    if (lane == 0 && my) atomicAdd(evals, (unsigned long long)my);
+  }
+  if (bi == bj) return;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int rr_ = warp + 8 * q;
+    const int j = bj * T1 + rr_, i = bi * T1 + tx;       // A[j][i] = tt[i][j]
+    if (i < n && j < n) A[(int64_t)j * lda + i] = tt[tx][rr_];
+  }
+}
+
 // value of the cross part at (p, q), p <= q, in the canonical order (cells of p outer)
 __device__ __forceinline__ double gather1d(const DevMesh& m, const Src1D& S, const double4* __restrict__ G,
                                            const int* __restrict__ dof_vertex, int p, int q, double negC) {
@@ -273,15 +673,16 @@ __global__ void tpos_kernel(const int* targets, int nt, int* tpos) {
 struct Src1DBuf {
   DBuf<double> x0, x1, lo, hi, h, lh;
   DBuf<int> v0, v1;
-  Src1D view() const { return Src1D{x0.p, x1.p, lo.p, hi.p, h.p, lh.p, v0.p, v1.p}; }
+  DBuf<float> lnhf, lhf;
+  Src1D view() const { return Src1D{x0.p, x1.p, lo.p, hi.p, h.p, lh.p, v0.p, v1.p, lnhf.p, lhf.p}; }
 };
 
 static void build_src1d(const DevMesh& m, Src1DBuf& B, cudaStream_t st) {
   const int nc = m.nc;
   B.x0.alloc(nc); B.x1.alloc(nc); B.lo.alloc(nc); B.hi.alloc(nc); B.h.alloc(nc); B.lh.alloc(nc);
-  B.v0.alloc(nc); B.v1.alloc(nc);
+  B.v0.alloc(nc); B.v1.alloc(nc); B.lnhf.alloc(nc); B.lhf.alloc(nc);
   build_src1d_kernel<<<(nc + 255) / 256, 256, 0, st>>>(m, B.x0.p, B.x1.p, B.lo.p, B.hi.p, B.h.p, B.lh.p, B.v0.p,
-                                                        B.v1.p), ::fl::note_launch();
+                                                        B.v1.p, B.lnhf.p, B.lhf.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -311,6 +712,35 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
   build_src1d(m, B, st);
   const Src1D S = B.view();
   const double negC = -Cds;   // (C/2) * (-2) (assembly.py:723, :1100)
+  const char* path = getenv("FRACLAP_CROSS1D");
+  const bool force_pairs = path && std::string(path) == "pairs";
+  if (symmetric && !force_pairs && m.n > 0) {
+    // fused DoF tiles when every tile's cells fit the shared-memory pair table
+    const int nt = (m.n + T1 - 1) / T1;
+    DBuf<int> tcnt(nt), tcell((size_t)nt * T1C), dslot((size_t)2 * m.n), owner(m.nc), mx(1);
+    FL_CUDA(cudaMemsetAsync(owner.p, 0x7f, sizeof(int) * m.nc, st));
+    FL_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), st));
+    tile1d_cells_kernel<<<(nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, m.n, nt, tcnt.p, tcell.p, dslot.p, owner.p, mx.p),
+        ::fl::note_launch();
+    FL_CHECK_LAUNCH();
+    int mc = 0;
+    FL_CUDA(cudaMemcpyAsync(&mc, mx.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    if (mc <= T1C) {
+      mc = std::max(mc, 1);
+      const size_t smem = (sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc;
+      const int64_t ntp = (int64_t)nt * (nt + 1) / 2;
+      FL_E4_SWITCH1(e4, {
+        auto kern = cross1d_tile_kernel<E4>;
+        FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)ntp, 256, smem, st>>>(m, t.data, t, oc, ex, S, nt, tcnt.p, tcell.p, dslot.p, owner.p, mc,
+                                               m.n, negC, A, lda, evals);
+        ::fl::note_launch();
+      });
+      FL_CHECK_LAUNCH();
+      return;
+    }
+  }
   if (symmetric) {
     DBuf<double4> G((size_t)std::max<int64_t>((int64_t)m.nc * (m.nc - 1) / 2, 1));
     FL_E4_SWITCH1(e4, (cross1d_pairs_kernel<E4><<<m.nc, 256, 0, st>>>(m, t.data, t, oc, ex, S, G.p, evals),
@@ -333,7 +763,6 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
         ::fl::note_launch();
     FL_CHECK_LAUNCH();
   }
-  FL_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace fl
