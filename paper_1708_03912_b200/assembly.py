@@ -70,7 +70,13 @@ def _device_index(device):
 
 def _tables(mesh, dofmap, s, params):
     from .quadrature import needed_orders
-    kt, kb = needed_orders(mesh, dofmap, float(s), params)
+    # the needed-order sets depend on the cell diameters, n, s and params only; cached on the
+    # mesh like its patches / diameters (meshes are not mutated after construction)
+    cache = mesh.__dict__.setdefault("_fl_orders", {})
+    key = (int(dofmap.n), float(s), None if params is None else tuple(vars(params).items()))
+    if key not in cache:
+        cache[key] = needed_orders(mesh, dofmap, float(s), params)
+    kt, kb = cache[key]
     dir_, data = pack_tables(mesh.vertices.shape[1], float(s), kt, kb)
     return dir_, data, _lib.fl_tables(dir_.ctypes.data, data.ctypes.data, len(data))
 

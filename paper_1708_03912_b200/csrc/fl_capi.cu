@@ -6,6 +6,7 @@
 #include <memory>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -241,7 +242,21 @@ struct Timer {
   ~Timer() {
     for (auto& x : e) cudaEventDestroy(x);
   }
-  void mark() { cudaEventRecord(e[k++], st); }
+  // FRACLAP_TRACE=1: host-side timestamps of every mark (to find host gaps between launches)
+  std::chrono::steady_clock::time_point h0 = std::chrono::steady_clock::now(), hm[16];
+  bool trace = getenv("FRACLAP_TRACE") != nullptr;
+  void mark() {
+    if (trace) hm[k] = std::chrono::steady_clock::now();
+    cudaEventRecord(e[k++], st);
+  }
+  void report() {
+    if (!trace) return;
+    fprintf(stderr, "[fl trace] host us at marks:");
+    for (int i = 0; i < k; ++i)
+      fprintf(stderr, " %.1f", std::chrono::duration<double, std::micro>(hm[i] - h0).count());
+    fprintf(stderr, " | end %.1f\n",
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
+  }
   double ms(int a, int b) {
     float f = 0;
     cudaEventElapsedTime(&f, e[a], e[b]);
@@ -257,6 +272,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
                           const fl_order_params* params, const fl_tables* tables, int64_t n_limit,
                           int64_t row_begin, int64_t row_end, int32_t device, void* stream, fl_dense** out) {
   FL_API_BEGIN
+  const auto t_enter = std::chrono::steady_clock::now();
   if (!out) return fail(FL_E_ARG, "null output handle");
   *out = nullptr;
   check_inputs(mesh, dofmap, kernel, params, tables);
@@ -286,6 +302,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   const int64_t rows = row_end - row_begin;
 
   Timer tm(st);
+  tm.h0 = t_enter;
   tm.mark();  // 0
   Uploaded U;
   upload(mesh, dofmap, tables, U, st);
@@ -419,6 +436,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   S.ms_cross = tm.ms(5, 6);
   S.ms_local = tm.ms(6, 7);
   S.ms_total = tm.ms(0, 7);
+  tm.report();
   S.cross_tile_pairs = ntp;
   S.near_pairs = near.n;
   if (ntiles > 0) {

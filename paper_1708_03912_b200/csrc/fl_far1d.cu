@@ -24,13 +24,22 @@
 
 namespace fl {
 
+// one 32-byte record per cell for the tail's source stream (two 16-byte loads per source);
+// lo/hi/h are recomputed exactly: min/max of the end points and |x1 - x0| (fl_prep.cu diam)
+struct __align__(16) Rec1D {
+  double x0, x1;
+  int v0, v1;
+  float lnhf, lhf;
+};
+
 struct Src1D {
+  const Rec1D* rec;
   const double *x0, *x1, *lo, *hi, *h, *lh;
   const int *v0, *v1;
   const float *lnhf, *lhf;      // __logf((float)h), (float)|ln h| for the fp32 order estimate
 };
 
-__global__ void build_src1d_kernel(DevMesh m, double* x0, double* x1, double* lo, double* hi, double* h,
+__global__ void build_src1d_kernel(DevMesh m, Rec1D* rec, double* x0, double* x1, double* lo, double* hi, double* h,
                                    double* lh, int* v0, int* v1, float* lnhf, float* lhf) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= m.nc) return;
@@ -45,6 +54,14 @@ __global__ void build_src1d_kernel(DevMesh m, double* x0, double* x1, double* lo
   v1[c] = g.v[1];
   lnhf[c] = __logf((float)g.diam);
   lhf[c] = (float)g.ldiam;
+  Rec1D r;
+  r.x0 = g.p[0][0];
+  r.x1 = g.p[1][0];
+  r.v0 = g.v[0];
+  r.v1 = g.v[1];
+  r.lnhf = lnhf[c];
+  r.lhf = lhf[c];
+  rec[c] = r;
 }
 
 // the exact fp64 order (rare: the fp32 estimate is within ORDER_DELTA of an integer), kept out
@@ -56,14 +73,35 @@ static __device__ __noinline__ int order_exact1d(const OrderConsts& oc, double c
 
 // ------------------------------------------------------------------ tail
 template <int E4>
+__device__ __forceinline__ void tail1d_source(const double* __restrict__ tab, const DevTables& dir, double ex,
+                                              const double (&xq)[6], double (&acc)[6], double x0, double e, double J,
+                                              int k) {
+  const RuleRef rr = dir.rule(T_DISJ, k);
+  for (int r = 0; r < k; ++r) {
+    const double* nd = tab + (size_t)(rr.off + r) * NODE;
+    const double y = x0 + nd[0] * e;
+    const double jw = J * nd[2];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const double d = xq[q] - y;
+      acc[q] = fma(jw, kpow<E4>(d * d, ex), acc[q]);
+    }
+  }
+}
+
+// Warp per target cell, lane per source cell.  Sources of order 2 (~80%) are evaluated inline
+// with the two rule nodes in registers; the others are compacted (ballot, deterministic order)
+// into a per-warp queue and evaluated 32 at a time, so a warp's lanes share one code path.
+template <int E4>
 __global__ void __launch_bounds__(128, 4) tail1d_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                      OrderConsts oc, double ex, Src1D S,
                                                      const int* __restrict__ targets, int ntargets,
                                                      double* __restrict__ psi,
                                                      unsigned long long* __restrict__ evals) {
   constexpr int Q = 6;
-  const int lane = threadIdx.x & 31;
-  const int ti = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  __shared__ int qs[4][64], qk[4][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int ti = blockIdx.x * (blockDim.x >> 5) + w;
   if (ti >= ntargets) return;
   const int K = targets[ti];
   const double alo = S.lo[K], ahi = S.hi[K], ah = S.h[K], alh = S.lh[K];
@@ -75,31 +113,84 @@ __global__ void __launch_bounds__(128, 4) tail1d_kernel(DevMesh m, const double*
     xq[q] = m.X[(size_t)K * Q + q];
     acc[q] = 0.0;
   }
-  unsigned long long nodes = 0;
-  for (int s = lane; s < m.nc; s += 32) {
-    const int bv0 = S.v0[s], bv1 = S.v1[s];
-    if (s == K || bv0 == av0 || bv0 == av1 || bv1 == av0 || bv1 == av1) continue;   // N(K) (:999-1009)
-    const double blo = S.lo[s], bhi = S.hi[s];
-    const double dist = fmax(fmax(__dsub_rn(blo, ahi), __dsub_rn(alo, bhi)), 0.0);   // (:750-752)
-    const double J = S.h[s];
-    int k = 0;
-    if (dist > 1e-30)
-      k = order_from_estimate(order_estimate_f(oc, oc.coff_tail_f, alnf, alhf, S.lnhf[s], S.lhf[s],
-                                               __logf((float)dist)), oc.cap_disjoint);
-    if (!k) k = order_exact1d(oc, oc.coff_tail, ah, alh, J, S.lh[s], dist);
-    const RuleRef rr = dir.rule(T_DISJ, k);
-    const double x0 = S.x0[s], e = S.x1[s] - x0;
-    nodes += (unsigned long long)k;
-    for (int r = 0; r < k; ++r) {
-      const double* nd = tab + (size_t)(rr.off + r) * NODE;
-      const double y = x0 + nd[0] * e;
-      const double jw = J * nd[2];
+  const double* n2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
+  const double t0 = n2[0], w0 = n2[2], t1 = n2[NODE], w1 = n2[NODE + 2];
+  unsigned nodes = 0;
+  int qn = 0;                                   // warp-uniform queue length
+  const unsigned lt = (1u << lane) - 1u;
+  const int4* R = reinterpret_cast<const int4*>(S.rec);
+  int4 na = make_int4(0, 0, 0, 0), nb = na;     // prefetched record of the next source
+  if (lane < m.nc) { na = __ldg(R + 2 * lane); nb = __ldg(R + 2 * lane + 1); }
+  for (int s0 = 0; s0 < m.nc; s0 += 32) {
+    const int s = s0 + lane;
+    const int4 ra = na, rb = nb;
+    if (s + 32 < m.nc) { na = __ldg(R + 2 * (s + 32)); nb = __ldg(R + 2 * (s + 32) + 1); }
+    const double sx0 = __hiloint2double(ra.y, ra.x), sx1 = __hiloint2double(ra.w, ra.z);
+    const int bv0 = rb.x, bv1 = rb.y;
+    int k = -1;                                 // -1: not a tail source
+    double x0 = 0.0, e = 0.0, J = 0.0;
+    if (s < m.nc && !(s == K || bv0 == av0 || bv0 == av1 || bv1 == av0 || bv1 == av1)) {   // N(K) (:999-1009)
+      const double blo = fmin(sx0, sx1), bhi = fmax(sx0, sx1);
+      const double dist = fmax(fmax(__dsub_rn(blo, ahi), __dsub_rn(alo, bhi)), 0.0);   // (:750-752)
+      k = 0;
+      if (dist > 1e-30)
+        k = order_from_estimate(order_estimate_f(oc, oc.coff_tail_f, alnf, alhf, __int_as_float(rb.z),
+                                                 __int_as_float(rb.w), __logf((float)dist)), oc.cap_disjoint);
+      x0 = sx0;
+      e = sx1 - sx0;
+      J = fabs(e);
+    }
+    if (k == 2) {
+      const double y0 = x0 + t0 * e, y1 = x0 + t1 * e;
+      const double j0 = J * w0, j1 = J * w1;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const double d = xq[q] - y;
-        acc[q] = fma(jw, kpow<E4>(d * d, ex), acc[q]);
+        const double d0 = xq[q] - y0;
+        acc[q] = fma(j0, kpow<E4>(d0 * d0, ex), acc[q]);
+        const double d1 = xq[q] - y1;
+        acc[q] = fma(j1, kpow<E4>(d1 * d1, ex), acc[q]);
       }
+      nodes += 2;
     }
+    const bool dq = k == 0 || k > 2;
+    const unsigned bm = __ballot_sync(0xffffffffu, dq);
+    if (dq) {
+      const int pos = qn + __popc(bm & lt);
+      qs[w][pos] = s;
+      qk[w][pos] = k;
+    }
+    qn += __popc(bm);
+    if (qn >= 32) {
+      __syncwarp();
+      const int ss = qs[w][lane];
+      int kk = qk[w][lane];
+      const double sx0 = S.x0[ss], sJ = S.h[ss];
+      if (!kk) {
+        const double dist = fmax(fmax(__dsub_rn(S.lo[ss], ahi), __dsub_rn(alo, S.hi[ss])), 0.0);
+        kk = order_exact1d(oc, oc.coff_tail, ah, alh, sJ, S.lh[ss], dist);
+      }
+      tail1d_source<E4>(tab, dir, ex, xq, acc, sx0, S.x1[ss] - sx0, sJ, kk);
+      nodes += kk;
+      __syncwarp();
+      if (lane < qn - 32) {
+        qs[w][lane] = qs[w][32 + lane];
+        qk[w][lane] = qk[w][32 + lane];
+      }
+      __syncwarp();
+      qn -= 32;
+    }
+  }
+  __syncwarp();
+  if (lane < qn) {
+    const int ss = qs[w][lane];
+    int kk = qk[w][lane];
+    const double sx0 = S.x0[ss], sJ = S.h[ss];
+    if (!kk) {
+      const double dist = fmax(fmax(__dsub_rn(S.lo[ss], ahi), __dsub_rn(alo, S.hi[ss])), 0.0);
+      kk = order_exact1d(oc, oc.coff_tail, ah, alh, sJ, S.lh[ss], dist);
+    }
+    tail1d_source<E4>(tab, dir, ex, xq, acc, sx0, S.x1[ss] - sx0, sJ, kk);
+    nodes += kk;
   }
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -109,7 +200,7 @@ __global__ void __launch_bounds__(128, 4) tail1d_kernel(DevMesh m, const double*
   if (evals) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nodes += __shfl_xor_sync(0xffffffffu, nodes, o);
-    if (lane == 0) atomicAdd(evals, nodes * Q);
+    if (lane == 0) atomicAdd(evals, (unsigned long long)nodes * Q);
   }
 }
 
@@ -674,14 +765,15 @@ struct Src1DBuf {
   DBuf<double> x0, x1, lo, hi, h, lh;
   DBuf<int> v0, v1;
   DBuf<float> lnhf, lhf;
-  Src1D view() const { return Src1D{x0.p, x1.p, lo.p, hi.p, h.p, lh.p, v0.p, v1.p, lnhf.p, lhf.p}; }
+  DBuf<Rec1D> rec;
+  Src1D view() const { return Src1D{rec.p, x0.p, x1.p, lo.p, hi.p, h.p, lh.p, v0.p, v1.p, lnhf.p, lhf.p}; }
 };
 
 static void build_src1d(const DevMesh& m, Src1DBuf& B, cudaStream_t st) {
   const int nc = m.nc;
   B.x0.alloc(nc); B.x1.alloc(nc); B.lo.alloc(nc); B.hi.alloc(nc); B.h.alloc(nc); B.lh.alloc(nc);
-  B.v0.alloc(nc); B.v1.alloc(nc); B.lnhf.alloc(nc); B.lhf.alloc(nc);
-  build_src1d_kernel<<<(nc + 255) / 256, 256, 0, st>>>(m, B.x0.p, B.x1.p, B.lo.p, B.hi.p, B.h.p, B.lh.p, B.v0.p,
+  B.v0.alloc(nc); B.v1.alloc(nc); B.lnhf.alloc(nc); B.lhf.alloc(nc); B.rec.alloc(nc);
+  build_src1d_kernel<<<(nc + 255) / 256, 256, 0, st>>>(m, B.rec.p, B.x0.p, B.x1.p, B.lo.p, B.hi.p, B.h.p, B.lh.p, B.v0.p,
                                                         B.v1.p, B.lnhf.p, B.lhf.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
