@@ -22,6 +22,13 @@
 #include <cstdlib>
 #include <string>
 
+#ifndef FL_TAIL1D_MINB
+#define FL_TAIL1D_MINB 4     // resident 128-thread CTAs per SM the tail is compiled for
+#endif
+#ifndef FL_TILE1D_MINB
+#define FL_TILE1D_MINB 3     // resident 256-thread CTAs per SM of the fused cross tiles
+#endif
+
 namespace fl {
 
 // one 32-byte record per cell for the tail's source stream (two 16-byte loads per source);
@@ -93,7 +100,7 @@ __device__ __forceinline__ void tail1d_source(const double* __restrict__ tab, co
 // with the two rule nodes in registers; the others are compacted (ballot, deterministic order)
 // into a per-warp queue and evaluated 32 at a time, so a warp's lanes share one code path.
 template <int E4>
-__global__ void __launch_bounds__(128, 4) tail1d_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
+__global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                      OrderConsts oc, double ex, Src1D S,
                                                      const int* __restrict__ targets, int ntargets,
                                                      double* __restrict__ psi,
@@ -494,7 +501,7 @@ __device__ __forceinline__ double4 block1d_warp(const double* __restrict__ tab, 
 constexpr int T1WARP = 6;    // orders >= this get a warp per pair
 
 template <int E4>
-__global__ void __launch_bounds__(256, 3) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
+__global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                            OrderConsts oc, double ex, Src1D S, int nt,
                                                            const int* __restrict__ tcnt, const int* __restrict__ tcell,
                                                            const int* __restrict__ dslot, const int* __restrict__ owner,
