@@ -276,20 +276,20 @@ __global__ void __launch_bounds__(256) cross1d_rect_kernel(DevMesh m, const doub
                                                            const int* __restrict__ targets, double4* __restrict__ G,
                                                            unsigned long long* __restrict__ evals) {
   const int K = targets[blockIdx.x];
-  const double alo = S.lo[K], ahi = S.hi[K], ah = S.h[K], alh = S.lh[K], kx0 = S.x0[K];
-  const double ke = S.x1[K] - kx0;
   const int av0 = S.v0[K], av1 = S.v1[K];
   unsigned long long my = 0;
   for (int L = threadIdx.x; L < m.nc; L += blockDim.x) {
     const int bv0 = S.v0[L], bv1 = S.v1[L];
     double4 out = make_double4(0, 0, 0, 0);
     if (L != K && !(bv0 == av0 || bv0 == av1 || bv1 == av0 || bv1 == av1)) {
-      // order in the reference's (min, max) orientation; block with K as the x cell
+      // order and block in the reference's (min, max) orientation, stored with K first
       const int P = min(K, L), Qc = max(K, L);
       const double dist = fmax(fmax(__dsub_rn(S.lo[Qc], S.hi[P]), __dsub_rn(S.lo[P], S.hi[Qc])), 0.0);
       const int k = order_disjoint_fast_s(oc, oc.coff, S.h[P], S.lh[P], S.h[Qc], S.lh[Qc], dist);
-      const double lx0 = S.x0[L];
-      out = block1d<E4>(tab, dir.rule(T_DISJ, k), kx0, ke, lx0, S.x1[L] - lx0, ah * S.h[L], ex);
+      const double px0 = S.x0[P], qx0 = S.x0[Qc];
+      const double4 g = block1d<E4>(tab, dir.rule(T_DISJ, k), px0, S.x1[P] - px0, qx0, S.x1[Qc] - qx0,
+                                    S.h[P] * S.h[Qc], ex);
+      out = K < L ? g : make_double4(g.x, g.z, g.y, g.w);
       my += (unsigned long long)(k * k);
     }
     G[(int64_t)blockIdx.x * m.nc + L] = out;
@@ -318,17 +318,19 @@ constexpr int T1K = 33;      // order buckets (KDIR)
 
 // one warp per DoF tile: sorted unique cells of the patches of its DoFs; per DoF the
 // (slot << 1 | basis) of each patch cell (-1 = none); the owning tile of every cell
-__global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_vertex, int n, int nt,
+// (tiling of the DoF range [off, off + len): tile t = DoFs off + 32 t ...; dslot is indexed
+// relative to off)
+__global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_vertex, int off, int len, int nt,
                                     int* __restrict__ tcnt, int* __restrict__ tcell, int* __restrict__ dslot,
                                     int* __restrict__ owner, int* __restrict__ maxcnt) {
   __shared__ int cand[4][2 * T1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 4 + w;
   if (t >= nt) return;
-  const int i = t * T1 + lane;
+  const int li = t * T1 + lane;
   int c0 = INT_MAX, c1 = INT_MAX, vi = -1, np = 0;
-  if (i < n) {
-    vi = dof_vertex[i];
+  if (li < len) {
+    vi = dof_vertex[off + li];
     const int b = m.patch_off[vi];
     np = m.patch_off[vi + 1] - b;
     if (np > 0) c0 = m.patch_cells[b];
@@ -375,9 +377,9 @@ __global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_verte
       atomicMin(&owner[c], t);
     }
   }
-  if (i < n) {
-    dslot[2 * i] = c0 != INT_MAX ? (rk[0] << 1 | (m.cells[2 * c0] == vi ? 0 : 1)) : -1;
-    dslot[2 * i + 1] = c1 != INT_MAX ? (rk[1] << 1 | (m.cells[2 * c1] == vi ? 0 : 1)) : -1;
+  if (li < len) {
+    dslot[2 * li] = c0 != INT_MAX ? (rk[0] << 1 | (m.cells[2 * c0] == vi ? 0 : 1)) : -1;
+    dslot[2 * li + 1] = c1 != INT_MAX ? (rk[1] << 1 | (m.cells[2 * c1] == vi ? 0 : 1)) : -1;
   }
 }
 
@@ -500,28 +502,45 @@ __device__ __forceinline__ double4 block1d_warp(const double* __restrict__ tab, 
 
 constexpr int T1WARP = 6;    // orders >= this get a warp per pair
 
-template <int E4>
+// one DoF tiling (rows or columns): cells per tile, per-DoF (slot << 1 | basis), cell owners
+struct Tiling1D {
+  const int *cnt, *cell, *dslot, *owner;
+  int off, len, nt;
+};
+
+// RECT = false: the symmetric whole matrix, upper-triangular tile pairs (diagonal-major,
+// heavy first), each off-diagonal tile mirrored.  RECT = true: rows [R.off, R.off + R.len)
+// (one GPU's row block) x all columns, every tile pair computed (owner computes).  Both give
+// bitwise the same entries: the pair blocks are computed in the reference orientation and
+// summed in gather1d's canonical order.
+template <int E4, bool RECT>
 __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
-                                                           OrderConsts oc, double ex, Src1D S, int nt,
-                                                           const int* __restrict__ tcnt, const int* __restrict__ tcell,
-                                                           const int* __restrict__ dslot, const int* __restrict__ owner,
-                                                           int mc, int n, double negC, double* __restrict__ A,
+                                                           OrderConsts oc, double ex, Src1D S, Tiling1D R,
+                                                           Tiling1D Cn, int mc, double negC, double* __restrict__ A,
                                                            int64_t lda, unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem1d[];
   __shared__ Cell1S cr, cc;
   __shared__ int bcnt[T1K], boff[T1K + 1], ndefer;
-  __shared__ int rA[T1][2], rB[T1][2], cA[T1][2], cB[T1][2];
+  __shared__ int rA[T1][2], cB[T1][2];
   __shared__ double tt[T1][T1 + 1];
-  // diagonal-major tile order (near-diagonal tiles hold the high orders: heavy first)
   const int64_t bx = blockIdx.x;
-  const double q2 = 2.0 * nt + 1.0;
-  int dg = (int)((q2 - sqrt(q2 * q2 - 8.0 * (double)bx)) * 0.5);
-  auto cum = [&](int64_t e) { return e * nt - e * (e - 1) / 2; };
-  while (dg > 0 && cum(dg) > bx) --dg;
-  while (cum(dg + 1) <= bx) ++dg;
-  const int bi = (int)(bx - cum(dg)), bj = bi + dg;
+  int bi, bj;
+  if (RECT) {
+    bi = (int)(bx / Cn.nt);
+    bj = (int)(bx - (int64_t)bi * Cn.nt);
+  } else {
+    // diagonal-major tile order (near-diagonal tiles hold the high orders: heavy first)
+    const int nt = R.nt;
+    const double q2 = 2.0 * nt + 1.0;
+    int dg = (int)((q2 - sqrt(q2 * q2 - 8.0 * (double)bx)) * 0.5);
+    auto cum = [&](int64_t e) { return e * nt - e * (e - 1) / 2; };
+    while (dg > 0 && cum(dg) > bx) --dg;
+    while (cum(dg + 1) <= bx) ++dg;
+    bi = (int)(bx - cum(dg));
+    bj = bi + dg;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nr = tcnt[bi], ncl = tcnt[bj];
+  const int nr = R.cnt[bi], ncl = Cn.cnt[bj];
   const int np = nr * ncl;
   const unsigned inv = ((1u << 20) + ncl - 1) / ncl;                 // p / ncl for p < 1600
   double* M = reinterpret_cast<double*>(smem1d);                      // [np][2][2]
@@ -533,22 +552,21 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
     const int a = q < T1C ? q : q - T1C;
     const int cnt = q < T1C ? nr : ncl;
     if (a < cnt) {
-      const int c = tcell[(size_t)(q < T1C ? bi : bj) * T1C + a];
+      const int c = q < T1C ? R.cell[(size_t)bi * T1C + a] : Cn.cell[(size_t)bj * T1C + a];
       C.id[a] = c; C.x0[a] = S.x0[c]; C.x1[a] = S.x1[c]; C.lo[a] = S.lo[c]; C.hi[a] = S.hi[c];
       C.h[a] = S.h[c]; C.lh[a] = S.lh[c]; C.v0[a] = S.v0[c]; C.v1[a] = S.v1[c];
-      C.lnhf[a] = S.lnhf[c]; C.lhf[a] = S.lhf[c]; C.own[a] = owner[c];
+      C.lnhf[a] = S.lnhf[c]; C.lhf[a] = S.lhf[c]; C.own[a] = q < T1C ? R.owner[c] : Cn.owner[c];
     }
   }
   if (tid < T1K) bcnt[tid] = 0;
   if (tid == 0) ndefer = 0;
   if (tid < 2 * T1) {
-    // per DoF and patch cell: offsets into M as the outer (row) and inner (column) factor
+    // per DoF and patch cell: its part of the M offset (row DoFs: slot row + basis a; column
+    // DoFs: slot column + basis b), -1 = no such cell
     const int h = tid >> 5, a = tid & 31;
-    const int i = bi * T1 + a, j = bj * T1 + a;
-    const int si = i < n ? dslot[2 * i + h] : -1, sj = j < n ? dslot[2 * j + h] : -1;
+    const int li = bi * T1 + a, lj = bj * T1 + a;
+    const int si = li < R.len ? R.dslot[2 * li + h] : -1, sj = lj < Cn.len ? Cn.dslot[2 * lj + h] : -1;
     rA[a][h] = si < 0 ? -1 : 4 * (si >> 1) * ncl + 2 * (si & 1);
-    rB[a][h] = si < 0 ? -1 : 4 * (si >> 1) + (si & 1);
-    cA[a][h] = sj < 0 ? -1 : 4 * (sj >> 1) * ncl + 2 * (sj & 1);
     cB[a][h] = sj < 0 ? -1 : 4 * (sj >> 1) + (sj & 1);
   }
   __syncthreads();
@@ -568,7 +586,7 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
     const int k = K < L ? order_est1d(oc, cr, a, cc, b, dist) : order_est1d(oc, cc, b, cr, a, dist);
     // algorithmic count: each unordered pair once, in the tile of its cells' owners
     const int oK = cr.own[a], oL = cc.own[b];
-    const bool owned = K < L && min(oK, oL) == bi && max(oK, oL) == bj;
+    const bool owned = K < L && (RECT ? (oK == bi && oL == bj) : (min(oK, oL) == bi && max(oK, oL) == bj));
     if (k == 2) {
       const PairGeo1D g = pair_geo1d(cr, a, cc, b);
       store_block1d(Mp, block1d_k<2, E4>(tab + (size_t)dir.rule(T_DISJ, 2).off * NODE, g.px0, g.pe, g.qx0, g.qe,
@@ -600,7 +618,7 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
       defer[it] = p | (k << 16);
       atomicAdd(&bcnt[k], 1);
       const int oK = cr.own[a], oL = cc.own[b];
-      if (kl && min(oK, oL) == bi && max(oK, oL) == bj) my += (unsigned)(k * k);
+      if (kl && (RECT ? (oK == bi && oL == bj) : (min(oK, oL) == bi && max(oK, oL) == bj))) my += (unsigned)(k * k);
     }
     __syncthreads();
     // sort by order: ascending k, so [0, nsmall) are thread-per-pair and the rest warp-per-pair
@@ -641,45 +659,49 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
   }
   __syncthreads();
 
-  // phase 3: A[i][j] = -C sum_{K in P(i)} sum_{L in P(j)} M  (gather1d's canonical order: the
-  // cells of min(i, j) outer; touching / identical pairs hold zeros, which add nothing)
+  // phase 3: A[i][j] = -C sum_{K in P(p)} sum_{L in P(q)} M, p = min(i, j), q = max(i, j)
+  // (gather1d's canonical order; touching / identical pairs hold zeros, which add nothing)
   const int tx = lane;
   constexpr int RPT = T1 / 8;
   double v[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int rr_ = warp + 8 * q;
-    const int i = bi * T1 + rr_, j = bj * T1 + tx;
-    const bool sw = i > j;                     // only in diagonal tiles (one cell list)
-    const int* po = sw ? cA[tx] : rA[rr_];
-    const int* pi = sw ? rB[rr_] : cB[tx];
-    const int o0 = po[0], o1 = po[1], i0 = pi[0], i1 = pi[1];
+    const int i = R.off + bi * T1 + rr_, j = Cn.off + bj * T1 + tx;
+    const int o0 = rA[rr_][0], o1 = rA[rr_][1], i0 = cB[tx][0], i1 = cB[tx][1];
     double x = 0.0;
-    if (o0 >= 0 && i0 >= 0) x += negC * M[o0 + i0];
-    if (o0 >= 0 && i1 >= 0) x += negC * M[o0 + i1];
-    if (o1 >= 0 && i0 >= 0) x += negC * M[o1 + i0];
-    if (o1 >= 0 && i1 >= 0) x += negC * M[o1 + i1];
+    if (i <= j) {                                // cells of i outer
+      if (o0 >= 0 && i0 >= 0) x += negC * M[o0 + i0];
+      if (o0 >= 0 && i1 >= 0) x += negC * M[o0 + i1];
+      if (o1 >= 0 && i0 >= 0) x += negC * M[o1 + i0];
+      if (o1 >= 0 && i1 >= 0) x += negC * M[o1 + i1];
+    } else {                                     // cells of j outer
+      if (o0 >= 0 && i0 >= 0) x += negC * M[o0 + i0];
+      if (o1 >= 0 && i0 >= 0) x += negC * M[o1 + i0];
+      if (o0 >= 0 && i1 >= 0) x += negC * M[o0 + i1];
+      if (o1 >= 0 && i1 >= 0) x += negC * M[o1 + i1];
+    }
     v[q] = x;
   }
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int rr_ = warp + 8 * q;
-    const int i = bi * T1 + rr_, j = bj * T1 + tx;
-    tt[rr_][tx] = v[q];
-    if (i < n && j < n) A[(int64_t)i * lda + j] = v[q];
+    const int li = bi * T1 + rr_, lj = bj * T1 + tx;
+    if (!RECT) tt[rr_][tx] = v[q];
+    if (li < R.len && lj < Cn.len) A[(int64_t)(RECT ? li : R.off + li) * lda + Cn.off + lj] = v[q];
   }
   if (evals) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
     if (lane == 0 && my) atomicAdd(evals, (unsigned long long)my);
   }
-  if (bi == bj) return;
+  if (RECT || bi == bj) return;
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int rr_ = warp + 8 * q;
-    const int j = bj * T1 + rr_, i = bi * T1 + tx;       // A[j][i] = tt[i][j]
-    if (i < n && j < n) A[(int64_t)j * lda + i] = tt[tx][rr_];
+    const int lj = bj * T1 + rr_, li = bi * T1 + tx;       // A[j][i] = tt[i][j]
+    if (li < R.len && lj < Cn.len) A[(int64_t)lj * lda + li] = tt[tx][rr_];
   }
 }
 
@@ -736,17 +758,20 @@ __global__ void __launch_bounds__(256) cross1d_gather_rows_kernel(DevMesh m, Src
   if (idx >= rows * n) return;
   const int i = r0 + (int)(idx / n), j = (int)(idx % n);
   const int vi = dof_vertex[i], vj = dof_vertex[j];
+  // gather1d's canonical order: the cells of min(i, j) outer; G rows are i's (target) cells
+  const bool sw = i > j;
+  const int vo = sw ? vj : vi, vn = sw ? vi : vj;
   double val = 0.0;
-  for (int a_ = m.patch_off[vi]; a_ < m.patch_off[vi + 1]; ++a_) {
+  for (int a_ = m.patch_off[vo]; a_ < m.patch_off[vo + 1]; ++a_) {
     const int K = m.patch_cells[a_];
     const int kv0 = S.v0[K], kv1 = S.v1[K];
-    const int a = (kv0 == vi) ? 0 : 1;
-    for (int b_ = m.patch_off[vj]; b_ < m.patch_off[vj + 1]; ++b_) {
+    const int a = (kv0 == vo) ? 0 : 1;
+    for (int b_ = m.patch_off[vn]; b_ < m.patch_off[vn + 1]; ++b_) {
       const int L = m.patch_cells[b_];
       const int lv0 = S.v0[L], lv1 = S.v1[L];
       if (K == L || lv0 == kv0 || lv0 == kv1 || lv1 == kv0 || lv1 == kv1) continue;
-      const int b = (lv0 == vj) ? 0 : 1;
-      val += negC * comp(G[(int64_t)tpos[K] * m.nc + L], a, b);
+      const int b = (lv0 == vn) ? 0 : 1;
+      val += negC * (sw ? comp(G[(int64_t)tpos[L] * m.nc + K], b, a) : comp(G[(int64_t)tpos[K] * m.nc + L], a, b));
     }
   }
   A[(int64_t)(i - r0) * lda + j] = val;
@@ -813,27 +838,45 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
   const double negC = -Cds;   // (C/2) * (-2) (assembly.py:723, :1100)
   const char* path = getenv("FRACLAP_CROSS1D");
   const bool force_pairs = path && std::string(path) == "pairs";
-  if (symmetric && !force_pairs && m.n > 0) {
+  if (!force_pairs && m.n > 0 && row_end > row_begin) {
     // fused DoF tiles when every tile's cells fit the shared-memory pair table
-    const int nt = (m.n + T1 - 1) / T1;
-    DBuf<int> tcnt(nt), tcell((size_t)nt * T1C), dslot((size_t)2 * m.n), owner(m.nc), mx(1);
-    FL_CUDA(cudaMemsetAsync(owner.p, 0x7f, sizeof(int) * m.nc, st));
+    struct TilingBuf {
+      DBuf<int> cnt, cell, dslot, owner;
+      int off = 0, len = 0, nt = 0;
+      Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, off, len, nt}; }
+    };
+    DBuf<int> mx(1);
     FL_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), st));
-    tile1d_cells_kernel<<<(nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, m.n, nt, tcnt.p, tcell.p, dslot.p, owner.p, mx.p),
-        ::fl::note_launch();
-    FL_CHECK_LAUNCH();
+    auto make = [&](TilingBuf& T, int off, int len) {
+      T.off = off; T.len = len; T.nt = (len + T1 - 1) / T1;
+      T.cnt.alloc(T.nt); T.cell.alloc((size_t)T.nt * T1C); T.dslot.alloc((size_t)2 * len); T.owner.alloc(m.nc);
+      FL_CUDA(cudaMemsetAsync(T.owner.p, 0x7f, sizeof(int) * m.nc, st));
+      tile1d_cells_kernel<<<(T.nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, off, len, T.nt, T.cnt.p, T.cell.p, T.dslot.p,
+                                                          T.owner.p, mx.p),
+          ::fl::note_launch();
+      FL_CHECK_LAUNCH();
+    };
+    TilingBuf TR, TC;
+    make(TC, 0, m.n);
+    if (!symmetric) make(TR, row_begin, row_end - row_begin);
     int mc = 0;
     FL_CUDA(cudaMemcpyAsync(&mc, mx.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     FL_CUDA(cudaStreamSynchronize(st));
     if (mc <= T1C) {
       mc = std::max(mc, 1);
       const size_t smem = (sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc;
-      const int64_t ntp = (int64_t)nt * (nt + 1) / 2;
+      const Tiling1D cv = TC.view(), rv = symmetric ? cv : TR.view();
+      const int64_t ntp = symmetric ? (int64_t)cv.nt * (cv.nt + 1) / 2 : (int64_t)rv.nt * cv.nt;
       FL_E4_SWITCH1(e4, {
-        auto kern = cross1d_tile_kernel<E4>;
-        FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)ntp, 256, smem, st>>>(m, t.data, t, oc, ex, S, nt, tcnt.p, tcell.p, dslot.p, owner.p, mc,
-                                               m.n, negC, A, lda, evals);
+        if (symmetric) {
+          auto kern = cross1d_tile_kernel<E4, false>;
+          FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          kern<<<(unsigned)ntp, 256, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+        } else {
+          auto kern = cross1d_tile_kernel<E4, true>;
+          FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          kern<<<(unsigned)ntp, 256, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+        }
         ::fl::note_launch();
       });
       FL_CHECK_LAUNCH();
