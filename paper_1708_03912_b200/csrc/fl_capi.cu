@@ -379,14 +379,24 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     build_tiles(m, (int)row_begin, (int)row_end, trow, st);
     if (!full) build_tiles(m, 0, (int)n, tcol, st);
     ntiles = trow.ntiles;
+    TilePairs tps;
+    build_tile_pairs(m, oc, trow, full ? trow : tcol, full, d == 1 ? KW1D : KW2D, tps, st);
+    ntp = tps.nall;
     tm.mark();  // 5
-    // pass 1 (discovery): the orders of every pair; near pairs (order >= KW) are recorded
-    unsigned int cap = (unsigned int)std::min<int64_t>((int64_t)m.nc * 1024, (int64_t)1 << 31);
+    // pass 1 (discovery): orders of the pairs of the tile pairs that can hold near pairs (order
+    // >= KW, by the tile bound); near pairs are recorded.  Near-key list (with halo duplicates):
+    // generous, bounded by a quarter of the free memory
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    unsigned int cap = (unsigned int)std::max<int64_t>(
+        1024, std::min<int64_t>({(int64_t)m.nc * 4096, (int64_t)(fr / 4 / sizeof(unsigned long long)),
+                                 ((int64_t)1 << 31) - 1}));
     for (int attempt = 0; attempt < 2; ++attempt) {
       near_keys.alloc(cap);
       FL_CUDA(cudaMemsetAsync(near_cnt.p, 0, sizeof(unsigned int), st));
-      launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
-                         D->lda, ncolors, ntp, evc.p + 1, near_keys.p, near_cnt.p, cap, 1, nullptr, 0, nullptr, st);
+      launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, tps.near.p, tps.nnear, full,
+                         (int)row_begin, (int)row_end, D->A.p, D->lda, evc.p + 1, near_keys.p, near_cnt.p, cap, 1,
+                         nullptr, nullptr, 0, nullptr, st);
       unsigned int cnt = 0;
       FL_CUDA(cudaMemcpyAsync(&cnt, near_cnt.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
       FL_CUDA(cudaStreamSynchronize(st));
@@ -399,8 +409,9 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     near_pairs_build(m, U.t, oc, ex, e4, near_keys.p, nkeys, near, evc.p + 1, st);
     near_keys.free();
     cudaEventRecord(xev[1], st);
-    launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, full, (int)row_begin, (int)row_end, D->A.p,
-                       D->lda, ncolors, ntp, evc.p + 1, nullptr, nullptr, 0, 0, near.U.p, near.n, near.G.p, st);
+    launch_cross_tiles(m, U.t, oc, ex, e4, C, trow, full ? trow : tcol, tps.all.p, tps.nall, full, (int)row_begin,
+                       (int)row_end, D->A.p, D->lda, evc.p + 1, nullptr, nullptr, 0, 0, near.hkey.p, near.hidx.p,
+                       near.hmask, near.G.p, st);
   }
   tm.mark();  // 6
   DBuf<double> Lc((size_t)m.nc * 9);

@@ -192,11 +192,42 @@ struct CrossShared {
   int qlarge, qsmall, nlarge, nsmall, tile;
   int rdof[TILE], cdof[TILE];
   int kofs[KDIR];
-  short cgl[4][SBC * 3];                // column-class lists of the current column sub-block: cc*4 + b
-  unsigned char cgs[4][SBC * 3];        //   ... and the tile column slot
-  int cgn[4];
+  // phase-C entry lists: per tile column its (column cell, slot) entries in the current column
+  // sub-block; per tile row its rowl range in the current row sub-block; touched rows / columns
+  short cent[TILE][ROWL];
+  unsigned char ccnt[TILE];
+  short rr0[TILE], rr1[TILE];
+  unsigned char trow[TILE], tcol[TILE];
+  int ntr, ntc;
+  // order inputs staged per tile (rows) / per column sub-block (columns): centroid, radius,
+  // fp32 ln h and |ln h| (2D fast order path)
+  double rcx[TILE_MAXC], rcy[TILE_MAXC], rrad[TILE_MAXC];
+  float rlnh[TILE_MAXC], rlh[TILE_MAXC];
+  double ccx[SBC], ccy[SBC], crad[SBC];
+  float clnh[SBC], clh[SBC];
+  // phase-B chunks of far pairs of one order: a warp takes 32 / L pairs, L lanes per pair
+  short chs[SBP / 4 + 8];
+  unsigned char chn[SBP / 4 + 8], chk[SBP / 4 + 8];
+  int nchunk;
   // followed by the packed disjoint rules: per node u0 u1 lw0 lw1 lw2 (5 doubles)
 };
+
+// Fast 2D disjoint order from staged centroids / radii / fp32 log sizes: 0 when the exact path
+// is needed (close pair — the reference then uses the exact simplex distance — or an fp32
+// estimate within ORDER_DELTA of an integer), else k.  A pair classified far here is far in the
+// reference arithmetic too: the centroid-gap bound carries a 1e-12 relative margin, far above
+// the few-ulp error of the approximate square root.
+__device__ __forceinline__ int order2d_fast(const OrderConsts& oc, double dx, double dy, double ra, double rb,
+                                            float lnA, float lA, float lnB, float lB) {
+  const double r2 = fma(dy, dy, dx * dx);
+  if (!(r2 > 1e-200)) return 0;
+  const double dc = r2 * rsqrt_nb(r2);
+  const double sr = ra + rb;
+  const double lower = dc - sr;
+  if (!(lower > 2.0 * sr * (1.0 + 1e-12))) return 0;
+  return order_from_estimate(order_estimate_f(oc, oc.coff_f, lnA, lA, lnB, lB, __logf((float)lower)),
+                             oc.cap_disjoint);
+}
 
 template <int D>
 __device__ __forceinline__ int pre_off(int k) {   // offset of order k in CrossShared::nodes
@@ -344,6 +375,151 @@ __device__ __forceinline__ void cross_gen(const double* __restrict__ rt, int nn,
     }
 }
 
+// lanes sharing one far pair in phase B (2D: 16 / 81 / 256 evaluations for k = 2 / 3 / 4)
+template <int D>
+__device__ __forceinline__ int lanes_per_pair(int k) {
+  return D == 2 ? (k <= 2 ? 1 : k == 3 ? 3 : 8) : 1;
+}
+
+// partial 3x3 block over the x nodes x0, x0 + xs, ... (precomputed node coordinates)
+template <int D, int E4>
+__device__ __forceinline__ void cross_part_pre(const double2* __restrict__ Xn, const double2* __restrict__ Yn,
+                                               const double* __restrict__ rt, int nn, int x0, int xs, double ex,
+                                               double (&Gm)[3][3]) {
+  for (int i = x0; i < nn; i += xs) {
+    const double2 X = Xn[i];
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 2
+    for (int j = 0; j < nn; ++j) {
+      const double2 Y = Yn[j];
+      const double d0 = X.x - Y.x;
+      double r2;
+      if (D == 1) {
+        r2 = d0 * d0;
+      } else {
+        const double d1 = X.y - Y.y;
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+      const double* ny = rt + 5 * j;
+      t0 = fma(v, ny[2], t0);
+      t1 = fma(v, ny[3], t1);
+      if (D == 2) t2 = fma(v, ny[4], t2);
+    }
+    const double* nx = rt + 5 * i;
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      Gm[a][0] = fma(nx[2 + a], t0, Gm[a][0]);
+      Gm[a][1] = fma(nx[2 + a], t1, Gm[a][1]);
+      if (D == 2) Gm[a][2] = fma(nx[2 + a], t2, Gm[a][2]);
+    }
+  }
+}
+
+// y-outer variant for the multi-lane orders (2D k = 3: 3 lanes x 3 x-nodes; k = 4: 8 lanes x 2
+// x-nodes): each y node (and its weights) is loaded / mapped once and reused for the lane's NX
+// x nodes.  Per x node the sums over y run in the same order as cross_part_pre.
+template <int E4, int NX, bool PRE>
+__device__ __forceinline__ void cross_part_yo(const double2* __restrict__ Xn, const double2* __restrict__ Yn,
+                                              const double* __restrict__ rt, int nn, int x0, int xs,
+                                              const CellGeo& K, const CellGeo& L, double ex, double (&Gm)[3][3]) {
+  double X0[NX], X1[NX], t[NX][3];
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    const int x = x0 + i * xs;
+    if (PRE) {
+      X0[i] = Xn[x].x;
+      X1[i] = Xn[x].y;
+    } else {
+      const double* nx = rt + 5 * x;
+      X0[i] = K.p[0][0] + (nx[0] * (K.p[1][0] - K.p[0][0]) + nx[1] * (K.p[2][0] - K.p[0][0]));
+      X1[i] = K.p[0][1] + (nx[0] * (K.p[1][1] - K.p[0][1]) + nx[1] * (K.p[2][1] - K.p[0][1]));
+    }
+    t[i][0] = t[i][1] = t[i][2] = 0.0;
+  }
+  double le00 = 0, le01 = 0, le10 = 0, le11 = 0;
+  if (!PRE) {
+    le00 = L.p[1][0] - L.p[0][0]; le01 = L.p[1][1] - L.p[0][1];
+    le10 = L.p[2][0] - L.p[0][0]; le11 = L.p[2][1] - L.p[0][1];
+  }
+  for (int y = 0; y < nn; ++y) {
+    const double* ny = rt + 5 * y;
+    double Y0, Y1;
+    if (PRE) {
+      const double2 Y = Yn[y];
+      Y0 = Y.x;
+      Y1 = Y.y;
+    } else {
+      Y0 = L.p[0][0] + (ny[0] * le00 + ny[1] * le10);
+      Y1 = L.p[0][1] + (ny[0] * le01 + ny[1] * le11);
+    }
+    const double w0 = ny[2], w1 = ny[3], w2 = ny[4];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      const double d0 = X0[i] - Y0, d1 = X1[i] - Y1;
+      const double v = kpow<E4>(fma(d1, d1, d0 * d0), ex);
+      t[i][0] = fma(v, w0, t[i][0]);
+      t[i][1] = fma(v, w1, t[i][1]);
+      t[i][2] = fma(v, w2, t[i][2]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NX; ++i) {
+    const double* nx = rt + 5 * (x0 + i * xs);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      Gm[a][0] = fma(nx[2 + a], t[i][0], Gm[a][0]);
+      Gm[a][1] = fma(nx[2 + a], t[i][1], Gm[a][1]);
+      Gm[a][2] = fma(nx[2 + a], t[i][2], Gm[a][2]);
+    }
+  }
+}
+
+// same with the nodes mapped on the fly (orders above KPRE)
+template <int D, int E4>
+__device__ __forceinline__ void cross_part_gen(const double* __restrict__ rt, int nn, int x0, int xs,
+                                               const CellGeo& K, const CellGeo& L, double ex, double (&Gm)[3][3]) {
+  const double ke00 = K.p[1][0] - K.p[0][0], ke01 = K.p[1][1] - K.p[0][1];
+  const double ke10 = K.p[2][0] - K.p[0][0], ke11 = K.p[2][1] - K.p[0][1];
+  const double le00 = L.p[1][0] - L.p[0][0], le01 = L.p[1][1] - L.p[0][1];
+  const double le10 = L.p[2][0] - L.p[0][0], le11 = L.p[2][1] - L.p[0][1];
+  for (int x = x0; x < nn; x += xs) {
+    const double* nx = rt + 5 * x;
+    double X0, X1 = 0.0;
+    if (D == 1) {
+      X0 = K.p[0][0] + nx[0] * ke00;
+    } else {
+      X0 = K.p[0][0] + (nx[0] * ke00 + nx[1] * ke10);
+      X1 = K.p[0][1] + (nx[0] * ke01 + nx[1] * ke11);
+    }
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 2
+    for (int y = 0; y < nn; ++y) {
+      const double* ny = rt + 5 * y;
+      double r2;
+      if (D == 1) {
+        const double d0 = X0 - (L.p[0][0] + ny[0] * le00);
+        r2 = d0 * d0;
+      } else {
+        const double d0 = X0 - (L.p[0][0] + (ny[0] * le00 + ny[1] * le10));
+        const double d1 = X1 - (L.p[0][1] + (ny[0] * le01 + ny[1] * le11));
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+      t0 = fma(v, ny[2], t0);
+      t1 = fma(v, ny[3], t1);
+      if (D == 2) t2 = fma(v, ny[4], t2);
+    }
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      const double lx = nx[2 + a];
+      Gm[a][0] = fma(lx, t0, Gm[a][0]);
+      Gm[a][1] = fma(lx, t1, Gm[a][1]);
+      if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
+    }
+  }
+}
+
 template <int D, int E4>
 __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const double* __restrict__ tab,
                                                            DevTables dir, OrderConsts oc, double ex,
@@ -356,8 +532,9 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
                                                            unsigned long long* __restrict__ near_keys,
                                                            unsigned int* __restrict__ near_count,
                                                            unsigned int near_cap, int discover,
-                                                           const unsigned long long* __restrict__ nearU,
-                                                           int64_t nU, const double* __restrict__ nearG) {
+                                                           const unsigned long long* __restrict__ nearH,
+                                                           const int* __restrict__ nearI, unsigned long long hmask,
+                                                           const double* __restrict__ nearG) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CrossShared& S = *reinterpret_cast<CrossShared*>(smem_raw);
   double* rtab = reinterpret_cast<double*>(smem_raw + ((sizeof(CrossShared) + 15) / 16) * 16);
@@ -394,8 +571,14 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
 
     // ---- stage the tile metadata
     for (int i = tid; i < nR; i += XT) {
-      S.rowc[i] = R.cells[tr * TILE_MAXC + i];
+      const int c = R.cells[tr * TILE_MAXC + i];
+      S.rowc[i] = c;
       for (int a = 0; a < 3; ++a) S.rslot[i][a] = (signed char)R.slots[(tr * TILE_MAXC + i) * 3 + a];
+      if (D == 2) {
+        const CellGeo& g = m.geo[c];
+        S.rcx[i] = g.cx; S.rcy[i] = g.cy; S.rrad[i] = g.rad;
+        S.rlnh[i] = __logf((float)g.diam); S.rlh[i] = (float)g.ldiam;
+      }
     }
     for (int i = tid; i < nC; i += XT) {
       S.colc[i] = Cv.cells[tc * TILE_MAXC + i];
@@ -414,51 +597,94 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
           if (S.rslot[i][a] == tid && c < ROWL) S.rowl[tid][c++] = (short)(i * 4 + a);
       S.rown[tid] = (unsigned char)c;
     }
+    __syncthreads();                     // rowl / rown are read by other warps below
 
     for (int cs0 = 0; cs0 < nC; cs0 += SBC) {
-      if (tid < 4) {                     // column class c % 4 -> (column cell, slot) entries
+      if (D == 2 && tid >= 32 && tid < 32 + SBC && cs0 + tid - 32 < nC) {
+        const int i = tid - 32;
+        const CellGeo& g = m.geo[S.colc[cs0 + i]];
+        S.ccx[i] = g.cx; S.ccy[i] = g.cy; S.crad[i] = g.rad;
+        S.clnh[i] = __logf((float)g.diam); S.clh[i] = (float)g.ldiam;
+      }
+      if (tid >= 64 && tid < 64 + TILE) {   // tile column -> its (column cell, slot) entries here
+        const int col = tid - 64;
         int c = 0;
         for (int cc = 0; cc < SBC && cs0 + cc < nC; ++cc)
-          for (int b = 0; b <= D; ++b) {
-            const int cs = S.cslot[cs0 + cc][b];
-            if (cs >= 0 && (cs & 3) == tid) {
-              S.cgl[tid][c] = (short)(cc * 4 + b);
-              S.cgs[tid][c] = (unsigned char)cs;
-              ++c;
-            }
-          }
-        S.cgn[tid] = c;
+          for (int b = 0; b <= D; ++b)
+            if (S.cslot[cs0 + cc][b] == col && c < ROWL) S.cent[col][c++] = (short)(cc * 4 + b);
+        S.ccnt[col] = (unsigned char)c;
       }
       for (int rs0 = 0; rs0 < nR; rs0 += SBR) {
         // ---- (A) orders of the 512 pairs of this sub-block
         if (tid <= KDIR) S.hist[tid] = 0;
+        if (tid >= 64 && tid < 64 + TILE) {   // tile row -> its rowl range in this row sub-block
+          const int r = tid - 64;
+          int e0 = 0;
+          while (e0 < S.rown[r] && (S.rowl[r][e0] >> 2) < rs0) ++e0;
+          int e1 = e0;
+          while (e1 < S.rown[r] && (S.rowl[r][e1] >> 2) < rs0 + SBR) ++e1;
+          S.rr0[r] = (short)e0;
+          S.rr1[r] = (short)e1;
+        }
         __syncthreads();
+        if (tid < 32) {                       // touched rows / columns, ascending
+          const bool r0 = S.rr1[tid] > S.rr0[tid], r1 = S.rr1[tid + 32] > S.rr0[tid + 32];
+          const bool c0 = S.ccnt[tid] > 0, c1 = S.ccnt[tid + 32] > 0;
+          const unsigned br0 = __ballot_sync(0xffffffffu, r0), br1 = __ballot_sync(0xffffffffu, r1);
+          const unsigned bc0 = __ballot_sync(0xffffffffu, c0), bc1 = __ballot_sync(0xffffffffu, c1);
+          const unsigned lt = (1u << tid) - 1u;
+          if (r0) S.trow[__popc(br0 & lt)] = (unsigned char)tid;
+          if (r1) S.trow[__popc(br0) + __popc(br1 & lt)] = (unsigned char)(tid + 32);
+          if (c0) S.tcol[__popc(bc0 & lt)] = (unsigned char)tid;
+          if (c1) S.tcol[__popc(bc0) + __popc(bc1 & lt)] = (unsigned char)(tid + 32);
+          if (tid == 0) { S.ntr = __popc(br0) + __popc(br1); S.ntc = __popc(bc0) + __popc(bc1); }
+        }
         for (int p = tid; p < SBP; p += XT) {
           const int rc = rs0 + p / SBC, cc = cs0 + p % SBC;
           int k = 0;
           if (rc < nR && cc < nC) {
             const int idK = S.rowc[rc], idL = S.colc[cc];
-            const CellGeo& Kg = m.geo[idK];
-            const CellGeo& Lg = m.geo[idL];
-            if (!touching<D>(Kg, Lg)) {
-              // the reference orders a disjoint pair as (min id, max id) (assembly.py:973-982, :705)
-              const CellGeo& P = (idK < idL) ? Kg : Lg;
-              const CellGeo& Qg = (idK < idL) ? Lg : Kg;
-              k = order_disjoint_fast(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
+            int kf = 0;
+            if (D == 2) {
+              const int lc = p % SBC;
+              kf = order2d_fast(oc, S.rcx[rc] - S.ccx[lc], S.rcy[rc] - S.ccy[lc], S.rrad[rc], S.crad[lc],
+                                S.rlnh[rc], S.rlh[rc], S.clnh[lc], S.clh[lc]);
+            }
+            bool disjoint = kf > 0;
+            if (!disjoint) {
+              // close / ambiguous pair: exact reference arithmetic on the cell records; the
+              // reference orders a disjoint pair as (min id, max id) (assembly.py:973-982, :705)
+              const CellGeo& Kg = m.geo[idK];
+              const CellGeo& Lg = m.geo[idL];
+              if (!touching<D>(Kg, Lg)) {
+                const CellGeo& P = (idK < idL) ? Kg : Lg;
+                const CellGeo& Qg = (idK < idL) ? Lg : Kg;
+                kf = order_disjoint_fast(oc, oc.coff, P, Qg, dist_estimate<D>(P, Qg));
+                disjoint = true;
+              }
+            }
+            if (disjoint) {
+              k = kf;
               if (k >= KW && (discover || nearG != nullptr)) {
                 // near pair: its block is computed once by the near-pair kernel (fl_near.cu)
-                const unsigned long long key = ((unsigned long long)min(idK, idL) << 32) | (unsigned)max(idK, idL);
+                const unsigned long long key = near_key(idK, idL, k);
                 if (discover) {
-                  const unsigned int slot = atomicAdd(near_count, 1u);
+                  // warp-aggregated append (one atomic per warp and sub-block pass)
+                  const unsigned am = __activemask();
+                  const int leader = __ffs(am) - 1;
+                  unsigned int base = 0;
+                  if (lane == leader) base = atomicAdd(near_count, (unsigned)__popc(am));
+                  base = __shfl_sync(am, base, leader);
+                  const unsigned int slot = base + __popc(am & ((1u << lane) - 1u));
                   if (slot < near_cap) near_keys[slot] = key;
                   k = 0;
                 } else {
-                  int64_t lo = 0, hi = nU - 1;                 // binary search in the sorted unique keys
-                  while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (nearU[mid] < key) lo = mid + 1; else hi = mid;
-                  }
-                  if (nearU[lo] != key) atomicOr(m.err, 4);       // cannot happen: same orders as discovery
+                  unsigned long long h = near_hash(key) & hmask;   // open-addressing lookup
+                  unsigned long long hk;
+                  while ((hk = nearH[h]) != key && hk != NEAR_EMPTY) h = (h + 1) & hmask;
+                  int64_t lo = 0;
+                  if (hk == key) lo = nearI[h];
+                  else atomicOr(m.err, 4);                         // cannot happen: same orders as discovery
                   const double* g = nearG + lo * 9;
                   const bool tr = idK > idL;                     // M^{min,max}: transpose when K is the max
 #pragma unroll
@@ -484,6 +710,17 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
           S.nsmall = off - nl;
           S.qlarge = 0;
           S.qsmall = 0;
+          int nch = 0;
+          for (int k = KW - 1; k >= 2; --k) {
+            const int ppc = 32 / lanes_per_pair<D>(k);
+            for (int s0 = 0; s0 < S.hist[k]; s0 += ppc) {
+              S.chs[nch] = (short)(S.cursor[k] + s0);
+              S.chn[nch] = (unsigned char)min(ppc, S.hist[k] - s0);
+              S.chk[nch] = (unsigned char)k;
+              ++nch;
+            }
+          }
+          S.nchunk = nch;
         }
         // ---- (A2) node coordinates of the sub-block's cells for the small orders present
         for (int k = 2; k <= KPRE; ++k) {
@@ -526,46 +763,88 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
           if (lane == 0) my_evals += (unsigned long long)nn * nn;
         }
         for (;;) {
-          int i = 0;
-          if (lane == 0) i = atomicAdd(&S.qsmall, 32);
-          i = __shfl_sync(0xffffffffu, i, 0) + lane;
-          if (i - lane >= ns) break;
-          if (i < ns) {
-            const int p = S.plist[nl + i];
-            const int k = S.pk[p];
-            const int nn = (D == 1) ? k : k * k;
-            const int r = p / SBC, c = p % SBC;
-            const double* rt = rtab + 5 * S.kofs[k];
-            if (k <= KPRE) {
+          int ch = 0;
+          if (lane == 0) ch = atomicAdd(&S.qsmall, 1);
+          ch = __shfl_sync(0xffffffffu, ch, 0);
+          if (ch >= S.nchunk) break;
+          const int k = S.chk[ch];
+          const int L = lanes_per_pair<D>(k);
+          const int g = lane / L, sub = lane - g * L;
+          const bool act = g < S.chn[ch];
+          const int p = act ? S.plist[S.chs[ch] + g] : 0;
+          const int nn = (D == 1) ? k : k * k;
+          const int r = p / SBC, c = p % SBC;
+          const double* rt = rtab + 5 * S.kofs[k];
+          if (k == 2) {                       // one lane per pair, fully unrolled
+            if (act) {
               const double JJ = m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
-              const double2* Xn = &S.nodes[r][pre_off<D>(k)];
-              const double2* Yn = &S.nodes[SBR + c][pre_off<D>(k)];
-              if (k == 2) cross_fixed<D, E4, 2>(Xn, Yn, rt, JJ, ex, S.Gs[p]);
-#if FL_FIXED3
-              else if (k == 3) cross_fixed<D, E4, 3>(Xn, Yn, rt, JJ, ex, S.Gs[p]);
-#endif
-              else cross_pre<D, E4>(Xn, Yn, rt, nn, JJ, ex, S.Gs[p]);
-            } else {
-              cross_gen<D, E4>(rt, nn, m.geo[S.rowc[rs0 + r]], m.geo[S.colc[cs0 + c]], ex, S.Gs[p], false);
+              cross_fixed<D, E4, 2>(&S.nodes[r][pre_off<D>(2)], &S.nodes[SBR + c][pre_off<D>(2)], rt, JJ, ex, S.Gs[p]);
+              my_evals += (unsigned long long)nn * nn;
             }
+            continue;
+          }
+          double Gm[3][3] = {};
+          if (act) {
+            if (D == 2 && k == 3) {
+              cross_part_yo<E4, 3, true>(&S.nodes[r][pre_off<D>(3)], &S.nodes[SBR + c][pre_off<D>(3)], rt, nn, sub,
+                                         L, m.geo[0], m.geo[0], ex, Gm);
+            } else if (D == 2 && k == 4) {
+              cross_part_yo<E4, 2, false>(nullptr, nullptr, rt, nn, sub, L, m.geo[S.rowc[rs0 + r]],
+                                          m.geo[S.colc[cs0 + c]], ex, Gm);
+            } else if (k <= KPRE) {
+              cross_part_pre<D, E4>(&S.nodes[r][pre_off<D>(k)], &S.nodes[SBR + c][pre_off<D>(k)], rt, nn, sub, L, ex,
+                                    Gm);
+            } else {
+              cross_part_gen<D, E4>(rt, nn, sub, L, m.geo[S.rowc[rs0 + r]], m.geo[S.colc[cs0 + c]], ex, Gm);
+            }
+          }
+          // fixed-order reduction over the L lanes of the pair (L = 1, 3 or 8)
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              double v = Gm[a][b];
+              if (L == 3) {
+                const double v1 = __shfl_down_sync(0xffffffffu, v, 1), v2 = __shfl_down_sync(0xffffffffu, v, 2);
+                v = (v + v1) + v2;
+              } else if (L == 8) {
+                v += __shfl_down_sync(0xffffffffu, v, 4);
+                v += __shfl_down_sync(0xffffffffu, v, 2);
+                v += __shfl_down_sync(0xffffffffu, v, 1);
+              }
+              Gm[a][b] = v;
+            }
+          if (act && sub == 0) {
+            const double JJ = m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) S.Gs[p][a * 3 + b] = Gm[a][b] * JJ;
             my_evals += (unsigned long long)nn * nn;
           }
         }
         __syncthreads();
-        // ---- (C) row-owner scatter: 4 threads per tile row, column classes c % 4
+        // ---- (C) entry-parallel scatter: every touched (row, column) of the tile sums its
+        // terms of this sub-block in (row entry, column entry) order, then adds once
         {
-          const int r = tid >> 2, cg = tid & 3;
-          const int ng = S.cgn[cg];
-          for (int e = 0; e < S.rown[r]; ++e) {
-            const int rc = S.rowl[r][e] >> 2, a = S.rowl[r][e] & 3;
-            if (rc < rs0 || rc >= rs0 + SBR) continue;
-            const int pr = (rc - rs0) * SBC;
-            for (int u = 0; u < ng; ++u) {
-              const int it = S.cgl[cg][u];
-              const int p = pr + (it >> 2);
-              if (S.pk[p] == 0) continue;
-              S.At[r][S.cgs[cg][u]] += negC * S.Gs[p][a * 3 + (it & 3)];
+          const int ntr = S.ntr, ntc = S.ntc, nit = ntr * ntc;
+          const unsigned long long mg = ntc ? ((1ull << 32) + ntc - 1) / (unsigned)ntc : 0;   // it / ntc, it < 2^16
+          for (int it = tid; it < nit; it += XT) {
+            const int ri = (int)(((unsigned long long)it * mg) >> 32), ci = it - ri * ntc;
+            const int r = S.trow[ri], c = S.tcol[ci];
+            const int nce = S.ccnt[c];
+            double v = 0.0;
+            for (int e = S.rr0[r]; e < S.rr1[r]; ++e) {
+              const int rc = S.rowl[r][e] >> 2, a = S.rowl[r][e] & 3;
+              const int pr = (rc - rs0) * SBC;
+              for (int f = 0; f < nce; ++f) {
+                const int ent = S.cent[c][f];
+                const int p = pr + (ent >> 2);
+                if (S.pk[p] == 0) continue;
+                v += negC * S.Gs[p][a * 3 + (ent & 3)];
+              }
             }
+            S.At[r][c] += v;
           }
         }
         __syncthreads();
@@ -704,45 +983,17 @@ void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const 
 }
 
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
-                        double Cds, const Tiles& rows, const Tiles& cols, bool symmetric, int row_begin,
-                        int row_end, double* A, int64_t lda, int ncolors, int64_t& ntilepairs,
+                        double Cds, const Tiles& rows, const Tiles& cols, const int2* tpairs, int ntp,
+                        bool symmetric, int row_begin, int row_end, double* A, int64_t lda,
                         unsigned long long* evals, unsigned long long* near_keys, unsigned int* near_count,
-                        unsigned int near_cap, int discover, const unsigned long long* nearU, int64_t nU,
-                        const double* nearG, cudaStream_t st) {
-  (void)ncolors;
-  std::vector<int2> hp;
-  for (int r = 0; r < rows.ntiles; ++r)
-    for (int c = symmetric ? r : 0; c < cols.ntiles; ++c) hp.push_back(make_int2(r, c));
-  ntilepairs = (int64_t)hp.size();
-  {
-    // heavy (near) tile pairs first: higher orders live there; sorting by tile distance keeps the
-    // expensive CTAs out of the tail of the grid
-    std::vector<double> gr((size_t)rows.ntiles * 3), gc((size_t)cols.ntiles * 3);
-    FL_CUDA(cudaMemcpyAsync(gr.data(), rows.geo3.p, gr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-    FL_CUDA(cudaMemcpyAsync(gc.data(), cols.geo3.p, gc.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-    FL_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> key(hp.size());
-    for (size_t i = 0; i < hp.size(); ++i) {
-      const double* a = &gr[3 * hp[i].x];
-      const double* b = &gc[3 * hp[i].y];
-      key[i] = std::hypot(a[0] - b[0], a[1] - b[1]) - a[2] - b[2];
-    }
-    std::vector<size_t> idx(hp.size());
-    for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
-    std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return key[a] < key[b]; });
-    std::vector<int2> sorted(hp.size());
-    for (size_t i = 0; i < idx.size(); ++i) sorted[i] = hp[idx[i]];
-    hp.swap(sorted);
-  }
-  if (hp.empty()) return;
-  DBuf<int2> dp(hp.size());
-  FL_CUDA(cudaMemcpyAsync(dp.p, hp.data(), hp.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+                        unsigned int near_cap, int discover, const unsigned long long* nearH, const int* nearI,
+                        unsigned long long hmask, const double* nearG, cudaStream_t st) {
+  if (ntp <= 0) return;
   TileView R{rows.dofs.p, rows.ncell.p, rows.cells.p, rows.slots.p, rows.cstart.p};
   TileView C{cols.dofs.p, cols.ncell.p, cols.cells.p, cols.slots.p, cols.cstart.p};
   const size_t smem = cross_smem_bytes(m.d);
   const double negC = -Cds;   // (C/2) * (-2)  (assembly.py:723, :1100)
   const int kmax = oc.cap_disjoint;
-  const int ntp = (int)hp.size();
   DBuf<int> queue(1);
   FL_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
   int dev = 0, sms = 148;
@@ -752,20 +1003,21 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
   if (m.d == 1) {
     FL_E4_SWITCH(e4, {
       FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<1, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      cross_tile_kernel<1, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p, ntp, queue.p, kmax,
+      cross_tile_kernel<1, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, tpairs, ntp, queue.p, kmax,
                                                      symmetric ? 1 : 0, row_begin, row_end, A, lda, evals, near_keys,
-                                                     near_count, near_cap, discover, nearU, nU, nearG), ::fl::note_launch();
+                                                     near_count, near_cap, discover, nearH, nearI, hmask, nearG),
+          ::fl::note_launch();
     });
   } else {
     FL_E4_SWITCH(e4, {
       FL_CUDA(cudaFuncSetAttribute(cross_tile_kernel<2, E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      cross_tile_kernel<2, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, dp.p, ntp, queue.p, kmax,
+      cross_tile_kernel<2, E4><<<grid, XT, smem, st>>>(m, t.data, t, oc, ex, negC, R, C, tpairs, ntp, queue.p, kmax,
                                                      symmetric ? 1 : 0, row_begin, row_end, A, lda, evals, near_keys,
-                                                     near_count, near_cap, discover, nearU, nU, nearG), ::fl::note_launch();
+                                                     near_count, near_cap, discover, nearH, nearI, hmask, nearG),
+          ::fl::note_launch();
     });
   }
   FL_CHECK_LAUNCH();
-  FL_CUDA(cudaStreamSynchronize(st));   // dp is freed on return
 }
 
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,

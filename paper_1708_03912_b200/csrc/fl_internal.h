@@ -137,7 +137,17 @@ struct Tiles {
   DBuf<int> slots;    // ntiles*TILE_MAXC*3 (-1: vertex not a DoF of this tile)
   DBuf<int> cstart;   // ntiles*(maxcolors+1): colour class ranges in the cell list
   DBuf<double> geo3;  // ntiles*3: centre (x, y) and radius of the tile's DoF vertices
+  DBuf<double> stat;  // ntiles*8: centre (x, y), R = max |c_K - centre| + rad_K, h min/max, |ln h| min/max
 };
+
+// Tile pairs of the cross term, heavy first (sorted by the tile gap), and the subset that can
+// hold near pairs (a rigorous upper bound of the disjoint order formula reaches KW).
+struct TilePairs {
+  DBuf<int2> all, near;
+  int nall = 0, nnear = 0;
+};
+void build_tile_pairs(const DevMesh& m, const OrderConsts& oc, const Tiles& rows, const Tiles& cols, bool symmetric,
+                      int kw, TilePairs& tp, cudaStream_t st);
 constexpr int MAXCOLORS = 32;
 void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& t, cudaStream_t st);
 
@@ -158,18 +168,35 @@ void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, do
 void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const int* targets,
                  int ntargets, double* win /*nc*q*/, cudaStream_t st);
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,
-                        int e4, double Cds, const Tiles& rows, const Tiles& cols, bool symmetric,
-                        int row_begin, int row_end, double* A, int64_t lda, int ncolors,
-                        int64_t& ntilepairs, unsigned long long* evals, unsigned long long* near_keys,
+                        int e4, double Cds, const Tiles& rows, const Tiles& cols, const int2* tpairs, int ntp,
+                        bool symmetric, int row_begin, int row_end, double* A, int64_t lda,
+                        unsigned long long* evals, unsigned long long* near_keys,
                         unsigned int* near_count, unsigned int near_cap, int discover,
-                        const unsigned long long* nearU, int64_t nU, const double* nearG, cudaStream_t st);
+                        const unsigned long long* nearH, const int* nearI, unsigned long long hmask,
+                        const double* nearG, cudaStream_t st);
 // fl_near.cu: near disjoint pairs (order >= KW) collected by the cross tiles, one block each
 constexpr int KW2D = 5, KW1D = 12;
+// near-pair key: (min cell << 34) | (max cell << 6) | k  (cells < 2^28, k <= 32): sorting by key
+// is sorting by the reference's (min, max) orientation
+__host__ __device__ inline unsigned long long near_key(int a, int b, int k) {
+  const unsigned long long lo = (unsigned)(a < b ? a : b), hi = (unsigned)(a < b ? b : a);
+  return (lo << 34) | (hi << 6) | (unsigned long long)k;
+}
+__host__ __device__ inline unsigned long long near_hash(unsigned long long x) {   // splitmix64 finaliser
+  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27; x *= 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+constexpr unsigned long long NEAR_EMPTY = ~0ull;
+
 struct NearPairs {
   int64_t n = 0;
-  DBuf<unsigned long long> U;           // sorted unique keys (min << 32 | max)
-  DBuf<int> P, Q;                       // the two cells of each key
+  DBuf<unsigned long long> U;           // sorted unique keys (near_key)
+  DBuf<int> P, Q, K;                    // the two cells and the order of each key
   DBuf<double> G;                       // n*9: M^{P,Q} (cross_matrices orientation)
+  DBuf<unsigned long long> hkey;        // open-addressing table key -> index (linear probing)
+  DBuf<int> hidx;
+  unsigned long long hmask = 0;
 };
 void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                       unsigned long long* keys, int64_t nkeys, NearPairs& np, unsigned long long* evals,

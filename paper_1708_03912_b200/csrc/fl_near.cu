@@ -18,7 +18,8 @@ template <int D, int E4>
 __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const double* __restrict__ tab,
                                                              DevTables dir, OrderConsts oc, double ex,
                                                              const int* __restrict__ P, const int* __restrict__ Q,
-                                                             int64_t n, double* __restrict__ G,
+                                                             const int* __restrict__ KK, int64_t n,
+                                                             double* __restrict__ G,
                                                              unsigned long long* __restrict__ evals) {
   __shared__ double2 sy[NW][NMAXN];
   __shared__ double slw[NW][NMAXN][3];
@@ -27,7 +28,7 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
   for (int64_t pi = (int64_t)blockIdx.x * NW + w; pi < n; pi += (int64_t)gridDim.x * NW) {
     const CellGeo& A = m.geo[P[pi]];
     const CellGeo& B = m.geo[Q[pi]];
-    const int k = order_disjoint_fast(oc, oc.coff, A, B, dist_estimate<D>(A, B));   // (min, max) orientation
+    const int k = KK[pi];                 // the order found by the cross tiles (reference orientation)
     const RuleRef rr = dir.rule(T_DISJ, k);
     const int nn = rr.cnt;
     // stage the y (column cell) nodes, absolute coordinates as _map_points forms them
@@ -108,12 +109,20 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
   if (lane == 0 && evals && my) atomicAdd(evals, my);
 }
 
-__global__ void split_keys_kernel(const unsigned long long* keys, int64_t n, int* P, int* Q, int* idx) {
+__global__ void split_keys_kernel(const unsigned long long* keys, int64_t n, int* P, int* Q, int* K,
+                                  unsigned long long* hkey, int* hidx, unsigned long long hmask) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  P[i] = (int)(keys[i] >> 32);
-  Q[i] = (int)(keys[i] & 0xffffffffu);
-  idx[i] = (int)i;
+  const unsigned long long key = keys[i];
+  P[i] = (int)(key >> 34);
+  Q[i] = (int)((key >> 6) & ((1ull << 28) - 1));
+  K[i] = (int)(key & 63);
+  unsigned long long h = near_hash(key) & hmask;
+  for (;;) {
+    const unsigned long long prev = atomicCAS(&hkey[h], NEAR_EMPTY, key);
+    if (prev == NEAR_EMPTY) { hidx[h] = (int)i; break; }
+    h = (h + 1) & hmask;
+  }
 }
 #define FL_E4_SWITCHN(e4, ...)                                \
   switch (e4) {                                               \
@@ -130,7 +139,9 @@ void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& o
                       cudaStream_t st) {
   np.n = 0;
   if (nkeys <= 0) {
-    np.U.alloc(1); np.P.alloc(1); np.Q.alloc(1); np.G.alloc(1);
+    np.U.alloc(1); np.P.alloc(1); np.Q.alloc(1); np.K.alloc(1); np.G.alloc(1);
+    np.hkey.alloc(1); np.hidx.alloc(1); np.hmask = 0;
+    FL_CUDA(cudaMemsetAsync(np.hkey.p, 0xff, sizeof(unsigned long long), st));
     return;
   }
   // sort + unique of the (min, max) keys: deterministic order of the pairs
@@ -151,19 +162,24 @@ void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& o
   FL_CUDA(cudaMemcpyAsync(&nu, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   np.n = nu;
-  np.P.alloc(nu); np.Q.alloc(nu); np.G.alloc((size_t)nu * 9);
-  DBuf<int> idx(nu);
-  split_keys_kernel<<<(nu + 255) / 256, 256, 0, st>>>(np.U.p, nu, np.P.p, np.Q.p, idx.p), ::fl::note_launch();
+  np.P.alloc(nu); np.Q.alloc(nu); np.K.alloc(nu); np.G.alloc((size_t)nu * 9);
+  unsigned long long cap = 1024;
+  while (cap < 2ull * (unsigned long long)nu) cap <<= 1;
+  np.hmask = cap - 1;
+  np.hkey.alloc(cap); np.hidx.alloc(cap);
+  FL_CUDA(cudaMemsetAsync(np.hkey.p, 0xff, cap * sizeof(unsigned long long), st));
+  split_keys_kernel<<<(nu + 255) / 256, 256, 0, st>>>(np.U.p, nu, np.P.p, np.Q.p, np.K.p, np.hkey.p, np.hidx.p,
+                                                       np.hmask), ::fl::note_launch();
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>((nu + NW - 1) / NW, (int64_t)sms * 8);
   if (m.d == 1) {
-    FL_E4_SWITCHN(e4, (near_block_kernel<1, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, np.P.p, np.Q.p, nu,
-                                                                         np.G.p, evals), ::fl::note_launch()));
+    FL_E4_SWITCHN(e4, (near_block_kernel<1, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, np.P.p, np.Q.p, np.K.p,
+                                                                         nu, np.G.p, evals), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCHN(e4, (near_block_kernel<2, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, np.P.p, np.Q.p, nu,
-                                                                         np.G.p, evals), ::fl::note_launch()));
+    FL_E4_SWITCHN(e4, (near_block_kernel<2, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, np.P.p, np.Q.p, np.K.p,
+                                                                         nu, np.G.p, evals), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }

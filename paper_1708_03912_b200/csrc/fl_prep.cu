@@ -462,7 +462,7 @@ constexpr int CAND = 1024;
 __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* sorted_dofs, int nrows,
                                                          const int* dof_vertex, int* tdofs, int* tncell,
                                                          int* tcells, int* tslots, int* tcstart, double* tgeo,
-                                                         int* err) {
+                                                         double* tstat, int* err) {
   const int t = blockIdx.x;
   __shared__ int sd[TILE];
   __shared__ unsigned long long key[CAND];
@@ -550,6 +550,31 @@ __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* s
       tslots[(t * TILE_MAXC + i) * 3 + a] = slot;
     }
   }
+  // tile statistics for the order bounds: cell-covering radius about the DoF centre, h and |ln h| ranges
+  {
+    __shared__ double red[5][256];
+    double R = 0.0, hmn = 1e300, hmx = 0.0, lmn = 1e300, lmx = 0.0;
+    const double cx = tgeo[3 * t], cy = tgeo[3 * t + 1];
+    for (int i = tid; i < nu; i += blockDim.x) {
+      const CellGeo& g = m.geo[(int)(key[i] & 0xffffffffu)];
+      const double dx = g.cx - cx, dy = g.cy - cy;
+      R = fmax(R, sqrt(dx * dx + dy * dy) * (1.0 + 1e-12) + g.rad);
+      hmn = fmin(hmn, g.diam); hmx = fmax(hmx, g.diam);
+      lmn = fmin(lmn, g.ldiam); lmx = fmax(lmx, g.ldiam);
+    }
+    red[0][tid] = R; red[1][tid] = -hmn; red[2][tid] = hmx; red[3][tid] = -lmn; red[4][tid] = lmx;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (tid < o)
+        for (int q = 0; q < 5; ++q) red[q][tid] = fmax(red[q][tid], red[q][tid + o]);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      double* st = tstat + 8 * t;
+      st[0] = cx; st[1] = cy; st[2] = red[0][0]; st[3] = -red[1][0]; st[4] = red[2][0];
+      st[5] = -red[3][0]; st[6] = red[4][0]; st[7] = 0.0;
+    }
+  }
   // colour class starts
   for (int col = tid; col <= MAXCOLORS; col += blockDim.x) {
     int lo = 0;
@@ -590,15 +615,97 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   T.slots.alloc((size_t)T.ntiles * TILE_MAXC * 3);
   T.cstart.alloc((size_t)T.ntiles * (MAXCOLORS + 1));
   T.geo3.alloc((size_t)T.ntiles * 3);
+  T.stat.alloc((size_t)T.ntiles * 8);
   DBuf<int> err(1);
   FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
   tile_cells_kernel<<<T.ntiles, 256, 0, st>>>(m, vals2.p, nrows, dof_vertex.p, T.dofs.p, T.ncell.p,
-                                              T.cells.p, T.slots.p, T.cstart.p, T.geo3.p, err.p), ::fl::note_launch();
+                                              T.cells.p, T.slots.p, T.cstart.p, T.geo3.p, T.stat.p, err.p),
+      ::fl::note_launch();
   FL_CHECK_LAUNCH();
   int herr = 0;
   FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   if (herr) throw Error(-2, "DoF tile touches more than 256 cells (vertex valence too high)");
+}
+
+__global__ void gather_pairs_kernel(const int2* raw, const int* flag, const int* idx, int n, int2* out, int* oflag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { out[i] = raw[idx[i]]; oflag[i] = flag[idx[i]]; }
+}
+
+// Upper bound of select_order's disjoint formula (quadrature.py:159-168) over all pairs of two
+// tiles: dist >= Dmin (the reference's estimate is >= the centroid gap minus the radii, which is
+// >= the tile gap), h in [hmin, hmax], |ln h| in [lmin, lmax]; every term of the numerator is
+// bounded above and the denominator below (it is >= ln rho2 > 0).
+__device__ double order_bound_hi(const OrderConsts& oc, double Dmin, double hmin, double hmax, double lmin,
+                                 double lmax) {
+  (void)hmin;
+  if (!(Dmin > 0.0)) return 1e30;
+  const double num = oc.lead_lnn + oc.sm1 * lmin + lmax - oc.s * log(Dmin) + oc.s * log(hmax) - oc.coff;
+  const double den = fmax(log(Dmin / hmax), 0.0) + oc.ln_rho2;
+  return num > 0.0 ? num / den : 0.0;
+}
+
+__global__ void tile_pairs_kernel(OrderConsts oc, const double* __restrict__ rs, const double* __restrict__ cs,
+                                  int nrt, int nct, int symmetric, int kw, int64_t npairs, int2* __restrict__ pairs,
+                                  unsigned* __restrict__ key, int* __restrict__ nearflag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npairs) return;
+  int r, c;
+  if (symmetric) {   // row-major upper triangle
+    const double q = 2.0 * nrt + 1.0;
+    r = (int)((q - sqrt(q * q - 8.0 * (double)i)) * 0.5);
+    auto cum = [&](int64_t e) { return e * nrt - e * (e - 1) / 2; };
+    while (r > 0 && cum(r) > i) --r;
+    while (cum(r + 1) <= i) ++r;
+    c = r + (int)(i - cum(r));
+  } else {
+    r = (int)(i / nct);
+    c = (int)(i - (int64_t)r * nct);
+  }
+  const double* a = rs + 8 * r;
+  const double* b = cs + 8 * c;
+  const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
+  const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
+  const double hmn = fmin(a[3], b[3]), hmx = fmax(a[4], b[4]), lmn = fmin(a[5], b[5]), lmx = fmax(a[6], b[6]);
+  const double bh = order_bound_hi(oc, Dmin, hmn, hmx, lmn, lmx);
+  pairs[i] = make_int2(r, c);
+  nearflag[i] = (bh + 1e-9 > (double)(kw - 1)) ? 1 : 0;
+  // heavy first: ascending tile gap (float bits of a non-negative float are monotonic)
+  key[i] = __float_as_uint((float)fmax(Dmin, 0.0));
+}
+
+void build_tile_pairs(const DevMesh& m, const OrderConsts& oc, const Tiles& rows, const Tiles& cols, bool symmetric,
+                      int kw, TilePairs& tp, cudaStream_t st) {
+  (void)m;
+  const int nrt = rows.ntiles, nct = cols.ntiles;
+  const int64_t np = symmetric ? (int64_t)nrt * (nrt + 1) / 2 : (int64_t)nrt * nct;
+  tp.nall = (int)np;
+  tp.all.alloc(std::max<int64_t>(np, 1));
+  tp.near.alloc(std::max<int64_t>(np, 1));
+  tp.nnear = 0;
+  if (np == 0) return;
+  DBuf<int2> raw(np);
+  DBuf<unsigned> key(np), key2(np);
+  DBuf<int> flag(np), flag2(np), nsel(1);
+  tile_pairs_kernel<<<(int)((np + 255) / 256), 256, 0, st>>>(oc, rows.stat.p, cols.stat.p, nrt, nct, symmetric ? 1 : 0,
+                                                              kw, np, raw.p, key.p, flag.p), ::fl::note_launch();
+  FL_CHECK_LAUNCH();
+  // stable radix sort of (key -> pair, flag): deterministic heavy-first order
+  DBuf<int> idx(np), idx2(np);
+  iota_kernel<<<(int)((np + 255) / 256), 256, 0, st>>>(idx.p, (int)np), ::fl::note_launch();
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, key2.p, idx.p, idx2.p, (int)np, 0, 32, st);
+  DBuf<unsigned char> tb(tmp);
+  FL_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, key.p, key2.p, idx.p, idx2.p, (int)np, 0, 32, st));
+  gather_pairs_kernel<<<(int)((np + 255) / 256), 256, 0, st>>>(raw.p, flag.p, idx2.p, (int)np, tp.all.p, flag2.p),
+      ::fl::note_launch();
+  size_t tmp2 = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp2, tp.all.p, flag2.p, tp.near.p, nsel.p, (int)np, st);
+  DBuf<unsigned char> tb2(tmp2);
+  FL_CUDA(cub::DeviceSelect::Flagged(tb2.p, tmp2, tp.all.p, flag2.p, tp.near.p, nsel.p, (int)np, st));
+  FL_CUDA(cudaMemcpyAsync(&tp.nnear, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace fl
