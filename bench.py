@@ -101,6 +101,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def committed_traffic(cfg, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/r01/traffic.json,
+    dram__bytes_read.sum + dram__bytes_write.sum), or None when that kernel was not captured."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")) as f:
+            return json.load(f).get(cfg, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -266,8 +276,11 @@ def main():
     ms_k, ev_k = kern[dom]
     fl_per_eval = ALG_FLOPS[(mesh.d, dom)] + POW_FLOPS.get(e4, 60)
     achieved = ev_k * fl_per_eval / (ms_k * 1e-3) / 1e12 if ms_k > 0 else 0.0
-    roofline = {"bound": "fp64", "kernel": dom + "_kernel", "achieved": achieved, "peak": fp64,
-                "unit": "TFLOP/s", "frac": achieved / fp64 if fp64 else None, "traffic": None,
+    kname = {("tail", 1): "tail1d_kernel", ("tail", 2): "tail_kernel", ("cross", 1): "cross1d_tile_kernel",
+             ("cross", 2): "cross_tile_kernel"}[(dom, mesh.d)]
+    roofline = {"bound": "fp64", "kernel": kname, "achieved": achieved, "peak": fp64,
+                "unit": "TFLOP/s", "frac": achieved / fp64 if fp64 else None,
+                "traffic": committed_traffic(args.config, kname),
                 "peak_source": "fl_probe_fp64_peak (DFMA chains, this run)",
                 "flops_per_eval": fl_per_eval, "evals_per_launch": ev_k, "ms_per_launch": ms_k}
 
@@ -293,6 +306,7 @@ def main():
         dist.all_reduce(mvt, op=dist.ReduceOp.MAX)
     mv_gbs = (8.0 * n * n + 16.0 * n) / (float(mvt.item()) * 1e-3) / 1e9
     matvec = {"gbs": mv_gbs, "ms": float(mvt.item()), "bytes": 8.0 * n * n + 16.0 * n,
+              "traffic": committed_traffic(args.config, "matvec_kernel"),
               "frac_of_measured_copy_peak": mv_gbs / (pk["hbm_gbs"] * world), "peak_source": pk_src}
 
     # CG (Jacobi PCG to 1e-10, solve.py:52-109)
