@@ -43,7 +43,8 @@ CONFIG_TEXT = {
 # per-evaluation algorithmic fp64 FLOPs excluding the power and the
 # executed FLOPs of the specialised power r2^ex (ncu-measured)
 ALG_FLOPS = {(1, "tail"): 4, (1, "cross"): 6, (2, "tail"): 7, (2, "cross"): 11}
-POW_FLOPS = {6: 18, 8: 9, 10: 19, 12: 10, 14: 20, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh
+POW_FLOPS = {6: 18, 8: 9, 10: 19, 12: 10, 14: 20, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh (2D)
+POW_FLOPS_1D = {6: 10, 8: 10, 10: 11, 0: 60}                  # = kpow_abs_flops() (1D far field)
 
 
 def peaks():
@@ -274,7 +275,7 @@ def main():
     kern = {"tail": (stats["ms_tail"], stats["evals_tail"]), "cross": (stats["ms_cross"], stats["evals_cross"])}
     dom = max(kern, key=lambda k: kern[k][0])
     ms_k, ev_k = kern[dom]
-    fl_per_eval = ALG_FLOPS[(mesh.d, dom)] + POW_FLOPS.get(e4, 60)
+    fl_per_eval = ALG_FLOPS[(mesh.d, dom)] + (POW_FLOPS_1D if mesh.d == 1 else POW_FLOPS).get(e4, 60)
     achieved = ev_k * fl_per_eval / (ms_k * 1e-3) / 1e12 if ms_k > 0 else 0.0
     kname = {("tail", 1): "tail1d_kernel", ("tail", 2): "tail_kernel", ("cross", 1): "cross1d_tile_kernel",
              ("cross", 2): "cross_tile_kernel"}[(dom, mesh.d)]

@@ -196,9 +196,10 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
 int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
                             const fl_order_params* params, int32_t device, int64_t* cross_hist,
                             int64_t* tail_hist);
-/* The device's specialised kernel power r2^(-(d/2+s)) on n host values (parity of the
- * building block every quadrature uses). */
-int32_t fl_debug_kpow(int32_t d, double s, const double* r2, int64_t n, double* out, int32_t device);
+/* The device's specialised kernel power on n host values (parity of the building block every
+ * quadrature uses): d = 2: x = r2, out = r2^(-(1+s)); d = 1: x = |x - y| (the 1D far field
+ * works on the distance itself), out = |x - y|^(-(1+2s)). */
+int32_t fl_debug_kpow(int32_t d, double s, const double* x, int64_t n, double* out, int32_t device);
 /* Measured FP64 FMA peak of the device (TFLOP/s), the roofline denominator of assembly. */
 int32_t fl_probe_fp64_peak(int32_t device, double* tflops);
 /* Touching pairs as classify/canonicalize produce them (assembly.py:412-473):

@@ -1112,13 +1112,13 @@ double probe_fp64_tflops(cudaStream_t st) {
 
 namespace fl {
 template <int E4>
-__global__ void kpow_probe_kernel(const double* r2, int64_t n, double ex, double* out) {
+__global__ void kpow_probe_kernel(int d, const double* x, int64_t n, double ex, double* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = kpow<E4>(r2[i], ex);
+  if (i < n) out[i] = d == 1 ? kpow_abs<E4>(x[i], ex) : kpow<E4>(x[i], ex);
 }
-void launch_kpow_probe(int e4, const double* r2, int64_t n, double ex, double* out, cudaStream_t st) {
+void launch_kpow_probe(int d, int e4, const double* x, int64_t n, double ex, double* out, cudaStream_t st) {
   const int grid = (int)((n + 255) / 256);
-  FL_E4_SWITCH(e4, (kpow_probe_kernel<E4><<<grid, 256, 0, st>>>(r2, n, ex, out), ::fl::note_launch()));
+  FL_E4_SWITCH(e4, (kpow_probe_kernel<E4><<<grid, 256, 0, st>>>(d, x, n, ex, out), ::fl::note_launch()));
   FL_CHECK_LAUNCH();
 }
 }  // namespace fl

@@ -213,7 +213,7 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
 void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,
                        cudaStream_t st);
 double probe_fp64_tflops(cudaStream_t st);
-void launch_kpow_probe(int e4, const double* r2, int64_t n, double ex, double* out, cudaStream_t st);
+void launch_kpow_probe(int d, int e4, const double* x, int64_t n, double ex, double* out, cudaStream_t st);
 
 // fl_local.cu
 void launch_cell_local(const DevMesh& m, const DevTables& t, double Cds, double s, bool integral,
