@@ -43,8 +43,8 @@ CONFIG_TEXT = {
 # per-evaluation algorithmic fp64 FLOPs excluding the power and the
 # executed FLOPs of the specialised power r2^ex (ncu-measured)
 ALG_FLOPS = {(1, "tail"): 4, (1, "cross"): 6, (2, "tail"): 7, (2, "cross"): 11}
-POW_FLOPS = {6: 18, 8: 9, 10: 19, 12: 10, 14: 20, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh (2D)
-POW_FLOPS_1D = {6: 10, 8: 10, 10: 11, 0: 60}                  # = kpow_abs_flops() (1D far field)
+POW_FLOPS = {6: 11, 8: 8, 10: 11, 12: 9, 14: 12, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh (2D)
+POW_FLOPS_1D = {6: 9, 8: 9, 10: 10, 0: 60}                  # = kpow_abs_flops() (1D far field)
 
 
 def peaks():
