@@ -322,7 +322,7 @@ constexpr int T1K = 33;      // order buckets (KDIR)
 // relative to off)
 __global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_vertex, int off, int len, int nt,
                                     int* __restrict__ tcnt, int* __restrict__ tcell, int* __restrict__ dslot,
-                                    int* __restrict__ owner, int* __restrict__ maxcnt) {
+                                    int* __restrict__ owner, double* __restrict__ tstat, int* __restrict__ maxcnt) {
   __shared__ int cand[4][2 * T1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 4 + w;
@@ -364,6 +364,33 @@ __global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_verte
     rk[h] = r;
   }
   const int ncand_unique = __reduce_add_sync(0xffffffffu, (c0 != INT_MAX && first[0]) + (c1 != INT_MAX && first[1]));
+  {   // tile statistics for the order bound: x extent of the cells, max h, min / max |ln h|
+    double lo = 1e300, hi = -1e300, hmx = 0.0, lmn = 1e300, lmx = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = h ? c1 : c0;
+      if (c != INT_MAX) {
+        const CellGeo& g = m.geo[c];
+        lo = fmin(lo, fmin(g.p[0][0], g.p[1][0]));
+        hi = fmax(hi, fmax(g.p[0][0], g.p[1][0]));
+        hmx = fmax(hmx, g.diam);
+        lmn = fmin(lmn, g.ldiam);
+        lmx = fmax(lmx, g.ldiam);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      hmx = fmax(hmx, __shfl_xor_sync(0xffffffffu, hmx, o));
+      lmn = fmin(lmn, __shfl_xor_sync(0xffffffffu, lmn, o));
+      lmx = fmax(lmx, __shfl_xor_sync(0xffffffffu, lmx, o));
+    }
+    if (lane == 0) {
+      double* st = tstat + 5 * t;
+      st[0] = lo; st[1] = hi; st[2] = hmx; st[3] = lmn; st[4] = lmx;
+    }
+  }
   if (lane == 0) {
     tcnt[t] = ncand_unique;
     atomicMax(maxcnt, ncand_unique);
@@ -505,8 +532,22 @@ constexpr int T1WARP = 6;    // orders >= this get a warp per pair
 // one DoF tiling (rows or columns): cells per tile, per-DoF (slot << 1 | basis), cell owners
 struct Tiling1D {
   const int *cnt, *cell, *dslot, *owner;
+  const double* stat;    // per tile: x extent (lo, hi) of its cells, max h, min / max |ln h|
   int off, len, nt;
 };
+
+// True when every disjoint cell pair of the two tiles provably has order 2: the gap D between
+// the tiles' x extents bounds every pair distance from below and the disjoint order formula
+// (quadrature.py:159-168) from above (each numerator term bounded above, the denominator below);
+// 1e-9 of margin absorbs rounding, so the reference's ceil() is 2 as well (clip floor).
+__device__ __forceinline__ bool tile_pair_all_k2(const OrderConsts& oc, const double* a, const double* b) {
+  const double D = fmax(b[0] - a[1], a[0] - b[1]);
+  if (!(D > 0.0)) return false;
+  const double hmx = fmax(a[2], b[2]), lmn = fmin(a[3], b[3]), lmx = fmax(a[4], b[4]);
+  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * log(D) + oc.s * log(hmx) - oc.coff;
+  const double den = fmax(log(D / hmx), 0.0) + oc.ln_rho2;
+  return (num > 0.0 ? num / den : 0.0) <= 2.0 - 1e-9;
+}
 
 // RECT = false: the symmetric whole matrix, upper-triangular tile pairs (diagonal-major,
 // heavy first), each off-diagonal tile mirrored.  RECT = true: rows [R.off, R.off + R.len)
@@ -520,7 +561,7 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
                                                            int64_t lda, unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem1d[];
   __shared__ Cell1S cr, cc;
-  __shared__ int bcnt[T1K], boff[T1K + 1], ndefer;
+  __shared__ int bcnt[T1K], boff[T1K + 1], ndefer, uni2;
   __shared__ int rA[T1][2], cB[T1][2];
   __shared__ double tt[T1][T1 + 1];
   const int64_t bx = blockIdx.x;
@@ -559,7 +600,10 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
     }
   }
   if (tid < T1K) bcnt[tid] = 0;
-  if (tid == 0) ndefer = 0;
+  if (tid == 0) {
+    ndefer = 0;
+    uni2 = tile_pair_all_k2(oc, R.stat + 5 * bi, Cn.stat + 5 * bj) ? 1 : 0;
+  }
   if (tid < 2 * T1) {
     // per DoF and patch cell: its part of the M offset (row DoFs: slot row + basis a; column
     // DoFs: slot column + basis b), -1 = no such cell
@@ -571,9 +615,20 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
   }
   __syncthreads();
 
-  // phase 1: every cell pair's order; k = 2 pairs (~95%) get their block right away
+  // phase 1: every cell pair's order; k = 2 pairs (~95%) get their block right away.  Tile pairs
+  // whose pairs are all provably of order 2 (~92% at c2) skip the orders (and have no touching pair)
   unsigned my = 0;
-  for (int p = tid; p < np; p += blockDim.x) {
+  if (uni2) {
+    const double* nd2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
+    for (int p = tid; p < np; p += blockDim.x) {
+      const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
+      const PairGeo1D g = pair_geo1d(cr, a, cc, b);
+      store_block1d(M + 4 * p, block1d_k<2, E4>(nd2, g.px0, g.pe, g.qx0, g.qe, g.JJ, ex), g.kl);
+      const int oK = cr.own[a], oL = cc.own[b];
+      if (g.kl && (RECT ? (oK == bi && oL == bj) : (min(oK, oL) == bi && max(oK, oL) == bj))) my += 4u;
+    }
+  }
+  for (int p = uni2 ? np : tid; p < np; p += blockDim.x) {
     const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
     const int K = cr.id[a], L = cc.id[b];
     const int kv0 = cr.v0[a], kv1 = cr.v1[a], lv0 = cc.v0[b], lv1 = cc.v1[b];
@@ -842,17 +897,19 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
     // fused DoF tiles when every tile's cells fit the shared-memory pair table
     struct TilingBuf {
       DBuf<int> cnt, cell, dslot, owner;
+      DBuf<double> stat;
       int off = 0, len = 0, nt = 0;
-      Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, off, len, nt}; }
+      Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, stat.p, off, len, nt}; }
     };
     DBuf<int> mx(1);
     FL_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), st));
     auto make = [&](TilingBuf& T, int off, int len) {
       T.off = off; T.len = len; T.nt = (len + T1 - 1) / T1;
       T.cnt.alloc(T.nt); T.cell.alloc((size_t)T.nt * T1C); T.dslot.alloc((size_t)2 * len); T.owner.alloc(m.nc);
+      T.stat.alloc((size_t)T.nt * 5);
       FL_CUDA(cudaMemsetAsync(T.owner.p, 0x7f, sizeof(int) * m.nc, st));
       tile1d_cells_kernel<<<(T.nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, off, len, T.nt, T.cnt.p, T.cell.p, T.dslot.p,
-                                                          T.owner.p, mx.p),
+                                                          T.owner.p, T.stat.p, mx.p),
           ::fl::note_launch();
       FL_CHECK_LAUNCH();
     };
