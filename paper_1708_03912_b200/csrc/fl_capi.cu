@@ -127,9 +127,26 @@ void check_inputs(const fl_mesh* mesh, const fl_dofmap* dm, const fl_kernel* k, 
   if (!t->dir || !t->data || t->ndata <= 0) throw Error(FL_E_ARG, "missing quadrature tables");
 }
 
+// grow-only pinned staging area per host thread (one H2D copy per assembly); the copy has
+// completed before the next call on this thread reuses it (every call synchronises its stream)
+unsigned char* pinned_stage(size_t bytes) {
+  thread_local void* p = nullptr;
+  thread_local size_t cap = 0;
+  if (cap < bytes) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = bytes + bytes / 4 + 4096;
+    FL_CUDA(cudaHostAlloc(&p, want, cudaHostAllocDefault));
+    cap = want;
+  }
+  return static_cast<unsigned char*>(p);
+}
+
 struct Uploaded {
-  DBuf<double> vert, bnorm, tab, X, W;
-  DBuf<int> cells, v2d, bedges, patch_off, patch_cells, err;
+  DBuf<unsigned char> blob;           // vertices | normals | tables | cells | v2d | edges
+  DBuf<double> X, W;
+  DBuf<int> patch_off, patch_cells, err, maxv;
   DBuf<CellGeo> geo;
   DevMesh m;
   DevTables t;
@@ -138,8 +155,24 @@ struct Uploaded {
 void upload(const fl_mesh* mesh, const fl_dofmap* dm, const fl_tables* tb, Uploaded& U, cudaStream_t st) {
   const int d = mesh->d;
   const int64_t nv = mesh->nv, nc = mesh->nc, nb = mesh->nb;
-  std::vector<int> hc((size_t)nc * (d + 1)), hv2d(nv), hbe((size_t)std::max<int64_t>(nb, 1) * d);
-  for (size_t i = 0; i < hc.size(); ++i) {
+  // everything goes up in ONE copy from a pinned staging area: doubles first (vertices,
+  // boundary normals, quadrature tables), then the int32 index arrays (cells, vertex->DoF,
+  // boundary edges)
+  const size_t n_vert = (size_t)nv * d, n_bn = (size_t)std::max<int64_t>(nb, 1) * d, n_tab = (size_t)tb->ndata;
+  const size_t n_cells = (size_t)nc * (d + 1), n_v2d = (size_t)nv, n_be = (size_t)std::max<int64_t>(nb, 1) * d;
+  const size_t dbytes = 8 * (n_vert + n_bn + n_tab), ibytes = 4 * (n_cells + n_v2d + n_be);
+  unsigned char* stage = pinned_stage(dbytes + ibytes);
+  double* hvert = reinterpret_cast<double*>(stage);
+  double* hbn = hvert + n_vert;
+  double* htab = hbn + n_bn;
+  int* hc = reinterpret_cast<int*>(stage + dbytes);
+  int* hv2d = hc + n_cells;
+  int* hbe = hv2d + n_v2d;
+  std::memcpy(hvert, mesh->vertices, n_vert * sizeof(double));
+  if (nb > 0) std::memcpy(hbn, mesh->boundary_normals, (size_t)nb * d * sizeof(double));
+  else std::fill(hbn, hbn + n_bn, 0.0);
+  std::memcpy(htab, tb->data, n_tab * sizeof(double));
+  for (size_t i = 0; i < n_cells; ++i) {
     const int64_t c = mesh->cells[i];
     if (c < 0 || c >= nv) throw Error(FL_E_ARG, "cell vertex index out of range");
     hc[i] = (int)c;
@@ -150,48 +183,39 @@ void upload(const fl_mesh* mesh, const fl_dofmap* dm, const fl_tables* tb, Uploa
     maxdof = std::max<int64_t>(maxdof, dm->vertex_to_dof[v]);
   }
   if (maxdof + 1 != dm->n) throw Error(FL_E_ARG, "dofmap.n does not match vertex_to_dof");
-  for (int64_t i = 0; i < nb * d; ++i) hbe[i] = (int)mesh->boundary_edges[i];
-  U.vert.alloc(nv * d);
-  U.cells.alloc(hc.size());
-  U.v2d.alloc(nv);
-  U.bedges.alloc(hbe.size());
-  U.bnorm.alloc(std::max<int64_t>(nb, 1) * d);
-  FL_CUDA(cudaMemcpyAsync(U.vert.p, mesh->vertices, nv * d * sizeof(double), cudaMemcpyHostToDevice, st));
-  FL_CUDA(cudaMemcpyAsync(U.cells.p, hc.data(), hc.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  FL_CUDA(cudaMemcpyAsync(U.v2d.p, hv2d.data(), nv * sizeof(int), cudaMemcpyHostToDevice, st));
-  if (nb > 0) {
-    FL_CUDA(cudaMemcpyAsync(U.bedges.p, hbe.data(), nb * d * sizeof(int), cudaMemcpyHostToDevice, st));
-    FL_CUDA(cudaMemcpyAsync(U.bnorm.p, mesh->boundary_normals, nb * d * sizeof(double), cudaMemcpyHostToDevice, st));
-  }
-  U.tab.alloc(tb->ndata);
-  FL_CUDA(cudaMemcpyAsync(U.tab.p, tb->data, tb->ndata * sizeof(double), cudaMemcpyHostToDevice, st));
+  for (size_t i = 0; i < n_be; ++i) hbe[i] = i < (size_t)nb * d ? (int)mesh->boundary_edges[i] : 0;
+  U.blob.alloc(dbytes + ibytes);
+  FL_CUDA(cudaMemcpyAsync(U.blob.p, stage, dbytes + ibytes, cudaMemcpyHostToDevice, st));
+  const double* dvert = reinterpret_cast<const double*>(U.blob.p);
+  const double* dbn = dvert + n_vert;
+  const double* dtab = dbn + n_bn;
+  const int* dcells = reinterpret_cast<const int*>(U.blob.p + dbytes);
+  const int* dv2d = dcells + n_cells;
+  const int* dbe = dv2d + n_v2d;
   for (int i = 0; i < NTOPO * KDIR; ++i) {
     const int64_t off = tb->dir[2 * i], cnt = tb->dir[2 * i + 1];
     if (cnt < 0 || off < 0 || (off + cnt) * NODE > tb->ndata) throw Error(FL_E_ARG, "corrupt quadrature table");
     U.t.dir[i] = RuleRef{(int)off, (int)cnt};
   }
-  U.t.data = U.tab.p;
+  U.t.data = dtab;
   if (U.t.rule(T_CELL, 0).cnt <= 0) throw Error(FL_E_ARG, "missing cell rule");
   DevMesh& m = U.m;
   m.d = d; m.nv = (int)nv; m.nc = (int)nc; m.nb = (int)nb; m.n = (int)dm->n;
   m.q = U.t.rule(T_CELL, 0).cnt;
   if (m.q != (d == 1 ? 6 : 16)) throw Error(FL_E_ARG, "cell rule must have 6 (1D) / 16 (2D) nodes (XQ_ORDER)");
-  m.vert = U.vert.p; m.cells = U.cells.p; m.v2d = U.v2d.p; m.bedges = U.bedges.p; m.bnorm = U.bnorm.p;
+  m.vert = dvert; m.cells = dcells; m.v2d = dv2d; m.bedges = dbe; m.bnorm = dbn;
   U.err.alloc(1);
   FL_CUDA(cudaMemsetAsync(U.err.p, 0, sizeof(int), st));
   m.err = U.err.p;
-  build_patches((int)nv, (int)nc, d, U.cells.p, U.patch_off, U.patch_cells, st);
+  build_patches((int)nv, (int)nc, d, dcells, U.patch_off, U.patch_cells, st);
   m.patch_off = U.patch_off.p;
   m.patch_cells = U.patch_cells.p;
-  {
-    std::vector<int> po(nv + 1);
-    FL_CUDA(cudaMemcpyAsync(po.data(), U.patch_off.p, (nv + 1) * sizeof(int), cudaMemcpyDeviceToHost, st));
-    FL_CUDA(cudaStreamSynchronize(st));
-    int mv = 0;
-    for (int64_t v = 0; v < nv; ++v) mv = std::max(mv, po[v + 1] - po[v]);
-    if (mv > MAX_VALENCE)
-      throw Error(FL_E_ASSEMBLY, "vertex valence " + std::to_string(mv) + " exceeds " + std::to_string(MAX_VALENCE));
-  }
+  // max vertex valence on the device; checked (check_valence / the size read-back of
+  // fl_assemble_dense) before anything that depends on it is used — every kernel guards its
+  // valence-bounded lists, so a too-high valence fails loudly and never writes out of bounds
+  U.maxv.alloc(1);
+  FL_CUDA(cudaMemsetAsync(U.maxv.p, 0, sizeof(int), st));
+  launch_max_valence(U.patch_off.p, (int)nv, U.maxv.p, st);
   U.geo.alloc(nc);
   launch_prep_cells(m, U.geo.p, st);
   m.geo = U.geo.p;
@@ -200,6 +224,29 @@ void upload(const fl_mesh* mesh, const fl_dofmap* dm, const fl_tables* tb, Uploa
   launch_cell_nodes(m, U.t, U.X.p, U.W.p, st);
   m.X = U.X.p;
   m.W = U.W.p;
+}
+
+void valence_error(int mv) {
+  if (mv > MAX_VALENCE)
+    throw Error(FL_E_ASSEMBLY, "vertex valence " + std::to_string(mv) + " exceeds " + std::to_string(MAX_VALENCE));
+}
+void check_valence(const Uploaded& U, cudaStream_t st) {
+  int mv = 0;
+  FL_CUDA(cudaMemcpyAsync(&mv, U.maxv.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  valence_error(mv);
+}
+
+// small pinned read-back area per host thread (sizes read back together with one sync)
+int* pinned_scratch() {
+  thread_local int* hs = nullptr;
+  if (!hs) FL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hs), 64 * sizeof(int), cudaHostAllocDefault));
+  return hs;
+}
+
+__global__ void zero_pad_kernel(double* A, int64_t rows, int64_t n, int64_t lda) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, w = lda - n;
+  if (i < rows * w) A[(i / w) * lda + n + i % w] = 0.0;
 }
 
 __global__ void flag_target_cells(DevMesh m, int r0, int r1, int* flags) {
@@ -321,19 +368,31 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, all.p, flags.p, targets.p, nsel.p, m.nc, st));
     FL_CHECK_LAUNCH();
   }
-  int ntargets = 0;
-  FL_CUDA(cudaMemcpyAsync(&ntargets, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   DBuf<int> row_vertex(n > 0 ? n : 1);
   dof_vertex2<<<(m.nv + 255) / 256, 256, 0, st>>>(m, row_vertex.p), ::fl::note_launch();
 
-  // classification (quadrature.py:90-110, assembly.py:412-473, :784-841)
+  // classification (quadrature.py:90-110, assembly.py:412-473, :784-841): counts, then one
+  // read-back of every size (targets, touching pairs, boundary items, max valence), then fills
   DBuf<TouchPair> tpairs;
-  DBuf<int> ident_k;
+  DBuf<int> ident_k, tcounts, toffs, bcounts, boffs;
   int64_t npairs = 0, nitems = 0;
-  classify_touching(m, oc, tpairs, npairs, ident_k, st);
-  DBuf<BndPair> bitems;
   const bool do_bnd = integral && m.nb > 0;
-  if (do_bnd) classify_boundary(m, oc, bitems, nitems, st);
+  touching_count(m, tcounts, toffs, st);
+  if (do_bnd) boundary_count(m, bcounts, boffs, st);
+  int* hs = pinned_scratch();
+  hs[2] = 0;
+  FL_CUDA(cudaMemcpyAsync(&hs[0], nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&hs[1], toffs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (do_bnd) FL_CUDA(cudaMemcpyAsync(&hs[2], boffs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&hs[3], U.maxv.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  const int ntargets = hs[0];
+  npairs = hs[1];
+  nitems = hs[2];
+  valence_error(hs[3]);
+  touching_fill(m, oc, toffs, npairs, tpairs, ident_k, st);
+  DBuf<BndPair> bitems;
+  if (do_bnd) boundary_fill(m, oc, boffs, nitems, bitems, st);
   else bitems.alloc(1);
   tm.mark();  // 1
 
@@ -359,22 +418,27 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   // dense rows: cross term tiles, then the local/sparse pull
   D->A.alloc((size_t)std::max<int64_t>(rows, 1) * D->lda);
   D->A.st = D->stream;
-  if (D->lda > n && rows > 0)
-    FL_CUDA(cudaMemset2DAsync(D->A.p + n, D->lda * sizeof(double), 0, (D->lda - n) * sizeof(double), rows, st));
+  if (D->lda > n && rows > 0) {
+    const int64_t padn = (int64_t)rows * (D->lda - n);
+    zero_pad_kernel<<<(unsigned)((padn + 255) / 256), 256, 0, st>>>(D->A.p, rows, n, D->lda), ::fl::note_launch();
+    FL_CHECK_LAUNCH();
+  }
   const bool full = (row_begin == 0 && row_end == n);
   int64_t ntp = 0, nkeys = 0;
   int ntiles = 0;
   DBuf<unsigned long long> near_keys;
   DBuf<unsigned int> near_cnt(1);
   NearPairs near;
-  cudaEvent_t xev[2];
-  cudaEventCreate(&xev[0]);
-  cudaEventCreate(&xev[1]);
-  if (d == 1 && cross1d_fits(m, ntargets, full)) {
+  cudaEvent_t xev[2] = {nullptr, nullptr};
+  bool done1d = false;
+  if (d == 1) {
     tm.mark();  // 5
-    launch_cross1d(m, U.t, oc, ex, e4, C, targets.p, ntargets, row_vertex.p, full, (int)row_begin, (int)row_end,
-                   D->A.p, D->lda, evc.p + 1, st);
-  } else {
+    done1d = launch_cross1d(m, U.t, oc, ex, e4, C, targets.p, ntargets, row_vertex.p, full, (int)row_begin,
+                            (int)row_end, D->A.p, D->lda, evc.p + 1, st);
+  }
+  if (!done1d) {
+    cudaEventCreate(&xev[0]);
+    cudaEventCreate(&xev[1]);
     Tiles trow, tcol;
     build_tiles(m, (int)row_begin, (int)row_end, trow, st);
     if (!full) build_tiles(m, 0, (int)n, tcol, st);
@@ -382,7 +446,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     TilePairs tps;
     build_tile_pairs(m, oc, trow, full ? trow : tcol, full, d == 1 ? KW1D : KW2D, tps, st);
     ntp = tps.nall;
-    tm.mark();  // 5
+    if (d != 1) tm.mark();  // 5 (1D fallback: already marked)
     // pass 1 (discovery): orders of the pairs of the tile pairs that can hold near pairs (order
     // >= KW, by the tile bound); near pairs are recorded.  Near-key list (with halo duplicates):
     // generous, bounded by a quarter of the free memory
@@ -421,11 +485,11 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
                      (int)row_begin, (int)row_end, D->A.p, D->lda, st);
   tm.mark();  // 7
-  unsigned long long hev[2] = {0, 0};
-  int herr = 0;
-  FL_CUDA(cudaMemcpyAsync(hev, evc.p, sizeof(hev), cudaMemcpyDeviceToHost, st));
-  FL_CUDA(cudaMemcpyAsync(&herr, m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  unsigned long long* hev = reinterpret_cast<unsigned long long*>(hs + 8);
+  FL_CUDA(cudaMemcpyAsync(hev, evc.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&hs[4], m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  const int herr = hs[4];
   if (herr & 1) throw Error(FL_E_QUAD, "a quadrature rule for a selected order is missing from the tables");
   if (herr & 4) throw Error(FL_E_CUDA, "internal: a near pair missing from the discovery pass");
 
@@ -457,8 +521,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     cudaEventElapsedTime(&c, xev[1], tm.e[6]);
     S.ms_discover = a; S.ms_near = b; S.ms_cross_compute = c;
   }
-  cudaEventDestroy(xev[0]);
-  cudaEventDestroy(xev[1]);
+  for (auto& e : xev)
+    if (e) cudaEventDestroy(e);
   S.ncolors = ncolors;
   S.ntiles = ntiles;
   *out = D.release();
@@ -682,6 +746,7 @@ int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_k
   fl_tables t{dir.data(), data.data(), (int64_t)data.size()};
   Uploaded U;
   upload(mesh, dofmap, &t, U, st);
+  check_valence(U, st);
   const OrderConsts oc = make_order_consts(*params, mesh->d, kernel->s, dofmap->n);
   const int64_t tot = mesh->nc * mesh->nc;
   DBuf<int8_t> ck(tot), tk(tot);
@@ -711,6 +776,7 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
   fl_tables t{dir.data(), data.data(), (int64_t)data.size()};
   Uploaded U;
   upload(mesh, dofmap, &t, U, st);
+  check_valence(U, st);
   const OrderConsts oc = make_order_consts(*params, mesh->d, kernel->s, dofmap->n);
   DBuf<unsigned long long> h(2 * KDIR);
   FL_CUDA(cudaMemsetAsync(h.p, 0, 2 * KDIR * sizeof(unsigned long long), st));
@@ -774,6 +840,7 @@ int32_t fl_debug_touching(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   fl_tables t{dir.data(), data.data(), (int64_t)data.size()};
   Uploaded U;
   upload(mesh, dofmap, &t, U, st);
+  check_valence(U, st);
   const OrderConsts oc = make_order_consts(*params, mesh->d, kernel->s, dofmap->n);
   DBuf<TouchPair> tp;
   DBuf<int> ik;

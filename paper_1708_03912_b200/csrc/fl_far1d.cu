@@ -884,7 +884,7 @@ bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric) {
   return need < 0.5 * (double)fr;
 }
 
-void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                     const int* targets, int ntargets, const int* dof_vertex, bool symmetric, int row_begin,
                     int row_end, double* A, int64_t lda, unsigned long long* evals, cudaStream_t st) {
   Src1DBuf B;
@@ -937,9 +937,10 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
         ::fl::note_launch();
       });
       FL_CHECK_LAUNCH();
-      return;
+      return true;
     }
   }
+  if (!cross1d_fits(m, ntargets, symmetric)) return false;   // pair buffer too large: caller uses tiles
   if (symmetric) {
     DBuf<double4> G((size_t)std::max<int64_t>((int64_t)m.nc * (m.nc - 1) / 2, 1));
     FL_E4_SWITCH1(e4, (cross1d_pairs_kernel<E4><<<m.nc, 256, 0, st>>>(m, t.data, t, oc, ex, S, G.p, evals),
@@ -962,6 +963,7 @@ void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
         ::fl::note_launch();
     FL_CHECK_LAUNCH();
   }
+  return true;
 }
 
 }  // namespace fl

@@ -120,6 +120,13 @@ void launch_cell_nodes(const DevMesh& m, const DevTables& t, double* X, double* 
 void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf<int>& data,
                    cudaStream_t st);
 int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st);  // returns #colours
+void touching_count(const DevMesh& m, DBuf<int>& counts, DBuf<int>& offs, cudaStream_t st);
+void touching_fill(const DevMesh& m, const OrderConsts& oc, const DBuf<int>& offs, int64_t total,
+                   DBuf<TouchPair>& pairs, DBuf<int>& ident_k, cudaStream_t st);
+void boundary_count(const DevMesh& m, DBuf<int>& counts, DBuf<int>& offs, cudaStream_t st);
+void boundary_fill(const DevMesh& m, const OrderConsts& oc, const DBuf<int>& offs, int64_t total,
+                   DBuf<BndPair>& items, cudaStream_t st);
+void launch_max_valence(const int* off, int nv, int* mx, cudaStream_t st);
 void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>& pairs,
                        int64_t& npairs, DBuf<int>& ident_k, cudaStream_t st);
 void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& items,
@@ -207,7 +214,7 @@ void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_
 void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                    const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st);
 bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric);
-void launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                     const int* targets, int ntargets, const int* dof_vertex, bool symmetric, int row_begin,
                     int row_end, double* A, int64_t lda, unsigned long long* evals, cudaStream_t st);
 void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,

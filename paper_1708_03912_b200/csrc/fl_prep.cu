@@ -111,6 +111,18 @@ __global__ void flat_to_cell_kernel(const int* flat, int m, int dp1, int* cellv)
 }
 
 // mesh.py:114-125: argsort(cells.ravel(), kind="stable") -> per vertex, ascending cell ids.
+__global__ void max_valence_kernel(const int* off, int nv, int* mx) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  int val = v < nv ? off[v + 1] - off[v] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) val = max(val, __shfl_xor_sync(0xffffffffu, val, o));
+  if ((threadIdx.x & 31) == 0 && val > 0) atomicMax(mx, val);
+}
+void launch_max_valence(const int* off, int nv, int* mx, cudaStream_t st) {
+  max_valence_kernel<<<(nv + 255) / 256, 256, 0, st>>>(off, nv, mx), ::fl::note_launch();
+  FL_CHECK_LAUNCH();
+}
+
 void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf<int>& data,
                    cudaStream_t st) {
   const int m = nc * (d + 1);
@@ -293,10 +305,10 @@ __global__ void touch_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, To
   }
 }
 
-void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>& pairs,
-                       int64_t& npairs, DBuf<int>& ident_k, cudaStream_t st) {
+void touching_count(const DevMesh& m, DBuf<int>& counts, DBuf<int>& offs, cudaStream_t st) {
   const int tb = 128, nb = (m.nc + tb - 1) / tb;
-  DBuf<int> counts(m.nc + 1), offs(m.nc + 1);
+  counts.alloc(m.nc + 1);
+  offs.alloc(m.nc + 1);
   FL_CUDA(cudaMemsetAsync(counts.p, 0, (m.nc + 1) * sizeof(int), st));
   if (m.d == 1) touch_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
   else touch_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
@@ -305,15 +317,27 @@ void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>&
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offs.p, m.nc + 1, st);
   DBuf<unsigned char> t(tmp);
   FL_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, counts.p, offs.p, m.nc + 1, st));
-  int total = 0;
-  FL_CUDA(cudaMemcpyAsync(&total, offs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FL_CUDA(cudaStreamSynchronize(st));
-  npairs = total;
+}
+
+void touching_fill(const DevMesh& m, const OrderConsts& oc, const DBuf<int>& offs, int64_t total,
+                   DBuf<TouchPair>& pairs, DBuf<int>& ident_k, cudaStream_t st) {
+  const int tb = 128, nb = (m.nc + tb - 1) / tb;
   pairs.alloc(total > 0 ? total : 1);
   ident_k.alloc(m.nc);
   if (m.d == 1) touch_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p), ::fl::note_launch();
   else touch_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, pairs.p, ident_k.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
+}
+
+void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>& pairs,
+                       int64_t& npairs, DBuf<int>& ident_k, cudaStream_t st) {
+  DBuf<int> counts, offs;
+  touching_count(m, counts, offs, st);
+  int total = 0;
+  FL_CUDA(cudaMemcpyAsync(&total, offs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  npairs = total;
+  touching_fill(m, oc, offs, total, pairs, ident_k, st);
 }
 
 // ---------------------------------------------------------------- boundary pairs
@@ -400,12 +424,10 @@ __global__ void bnd_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, BndP
   }
 }
 
-void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& items,
-                       int64_t& nitems, cudaStream_t st) {
-  nitems = 0;
-  if (m.nb == 0) { items.alloc(1); return; }
+void boundary_count(const DevMesh& m, DBuf<int>& counts, DBuf<int>& offs, cudaStream_t st) {
   const int tb = 64, nb = (m.nb + tb - 1) / tb;
-  DBuf<int> counts(m.nb + 1), offs(m.nb + 1);
+  counts.alloc(m.nb + 1);
+  offs.alloc(m.nb + 1);
   FL_CUDA(cudaMemsetAsync(counts.p, 0, (m.nb + 1) * sizeof(int), st));
   if (m.d == 1) bnd_count_kernel<1><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
   else bnd_count_kernel<2><<<nb, tb, 0, st>>>(m, counts.p), ::fl::note_launch();
@@ -414,14 +436,28 @@ void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& i
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, counts.p, offs.p, m.nb + 1, st);
   DBuf<unsigned char> t(tmp);
   FL_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, counts.p, offs.p, m.nb + 1, st));
-  int total = 0;
-  FL_CUDA(cudaMemcpyAsync(&total, offs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FL_CUDA(cudaStreamSynchronize(st));
-  nitems = total;
+}
+
+void boundary_fill(const DevMesh& m, const OrderConsts& oc, const DBuf<int>& offs, int64_t total,
+                   DBuf<BndPair>& items, cudaStream_t st) {
+  const int tb = 64, nb = (m.nb + tb - 1) / tb;
   items.alloc(total > 0 ? total : 1);
   if (m.d == 1) bnd_fill_kernel<1><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p), ::fl::note_launch();
   else bnd_fill_kernel<2><<<nb, tb, 0, st>>>(m, oc, offs.p, items.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
+}
+
+void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& items,
+                       int64_t& nitems, cudaStream_t st) {
+  nitems = 0;
+  if (m.nb == 0) { items.alloc(1); return; }
+  DBuf<int> counts, offs;
+  boundary_count(m, counts, offs, st);
+  int total = 0;
+  FL_CUDA(cudaMemcpyAsync(&total, offs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  nitems = total;
+  boundary_fill(m, oc, offs, total, items, st);
 }
 
 // ---------------------------------------------------------------- DoF tiles
