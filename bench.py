@@ -327,22 +327,33 @@ def main():
                   "converged": rep["converged"]}
         cg["ms_per_iteration"] = 1e3 * cg["seconds"] / max(cg["iterations"], 1)
 
-    # e2e through the public API with host buffers: assemble_dense -> (n, n) ndarray
+    # e2e through the public API with host buffers: assemble_dense -> (n, n) ndarray (N = 1), or
+    # each rank's row block assemble_dense_device(rows) -> to_host (N > 1); max over ranks
     e2e = None
-    if world == 1 and 8.0 * n * n <= 4e9:     # host copy of A must fit comfortably in pinned RAM
+    if 8.0 * (r1 - r0) * n <= 4e9:     # host copy of the rows must fit comfortably in pinned RAM
         Mh = A._lib.Marshal(mesh, dm, ker, None)
         tdir, tdata, _ = A._tables(mesh, dm, s, None)
         h2d = (Mh.vertices.nbytes + Mh.cells.nbytes + Mh.bedges.nbytes + Mh.bnormals.nbytes + Mh.v2d.nbytes
                + tdir.nbytes + tdata.nbytes)
-        out = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+        out = torch.empty((r1 - r0, n), dtype=torch.float64, pin_memory=True).numpy()
         et = []
         for i in range(max(2, args.steps)):
             flush.fill_(float(i))
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            A.assemble_dense(mesh, dm, ker, n_limit=10 ** 7, out=out)
-            et.append(time.perf_counter() - t0)
-        e2e = {"value": pairs / float(np.median(et)), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+            if world == 1:
+                A.assemble_dense(mesh, dm, ker, n_limit=10 ** 7, out=out)
+            else:
+                ope = A.assemble_dense_device(mesh, dm, ker, rows=(r0, r1), device=local, stream=sptr)
+                ope.to_host(out)
+                ope.free()
+            tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et.append(float(tt.item()))
+        e2e = {"value": pairs / float(np.median(et)), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d * world),
                "d2h_bytes_per_step": int(8 * n * n), "seconds_per_step": float(np.median(et))}
 
     cpu = None
