@@ -33,6 +33,22 @@ def make_mesh(kind, N):
     raise ValueError(kind)
 
 
+def irregular_cases():
+    """(key, s) of the jittered / relabelled meshes in tests/golden/irregular.npz."""
+    path = os.path.join(GOLDEN, "irregular.npz")
+    if not os.path.exists(path):
+        return []
+    G = np.load(path)
+    return [(k, float(G[k + "/s"])) for k in sorted({f.split("/")[0] for f in G.files})]
+
+
+def irregular_mesh(key):
+    """The reference-finished irregular mesh stored in the fixture (vertices, cells, boundary)."""
+    from paper_1708_03912_b200 import mesh as M
+    G = golden("irregular")
+    return M.Mesh(G[key + "/vertices"], G[key + "/cells"], G[key + "/bedges"], G[key + "/bnormals"])
+
+
 def small_cases():
     path = os.path.join(GOLDEN, "small.npz")
     if not os.path.exists(path):

@@ -433,6 +433,68 @@ def t_small():
     save("small", recs)
 
 
+# irregular meshes: jittered + relabelled triangulations of the unit square (through the
+# reference's own _finish_polygon_mesh) and random, shuffled partitions of (-1, 1)
+IRREG = [("jit2d", 6, 0.25, 11), ("jit2d", 8, 0.5, 12), ("jit2d", 7, 0.75, 13),
+         ("rand1d", 40, 0.5, 14), ("rand1d", 33, 0.25, 15)]
+
+
+def irregular_mesh(kind, N, seed):
+    from fraclap import mesh as M
+    rng = np.random.default_rng(seed)
+    if kind == "jit2d":
+        g = np.linspace(0.0, 1.0, N + 1)
+        X, Y = np.meshgrid(g, g, indexing="xy")
+        V = np.stack([X.ravel(), Y.ravel()], axis=1)
+        interior = (V[:, 0] > 0) & (V[:, 0] < 1) & (V[:, 1] > 0) & (V[:, 1] < 1)
+        V[interior] += rng.uniform(-0.25, 0.25, (interior.sum(), 2)) / N
+        tris = []
+        for j in range(N):
+            for i in range(N):
+                sw = j * (N + 1) + i
+                se, nw = sw + 1, sw + N + 1
+                ne = nw + 1
+                tris.append((sw, se, ne) if (i + j) % 2 == 0 else (sw, se, nw))
+                tris.append((sw, ne, nw) if (i + j) % 2 == 0 else (se, ne, nw))
+        T = np.asarray(tris, np.int64)
+        pv = rng.permutation(len(V))                       # relabel vertices and cells
+        inv = np.empty_like(pv)
+        inv[pv] = np.arange(len(pv))
+        V = V[pv]
+        T = inv[T][rng.permutation(len(T))]
+        return M._finish_polygon_mesh(V, T)
+    if kind == "rand1d":
+        x = np.sort(np.concatenate([[-1.0, 1.0], rng.uniform(-1, 1, N - 1)]))
+        pv = rng.permutation(N + 1)
+        inv = np.empty_like(pv)
+        inv[pv] = np.arange(N + 1)
+        cells = inv[np.stack([np.arange(N), np.arange(1, N + 1)], axis=1)][rng.permutation(N)]
+        flip = rng.random(N) < 0.5
+        cells[flip] = cells[flip][:, ::-1]
+        return M.Mesh(x[pv][:, None], cells, np.array([[inv[0]], [inv[N]]]), np.array([[-1.0], [1.0]]))
+    raise ValueError(kind)
+
+
+def t_irregular():
+    from fraclap import mesh as M, assembly as A
+    fp64_variant()
+    recs = {}
+    for kind, N, s, seed in IRREG:
+        tag = "%s_%d_%g" % (kind, N, s)
+        mesh = irregular_mesh(kind, N, seed)
+        dm = M.DofMap(mesh, s)
+        ker = A.FractionalKernel(mesh.d, s)
+        Ad = A.assemble_dense(mesh, dm, ker, n_limit=10 ** 6)
+        b = A.load_vector(mesh, dm, lambda X: np.ones(len(X)))
+        x, rep = solve(Ad, b)
+        rec = dict(A=Ad, b=b, x=x, iters=rep.iterations, vertices=mesh.vertices, cells=mesh.cells,
+                   bedges=mesh.boundary_edges, bnormals=mesh.boundary_normals, s=s)
+        for k, v in rec.items():
+            recs[tag + "/" + k] = v
+        print(tag, "n=%d" % dm.n, "iters=%d" % rep.iterations, flush=True)
+    save("irregular", recs)
+
+
 def t_cfg(name, unmodified=False, full=False):
     kind, N, s = CONFIGS[name]
     from fraclap import mesh as M
@@ -469,6 +531,7 @@ TARGETS = {
     "tables": t_tables,
     "meshes": t_meshes,
     "small": t_small,
+    "irregular": t_irregular,
     "c1": lambda: t_cfg("c1", full=True),
     "c2": lambda: t_cfg("c2"),
     "c3": lambda: t_cfg("c3"),

@@ -5,7 +5,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import golden, make_mesh, small_cases
+from conftest import golden, irregular_cases, irregular_mesh, make_mesh, small_cases
 from oracle import fraclap_oracle as O
 
 
@@ -107,3 +107,18 @@ def test_normalisation_known_answers():
         assert normalisation(int(d), s) == c
     with pytest.raises(ValueError):
         normalisation(1, 1.0)
+
+
+@pytest.mark.parametrize("key,s", irregular_cases())
+def test_oracle_irregular_meshes(key, s):
+    """Jittered + relabelled 2D triangulations and shuffled random 1D partitions (the reference's
+    own _finish_polygon_mesh orientation): full A, b and the CG solution."""
+    from paper_1708_03912_b200 import mesh as M
+    G = golden("irregular")
+    mesh = irregular_mesh(key)
+    dm = M.DofMap(mesh, s)
+    A = O.assemble_dense(mesh, dm, s)
+    Ar = G[key + "/A"]
+    assert np.abs(A - Ar).max() <= 1e-13 * np.abs(Ar).max()
+    b = O.load_vector(mesh, dm)
+    assert np.allclose(b, G[key + "/b"], rtol=1e-14, atol=1e-16)
