@@ -91,7 +91,7 @@ __device__ __forceinline__ void tail1d_source(const double* __restrict__ tab, co
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
       const double d = xq[q] - y;
-      acc[q] = fma(jw, kpow_abs<E4>(fabs(d), ex), acc[q]);
+      acc[q] = fma(jw, kpow_abs<E4>(d, ex), acc[q]);
     }
   }
 }
@@ -153,9 +153,9 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const double d0 = xq[q] - y0;
-        acc[q] = fma(j0, kpow_abs<E4>(fabs(d0), ex), acc[q]);
+        acc[q] = fma(j0, kpow_abs<E4>(d0, ex), acc[q]);
         const double d1 = xq[q] - y1;
-        acc[q] = fma(j1, kpow_abs<E4>(fabs(d1), ex), acc[q]);
+        acc[q] = fma(j1, kpow_abs<E4>(d1, ex), acc[q]);
       }
       nodes += 2;
     }
@@ -227,7 +227,7 @@ __device__ __forceinline__ double4 block1d(const double* __restrict__ tab, RuleR
     for (int y = 0; y < rr.cnt; ++y) {
       const double* ny = tab + (size_t)(rr.off + y) * NODE;
       const double d = X - (lx0 + ny[0] * le);
-      const double v = kpow_abs<E4>(fabs(d), ex);
+      const double v = kpow_abs<E4>(d, ex);
       t0 = fma(v, ny[3], t0);
       t1 = fma(v, ny[4], t1);
     }
@@ -429,7 +429,7 @@ __device__ __forceinline__ double4 block1d_k(const double* __restrict__ nd, doub
 #pragma unroll
     for (int y = 0; y < KK; ++y) {
       const double d = X - Y[y];
-      const double v = kpow_abs<E4>(fabs(d), ex);
+      const double v = kpow_abs<E4>(d, ex);
       t0 = fma(v, w0[y], t0);
       t1 = fma(v, w1[y], t1);
     }
@@ -510,7 +510,7 @@ __device__ __forceinline__ double4 block1d_warp(const double* __restrict__ tab, 
     for (int y = 0; y < rr.cnt; ++y) {
       const double* ny = tab + (size_t)(rr.off + y) * NODE;
       const double d = X - (lx0 + ny[0] * le);
-      const double v = kpow_abs<E4>(fabs(d), ex);
+      const double v = kpow_abs<E4>(d, ex);
       t0 = fma(v, ny[3], t0);
       t1 = fma(v, ny[4], t1);
     }
