@@ -33,6 +33,19 @@ def make_mesh(kind, N):
     raise ValueError(kind)
 
 
+def tiny_cases():
+    """(key, kind, N, s) of tests/golden/tiny.npz: n = 1, 2, ... and non-specialised s."""
+    path = os.path.join(GOLDEN, "tiny.npz")
+    if not os.path.exists(path):
+        return []
+    keys = sorted({k.split("/")[0] for k in np.load(path).files})
+    out = []
+    for key in keys:
+        kind, N, s = key.rsplit("_", 2)
+        out.append((key, kind, int(N), float(s)))
+    return out
+
+
 def irregular_cases():
     """(key, s) of the jittered / relabelled meshes in tests/golden/irregular.npz."""
     path = os.path.join(GOLDEN, "irregular.npz")

@@ -495,6 +495,22 @@ def t_irregular():
     save("irregular", recs)
 
 
+# tiny meshes (n = 1, 2, ...) and exponents outside the specialised s in {1/4, 1/2, 3/4}
+TINY = [("uniform1d", 2, 0.75), ("uniform1d", 3, 0.5), ("graded1d", 5, 0.3), ("uniform1d", 20, 0.6),
+        ("square2d", 2, 0.25), ("square2d", 2, 0.75), ("square2d", 4, 0.3), ("square2d", 3, 0.6)]
+
+
+def t_tiny():
+    recs = {}
+    for kind, N, s in TINY:
+        tag = "%s_%d_%g" % (kind, N, s)
+        rec, Ad = dense_case(kind, N, s, full=True)
+        for k, v in rec.items():
+            recs[tag + "/" + k] = v
+        print(tag, "n=%d" % rec["n"], "iters=%d" % rec["iters"], flush=True)
+    save("tiny", recs)
+
+
 def t_cfg(name, unmodified=False, full=False):
     kind, N, s = CONFIGS[name]
     from fraclap import mesh as M
@@ -532,6 +548,7 @@ TARGETS = {
     "meshes": t_meshes,
     "small": t_small,
     "irregular": t_irregular,
+    "tiny": t_tiny,
     "c1": lambda: t_cfg("c1", full=True),
     "c2": lambda: t_cfg("c2"),
     "c3": lambda: t_cfg("c3"),

@@ -5,7 +5,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from conftest import golden, irregular_cases, irregular_mesh, make_mesh, small_cases
+from conftest import golden, irregular_cases, irregular_mesh, make_mesh, small_cases, tiny_cases
 from oracle import fraclap_oracle as O
 
 
@@ -122,3 +122,16 @@ def test_oracle_irregular_meshes(key, s):
     assert np.abs(A - Ar).max() <= 1e-13 * np.abs(Ar).max()
     b = O.load_vector(mesh, dm)
     assert np.allclose(b, G[key + "/b"], rtol=1e-14, atol=1e-16)
+
+
+@pytest.mark.parametrize("key,kind,N,s", tiny_cases())
+def test_oracle_tiny_and_generic_s(key, kind, N, s):
+    """n = 1, 2 meshes and exponents outside {1/4, 1/2, 3/4} (the generic-power path)."""
+    from paper_1708_03912_b200 import mesh as M
+    G = golden("tiny")
+    mesh = make_mesh(kind, N)
+    dm = M.DofMap(mesh, s)
+    A = O.assemble_dense(mesh, dm, s)
+    Ar = G[key + "/A"]
+    assert A.shape == Ar.shape
+    assert np.abs(A - Ar).max() <= 1e-13 * np.abs(Ar).max()
