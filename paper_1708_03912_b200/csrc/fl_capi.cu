@@ -450,11 +450,10 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
     // pass 1 (discovery): orders of the pairs of the tile pairs that can hold near pairs (order
     // >= KW, by the tile bound); near pairs are recorded.  Near-key list (with halo duplicates):
     // generous, bounded by a quarter of the free memory
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
+    // capacity: the exact bound from the tile pairs (a pair is scanned once per tile pair holding
+    // it), capped; a rare overflow grows the list and rediscovers
     unsigned int cap = (unsigned int)std::max<int64_t>(
-        1024, std::min<int64_t>({(int64_t)m.nc * 4096, (int64_t)(fr / 4 / sizeof(unsigned long long)),
-                                 ((int64_t)1 << 31) - 1}));
+        1024, std::min<int64_t>({tps.near_candidates, (int64_t)m.nc * 4096, ((int64_t)1 << 31) - 1}));
     for (int attempt = 0; attempt < 2; ++attempt) {
       near_keys.alloc(cap);
       FL_CUDA(cudaMemsetAsync(near_cnt.p, 0, sizeof(unsigned int), st));

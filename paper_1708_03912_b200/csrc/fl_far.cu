@@ -201,9 +201,9 @@ struct CrossShared {
   int ntr, ntc;
   // order inputs staged per tile (rows) / per column sub-block (columns): centroid, radius,
   // fp32 ln h and |ln h| (2D fast order path)
-  double rcx[TILE_MAXC], rcy[TILE_MAXC], rrad[TILE_MAXC];
+  double rcx[TILE_MAXC], rcy[TILE_MAXC], rrad[TILE_MAXC], rJ[TILE_MAXC];
   float rlnh[TILE_MAXC], rlh[TILE_MAXC];
-  double ccx[SBC], ccy[SBC], crad[SBC];
+  double ccx[SBC], ccy[SBC], crad[SBC], cJ[SBC];
   float clnh[SBC], clh[SBC];
   // phase-B chunks of far pairs of one order: a warp takes 32 / L pairs, L lanes per pair
   short chs[SBP / 4 + 8];
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
       for (int a = 0; a < 3; ++a) S.rslot[i][a] = (signed char)R.slots[(tr * TILE_MAXC + i) * 3 + a];
       if (D == 2) {
         const CellGeo& g = m.geo[c];
-        S.rcx[i] = g.cx; S.rcy[i] = g.cy; S.rrad[i] = g.rad;
+        S.rcx[i] = g.cx; S.rcy[i] = g.cy; S.rrad[i] = g.rad; S.rJ[i] = g.J;
         S.rlnh[i] = __logf((float)g.diam); S.rlh[i] = (float)g.ldiam;
       }
     }
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
       if (D == 2 && tid >= 32 && tid < 32 + SBC && cs0 + tid - 32 < nC) {
         const int i = tid - 32;
         const CellGeo& g = m.geo[S.colc[cs0 + i]];
-        S.ccx[i] = g.cx; S.ccy[i] = g.cy; S.crad[i] = g.rad;
+        S.ccx[i] = g.cx; S.ccy[i] = g.cy; S.crad[i] = g.rad; S.cJ[i] = g.J;
         S.clnh[i] = __logf((float)g.diam); S.clh[i] = (float)g.ldiam;
       }
       if (tid >= 64 && tid < 64 + TILE) {   // tile column -> its (column cell, slot) entries here
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
           const double* rt = rtab + 5 * S.kofs[k];
           if (k == 2) {                       // one lane per pair, fully unrolled
             if (act) {
-              const double JJ = m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
+              const double JJ = D == 2 ? S.rJ[rs0 + r] * S.cJ[c] : m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
               cross_fixed<D, E4, 2>(&S.nodes[r][pre_off<D>(2)], &S.nodes[SBR + c][pre_off<D>(2)], rt, JJ, ex, S.Gs[p]);
               my_evals += (unsigned long long)nn * nn;
             }
@@ -815,7 +815,7 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
               Gm[a][b] = v;
             }
           if (act && sub == 0) {
-            const double JJ = m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
+            const double JJ = D == 2 ? S.rJ[rs0 + r] * S.cJ[c] : m.geo[S.rowc[rs0 + r]].J * m.geo[S.colc[cs0 + c]].J;
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -873,6 +873,9 @@ __global__ void __launch_bounds__(XT, 2) cross_tile_kernel(DevMesh m, const doub
   }
 }
 
+// two CTAs per SM (2 x 113.5 KB of the 228 KB) must fit for the 2D tiles
+static_assert(((sizeof(CrossShared) + 15) / 16) * 16 + sizeof(double) * 5 * (9 * 10 * 19 / 6 - 1) <= 113 * 1024,
+              "cross_tile_kernel shared memory exceeds two CTAs per SM");
 size_t cross_smem_bytes(int d) {
   const int nodes = (d == 1) ? (32 * 33 / 2 - 1) : (9 * 10 * 19 / 6 - 1);   // sum_{k=2}^{kmax} k^d
   return ((sizeof(CrossShared) + 15) / 16) * 16 + sizeof(double) * 5 * nodes;

@@ -152,6 +152,7 @@ struct Tiles {
 struct TilePairs {
   DBuf<int2> all, near;
   int nall = 0, nnear = 0;
+  int64_t near_candidates = 0;   // sum of nR * nC over `near`: bound of the discovery's near keys
 };
 void build_tile_pairs(const DevMesh& m, const OrderConsts& oc, const Tiles& rows, const Tiles& cols, bool symmetric,
                       int kw, TilePairs& tp, cudaStream_t st);

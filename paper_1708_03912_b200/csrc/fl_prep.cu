@@ -664,6 +664,15 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   if (herr) throw Error(-2, "DoF tile touches more than 256 cells (vertex valence too high)");
 }
 
+__global__ void pair_cells_kernel(const int2* pairs, const int* n, const int* rcnt, const int* ccnt,
+                                  unsigned long long* sum) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (i < *n) v = (unsigned long long)rcnt[pairs[i].x] * (unsigned long long)ccnt[pairs[i].y];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(sum, v);
+}
 __global__ void gather_pairs_kernel(const int2* raw, const int* flag, const int* idx, int n, int2* out, int* oflag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) { out[i] = raw[idx[i]]; oflag[i] = flag[idx[i]]; }
@@ -740,8 +749,17 @@ void build_tile_pairs(const DevMesh& m, const OrderConsts& oc, const Tiles& rows
   cub::DeviceSelect::Flagged(nullptr, tmp2, tp.all.p, flag2.p, tp.near.p, nsel.p, (int)np, st);
   DBuf<unsigned char> tb2(tmp2);
   FL_CUDA(cub::DeviceSelect::Flagged(tb2.p, tmp2, tp.all.p, flag2.p, tp.near.p, nsel.p, (int)np, st));
+  // upper bound of the near keys the discovery pass can emit: sum of nR * nC over its tile pairs
+  DBuf<unsigned long long> cand(1);
+  FL_CUDA(cudaMemsetAsync(cand.p, 0, sizeof(unsigned long long), st));
+  pair_cells_kernel<<<(int)((np + 255) / 256), 256, 0, st>>>(tp.near.p, nsel.p, rows.ncell.p, cols.ncell.p, cand.p),
+      ::fl::note_launch();
+  FL_CHECK_LAUNCH();
+  unsigned long long hc = 0;
   FL_CUDA(cudaMemcpyAsync(&tp.nnear, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&hc, cand.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  tp.near_candidates = (int64_t)hc;
 }
 
 }  // namespace fl
