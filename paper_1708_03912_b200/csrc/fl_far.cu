@@ -23,11 +23,17 @@ namespace fl {
 // ====================================================================== tail Psi_K
 constexpr int TAIL_WARPS = 4;
 constexpr int TAIL_WIN = 256;
-constexpr int TAIL_U = 4;   // source nodes per lane per step
-constexpr int TAIL_T = 2;   // target nodes per lane
+#ifndef FL_TAIL_U
+#define FL_TAIL_U 4
+#endif
+#ifndef FL_TAIL_MINB
+#define FL_TAIL_MINB 5
+#endif
+constexpr int TAIL_U = FL_TAIL_U;   // source nodes per lane per step
+constexpr int TAIL_T = 2;           // target nodes per lane
 
 template <int D, int E4>
-__global__ void __launch_bounds__(TAIL_WARPS * 32, 4) tail_kernel(DevMesh m, const double* __restrict__ tab,
+__global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(DevMesh m, const double* __restrict__ tab,
                                                                   DevTables dir, OrderConsts oc, double ex,
                                                                   const int* __restrict__ targets, int ntargets,
                                                                   double* __restrict__ psi,
