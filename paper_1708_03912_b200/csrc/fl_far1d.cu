@@ -25,6 +25,9 @@
 #ifndef FL_TAIL1D_MINB
 #define FL_TAIL1D_MINB 4     // resident 128-thread CTAs per SM the tail is compiled for
 #endif
+#ifndef FL_TAIL1D_NT
+#define FL_TAIL1D_NT 1       // target cells per warp in the 1D tail (2 measured slower: registers)
+#endif
 #ifndef FL_TILE1D_MINB
 #define FL_TILE1D_MINB 3     // resident 256-thread CTAs per SM of the fused cross tiles
 #endif
@@ -96,34 +99,47 @@ __device__ __forceinline__ void tail1d_source(const double* __restrict__ tab, co
   }
 }
 
-// Warp per target cell, lane per source cell.  Sources of order 2 (~80%) are evaluated inline
-// with the two rule nodes in registers; the others are compacted (ballot, deterministic order)
-// into a per-warp queue and evaluated 32 at a time, so a warp's lanes share one code path.
-template <int E4>
+// Warp per NT target cells (NT = 2 by default), lane per source cell.  The source record, its two
+// order-2 nodes and weights are shared by the NT targets; sources of order 2 for a target (~80%)
+// are evaluated inline with the rule in registers, the others are compacted (ballot,
+// deterministic order) into that target's per-warp queue and evaluated 32 at a time.  Per target
+// the accumulation order is the same as with one target per warp.
+template <int E4, int NT>
 __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                      OrderConsts oc, double ex, Src1D S,
                                                      const int* __restrict__ targets, int ntargets,
                                                      double* __restrict__ psi,
                                                      unsigned long long* __restrict__ evals) {
   constexpr int Q = 6;
-  __shared__ int qs[4][64], qk[4][64];
+  __shared__ int qs[4][NT][64], qk[4][NT][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int ti = blockIdx.x * (blockDim.x >> 5) + w;
-  if (ti >= ntargets) return;
-  const int K = targets[ti];
-  const double alo = S.lo[K], ahi = S.hi[K], ah = S.h[K], alh = S.lh[K];
-  const float alnf = S.lnhf[K], alhf = S.lhf[K];
-  const int av0 = S.v0[K], av1 = S.v1[K];
-  double xq[Q], acc[Q];
+  const int wi = blockIdx.x * (blockDim.x >> 5) + w;
+  if (wi * NT >= ntargets) return;
+  int K[NT], av0[NT], av1[NT];
+  bool valid[NT];
+  double alo[NT], ahi[NT], ah[NT], alh[NT];
+  float alnf[NT], alhf[NT];
+  double xq[NT][Q], acc[NT][Q];
 #pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    xq[q] = m.X[(size_t)K * Q + q];
-    acc[q] = 0.0;
+  for (int t = 0; t < NT; ++t) {
+    const int ti = wi * NT + t;
+    valid[t] = ti < ntargets;
+    K[t] = targets[valid[t] ? ti : wi * NT];
+    alo[t] = S.lo[K[t]]; ahi[t] = S.hi[K[t]]; ah[t] = S.h[K[t]]; alh[t] = S.lh[K[t]];
+    alnf[t] = S.lnhf[K[t]]; alhf[t] = S.lhf[K[t]];
+    av0[t] = S.v0[K[t]]; av1[t] = S.v1[K[t]];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      xq[t][q] = m.X[(size_t)K[t] * Q + q];
+      acc[t][q] = 0.0;
+    }
   }
   const double* n2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
   const double t0 = n2[0], w0 = n2[2], t1 = n2[NODE], w1 = n2[NODE + 2];
-  unsigned nodes = 0;
-  int qn = 0;                                   // warp-uniform queue length
+  unsigned nodes[NT];
+  int qn[NT];                                   // warp-uniform queue lengths
+#pragma unroll
+  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; }
   const unsigned lt = (1u << lane) - 1u;
   const int4* R = reinterpret_cast<const int4*>(S.rec);
   int4 na = make_int4(0, 0, 0, 0), nb = na;     // prefetched record of the next source
@@ -134,80 +150,84 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
     if (s + 32 < m.nc) { na = __ldg(R + 2 * (s + 32)); nb = __ldg(R + 2 * (s + 32) + 1); }
     const double sx0 = __hiloint2double(ra.y, ra.x), sx1 = __hiloint2double(ra.w, ra.z);
     const int bv0 = rb.x, bv1 = rb.y;
-    int k = -1;                                 // -1: not a tail source
-    double x0 = 0.0, e = 0.0, J = 0.0;
-    if (s < m.nc && !(s == K || bv0 == av0 || bv0 == av1 || bv1 == av0 || bv1 == av1)) {   // N(K) (:999-1009)
-      const double blo = fmin(sx0, sx1), bhi = fmax(sx0, sx1);
-      const double dist = fmax(fmax(__dsub_rn(blo, ahi), __dsub_rn(alo, bhi)), 0.0);   // (:750-752)
-      k = 0;
-      if (dist > 1e-30)
-        k = order_from_estimate(order_estimate_f(oc, oc.coff_tail_f, alnf, alhf, __int_as_float(rb.z),
-                                                 __int_as_float(rb.w), __logf((float)dist)), oc.cap_disjoint);
-      x0 = sx0;
-      e = sx1 - sx0;
-      J = fabs(e);
-    }
-    if (k == 2) {
-      const double y0 = x0 + t0 * e, y1 = x0 + t1 * e;
-      const double j0 = J * w0, j1 = J * w1;
+    const double blo = fmin(sx0, sx1), bhi = fmax(sx0, sx1);
+    const double e = sx1 - sx0, J = fabs(e);
+    const double y0 = sx0 + t0 * e, y1 = sx0 + t1 * e;
+    const double j0 = J * w0, j1 = J * w1;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const double d0 = xq[q] - y0;
-        acc[q] = fma(j0, kpow_abs<E4>(d0, ex), acc[q]);
-        const double d1 = xq[q] - y1;
-        acc[q] = fma(j1, kpow_abs<E4>(d1, ex), acc[q]);
+    for (int t = 0; t < NT; ++t) {
+      int k = -1;                               // -1: not a tail source of target t
+      if (s < m.nc && !(s == K[t] || bv0 == av0[t] || bv0 == av1[t] || bv1 == av0[t] || bv1 == av1[t])) {  // N(K) (:999-1009)
+        const double dist = fmax(fmax(__dsub_rn(blo, ahi[t]), __dsub_rn(alo[t], bhi)), 0.0);   // (:750-752)
+        k = 0;
+        if (dist > 1e-30)
+          k = order_from_estimate(order_estimate_f(oc, oc.coff_tail_f, alnf[t], alhf[t], __int_as_float(rb.z),
+                                                   __int_as_float(rb.w), __logf((float)dist)), oc.cap_disjoint);
       }
-      nodes += 2;
-    }
-    const bool dq = k == 0 || k > 2;
-    const unsigned bm = __ballot_sync(0xffffffffu, dq);
-    if (dq) {
-      const int pos = qn + __popc(bm & lt);
-      qs[w][pos] = s;
-      qk[w][pos] = k;
-    }
-    qn += __popc(bm);
-    if (qn >= 32) {
-      __syncwarp();
-      const int ss = qs[w][lane];
-      int kk = qk[w][lane];
-      const double sx0 = S.x0[ss], sJ = S.h[ss];
-      if (!kk) {
-        const double dist = fmax(fmax(__dsub_rn(S.lo[ss], ahi), __dsub_rn(alo, S.hi[ss])), 0.0);
-        kk = order_exact1d(oc, oc.coff_tail, ah, alh, sJ, S.lh[ss], dist);
+      if (k == 2) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const double d0 = xq[t][q] - y0;
+          acc[t][q] = fma(j0, kpow_abs<E4>(d0, ex), acc[t][q]);
+          const double d1 = xq[t][q] - y1;
+          acc[t][q] = fma(j1, kpow_abs<E4>(d1, ex), acc[t][q]);
+        }
+        nodes[t] += 2;
       }
-      tail1d_source<E4>(tab, dir, ex, xq, acc, sx0, S.x1[ss] - sx0, sJ, kk);
-      nodes += kk;
-      __syncwarp();
-      if (lane < qn - 32) {
-        qs[w][lane] = qs[w][32 + lane];
-        qk[w][lane] = qk[w][32 + lane];
+      const bool dq = k == 0 || k > 2;
+      const unsigned bm = __ballot_sync(0xffffffffu, dq);
+      if (dq) {
+        const int pos = qn[t] + __popc(bm & lt);
+        qs[w][t][pos] = s;
+        qk[w][t][pos] = k;
       }
-      __syncwarp();
-      qn -= 32;
+      qn[t] += __popc(bm);
+      if (qn[t] >= 32) {
+        __syncwarp();
+        const int ss = qs[w][t][lane];
+        int kk = qk[w][t][lane];
+        const double qx0 = S.x0[ss], qJ = S.h[ss];
+        if (!kk) {
+          const double dist = fmax(fmax(__dsub_rn(S.lo[ss], ahi[t]), __dsub_rn(alo[t], S.hi[ss])), 0.0);
+          kk = order_exact1d(oc, oc.coff_tail, ah[t], alh[t], qJ, S.lh[ss], dist);
+        }
+        tail1d_source<E4>(tab, dir, ex, xq[t], acc[t], qx0, S.x1[ss] - qx0, qJ, kk);
+        nodes[t] += kk;
+        __syncwarp();
+        if (lane < qn[t] - 32) {
+          qs[w][t][lane] = qs[w][t][32 + lane];
+          qk[w][t][lane] = qk[w][t][32 + lane];
+        }
+        __syncwarp();
+        qn[t] -= 32;
+      }
     }
   }
   __syncwarp();
-  if (lane < qn) {
-    const int ss = qs[w][lane];
-    int kk = qk[w][lane];
-    const double sx0 = S.x0[ss], sJ = S.h[ss];
-    if (!kk) {
-      const double dist = fmax(fmax(__dsub_rn(S.lo[ss], ahi), __dsub_rn(alo, S.hi[ss])), 0.0);
-      kk = order_exact1d(oc, oc.coff_tail, ah, alh, sJ, S.lh[ss], dist);
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    if (lane < qn[t]) {
+      const int ss = qs[w][t][lane];
+      int kk = qk[w][t][lane];
+      const double qx0 = S.x0[ss], qJ = S.h[ss];
+      if (!kk) {
+        const double dist = fmax(fmax(__dsub_rn(S.lo[ss], ahi[t]), __dsub_rn(alo[t], S.hi[ss])), 0.0);
+        kk = order_exact1d(oc, oc.coff_tail, ah[t], alh[t], qJ, S.lh[ss], dist);
+      }
+      tail1d_source<E4>(tab, dir, ex, xq[t], acc[t], qx0, S.x1[ss] - qx0, qJ, kk);
+      nodes[t] += kk;
     }
-    tail1d_source<E4>(tab, dir, ex, xq, acc, sx0, S.x1[ss] - sx0, sJ, kk);
-    nodes += kk;
-  }
 #pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const double v = warp_sum(acc[q]);
-    if (lane == 0) psi[(size_t)K * Q + q] = v;
-  }
-  if (evals) {
+    for (int q = 0; q < Q; ++q) {
+      const double v = warp_sum(acc[t][q]);
+      if (lane == 0 && valid[t]) psi[(size_t)K[t] * Q + q] = v;
+    }
+    if (evals && valid[t]) {
+      unsigned long long nd = nodes[t];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nodes += __shfl_xor_sync(0xffffffffu, nodes, o);
-    if (lane == 0) atomicAdd(evals, (unsigned long long)nodes * Q);
+      for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
+      if (lane == 0) atomicAdd(evals, nd * Q);
+    }
   }
 }
 
@@ -871,8 +891,10 @@ void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, 
   Src1DBuf B;
   build_src1d(m, B, st);
   const Src1D S = B.view();
-  const int grid = (ntargets + 3) / 4;
-  FL_E4_SWITCH1(e4, (tail1d_kernel<E4><<<grid, 128, 0, st>>>(m, t.data, t, oc, ex, S, targets, ntargets, psi, evals),
+  constexpr int NT = FL_TAIL1D_NT;
+  const int grid = (ntargets + 4 * NT - 1) / (4 * NT);
+  FL_E4_SWITCH1(e4, (tail1d_kernel<E4, NT><<<grid, 128, 0, st>>>(m, t.data, t, oc, ex, S, targets, ntargets, psi,
+                                                                 evals),
                      ::fl::note_launch()));
   FL_CHECK_LAUNCH();
 }
