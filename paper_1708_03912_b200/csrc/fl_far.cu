@@ -181,7 +181,7 @@ constexpr int KPRE = 3;                 // node coordinates precomputed per sub-
 constexpr int NPRE = 4 + 9;             // sum_{k=2}^{KPRE} k^2 (2D; 1D uses the first 5)
 
 struct TileView {
-  const int* dofs; const int* ncell; const int* cells; const int* slots; const int* cstart;
+  const int* dofs; const int* ncell; const int* cells; const int* slots;
 };
 
 struct CrossShared {
@@ -998,8 +998,8 @@ void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts&
                         unsigned int near_cap, int discover, const unsigned long long* nearH, const int* nearI,
                         unsigned long long hmask, const double* nearG, cudaStream_t st) {
   if (ntp <= 0) return;
-  TileView R{rows.dofs.p, rows.ncell.p, rows.cells.p, rows.slots.p, rows.cstart.p};
-  TileView C{cols.dofs.p, cols.ncell.p, cols.cells.p, cols.slots.p, cols.cstart.p};
+  TileView R{rows.dofs.p, rows.ncell.p, rows.cells.p, rows.slots.p};
+  TileView C{cols.dofs.p, cols.ncell.p, cols.cells.p, cols.slots.p};
   const size_t smem = cross_smem_bytes(m.d);
   const double negC = -Cds;   // (C/2) * (-2)  (assembly.py:723, :1100)
   const int kmax = oc.cap_disjoint;

@@ -119,7 +119,6 @@ void launch_prep_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st);
 void launch_cell_nodes(const DevMesh& m, const DevTables& t, double* X, double* W, cudaStream_t st);
 void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf<int>& data,
                    cudaStream_t st);
-int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st);  // returns #colours
 void touching_count(const DevMesh& m, DBuf<int>& counts, DBuf<int>& offs, cudaStream_t st);
 void touching_fill(const DevMesh& m, const OrderConsts& oc, const DBuf<int>& offs, int64_t total,
                    DBuf<TouchPair>& pairs, DBuf<int>& ident_k, cudaStream_t st);
@@ -131,7 +130,7 @@ void classify_touching(const DevMesh& m, const OrderConsts& oc, DBuf<TouchPair>&
                        int64_t& npairs, DBuf<int>& ident_k, cudaStream_t st);
 void classify_boundary(const DevMesh& m, const OrderConsts& oc, DBuf<BndPair>& items,
                        int64_t& nitems, cudaStream_t st);
-// DoF tiles of TILE dofs in Morton order; per tile the sorted (colour, id) list of cells that
+// DoF tiles of TILE dofs in Morton order; per tile the sorted id list of cells that
 // touch one of its DoFs, with the tile-local slot of each cell vertex.
 constexpr int TILE = 64;
 constexpr int TILE_MAXC = 256;
@@ -142,7 +141,6 @@ struct Tiles {
   DBuf<int> ncell;    // ntiles
   DBuf<int> cells;    // ntiles*TILE_MAXC
   DBuf<int> slots;    // ntiles*TILE_MAXC*3 (-1: vertex not a DoF of this tile)
-  DBuf<int> cstart;   // ntiles*(maxcolors+1): colour class ranges in the cell list
   DBuf<double> geo3;  // ntiles*3: centre (x, y) and radius of the tile's DoF vertices
   DBuf<double> stat;  // ntiles*8: centre (x, y), R = max |c_K - centre| + rad_K, h min/max, |ln h| min/max
 };
@@ -156,7 +154,6 @@ struct TilePairs {
 };
 void build_tile_pairs(const DevMesh& m, const OrderConsts& oc, const Tiles& rows, const Tiles& cols, bool symmetric,
                       int kw, TilePairs& tp, cudaStream_t st);
-constexpr int MAXCOLORS = 32;
 void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& t, cudaStream_t st);
 
 // fl_singular.cu

@@ -1,5 +1,5 @@
 // Mesh preparation on the device: per-cell geometry, cell quadrature nodes, vertex patches,
-// vertex-disjoint colouring, touching-pair / boundary-pair classification and the DoF tiles
+// touching-pair / boundary-pair classification and the DoF tiles
 // of the cross kernel.
 //
 // Reference: mesh.py:76-130 (diameters, patches), assembly.py:282-298 (cell rule),
@@ -51,7 +51,6 @@ __global__ void prep_cells_kernel(DevMesh m, CellGeo* geo) {
     g.rad = r;                                                 // :773
   }
   g.ldiam = fabs(log(g.diam));
-  g.color = -1;
   g.pad = 0;
   geo[c] = g;
 }
@@ -139,76 +138,6 @@ void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf
   patch_offsets_kernel<<<(m + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p), ::fl::note_launch();
   flat_to_cell_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx_out.p, m, d + 1, data.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
-}
-
-// ---------------------------------------------------------------- colouring
-// Jones-Plassmann with a fixed hash priority and double-buffered colours: deterministic.
-__device__ __forceinline__ uint32_t prio(uint32_t c) {
-  uint32_t h = c * 0x9E3779B1u;
-  h ^= h >> 15; h *= 0x85EBCA77u; h ^= h >> 13; h *= 0xC2B2AE3Du; h ^= h >> 16;
-  return h;
-}
-template <int D>
-__global__ void jp_round_kernel(DevMesh m, const int* col_in, int* col_out, int* remaining, int* overflow) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= m.nc) return;
-  const int cur = col_in[c];
-  col_out[c] = cur;
-  if (cur >= 0) return;
-  const uint32_t pc = prio(c);
-  uint32_t used = 0;
-  bool is_max = true;
-  for (int i = 0; i <= D && is_max; ++i) {
-    const int v = m.cells[c * (D + 1) + i];
-    for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
-      const int o = m.patch_cells[p];
-      if (o == c) continue;
-      const int co = col_in[o];
-      if (co >= 0) {
-        if (co < 32) used |= 1u << co;
-      } else {
-        const uint32_t po = prio(o);
-        if (po > pc || (po == pc && o > c)) { is_max = false; break; }
-      }
-    }
-  }
-  if (!is_max) { atomicAdd(remaining, 1); return; }
-  const int color = __ffs(~used) - 1;
-  if (color < 0 || color >= MAXCOLORS) { atomicAdd(overflow, 1); return; }
-  col_out[c] = color;
-}
-__global__ void fill_kernel(int* a, int n, int v) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] = v;
-}
-__global__ void store_colors_kernel(CellGeo* geo, const int* col, int nc, int* maxc) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nc) return;
-  geo[c].color = col[c];
-  atomicMax(maxc, col[c]);
-}
-
-int color_cells(const DevMesh& m, CellGeo* geo, cudaStream_t st) {
-  DBuf<int> a(m.nc), b(m.nc), cnt(3);
-  const int tb = 256, nb = (m.nc + tb - 1) / tb;
-  fill_kernel<<<nb, tb, 0, st>>>(a.p, m.nc, -1), ::fl::note_launch();
-  int h[3];
-  for (int round = 0; round < 10000; ++round) {
-    FL_CUDA(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(int), st));
-    if (m.d == 1) jp_round_kernel<1><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1), ::fl::note_launch();
-    else jp_round_kernel<2><<<nb, tb, 0, st>>>(m, a.p, b.p, cnt.p, cnt.p + 1), ::fl::note_launch();
-    FL_CHECK_LAUNCH();
-    FL_CUDA(cudaMemcpyAsync(h, cnt.p, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    FL_CUDA(cudaStreamSynchronize(st));
-    std::swap(a.p, b.p);
-    if (h[1]) throw Error(-2, "cell colouring needs more than 32 colours (vertex valence too high)");
-    if (h[0] == 0) break;
-  }
-  FL_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
-  store_colors_kernel<<<nb, tb, 0, st>>>(geo, a.p, m.nc, cnt.p), ::fl::note_launch();
-  FL_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FL_CUDA(cudaStreamSynchronize(st));
-  return h[0] + 1;
 }
 
 // ---------------------------------------------------------------- touching pairs
@@ -497,7 +426,7 @@ __global__ void morton_kernel(DevMesh m, const int* dof_vertex, int r0, int r1, 
 constexpr int CAND = 1024;
 __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* sorted_dofs, int nrows,
                                                          const int* dof_vertex, int* tdofs, int* tncell,
-                                                         int* tcells, int* tslots, int* tcstart, double* tgeo,
+                                                         int* tcells, int* tslots, double* tgeo,
                                                          double* tstat, int* err) {
   const int t = blockIdx.x;
   __shared__ int sd[TILE];
@@ -538,7 +467,7 @@ __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* s
     for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
       const int c = m.patch_cells[p];
       const int slot = atomicAdd(&ncand, 1);
-      if (slot < CAND) key[slot] = ((unsigned long long)(unsigned)m.geo[c].color << 32) | (unsigned)c;
+      if (slot < CAND) key[slot] = (unsigned long long)(unsigned)c;
     }
   }
   __syncthreads();
@@ -546,7 +475,7 @@ __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* s
   if (nc_ > CAND) { if (tid == 0) atomicAdd(err, 1); return; }
   for (int i = nc_ + tid; i < CAND; i += blockDim.x) key[i] = ~0ull;
   __syncthreads();
-  // bitonic sort of CAND keys (colour, cell id)
+  // bitonic sort of the CAND candidate cell ids
   for (int k = 2; k <= CAND; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int i = tid; i < CAND; i += blockDim.x) {
@@ -611,12 +540,6 @@ __global__ void __launch_bounds__(256) tile_cells_kernel(DevMesh m, const int* s
       st[5] = -red[3][0]; st[6] = red[4][0]; st[7] = 0.0;
     }
   }
-  // colour class starts
-  for (int col = tid; col <= MAXCOLORS; col += blockDim.x) {
-    int lo = 0;
-    while (lo < nu && (int)(key[lo] >> 32) < col) ++lo;
-    tcstart[t * (MAXCOLORS + 1) + col] = lo;
-  }
 }
 
 void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStream_t st) {
@@ -649,13 +572,12 @@ void build_tiles(const DevMesh& m, int row_begin, int row_end, Tiles& T, cudaStr
   T.ncell.alloc(T.ntiles);
   T.cells.alloc((size_t)T.ntiles * TILE_MAXC);
   T.slots.alloc((size_t)T.ntiles * TILE_MAXC * 3);
-  T.cstart.alloc((size_t)T.ntiles * (MAXCOLORS + 1));
   T.geo3.alloc((size_t)T.ntiles * 3);
   T.stat.alloc((size_t)T.ntiles * 8);
   DBuf<int> err(1);
   FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
   tile_cells_kernel<<<T.ntiles, 256, 0, st>>>(m, vals2.p, nrows, dof_vertex.p, T.dofs.p, T.ncell.p,
-                                              T.cells.p, T.slots.p, T.cstart.p, T.geo3.p, T.stat.p, err.p),
+                                              T.cells.p, T.slots.p, T.geo3.p, T.stat.p, err.p),
       ::fl::note_launch();
   FL_CHECK_LAUNCH();
   int herr = 0;
