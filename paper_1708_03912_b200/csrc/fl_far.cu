@@ -167,9 +167,6 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
 }
 
 // ====================================================================== cross tiles
-#ifndef FL_FIXED3
-#define FL_FIXED3 0
-#endif
 #ifndef FL_PERSISTENT
 #define FL_PERSISTENT 1
 #endif
@@ -284,46 +281,6 @@ __device__ __forceinline__ void cross_fixed(const double2* __restrict__ Xn, cons
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int b = 0; b < 3; ++b) out[a * 3 + b] = (a <= D && b <= D) ? Gm[a < D + 1 ? a : 0][b < D + 1 ? b : 0] * JJ : 0.0;
-}
-
-// precomputed nodes, runtime k (k <= KPRE)
-template <int D, int E4>
-__device__ __forceinline__ void cross_pre(const double2* __restrict__ Xn, const double2* __restrict__ Yn,
-                                          const double* __restrict__ rt, int nn, double JJ, double ex,
-                                          double* __restrict__ out) {
-  double Gm[3][3] = {};
-  for (int i = 0; i < nn; ++i) {
-    const double2 X = Xn[i];
-    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-#pragma unroll 2
-    for (int j = 0; j < nn; ++j) {
-      const double2 Y = Yn[j];
-      const double d0 = X.x - Y.x;
-      double r2;
-      if (D == 1) {
-        r2 = d0 * d0;
-      } else {
-        const double d1 = X.y - Y.y;
-        r2 = fma(d1, d1, d0 * d0);
-      }
-      const double v = kpow<E4>(r2, ex);
-      const double* ny = rt + 5 * j;
-      t0 = fma(v, ny[2], t0);
-      t1 = fma(v, ny[3], t1);
-      if (D == 2) t2 = fma(v, ny[4], t2);
-    }
-    const double* nx = rt + 5 * i;
-#pragma unroll
-    for (int a = 0; a <= D; ++a) {
-      Gm[a][0] = fma(nx[2 + a], t0, Gm[a][0]);
-      Gm[a][1] = fma(nx[2 + a], t1, Gm[a][1]);
-      if (D == 2) Gm[a][2] = fma(nx[2 + a], t2, Gm[a][2]);
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 3; ++b) out[a * 3 + b] = Gm[a][b] * JJ;
 }
 
 // on-the-fly mapping (any k); `lanes` = 32 (warp-cooperative over x nodes) or 1 (one thread)
