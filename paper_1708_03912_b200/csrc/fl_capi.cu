@@ -3,7 +3,9 @@
 // assembly phases of assemble_dense (assembly.py:1059-1104) on one stream.
 #include <algorithm>
 #include <chrono>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -39,6 +41,32 @@ void init_pool(int device) {
 }
 }  // namespace fl
 
+namespace fl {
+// Recycled non-blocking streams per device (an operator's own stream, the side stream of an
+// assembly): creating a stream costs more than the small phases of a 1D assembly.
+std::mutex g_stream_mu;
+std::map<int, std::vector<cudaStream_t>> g_stream_pool;
+cudaStream_t acquire_stream(int device) {
+  {
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    auto& v = g_stream_pool[device];
+    if (!v.empty()) {
+      cudaStream_t s = v.back();
+      v.pop_back();
+      return s;
+    }
+  }
+  cudaStream_t s = nullptr;
+  FL_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+void release_stream(int device, cudaStream_t s) {   // pending stream-ordered work stays ordered
+  if (!s) return;
+  std::lock_guard<std::mutex> lk(g_stream_mu);
+  g_stream_pool[device].push_back(s);
+}
+}  // namespace fl
+
 struct fl_dense {
   int device = 0;
   int64_t n = 0, row0 = 0, row1 = 0, lda = 0;
@@ -48,7 +76,7 @@ struct fl_dense {
   fl_assembly_stats stats{};
   ~fl_dense() {
     A.free();
-    if (own_stream && stream) cudaStreamDestroy(stream);
+    if (own_stream && stream) fl::release_stream(device, stream);
   }
 };
 
@@ -337,7 +365,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   D->row1 = row_end;
   D->lda = ((n + 31) / 32) * 32;
   init_pool(device);
-  FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));   // the operator's own stream
+  D->stream = acquire_stream(device);                                      // the operator's own stream
   D->own_stream = true;
   cudaStream_t st = stream ? (cudaStream_t)stream : D->stream;             // the assembly's stream
   StreamScope scope(st);
@@ -395,6 +423,31 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   if (do_bnd) boundary_fill(m, oc, boffs, nitems, bitems, st);
   else bitems.alloc(1);
   tm.mark();  // 1
+  // the CSR indexes of the local pull depend only on the classification: built on a side stream
+  // while the main stream runs the singular / tail / cross kernels, joined before the pull.
+  // (SparseIndex is destroyed after the final synchronisation, so its stream-ordered frees on
+  // the side stream cannot overtake the pull.)
+  struct SideStream {                  // returned to the pool after everything declared later
+    int dev; cudaStream_t s; cudaEvent_t e[2] = {nullptr, nullptr};
+    explicit SideStream(int d) : dev(d), s(acquire_stream(d)) {
+      for (auto& x : e) FL_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    ~SideStream() {
+      for (auto& x : e)
+        if (x) cudaEventDestroy(x);
+      release_stream(dev, s);
+    }
+  } sides(device);
+  SparseIndex si;
+  cudaStream_t side = sides.s;
+  cudaEvent_t ev_cls = sides.e[0], ev_si = sides.e[1];
+  FL_CUDA(cudaEventRecord(ev_cls, st));
+  FL_CUDA(cudaStreamWaitEvent(side, ev_cls, 0));
+  {
+    StreamScope sc(side);
+    build_sparse_index(m, tpairs.p, npairs, bitems.p, nitems, si, side);
+  }
+  FL_CUDA(cudaEventRecord(ev_si, side));
 
   // singular pairs
   DBuf<double> ident((size_t)m.nc * 9), tloc((size_t)std::max<int64_t>(npairs, 1) * 25),
@@ -479,8 +532,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   tm.mark();  // 6
   DBuf<double> Lc((size_t)m.nc * 9);
   launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
-  SparseIndex si;
-  build_sparse_index(m, tpairs.p, npairs, bitems.p, nitems, si, st);
+  FL_CUDA(cudaStreamWaitEvent(st, ev_si, 0));
   launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
                      (int)row_begin, (int)row_end, D->A.p, D->lda, st);
   tm.mark();  // 7
@@ -541,7 +593,7 @@ int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense*
   D->row1 = n;
   D->lda = ((n + 31) / 32) * 32;
   init_pool(device);
-  FL_CUDA(cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking));
+  D->stream = acquire_stream(device);
   D->own_stream = true;
   StreamScope scope(D->stream);
   D->A.alloc((size_t)n * D->lda);
