@@ -308,14 +308,19 @@ struct OwnedStream {          // destroyed after every buffer declared later in 
 };
 
 struct Timer {
-  cudaEvent_t e[12];
+  cudaEvent_t* e;                      // per host thread and device, created once (calls are synchronous)
   int k = 0;
   cudaStream_t st;
   explicit Timer(cudaStream_t s) : st(s) {
-    for (auto& x : e) cudaEventCreate(&x);
-  }
-  ~Timer() {
-    for (auto& x : e) cudaEventDestroy(x);
+    thread_local std::map<int, std::vector<cudaEvent_t>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto& v = cache[dev];
+    if (v.empty()) {
+      v.resize(12);
+      for (auto& x : v) cudaEventCreate(&x);
+    }
+    e = v.data();
   }
   // FRACLAP_TRACE=1: host-side timestamps of every mark (to find host gaps between launches)
   std::chrono::steady_clock::time_point h0 = std::chrono::steady_clock::now(), hm[16];
