@@ -332,8 +332,13 @@ __device__ __forceinline__ double comp(const double4& g, int a, int b) {
 // into shared memory and sums them into the tile in the same canonical order as gather1d.
 // Cell pairs are bucketed by order inside the CTA so every warp evaluates 32 pairs of one
 // order with the rule nodes in registers (no divergence, fully unrolled for k <= 6).
-constexpr int T1 = 32;       // DoFs per tile side
-constexpr int T1C = 40;      // max cells behind one DoF tile on the fused path
+#ifndef FL_T1
+#define FL_T1 32         // 64 measured slower (one 512-thread CTA per SM)
+#endif
+constexpr int T1 = FL_T1;                     // DoFs per tile side (32 or 64)
+constexpr int T1C = T1 + 8;                   // max cells behind one DoF tile on the fused path
+constexpr int T1X = T1 == 64 ? 512 : 256;     // threads of a tile CTA
+constexpr int T1B = T1 == 64 ? 1 : FL_TILE1D_MINB;   // resident tile CTAs per SM
 constexpr int T1K = 33;      // order buckets (KDIR)
 
 // one warp per DoF tile: sorted unique cells of the patches of its DoFs; per DoF the
@@ -343,61 +348,79 @@ constexpr int T1K = 33;      // order buckets (KDIR)
 __global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_vertex, int off, int len, int nt,
                                     int* __restrict__ tcnt, int* __restrict__ tcell, int* __restrict__ dslot,
                                     int* __restrict__ owner, double* __restrict__ tstat, int* __restrict__ maxcnt) {
-  __shared__ int cand[4][2 * T1];
+  constexpr int DPL = T1 / 32;                  // DoFs per lane
+  constexpr int NCAND = 2 * T1;                 // candidate position q = (u * 2 + h) * 32 + lane
+  __shared__ int cand[4][NCAND];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 4 + w;
   if (t >= nt) return;
-  const int li = t * T1 + lane;
-  int c0 = INT_MAX, c1 = INT_MAX, vi = -1, np = 0;
-  if (li < len) {
-    vi = dof_vertex[off + li];
-    const int b = m.patch_off[vi];
-    np = m.patch_off[vi + 1] - b;
-    if (np > 0) c0 = m.patch_cells[b];
-    if (np > 1) c1 = m.patch_cells[b + 1];
+  int c[DPL][2], vi[DPL];
+  bool anyover = false;
+#pragma unroll
+  for (int u = 0; u < DPL; ++u) {
+    const int li = t * T1 + u * 32 + lane;
+    c[u][0] = c[u][1] = INT_MAX;
+    vi[u] = -1;
+    if (li < len) {
+      vi[u] = dof_vertex[off + li];
+      const int b = m.patch_off[vi[u]];
+      const int np = m.patch_off[vi[u] + 1] - b;
+      if (np > 0) c[u][0] = m.patch_cells[b];
+      if (np > 1) c[u][1] = m.patch_cells[b + 1];
+      anyover |= np > 2;
+    }
   }
-  if (__any_sync(0xffffffffu, np > 2)) {        // not an interval mesh patch: no fused path
+  if (__any_sync(0xffffffffu, anyover)) {       // not an interval mesh patch: no fused path
     if (lane == 0) atomicMax(maxcnt, 1 << 20);
     return;
   }
-  cand[w][lane] = c0;
-  cand[w][32 + lane] = c1;
+#pragma unroll
+  for (int u = 0; u < DPL; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) cand[w][(u * 2 + h) * 32 + lane] = c[u][h];
   __syncwarp();
-  // first occurrence flags, then unique rank = number of distinct values below
-  int first[2], rk[2];
+  // first occurrence flags (per 32-candidate group), then unique rank = distinct values below
+  bool first[DPL][2];
+  unsigned fm[2 * DPL];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int v = h ? c1 : c0, me = h * 32 + lane;
-    int f = 1;
-    for (int q = 0; q < me; ++q) f &= (cand[w][q] != v);
-    first[h] = f;
-  }
-  const unsigned f0 = __ballot_sync(0xffffffffu, first[0]), f1 = __ballot_sync(0xffffffffu, first[1]);
+  for (int u = 0; u < DPL; ++u)
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int v = h ? c1 : c0;
-    int r = 0;
-    for (int q = 0; q < 2 * T1; ++q) {
-      const bool fq = q < 32 ? ((f0 >> q) & 1u) : ((f1 >> (q - 32)) & 1u);
-      r += (fq && cand[w][q] < v);
+    for (int h = 0; h < 2; ++h) {
+      const int v = c[u][h], me = (u * 2 + h) * 32 + lane;
+      bool f = true;
+      for (int q = 0; q < me; ++q) f = f && (cand[w][q] != v);
+      first[u][h] = f;
+      fm[u * 2 + h] = __ballot_sync(0xffffffffu, f);
     }
-    rk[h] = r;
-  }
-  const int ncand_unique = __reduce_add_sync(0xffffffffu, (c0 != INT_MAX && first[0]) + (c1 != INT_MAX && first[1]));
+  int rk[DPL][2];
+  int nuniq = 0;
+#pragma unroll
+  for (int u = 0; u < DPL; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int v = c[u][h];
+      int r = 0;
+      for (int q = 0; q < NCAND; ++q) r += (((fm[q >> 5] >> (q & 31)) & 1u) && cand[w][q] < v);
+      rk[u][h] = r;
+      nuniq += (v != INT_MAX && first[u][h]);
+    }
+  const int ncand_unique = __reduce_add_sync(0xffffffffu, nuniq);
   {   // tile statistics for the order bound: x extent of the cells, max h, min / max |ln h|
     double lo = 1e300, hi = -1e300, hmx = 0.0, lmn = 1e300, lmx = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = h ? c1 : c0;
-      if (c != INT_MAX) {
-        const CellGeo& g = m.geo[c];
-        lo = fmin(lo, fmin(g.p[0][0], g.p[1][0]));
-        hi = fmax(hi, fmax(g.p[0][0], g.p[1][0]));
-        hmx = fmax(hmx, g.diam);
-        lmn = fmin(lmn, g.ldiam);
-        lmx = fmax(lmx, g.ldiam);
+    for (int u = 0; u < DPL; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = c[u][h];
+        if (cc != INT_MAX) {
+          const CellGeo& g = m.geo[cc];
+          lo = fmin(lo, fmin(g.p[0][0], g.p[1][0]));
+          hi = fmax(hi, fmax(g.p[0][0], g.p[1][0]));
+          hmx = fmax(hmx, g.diam);
+          lmn = fmin(lmn, g.ldiam);
+          lmx = fmax(lmx, g.ldiam);
+        }
       }
-    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -417,16 +440,19 @@ __global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_verte
   }
   if (ncand_unique > T1C) return;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = h ? c1 : c0;
-    if (c != INT_MAX && first[h]) {
-      tcell[(size_t)t * T1C + rk[h]] = c;
-      atomicMin(&owner[c], t);
+  for (int u = 0; u < DPL; ++u) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (c[u][h] != INT_MAX && first[u][h]) {
+        tcell[(size_t)t * T1C + rk[u][h]] = c[u][h];
+        atomicMin(&owner[c[u][h]], t);
+      }
+    const int li = t * T1 + u * 32 + lane;
+    if (li < len) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        dslot[2 * li + h] = c[u][h] != INT_MAX ? (rk[u][h] << 1 | (m.cells[2 * c[u][h]] == vi[u] ? 0 : 1)) : -1;
     }
-  }
-  if (li < len) {
-    dslot[2 * li] = c0 != INT_MAX ? (rk[0] << 1 | (m.cells[2 * c0] == vi ? 0 : 1)) : -1;
-    dslot[2 * li + 1] = c1 != INT_MAX ? (rk[1] << 1 | (m.cells[2 * c1] == vi ? 0 : 1)) : -1;
   }
 }
 
@@ -575,7 +601,7 @@ __device__ __forceinline__ bool tile_pair_all_k2(const OrderConsts& oc, const do
 // bitwise the same entries: the pair blocks are computed in the reference orientation and
 // summed in gather1d's canonical order.
 template <int E4, bool RECT>
-__global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
+__global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                            OrderConsts oc, double ex, Src1D S, Tiling1D R,
                                                            Tiling1D Cn, int mc, double negC, double* __restrict__ A,
                                                            int64_t lda, unsigned long long* __restrict__ evals) {
@@ -583,7 +609,6 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
   __shared__ Cell1S cr, cc;
   __shared__ int bcnt[T1K], boff[T1K + 1], ndefer, uni2;
   __shared__ int rA[T1][2], cB[T1][2];
-  __shared__ double tt[T1][T1 + 1];
   const int64_t bx = blockIdx.x;
   int bi, bj;
   if (RECT) {
@@ -627,7 +652,7 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
   if (tid < 2 * T1) {
     // per DoF and patch cell: its part of the M offset (row DoFs: slot row + basis a; column
     // DoFs: slot column + basis b), -1 = no such cell
-    const int h = tid >> 5, a = tid & 31;
+    const int h = tid / T1, a = tid % T1;
     const int li = bi * T1 + a, lj = bj * T1 + a;
     const int si = li < R.len ? R.dslot[2 * li + h] : -1, sj = lj < Cn.len ? Cn.dslot[2 * lj + h] : -1;
     rA[a][h] = si < 0 ? -1 : 4 * (si >> 1) * ncl + 2 * (si & 1);
@@ -736,12 +761,11 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
 
   // phase 3: A[i][j] = -C sum_{K in P(p)} sum_{L in P(q)} M, p = min(i, j), q = max(i, j)
   // (gather1d's canonical order; touching / identical pairs hold zeros, which add nothing)
-  const int tx = lane;
-  constexpr int RPT = T1 / 8;
-  double v[RPT];
+  constexpr int EPT = T1 * T1 / T1X;            // entries per thread
+  double v[EPT];
 #pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int rr_ = warp + 8 * q;
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = tid + q * T1X, rr_ = idx / T1, tx = idx % T1;
     const int i = R.off + bi * T1 + rr_, j = Cn.off + bj * T1 + tx;
     const int o0 = rA[rr_][0], o1 = rA[rr_][1], i0 = cB[tx][0], i1 = cB[tx][1];
     double x = 0.0;
@@ -759,10 +783,9 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
     v[q] = x;
   }
 #pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int rr_ = warp + 8 * q;
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = tid + q * T1X, rr_ = idx / T1, tx = idx % T1;
     const int li = bi * T1 + rr_, lj = bj * T1 + tx;
-    if (!RECT) tt[rr_][tx] = v[q];
     if (li < R.len && lj < Cn.len) A[(int64_t)(RECT ? li : R.off + li) * lda + Cn.off + lj] = v[q];
   }
   if (evals) {
@@ -771,12 +794,20 @@ __global__ void __launch_bounds__(256, FL_TILE1D_MINB) cross1d_tile_kernel(DevMe
     if (lane == 0 && my) atomicAdd(evals, (unsigned long long)my);
   }
   if (RECT || bi == bj) return;
+  // mirror through shared memory (reusing the pair-block buffer once every entry is read)
+  __syncthreads();
+  double* tt = M;                                // [T1][T1 + 1]
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = tid + q * T1X, rr_ = idx / T1, tx = idx % T1;
+    tt[rr_ * (T1 + 1) + tx] = v[q];
+  }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int rr_ = warp + 8 * q;
+  for (int q = 0; q < EPT; ++q) {
+    const int idx = tid + q * T1X, rr_ = idx / T1, tx = idx % T1;
     const int lj = bj * T1 + rr_, li = bi * T1 + tx;       // A[j][i] = tt[i][j]
-    if (li < R.len && lj < Cn.len) A[(int64_t)lj * lda + li] = tt[tx][rr_];
+    if (li < R.len && lj < Cn.len) A[(int64_t)lj * lda + li] = tt[tx * (T1 + 1) + rr_];
   }
 }
 
@@ -943,18 +974,19 @@ bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
     FL_CUDA(cudaStreamSynchronize(st));
     if (mc <= T1C) {
       mc = std::max(mc, 1);
-      const size_t smem = (sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc;
+      const size_t smem = std::max((sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc,
+                                   sizeof(double) * (size_t)T1 * (T1 + 1));   // tt aliases the blocks
       const Tiling1D cv = TC.view(), rv = symmetric ? cv : TR.view();
       const int64_t ntp = symmetric ? (int64_t)cv.nt * (cv.nt + 1) / 2 : (int64_t)rv.nt * cv.nt;
       FL_E4_SWITCH1(e4, {
         if (symmetric) {
           auto kern = cross1d_tile_kernel<E4, false>;
           FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          kern<<<(unsigned)ntp, 256, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+          kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
         } else {
           auto kern = cross1d_tile_kernel<E4, true>;
           FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          kern<<<(unsigned)ntp, 256, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+          kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
         }
         ::fl::note_launch();
       });
