@@ -410,24 +410,45 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   DBuf<int> ident_k, tcounts, toffs, bcounts, boffs;
   int64_t npairs = 0, nitems = 0;
   const bool do_bnd = integral && m.nb > 0;
+  // 1D: the far-field mesh data (source records, DoF tilings) is built here too, and the tail —
+  // which needs nothing the host has to know — is enqueued before the host waits for the sizes,
+  // so the host-side work below overlaps the tail instead of leaving the GPU idle
+  const bool early_tail = d == 1;
+  std::unique_ptr<Plan1D, void (*)(Plan1D*)> P1(nullptr, plan1d_free);
+  if (early_tail) P1.reset(plan1d_create(m, row_vertex.p, row_begin == 0 && row_end == n, (int)row_begin,
+                                         (int)row_end, st));
   touching_count(m, tcounts, toffs, st);
   if (do_bnd) boundary_count(m, bcounts, boffs, st);
   int* hs = pinned_scratch();
   hs[2] = 0;
+  hs[5] = 0;
   FL_CUDA(cudaMemcpyAsync(&hs[0], nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[1], toffs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (do_bnd) FL_CUDA(cudaMemcpyAsync(&hs[2], boffs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[3], U.maxv.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FL_CUDA(cudaStreamSynchronize(st));
+  if (early_tail) FL_CUDA(cudaMemcpyAsync(&hs[5], plan1d_maxcells(P1.get()), sizeof(int), cudaMemcpyDeviceToHost, st));
+  cudaEvent_t ev_sizes = tm.e[11];                 // (the last timing event doubles as the size fence)
+  FL_CUDA(cudaEventRecord(ev_sizes, st));
+  DBuf<unsigned long long> evc(2);
+  FL_CUDA(cudaMemsetAsync(evc.p, 0, 2 * sizeof(unsigned long long), st));
+  DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
+  FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
+  if (early_tail) {
+    tm.mark();  // 1
+    launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, st);
+    tm.mark();  // 2
+  }
+  FL_CUDA(cudaEventSynchronize(ev_sizes));
   const int ntargets = hs[0];
   npairs = hs[1];
   nitems = hs[2];
   valence_error(hs[3]);
+  const int maxcells1d = hs[5];
   touching_fill(m, oc, toffs, npairs, tpairs, ident_k, st);
   DBuf<BndPair> bitems;
   if (do_bnd) boundary_fill(m, oc, boffs, nitems, bitems, st);
   else bitems.alloc(1);
-  tm.mark();  // 1
+  if (!early_tail) tm.mark();  // 1
   // the CSR indexes of the local pull depend only on the classification: built on a side stream
   // while the main stream runs the singular / tail / cross kernels, joined before the pull.
   // (SparseIndex is destroyed after the final synchronisation, so its stream-ordered frees on
@@ -460,15 +481,11 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   launch_singular_identical(m, U.t, ex, e4, ident_k.p, ident.p, st);
   launch_singular_touching(m, U.t, ex, e4, tpairs.p, npairs, tloc.p, st);
   if (do_bnd) launch_singular_boundary(m, U.t, ex, e4, bitems.p, nitems, bloc.p, st);
-  tm.mark();  // 2
-
-  // tail + flux at the nodes of the target cells
-  DBuf<unsigned long long> evc(2);
-  FL_CUDA(cudaMemsetAsync(evc.p, 0, 2 * sizeof(unsigned long long), st));
-  DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
-  FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
-  if (d == 1) launch_tail1d(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
-  else launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+  if (!early_tail) {
+    tm.mark();  // 2
+    // tail at the nodes of the target cells
+    launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+  }
   tm.mark();  // 3
   if (do_bnd) launch_flux(m, U.t, ex, e4, targets.p, ntargets, win.p, st);
   tm.mark();  // 4
@@ -491,8 +508,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   bool done1d = false;
   if (d == 1) {
     tm.mark();  // 5
-    done1d = launch_cross1d(m, U.t, oc, ex, e4, C, targets.p, ntargets, row_vertex.p, full, (int)row_begin,
-                            (int)row_end, D->A.p, D->lda, evc.p + 1, st);
+    done1d = launch_cross1d(m, U.t, oc, ex, e4, C, P1.get(), maxcells1d, targets.p, ntargets, row_vertex.p, D->A.p,
+                            D->lda, evc.p + 1, st);
   }
   if (!done1d) {
     cudaEventCreate(&xev[0]);
@@ -560,8 +577,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   S.evals_tail = (double)hev[0];
   S.evals_cross = (double)hev[1];
   S.ms_prep = tm.ms(0, 1);
-  S.ms_singular = tm.ms(1, 2);
-  S.ms_tail = tm.ms(2, 3);
+  S.ms_singular = early_tail ? tm.ms(2, 3) : tm.ms(1, 2);   // 1D: tail (1 -> 2) runs before the singular kernels
+  S.ms_tail = early_tail ? tm.ms(1, 2) : tm.ms(2, 3);
   S.ms_flux = tm.ms(3, 4);
   S.ms_tiles = tm.ms(4, 5);
   S.ms_cross = tm.ms(5, 6);

@@ -19,6 +19,7 @@
 #include "fl_internal.h"
 
 #include <climits>
+#include <memory>
 #include <cstdlib>
 #include <string>
 
@@ -107,13 +108,15 @@ __device__ __forceinline__ void tail1d_source(const double* __restrict__ tab, co
 template <int E4, int NT>
 __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                      OrderConsts oc, double ex, Src1D S,
-                                                     const int* __restrict__ targets, int ntargets,
+                                                     const int* __restrict__ targets,
+                                                     const int* __restrict__ d_ntargets,
                                                      double* __restrict__ psi,
                                                      unsigned long long* __restrict__ evals) {
   constexpr int Q = 6;
   __shared__ int qs[4][NT][64], qk[4][NT][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int wi = blockIdx.x * (blockDim.x >> 5) + w;
+  const int ntargets = *d_ntargets;             // device count: launched before the host knows it
   if (wi * NT >= ntargets) return;
   int K[NT], av0[NT], av1[NT];
   bool valid[NT];
@@ -916,15 +919,63 @@ static void build_src1d(const DevMesh& m, Src1DBuf& B, cudaStream_t st) {
   FL_CHECK_LAUNCH();
 }
 
-void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
-                   const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st) {
-  if (ntargets <= 0) return;
+struct TilingBuf {
+  DBuf<int> cnt, cell, dslot, owner;
+  DBuf<double> stat;
+  int off = 0, len = 0, nt = 0;
+  Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, stat.p, off, len, nt}; }
+};
+
+// Everything the 1D far field needs from the mesh, enqueued without host synchronisation: the
+// source records and, for the fused cross tiles, the DoF tilings with the max cells per tile on
+// the device (read back together with the other sizes).
+struct Plan1D {
   Src1DBuf B;
-  build_src1d(m, B, st);
-  const Src1D S = B.view();
+  TilingBuf TR, TC;
+  DBuf<int> mx;
+  bool fused = false, symmetric = true;
+  int row_begin = 0, row_end = 0;
+};
+
+Plan1D* plan1d_create(const DevMesh& m, const int* dof_vertex, bool symmetric, int row_begin, int row_end,
+                      cudaStream_t st) {
+  std::unique_ptr<Plan1D> P(new Plan1D());
+  P->symmetric = symmetric;
+  P->row_begin = row_begin;
+  P->row_end = row_end;
+  build_src1d(m, P->B, st);
+  P->mx.alloc(1);
+  FL_CUDA(cudaMemsetAsync(P->mx.p, 0, sizeof(int), st));
+  const char* path = getenv("FRACLAP_CROSS1D");
+  const bool force_pairs = path && std::string(path) == "pairs";
+  P->fused = !force_pairs && m.n > 0 && row_end > row_begin;
+  if (P->fused) {
+    auto make = [&](TilingBuf& T, int off, int len) {
+      T.off = off; T.len = len; T.nt = (len + T1 - 1) / T1;
+      T.cnt.alloc(T.nt); T.cell.alloc((size_t)T.nt * T1C); T.dslot.alloc((size_t)2 * len); T.owner.alloc(m.nc);
+      T.stat.alloc((size_t)T.nt * 5);
+      FL_CUDA(cudaMemsetAsync(T.owner.p, 0x7f, sizeof(int) * m.nc, st));
+      tile1d_cells_kernel<<<(T.nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, off, len, T.nt, T.cnt.p, T.cell.p, T.dslot.p,
+                                                          T.owner.p, T.stat.p, P->mx.p),
+          ::fl::note_launch();
+      FL_CHECK_LAUNCH();
+    };
+    make(P->TC, 0, m.n);
+    if (!symmetric) make(P->TR, row_begin, row_end - row_begin);
+  }
+  return P.release();
+}
+void plan1d_free(Plan1D* P) { delete P; }
+const int* plan1d_maxcells(const Plan1D* P) { return P->mx.p; }
+
+void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, const Plan1D* P,
+                   const int* targets, const int* d_ntargets, int ntargets_ub, double* psi,
+                   unsigned long long* evals, cudaStream_t st) {
+  if (ntargets_ub <= 0) return;
+  const Src1D S = P->B.view();
   constexpr int NT = FL_TAIL1D_NT;
-  const int grid = (ntargets + 4 * NT - 1) / (4 * NT);
-  FL_E4_SWITCH1(e4, (tail1d_kernel<E4, NT><<<grid, 128, 0, st>>>(m, t.data, t, oc, ex, S, targets, ntargets, psi,
+  const int grid = (ntargets_ub + 4 * NT - 1) / (4 * NT);
+  FL_E4_SWITCH1(e4, (tail1d_kernel<E4, NT><<<grid, 128, 0, st>>>(m, t.data, t, oc, ex, S, targets, d_ntargets, psi,
                                                                  evals),
                      ::fl::note_launch()));
   FL_CHECK_LAUNCH();
@@ -938,61 +989,33 @@ bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric) {
 }
 
 bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
-                    const int* targets, int ntargets, const int* dof_vertex, bool symmetric, int row_begin,
-                    int row_end, double* A, int64_t lda, unsigned long long* evals, cudaStream_t st) {
-  Src1DBuf B;
-  build_src1d(m, B, st);
-  const Src1D S = B.view();
+                    const Plan1D* P, int maxcells, const int* targets, int ntargets, const int* dof_vertex,
+                    double* A, int64_t lda, unsigned long long* evals, cudaStream_t st) {
+  const Src1D S = P->B.view();
+  const bool symmetric = P->symmetric;
+  const int row_begin = P->row_begin, row_end = P->row_end;
   const double negC = -Cds;   // (C/2) * (-2) (assembly.py:723, :1100)
-  const char* path = getenv("FRACLAP_CROSS1D");
-  const bool force_pairs = path && std::string(path) == "pairs";
-  if (!force_pairs && m.n > 0 && row_end > row_begin) {
-    // fused DoF tiles when every tile's cells fit the shared-memory pair table
-    struct TilingBuf {
-      DBuf<int> cnt, cell, dslot, owner;
-      DBuf<double> stat;
-      int off = 0, len = 0, nt = 0;
-      Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, stat.p, off, len, nt}; }
-    };
-    DBuf<int> mx(1);
-    FL_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), st));
-    auto make = [&](TilingBuf& T, int off, int len) {
-      T.off = off; T.len = len; T.nt = (len + T1 - 1) / T1;
-      T.cnt.alloc(T.nt); T.cell.alloc((size_t)T.nt * T1C); T.dslot.alloc((size_t)2 * len); T.owner.alloc(m.nc);
-      T.stat.alloc((size_t)T.nt * 5);
-      FL_CUDA(cudaMemsetAsync(T.owner.p, 0x7f, sizeof(int) * m.nc, st));
-      tile1d_cells_kernel<<<(T.nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, off, len, T.nt, T.cnt.p, T.cell.p, T.dslot.p,
-                                                          T.owner.p, T.stat.p, mx.p),
-          ::fl::note_launch();
-      FL_CHECK_LAUNCH();
-    };
-    TilingBuf TR, TC;
-    make(TC, 0, m.n);
-    if (!symmetric) make(TR, row_begin, row_end - row_begin);
-    int mc = 0;
-    FL_CUDA(cudaMemcpyAsync(&mc, mx.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FL_CUDA(cudaStreamSynchronize(st));
-    if (mc <= T1C) {
-      mc = std::max(mc, 1);
-      const size_t smem = std::max((sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc,
-                                   sizeof(double) * (size_t)T1 * (T1 + 1));   // tt aliases the blocks
-      const Tiling1D cv = TC.view(), rv = symmetric ? cv : TR.view();
-      const int64_t ntp = symmetric ? (int64_t)cv.nt * (cv.nt + 1) / 2 : (int64_t)rv.nt * cv.nt;
-      FL_E4_SWITCH1(e4, {
-        if (symmetric) {
-          auto kern = cross1d_tile_kernel<E4, false>;
-          FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
-        } else {
-          auto kern = cross1d_tile_kernel<E4, true>;
-          FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
-        }
-        ::fl::note_launch();
-      });
-      FL_CHECK_LAUNCH();
-      return true;
-    }
+  if (P->fused && maxcells <= T1C) {
+    // fused DoF tiles: every tile's cells fit the shared-memory pair table
+    const int mc = std::max(maxcells, 1);
+    const size_t smem = std::max((sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc,
+                                 sizeof(double) * (size_t)T1 * (T1 + 1));   // tt aliases the blocks
+    const Tiling1D cv = P->TC.view(), rv = symmetric ? cv : P->TR.view();
+    const int64_t ntp = symmetric ? (int64_t)cv.nt * (cv.nt + 1) / 2 : (int64_t)rv.nt * cv.nt;
+    FL_E4_SWITCH1(e4, {
+      if (symmetric) {
+        auto kern = cross1d_tile_kernel<E4, false>;
+        FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+      } else {
+        auto kern = cross1d_tile_kernel<E4, true>;
+        FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+      }
+      ::fl::note_launch();
+    });
+    FL_CHECK_LAUNCH();
+    return true;
   }
   if (!cross1d_fits(m, ntargets, symmetric)) return false;   // pair buffer too large: caller uses tiles
   if (symmetric) {

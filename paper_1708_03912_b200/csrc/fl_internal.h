@@ -209,12 +209,18 @@ void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& o
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
 // fl_far1d.cu (1D: lean tail, packed pair-block cross + gather)
-void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
-                   const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st);
+struct Plan1D;   // 1D far-field mesh data (fl_far1d.cu), built without host synchronisation
+Plan1D* plan1d_create(const DevMesh& m, const int* dof_vertex, bool symmetric, int row_begin, int row_end,
+                      cudaStream_t st);
+void plan1d_free(Plan1D* P);
+const int* plan1d_maxcells(const Plan1D* P);   // device: max cells behind one DoF tile
+void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, const Plan1D* P,
+                   const int* targets, const int* d_ntargets, int ntargets_ub, double* psi,
+                   unsigned long long* evals, cudaStream_t st);
 bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric);
 bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
-                    const int* targets, int ntargets, const int* dof_vertex, bool symmetric, int row_begin,
-                    int row_end, double* A, int64_t lda, unsigned long long* evals, cudaStream_t st);
+                    const Plan1D* P, int maxcells, const int* targets, int ntargets, const int* dof_vertex,
+                    double* A, int64_t lda, unsigned long long* evals, cudaStream_t st);
 void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,
                        cudaStream_t st);
 double probe_fp64_tflops(cudaStream_t st);

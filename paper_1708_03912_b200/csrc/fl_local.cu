@@ -90,7 +90,6 @@ static void sort_by_key(const int* keys, const int* vals, int* keys_out, int* va
   cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys_out, vals, vals_out, m, 0, bits, st);
   DBuf<unsigned char> t(tmp);
   FL_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, keys, keys_out, vals, vals_out, m, 0, bits, st));
-  FL_CUDA(cudaStreamSynchronize(st));
 }
 
 void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs, const BndPair* items,
