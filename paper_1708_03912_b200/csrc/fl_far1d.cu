@@ -48,11 +48,37 @@ struct Src1D {
   const double *x0, *x1, *lo, *hi, *h, *lh;
   const int *v0, *v1;
   const float *lnhf, *lhf;      // __logf((float)h), (float)|ln h| for the fp32 order estimate
+  const double* cstat;          // per 32-cell chunk: CSTAT doubles (chunk_all_k2)
 };
 
+// Per chunk of 32 consecutive cells: x extent (lo, hi), max h, min / max |ln h|, ln(max h).
+constexpr int CSTAT = 8;
+
 __global__ void build_src1d_kernel(DevMesh m, Rec1D* rec, double* x0, double* x1, double* lo, double* hi, double* h,
-                                   double* lh, int* v0, int* v1, float* lnhf, float* lhf) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+                                   double* lh, int* v0, int* v1, float* lnhf, float* lhf, double* cstat) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;   // blockDim a multiple of 32: warp = chunk
+  {
+    double clo = 1e300, chi = -1e300, hmx = 0.0, lmn = 1e300, lmx = 0.0;
+    if (c < m.nc) {
+      const CellGeo& g = m.geo[c];
+      clo = fmin(g.p[0][0], g.p[1][0]);
+      chi = fmax(g.p[0][0], g.p[1][0]);
+      hmx = g.diam;
+      lmn = lmx = g.ldiam;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      clo = fmin(clo, __shfl_xor_sync(0xffffffffu, clo, o));
+      chi = fmax(chi, __shfl_xor_sync(0xffffffffu, chi, o));
+      hmx = fmax(hmx, __shfl_xor_sync(0xffffffffu, hmx, o));
+      lmn = fmin(lmn, __shfl_xor_sync(0xffffffffu, lmn, o));
+      lmx = fmax(lmx, __shfl_xor_sync(0xffffffffu, lmx, o));
+    }
+    if ((c & 31) == 0 && c < m.nc) {
+      double* cs = cstat + (size_t)CSTAT * (c >> 5);
+      cs[0] = clo; cs[1] = chi; cs[2] = hmx; cs[3] = lmn; cs[4] = lmx; cs[5] = log(hmx); cs[6] = 0.0; cs[7] = 0.0;
+    }
+  }
   if (c >= m.nc) return;
   const CellGeo& g = m.geo[c];
   x0[c] = g.p[0][0];
@@ -83,6 +109,23 @@ static __device__ __noinline__ int order_exact1d(const OrderConsts& oc, double c
 }
 
 // ------------------------------------------------------------------ tail
+// True when every source cell of a 32-cell chunk provably has tail order 2 for the target cell
+// (alo, ahi, h = ah, |ln h| = alh, ln h = lah): the gap D between the target and the chunk's x
+// extent bounds every pair distance from below, so the disjoint order formula with the tail's
+// C_offset - 4 (quadrature.py:159-168, assembly.py:997) is bounded above term by term (numerator
+// up, denominator down); 1e-9 of margin absorbs rounding, so the reference's ceil() clips to 2.
+// D > 0 also excludes K and every cell sharing a vertex with it (N(K), assembly.py:999-1009).
+__device__ __forceinline__ bool chunk_all_k2(const OrderConsts& oc, double alo, double ahi, double alh, double lah,
+                                             const double* __restrict__ cs) {
+  const double D = fmax(cs[0] - ahi, alo - cs[1]);
+  if (!(D > 0.0)) return false;
+  const double lmn = fmin(alh, cs[3]), lmx = fmax(alh, cs[4]), lhmx = fmax(lah, cs[5]);
+  const double lD = log(D);
+  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * lD + oc.s * lhmx - oc.coff_tail;
+  const double den = fmax(lD - lhmx, 0.0) + oc.ln_rho2;
+  return (num > 0.0 ? num / den : 0.0) <= 2.0 - 1e-9;
+}
+
 template <int E4>
 __device__ __forceinline__ void tail1d_source(const double* __restrict__ tab, const DevTables& dir, double ex,
                                               const double (&xq)[6], double (&acc)[6], double x0, double e, double J,
@@ -120,7 +163,7 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
   if (wi * NT >= ntargets) return;
   int K[NT], av0[NT], av1[NT];
   bool valid[NT];
-  double alo[NT], ahi[NT], ah[NT], alh[NT];
+  double alo[NT], ahi[NT], ah[NT], alh[NT], alg[NT];
   float alnf[NT], alhf[NT];
   double xq[NT][Q], acc[NT][Q];
 #pragma unroll
@@ -129,6 +172,7 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
     valid[t] = ti < ntargets;
     K[t] = targets[valid[t] ? ti : wi * NT];
     alo[t] = S.lo[K[t]]; ahi[t] = S.hi[K[t]]; ah[t] = S.h[K[t]]; alh[t] = S.lh[K[t]];
+    alg[t] = log(ah[t]);
     alnf[t] = S.lnhf[K[t]]; alhf[t] = S.lhf[K[t]];
     av0[t] = S.v0[K[t]]; av1[t] = S.v1[K[t]];
 #pragma unroll
@@ -139,10 +183,11 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
   }
   const double* n2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
   const double t0 = n2[0], w0 = n2[2], t1 = n2[NODE], w1 = n2[NODE + 2];
-  unsigned nodes[NT];
+  unsigned nodes[NT], umask[NT];
   int qn[NT];                                   // warp-uniform queue lengths
+  const int nchunks = (m.nc + 31) >> 5;
 #pragma unroll
-  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; }
+  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; umask[t] = 0; }
   const unsigned lt = (1u << lane) - 1u;
   const int4* R = reinterpret_cast<const int4*>(S.rec);
   int4 na = make_int4(0, 0, 0, 0), nb = na;     // prefetched record of the next source
@@ -157,8 +202,30 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
     const double e = sx1 - sx0, J = fabs(e);
     const double y0 = sx0 + t0 * e, y1 = sx0 + t1 * e;
     const double j0 = J * w0, j1 = J * w1;
+    const int ci = s0 >> 5;
+    if ((ci & 31) == 0) {                       // order-2 flags of the next 32 chunks, one per lane
+      const int cj = ci + lane;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        umask[t] = __ballot_sync(0xffffffffu, cj < nchunks &&
+                                                  chunk_all_k2(oc, alo[t], ahi[t], alh[t], alg[t],
+                                                               S.cstat + (size_t)CSTAT * cj));
+    }
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
+      if ((umask[t] >> (ci & 31)) & 1u) {       // warp-uniform: the whole chunk is k = 2
+        if (s < m.nc) {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const double d0 = xq[t][q] - y0;
+            acc[t][q] = fma(j0, kpow_abs<E4>(d0, ex), acc[t][q]);
+            const double d1 = xq[t][q] - y1;
+            acc[t][q] = fma(j1, kpow_abs<E4>(d1, ex), acc[t][q]);
+          }
+          nodes[t] += 2;
+        }
+        continue;
+      }
       int k = -1;                               // -1: not a tail source of target t
       if (s < m.nc && !(s == K[t] || bv0 == av0[t] || bv0 == av1[t] || bv1 == av0[t] || bv1 == av1[t])) {  // N(K) (:999-1009)
         const double dist = fmax(fmax(__dsub_rn(blo, ahi[t]), __dsub_rn(alo[t], bhi)), 0.0);   // (:750-752)
@@ -907,15 +974,17 @@ struct Src1DBuf {
   DBuf<int> v0, v1;
   DBuf<float> lnhf, lhf;
   DBuf<Rec1D> rec;
-  Src1D view() const { return Src1D{rec.p, x0.p, x1.p, lo.p, hi.p, h.p, lh.p, v0.p, v1.p, lnhf.p, lhf.p}; }
+  DBuf<double> cstat;
+  Src1D view() const { return Src1D{rec.p, x0.p, x1.p, lo.p, hi.p, h.p, lh.p, v0.p, v1.p, lnhf.p, lhf.p, cstat.p}; }
 };
 
 static void build_src1d(const DevMesh& m, Src1DBuf& B, cudaStream_t st) {
   const int nc = m.nc;
   B.x0.alloc(nc); B.x1.alloc(nc); B.lo.alloc(nc); B.hi.alloc(nc); B.h.alloc(nc); B.lh.alloc(nc);
   B.v0.alloc(nc); B.v1.alloc(nc); B.lnhf.alloc(nc); B.lhf.alloc(nc); B.rec.alloc(nc);
+  B.cstat.alloc((size_t)CSTAT * ((nc + 31) / 32));
   build_src1d_kernel<<<(nc + 255) / 256, 256, 0, st>>>(m, B.rec.p, B.x0.p, B.x1.p, B.lo.p, B.hi.p, B.h.p, B.lh.p, B.v0.p,
-                                                        B.v1.p, B.lnhf.p, B.lhf.p), ::fl::note_launch();
+                                                        B.v1.p, B.lnhf.p, B.lhf.p, B.cstat.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
