@@ -147,6 +147,14 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap,
                           int64_t row_begin, int64_t row_end,
                           int32_t device, void* stream, fl_dense** out);
 
+/* The whole (n x n) matrix written straight into host memory `A_host` (row-major, n*n doubles):
+ * the ndarray that assembly.assemble_dense returns (assembly.py:1059-1104, :1096-1104).
+ * Page-locked A_host copies at full PCIe rate.  On error A_host is left unspecified. */
+int32_t fl_assemble_dense_host(const fl_mesh* mesh, const fl_dofmap* dofmap,
+                               const fl_kernel* kernel, const fl_order_params* params,
+                               const fl_tables* tables, int64_t n_limit, int32_t device,
+                               double* A_host);
+
 /* Wrap an existing dense host matrix (n x n, row-major) as a device operator — the
  * `Ad = np.asarray(A)` branch of LinearOperatorHandle.from_matrix (solve.py:31-32). */
 int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out);

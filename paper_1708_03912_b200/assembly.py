@@ -108,11 +108,20 @@ def assemble_dense(mesh, dofmap, kernel, params: OrderParams | None = None, n_li
     `out` (keyword only): a preallocated C-contiguous (n, n) float64 array, e.g. pinned."""
     if dofmap.n > n_limit:
         raise AssemblyError("dense assembly refused beyond %d dofs" % n_limit)
-    op = assemble_dense_device(mesh, dofmap, kernel, params, n_limit=n_limit)
-    try:
-        return op.to_host(out)
-    finally:
-        op.free()
+    lib = _lib.load()
+    variant = getattr(getattr(kernel, "variant", Variant.INTEGRAL), "value", "integral")
+    if variant == "symmetrized":
+        raise AssemblyError("symmetrized kernels are not supported by the dense device path")
+    n = int(dofmap.n)
+    if out is None:
+        out = np.empty((n, n))
+    elif out.shape != (n, n) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 array of shape %r" % ((n, n),))
+    m = _lib.Marshal(mesh, dofmap, kernel, params)
+    dir_, data, tb = _tables(mesh, dofmap, float(kernel.s), params)
+    _lib.check(lib.fl_assemble_dense_host(C.byref(m.mesh), C.byref(m.dofmap), C.byref(m.kernel), C.byref(m.params),
+                                          C.byref(tb), int(n_limit), _device_index(None), out.ctypes.data))
+    return out
 
 
 def load_vector(mesh, dofmap, f, order=4):

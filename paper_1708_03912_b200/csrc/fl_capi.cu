@@ -348,10 +348,19 @@ struct Timer {
 
 extern "C" {
 
-int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
-                          const fl_order_params* params, const fl_tables* tables, int64_t n_limit,
-                          int64_t row_begin, int64_t row_end, int32_t device, void* stream, fl_dense** out) {
+}  // extern "C"
+
+// The assembly.  host != nullptr (whole matrix, 1D, fused cross tiles): the rows are finished
+// band by band (tail, cell-local matrices, cross tiles and the local pull of one DoF row band)
+// and each band is copied to `host` on a copy stream while the next band is assembled, so the
+// PCIe copy — ~4x the assembly at c2 — starts after the first band instead of after the whole
+// matrix.  The entries are bitwise those of the unbanded assembly.
+static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                             const fl_order_params* params, const fl_tables* tables, int64_t n_limit,
+                             int64_t row_begin, int64_t row_end, int32_t device, void* stream, fl_dense** out,
+                             double* host, bool* host_done) {
   FL_API_BEGIN
+  if (host_done) *host_done = false;
   const auto t_enter = std::chrono::steady_clock::now();
   if (!out) return fail(FL_E_ARG, "null output handle");
   *out = nullptr;
@@ -413,10 +422,42 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   // 1D: the far-field mesh data (source records, DoF tilings) is built here too, and the tail —
   // which needs nothing the host has to know — is enqueued before the host waits for the sizes,
   // so the host-side work below overlaps the tail instead of leaving the GPU idle
-  const bool early_tail = d == 1;
+  int nbands = 0;
+  if (host && d == 1 && row_begin == 0 && row_end == n) {
+    const char* env = getenv("FRACLAP_HOST_BANDS");
+    nbands = env ? atoi(env) : (n >= 2048 ? 8 : 0);
+    if (nbands < 2) nbands = 0;
+  }
+  // band cut points: a short first band (the copy starts early), then equal tile-aligned bands
+  std::vector<int> cut;
+  if (nbands) {
+    const int T = cross1d_tile_dofs();
+    const int first = std::min<int>((int)n, 16 * T);
+    const int rest = (int)((n - first + nbands - 2) / (nbands - 1));
+    const int blk = std::max(T, (rest + T - 1) / T * T);
+    cut.push_back(0);
+    cut.push_back(first);
+    while (cut.back() < n) cut.push_back(std::min<int>((int)n, cut.back() + blk));
+    nbands = (int)cut.size() - 1;
+    if (nbands > 48) throw Error(FL_E_CUDA, "internal: too many host bands");
+  }
+  const bool early_tail = d == 1 && !nbands;
   std::unique_ptr<Plan1D, void (*)(Plan1D*)> P1(nullptr, plan1d_free);
-  if (early_tail) P1.reset(plan1d_create(m, row_vertex.p, row_begin == 0 && row_end == n, (int)row_begin,
-                                         (int)row_end, st));
+  if (d == 1) P1.reset(plan1d_create(m, row_vertex.p, row_begin == 0 && row_end == n, (int)row_begin,
+                                     (int)row_end, st));
+  // banded: the target cells of every band (cells with a vertex DoF in the band), counts read
+  // back with the other sizes
+  std::vector<DBuf<int>> btgt(nbands);
+  DBuf<int> bcnt(std::max(nbands, 1));
+  for (int b = 0; b < nbands; ++b) {
+    btgt[b].alloc(m.nc);
+    flag_target_cells<<<(m.nc + 255) / 256, 256, 0, st>>>(m, cut[b], cut[b + 1], flags.p), ::fl::note_launch();
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, all.p, flags.p, btgt[b].p, bcnt.p + b, m.nc, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, all.p, flags.p, btgt[b].p, bcnt.p + b, m.nc, st));
+    FL_CHECK_LAUNCH();
+  }
   touching_count(m, tcounts, toffs, st);
   if (do_bnd) boundary_count(m, bcounts, boffs, st);
   int* hs = pinned_scratch();
@@ -426,7 +467,8 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   FL_CUDA(cudaMemcpyAsync(&hs[1], toffs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (do_bnd) FL_CUDA(cudaMemcpyAsync(&hs[2], boffs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[3], U.maxv.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  if (early_tail) FL_CUDA(cudaMemcpyAsync(&hs[5], plan1d_maxcells(P1.get()), sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (d == 1) FL_CUDA(cudaMemcpyAsync(&hs[5], plan1d_maxcells(P1.get()), sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (nbands) FL_CUDA(cudaMemcpyAsync(&hs[16], bcnt.p, nbands * sizeof(int), cudaMemcpyDeviceToHost, st));
   cudaEvent_t ev_sizes = tm.e[11];                 // (the last timing event doubles as the size fence)
   FL_CUDA(cudaEventRecord(ev_sizes, st));
   DBuf<unsigned long long> evc(2);
@@ -444,6 +486,7 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   nitems = hs[2];
   valence_error(hs[3]);
   const int maxcells1d = hs[5];
+  if (nbands && !cross1d_fused(P1.get(), maxcells1d)) nbands = 0;   // not fused: unbanded, late tail
   touching_fill(m, oc, toffs, npairs, tpairs, ident_k, st);
   DBuf<BndPair> bitems;
   if (do_bnd) boundary_fill(m, oc, boffs, nitems, bitems, st);
@@ -483,8 +526,9 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   if (do_bnd) launch_singular_boundary(m, U.t, ex, e4, bitems.p, nitems, bloc.p, st);
   if (!early_tail) {
     tm.mark();  // 2
-    // tail at the nodes of the target cells
-    launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+    // tail at the nodes of the target cells (banded 1D: per band, below)
+    if (d == 2) launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+    else if (!nbands) launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, st);
   }
   tm.mark();  // 3
   if (do_bnd) launch_flux(m, U.t, ex, e4, targets.p, ntargets, win.p, st);
@@ -506,7 +550,42 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   NearPairs near;
   cudaEvent_t xev[2] = {nullptr, nullptr};
   bool done1d = false;
-  if (d == 1) {
+  DBuf<double> Lc((size_t)m.nc * 9);
+  struct CopyStream {                  // device -> host copies of finished bands
+    int dev; cudaStream_t s = nullptr; std::vector<cudaEvent_t> e;
+    CopyStream(int d, int nb) : dev(d) {
+      if (!nb) return;
+      s = acquire_stream(d);
+      e.resize(nb, nullptr);
+      for (auto& x : e) FL_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    }
+    ~CopyStream() {
+      if (!s) return;
+      cudaStreamSynchronize(s);
+      for (auto& x : e)
+        if (x) cudaEventDestroy(x);
+      release_stream(dev, s);
+    }
+  } cps(device, nbands);
+  if (nbands) {
+    tm.mark();  // 5
+    for (int b = 0; b < nbands; ++b) {
+      const int nt_b = hs[16 + b];
+      launch_tail1d(m, U.t, oc, ex, e4, P1.get(), btgt[b].p, bcnt.p + b, nt_b, psi.p, evc.p, st);
+      launch_cell_local(m, U.t, C, s, integral && m.nb > 0, btgt[b].p, nt_b, ident.p, psi.p, win.p, Lc.p, st);
+      launch_cross1d(m, U.t, oc, ex, e4, C, P1.get(), maxcells1d, targets.p, ntargets, row_vertex.p, D->A.p, D->lda,
+                     evc.p + 1, st, cut[b], cut[b + 1]);
+      if (b == 0) FL_CUDA(cudaStreamWaitEvent(st, ev_si, 0));
+      launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
+                         cut[b], cut[b + 1], D->A.p + (int64_t)cut[b] * D->lda, D->lda, st);   // (rows from cut[b])
+      FL_CUDA(cudaEventRecord(cps.e[b], st));
+      FL_CUDA(cudaStreamWaitEvent(cps.s, cps.e[b], 0));
+      FL_CUDA(cudaMemcpy2DAsync(host + (int64_t)cut[b] * n, n * sizeof(double), D->A.p + (int64_t)cut[b] * D->lda,
+                                D->lda * sizeof(double), n * sizeof(double), cut[b + 1] - cut[b],
+                                cudaMemcpyDeviceToHost, cps.s));
+    }
+    done1d = true;
+  } else if (d == 1) {
     tm.mark();  // 5
     done1d = launch_cross1d(m, U.t, oc, ex, e4, C, P1.get(), maxcells1d, targets.p, ntargets, row_vertex.p, D->A.p,
                             D->lda, evc.p + 1, st);
@@ -552,16 +631,21 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
                        near.hmask, near.G.p, st);
   }
   tm.mark();  // 6
-  DBuf<double> Lc((size_t)m.nc * 9);
-  launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
-  FL_CUDA(cudaStreamWaitEvent(st, ev_si, 0));
-  launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
-                     (int)row_begin, (int)row_end, D->A.p, D->lda, st);
+  if (!nbands) {
+    launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
+    FL_CUDA(cudaStreamWaitEvent(st, ev_si, 0));
+    launch_sparse_pull(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
+                       (int)row_begin, (int)row_end, D->A.p, D->lda, st);
+  }
   tm.mark();  // 7
   unsigned long long* hev = reinterpret_cast<unsigned long long*>(hs + 8);
   FL_CUDA(cudaMemcpyAsync(hev, evc.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[4], m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  if (nbands) {
+    FL_CUDA(cudaStreamSynchronize(cps.s));
+    if (host_done) *host_done = true;
+  }
   const int herr = hs[4];
   if (herr & 1) throw Error(FL_E_QUAD, "a quadrature rule for a selected order is missing from the tables");
   if (herr & 4) throw Error(FL_E_CUDA, "internal: a near pair missing from the discovery pass");
@@ -601,6 +685,32 @@ int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl
   *out = D.release();
   return FL_OK;
   FL_API_END
+}
+
+extern "C" {
+
+int32_t fl_assemble_dense(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                          const fl_order_params* params, const fl_tables* tables, int64_t n_limit,
+                          int64_t row_begin, int64_t row_end, int32_t device, void* stream, fl_dense** out) {
+  return assemble_impl(mesh, dofmap, kernel, params, tables, n_limit, row_begin, row_end, device, stream, out,
+                       nullptr, nullptr);
+}
+
+// Whole matrix straight into host memory: the ndarray assembly.assemble_dense returns
+// (assembly.py:1059-1104).  1D: banded, each finished row band copied while the next one is
+// assembled (assemble_impl); otherwise one assembly, then one pitched device->host copy.
+int32_t fl_assemble_dense_host(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                               const fl_order_params* params, const fl_tables* tables, int64_t n_limit,
+                               int32_t device, double* host) {
+  if (!host || !dofmap) return fail(FL_E_ARG, "null argument");
+  fl_dense* D = nullptr;
+  bool copied = false;
+  int32_t rc = assemble_impl(mesh, dofmap, kernel, params, tables, n_limit, 0, dofmap->n, device, nullptr, &D, host,
+                             &copied);
+  if (rc != FL_OK) return rc;
+  if (!copied) rc = fl_dense_to_host(D, host);
+  fl_dense_free(D);
+  return rc;
 }
 
 int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out) {

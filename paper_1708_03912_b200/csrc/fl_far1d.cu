@@ -16,6 +16,7 @@
 //             with the same canonical order; bitwise identical results.
 // Row-block (multi-GPU) mode computes the ordered pairs (K in the owned rows' cells, all L)
 // into a rectangular buffer instead.
+#include "../../include/fraclap_b200.h"
 #include "fl_internal.h"
 
 #include <climits>
@@ -674,7 +675,8 @@ template <int E4, bool RECT>
 __global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                            OrderConsts oc, double ex, Src1D S, Tiling1D R,
                                                            Tiling1D Cn, int mc, double negC, double* __restrict__ A,
-                                                           int64_t lda, unsigned long long* __restrict__ evals) {
+                                                           int64_t lda, unsigned long long* __restrict__ evals,
+                                                           int band0, int band1) {
   extern __shared__ __align__(16) unsigned char smem1d[];
   __shared__ Cell1S cr, cc;
   __shared__ int bcnt[T1K], boff[T1K + 1], ndefer, uni2;
@@ -684,6 +686,21 @@ __global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const
   if (RECT) {
     bi = (int)(bx / Cn.nt);
     bj = (int)(bx - (int64_t)bi * Cn.nt);
+  } else if (band1 > band0) {
+    // band of tile rows [band0, band1): row-major over the upper-triangular tile pairs of those
+    // rows (the diagonal tile, the heaviest, first in each row); the rows of the band are final
+    // once the earlier bands (their mirrors) and this one have run
+    const int nt = R.nt;
+    auto cum = [&](int64_t r) { return (r - band0) * nt - (r * (r - 1) - (int64_t)band0 * (band0 - 1)) / 2; };
+    // cum(r) = bx  <=>  r^2 - (2 nt + 1) r + 2 bx + 2 b0 nt - b0 (b0 - 1) = 0; then fix up
+    const double q2 = 2.0 * nt + 1.0, b0 = band0;
+    const double disc = q2 * q2 - 4.0 * (2.0 * (double)bx + 2.0 * b0 * nt - b0 * (b0 - 1.0));
+    int r = (int)((q2 - sqrt(fmax(disc, 0.0))) * 0.5);
+    r = max(band0, min(r, band1 - 1));
+    while (r > band0 && cum(r) > bx) --r;
+    while (r + 1 < band1 && cum(r + 1) <= bx) ++r;
+    bi = r;
+    bj = bi + (int)(bx - cum(r));
   } else {
     // diagonal-major tile order (near-diagonal tiles hold the high orders: heavy first)
     const int nt = R.nt;
@@ -1057,9 +1074,13 @@ bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric) {
   return need < 0.5 * (double)fr;
 }
 
+bool cross1d_fused(const Plan1D* P, int maxcells) { return P->fused && maxcells <= T1C; }
+int cross1d_tile_dofs() { return T1; }
+
 bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                     const Plan1D* P, int maxcells, const int* targets, int ntargets, const int* dof_vertex,
-                    double* A, int64_t lda, unsigned long long* evals, cudaStream_t st) {
+                    double* A, int64_t lda, unsigned long long* evals, cudaStream_t st, int band_row0,
+                    int band_row1) {
   const Src1D S = P->B.view();
   const bool symmetric = P->symmetric;
   const int row_begin = P->row_begin, row_end = P->row_end;
@@ -1070,22 +1091,31 @@ bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
     const size_t smem = std::max((sizeof(double4) + 2 * sizeof(int)) * (size_t)mc * mc,
                                  sizeof(double) * (size_t)T1 * (T1 + 1));   // tt aliases the blocks
     const Tiling1D cv = P->TC.view(), rv = symmetric ? cv : P->TR.view();
-    const int64_t ntp = symmetric ? (int64_t)cv.nt * (cv.nt + 1) / 2 : (int64_t)rv.nt * cv.nt;
+    int64_t ntp = symmetric ? (int64_t)cv.nt * (cv.nt + 1) / 2 : (int64_t)rv.nt * cv.nt;
+    int b0 = 0, b1 = 0;   // band of tile rows (symmetric whole matrix only; b1 = 0: all tiles)
+    if (symmetric && band_row1 > band_row0) {
+      if (band_row0 % T1) throw Error(FL_E_CUDA, "internal: band start not tile aligned");
+      b0 = band_row0 / T1;
+      b1 = std::min(cv.nt, (band_row1 + T1 - 1) / T1);
+      ntp = (int64_t)(b1 - b0) * cv.nt - ((int64_t)b1 * (b1 - 1) - (int64_t)b0 * (b0 - 1)) / 2;
+      if (ntp <= 0) return true;
+    }
     FL_E4_SWITCH1(e4, {
       if (symmetric) {
         auto kern = cross1d_tile_kernel<E4, false>;
         FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals, b0, b1);
       } else {
         auto kern = cross1d_tile_kernel<E4, true>;
         FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals);
+        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals, 0, 0);
       }
       ::fl::note_launch();
     });
     FL_CHECK_LAUNCH();
     return true;
   }
+  if (band_row1 > band_row0) throw Error(FL_E_CUDA, "internal: banded cross term needs the fused tiles");
   if (!cross1d_fits(m, ntargets, symmetric)) return false;   // pair buffer too large: caller uses tiles
   if (symmetric) {
     DBuf<double4> G((size_t)std::max<int64_t>((int64_t)m.nc * (m.nc - 1) / 2, 1));

@@ -218,9 +218,14 @@ void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, 
                    const int* targets, const int* d_ntargets, int ntargets_ub, double* psi,
                    unsigned long long* evals, cudaStream_t st);
 bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric);
+// band_row0 < band_row1 (tile-aligned start): only the upper-triangular tile pairs whose row tile
+// lies in that DoF row band (needs the fused tiles: cross1d_fused)
 bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                     const Plan1D* P, int maxcells, const int* targets, int ntargets, const int* dof_vertex,
-                    double* A, int64_t lda, unsigned long long* evals, cudaStream_t st);
+                    double* A, int64_t lda, unsigned long long* evals, cudaStream_t st, int band_row0 = 0,
+                    int band_row1 = 0);
+bool cross1d_fused(const Plan1D* P, int maxcells);
+int cross1d_tile_dofs();
 void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long long* hc, unsigned long long* ht,
                        cudaStream_t st);
 double probe_fp64_tflops(cudaStream_t st);

@@ -5,6 +5,10 @@
 // iterations, so the iteration count is exactly the reference's.
 #include "fl_internal.h"
 
+#ifndef FL_MV_U
+#define FL_MV_U 4      // double2 loads per lane in flight per row and main-loop step
+#endif
+
 namespace fl {
 
 // ----------------------------------------------------------------- matvec
@@ -27,18 +31,19 @@ __global__ void __launch_bounds__(256) matvec_kernel(const double* __restrict__ 
     a2[r] = reinterpret_cast<const double2*>(A + row * lda);
     acc[r] = 0.0;
   }
+  constexpr int U = FL_MV_U;
   int64_t j = lane;
-  for (; j + 96 < ncol2; j += 128) {
-    double2 xv[4];
+  for (; j + 32 * (U - 1) < ncol2; j += 32 * U) {
+    double2 xv[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = __ldg(x2 + j + 32 * u);
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x2 + j + 32 * u);
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
-      double2 av[4];
+      double2 av[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) av[u] = __ldcs(a2[r] + j + 32 * u);
+      for (int u = 0; u < U; ++u) av[u] = __ldcs(a2[r] + j + 32 * u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[r] = fma(av[u].y, xv[u].y, fma(av[u].x, xv[u].x, acc[r]));
+      for (int u = 0; u < U; ++u) acc[r] = fma(av[u].y, xv[u].y, fma(av[u].x, xv[u].x, acc[r]));
     }
   }
   for (; j < ncol2; j += 32) {
