@@ -170,6 +170,27 @@ int32_t fl_dense_rows(const fl_dense* A, int64_t nrows, const int64_t* rows, dou
 /* diagonal entries of the owned rows (host) */
 int32_t fl_dense_diag(const fl_dense* A, double* host_diag);
 
+/* ------------------------------------------------------------- driver steps (host O(n) in the
+ * reference), on the device
+ * _finish_polygon_mesh + _boundary_of (mesh.py:351-403): cells_out (nc x 3) CCW with the longest
+ * (refinement) edge first; boundary edges (lexicographic (lo, hi), as np.unique) with outward unit
+ * normals.  capacity = rows available in the edge/normal outputs; *nb_out is always set and
+ * FL_E_ARG is returned when it exceeds capacity (3*nc always suffices). */
+int32_t fl_finish_polygon_mesh(const double* vertices, int64_t nv, const int64_t* cells_in, int64_t nc,
+                               int32_t device, int64_t* cells_out, int64_t* boundary_edges_out,
+                               double* boundary_normals_out, int64_t capacity, int64_t* nb_out);
+/* DofMap (mesh.py:200-240, no `identify`): all vertices for s < 1/2, else the vertices on no
+ * boundary edge; vertex_to_dof_out (nv,) with -1 for a non-DoF, *n_out = DoF count. */
+int32_t fl_build_dofmap(const fl_mesh* mesh, double s, int32_t device, int64_t* vertex_to_dof_out, int64_t* n_out);
+/* Physical nodes of a per-cell reference rule (q nodes `pts`, q x d): X_out (nc, q, d)
+ * (cell_quadrature / _map_points, assembly.py:129-132, :290-298) — where the caller evaluates f. */
+int32_t fl_cell_rule_nodes(const fl_mesh* mesh, const double* pts, int64_t q, int32_t device, double* X_out);
+/* load_vector (assembly.py:550-570, no discontinuity splitting): b_i = sum_K sum_q J_K w_q f_q
+ * lambda_a(q) with f_q = f_values[K*q + r] (nc x q, at fl_cell_rule_nodes' nodes) or f_const
+ * when f_values is NULL; per DoF in ascending cell order (np.add.at). b_out (n,). */
+int32_t fl_load_vector(const fl_mesh* mesh, const fl_dofmap* dofmap, const double* pts, const double* w,
+                       int64_t q, const double* f_values, double f_const, int32_t device, double* b_out);
+
 /* ------------------------------------------------------------- matvec
  * y[rows] = A[rows, :] @ x  (solve.py:31-32).  ptr_kind 0: host pointers, 1: device. */
 int32_t fl_matvec(const fl_dense* A, const double* x, double* y, int32_t ptr_kind);

@@ -17,7 +17,8 @@ FL_OK, FL_E_ARG, FL_E_ASSEMBLY, FL_E_QUAD, FL_E_SOLVER, FL_E_CUDA, FL_E_OOM = 0,
 VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
 
 EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_count", "fl_assemble_dense",
-           "fl_assemble_dense_host",
+           "fl_assemble_dense_host", "fl_finish_polygon_mesh", "fl_build_dofmap", "fl_cell_rule_nodes",
+           "fl_load_vector",
            "fl_dense_from_host",
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_rows", "fl_dense_diag", "fl_matvec",
@@ -91,6 +92,11 @@ def load():
                                           P(vp)]),
         "fl_assemble_dense_host": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),
                                                P(fl_tables), C.c_int64, C.c_int32, vp]),
+        "fl_finish_polygon_mesh": (C.c_int32, [vp, C.c_int64, vp, C.c_int64, C.c_int32, vp, vp, vp, C.c_int64,
+                                               P(C.c_int64)]),
+        "fl_build_dofmap": (C.c_int32, [P(fl_mesh), C.c_double, C.c_int32, vp, P(C.c_int64)]),
+        "fl_cell_rule_nodes": (C.c_int32, [P(fl_mesh), vp, C.c_int64, C.c_int32, vp]),
+        "fl_load_vector": (C.c_int32, [P(fl_mesh), P(fl_dofmap), vp, vp, C.c_int64, vp, C.c_double, C.c_int32, vp]),
         "fl_dense_from_host": (C.c_int32, [vp, C.c_int64, C.c_int32, P(vp)]),
         "fl_dense_free": (None, [vp]),
         "fl_dense_info": (C.c_int32, [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(vp)]),

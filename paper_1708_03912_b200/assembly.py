@@ -124,24 +124,31 @@ def assemble_dense(mesh, dofmap, kernel, params: OrderParams | None = None, n_li
     return out
 
 
-def load_vector(mesh, dofmap, f, order=4):
-    """b_i = int f phi_i by the per-cell rule of `order` (assembly.py:550-570).  Host O(n)
-    work outside the accelerated path; no discontinuity splitting."""
-    d = mesh.vertices.shape[1]
+def load_vector(mesh, dofmap, f, order=4, discontinuity=None, device=None):
+    """b_i = int f phi_i by the per-cell rule of `order` (assembly.py:550-570) on the GPU
+    (fl_load_vector).  `f` is a callable on (m, d) points, as in the reference — evaluated on the
+    host at the rule nodes the device maps (fl_cell_rule_nodes) — or a number (f constant: no
+    host evaluation at all).  Per DoF the cell contributions are summed in ascending cell order,
+    like np.add.at.  Cells cut by a `discontinuity` (split at assembly.py:574-596) are not
+    supported on the device path."""
+    if discontinuity is not None:
+        raise ValueError("load_vector: discontinuity splitting is not supported by the device path")
+    lib = _lib.load()
+    d = int(mesh.vertices.shape[1])
     pts, w = simplex_rule(d, order)
-    lam = np.stack([1 - pts[:, 0], pts[:, 0]], axis=1) if d == 1 else \
-        np.stack([1 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], axis=1)
-    P = mesh.vertices[mesh.cells]
-    E = P[:, 1:] - P[:, 0:1]
-    X = P[:, 0:1, :] + pts @ E
-    if d == 1:
-        J = np.abs(P[:, 1, 0] - P[:, 0, 0])
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    q = len(w)
+    m = _lib.Marshal(mesh, dofmap, FractionalKernel(d, 0.5), None)
+    dev = _device_index(device)
+    fvals, fconst = None, 0.0
+    if callable(f):
+        X = np.empty((mesh.num_cells, q, d))
+        _lib.check(lib.fl_cell_rule_nodes(C.byref(m.mesh), pts.ctypes.data, q, dev, X.ctypes.data))
+        fvals = np.ascontiguousarray(np.asarray(f(X.reshape(-1, d)), dtype=np.float64).reshape(mesh.num_cells, q))
     else:
-        a, b_ = P[:, 1] - P[:, 0], P[:, 2] - P[:, 0]
-        J = np.abs(a[:, 0] * b_[:, 1] - a[:, 1] * b_[:, 0])
-    fv = np.asarray(f(X.reshape(-1, d))).reshape(len(P), -1)
-    loc = np.einsum("cq,qa->ca", np.outer(J, w) * fv, lam)
-    b = np.zeros(dofmap.n)
-    gd = np.asarray(dofmap.cell_dofs)
-    np.add.at(b, gd[gd >= 0], loc[gd >= 0])
+        fconst = float(f)
+    b = np.empty(int(dofmap.n))
+    _lib.check(lib.fl_load_vector(C.byref(m.mesh), C.byref(m.dofmap), pts.ctypes.data, w.ctypes.data, q,
+                                  None if fvals is None else fvals.ctypes.data, fconst, dev, b.ctypes.data))
     return b

@@ -713,6 +713,48 @@ int32_t fl_assemble_dense_host(const fl_mesh* mesh, const fl_dofmap* dofmap, con
   return rc;
 }
 
+// ------------------------------------------------------------- host O(n) steps on the device
+int32_t fl_finish_polygon_mesh(const double* vertices, int64_t nv, const int64_t* cells_in, int64_t nc,
+                               int32_t device, int64_t* cells_out, int64_t* boundary_edges_out,
+                               double* boundary_normals_out, int64_t capacity, int64_t* nb_out) {
+  FL_API_BEGIN
+  if (!vertices || !cells_in || !cells_out || !nb_out || nv <= 0 || nc <= 0) return fail(FL_E_ARG, "bad argument");
+  if (3 * nc >= (1LL << 31) || nv >= (1LL << 31)) return fail(FL_E_ARG, "mesh too large");
+  for (int64_t i = 0; i < 3 * nc; ++i)
+    if (cells_in[i] < 0 || cells_in[i] >= nv) return fail(FL_E_ARG, "cell vertex index out of range");
+  const int32_t rc = fl::finish_polygon_mesh(vertices, nv, cells_in, nc, device, cells_out, boundary_edges_out,
+                                             boundary_normals_out, capacity, nb_out);
+  if (rc != FL_OK) return fail(rc, "boundary edge capacity too small");
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_build_dofmap(const fl_mesh* mesh, double s, int32_t device, int64_t* vertex_to_dof_out, int64_t* n_out) {
+  FL_API_BEGIN
+  if (!mesh || !vertex_to_dof_out || !n_out) return fail(FL_E_ARG, "null argument");
+  if (!(s > 0.0 && s < 1.0)) return fail(FL_E_ARG, "fractional order s must lie in (0,1)");   // mesh.py:208-209
+  if (mesh->nv <= 0 || mesh->nv >= (1LL << 31)) return fail(FL_E_ARG, "bad vertex count");
+  return fl::dofmap_build(mesh->boundary_edges, mesh->nb, mesh->d, mesh->nv, s, device, vertex_to_dof_out, n_out);
+  FL_API_END
+}
+
+int32_t fl_cell_rule_nodes(const fl_mesh* mesh, const double* pts, int64_t q, int32_t device, double* X_out) {
+  FL_API_BEGIN
+  if (!mesh || !pts || !X_out || q <= 0 || (mesh->d != 1 && mesh->d != 2)) return fail(FL_E_ARG, "bad argument");
+  return fl::cell_rule_nodes(mesh, pts, q, device, X_out);
+  FL_API_END
+}
+
+int32_t fl_load_vector(const fl_mesh* mesh, const fl_dofmap* dofmap, const double* pts, const double* w, int64_t q,
+                       const double* f_values, double f_const, int32_t device, double* b_out) {
+  FL_API_BEGIN
+  if (!mesh || !dofmap || !pts || !w || !b_out || q <= 0 || (mesh->d != 1 && mesh->d != 2))
+    return fail(FL_E_ARG, "bad argument");
+  if (mesh->nc * (mesh->d + 1) >= (1LL << 31) || dofmap->n >= (1LL << 31)) return fail(FL_E_ARG, "mesh too large");
+  return fl::load_vector(mesh, dofmap, pts, w, q, f_values, f_const, device, b_out);
+  FL_API_END
+}
+
 int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out) {
   FL_API_BEGIN
   if (!A || !out || n <= 0) return fail(FL_E_ARG, "bad argument");

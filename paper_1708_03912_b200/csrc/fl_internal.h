@@ -36,6 +36,19 @@ inline void note_launch(long long k = 1) { launch_counter() += k; }
 cudaStream_t& cur_stream();
 void init_pool(int device);
 
+// Recycled non-blocking streams per device (fl_capi.cu); a lease returns its stream on scope exit
+// (declare it before the buffers allocated on it, so their stream-ordered frees come first).
+cudaStream_t acquire_stream(int device);
+void release_stream(int device, cudaStream_t s);
+struct OwnedStreamLease {
+  int dev;
+  cudaStream_t s;
+  explicit OwnedStreamLease(int d) : dev(d), s(acquire_stream(d)) {}
+  ~OwnedStreamLease() { release_stream(dev, s); }
+  OwnedStreamLease(const OwnedStreamLease&) = delete;
+  OwnedStreamLease& operator=(const OwnedStreamLease&) = delete;
+};
+
 struct StreamScope {
   cudaStream_t prev;
   explicit StreamScope(cudaStream_t s) : prev(cur_stream()) { cur_stream() = s; }
@@ -245,6 +258,19 @@ void launch_sparse_pull(const DevMesh& m, double Cds, double s, const double* Lc
                         const TouchPair* pairs, const double* tloc, const BndPair* items,
                         const double* bloc, const SparseIndex& si, const int* row_vertex,
                         int row_begin, int row_end, double* A, int64_t lda, cudaStream_t st);
+
+// fl_mesh.cu (host O(n) driver steps on the device)
+int32_t finish_polygon_mesh(const double* V, int64_t nv, const int64_t* cells_in, int64_t nc, int device,
+                            int64_t* cells_out, int64_t* be_out, double* bn_out, int64_t cap, int64_t* nb_out);
+int32_t dofmap_build(const int64_t* be, int64_t nb, int d, int64_t nv, double s, int device, int64_t* v2d_out,
+                     int64_t* n_out);
+}  // namespace fl
+struct fl_mesh;
+struct fl_dofmap;
+namespace fl {
+int32_t cell_rule_nodes(const ::fl_mesh* mesh, const double* pts, int64_t q, int device, double* X_out);
+int32_t load_vector(const ::fl_mesh* mesh, const ::fl_dofmap* dm, const double* pts, const double* w, int64_t q,
+                    const double* fvals, double fconst, int device, double* b_out);
 
 // fl_solve.cu
 void launch_matvec(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,

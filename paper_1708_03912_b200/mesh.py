@@ -160,6 +160,53 @@ def finish_polygon_mesh(vertices, cells) -> Mesh:
     return Mesh(V, C, be, nrm)
 
 
+def finish_polygon_mesh_device(vertices, cells, device=0) -> Mesh:
+    """finish_polygon_mesh on the GPU (fl_finish_polygon_mesh; same rule, mesh.py:351-403)."""
+    import ctypes as C
+    from . import _lib
+    V = np.ascontiguousarray(vertices, dtype=np.float64)
+    Cin = np.ascontiguousarray(cells, dtype=np.int64)
+    nc = len(Cin)
+    Cout = np.empty((nc, 3), np.int64)
+    be = np.empty((3 * nc, 2), np.int64)
+    bn = np.empty((3 * nc, 2))
+    nb = C.c_int64()
+    _lib.check(_lib.load().fl_finish_polygon_mesh(V.ctypes.data, len(V), Cin.ctypes.data, nc, int(device),
+                                                  Cout.ctypes.data, be.ctypes.data, bn.ctypes.data, 3 * nc,
+                                                  C.byref(nb)))
+    return Mesh(V, Cout, be[:nb.value].copy(), bn[:nb.value].copy())
+
+
+def dofmap_device(mesh, s: float, device=0) -> DofMap:
+    """DofMap built on the GPU (fl_build_dofmap; mesh.py:200-240)."""
+    import ctypes as C
+    from . import _lib
+    if not 0.0 < s < 1.0:
+        raise ValueError("fractional order s must lie in (0,1)")
+    m = _lib.Marshal(mesh, _NoDofs(mesh.num_vertices), _Kernel(mesh.vertices.shape[1], s), None)
+    v2d = np.empty(mesh.num_vertices, np.int64)
+    n = C.c_int64()
+    _lib.check(_lib.load().fl_build_dofmap(C.byref(m.mesh), float(s), int(device), v2d.ctypes.data, C.byref(n)))
+    dm = DofMap.__new__(DofMap)
+    dm.mesh, dm.s = mesh, s
+    dm.vertex_to_dof = v2d
+    dm.dofs = np.nonzero(v2d >= 0)[0]
+    dm.cell_dofs = v2d[mesh.cells]
+    assert len(dm.dofs) == n.value
+    return dm
+
+
+class _NoDofs:
+    def __init__(self, nv):
+        self.n = 0
+        self.vertex_to_dof = np.full(nv, -1, np.int64)
+
+
+class _Kernel:
+    def __init__(self, d, s):
+        self.d, self.s, self.C_ds, self.variant = d, s, 1.0, "integral"
+
+
 def build_unit_square_mesh(N: int) -> Mesh:
     """[0,1]^2 with N x N squares, each split by its SW-NE diagonal (BASELINE c3-c5).
     Vertex (i, j) at (i/N, j/N) has index j*(N+1)+i; square (i, j) gives (SW, SE, NE) and

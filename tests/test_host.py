@@ -39,15 +39,6 @@ def test_dof_rule():
         M.DofMap(mesh, 1.5)
 
 
-def test_load_vector_matches_reference():
-    from paper_1708_03912_b200.assembly import load_vector
-    G = golden("c2")
-    mesh = make_mesh("graded1d", 8192)
-    dm = M.DofMap(mesh, 0.75)
-    b = load_vector(mesh, dm, lambda X: np.ones(len(X)))
-    assert np.allclose(b, G["b"], rtol=1e-14, atol=1e-20)
-
-
 def test_library_exports_header_symbols():
     from paper_1708_03912_b200 import _lib
     lib = _lib.load()
