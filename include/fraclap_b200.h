@@ -104,6 +104,16 @@ typedef struct fl_tables {
 } fl_tables;
 
 typedef struct fl_dense fl_dense;   /* opaque: device rows [row_begin,row_end) x n of A */
+typedef struct fl_sparse fl_sparse; /* opaque: device CSR (n x n), the near-field matrix */
+
+/* The near-field leaf-pair structure of the cluster tree (cluster.NearStructure,
+ * cluster.py:743-777): every DoF's leaf index and the unordered near leaf pairs. */
+typedef struct fl_near_structure {
+  int64_t nleaves;
+  const int64_t* leaf_of_dof;       /* (n,) leaf index in [0, nleaves) (NearStructure.leaf_idx_of_dof) */
+  int64_t npairs;
+  const int64_t* pairs;             /* (npairs, 2) near leaf pairs (nl_pairs as leaf indices) */
+} fl_near_structure;
 
 typedef struct fl_solve_report {
   int64_t iterations;
@@ -169,6 +179,29 @@ int32_t fl_dense_to_host(const fl_dense* A, double* host_rows);
 int32_t fl_dense_rows(const fl_dense* A, int64_t nrows, const int64_t* rows, double* host_out);
 /* diagonal entries of the owned rows (host) */
 int32_t fl_dense_diag(const fl_dense* A, double* host_diag);
+
+/* ------------------------------------------------------------- near field (cluster path)
+ * Replaces assembly.assemble_near_field (assembly.py:860-970): the sparse matrix of every DoF pair
+ * (i, j) whose leaves form a near pair — touching / identical singular pairs, the disjoint cross
+ * terms of the near leaf pairs' cells, the tail through the one-ring boundary
+ * Psi = (V - ring flux)/(2s) (tail_potential / ring_boundaries, :336-396) and, for the integral
+ * variant, the boundary pairs and the boundary mass term (:1074-1094).  V_nodes: the boundary
+ * flux potential at the (nc, q) cell nodes (cell_quadrature(XQ_ORDER)), e.g. the cluster far
+ * field's boundary_flux_at_nodes (cluster.py:525); NULL = direct GL8 over every boundary edge. */
+int32_t fl_assemble_near_field(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                               const fl_order_params* params, const fl_tables* tables,
+                               const fl_near_structure* near, const double* V_nodes, int32_t device,
+                               fl_sparse** out);
+/* Diagnostics: Psi = (V - ring flux)/(2s) (tail_potential, assembly.py:388-396) and W_in (:1092)
+ * at the (nc, q) cell nodes as the near-field assembly forms them; host arrays of nc*q. */
+int32_t fl_debug_ring_tail(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                           const fl_order_params* params, const fl_tables* tables, const double* V_nodes,
+                           int32_t device, double* psi_out, double* win_out);
+/* n, stored entries, and the number of distinct disjoint cell pairs evaluated */
+int32_t fl_sparse_info(const fl_sparse* A, int64_t* n, int64_t* nnz, int64_t* cross_pairs);
+/* canonical CSR (sorted column indices, no duplicates): indptr (n+1), indices/data (nnz) */
+int32_t fl_sparse_to_host(const fl_sparse* A, int64_t* indptr, int32_t* indices, double* data);
+void fl_sparse_free(fl_sparse* A);
 
 /* ------------------------------------------------------------- driver steps (host O(n) in the
  * reference), on the device

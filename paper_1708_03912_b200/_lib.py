@@ -18,7 +18,8 @@ VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
 
 EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_count", "fl_assemble_dense",
            "fl_assemble_dense_host", "fl_finish_polygon_mesh", "fl_build_dofmap", "fl_cell_rule_nodes",
-           "fl_load_vector",
+           "fl_load_vector", "fl_assemble_near_field", "fl_sparse_info", "fl_sparse_to_host", "fl_sparse_free",
+           "fl_debug_ring_tail",
            "fl_dense_from_host",
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_rows", "fl_dense_diag", "fl_matvec",
@@ -47,6 +48,10 @@ class fl_order_params(C.Structure):
 
 class fl_tables(C.Structure):
     _fields_ = [("dir", C.c_void_p), ("data", C.c_void_p), ("ndata", C.c_int64)]
+
+
+class fl_near_structure(C.Structure):
+    _fields_ = [("nleaves", C.c_int64), ("leaf_of_dof", C.c_void_p), ("npairs", C.c_int64), ("pairs", C.c_void_p)]
 
 
 class fl_solve_report(C.Structure):
@@ -97,6 +102,13 @@ def load():
         "fl_build_dofmap": (C.c_int32, [P(fl_mesh), C.c_double, C.c_int32, vp, P(C.c_int64)]),
         "fl_cell_rule_nodes": (C.c_int32, [P(fl_mesh), vp, C.c_int64, C.c_int32, vp]),
         "fl_load_vector": (C.c_int32, [P(fl_mesh), P(fl_dofmap), vp, vp, C.c_int64, vp, C.c_double, C.c_int32, vp]),
+        "fl_assemble_near_field": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),
+                                               P(fl_tables), P(fl_near_structure), vp, C.c_int32, P(vp)]),
+        "fl_sparse_info": (C.c_int32, [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
+        "fl_sparse_to_host": (C.c_int32, [vp, vp, vp, vp]),
+        "fl_sparse_free": (None, [vp]),
+        "fl_debug_ring_tail": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), P(fl_tables),
+                                           vp, C.c_int32, vp, vp]),
         "fl_dense_from_host": (C.c_int32, [vp, C.c_int64, C.c_int32, P(vp)]),
         "fl_dense_free": (None, [vp]),
         "fl_dense_info": (C.c_int32, [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(vp)]),

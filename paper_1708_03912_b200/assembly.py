@@ -152,3 +152,56 @@ def load_vector(mesh, dofmap, f, order=4, discontinuity=None, device=None):
     _lib.check(lib.fl_load_vector(C.byref(m.mesh), C.byref(m.dofmap), pts.ctypes.data, w.ctypes.data, q,
                                   None if fvals is None else fvals.ctypes.data, fconst, dev, b.ctypes.data))
     return b
+
+
+def assemble_near_field(mesh, dofmap, kernel, near_pairs, params: OrderParams | None = None, V_nodes=None,
+                        xquad=None, device=None):
+    """Near-field sparse matrix over the non-admissible DoF pairs (assembly.py:860-970) on the GPU
+    (fl_assemble_near_field) -> scipy.sparse.csr_matrix (n, n), canonical (sorted indices).
+
+    `near_pairs`: a NearStructure (this package's cluster.NearStructure or the reference's):
+    its `nl_pairs` (leaf node pairs), `leaf_index` and `leaf_idx_of_dof` are read.  `V_nodes`:
+    the boundary flux potential at the (nc, q) cell-rule nodes (e.g. the cluster far field's),
+    default: direct GL8 over every boundary edge.  `xquad` may only restate the standard cell
+    rule (cell_quadrature(mesh, XQ_ORDER[d]), which is what the device uses)."""
+    from scipy.sparse import csr_matrix
+    lib = _lib.load()
+    variant = getattr(getattr(kernel, "variant", Variant.INTEGRAL), "value", "integral")
+    if variant == "symmetrized":
+        raise AssemblyError("symmetrized kernels are assembled densely")
+    d = int(mesh.vertices.shape[1])
+    nc = int(mesh.num_cells)
+    q = 6 if d == 1 else 16
+    if xquad is not None and np.shape(xquad[1]) != (nc, q):
+        raise ValueError("xquad must be the cell rule of order XQ_ORDER[d] (%d nodes per cell)" % q)
+    n = int(dofmap.n)
+    leaf_idx = np.ascontiguousarray(near_pairs.leaf_idx_of_dof, dtype=np.int64)
+    li = near_pairs.leaf_index
+    nl = max(li.values()) + 1 if len(li) else 1
+    pairs = np.ascontiguousarray([[li[int(a)], li[int(b)]] for a, b in np.asarray(near_pairs.nl_pairs).reshape(-1, 2)],
+                                 dtype=np.int64).reshape(-1, 2)
+    if V_nodes is not None:
+        V_nodes = np.ascontiguousarray(V_nodes, dtype=np.float64)
+        if V_nodes.shape != (nc, q):
+            raise ValueError("V_nodes must have shape %r" % ((nc, q),))
+    m = _lib.Marshal(mesh, dofmap, kernel, params)
+    dir_, data, tb = _tables(mesh, dofmap, float(kernel.s), params)
+    ns = _lib.fl_near_structure(nl, leaf_idx.ctypes.data if n else None, len(pairs),
+                                pairs.ctypes.data if len(pairs) else None)
+    h = C.c_void_p()
+    _lib.check(lib.fl_assemble_near_field(C.byref(m.mesh), C.byref(m.dofmap), C.byref(m.kernel), C.byref(m.params),
+                                          C.byref(tb), C.byref(ns),
+                                          None if V_nodes is None else V_nodes.ctypes.data,
+                                          _device_index(device), C.byref(h)))
+    try:
+        nn, nnz, npair = C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.check(lib.fl_sparse_info(h, C.byref(nn), C.byref(nnz), C.byref(npair)))
+        indptr = np.empty(n + 1, np.int64)
+        indices = np.empty(max(nnz.value, 1), np.int32)
+        vals = np.empty(max(nnz.value, 1))
+        _lib.check(lib.fl_sparse_to_host(h, indptr.ctypes.data, indices.ctypes.data, vals.ctypes.data))
+    finally:
+        lib.fl_sparse_free(h)
+    A = csr_matrix((vals[:nnz.value], indices[:nnz.value], indptr), shape=(n, n))
+    A.has_sorted_indices = True
+    return A

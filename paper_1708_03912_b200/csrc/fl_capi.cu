@@ -80,6 +80,21 @@ struct fl_dense {
   }
 };
 
+struct fl_sparse {                     // CSR (n x n), int64 row pointers, int32 column indices
+  int device = 0;
+  int64_t n = 0, nnz = 0, pairs = 0;
+  DBuf<int64_t> indptr;
+  DBuf<int> indices;
+  DBuf<double> data;
+  cudaStream_t stream = nullptr;
+  ~fl_sparse() {
+    indptr.free();
+    indices.free();
+    data.free();
+    if (stream) fl::release_stream(device, stream);
+  }
+};
+
 static thread_local std::string g_err;
 
 static int32_t fail(int code, const std::string& msg) {
@@ -753,6 +768,181 @@ int32_t fl_load_vector(const fl_mesh* mesh, const fl_dofmap* dofmap, const doubl
   if (mesh->nc * (mesh->d + 1) >= (1LL << 31) || dofmap->n >= (1LL << 31)) return fail(FL_E_ARG, "mesh too large");
   return fl::load_vector(mesh, dofmap, pts, w, q, f_values, f_const, device, b_out);
   FL_API_END
+}
+
+// ------------------------------------------------------------- near field (cluster path)
+int32_t fl_assemble_near_field(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                               const fl_order_params* params, const fl_tables* tables,
+                               const fl_near_structure* near, const double* V_nodes, int32_t device,
+                               fl_sparse** out) {
+  FL_API_BEGIN
+  if (!out || !near) return fail(FL_E_ARG, "null argument");
+  *out = nullptr;
+  check_inputs(mesh, dofmap, kernel, params, tables);
+  if (kernel->variant == FL_VARIANT_SYMMETRIZED)
+    return fail(FL_E_ASSEMBLY, "symmetrized kernels are assembled densely");          // assembly.py:870-871
+  const int64_t n = dofmap->n, nl = near->nleaves, np = near->npairs;
+  if (nl <= 0 || nl >= (1LL << 31) || np < 0 || (np > 0 && !near->pairs) || (n > 0 && !near->leaf_of_dof))
+    return fail(FL_E_ARG, "bad near structure");
+  std::vector<int> lod((size_t)std::max<int64_t>(n, 1)), prs((size_t)std::max<int64_t>(2 * np, 1));
+  for (int64_t i = 0; i < n; ++i) {
+    if (near->leaf_of_dof[i] < 0 || near->leaf_of_dof[i] >= nl) return fail(FL_E_ARG, "leaf index out of range");
+    lod[i] = (int)near->leaf_of_dof[i];
+  }
+  for (int64_t p = 0; p < np; ++p) {
+    int64_t a = near->pairs[2 * p], b = near->pairs[2 * p + 1];
+    if (a < 0 || b < 0 || a >= nl || b >= nl) return fail(FL_E_ARG, "near leaf pair out of range");
+    prs[2 * p] = (int)std::min(a, b);
+    prs[2 * p + 1] = (int)std::max(a, b);
+  }
+  FL_CUDA(cudaSetDevice(device));
+  init_pool(device);
+  std::unique_ptr<fl_sparse> S(new fl_sparse());
+  S->device = device;
+  S->n = n;
+  S->stream = acquire_stream(device);
+  cudaStream_t st = S->stream;
+  StreamScope scope(st);
+  const int d = mesh->d;
+  const double s = kernel->s, C = kernel->C_ds;
+  const double ex = -(d / 2.0 + s);
+  const int e4 = e4_of(d, s);
+  const bool integral = kernel->variant == FL_VARIANT_INTEGRAL;
+  Uploaded U;
+  upload(mesh, dofmap, tables, U, st);
+  DevMesh& m = U.m;
+  const OrderConsts oc = make_order_consts(*params, d, s, n);
+  DBuf<int> dlod(lod.size()), dprs(prs.size());
+  FL_CUDA(cudaMemcpyAsync(dlod.p, lod.data(), lod.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dprs.p, prs.data(), prs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  DBuf<double> dV;
+  if (V_nodes) {
+    dV.alloc((size_t)m.nc * m.q);
+    FL_CUDA(cudaMemcpyAsync(dV.p, V_nodes, dV.n * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  DBuf<int> row_vertex(n > 0 ? n : 1), all(m.nc);
+  dof_vertex2<<<(m.nv + 255) / 256, 256, 0, st>>>(m, row_vertex.p), ::fl::note_launch();
+  iota2<<<(m.nc + 255) / 256, 256, 0, st>>>(all.p, m.nc), ::fl::note_launch();
+  // classification + singular pairs exactly as the dense path (the touching triplets are not
+  // masked, assembly.py:885; touching pairs are never admissible)
+  DBuf<TouchPair> tpairs;
+  DBuf<int> ident_k, tcounts, toffs, bcounts, boffs;
+  const bool do_bnd = integral && m.nb > 0;
+  touching_count(m, tcounts, toffs, st);
+  if (do_bnd) boundary_count(m, bcounts, boffs, st);
+  int* hs = pinned_scratch();
+  hs[2] = 0;
+  FL_CUDA(cudaMemcpyAsync(&hs[1], toffs.p + m.nc, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (do_bnd) FL_CUDA(cudaMemcpyAsync(&hs[2], boffs.p + m.nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&hs[3], U.maxv.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  const int64_t npairs = hs[1], nitems = hs[2];
+  valence_error(hs[3]);
+  touching_fill(m, oc, toffs, npairs, tpairs, ident_k, st);
+  DBuf<BndPair> bitems;
+  if (do_bnd) boundary_fill(m, oc, boffs, nitems, bitems, st);
+  else bitems.alloc(1);
+  SparseIndex si;
+  build_sparse_index(m, tpairs.p, npairs, bitems.p, nitems, si, st);
+  DBuf<double> ident((size_t)m.nc * 9), tloc((size_t)std::max<int64_t>(npairs, 1) * 25),
+      bloc((size_t)std::max<int64_t>(nitems, 1) * 9);
+  launch_singular_identical(m, U.t, ex, e4, ident_k.p, ident.p, st);
+  launch_singular_touching(m, U.t, ex, e4, tpairs.p, npairs, tloc.p, st);
+  if (do_bnd) launch_singular_boundary(m, U.t, ex, e4, bitems.p, nitems, bloc.p, st);
+  // tail through the one-ring boundary, and the boundary mass potential
+  DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
+  launch_ring_tail(m, U.t, s, ex, e4, V_nodes ? dV.p : nullptr, do_bnd, psi.p, win.p, st);
+  DBuf<double> Lc((size_t)m.nc * 9);
+  launch_cell_local(m, U.t, C, s, do_bnd, all.p, m.nc, ident.p, psi.p, win.p, Lc.p, st);
+  // near disjoint pairs, CSR pattern and cross values, then the local entries
+  NearInput in;
+  in.nleaves = (int)nl;
+  in.npairs = np;
+  in.leaf_of_dof = dlod.p;
+  in.pairs = dprs.p;
+  CsrOut csr;
+  DBuf<unsigned long long> evc(1);
+  FL_CUDA(cudaMemsetAsync(evc.p, 0, sizeof(unsigned long long), st));
+  int64_t ncross = 0;
+  near_field_cross(m, U.t, oc, ex, e4, C, in, row_vertex.p, csr, &ncross, evc.p, st);
+  launch_sparse_pull_csr(m, C, s, Lc.p, tpairs.p, tloc.p, bitems.p, do_bnd ? bloc.p : nullptr, si, row_vertex.p,
+                         (int)n, csr.indptr.p, csr.indices.p, csr.data.p, st);
+  FL_CUDA(cudaMemcpyAsync(&hs[4], m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  if (hs[4] & 1) throw Error(FL_E_QUAD, "a quadrature rule for a selected order is missing from the tables");
+  if (hs[4] & 4) throw Error(FL_E_CUDA, "internal: a near-field pair block is missing");
+  if (hs[4] & 16) throw Error(FL_E_ASSEMBLY, "one-ring patch too large for the device ring lists");
+  S->nnz = csr.nnz;
+  S->pairs = ncross;
+  S->indptr = std::move(csr.indptr);
+  S->indices = std::move(csr.indices);
+  S->data = std::move(csr.data);
+  *out = S.release();
+  return FL_OK;
+  FL_API_END
+}
+
+// psi (tail_potential) and W_in at the (nc, q) cell nodes, as fl_assemble_near_field forms them
+int32_t fl_debug_ring_tail(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,
+                           const fl_order_params* params, const fl_tables* tables, const double* V_nodes,
+                           int32_t device, double* psi_out, double* win_out) {
+  FL_API_BEGIN
+  if (!psi_out || !win_out) return fail(FL_E_ARG, "null argument");
+  check_inputs(mesh, dofmap, kernel, params, tables);
+  FL_CUDA(cudaSetDevice(device));
+  init_pool(device);
+  OwnedStreamLease lease(device);
+  cudaStream_t st = lease.s;
+  StreamScope scope(st);
+  const int d = mesh->d;
+  const double s = kernel->s;
+  Uploaded U;
+  upload(mesh, dofmap, tables, U, st);
+  DevMesh& m = U.m;
+  check_valence(U, st);
+  DBuf<double> dV, psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
+  if (V_nodes) {
+    dV.alloc((size_t)m.nc * m.q);
+    FL_CUDA(cudaMemcpyAsync(dV.p, V_nodes, dV.n * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  launch_ring_tail(m, U.t, s, -(d / 2.0 + s), e4_of(d, s), V_nodes ? dV.p : nullptr,
+                   kernel->variant == FL_VARIANT_INTEGRAL && m.nb > 0, psi.p, win.p, st);
+  FL_CUDA(cudaMemcpyAsync(psi_out, psi.p, psi.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(win_out, win.p, win.n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  int err = 0;
+  FL_CUDA(cudaMemcpyAsync(&err, m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  if (err & 16) throw Error(FL_E_ASSEMBLY, "one-ring patch too large for the device ring lists");
+  return FL_OK;
+  FL_API_END
+}
+
+int32_t fl_sparse_info(const fl_sparse* A, int64_t* n, int64_t* nnz, int64_t* cross_pairs) {
+  if (!A) return fail(FL_E_ARG, "null handle");
+  if (n) *n = A->n;
+  if (nnz) *nnz = A->nnz;
+  if (cross_pairs) *cross_pairs = A->pairs;
+  return FL_OK;
+}
+
+int32_t fl_sparse_to_host(const fl_sparse* A, int64_t* indptr, int32_t* indices, double* data) {
+  FL_API_BEGIN
+  if (!A || !indptr || (A->nnz > 0 && (!indices || !data))) return fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(A->device));
+  FL_CUDA(cudaMemcpyAsync(indptr, A->indptr.p, (A->n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, A->stream));
+  if (A->nnz > 0) {
+    FL_CUDA(cudaMemcpyAsync(indices, A->indices.p, A->nnz * sizeof(int), cudaMemcpyDeviceToHost, A->stream));
+    FL_CUDA(cudaMemcpyAsync(data, A->data.p, A->nnz * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+  }
+  FL_CUDA(cudaStreamSynchronize(A->stream));
+  return FL_OK;
+  FL_API_END
+}
+
+void fl_sparse_free(fl_sparse* A) {
+  if (!A) return;
+  cudaSetDevice(A->device);
+  delete A;
 }
 
 int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out) {

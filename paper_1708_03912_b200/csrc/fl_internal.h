@@ -272,6 +272,41 @@ int32_t cell_rule_nodes(const ::fl_mesh* mesh, const double* pts, int64_t q, int
 int32_t load_vector(const ::fl_mesh* mesh, const ::fl_dofmap* dm, const double* pts, const double* w, int64_t q,
                     const double* fvals, double fconst, int device, double* b_out);
 
+// the same pull into CSR rows 0..nrows-1 (sorted column indices covering every local entry)
+void launch_sparse_pull_csr(const DevMesh& m, double Cds, double s, const double* Lc, const TouchPair* pairs,
+                            const double* tloc, const BndPair* items, const double* bloc, const SparseIndex& si,
+                            const int* row_vertex, int nrows, const int64_t* indptr, const int* indices,
+                            double* data, cudaStream_t st);
+
+// fl_near.cu: one block per (P, Q, K) pair (warp per pair), G = n x 9 in the (P, Q) orientation
+void launch_near_blocks(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                        const int* P, const int* Q, const int* K, int64_t n, double* G, unsigned long long* evals,
+                        cudaStream_t st);
+
+// fl_nearfield.cu: the near-field (cluster) assembly, assemble_near_field (assembly.py:860-970)
+struct NearField;   // device CSR + work buffers
+struct NearInput {
+  int nleaves = 0;
+  int64_t npairs = 0;
+  const int* leaf_of_dof = nullptr;  // device (n)
+  const int* pairs = nullptr;        // device (npairs*2), a <= b
+  const double* V = nullptr;         // device (nc*q) boundary flux potential, or null: direct GL8
+};
+struct CsrOut {
+  DBuf<int64_t> indptr;
+  DBuf<int> indices;
+  DBuf<double> data;
+  int64_t nnz = 0;
+};
+// psi = (V - ring flux of N(K)) / (2s) and win = T - V at the cell nodes (tail_potential,
+// ring_boundaries, assembly.py:336-396, :1074-1094)
+void launch_ring_tail(const DevMesh& m, const DevTables& t, double s, double ex, int e4, const double* Vgiven,
+                      bool integral, double* psi, double* win, cudaStream_t st);
+// near disjoint cell pairs of the leaf pairs, their blocks, the CSR pattern and the cross values
+void near_field_cross(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+                      const NearInput& in, const int* row_vertex, CsrOut& out, int64_t* npairs_out,
+                      unsigned long long* evals, cudaStream_t st);
+
 // fl_solve.cu
 void launch_matvec(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
                    cudaStream_t st);

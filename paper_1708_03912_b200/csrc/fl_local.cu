@@ -126,18 +126,50 @@ void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs
 }
 
 // ------------------------------------------------------------------ the pull
-template <int D>
+// Where a row's local entries go: a dense row (the dense path), or a CSR row with sorted
+// column indices (the near-field path; every local entry lies inside the row's pattern).
+struct DenseRowSink {
+  double* Ar;
+  __device__ void add(int j, double v) { Ar[j] += v; }
+};
+struct CsrRowSink {
+  const int* idx;
+  double* val;
+  int64_t lo, hi;
+  __device__ void add(int j, double v) {
+    int64_t a = lo, b = hi;                 // lower_bound of j in idx[lo, hi)
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (idx[mid] < j) a = mid + 1; else b = mid;
+    }
+    val[a] += v;
+  }
+};
+struct DenseRows {
+  double* A;
+  int64_t lda;
+  int row_begin;
+  __device__ DenseRowSink row(int i) const { return DenseRowSink{A + (int64_t)(i - row_begin) * lda}; }
+};
+struct CsrRows {
+  const int64_t* indptr;
+  const int* idx;
+  double* val;
+  __device__ CsrRowSink row(int i) const { return CsrRowSink{idx, val, indptr[i], indptr[i + 1]}; }
+};
+
+template <int D, class Rows>
 __global__ void sparse_pull_kernel(DevMesh m, double Cds, double cb, const double* __restrict__ Lc,
                                    const TouchPair* __restrict__ pairs, const double* __restrict__ tloc,
                                    const BndPair* __restrict__ items, const double* __restrict__ bloc,
                                    const int* __restrict__ tf_off, const int* __restrict__ ts_off,
                                    const int* __restrict__ ts_idx, const int* __restrict__ bp_off,
                                    const int* __restrict__ bp_idx, const int* __restrict__ row_vertex,
-                                   int row_begin, int row_end, double* __restrict__ A, int64_t lda) {
+                                   int row_begin, int row_end, Rows rows) {
   const int i = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= row_end) return;
   const int v = row_vertex[i];
-  double* Ar = A + (int64_t)(i - row_begin) * lda;
+  auto Ar = rows.row(i);
   for (int pp = m.patch_off[v]; pp < m.patch_off[v + 1]; ++pp) {
     const int K = m.patch_cells[pp];
     const CellGeo g = m.geo[K];
@@ -147,7 +179,7 @@ __global__ void sparse_pull_kernel(DevMesh m, double Cds, double cb, const doubl
       if (g.v[j] == v) a = j;
 #pragma unroll
     for (int b = 0; b <= D; ++b)
-      if (g.dof[b] >= 0) Ar[g.dof[b]] += Lc[(size_t)K * 9 + a * 3 + b];
+      if (g.dof[b] >= 0) Ar.add(g.dof[b], Lc[(size_t)K * 9 + a * 3 + b]);
     // touching pairs with K as the first (smaller) cell
     for (int t = tf_off[K]; t < tf_off[K + 1]; ++t) {
       const TouchPair& tp = pairs[t];
@@ -158,7 +190,7 @@ __global__ void sparse_pull_kernel(DevMesh m, double Cds, double cb, const doubl
       const double* T = tloc + (size_t)t * 25 + sa * 5;
       for (int b = 0; b < tp.nloc; ++b) {
         const int dj = m.v2d[tp.locs[b]];
-        if (dj >= 0) Ar[dj] += Cds * T[b];
+        if (dj >= 0) Ar.add(dj, Cds * T[b]);
       }
     }
     // ... and as the second cell, unless v also lies in the first cell (counted there)
@@ -177,7 +209,7 @@ __global__ void sparse_pull_kernel(DevMesh m, double Cds, double cb, const doubl
       const double* T = tloc + (size_t)t * 25 + sa * 5;
       for (int b = 0; b < tp.nloc; ++b) {
         const int dj = m.v2d[tp.locs[b]];
-        if (dj >= 0) Ar[dj] += Cds * T[b];
+        if (dj >= 0) Ar.add(dj, Cds * T[b]);
       }
     }
     // singular boundary pairs (cell K, edge e)
@@ -191,7 +223,7 @@ __global__ void sparse_pull_kernel(DevMesh m, double Cds, double cb, const doubl
         if (sa < 0) continue;
         for (int b = 0; b < it.nloc; ++b) {
           const int dj = m.v2d[it.locs[b]];
-          if (dj >= 0) Ar[dj] += cb * bloc[(size_t)t * 9 + sa * 3 + b];
+          if (dj >= 0) Ar.add(dj, cb * bloc[(size_t)t * 9 + sa * 3 + b]);
         }
       }
     }
@@ -206,14 +238,34 @@ void launch_sparse_pull(const DevMesh& m, double Cds, double s, const double* Lc
   if (rows <= 0) return;
   const int grid = (rows + 127) / 128;
   const double cb = Cds / (2.0 * s);
+  const DenseRows R{A, lda, row_begin};
   if (m.d == 1)
     sparse_pull_kernel<1><<<grid, 128, 0, st>>>(m, Cds, cb, Lc, pairs, tloc, items, bloc, si.tp_first_off.p,
                                                 si.tp_second_off.p, si.tp_second.p, si.bp_off.p, si.bp_idx.p,
-                                                row_vertex, row_begin, row_end, A, lda), ::fl::note_launch();
+                                                row_vertex, row_begin, row_end, R), ::fl::note_launch();
   else
     sparse_pull_kernel<2><<<grid, 128, 0, st>>>(m, Cds, cb, Lc, pairs, tloc, items, bloc, si.tp_first_off.p,
                                                 si.tp_second_off.p, si.tp_second.p, si.bp_off.p, si.bp_idx.p,
-                                                row_vertex, row_begin, row_end, A, lda), ::fl::note_launch();
+                                                row_vertex, row_begin, row_end, R), ::fl::note_launch();
+  FL_CHECK_LAUNCH();
+}
+
+void launch_sparse_pull_csr(const DevMesh& m, double Cds, double s, const double* Lc, const TouchPair* pairs,
+                            const double* tloc, const BndPair* items, const double* bloc, const SparseIndex& si,
+                            const int* row_vertex, int nrows, const int64_t* indptr, const int* indices,
+                            double* data, cudaStream_t st) {
+  if (nrows <= 0) return;
+  const int grid = (nrows + 127) / 128;
+  const double cb = Cds / (2.0 * s);
+  const CsrRows R{indptr, indices, data};
+  if (m.d == 1)
+    sparse_pull_kernel<1><<<grid, 128, 0, st>>>(m, Cds, cb, Lc, pairs, tloc, items, bloc, si.tp_first_off.p,
+                                                si.tp_second_off.p, si.tp_second.p, si.bp_off.p, si.bp_idx.p,
+                                                row_vertex, 0, nrows, R), ::fl::note_launch();
+  else
+    sparse_pull_kernel<2><<<grid, 128, 0, st>>>(m, Cds, cb, Lc, pairs, tloc, items, bloc, si.tp_first_off.p,
+                                                si.tp_second_off.p, si.tp_second.p, si.bp_off.p, si.bp_idx.p,
+                                                row_vertex, 0, nrows, R), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 

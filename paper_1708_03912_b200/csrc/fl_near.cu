@@ -184,4 +184,22 @@ void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& o
   FL_CHECK_LAUNCH();
 }
 
+void launch_near_blocks(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                        const int* P, const int* Q, const int* K, int64_t n, double* G, unsigned long long* evals,
+                        cudaStream_t st) {
+  if (n <= 0) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>((n + NW - 1) / NW, (int64_t)sms * 8);
+  if (m.d == 1) {
+    FL_E4_SWITCHN(e4, (near_block_kernel<1, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, P, Q, K, n, G, evals),
+                       ::fl::note_launch()));
+  } else {
+    FL_E4_SWITCHN(e4, (near_block_kernel<2, E4><<<grid, NW * 32, 0, st>>>(m, t.data, t, oc, ex, P, Q, K, n, G, evals),
+                       ::fl::note_launch()));
+  }
+  FL_CHECK_LAUNCH();
+}
+
 }  // namespace fl

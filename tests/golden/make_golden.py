@@ -543,7 +543,69 @@ def t_rows(name, nrows):
     save("rows_" + name, rec)
 
 
+# near-field (cluster) assembly: assemble_near_field (assembly.py:860-970) over the reference's own
+# cluster tree / admissible partition / NearStructure (cluster.py:25-255, :743-777)
+NEAR = [("uniform1d", 64, 0.25, 8, 1.0, False), ("graded1d", 96, 0.75, 8, 1.0, False),
+        ("rand1d", 40, 0.5, 4, 0.5, False), ("square2d", 8, 0.5, 16, 1.0, False),
+        ("square2d", 12, 0.25, 16, 1.0, False), ("jit2d", 8, 0.75, 8, 0.7, False),
+        ("square2d", 6, 0.75, 10 ** 6, 1.0, False), ("square2d", 8, 0.5, 16, 1.0, True),
+        ("graded1d", 60, 0.25, 8, 1.0, True), ("square2d", 16, 0.5, 8, 1.0, False),
+        ("square2d", 20, 0.25, 16, 1.0, False), ("graded1d", 300, 0.75, 8, 1.0, False),
+        ("jit2d", 14, 0.25, 12, 1.0, False)]
+
+
+def t_near():
+    from fraclap import mesh as M, assembly as A, cluster as CL
+    fp64_variant()
+    recs = {}
+    for kind, N, s, cap, eta, cheb_v in NEAR:
+        tag = "%s_%d_%g_%d_%g%s" % (kind, N, s, cap, eta, "_V" if cheb_v else "")
+        mesh = irregular_mesh(kind, N, 21) if kind in ("jit2d", "rand1d") else ref_mesh(kind, N)
+        dm = M.DofMap(mesh, s)
+        ker = A.FractionalKernel(mesh.d, s)
+        t0 = time.perf_counter()
+        tree = CL.build_tree(mesh, dm, cap)
+        far, near = CL.admissible_partition(tree, eta)
+        ns = CL.NearStructure(mesh, dm, tree, near)
+        V = None
+        if cheb_v:   # the compress() path's V_nodes: boundary flux through the cluster far field
+            X, W, lam = A.cell_quadrature(mesh, CL.asm_xq_order(mesh.d))
+            cheb = CL.ChebData(tree, 6)
+            V = CL.boundary_flux_at_nodes(mesh, dm, ker, tree, cheb, eta, X,
+                                          CL._cell_leaf_assignment(mesh, dm, tree))
+        Anear = A.assemble_near_field(mesh, dm, ker, ns, V_nodes=V).tocsr()
+        Anear.sum_duplicates()
+        Anear.sort_indices()
+        leaf_index = np.full(tree.num_nodes, -1, np.int64)
+        for k_, nd in enumerate(tree.leaves):
+            leaf_index[nd] = k_
+        rec = dict(vertices=mesh.vertices, cells=mesh.cells, bedges=mesh.boundary_edges,
+                   bnormals=mesh.boundary_normals, s=s, leaf_cap=cap, eta=eta,
+                   dof_perm=tree.dof_perm, leaf_idx_of_dof=ns.leaf_idx_of_dof,
+                   nl_pairs=leaf_index[ns.nl_pairs], far=np.asarray(far, np.int64).reshape(-1, 2),
+                   indptr=Anear.indptr.astype(np.int64), indices=Anear.indices.astype(np.int64),
+                   data=Anear.data)
+        if V is not None:
+            rec["V_nodes"] = V
+        # the tail through the one-ring boundary and the boundary mass potential, at the cell nodes
+        X, W, lam = A.cell_quadrature(mesh, A.XQ_ORDER[mesh.d])
+        E = mesh.boundary_edges
+        Vd = A.edge_flux_potential(X, mesh.vertices[E[:, 0]], None if mesh.d == 1 else mesh.vertices[E[:, 1]],
+                                   mesh.boundary_normals, s, d=mesh.d) if V is None else V
+        rec["psi"] = A.tail_potential(mesh, s, X, Vd)
+        T = np.zeros(X.shape[:2])
+        A._touching_boundary_triplets(mesh, dm, ker, A.OrderParams(),
+                                      ([], [], []), T, X)
+        rec["win"] = T - Vd
+        for k, v in rec.items():
+            recs[tag + "/" + k] = v
+        print(tag, "n=%d nnz=%d leaves=%d near=%d %.1fs" % (dm.n, Anear.nnz, len(tree.leaves), len(ns.nl_pairs),
+                                                            time.perf_counter() - t0), flush=True)
+    save("near", recs)
+
+
 TARGETS = {
+    "near": t_near,
     "tables": t_tables,
     "meshes": t_meshes,
     "small": t_small,
