@@ -203,6 +203,40 @@ int32_t fl_sparse_info(const fl_sparse* A, int64_t* n, int64_t* nnz, int64_t* cr
 int32_t fl_sparse_to_host(const fl_sparse* A, int64_t* indptr, int32_t* indices, double* data);
 void fl_sparse_free(fl_sparse* A);
 
+/* ------------------------------------------------------------- cluster operator (H-matrix)
+ * The operator cluster.compress builds (cluster.py:667-712) and its matvec (ClusterOperator.matvec,
+ * cluster.py:417-456): y = A_near x - C * far(x), far(x) through the leaf moments, the upward
+ * shifts, the far-pair kernel blocks, the downward shifts and the leaf evaluation.  Arrays are the
+ * operator's own (tree.parent / topo_order / ranges / dof_perm, cheb.shift, basis_coef,
+ * far_pairs, far_blocks, near CSR).  far_blocks NULL: built on the device from `points`
+ * (cheb.points, (num_nodes, M, d)) as |xi_a - xi_b|^(-d-2s) (compress, :683-694). */
+typedef struct fl_cluster fl_cluster;
+typedef struct fl_cluster_desc {
+  int32_t d, m;                     /* dimension; Chebyshev points per direction (M = m^d) */
+  int64_t n, num_nodes;
+  const int64_t* parent;            /* (num_nodes,) -1 at the root */
+  const int64_t* topo_order;        /* (num_nodes,) breadth-first, root first */
+  const int64_t* ranges;            /* (num_nodes, 2) slices of dof_perm */
+  const int64_t* dof_perm;          /* (n,) */
+  const double* shift;              /* (num_nodes, d, m, m): S[j][alpha, beta] = L_alpha^parent(xi_beta^node) */
+  const double* basis_coef;         /* (n, M): int phi_i L_alpha^leaf(i) */
+  int64_t npairs;
+  const int64_t* far_pairs;         /* (npairs, 2) unordered admissible node pairs */
+  const double* far_blocks;         /* (npairs, M, M) or NULL */
+  const double* points;             /* (num_nodes, M, d) or NULL */
+  double s, C;                      /* fractional order (device-built blocks); C(d, s) */
+  int64_t nnz;                      /* near field CSR (n x n) */
+  const int64_t* indptr;
+  const int64_t* indices;
+  const double* data;
+} fl_cluster_desc;
+int32_t fl_cluster_create(const fl_cluster_desc* desc, int32_t device, fl_cluster** out);
+/* y = A x (and y_far = the far part alone, if non-NULL); ptr_kind 0: host arrays, 1: device */
+int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_far, int32_t ptr_kind);
+/* the device far blocks (npairs, M, M) */
+int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out);
+void fl_cluster_free(fl_cluster* C);
+
 /* ------------------------------------------------------------- driver steps (host O(n) in the
  * reference), on the device
  * _finish_polygon_mesh + _boundary_of (mesh.py:351-403): cells_out (nc x 3) CCW with the longest

@@ -19,7 +19,7 @@ VARIANT_ID = {"integral": 0, "regional": 1, "symmetrized": 2}
 EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_count", "fl_assemble_dense",
            "fl_assemble_dense_host", "fl_finish_polygon_mesh", "fl_build_dofmap", "fl_cell_rule_nodes",
            "fl_load_vector", "fl_assemble_near_field", "fl_sparse_info", "fl_sparse_to_host", "fl_sparse_free",
-           "fl_debug_ring_tail",
+           "fl_debug_ring_tail", "fl_cluster_create", "fl_cluster_matvec", "fl_cluster_far_blocks", "fl_cluster_free",
            "fl_dense_from_host",
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_rows", "fl_dense_diag", "fl_matvec",
@@ -52,6 +52,14 @@ class fl_tables(C.Structure):
 
 class fl_near_structure(C.Structure):
     _fields_ = [("nleaves", C.c_int64), ("leaf_of_dof", C.c_void_p), ("npairs", C.c_int64), ("pairs", C.c_void_p)]
+
+
+class fl_cluster_desc(C.Structure):
+    _fields_ = [("d", C.c_int32), ("m", C.c_int32), ("n", C.c_int64), ("num_nodes", C.c_int64),
+                ("parent", C.c_void_p), ("topo_order", C.c_void_p), ("ranges", C.c_void_p), ("dof_perm", C.c_void_p),
+                ("shift", C.c_void_p), ("basis_coef", C.c_void_p), ("npairs", C.c_int64), ("far_pairs", C.c_void_p),
+                ("far_blocks", C.c_void_p), ("points", C.c_void_p), ("s", C.c_double), ("C", C.c_double),
+                ("nnz", C.c_int64), ("indptr", C.c_void_p), ("indices", C.c_void_p), ("data", C.c_void_p)]
 
 
 class fl_solve_report(C.Structure):
@@ -107,6 +115,10 @@ def load():
         "fl_sparse_info": (C.c_int32, [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64)]),
         "fl_sparse_to_host": (C.c_int32, [vp, vp, vp, vp]),
         "fl_sparse_free": (None, [vp]),
+        "fl_cluster_create": (C.c_int32, [P(fl_cluster_desc), C.c_int32, P(vp)]),
+        "fl_cluster_matvec": (C.c_int32, [vp, vp, vp, vp, C.c_int32]),
+        "fl_cluster_far_blocks": (C.c_int32, [vp, vp]),
+        "fl_cluster_free": (None, [vp]),
         "fl_debug_ring_tail": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), P(fl_tables),
                                            vp, C.c_int32, vp, vp]),
         "fl_dense_from_host": (C.c_int32, [vp, C.c_int64, C.c_int32, P(vp)]),

@@ -161,3 +161,113 @@ class NearStructure:
 
     def near_mask(self, I, J):
         return self.mask[self.leaf_idx_of_dof[I], self.leaf_idx_of_dof[J]]
+
+
+class ClusterOperatorDevice:
+    """The cluster (H-matrix) stiffness operator with its matvec on the GPU (fl_cluster_*):
+    ClusterOperator.matvec (cluster.py:417-456) = near CSR product + Chebyshev far field (leaf
+    moments, upward shifts, far-pair blocks, downward shifts, leaf evaluation), in the
+    reference's accumulation order.  Duck-types the reference's solver contract (`.matvec`,
+    `.diag()`, `@`), so the reference's own pcg / multigrid can run on it.
+
+    `from_operator(op)` wraps an operator built by the reference's `cluster.compress` (or any
+    object with its attributes: tree, cheb, near, far_pairs, far_blocks, basis_coef, kernel)."""
+
+    def __init__(self, handle, n, diag, d, M):
+        self._h = handle
+        self.n = int(n)
+        self._diag = diag
+        self.d, self.M = d, M
+        self.shape = (self.n, self.n)
+        self.dtype = np.float64
+
+    @classmethod
+    def from_arrays(cls, d, m, parent, topo_order, ranges, dof_perm, shift, basis_coef, far_pairs, far_blocks,
+                    points, s, C_ds, near, diag=None, device=None):
+        import ctypes as C
+        from scipy.sparse import csr_matrix
+        from . import _lib
+        i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)           # noqa: E731
+        f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)         # noqa: E731
+        near = csr_matrix(near)
+        near.sum_duplicates()
+        n = near.shape[0]
+        M = m ** d
+        keep = dict(parent=i64(parent), topo=i64(topo_order), ranges=i64(ranges).reshape(-1, 2),
+                    perm=i64(dof_perm), shift=f64(shift).reshape(-1, d, m, m), bc=f64(basis_coef).reshape(n, M),
+                    pairs=i64(far_pairs).reshape(-1, 2), indptr=i64(near.indptr), indices=i64(near.indices),
+                    data=f64(near.data))
+        keep["blocks"] = None if far_blocks is None else f64(far_blocks).reshape(-1, M, M)
+        keep["points"] = None if points is None else f64(points)
+        ptr = lambda a: None if a is None or a.size == 0 else a.ctypes.data   # noqa: E731
+        desc = _lib.fl_cluster_desc(d, m, n, len(keep["parent"]), ptr(keep["parent"]), ptr(keep["topo"]),
+                                    ptr(keep["ranges"]), ptr(keep["perm"]), ptr(keep["shift"]), ptr(keep["bc"]),
+                                    len(keep["pairs"]), ptr(keep["pairs"]), ptr(keep["blocks"]), ptr(keep["points"]),
+                                    float(s), float(C_ds), int(near.nnz), ptr(keep["indptr"]), ptr(keep["indices"]),
+                                    ptr(keep["data"]))
+        from .assembly import _device_index
+        h = C.c_void_p()
+        _lib.check(_lib.load().fl_cluster_create(C.byref(desc), _device_index(device), C.byref(h)))
+        return cls(h, n, near.diagonal().copy() if diag is None else np.asarray(diag, float), d, M)
+
+    @classmethod
+    def from_operator(cls, op, device=None, build_blocks_on_device=False):
+        tree, cheb = op.tree, op.cheb
+        d, m = int(cheb.d), int(cheb.m)
+        nn = int(tree.num_nodes)
+        shift = np.zeros((nn, d, m, m))
+        for nd in range(nn):
+            if cheb.shift[nd] is not None:
+                for j in range(d):
+                    shift[nd, j] = cheb.shift[nd][j]
+        return cls.from_arrays(d, m, tree.parent, tree.topo_order, tree.ranges, tree.dof_perm, shift, op.basis_coef,
+                               op.far_pairs, None if build_blocks_on_device else op.far_blocks, cheb.points,
+                               op.kernel.s, op.kernel.C_ds, op.near, op.diag(), device)
+
+    # ------------------------------------------------------------ contract
+    def _apply(self, x, want_far=False):
+        from . import _lib
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise ValueError("dimension mismatch")
+        y = np.empty(self.n)
+        yf = np.empty(self.n) if want_far else None
+        _lib.check(_lib.load().fl_cluster_matvec(self.handle, x.ctypes.data, y.ctypes.data,
+                                                 None if yf is None else yf.ctypes.data, 0))
+        return y, yf
+
+    def matvec(self, x):
+        return self._apply(x)[0]
+
+    def far_apply(self, x):
+        return self._apply(x, True)[1]
+
+    def __matmul__(self, x):
+        return self.matvec(x)
+
+    def diag(self):
+        return self._diag
+
+    def far_blocks(self, npairs):
+        from . import _lib
+        out = np.empty((int(npairs), self.M, self.M))
+        _lib.check(_lib.load().fl_cluster_far_blocks(self.handle, out.ctypes.data))
+        return out
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("operator already freed")
+        return self._h
+
+    def free(self):
+        if self._h is not None and self._h.value:
+            from . import _lib
+            _lib.load().fl_cluster_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

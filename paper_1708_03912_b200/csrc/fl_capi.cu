@@ -102,6 +102,10 @@ static int32_t fail(int code, const std::string& msg) {
   return code;
 }
 
+namespace fl {
+int32_t api_fail(int code, const char* msg) { return fail(code, msg ? msg : ""); }
+}  // namespace fl
+
 #define FL_API_BEGIN try {
 #define FL_API_END                                              \
   }                                                             \

@@ -1,0 +1,445 @@
+// Cluster (H-matrix) operator on the device: ClusterOperator.matvec (cluster.py:417-456) —
+// y = A_near x - C * far(x) with the Chebyshev far field of cluster.compress (:667-712):
+//
+//   leaf moments   mom[leaf] = sum_{i in leaf} x_i basis_coef[i, :]            (_moments, :427-434)
+//   upward pass    mom[parent] += S_child mom[child]   (2D: S0 V S1^T)        (ChebData.push_up, :339-356)
+//   far blocks     F[a] += B_p mom[b],  F[b] += B_p^T mom[a]  over far pairs  (_far_potentials, :436-447)
+//   downward pass  F[child] += S_child^T F[parent]   (2D: S0^T V S1)         (ChebData.push_down, :358-374)
+//   evaluation     y_far[i] = basis_coef[i, :] . F[leaf(i)]                   (far_apply, :449-457)
+//
+// Every accumulation has the reference's order (children of a parent in reversed BFS order;
+// far contributions first as the pair's first node in pair order, then as its second node), so
+// results are deterministic; the near CSR product is a warp-per-row fixed-order reduction.
+// The far blocks B_p = |xi_a - xi_b|^(2 ex) at the Chebyshev points (compress, :683-694) are
+// either uploaded or built here (one thread per block entry).
+#include <memory>
+#include <vector>
+
+#include "../../include/fraclap_b200.h"
+#include "fl_internal.h"
+
+struct fl_cluster {
+  int device = 0, d = 1, m = 0, M = 0;
+  int64_t n = 0, nn = 0, np = 0;
+  double C = 0.0;
+  fl::DBuf<int64_t> indptr;
+  fl::DBuf<int> indices;
+  fl::DBuf<double> data, diag;
+  fl::DBuf<double> shift, bc, blocks, mom, F, Fp, x, y, yfar;
+  fl::DBuf<int> leaf_nodes, leaf_lo, leaf_hi, dof_perm, leaf_of_dof, children, parent, pairs, plist_off, plist,
+      level_nodes;
+  std::vector<int64_t> level_off_up, level_off_down;   // offsets into level_nodes (host copies)
+  int nleaves = 0;
+  cudaStream_t stream = nullptr;
+  ~fl_cluster() {
+    for (auto* b : {&data, &diag, &shift, &bc, &blocks, &mom, &F, &Fp, &x, &y, &yfar}) b->free();
+    for (auto* b : {&leaf_nodes, &leaf_lo, &leaf_hi, &dof_perm, &leaf_of_dof, &children, &parent, &pairs, &plist_off,
+                    &plist, &level_nodes})
+      b->free();
+    indptr.free();
+    indices.free();
+    if (stream) fl::release_stream(device, stream);
+  }
+};
+
+namespace fl {
+namespace {
+
+int grid_of(int64_t m, int b = 256) { return (int)std::max<int64_t>(1, (m + b - 1) / b); }
+
+__global__ void csr_spmv_kernel(int64_t n, const int64_t* __restrict__ indptr, const int* __restrict__ idx,
+                                const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int64_t e = indptr[i] + lane; e < indptr[i + 1]; e += 32) s = fma(val[e], x[idx[e]], s);
+  s = warp_sum(s);
+  if (lane == 0) y[i] = s;
+}
+
+// mom[leaf] = x[dofs] @ basis_coef[dofs]   (dofs in dof_perm order); other nodes zeroed
+__global__ void moments_kernel(int nleaves, const int* __restrict__ leaf_nodes, const int* __restrict__ lo,
+                               const int* __restrict__ hi, const int* __restrict__ perm, const double* __restrict__ x,
+                               const double* __restrict__ bc, int M, double* __restrict__ mom) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nleaves * M) return;
+  const int l = (int)(t / M), a = (int)(t % M);
+  double s = 0.0;
+  for (int r = lo[l]; r < hi[l]; ++r) {
+    const int i = perm[r];
+    s = fma(x[i], bc[(int64_t)i * M + a], s);
+  }
+  mom[(int64_t)leaf_nodes[l] * M + a] = s;
+}
+
+// out[a0, a1] += sum_b1 S1[a1, b1] (sum_b0 S0[a0, b0] V[b0, b1])   (2D; 1D: sum_b S0[a, b] v[b])
+template <int D>
+__device__ __forceinline__ double shift_apply(const double* __restrict__ S, const double* __restrict__ v, int m,
+                                              int a, bool transpose) {
+  if (D == 1) {
+    double s = 0.0;
+    for (int b = 0; b < m; ++b) s = fma(transpose ? S[b * m + a] : S[a * m + b], v[b], s);
+    return s;
+  } else {
+    const double* S0 = S;
+    const double* S1 = S + m * m;
+    const int a0 = a / m, a1 = a % m;
+    double s = 0.0;
+    for (int b1 = 0; b1 < m; ++b1) {
+      double t = 0.0;
+      for (int b0 = 0; b0 < m; ++b0) t = fma(transpose ? S0[b0 * m + a0] : S0[a0 * m + b0], v[b0 * m + b1], t);
+      s = fma(t, transpose ? S1[b1 * m + a1] : S1[a1 * m + b1], s);
+    }
+    return s;
+  }
+}
+
+// upward: one thread per (parent, alpha): children in reversed BFS order (second child first)
+template <int D>
+__global__ void up_kernel(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
+                          const double* __restrict__ shift, int m, int M, double* __restrict__ mom) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)cnt * M) return;
+  const int p = nodes[t / M], a = (int)(t % M);
+  double acc = mom[(int64_t)p * M + a];
+  for (int k = 1; k >= 0; --k) {
+    const int c = children[2 * p + k];
+    if (c < 0) continue;
+    acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+  }
+  mom[(int64_t)p * M + a] = acc;
+}
+
+// far pairs: Fp[p] = (B mom[b], B^T mom[a])
+__global__ void far_pair_kernel(int64_t np, const int* __restrict__ pairs, const double* __restrict__ B, int M,
+                                const double* __restrict__ mom, double* __restrict__ Fp) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= np * 2 * M) return;
+  const int64_t p = t / (2 * M);
+  const int r = (int)(t % (2 * M));
+  const double* Bp = B + p * M * M;
+  double s = 0.0;
+  if (r < M) {
+    const double* mb = mom + (int64_t)pairs[2 * p + 1] * M;
+    for (int b = 0; b < M; ++b) s = fma(Bp[(int64_t)r * M + b], mb[b], s);
+  } else {
+    const int c = r - M;
+    const double* ma = mom + (int64_t)pairs[2 * p] * M;
+    for (int a = 0; a < M; ++a) s = fma(Bp[(int64_t)a * M + c], ma[a], s);
+  }
+  Fp[t] = s;
+}
+// F[node] = sum over its pair list (as first node, pair order, then as second node, pair order)
+__global__ void far_gather_kernel(int64_t nn, const int* __restrict__ off, const int* __restrict__ lst, int M,
+                                  const double* __restrict__ Fp, double* __restrict__ F) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nn * M) return;
+  const int64_t nd = t / M;
+  const int a = (int)(t % M);
+  double s = 0.0;
+  for (int k = off[nd]; k < off[nd + 1]; ++k) {
+    const int e = lst[k];                  // 2 p + role
+    s += Fp[(int64_t)(e >> 1) * 2 * M + (e & 1) * M + a];
+  }
+  F[t] = s;
+}
+
+// downward: one thread per (child, alpha): F[child] += S^T F[parent]
+template <int D>
+__global__ void down_kernel(const int* __restrict__ nodes, int cnt, const int* __restrict__ parent,
+                            const double* __restrict__ shift, int m, int M, double* __restrict__ F) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)cnt * M) return;
+  const int c = nodes[t / M], a = (int)(t % M);
+  F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)parent[c] * M, m, a, true);
+}
+
+// y[i] = y_near[i] - C * basis_coef[i, :] . F[leaf(i)]
+__global__ void eval_kernel(int64_t n, const int* __restrict__ leaf_of_dof, const double* __restrict__ bc, int M,
+                            const double* __restrict__ F, double negC, double* __restrict__ y,
+                            double* __restrict__ yfar) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* f = F + (int64_t)leaf_of_dof[i] * M;
+  double s = 0.0;
+  for (int a = 0; a < M; ++a) s = fma(bc[i * M + a], f[a], s);
+  const double v = negC * s;
+  yfar[i] = v;
+  y[i] += v;
+}
+
+template <int E4>
+__global__ void far_blocks_kernel(int64_t np, const int* __restrict__ pairs, const double* __restrict__ pts, int d,
+                                  int M, double ex, double* __restrict__ B) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= np * M * M) return;
+  const int64_t p = t / ((int64_t)M * M);
+  const int r = (int)(t % ((int64_t)M * M)), a = r / M, b = r % M;
+  const double* Pa = pts + ((int64_t)pairs[2 * p] * M + a) * d;
+  const double* Pb = pts + ((int64_t)pairs[2 * p + 1] * M + b) * d;
+  double r2 = 0.0;
+  for (int j = 0; j < d; ++j) {
+    const double df = Pa[j] - Pb[j];
+    r2 = __dadd_rn(r2, __dmul_rn(df, df));
+  }
+  B[t] = kpow<E4>(r2, ex);
+}
+
+}  // namespace
+
+int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) {
+  const fl_cluster_desc& D = *Dd;
+  if (D.d != 1 && D.d != 2) throw Error(FL_E_ARG, "cluster: d must be 1 or 2");
+  if (D.m < 1 || D.n < 0 || D.num_nodes < 1) throw Error(FL_E_ARG, "cluster: bad sizes");
+  const int d = D.d, m = D.m;
+  const int M = d == 1 ? m : m * m;
+  const int64_t n = D.n, nn = D.num_nodes, np = D.npairs;
+  if (n >= (1LL << 31) || nn >= (1LL << 30) || np >= (1LL << 30)) throw Error(FL_E_ARG, "cluster: too large");
+  // host-side structure: children, levels, leaves, per-node pair lists (validated)
+  std::vector<int> children(2 * nn, -1), par(nn), depth(nn, -1);
+  for (int64_t k = 0; k < nn; ++k) {
+    const int64_t p = D.parent[k];
+    if (p < -1 || p >= nn) throw Error(FL_E_ARG, "cluster: parent out of range");
+    par[k] = (int)p;
+  }
+  for (int64_t t = 0; t < nn; ++t) {                 // BFS order: children appended in order
+    const int64_t k = D.topo_order[t];
+    if (k < 0 || k >= nn) throw Error(FL_E_ARG, "cluster: topo_order out of range");
+    if (par[k] < 0) { depth[k] = 0; continue; }
+    const int p = par[k];
+    if (depth[p] < 0) throw Error(FL_E_ARG, "cluster: topo_order lists a child before its parent");
+    depth[k] = depth[p] + 1;
+    if (children[2 * p] < 0) children[2 * p] = (int)k;
+    else if (children[2 * p + 1] < 0) children[2 * p + 1] = (int)k;
+    else throw Error(FL_E_ARG, "cluster: more than two children");
+  }
+  int maxd = 0;
+  for (int64_t k = 0; k < nn; ++k) maxd = std::max(maxd, depth[k]);
+  std::vector<int> leaf_nodes, lo, hi, lod(std::max<int64_t>(n, 1), -1);
+  for (int64_t k = 0; k < nn; ++k) {
+    if (children[2 * k] >= 0) continue;
+    const int64_t a = D.ranges[2 * k], b = D.ranges[2 * k + 1];
+    if (a < 0 || b > n || a > b) throw Error(FL_E_ARG, "cluster: node range out of bounds");
+    leaf_nodes.push_back((int)k);
+    lo.push_back((int)a);
+    hi.push_back((int)b);
+    for (int64_t r = a; r < b; ++r) {
+      const int64_t i = D.dof_perm[r];
+      if (i < 0 || i >= n) throw Error(FL_E_ARG, "cluster: dof_perm out of range");
+      lod[i] = (int)k;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (lod[i] < 0) throw Error(FL_E_ARG, "cluster: a DoF lies in no leaf");
+  // levels: parents with children at depth L (upward, deepest first); nodes at depth L (downward)
+  std::vector<int> lvl_nodes;
+  std::vector<int64_t> off_up{0}, off_down;
+  for (int L = maxd - 1; L >= 0; --L) {
+    for (int64_t t = 0; t < nn; ++t) {
+      const int64_t k = D.topo_order[t];
+      if (depth[k] == L && children[2 * k] >= 0) lvl_nodes.push_back((int)k);
+    }
+    off_up.push_back((int64_t)lvl_nodes.size());
+  }
+  off_down.push_back((int64_t)lvl_nodes.size());
+  for (int L = 1; L <= maxd; ++L) {
+    for (int64_t t = 0; t < nn; ++t) {
+      const int64_t k = D.topo_order[t];
+      if (depth[k] == L) lvl_nodes.push_back((int)k);
+    }
+    off_down.push_back((int64_t)lvl_nodes.size());
+  }
+  // pair lists per node: first-node roles in pair order, then second-node roles
+  std::vector<int> prs(std::max<int64_t>(2 * np, 1)), cnt(nn + 1, 0);
+  for (int64_t p = 0; p < np; ++p) {
+    const int64_t a = D.far_pairs[2 * p], b = D.far_pairs[2 * p + 1];
+    if (a < 0 || b < 0 || a >= nn || b >= nn) throw Error(FL_E_ARG, "cluster: far pair out of range");
+    prs[2 * p] = (int)a;
+    prs[2 * p + 1] = (int)b;
+    cnt[a + 1]++;
+    cnt[b + 1]++;
+  }
+  for (int64_t k = 0; k < nn; ++k) cnt[k + 1] += cnt[k];
+  std::vector<int> lst(std::max<int64_t>(2 * np, 1)), fill(cnt.begin(), cnt.end() - 1);
+  for (int role = 0; role < 2; ++role)
+    for (int64_t p = 0; p < np; ++p) lst[fill[prs[2 * p + role]]++] = (int)(2 * p + role);
+
+  FL_CUDA(cudaSetDevice(device));
+  init_pool(device);
+  std::unique_ptr<fl_cluster> C(new fl_cluster());
+  C->device = device;
+  C->stream = acquire_stream(device);
+  cudaStream_t st = C->stream;
+  StreamScope scope(st);
+  C->d = d; C->m = m; C->M = M; C->n = n; C->nn = nn; C->np = np; C->C = D.C;
+  C->nleaves = (int)leaf_nodes.size();
+  C->level_off_up = off_up;
+  C->level_off_down = off_down;
+  auto up_i = [&](DBuf<int>& b, const std::vector<int>& h) {
+    b.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) FL_CUDA(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  };
+  auto up_d = [&](DBuf<double>& b, const double* h, size_t cnt_) {
+    b.alloc(std::max<size_t>(cnt_, 1));
+    if (cnt_) FL_CUDA(cudaMemcpyAsync(b.p, h, cnt_ * sizeof(double), cudaMemcpyHostToDevice, st));
+  };
+  std::vector<int> perm(std::max<int64_t>(n, 1));
+  for (int64_t r = 0; r < n; ++r) perm[r] = (int)D.dof_perm[r];
+  up_i(C->leaf_nodes, leaf_nodes); up_i(C->leaf_lo, lo); up_i(C->leaf_hi, hi); up_i(C->dof_perm, perm);
+  up_i(C->leaf_of_dof, lod); up_i(C->children, children); up_i(C->parent, par); up_i(C->pairs, prs);
+  up_i(C->plist_off, cnt); up_i(C->plist, lst); up_i(C->level_nodes, lvl_nodes);
+  up_d(C->shift, D.shift, (size_t)nn * d * m * m);
+  up_d(C->bc, D.basis_coef, (size_t)n * M);
+  // near CSR
+  if (D.nnz < 0 || (D.nnz > 0 && (!D.indptr || !D.indices || !D.data))) throw Error(FL_E_ARG, "cluster: bad near CSR");
+  C->indptr.alloc(n + 1);
+  FL_CUDA(cudaMemcpyAsync(C->indptr.p, D.indptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  std::vector<int> ci(std::max<int64_t>(D.nnz, 1));
+  for (int64_t e = 0; e < D.nnz; ++e) {
+    if (D.indices[e] < 0 || D.indices[e] >= n) throw Error(FL_E_ARG, "cluster: near column out of range");
+    ci[e] = (int)D.indices[e];
+  }
+  up_i(C->indices, ci);
+  up_d(C->data, D.data, (size_t)D.nnz);
+  // far blocks: uploaded, or built from the Chebyshev points
+  C->blocks.alloc(std::max<int64_t>(np * M * M, 1));
+  if (np > 0) {
+    if (D.far_blocks) {
+      FL_CUDA(cudaMemcpyAsync(C->blocks.p, D.far_blocks, (size_t)np * M * M * sizeof(double), cudaMemcpyHostToDevice,
+                              st));
+    } else {
+      if (!D.points) throw Error(FL_E_ARG, "cluster: neither far blocks nor Chebyshev points given");
+      DBuf<double> pts;
+      up_d(pts, D.points, (size_t)nn * M * d);
+      const double ex = -(d / 2.0 + D.s);
+      const int e4 = (D.s == 0.25 || D.s == 0.5 || D.s == 0.75) ? (int)std::lround(4.0 * (d + 2.0 * D.s)) : 0;
+      const int64_t tot = np * M * M;
+      switch (e4) {
+        case 6: far_blocks_kernel<6><<<grid_of(tot), 256, 0, st>>>(np, C->pairs.p, pts.p, d, M, ex, C->blocks.p); break;
+        case 8: far_blocks_kernel<8><<<grid_of(tot), 256, 0, st>>>(np, C->pairs.p, pts.p, d, M, ex, C->blocks.p); break;
+        case 10: far_blocks_kernel<10><<<grid_of(tot), 256, 0, st>>>(np, C->pairs.p, pts.p, d, M, ex, C->blocks.p); break;
+        case 12: far_blocks_kernel<12><<<grid_of(tot), 256, 0, st>>>(np, C->pairs.p, pts.p, d, M, ex, C->blocks.p); break;
+        case 14: far_blocks_kernel<14><<<grid_of(tot), 256, 0, st>>>(np, C->pairs.p, pts.p, d, M, ex, C->blocks.p); break;
+        default: far_blocks_kernel<0><<<grid_of(tot), 256, 0, st>>>(np, C->pairs.p, pts.p, d, M, ex, C->blocks.p); break;
+      }
+      note_launch();
+      FL_CHECK_LAUNCH();
+      FL_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  C->mom.alloc((size_t)nn * M);
+  C->F.alloc((size_t)nn * M);
+  C->Fp.alloc(std::max<int64_t>(np * 2 * M, 1));
+  C->x.alloc(std::max<int64_t>(n, 1));
+  C->y.alloc(std::max<int64_t>(n, 1));
+  C->yfar.alloc(std::max<int64_t>(n, 1));
+  FL_CUDA(cudaStreamSynchronize(st));
+  *out = C.release();
+  return FL_OK;
+}
+
+int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yfar, cudaStream_t st) {
+  const int64_t n = C->n, nn = C->nn, np = C->np;
+  const int M = C->M, m = C->m;
+  if (n == 0) return FL_OK;
+  csr_spmv_kernel<<<grid_of(n * 32), 256, 0, st>>>(n, C->indptr.p, C->indices.p, C->data.p, x, y), note_launch();
+  FL_CUDA(cudaMemsetAsync(C->mom.p, 0, (size_t)nn * M * sizeof(double), st));
+  moments_kernel<<<grid_of((int64_t)C->nleaves * M), 256, 0, st>>>(C->nleaves, C->leaf_nodes.p, C->leaf_lo.p,
+                                                                   C->leaf_hi.p, C->dof_perm.p, x, C->bc.p, M,
+                                                                   C->mom.p), note_launch();
+  for (size_t L = 0; L + 1 < C->level_off_up.size(); ++L) {
+    const int64_t a = C->level_off_up[L], cnt = C->level_off_up[L + 1] - a;
+    if (cnt <= 0) continue;
+    if (C->d == 1)
+      up_kernel<1><<<grid_of(cnt * M), 256, 0, st>>>(C->level_nodes.p + a, (int)cnt, C->children.p, C->shift.p, m, M,
+                                                     C->mom.p);
+    else
+      up_kernel<2><<<grid_of(cnt * M), 256, 0, st>>>(C->level_nodes.p + a, (int)cnt, C->children.p, C->shift.p, m, M,
+                                                     C->mom.p);
+    note_launch();
+  }
+  if (np > 0)
+    far_pair_kernel<<<grid_of(np * 2 * M), 256, 0, st>>>(np, C->pairs.p, C->blocks.p, M, C->mom.p, C->Fp.p),
+        note_launch();
+  far_gather_kernel<<<grid_of(nn * M), 256, 0, st>>>(nn, C->plist_off.p, C->plist.p, M, C->Fp.p, C->F.p),
+      note_launch();
+  for (size_t L = 0; L + 1 < C->level_off_down.size(); ++L) {
+    const int64_t a = C->level_off_down[L], cnt = C->level_off_down[L + 1] - a;
+    if (cnt <= 0) continue;
+    if (C->d == 1)
+      down_kernel<1><<<grid_of(cnt * M), 256, 0, st>>>(C->level_nodes.p + a, (int)cnt, C->parent.p, C->shift.p, m, M,
+                                                       C->F.p);
+    else
+      down_kernel<2><<<grid_of(cnt * M), 256, 0, st>>>(C->level_nodes.p + a, (int)cnt, C->parent.p, C->shift.p, m, M,
+                                                       C->F.p);
+    note_launch();
+  }
+  eval_kernel<<<grid_of(n), 256, 0, st>>>(n, C->leaf_of_dof.p, C->bc.p, M, C->F.p, -C->C, y, yfar), note_launch();
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+}  // namespace fl
+
+// ------------------------------------------------------------------ C ABI
+#define FL_TRY try {
+#define FL_CATCH                                                                   \
+  }                                                                                \
+  catch (const fl::Error& e) { return fl::api_fail(e.code, e.what()); }            \
+  catch (const std::bad_alloc&) { return fl::api_fail(FL_E_OOM, "host allocation failed"); } \
+  catch (const std::exception& e) { return fl::api_fail(FL_E_CUDA, e.what()); }
+
+extern "C" {
+
+int32_t fl_cluster_create(const fl_cluster_desc* desc, int32_t device, fl_cluster** out) {
+  FL_TRY
+  if (!desc || !out) return fl::api_fail(FL_E_ARG, "null argument");
+  *out = nullptr;
+  if (!desc->parent || !desc->topo_order || !desc->ranges || !desc->dof_perm || !desc->shift || !desc->basis_coef ||
+      (desc->npairs > 0 && !desc->far_pairs))
+    return fl::api_fail(FL_E_ARG, "cluster: null array");
+  return fl::cluster_create(desc, device, out);
+  FL_CATCH
+}
+
+int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_far, int32_t ptr_kind) {
+  FL_TRY
+  if (!C || !x || !y) return fl::api_fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(C->device));
+  cudaStream_t st = C->stream;
+  fl::StreamScope scope(st);
+  const int64_t n = C->n;
+  if (ptr_kind == 1) {
+    fl::cluster_matvec_dev(C, x, y, y_far ? y_far : C->yfar.p, st);
+    FL_CUDA(cudaStreamSynchronize(st));
+    return FL_OK;
+  }
+  FL_CUDA(cudaMemcpyAsync(C->x.p, x, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  fl::cluster_matvec_dev(C, C->x.p, C->y.p, C->yfar.p, st);
+  FL_CUDA(cudaMemcpyAsync(y, C->y.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (y_far) FL_CUDA(cudaMemcpyAsync(y_far, C->yfar.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  return FL_OK;
+  FL_CATCH
+}
+
+int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out) {
+  FL_TRY
+  if (!C || !blocks_out) return fl::api_fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(C->device));
+  if (C->np > 0)
+    FL_CUDA(cudaMemcpyAsync(blocks_out, C->blocks.p, (size_t)C->np * C->M * C->M * sizeof(double),
+                            cudaMemcpyDeviceToHost, C->stream));
+  FL_CUDA(cudaStreamSynchronize(C->stream));
+  return FL_OK;
+  FL_CATCH
+}
+
+void fl_cluster_free(fl_cluster* C) {
+  if (!C) return;
+  cudaSetDevice(C->device);
+  delete C;
+}
+
+}  // extern "C"

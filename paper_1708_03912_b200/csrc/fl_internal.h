@@ -307,6 +307,16 @@ void near_field_cross(const DevMesh& m, const DevTables& t, const OrderConsts& o
                       const NearInput& in, const int* row_vertex, CsrOut& out, int64_t* npairs_out,
                       unsigned long long* evals, cudaStream_t st);
 
+// fl_cluster.cu: the cluster (H-matrix) operator
+}  // namespace fl
+struct fl_cluster;
+struct fl_cluster_desc;
+namespace fl {
+int32_t cluster_create(const ::fl_cluster_desc* D, int device, ::fl_cluster** out);
+int32_t cluster_matvec_dev(::fl_cluster* C, const double* x, double* y, double* yfar, cudaStream_t st);
+// sets fl_last_error() and returns code (fl_capi.cu)
+int32_t api_fail(int code, const char* msg);
+
 // fl_solve.cu
 void launch_matvec(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
                    cudaStream_t st);

@@ -604,7 +604,49 @@ def t_near():
     save("near", recs)
 
 
+# cluster operator (cluster.compress, cluster.py:667-712) and its matvec (:417-456)
+CLUSTER = [("uniform1d", 96, 0.25, 8, 1.0, 8), ("graded1d", 200, 0.75, 8, 1.0, 10),
+           ("square2d", 16, 0.5, 8, 1.0, 5), ("jit2d", 14, 0.25, 12, 1.0, 6), ("square2d", 20, 0.25, 16, 1.0, 4)]
+
+
+def t_cluster():
+    from fraclap import mesh as M, assembly as A, cluster as CL
+    fp64_variant()
+    recs = {}
+    for kind, N, s, cap, eta, mo in CLUSTER:
+        tag = "%s_%d_%g_%d_m%d" % (kind, N, s, cap, mo)
+        mesh = irregular_mesh(kind, N, 31) if kind in ("jit2d", "rand1d") else ref_mesh(kind, N)
+        dm = M.DofMap(mesh, s)
+        ker = A.FractionalKernel(mesh.d, s)
+        t0 = time.perf_counter()
+        tree = CL.build_tree(mesh, dm, cap)
+        op = CL.compress(mesh, dm, ker, tree, eta, mo)
+        x = np.random.default_rng(7).uniform(-1, 1, dm.n)
+        y = op.matvec(x)
+        nn = tree.num_nodes
+        shift = np.zeros((nn, mesh.d, mo, mo))
+        for nd in range(nn):
+            if op.cheb.shift[nd] is not None:
+                for j in range(mesh.d):
+                    shift[nd, j] = op.cheb.shift[nd][j]
+        near = op.near.tocsr()
+        rec = dict(vertices=mesh.vertices, cells=mesh.cells, bedges=mesh.boundary_edges,
+                   bnormals=mesh.boundary_normals, s=s, leaf_cap=cap, eta=eta, m=mo, C=ker.C_ds,
+                   indptr=near.indptr.astype(np.int64), indices=near.indices.astype(np.int64), data=near.data,
+                   far_pairs=op.far_pairs, far_blocks=op.far_blocks, basis_coef=op.basis_coef,
+                   parent=np.asarray(tree.parent, np.int64), topo_order=np.asarray(tree.topo_order, np.int64),
+                   ranges=np.asarray(tree.ranges, np.int64), dof_perm=tree.dof_perm,
+                   leaves=np.asarray(tree.leaves, np.int64), shift=shift, points=op.cheb.points,
+                   x=x, y=y, y_far=op.far_apply(x), diag=op.diag())
+        for k, v in rec.items():
+            recs[tag + "/" + k] = v
+        print(tag, "n=%d far=%d M=%d nnz=%d %.1fs" % (dm.n, len(op.far_pairs), op.cheb.M, near.nnz,
+                                                     time.perf_counter() - t0), flush=True)
+    save("cluster", recs)
+
+
 TARGETS = {
+    "cluster": t_cluster,
     "near": t_near,
     "tables": t_tables,
     "meshes": t_meshes,
