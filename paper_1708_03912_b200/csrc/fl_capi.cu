@@ -494,9 +494,37 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   FL_CUDA(cudaMemsetAsync(evc.p, 0, 2 * sizeof(unsigned long long), st));
   DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
   FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
+  // 1D: the tail runs on its own stream, so the cross tiles (issued on `st` once the sizes are
+  // back) fill the SMs its last partial wave leaves idle; joined before the cell-local matrices
+  struct TailStream {
+    int dev; cudaStream_t s = nullptr; cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    TailStream(int d, bool on) : dev(d) {
+      if (!on) return;
+      s = acquire_stream(d);
+      for (auto& x : e) FL_CUDA(cudaEventCreate(&x));
+    }
+    ~TailStream() {
+      for (auto& x : e)
+        if (x) cudaEventDestroy(x);
+      if (s) release_stream(dev, s);
+    }
+  };
+  static const bool tail_concurrent = [] {
+    const char* v = getenv("FRACLAP_TAIL_CONCURRENT");
+    return !v || atoi(v) != 0;
+  }();
+  TailStream tstream(device, early_tail && tail_concurrent);
   if (early_tail) {
     tm.mark();  // 1
-    launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, st);
+    if (tstream.s) {
+      FL_CUDA(cudaEventRecord(tstream.e[0], st));
+      FL_CUDA(cudaStreamWaitEvent(tstream.s, tstream.e[0], 0));
+      FL_CUDA(cudaEventRecord(tstream.e[1], tstream.s));
+      launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, tstream.s);
+      FL_CUDA(cudaEventRecord(tstream.e[2], tstream.s));
+    } else {
+      launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, st);
+    }
     tm.mark();  // 2
   }
   FL_CUDA(cudaEventSynchronize(ev_sizes));
@@ -650,6 +678,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
                        near.hmask, near.G.p, st);
   }
   tm.mark();  // 6
+  if (tstream.s) FL_CUDA(cudaStreamWaitEvent(st, tstream.e[2], 0));   // psi complete
   if (!nbands) {
     launch_cell_local(m, U.t, C, s, integral && m.nb > 0, targets.p, ntargets, ident.p, psi.p, win.p, Lc.p, st);
     FL_CUDA(cudaStreamWaitEvent(st, ev_si, 0));
@@ -682,6 +711,11 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   S.ms_prep = tm.ms(0, 1);
   S.ms_singular = early_tail ? tm.ms(2, 3) : tm.ms(1, 2);   // 1D: tail (1 -> 2) runs before the singular kernels
   S.ms_tail = early_tail ? tm.ms(1, 2) : tm.ms(2, 3);
+  if (tstream.s) {   // concurrent tail: its own span on its stream
+    float a = 0.f;
+    cudaEventElapsedTime(&a, tstream.e[1], tstream.e[2]);
+    S.ms_tail = a;
+  }
   S.ms_flux = tm.ms(3, 4);
   S.ms_tiles = tm.ms(4, 5);
   S.ms_cross = tm.ms(5, 6);
