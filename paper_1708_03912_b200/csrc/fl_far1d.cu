@@ -411,6 +411,7 @@ constexpr int T1C = T1 + 8;                   // max cells behind one DoF tile o
 constexpr int T1X = T1 == 64 ? 512 : 256;     // threads of a tile CTA
 constexpr int T1B = T1 == 64 ? 1 : FL_TILE1D_MINB;   // resident tile CTAs per SM
 constexpr int T1K = 33;      // order buckets (KDIR)
+constexpr int TSTAT = 8;     // doubles of tile statistics: x extent, max h, min / max |ln h|, ln(max h)
 
 // one warp per DoF tile: sorted unique cells of the patches of its DoFs; per DoF the
 // (slot << 1 | basis) of each patch cell (-1 = none); the owning tile of every cell
@@ -501,8 +502,8 @@ __global__ void tile1d_cells_kernel(DevMesh m, const int* __restrict__ dof_verte
       lmx = fmax(lmx, __shfl_xor_sync(0xffffffffu, lmx, o));
     }
     if (lane == 0) {
-      double* st = tstat + 5 * t;
-      st[0] = lo; st[1] = hi; st[2] = hmx; st[3] = lmn; st[4] = lmx;
+      double* st = tstat + TSTAT * t;
+      st[0] = lo; st[1] = hi; st[2] = hmx; st[3] = lmn; st[4] = lmx; st[5] = log(hmx); st[6] = 0.0; st[7] = 0.0;
     }
   }
   if (lane == 0) {
@@ -646,10 +647,19 @@ __device__ __forceinline__ double4 block1d_warp(const double* __restrict__ tab, 
 
 constexpr int T1WARP = 6;    // orders >= this get a warp per pair
 
+// a tile's cell as the cross tiles stage it: one 80-byte record, tile-contiguous (one round trip)
+struct __align__(16) TileCell {
+  double x0, x1, lo, hi, h, lh;
+  int id, v0, v1, own;
+  float lnhf, lhf;
+  int pad[2];
+};
+
 // one DoF tiling (rows or columns): cells per tile, per-DoF (slot << 1 | basis), cell owners
 struct Tiling1D {
   const int *cnt, *cell, *dslot, *owner;
-  const double* stat;    // per tile: x extent (lo, hi) of its cells, max h, min / max |ln h|
+  const double* stat;    // per tile: x extent (lo, hi) of its cells, max h, min / max |ln h|, ln max h
+  const TileCell* rec;   // per tile: T1C packed cell records
   int off, len, nt;
 };
 
@@ -657,12 +667,14 @@ struct Tiling1D {
 // the tiles' x extents bounds every pair distance from below and the disjoint order formula
 // (quadrature.py:159-168) from above (each numerator term bounded above, the denominator below);
 // 1e-9 of margin absorbs rounding, so the reference's ceil() is 2 as well (clip floor).
+// (ln(max h) comes precomputed per tile: one log per tile pair)
 __device__ __forceinline__ bool tile_pair_all_k2(const OrderConsts& oc, const double* a, const double* b) {
   const double D = fmax(b[0] - a[1], a[0] - b[1]);
   if (!(D > 0.0)) return false;
-  const double hmx = fmax(a[2], b[2]), lmn = fmin(a[3], b[3]), lmx = fmax(a[4], b[4]);
-  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * log(D) + oc.s * log(hmx) - oc.coff;
-  const double den = fmax(log(D / hmx), 0.0) + oc.ln_rho2;
+  const double lhmx = fmax(a[5], b[5]), lmn = fmin(a[3], b[3]), lmx = fmax(a[4], b[4]);
+  const double lD = log(D);
+  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * lD + oc.s * lhmx - oc.coff;
+  const double den = fmax(lD - lhmx, 0.0) + oc.ln_rho2;
   return (num > 0.0 ? num / den : 0.0) <= 2.0 - 1e-9;
 }
 
@@ -676,7 +688,8 @@ __global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const
                                                            OrderConsts oc, double ex, Src1D S, Tiling1D R,
                                                            Tiling1D Cn, int mc, double negC, double* __restrict__ A,
                                                            int64_t lda, unsigned long long* __restrict__ evals,
-                                                           int band0, int band1) {
+                                                           int band0, int band1,
+                                                           const unsigned char* __restrict__ k2flags) {
   extern __shared__ __align__(16) unsigned char smem1d[];
   __shared__ Cell1S cr, cc;
   __shared__ int bcnt[T1K], boff[T1K + 1], ndefer, uni2;
@@ -723,18 +736,17 @@ __global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const
   for (int q = tid; q < 2 * T1C; q += blockDim.x) {
     Cell1S& C = q < T1C ? cr : cc;
     const int a = q < T1C ? q : q - T1C;
-    const int cnt = q < T1C ? nr : ncl;
-    if (a < cnt) {
-      const int c = q < T1C ? R.cell[(size_t)bi * T1C + a] : Cn.cell[(size_t)bj * T1C + a];
-      C.id[a] = c; C.x0[a] = S.x0[c]; C.x1[a] = S.x1[c]; C.lo[a] = S.lo[c]; C.hi[a] = S.hi[c];
-      C.h[a] = S.h[c]; C.lh[a] = S.lh[c]; C.v0[a] = S.v0[c]; C.v1[a] = S.v1[c];
-      C.lnhf[a] = S.lnhf[c]; C.lhf[a] = S.lhf[c]; C.own[a] = q < T1C ? R.owner[c] : Cn.owner[c];
-    }
+    // every slot is staged (slots past the tile's count hold zeros and are never read), so the
+    // record loads do not wait for the count
+    const TileCell t = q < T1C ? R.rec[(size_t)bi * T1C + a] : Cn.rec[(size_t)bj * T1C + a];
+    C.id[a] = t.id; C.x0[a] = t.x0; C.x1[a] = t.x1; C.lo[a] = t.lo; C.hi[a] = t.hi;
+    C.h[a] = t.h; C.lh[a] = t.lh; C.v0[a] = t.v0; C.v1[a] = t.v1;
+    C.lnhf[a] = t.lnhf; C.lhf[a] = t.lhf; C.own[a] = t.own;
   }
   if (tid < T1K) bcnt[tid] = 0;
   if (tid == 0) {
     ndefer = 0;
-    uni2 = tile_pair_all_k2(oc, R.stat + 5 * bi, Cn.stat + 5 * bj) ? 1 : 0;
+    uni2 = k2flags[(size_t)bi * Cn.nt + bj];     // tile_pair_all_k2, precomputed (tile_flags_kernel)
   }
   if (tid < 2 * T1) {
     // per DoF and patch cell: its part of the M offset (row DoFs: slot row + basis a; column
@@ -1008,9 +1020,25 @@ static void build_src1d(const DevMesh& m, Src1DBuf& B, cudaStream_t st) {
 struct TilingBuf {
   DBuf<int> cnt, cell, dslot, owner;
   DBuf<double> stat;
+  DBuf<TileCell> rec;
   int off = 0, len = 0, nt = 0;
-  Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, stat.p, off, len, nt}; }
+  Tiling1D view() const { return Tiling1D{cnt.p, cell.p, dslot.p, owner.p, stat.p, rec.p, off, len, nt}; }
 };
+
+// the packed records of every tile's cells (after the owners are final)
+__global__ void pack_tile_cells_kernel(Src1D S, const int* __restrict__ tcnt, const int* __restrict__ tcell,
+                                       const int* __restrict__ owner, int nt, TileCell* __restrict__ rec) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (int64_t)nt * T1C) return;
+  const int t = (int)(q / T1C), a = (int)(q % T1C);
+  if (tcnt[t] > T1C || a >= tcnt[t]) return;      // (over-full tiles: no fused path)
+  const int c = tcell[q];
+  TileCell r;
+  r.x0 = S.x0[c]; r.x1 = S.x1[c]; r.lo = S.lo[c]; r.hi = S.hi[c]; r.h = S.h[c]; r.lh = S.lh[c];
+  r.id = c; r.v0 = S.v0[c]; r.v1 = S.v1[c]; r.own = owner[c];
+  r.lnhf = S.lnhf[c]; r.lhf = S.lhf[c]; r.pad[0] = r.pad[1] = 0;
+  rec[q] = r;
+}
 
 // Everything the 1D far field needs from the mesh, enqueued without host synchronisation: the
 // source records and, for the fused cross tiles, the DoF tilings with the max cells per tile on
@@ -1039,10 +1067,15 @@ Plan1D* plan1d_create(const DevMesh& m, const int* dof_vertex, bool symmetric, i
     auto make = [&](TilingBuf& T, int off, int len) {
       T.off = off; T.len = len; T.nt = (len + T1 - 1) / T1;
       T.cnt.alloc(T.nt); T.cell.alloc((size_t)T.nt * T1C); T.dslot.alloc((size_t)2 * len); T.owner.alloc(m.nc);
-      T.stat.alloc((size_t)T.nt * 5);
+      T.stat.alloc((size_t)T.nt * TSTAT);
       FL_CUDA(cudaMemsetAsync(T.owner.p, 0x7f, sizeof(int) * m.nc, st));
       tile1d_cells_kernel<<<(T.nt + 3) / 4, 128, 0, st>>>(m, dof_vertex, off, len, T.nt, T.cnt.p, T.cell.p, T.dslot.p,
                                                           T.owner.p, T.stat.p, P->mx.p),
+          ::fl::note_launch();
+      T.rec.alloc((size_t)T.nt * T1C);
+      FL_CUDA(cudaMemsetAsync(T.rec.p, 0, (size_t)T.nt * T1C * sizeof(TileCell), st));
+      pack_tile_cells_kernel<<<(unsigned)(((int64_t)T.nt * T1C + 255) / 256), 256, 0, st>>>(
+          P->B.view(), T.cnt.p, T.cell.p, T.owner.p, T.nt, T.rec.p),
           ::fl::note_launch();
       FL_CHECK_LAUNCH();
     };
@@ -1074,6 +1107,16 @@ bool cross1d_fits(const DevMesh& m, int64_t ntargets, bool symmetric) {
   return need < 0.5 * (double)fr;
 }
 
+// tile_pair_all_k2 of every (row tile, column tile) in row tiles [r0, r1), ahead of the tile kernel
+// (its fp64 log would otherwise sit on one thread in front of the tile's first barrier)
+__global__ void tile_flags_kernel(OrderConsts oc, const double* __restrict__ rstat, const double* __restrict__ cstat,
+                                  int r0, int r1, int ntc, unsigned char* __restrict__ flags) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)(r1 - r0) * ntc) return;
+  const int bi = r0 + (int)(t / ntc), bj = (int)(t % ntc);
+  flags[(size_t)bi * ntc + bj] = tile_pair_all_k2(oc, rstat + TSTAT * bi, cstat + TSTAT * bj) ? 1 : 0;
+}
+
 bool cross1d_fused(const Plan1D* P, int maxcells) { return P->fused && maxcells <= T1C; }
 int cross1d_tile_dofs() { return T1; }
 
@@ -1100,15 +1143,24 @@ bool launch_cross1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc,
       ntp = (int64_t)(b1 - b0) * cv.nt - ((int64_t)b1 * (b1 - 1) - (int64_t)b0 * (b0 - 1)) / 2;
       if (ntp <= 0) return true;
     }
+    DBuf<unsigned char> flags((size_t)rv.nt * cv.nt);
+    {
+      const int r0 = b1 > b0 ? b0 : 0, r1 = b1 > b0 ? b1 : rv.nt;
+      const int64_t tot = (int64_t)(r1 - r0) * cv.nt;
+      tile_flags_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(oc, rv.stat, cv.stat, r0, r1, cv.nt, flags.p);
+      ::fl::note_launch();
+    }
     FL_E4_SWITCH1(e4, {
       if (symmetric) {
         auto kern = cross1d_tile_kernel<E4, false>;
         FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals, b0, b1);
+        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals, b0, b1,
+                                               flags.p);
       } else {
         auto kern = cross1d_tile_kernel<E4, true>;
         FL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals, 0, 0);
+        kern<<<(unsigned)ntp, T1X, smem, st>>>(m, t.data, t, oc, ex, S, rv, cv, mc, negC, A, lda, evals, 0, 0,
+                                               flags.p);
       }
       ::fl::note_launch();
     });
