@@ -559,6 +559,37 @@ __device__ __forceinline__ double4 block1d_k(const double* __restrict__ nd, doub
   return make_double4(m00 * JJ, m01 * JJ, m10 * JJ, m11 * JJ);
 }
 
+// the order-2 rule held in registers (loaded once per CTA instead of once per pair)
+struct Rule2 {
+  double tq[2], w0[2], w1[2];
+  __device__ explicit Rule2(const double* __restrict__ nd) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      tq[r] = __ldg(nd + r * NODE);
+      w0[r] = __ldg(nd + r * NODE + 3);
+      w1[r] = __ldg(nd + r * NODE + 4);
+    }
+  }
+};
+template <int E4>
+__device__ __forceinline__ double4 block1d_2(const Rule2& R2, double kx0, double ke, double lx0, double le, double JJ,
+                                             double ex) {
+  const double Y0 = lx0 + R2.tq[0] * le, Y1 = lx0 + R2.tq[1] * le;
+  double m00 = 0, m01 = 0, m10 = 0, m11 = 0;
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const double X = kx0 + R2.tq[x] * ke;
+    const double v0 = kpow_abs<E4>(X - Y0, ex), v1 = kpow_abs<E4>(X - Y1, ex);
+    const double t0 = fma(v1, R2.w0[1], v0 * R2.w0[0]);
+    const double t1 = fma(v1, R2.w1[1], v0 * R2.w1[0]);
+    m00 = fma(R2.w0[x], t0, m00);
+    m01 = fma(R2.w0[x], t1, m01);
+    m10 = fma(R2.w1[x], t0, m10);
+    m11 = fma(R2.w1[x], t1, m11);
+  }
+  return make_double4(m00 * JJ, m01 * JJ, m10 * JJ, m11 * JJ);
+}
+
 struct Cell1S {   // shared-memory copy of a tile's cells
   double x0[T1C], x1[T1C], lo[T1C], hi[T1C], h[T1C], lh[T1C];
   float lnhf[T1C], lhf[T1C];
@@ -762,12 +793,12 @@ __global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const
   // phase 1: every cell pair's order; k = 2 pairs (~95%) get their block right away.  Tile pairs
   // whose pairs are all provably of order 2 (~92% at c2) skip the orders (and have no touching pair)
   unsigned my = 0;
+  const Rule2 R2(tab + (size_t)dir.rule(T_DISJ, 2).off * NODE);
   if (uni2) {
-    const double* nd2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
     for (int p = tid; p < np; p += blockDim.x) {
       const int a = (int)(((unsigned)p * inv) >> 20), b = p - a * ncl;
       const PairGeo1D g = pair_geo1d(cr, a, cc, b);
-      store_block1d(M + 4 * p, block1d_k<2, E4>(nd2, g.px0, g.pe, g.qx0, g.qe, g.JJ, ex), g.kl);
+      store_block1d(M + 4 * p, block1d_2<E4>(R2, g.px0, g.pe, g.qx0, g.qe, g.JJ, ex), g.kl);
       const int oK = cr.own[a], oL = cc.own[b];
       if (g.kl && (RECT ? (oK == bi && oL == bj) : (min(oK, oL) == bi && max(oK, oL) == bj))) my += 4u;
     }
@@ -788,8 +819,7 @@ __global__ void __launch_bounds__(T1X, T1B) cross1d_tile_kernel(DevMesh m, const
     const bool owned = K < L && (RECT ? (oK == bi && oL == bj) : (min(oK, oL) == bi && max(oK, oL) == bj));
     if (k == 2) {
       const PairGeo1D g = pair_geo1d(cr, a, cc, b);
-      store_block1d(Mp, block1d_k<2, E4>(tab + (size_t)dir.rule(T_DISJ, 2).off * NODE, g.px0, g.pe, g.qx0, g.qe,
-                                         g.JJ, ex), g.kl);
+      store_block1d(Mp, block1d_2<E4>(R2, g.px0, g.pe, g.qx0, g.qe, g.JJ, ex), g.kl);
       my += owned ? 4u : 0u;
     } else {
       if (k) {
