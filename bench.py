@@ -203,6 +203,7 @@ def main():
     ap.add_argument("--matvecs", type=int, default=100)
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-near", action="store_true", help="skip the near-field (cluster path) timing")
     ap.add_argument("--ref-budget", type=float, default=8.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -356,6 +357,26 @@ def main():
         e2e = {"value": pairs / float(np.median(et)), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d * world),
                "d2h_bytes_per_step": int(8 * n * n), "seconds_per_step": float(np.median(et))}
 
+    # near-field (cluster path) assembly of the same mesh, SPEC defaults (leaf cap 8 / 16, eta 1):
+    # assemble_near_field through the public API (host tree + partition excluded, CSR returned to
+    # the host included), median of 3 after one warm-up
+    near = None
+    if rank == 0 and world == 1 and not args.no_near:
+        from paper_1708_03912_b200 import cluster as CL
+        th = time.perf_counter()
+        tree = CL.build_tree(mesh, dm, 8 if mesh.d == 1 else 16)
+        far_nodes, near_nodes = CL.admissible_partition(tree, 1.0)
+        ns = CL.NearStructure(mesh, dm, tree, near_nodes)
+        host_s = time.perf_counter() - th
+        nts = []
+        for i in range(4):
+            t0 = time.perf_counter()
+            An = A.assemble_near_field(mesh, dm, ker, ns)
+            nts.append(time.perf_counter() - t0)
+        near = {"ms": 1e3 * float(np.median(nts[1:])), "nnz": int(An.nnz), "leaf_cap": 8 if mesh.d == 1 else 16,
+                "eta": 1.0, "near_leaf_pairs": int(len(ns.nl_pairs)), "far_node_pairs": int(len(far_nodes)),
+                "host_tree_partition_s": host_s}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, info = cpu_sample(args.config)
@@ -376,7 +397,8 @@ def main():
                                                                "ms_cross_compute", "ms_local", "ms_total")},
                            "near_pairs": stats["near_pairs"], "evals_tail": stats["evals_tail"],
                            "evals_cross": stats["evals_cross"]},
-                "roofline": roofline, "matvec": matvec, "cg": cg, "e2e": e2e, "cpu_baseline": cpu,
+                "roofline": roofline, "matvec": matvec, "cg": cg, "e2e": e2e, "near_field": near,
+                "cpu_baseline": cpu,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
     op.free()

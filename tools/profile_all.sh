@@ -5,14 +5,14 @@ set -u
 mkdir -p gpurun_out
 run() {   # run <tag> <config> [extra bench args]
   local TAG=$1 CFG=$2; shift 2
-  local CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cg --no-cpu --matvecs 3 $*"
+  local CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cg --no-cpu --no-near --matvecs 3 $*"
   $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run $TAG failed"; return 1; }
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
       $CMD > gpurun_out/ncu_l_$TAG.log 2>&1
 }
 full() {  # full <tag> <config> <kernel-regex> <skip> <count>
   local TAG=$1 CFG=$2 KRE=$3 SKIP=$4 CNT=$5
-  local CMD="python bench.py --config $CFG --steps 1 --warmup 0 --no-cg --no-cpu --matvecs 3"
+  local CMD="python bench.py --config $CFG --steps 1 --warmup 0 --no-cg --no-cpu --no-near --matvecs 3"
   $CMD > gpurun_out/plain_f_$TAG.log 2>&1 || { echo "plain run $TAG failed"; return 1; }
   ncu --set full --clock-control none --import-source on -k regex:"$KRE" --launch-skip $SKIP -c $CNT \
       -o gpurun_out/prof_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
