@@ -184,11 +184,11 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
   }
   const double* n2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
   const double t0 = n2[0], w0 = n2[2], t1 = n2[NODE], w1 = n2[NODE + 2];
-  unsigned nodes[NT], umask[NT];
+  unsigned nodes[NT], umask[NT], rmask[NT];
   int qn[NT];                                   // warp-uniform queue lengths
   const int nchunks = (m.nc + 31) >> 5;
 #pragma unroll
-  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; umask[t] = 0; }
+  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; umask[t] = 0; rmask[t] = 0; }
   const unsigned lt = (1u << lane) - 1u;
   const int4* R = reinterpret_cast<const int4*>(S.rec);
   int4 na = make_int4(0, 0, 0, 0), nb = na;     // prefetched record of the next source
@@ -207,21 +207,31 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
     if ((ci & 31) == 0) {                       // order-2 flags of the next 32 chunks, one per lane
       const int cj = ci + lane;
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
+      for (int t = 0; t < NT; ++t) {
         umask[t] = __ballot_sync(0xffffffffu, cj < nchunks &&
                                                   chunk_all_k2(oc, alo[t], ahi[t], alh[t], alg[t],
                                                                S.cstat + (size_t)CSTAT * cj));
+        rmask[t] = __ballot_sync(0xffffffffu, cj < nchunks && S.cstat[(size_t)CSTAT * cj] > ahi[t]);
+      }
     }
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       if ((umask[t] >> (ci & 31)) & 1u) {       // warp-uniform: the whole chunk is k = 2
+        // the chunk lies on one side of the target (gap > 0): the distance is y - x or x - y,
+        // positive, so the kernel power needs no |.| (bitwise the same values)
         if (s < m.nc) {
+          if ((rmask[t] >> (ci & 31)) & 1u) {
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const double d0 = xq[t][q] - y0;
-            acc[t][q] = fma(j0, kpow_abs<E4>(d0, ex), acc[t][q]);
-            const double d1 = xq[t][q] - y1;
-            acc[t][q] = fma(j1, kpow_abs<E4>(d1, ex), acc[t][q]);
+            for (int q = 0; q < Q; ++q) {
+              acc[t][q] = fma(j0, kpow_pos<E4>(y0 - xq[t][q], ex), acc[t][q]);
+              acc[t][q] = fma(j1, kpow_pos<E4>(y1 - xq[t][q], ex), acc[t][q]);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+              acc[t][q] = fma(j0, kpow_pos<E4>(xq[t][q] - y0, ex), acc[t][q]);
+              acc[t][q] = fma(j1, kpow_pos<E4>(xq[t][q] - y1, ex), acc[t][q]);
+            }
           }
           nodes[t] += 2;
         }
