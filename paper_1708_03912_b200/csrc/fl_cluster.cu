@@ -15,6 +15,8 @@
 #include <memory>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "../../include/fraclap_b200.h"
 #include "fl_internal.h"
 
@@ -29,6 +31,9 @@ struct fl_cluster {
   fl::DBuf<int> leaf_nodes, leaf_lo, leaf_hi, dof_perm, leaf_of_dof, children, parent, pairs, plist_off, plist,
       level_nodes;
   std::vector<int64_t> level_off_up, level_off_down;   // offsets into level_nodes (host copies)
+  fl::DBuf<int64_t> d_off_up, d_off_down;               // ... and device copies (fused far field)
+  bool fused = false;
+  int coop_blocks = 0;                                  // resident blocks of the cooperative far field
   int nleaves = 0;
   cudaStream_t stream = nullptr;
   ~fl_cluster() {
@@ -38,6 +43,8 @@ struct fl_cluster {
       b->free();
     indptr.free();
     indices.free();
+    d_off_up.free();
+    d_off_down.free();
     if (stream) fl::release_stream(device, stream);
   }
 };
@@ -167,6 +174,88 @@ __global__ void eval_kernel(int64_t n, const int* __restrict__ leaf_of_dof, cons
   const double v = negC * s;
   yfar[i] = v;
   y[i] += v;
+}
+
+// The whole far field in ONE cooperative launch (small / medium operators, e.g. 1D at c2: ~2k
+// nodes, M <= 12): the same phases and accumulation orders as the kernels above, separated by
+// grid-wide barriers instead of ~2 x depth + 4 launches.
+template <int D>
+__global__ void __launch_bounds__(256) far_fused_kernel(
+    int nleaves, const int* __restrict__ leaf_nodes, const int* __restrict__ lo, const int* __restrict__ hi,
+    const int* __restrict__ perm, const double* __restrict__ x, const double* __restrict__ bc, int m, int M,
+    int64_t nn, const int* __restrict__ level_nodes, const int64_t* __restrict__ off_up, int nup,
+    const int64_t* __restrict__ off_down, int ndown, const int* __restrict__ children, const int* __restrict__ parent,
+    const double* __restrict__ shift, int64_t np, const int* __restrict__ pairs, const double* __restrict__ B,
+    const int* __restrict__ poff, const int* __restrict__ plist, double* __restrict__ mom, double* __restrict__ Fp,
+    double* __restrict__ F, int64_t n, const int* __restrict__ leaf_of_dof, double negC, double* __restrict__ y,
+    double* __restrict__ yfar) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = tid; t < nn * M; t += nt) mom[t] = 0.0;
+  grid.sync();
+  for (int64_t t = tid; t < (int64_t)nleaves * M; t += nt) {
+    const int l = (int)(t / M), a = (int)(t % M);
+    double s = 0.0;
+    for (int r = lo[l]; r < hi[l]; ++r) s = fma(x[perm[r]], bc[(int64_t)perm[r] * M + a], s);
+    mom[(int64_t)leaf_nodes[l] * M + a] = s;
+  }
+  grid.sync();
+  for (int L = 0; L < nup; ++L) {
+    const int64_t a0 = off_up[L], cnt = off_up[L + 1] - a0;
+    for (int64_t t = tid; t < cnt * M; t += nt) {
+      const int p = level_nodes[a0 + t / M], a = (int)(t % M);
+      double acc = mom[(int64_t)p * M + a];
+      for (int k = 1; k >= 0; --k) {
+        const int c = children[2 * p + k];
+        if (c >= 0) acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+      }
+      mom[(int64_t)p * M + a] = acc;
+    }
+    grid.sync();
+  }
+  for (int64_t t = tid; t < np * 2 * M; t += nt) {
+    const int64_t p = t / (2 * M);
+    const int r = (int)(t % (2 * M));
+    const double* Bp = B + p * M * M;
+    double s = 0.0;
+    if (r < M) {
+      const double* mb = mom + (int64_t)pairs[2 * p + 1] * M;
+      for (int b = 0; b < M; ++b) s = fma(Bp[(int64_t)r * M + b], mb[b], s);
+    } else {
+      const double* ma = mom + (int64_t)pairs[2 * p] * M;
+      for (int a = 0; a < M; ++a) s = fma(Bp[(int64_t)a * M + (r - M)], ma[a], s);
+    }
+    Fp[t] = s;
+  }
+  grid.sync();
+  for (int64_t t = tid; t < nn * M; t += nt) {
+    const int64_t nd = t / M;
+    const int a = (int)(t % M);
+    double s = 0.0;
+    for (int k = poff[nd]; k < poff[nd + 1]; ++k) {
+      const int e = plist[k];
+      s += Fp[(int64_t)(e >> 1) * 2 * M + (e & 1) * M + a];
+    }
+    F[t] = s;
+  }
+  grid.sync();
+  for (int L = 0; L < ndown; ++L) {
+    const int64_t a0 = off_down[L], cnt = off_down[L + 1] - a0;
+    for (int64_t t = tid; t < cnt * M; t += nt) {
+      const int c = level_nodes[a0 + t / M], a = (int)(t % M);
+      F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)parent[c] * M, m, a, true);
+    }
+    grid.sync();
+  }
+  for (int64_t i = tid; i < n; i += nt) {
+    const double* f = F + (int64_t)leaf_of_dof[i] * M;
+    double s = 0.0;
+    for (int a = 0; a < M; ++a) s = fma(bc[i * M + a], f[a], s);
+    const double v = negC * s;
+    yfar[i] = v;
+    y[i] += v;
+  }
 }
 
 template <int E4>
@@ -328,6 +417,23 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
       FL_CUDA(cudaStreamSynchronize(st));
     }
   }
+  auto up_l = [&](DBuf<int64_t>& b, const std::vector<int64_t>& h) {
+    b.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty()) FL_CUDA(cudaMemcpyAsync(b.p, h.data(), h.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  };
+  up_l(C->d_off_up, off_up);
+  up_l(C->d_off_down, off_down);
+  // one block does the far field when it is small (work ~ far blocks + shifts), else level kernels
+  C->fused = (double)np * M * M + (double)nn * M * m * (d == 2 ? m : 1) <= 8.0e6;
+  if (C->fused) {
+    int sms = 148, per = 0, coop = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, d == 1 ? (const void*)far_fused_kernel<1>
+                                                               : (const void*)far_fused_kernel<2>, 256, 0);
+    C->coop_blocks = sms * std::min(per, getenv("FRACLAP_COOP_PER_SM") ? atoi(getenv("FRACLAP_COOP_PER_SM")) : 1);
+    C->fused = coop && C->coop_blocks > 0;
+  }
   C->mom.alloc((size_t)nn * M);
   C->F.alloc((size_t)nn * M);
   C->Fp.alloc(std::max<int64_t>(np * 2 * M, 1));
@@ -344,6 +450,22 @@ int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yf
   const int M = C->M, m = C->m;
   if (n == 0) return FL_OK;
   csr_spmv_kernel<<<grid_of(n * 32), 256, 0, st>>>(n, C->indptr.p, C->indices.p, C->data.p, x, y), note_launch();
+  if (C->fused) {
+    int nup = (int)C->level_off_up.size() - 1, ndown = (int)C->level_off_down.size() - 1;
+    int nl = C->nleaves;
+    double negC = -C->C;
+    int64_t nn_ = nn, np_ = np, n_ = n;
+    int m_ = m, M_ = M;
+    void* args[] = {&nl, &C->leaf_nodes.p, &C->leaf_lo.p, &C->leaf_hi.p, &C->dof_perm.p, &x, &C->bc.p, &m_, &M_,
+                    &nn_, &C->level_nodes.p, &C->d_off_up.p, &nup, &C->d_off_down.p, &ndown, &C->children.p,
+                    &C->parent.p, &C->shift.p, &np_, &C->pairs.p, &C->blocks.p, &C->plist_off.p, &C->plist.p,
+                    &C->mom.p, &C->Fp.p, &C->F.p, &n_, &C->leaf_of_dof.p, &negC, &y, &yfar};
+    const void* fn = C->d == 1 ? (const void*)far_fused_kernel<1> : (const void*)far_fused_kernel<2>;
+    FL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(C->coop_blocks), dim3(256), args, 0, st));
+    note_launch();
+    FL_CHECK_LAUNCH();
+    return FL_OK;
+  }
   FL_CUDA(cudaMemsetAsync(C->mom.p, 0, (size_t)nn * M * sizeof(double), st));
   moments_kernel<<<grid_of((int64_t)C->nleaves * M), 256, 0, st>>>(C->nleaves, C->leaf_nodes.p, C->leaf_lo.p,
                                                                    C->leaf_hi.p, C->dof_perm.p, x, C->bc.p, M,
