@@ -3,6 +3,8 @@
 // (fixed grid, fixed per-thread order, fixed shuffle pattern): results are bitwise
 // reproducible.  The CG scalars live on the device; the host polls a `done` flag every few
 // iterations, so the iteration count is exactly the reference's.
+#include <cstdlib>
+
 #include "fl_internal.h"
 
 #ifndef FL_MV_U
@@ -61,14 +63,58 @@ __global__ void __launch_bounds__(256) matvec_kernel(const double* __restrict__ 
   }
 }
 
+// One CTA (256 threads) per row: short rows (n ~ 8k) are split over 8 warps, so a matrix of a
+// few hundred MB streams in many small, evenly sized pieces (fixed per-thread column sets and a
+// fixed reduction tree: deterministic).
+__global__ void __launch_bounds__(256) matvec_rowcta_kernel(const double* __restrict__ A, int64_t rows,
+                                                            int64_t ncol2, int64_t lda, const double* __restrict__ x,
+                                                            double* __restrict__ y, const int* __restrict__ done) {
+  if (done != nullptr && *done) return;
+  __shared__ double red[8];
+  const int64_t r = blockIdx.x;
+  const double2* a2 = reinterpret_cast<const double2*>(A + r * lda);
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double acc = 0.0;
+  int64_t j = threadIdx.x;
+  for (; j + 256 * 3 < ncol2; j += 256 * 4) {
+    double2 av[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { av[u] = __ldcs(a2 + j + 256 * u); xv[u] = __ldg(x2 + j + 256 * u); }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc = fma(av[u].y, xv[u].y, fma(av[u].x, xv[u].x, acc));
+  }
+  for (; j < ncol2; j += 256) {
+    const double2 av = __ldcs(a2 + j), xv = __ldg(x2 + j);
+    acc = fma(av.y, xv.y, fma(av.x, xv.x, acc));
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < 8 ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) y[r] = v;
+  }
+}
+
 void launch_matvec_flag(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
                         const int* done, cudaStream_t st) {
   if (rows <= 0) return;
   const int64_t ncol2 = (n + 1) / 2;
-  if (rows >= 148LL * 64 * 4) {
+  static const int rpw_env = [] { const char* v = getenv("FL_MV_RPW"); return v ? atoi(v) : 0; }();
+  // CTA per row: fastest at c2 (537 MB, 6.1 vs 5.1 TB/s) and c4 (2.2 GB); a warp per 4 rows for
+  // very many rows (c5, 65k rows of 520 KB: 6.94 vs 6.80 TB/s)
+  const int rpw = rpw_env ? rpw_env : (rows >= 148LL * 64 * 4 ? 4 : 8);
+  if (rpw == 8) {      // (FL_MV_RPW=8: the CTA-per-row variant)
+    matvec_rowcta_kernel<<<(unsigned)rows, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done), ::fl::note_launch();
+  } else if (rpw == 4) {
     const int64_t warps = (rows + 3) / 4;
     const int grid = (int)((warps * 32 + 255) / 256);
     matvec_kernel<4><<<grid, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done), ::fl::note_launch();
+  } else if (rpw == 2) {
+    const int64_t warps = (rows + 1) / 2;
+    const int grid = (int)((warps * 32 + 255) / 256);
+    matvec_kernel<2><<<grid, 256, 0, st>>>(A, rows, ncol2, lda, x, y, done), ::fl::note_launch();
   } else {
     const int64_t warps = rows;
     const int grid = (int)((warps * 32 + 255) / 256);
