@@ -229,10 +229,26 @@ typedef struct fl_cluster_desc {
   const int64_t* indptr;
   const int64_t* indices;
   const double* data;
+  /* optional (point evaluation, fl_cluster_strong_form): node boxes and the Chebyshev nodes */
+  const double* center;             /* (num_nodes, d) tree.center */
+  const double* half;               /* (num_nodes,) tree.half */
+  const double* ref;                /* (m,) cheb.ref = cos((2j+1) pi / 2m) */
 } fl_cluster_desc;
 int32_t fl_cluster_create(const fl_cluster_desc* desc, int32_t device, fl_cluster** out);
 /* y = A x (and y_far = the far part alone, if non-NULL); ptr_kind 0: host arrays, 1: device */
 int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_far, int32_t ptr_kind);
+/* (-Delta)^s u_h at per-cell nodes X (nc, q, d): adapt.strong_form_at (adapt.py:81-214) — the
+ * cluster far field evaluated at the points (evaluate_far_field_at_points, cluster.py:469-485) plus
+ * the surface terms of the owning leaf's near cells (u restricted to the near DoFs) and of the
+ * point's own cell.  cell_leaf: leaf node of every cell (_cell_leaf_assignment); near leaf nodes of
+ * every node as CSR (near_off (num_nodes+1), near_val; ClusterOperator.near_dof_leaves); near cells
+ * of every node as CSR (ncell_off, ncell_val; cells supporting the near leaves' DoFs); the edge
+ * rule (gl_x, gl_w on [0, 1]).  out / far_out: (nc, q). */
+int32_t fl_cluster_strong_form(fl_cluster* C, const fl_mesh* mesh, const fl_dofmap* dofmap, double s,
+                               const double* u, int64_t q, const double* X, const int64_t* cell_leaf,
+                               const int64_t* near_off, const int64_t* near_val, const int64_t* ncell_off,
+                               const int64_t* ncell_val, const double* gl_x, const double* gl_w, int64_t ngl,
+                               double* out, double* far_out);
 /* the device far blocks (npairs, M, M) */
 int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out);
 void fl_cluster_free(fl_cluster* C);

@@ -173,17 +173,21 @@ class ClusterOperatorDevice:
     `from_operator(op)` wraps an operator built by the reference's `cluster.compress` (or any
     object with its attributes: tree, cheb, near, far_pairs, far_blocks, basis_coef, kernel)."""
 
-    def __init__(self, handle, n, diag, d, M):
+    def __init__(self, handle, n, diag, d, M, s=None, tree_info=None):
         self._h = handle
         self.n = int(n)
         self._diag = diag
         self.d, self.M = d, M
+        self.s = s
+        self.tree_info = tree_info      # host tree data for adapt.strong_form_at (or None)
         self.shape = (self.n, self.n)
         self.dtype = np.float64
 
     @classmethod
     def from_arrays(cls, d, m, parent, topo_order, ranges, dof_perm, shift, basis_coef, far_pairs, far_blocks,
-                    points, s, C_ds, near, diag=None, device=None):
+                    points, s, C_ds, near, diag=None, device=None, center=None, half=None, near_leaf_map=None):
+        """`center`, `half` (tree boxes) and `near_leaf_map` (node -> near leaf nodes,
+        ClusterOperator.near_dof_leaves) enable adapt.strong_form_at on this operator."""
         import ctypes as C
         from scipy.sparse import csr_matrix
         from . import _lib
@@ -199,16 +203,33 @@ class ClusterOperatorDevice:
                     data=f64(near.data))
         keep["blocks"] = None if far_blocks is None else f64(far_blocks).reshape(-1, M, M)
         keep["points"] = None if points is None else f64(points)
+        have_boxes = center is not None and half is not None
+        keep["center"] = f64(center).reshape(-1, d) if have_boxes else None
+        keep["half"] = f64(half).reshape(-1) if have_boxes else None
+        j = np.arange(m)
+        keep["ref"] = f64(np.cos((2 * j + 1) * np.pi / (2 * m))) if have_boxes else None   # cheb_points_1d
         ptr = lambda a: None if a is None or a.size == 0 else a.ctypes.data   # noqa: E731
         desc = _lib.fl_cluster_desc(d, m, n, len(keep["parent"]), ptr(keep["parent"]), ptr(keep["topo"]),
                                     ptr(keep["ranges"]), ptr(keep["perm"]), ptr(keep["shift"]), ptr(keep["bc"]),
                                     len(keep["pairs"]), ptr(keep["pairs"]), ptr(keep["blocks"]), ptr(keep["points"]),
                                     float(s), float(C_ds), int(near.nnz), ptr(keep["indptr"]), ptr(keep["indices"]),
-                                    ptr(keep["data"]))
+                                    ptr(keep["data"]), ptr(keep["center"]), ptr(keep["half"]), ptr(keep["ref"]))
         from .assembly import _device_index
         h = C.c_void_p()
         _lib.check(_lib.load().fl_cluster_create(C.byref(desc), _device_index(device), C.byref(h)))
-        return cls(h, n, near.diagonal().copy() if diag is None else np.asarray(diag, float), d, M)
+        info = None
+        if have_boxes and near_leaf_map is not None:
+            rng, perm, par = keep["ranges"], keep["perm"], keep["parent"]
+            nn = len(par)
+            internal = np.zeros(nn, bool)
+            internal[par[par >= 0]] = True
+            leaf_of_dof = np.empty(n, np.int64)
+            for nd in np.nonzero(~internal)[0]:
+                leaf_of_dof[perm[rng[nd, 0]:rng[nd, 1]]] = nd
+            info = {"num_nodes": nn, "node_dofs": lambda nd: perm[rng[nd, 0]:rng[nd, 1]],
+                    "near_leaf_map": {int(k): np.asarray(v) for k, v in near_leaf_map.items()},
+                    "leaf_of_dof": leaf_of_dof}
+        return cls(h, n, near.diagonal().copy() if diag is None else np.asarray(diag, float), d, M, float(s), info)
 
     @classmethod
     def from_operator(cls, op, device=None, build_blocks_on_device=False):
@@ -222,7 +243,8 @@ class ClusterOperatorDevice:
                     shift[nd, j] = cheb.shift[nd][j]
         return cls.from_arrays(d, m, tree.parent, tree.topo_order, tree.ranges, tree.dof_perm, shift, op.basis_coef,
                                op.far_pairs, None if build_blocks_on_device else op.far_blocks, cheb.points,
-                               op.kernel.s, op.kernel.C_ds, op.near, op.diag(), device)
+                               op.kernel.s, op.kernel.C_ds, op.near, op.diag(), device, tree.center, tree.half,
+                               op.near_dof_leaves())
 
     # ------------------------------------------------------------ contract
     def _apply(self, x, want_far=False):

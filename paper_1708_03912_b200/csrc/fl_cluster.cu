@@ -32,6 +32,7 @@ struct fl_cluster {
       level_nodes;
   std::vector<int64_t> level_off_up, level_off_down;   // offsets into level_nodes (host copies)
   fl::DBuf<int64_t> d_off_up, d_off_down;               // ... and device copies (fused far field)
+  fl::DBuf<double> center, half, ref;                   // node boxes and Chebyshev nodes (point evaluation)
   bool fused = false;
   int coop_blocks = 0;                                  // resident blocks of the cooperative far field
   int nleaves = 0;
@@ -45,6 +46,9 @@ struct fl_cluster {
     indices.free();
     d_off_up.free();
     d_off_down.free();
+    center.free();
+    half.free();
+    ref.free();
     if (stream) fl::release_stream(device, stream);
   }
 };
@@ -380,6 +384,11 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
   up_i(C->plist_off, cnt); up_i(C->plist, lst); up_i(C->level_nodes, lvl_nodes);
   up_d(C->shift, D.shift, (size_t)nn * d * m * m);
   up_d(C->bc, D.basis_coef, (size_t)n * M);
+  if (D.center && D.half && D.ref) {
+    up_d(C->center, D.center, (size_t)nn * d);
+    up_d(C->half, D.half, (size_t)nn);
+    up_d(C->ref, D.ref, (size_t)m);
+  }
   // near CSR
   if (D.nnz < 0 || (D.nnz > 0 && (!D.indptr || !D.indices || !D.data))) throw Error(FL_E_ARG, "cluster: bad near CSR");
   C->indptr.alloc(n + 1);
@@ -445,6 +454,8 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
   return FL_OK;
 }
 
+void far_potentials(fl_cluster* C, const double* x, cudaStream_t st);
+
 int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yfar, cudaStream_t st) {
   const int64_t n = C->n, nn = C->nn, np = C->np;
   const int M = C->M, m = C->m;
@@ -466,6 +477,16 @@ int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yf
     FL_CHECK_LAUNCH();
     return FL_OK;
   }
+  far_potentials(C, x, st);
+  eval_kernel<<<grid_of(n), 256, 0, st>>>(n, C->leaf_of_dof.p, C->bc.p, M, C->F.p, -C->C, y, yfar), note_launch();
+  FL_CHECK_LAUNCH();
+  return FL_OK;
+}
+
+// F = the far potentials of x at every tree node (moments, upward pass, far pairs, downward pass)
+void far_potentials(fl_cluster* C, const double* x, cudaStream_t st) {
+  const int64_t nn = C->nn, np = C->np;
+  const int M = C->M, m = C->m;
   FL_CUDA(cudaMemsetAsync(C->mom.p, 0, (size_t)nn * M * sizeof(double), st));
   moments_kernel<<<grid_of((int64_t)C->nleaves * M), 256, 0, st>>>(C->nleaves, C->leaf_nodes.p, C->leaf_lo.p,
                                                                    C->leaf_hi.p, C->dof_perm.p, x, C->bc.p, M,
@@ -497,7 +518,227 @@ int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yf
                                                        C->F.p);
     note_launch();
   }
-  eval_kernel<<<grid_of(n), 256, 0, st>>>(n, C->leaf_of_dof.p, C->bc.p, M, C->F.p, -C->C, y, yfar), note_launch();
+  FL_CHECK_LAUNCH();
+}
+
+}  // namespace fl
+
+// ------------------------------------------------------------------ strong form (adapt.py:81-214)
+namespace fl {
+namespace {
+
+// Lagrange basis at the Chebyshev nodes `ref` (lagrange_eval, cluster.py:276-287): products in order
+__device__ __forceinline__ double lagrange1(const double* __restrict__ ref, int m, double t, int a) {
+  double num = 1.0, den = 1.0;
+  for (int b = 0; b < m; ++b) {
+    if (b == a) continue;
+    num *= t - ref[b];
+    den *= ref[a] - ref[b];
+  }
+  return num / den;
+}
+
+// -C * L(x) . F[owner]   (evaluate_far_field_at_points, cluster.py:469-485; eval_basis :327-337)
+template <int D>
+__global__ void far_points_kernel(int64_t npts, int q, const double* __restrict__ X,
+                                  const int64_t* __restrict__ cell_leaf, const double* __restrict__ center,
+                                  const double* __restrict__ half, const double* __restrict__ ref, int m, int M,
+                                  const double* __restrict__ F, double negC, double* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npts) return;
+  const int64_t nd = cell_leaf[p / q];             // the owning leaf of the point's cell
+  double l0[16], l1[16];
+  const double t0 = (X[p * D] - center[nd * D]) / half[nd];
+  for (int a = 0; a < m; ++a) l0[a] = lagrange1(ref, m, t0, a);
+  if (D == 2) {
+    const double t1 = (X[p * D + 1] - center[nd * D + 1]) / half[nd];
+    for (int a = 0; a < m; ++a) l1[a] = lagrange1(ref, m, t1, a);
+  }
+  const double* f = F + nd * M;
+  double s = 0.0;
+  for (int a = 0; a < M; ++a) s = fma(D == 1 ? l0[a] : l0[a / m] * l1[a % m], f[a], s);
+  out[p] = negC * s;
+}
+
+struct CellSurf {                     // one cell's vertices, hat values and gradient
+  double P[3][2], v[3], g[2];
+};
+// grad u_K from the vertex values: 1D (v1 - v0) / (P1 - P0); 2D the reference's
+// inv(E^T) [v1 - v0, v2 - v0] with E rows the edge vectors (_cell_gradients_fixed, adapt.py:45-54)
+template <int D>
+__device__ __forceinline__ void cell_grad(CellSurf& c) {
+  if (D == 1) {
+    c.g[0] = (c.v[1] - c.v[0]) / (c.P[1][0] - c.P[0][0]);
+  } else {
+    const double e1x = c.P[1][0] - c.P[0][0], e1y = c.P[1][1] - c.P[0][1];
+    const double e2x = c.P[2][0] - c.P[0][0], e2y = c.P[2][1] - c.P[0][1];
+    const double r0 = c.v[1] - c.v[0], r1 = c.v[2] - c.v[0];
+    const double det = e1x * e2y - e2x * e1y;           // E^T = [[e1x, e2x], [e1y, e2y]]
+    c.g[0] = (e2y * r0 - e2x * r1) / det;
+    c.g[1] = (e1x * r1 - e1y * r0) / det;
+  }
+}
+
+struct SurfConsts {
+  double s, ex_flux, p_grad, cgrad_near, cgrad_own;   // gradient-term divisors of the near / own formulas
+  int log_case, ngl;
+  const double* glx;
+  const double* glw;
+};
+
+// surface terms of cell c at point x: returns (gradient term, flux term) sums over the cell's edges
+// (1D: its two end points), the flux term WITHOUT the u factor when `flux_only` (own cell)
+template <int D>
+__device__ void surf_terms(const CellSurf& c, double x0, double x1, const SurfConsts& K, bool own, double& tg,
+                           double& tf) {
+  tg = 0.0;
+  tf = 0.0;
+  if (D == 1) {
+    const double sg = c.P[1][0] - c.P[0][0] > 0.0 ? 1.0 : (c.P[1][0] - c.P[0][0] < 0.0 ? -1.0 : 0.0);
+    for (int e = 0; e < 2; ++e) {
+      const double pn = e == 0 ? -sg : sg;
+      const double diff = x0 - c.P[e][0], r = fabs(diff);
+      const double gp = c.g[0] * pn;
+      tg += K.log_case ? gp * log(1.0 / r) : gp * pow(r, K.p_grad);
+      const double fl = pn * diff * pow(r, -1.0 - 2.0 * K.s);
+      tf += own ? fl : c.v[e] * fl;
+    }
+  } else {
+    const double cx = (c.P[0][0] + c.P[1][0] + c.P[2][0]) / 3.0, cy = (c.P[0][1] + c.P[1][1] + c.P[2][1]) / 3.0;
+    for (int e = 0; e < 3; ++e) {
+      const int a = e, b = (e + 1) % 3;
+      const double tx = c.P[b][0] - c.P[a][0], ty = c.P[b][1] - c.P[a][1];
+      const double EL = sqrt(tx * tx + ty * ty);
+      double nx = ty / EL, ny = -tx / EL;
+      const double mx = 0.5 * (c.P[a][0] + c.P[b][0]) - cx, my = 0.5 * (c.P[a][1] + c.P[b][1]) - cy;
+      if (mx * nx + my * ny < 0.0) { nx = -nx; ny = -ny; }
+      const double gn = c.g[0] * nx + c.g[1] * ny;
+      double sg = 0.0, sf = 0.0;
+      for (int qq = 0; qq < K.ngl; ++qq) {
+        const double t = K.glx[qq], w = K.glw[qq];
+        const double yx = c.P[a][0] + t * tx, yy = c.P[a][1] + t * ty;
+        const double dx = x0 - yx, dy = x1 - yy;
+        const double r2 = dx * dx + dy * dy;
+        sg += w * (K.log_case ? -0.5 * log(r2) : pow(r2, 0.5 * K.p_grad));
+        const double uY = own ? 1.0 : c.v[a] * (1.0 - t) + c.v[b] * t;
+        sf += w * uY * (dx * nx + dy * ny) * pow(r2, K.ex_flux);
+      }
+      tg += gn * sg * EL;
+      tf += sf * EL;
+    }
+  }
+}
+
+// warp per point: near cells of the owning leaf (lanes; u restricted to the near DoFs, the point's
+// own cell excluded) + the own cell with the full u; out = far + C * contrib
+template <int D>
+__global__ void __launch_bounds__(256) strong_near_kernel(
+    DevMesh m, int64_t npts, int q, const double* __restrict__ X, const int64_t* __restrict__ cell_leaf,
+    const int64_t* __restrict__ near_off, const int64_t* __restrict__ near_val, const int64_t* __restrict__ ncell_off,
+    const int64_t* __restrict__ ncell_val, const int* __restrict__ leaf_of_dof, const double* __restrict__ u,
+    SurfConsts K, double Cds, const double* __restrict__ far, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= npts) return;
+  const int c = (int)(p / q);
+  const int64_t leaf = cell_leaf[c];
+  const double x0 = X[p * D], x1 = D == 2 ? X[p * D + 1] : 0.0;
+  const int64_t nl0 = near_off[leaf], nl1 = near_off[leaf + 1];
+  double acc = 0.0;
+  for (int64_t k = ncell_off[leaf] + lane; k < ncell_off[leaf + 1]; k += 32) {
+    const int Kc = (int)ncell_val[k];
+    if (Kc == c) continue;
+    CellSurf cs;
+    for (int j = 0; j <= D; ++j) {
+      const int v = m.cells[Kc * (D + 1) + j];
+      cs.P[j][0] = m.vert[v * D];
+      cs.P[j][1] = D == 2 ? m.vert[v * D + 1] : 0.0;
+      const int dof = m.v2d[v];
+      double val = 0.0;
+      if (dof >= 0) {                            // u restricted to the DoFs of the near leaves
+        const int64_t lf = leaf_of_dof[dof];
+        int64_t a = nl0, b = nl1;
+        while (a < b) {
+          const int64_t mid = (a + b) >> 1;
+          if (near_val[mid] < lf) a = mid + 1; else b = mid;
+        }
+        if (a < nl1 && near_val[a] == lf) val = u[dof];
+      }
+      cs.v[j] = val;
+    }
+    cell_grad<D>(cs);
+    double tg, tf;
+    surf_terms<D>(cs, x0, x1, K, false, tg, tf);
+    acc += tg / K.cgrad_near - tf / (2.0 * K.s);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    CellSurf cs;
+    for (int j = 0; j <= D; ++j) {
+      const int v = m.cells[c * (D + 1) + j];
+      cs.P[j][0] = m.vert[v * D];
+      cs.P[j][1] = D == 2 ? m.vert[v * D + 1] : 0.0;
+      const int dof = m.v2d[v];
+      cs.v[j] = dof >= 0 ? u[dof] : 0.0;
+    }
+    cell_grad<D>(cs);
+    double tg, tf;
+    surf_terms<D>(cs, x0, x1, K, true, tg, tf);
+    double ux;                                   // the affine u_c at x (_affine_on_cells, adapt.py:217-233)
+    if (D == 1) {
+      const double t = (x0 - cs.P[0][0]) / (cs.P[1][0] - cs.P[0][0]);
+      ux = cs.v[0] * (1.0 - t) + cs.v[1] * t;
+    } else {
+      const double e1x = cs.P[1][0] - cs.P[0][0], e1y = cs.P[1][1] - cs.P[0][1];
+      const double e2x = cs.P[2][0] - cs.P[0][0], e2y = cs.P[2][1] - cs.P[0][1];
+      const double rx = x0 - cs.P[0][0], ry = x1 - cs.P[0][1];
+      const double det = e1x * e2y - e2x * e1y;
+      const double a1 = (rx * e2y - ry * e2x) / det, a2 = (e1x * ry - e1y * rx) / det;
+      ux = cs.v[0] * (1.0 - a1 - a2) + cs.v[1] * a1 + cs.v[2] * a2;
+    }
+    acc += tg / K.cgrad_own - ux * tf / (2.0 * K.s);
+    out[p] = far[p] + Cds * acc;
+  }
+}
+
+}  // namespace
+
+int32_t cluster_strong_form(fl_cluster* C, const DevMesh& m, double s, const double* u_dev, int64_t q,
+                            const double* X_dev, const int64_t* cell_leaf, const int64_t* near_off,
+                            const int64_t* near_val, const int64_t* ncell_off, const int64_t* ncell_val,
+                            const double* glx, const double* glw, int ngl, double* out_dev, double* far_dev,
+                            cudaStream_t st) {
+  const int d = m.d;
+  const int64_t npts = (int64_t)m.nc * q;
+  if (!C->center.p || !C->ref.p) throw Error(FL_E_ARG, "cluster: strong form needs the node boxes (center, half, ref)");
+  if (C->m > 16) throw Error(FL_E_ARG, "cluster: Chebyshev order above 16");
+  far_potentials(C, u_dev, st);
+  if (d == 1)
+    far_points_kernel<1><<<grid_of(npts), 256, 0, st>>>(npts, (int)q, X_dev, cell_leaf, C->center.p, C->half.p, C->ref.p,
+                                                        C->m, C->M, C->F.p, -C->C, far_dev);
+  else
+    far_points_kernel<2><<<grid_of(npts), 256, 0, st>>>(npts, (int)q, X_dev, cell_leaf, C->center.p, C->half.p, C->ref.p,
+                                                        C->m, C->M, C->F.p, -C->C, far_dev);
+  note_launch();
+  SurfConsts K;
+  K.s = s;
+  K.ex_flux = -(d / 2.0 + s);
+  K.p_grad = 2.0 - d - 2.0 * s;
+  K.log_case = std::fabs(s - (1.0 - d / 2.0)) < 1e-12;      // LOG_CASE_TOL (adapt.py:25)
+  K.cgrad_near = K.log_case ? 2.0 * s : 2.0 * s * (d + 2.0 * s - 2.0);
+  K.cgrad_own = K.log_case ? 1.0 : (d + 2.0 * s - 2.0);
+  K.ngl = ngl;
+  K.glx = glx;
+  K.glw = glw;
+  if (d == 1)
+    strong_near_kernel<1><<<grid_of(npts * 32), 256, 0, st>>>(m, npts, (int)q, X_dev, cell_leaf, near_off, near_val,
+                                                              ncell_off, ncell_val, C->leaf_of_dof.p, u_dev, K, C->C,
+                                                              far_dev, out_dev);
+  else
+    strong_near_kernel<2><<<grid_of(npts * 32), 256, 0, st>>>(m, npts, (int)q, X_dev, cell_leaf, near_off, near_val,
+                                                              ncell_off, ncell_val, C->leaf_of_dof.p, u_dev, K, C->C,
+                                                              far_dev, out_dev);
+  note_launch();
   FL_CHECK_LAUNCH();
   return FL_OK;
 }
@@ -541,6 +782,64 @@ int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_f
   fl::cluster_matvec_dev(C, C->x.p, C->y.p, C->yfar.p, st);
   FL_CUDA(cudaMemcpyAsync(y, C->y.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
   if (y_far) FL_CUDA(cudaMemcpyAsync(y_far, C->yfar.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  return FL_OK;
+  FL_CATCH
+}
+
+int32_t fl_cluster_strong_form(fl_cluster* C, const fl_mesh* mesh, const fl_dofmap* dofmap, double s,
+                               const double* u, int64_t q, const double* X, const int64_t* cell_leaf,
+                               const int64_t* near_off, const int64_t* near_val, const int64_t* ncell_off,
+                               const int64_t* ncell_val, const double* gl_x, const double* gl_w, int64_t ngl,
+                               double* out, double* far_out) {
+  FL_TRY
+  if (!C || !mesh || !dofmap || !u || !X || !cell_leaf || !near_off || !near_val || !ncell_off || !ncell_val ||
+      !gl_x || !gl_w || !out)
+    return fl::api_fail(FL_E_ARG, "null argument");
+  if (!(s > 0.0 && s < 1.0)) return fl::api_fail(FL_E_ARG, "s must lie in (0,1)");
+  const int d = mesh->d;
+  if (d != C->d || dofmap->n != C->n || q <= 0 || ngl <= 0 || ngl > 64) return fl::api_fail(FL_E_ARG, "bad sizes");
+  const int64_t nv = mesh->nv, nc = mesh->nc, nn = C->nn;
+  for (int64_t c = 0; c < nc; ++c)
+    if (cell_leaf[c] < 0 || cell_leaf[c] >= nn) return fl::api_fail(FL_E_ARG, "cell leaf out of range");
+  FL_CUDA(cudaSetDevice(C->device));
+  cudaStream_t st = C->stream;
+  fl::StreamScope scope(st);
+  std::vector<int> cells((size_t)nc * (d + 1)), v2d((size_t)nv);
+  for (int64_t i = 0; i < nc * (d + 1); ++i) {
+    if (mesh->cells[i] < 0 || mesh->cells[i] >= nv) return fl::api_fail(FL_E_ARG, "cell vertex index out of range");
+    cells[i] = (int)mesh->cells[i];
+  }
+  for (int64_t v = 0; v < nv; ++v) v2d[v] = (int)dofmap->vertex_to_dof[v];
+  fl::DBuf<double> dvert((size_t)nv * d), du((size_t)std::max<int64_t>(C->n, 1)), dX((size_t)nc * q * d),
+      dglx(ngl), dglw(ngl), dout((size_t)nc * q), dfar((size_t)nc * q);
+  fl::DBuf<int> dcells(cells.size()), dv2d(v2d.size());
+  fl::DBuf<int64_t> dleaf(nc), dnoff(nn + 1), dnval, dcoff(nn + 1), dcval;
+  const int64_t nnv = near_off[nn], ncv = ncell_off[nn];
+  dnval.alloc(std::max<int64_t>(nnv, 1));
+  dcval.alloc(std::max<int64_t>(ncv, 1));
+  auto h2d = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) FL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  };
+  h2d(dvert.p, mesh->vertices, (size_t)nv * d * 8);
+  h2d(du.p, u, (size_t)C->n * 8);
+  h2d(dX.p, X, (size_t)nc * q * d * 8);
+  h2d(dglx.p, gl_x, (size_t)ngl * 8);
+  h2d(dglw.p, gl_w, (size_t)ngl * 8);
+  h2d(dcells.p, cells.data(), cells.size() * 4);
+  h2d(dv2d.p, v2d.data(), v2d.size() * 4);
+  h2d(dleaf.p, cell_leaf, (size_t)nc * 8);
+  h2d(dnoff.p, near_off, (size_t)(nn + 1) * 8);
+  h2d(dnval.p, near_val, (size_t)nnv * 8);
+  h2d(dcoff.p, ncell_off, (size_t)(nn + 1) * 8);
+  h2d(dcval.p, ncell_val, (size_t)ncv * 8);
+  fl::DevMesh m;
+  m.d = d; m.nv = (int)nv; m.nc = (int)nc; m.n = (int)C->n;
+  m.vert = dvert.p; m.cells = dcells.p; m.v2d = dv2d.p;
+  fl::cluster_strong_form(C, m, s, du.p, q, dX.p, dleaf.p, dnoff.p, dnval.p, dcoff.p, dcval.p, dglx.p, dglw.p,
+                          (int)ngl, dout.p, dfar.p, st);
+  FL_CUDA(cudaMemcpyAsync(out, dout.p, (size_t)nc * q * 8, cudaMemcpyDeviceToHost, st));
+  if (far_out) FL_CUDA(cudaMemcpyAsync(far_out, dfar.p, (size_t)nc * q * 8, cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   return FL_OK;
   FL_CATCH

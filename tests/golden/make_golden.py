@@ -606,6 +606,7 @@ def t_near():
 
 # cluster operator (cluster.compress, cluster.py:667-712) and its matvec (:417-456)
 CLUSTER = [("uniform1d", 96, 0.25, 8, 1.0, 8), ("graded1d", 200, 0.75, 8, 1.0, 10),
+           ("uniform1d", 120, 0.5, 8, 1.0, 8),
            ("square2d", 16, 0.5, 8, 1.0, 5), ("jit2d", 14, 0.25, 12, 1.0, 6), ("square2d", 20, 0.25, 16, 1.0, 4)]
 
 
@@ -637,7 +638,24 @@ def t_cluster():
                    parent=np.asarray(tree.parent, np.int64), topo_order=np.asarray(tree.topo_order, np.int64),
                    ranges=np.asarray(tree.ranges, np.int64), dof_perm=tree.dof_perm,
                    leaves=np.asarray(tree.leaves, np.int64), shift=shift, points=op.cheb.points,
-                   x=x, y=y, y_far=op.far_apply(x), diag=op.diag())
+                   x=x, y=y, y_far=op.far_apply(x), diag=op.diag(),
+                   center=np.asarray(tree.center), half=np.asarray(tree.half))
+        # strong form of u_h = x at the order-4 cell nodes (adapt.strong_form_at, adapt.py:81-214), its
+        # far part alone (ClusterOperator.evaluate_far_field_at_points, cluster.py:469-485) and the
+        # residual norms with f = 1 (adapt.residual_norms, :248-254)
+        from fraclap import adapt as AD
+        X4, W4, _ = A.cell_quadrature(mesh, 4)
+        cell_leaf = CL._cell_leaf_assignment(mesh, dm, tree)
+        rec["cell_leaf"] = np.asarray(cell_leaf, np.int64)
+        rec["X4"] = X4
+        rec["far_at_points"] = op.evaluate_far_field_at_points(x, X4.reshape(-1, mesh.d),
+                                                               np.repeat(cell_leaf, X4.shape[1]))
+        rec["strong_form"] = AD.strong_form_at(x, mesh, dm, op, X=X4)
+        rec["residual_norms"] = AD.residual_norms(x, lambda P: np.ones(len(P)), mesh, dm, op)
+        nlm = op.near_dof_leaves()
+        rec["near_leaf_keys"] = np.asarray(sorted(nlm), np.int64)
+        rec["near_leaf_off"] = np.cumsum([0] + [len(nlm[k]) for k in sorted(nlm)]).astype(np.int64)
+        rec["near_leaf_val"] = np.concatenate([nlm[k] for k in sorted(nlm)]).astype(np.int64)
         for k, v in rec.items():
             recs[tag + "/" + k] = v
         print(tag, "n=%d far=%d M=%d nnz=%d %.1fs" % (dm.n, len(op.far_pairs), op.cheb.M, near.nnz,
