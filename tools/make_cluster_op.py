@@ -25,6 +25,9 @@ x = np.random.default_rng(0).uniform(-1, 1, dm.n)
 ts = []
 for i in range(5):
     a = time.perf_counter(); y = op.matvec(x); ts.append(time.perf_counter() - a)
+from fraclap import adapt as AD
+a = time.perf_counter(); sf = AD.strong_form_at(x, mesh, dm, op); ref_sf_s = time.perf_counter() - a
+nlm = op.near_dof_leaves()
 nn = tree.num_nodes
 shift = np.zeros((nn, mesh.d, m, m))
 for nd in range(nn):
@@ -37,6 +40,11 @@ np.savez("bench_data/cluster_%s.npz" % cfg, d=mesh.d, m=m, s=s, C=ker.C_ds, pare
          topo_order=np.asarray(tree.topo_order), ranges=np.asarray(tree.ranges), dof_perm=tree.dof_perm,
          shift=shift, basis_coef=op.basis_coef, far_pairs=op.far_pairs, points=op.cheb.points,
          indptr=near.indptr, indices=near.indices, data=near.data, x=x, y=y,
-         ref_matvec_s=np.median(ts), ref_compress_s=t1 - t0, cores=os.cpu_count())
+         ref_matvec_s=np.median(ts), ref_compress_s=t1 - t0, cores=os.cpu_count(),
+         center=np.asarray(tree.center), half=np.asarray(tree.half), strong_form=sf, ref_strong_form_s=ref_sf_s,
+         near_leaf_keys=np.asarray(sorted(nlm), np.int64),
+         near_leaf_off=np.cumsum([0] + [len(nlm[k]) for k in sorted(nlm)]).astype(np.int64),
+         near_leaf_val=np.concatenate([nlm[k] for k in sorted(nlm)]).astype(np.int64),
+         vertices=mesh.vertices, cells=mesh.cells, bedges=mesh.boundary_edges, bnormals=mesh.boundary_normals)
 print(cfg, "n", dm.n, "far pairs", len(op.far_pairs), "nnz", near.nnz, "compress %.1f s" % (t1 - t0),
-      "reference matvec %.2f ms" % (1e3 * np.median(ts)))
+      "reference matvec %.2f ms" % (1e3 * np.median(ts)), "strong form %.2f s" % ref_sf_s)
