@@ -293,3 +293,308 @@ class ClusterOperatorDevice:
             self.free()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ Chebyshev data (host setup)
+def cheb_points_1d(m):
+    """cluster.py:271-273."""
+    j = np.arange(m)
+    return np.cos((2 * j + 1) * np.pi / (2 * m))
+
+
+def lagrange_eval(ref_nodes, t):
+    """Lagrange basis at the Chebyshev nodes evaluated at t (..., ) -> (..., m) (cluster.py:276-287)."""
+    m = len(ref_nodes)
+    t = np.asarray(t, float)
+    diff = t[..., None] - ref_nodes
+    out = np.empty(t.shape + (m,))
+    for a in range(m):
+        keep = np.arange(m) != a
+        out[..., a] = np.prod(diff[..., keep], axis=-1) / np.prod(ref_nodes[a] - ref_nodes[keep])
+    return out
+
+
+def choose_order(mesh_stats, tol=1e-6):
+    """m = ceil(c0 + c1 |log h_min| + log3(1e-6 / tol)) clipped to [3, 12] (cluster.py:256-268)."""
+    h_min = max(mesh_stats.h_min, 1e-300)
+    c0, c1 = (2.4, 0.85) if getattr(mesh_stats, "dim", None) == 1 else (2.0, 0.55)
+    m = c0 + c1 * abs(np.log(h_min)) + np.log(max(1e-6 / tol, 1.0)) / np.log(3.0)
+    return int(np.clip(np.ceil(m), 3, 12))
+
+
+class _Boxes:
+    """Tensor Chebyshev points, parent shift matrices and basis evaluation over a tree of boxes
+    (ChebData / ChebDataEdges, cluster.py:290-374, :596-664)."""
+
+    def __init__(self, center, half, parent, order, d, m, half_floor=None):
+        self.m, self.d, self.M = m, d, m ** d
+        self.ref = cheb_points_1d(m)
+        self.multi = np.arange(m)[:, None] if d == 1 else \
+            np.stack([a.ravel() for a in np.meshgrid(np.arange(m), np.arange(m), indexing="ij")], axis=1)
+        cen = np.asarray(center)
+        half = np.asarray(half) if half_floor is None else np.maximum(np.asarray(half), half_floor)
+        self.cen, self.half = cen, half
+        pts1 = cen[:, None, :] + half[:, None, None] * self.ref[None, :, None]
+        P = np.empty((len(cen), self.M, d))
+        for j in range(d):
+            P[:, :, j] = pts1[:, self.multi[:, j], j]
+        self.points = P
+        self.parent = np.asarray(parent)
+        self.order = list(order)
+        self.shift = [None] * len(cen)
+        for nd in self.order:
+            par = self.parent[nd]
+            if par < 0:
+                continue
+            self.shift[nd] = [lagrange_eval(self.ref, (cen[nd, j] + half[nd] * self.ref - cen[par, j]) / half[par]).T
+                              for j in range(d)]
+
+    def eval_basis(self, nd, X):
+        per = [lagrange_eval(self.ref, (X[..., j] - self.cen[nd][j]) / self.half[nd]) for j in range(self.d)]
+        return per[0] if self.d == 1 else per[0][..., self.multi[:, 0]] * per[1][..., self.multi[:, 1]]
+
+    def push_up(self, vals):
+        for nd in reversed(self.order):
+            par = self.parent[nd]
+            if par < 0 or not np.any(vals[nd]):
+                continue
+            if self.d == 1:
+                vals[par] += self.shift[nd][0] @ vals[nd]
+            else:
+                V = vals[nd].reshape(self.m, self.m)
+                vals[par] += (self.shift[nd][0] @ V @ self.shift[nd][1].T).ravel()
+        return vals
+
+    def push_down(self, vals):
+        for nd in self.order:
+            par = self.parent[nd]
+            if par < 0 or not np.any(vals[par]):
+                continue
+            if self.d == 1:
+                vals[nd] += self.shift[nd][0].T @ vals[par]
+            else:
+                V = vals[par].reshape(self.m, self.m)
+                vals[nd] += (self.shift[nd][0].T @ V @ self.shift[nd][1]).ravel()
+        return vals
+
+
+class EdgeTree:
+    """Cluster tree over the boundary edges (boxes cover whole edges; cluster.py:120-192)."""
+
+    def __init__(self, mesh, leaf_cap=8):
+        d = mesh.vertices.shape[1]
+        E = np.asarray(mesh.boundary_edges)
+        if d == 1:
+            lo = hi = pts = mesh.vertices[E[:, 0]]
+        else:
+            p0, p1 = mesh.vertices[E[:, 0]], mesh.vertices[E[:, 1]]
+            lo, hi, pts = np.minimum(p0, p1), np.maximum(p0, p1), 0.5 * (p0 + p1)
+        self.perm = np.arange(len(E))
+        self.ranges, self.children, center, half = [], [], [], []
+
+        def add(a, b):
+            sel = self.perm[a:b]
+            l, h = lo[sel].min(axis=0), hi[sel].max(axis=0)
+            self.ranges.append((a, b))
+            self.children.append([])
+            center.append(0.5 * (l + h))
+            half.append(0.5 * float((h - l).max()) if b > a else 0.0)
+            return len(self.ranges) - 1
+
+        todo = [add(0, len(E))]
+        while todo:
+            nd = todo.pop()
+            a, b = self.ranges[nd]
+            if b - a <= leaf_cap:
+                continue
+            sel = self.perm[a:b]
+            P = pts[sel]
+            axis = int(np.argmax(P.max(axis=0) - P.min(axis=0)))
+            left = P[:, axis] <= 0.5 * (P[:, axis].max() + P[:, axis].min())
+            if left.all() or not left.any():
+                left = np.zeros(b - a, bool)
+                left[np.argsort(P[:, axis], kind="stable")[:(b - a) // 2]] = True
+            self.perm[a:b] = np.concatenate([sel[left], sel[~left]])
+            mid = a + int(left.sum())
+            kids = [add(a, mid), add(mid, b)]
+            self.children[nd] = kids
+            todo.extend(kids)
+        self.center, self.half = np.asarray(center), np.asarray(half)
+        self.num_nodes = len(self.ranges)
+        self.d = d
+
+    def node_edges(self, nd):
+        a, b = self.ranges[nd]
+        return self.perm[a:b]
+
+    def diam(self, nd):
+        return 2.0 * self.half[nd] * np.sqrt(self.d)
+
+
+def dual_partition(tree, etree, eta):
+    """Far / near pairs between DoF clusters and boundary-edge clusters (cluster.py:230-253)."""
+    far, near = [], []
+    if etree.num_nodes == 0 or len(etree.node_edges(0)) == 0:
+        return far, near
+    todo = [(0, 0)]
+    while todo:
+        a, b = todo.pop()
+        gap = np.abs(tree.center[a] - etree.center[b]) - (tree.half[a] + etree.half[b])
+        dist = float(np.linalg.norm(np.maximum(gap, 0.0)))
+        if eta * dist >= max(tree.diam(a), etree.diam(b)) and dist > 0:
+            far.append((a, b))
+            continue
+        ka, kb = tree.children[a], etree.children[b]
+        if not ka and not kb:
+            near.append((a, b))
+            continue
+        todo.extend([(c, b) for c in ka] if ka and (not kb or tree.half[a] >= etree.half[b]) else
+                    [(a, c) for c in kb])
+    return far, near
+
+
+def _edge_flux(X, p0, p1, nrm, s, d, gl):
+    """edge_flux_potential (assembly.py:303-333) for a few edges, host numpy (near edges only)."""
+    ex = -(d / 2.0 + s)
+    Xf = X.reshape(-1, d)
+    if d == 1:
+        diff = Xf[:, None, :] - p0[None, :, :]
+        return np.sum(np.einsum("xed,ed->xe", diff, nrm) * np.sum(diff ** 2, axis=-1) ** ex, axis=1)
+    gl_x, gl_w = gl
+    Y = p0[:, None, :] + gl_x[None, :, None] * (p1 - p0)[:, None, :]
+    L = np.linalg.norm(p1 - p0, axis=1)
+    diff = Xf[:, None, None, :] - Y[None]
+    r2 = np.sum(diff ** 2, axis=-1)
+    nd = np.einsum("xeqd,ed->xeq", diff, nrm)
+    return np.einsum("xeq,q,e->x", nd * r2 ** ex, gl_w, L, optimize=True)
+
+
+def boundary_flux_at_nodes(mesh, s, tree, cheb, eta, X, cell_leaf):
+    """V(x) = int_dOmega n_out.(x-y)|x-y|^(-d-2s) dy at the cell nodes through the dual (DoF tree x
+    edge tree) partition (cluster.py:525-593).  1D / <= 16 edges: None (the device computes V
+    directly with the same rule)."""
+    from .quadrature import gauss_legendre
+    d = mesh.vertices.shape[1]
+    E = np.asarray(mesh.boundary_edges)
+    if d == 1 or len(E) <= 16:
+        return None
+    nc, q, _ = X.shape
+    etree = EdgeTree(mesh)
+    far, near = dual_partition(tree, etree, eta)
+    gl = gauss_legendre(8)
+    p0, p1 = mesh.vertices[E[:, 0]], mesh.vertices[E[:, 1]]
+    nrm = np.asarray(mesh.boundary_normals)
+    L = np.linalg.norm(p1 - p0, axis=1)
+    Y = p0[:, None, :] + gl[0][None, :, None] * (p1 - p0)[:, None, :]
+    eparent = np.full(etree.num_nodes, -1, np.int64)
+    for nd in range(etree.num_nodes):
+        for c in etree.children[nd]:
+            eparent[c] = nd
+    eorder = [0]
+    for nd in eorder:
+        eorder.extend(etree.children[nd])
+    echeb = _Boxes(etree.center, etree.half, eparent, eorder, d, cheb.m, half_floor=1e-300)
+    emom = np.zeros((etree.num_nodes, cheb.M, d))
+    for nd in range(etree.num_nodes):
+        if etree.children[nd]:
+            continue
+        eids = etree.node_edges(nd)
+        if not len(eids):
+            continue
+        Lb = echeb.eval_basis(nd, Y[eids].reshape(-1, d)).reshape(len(eids), len(gl[0]), -1)
+        base = np.einsum("eqm,q,e->em", Lb, gl[1], L[eids], optimize=True)
+        for j in range(d):
+            emom[nd, :, j] = nrm[eids][:, j] @ base
+    for j in range(d):
+        echeb.push_up(emom[:, :, j])
+    F = np.zeros((tree.num_nodes, cheb.M))
+    ex = -(d / 2.0 + s)
+    for a, b in far:
+        diff = cheb.points[a][:, None, :] - echeb.points[b][None, :, :]
+        kern = np.sum(diff ** 2, axis=-1) ** ex
+        for j in range(d):
+            F[a] += (diff[:, :, j] * kern) @ emom[b, :, j]
+    cheb.push_down(F)
+    V = np.zeros((nc, q))
+    near_map = {}
+    for a, b in near:
+        near_map.setdefault(a, []).append(b)
+    by_leaf = {}
+    for c in range(nc):
+        by_leaf.setdefault(cell_leaf[c], []).append(c)
+    for nd, cs in by_leaf.items():
+        cs = np.asarray(cs)
+        V[cs] = (cheb.eval_basis(nd, X[cs].reshape(-1, d)) @ F[nd]).reshape(len(cs), q)
+        if near_map.get(nd):
+            eids = np.concatenate([etree.node_edges(b) for b in near_map[nd]])
+            if len(eids):
+                V[cs] += _edge_flux(X[cs], p0[eids], p1[eids], nrm[eids], s, d, gl).reshape(len(cs), q)
+    return V
+
+
+def _basis_coefficients(mesh, dofmap, tree, cheb):
+    """int phi_i L_alpha^leaf(i) over supp phi_i by the order m+1 cell rule (cluster.py:719-740)."""
+    from .adapt import cell_nodes
+    from .quadrature import simplex_rule
+    d = mesh.vertices.shape[1]
+    n = int(dofmap.n)
+    out = np.zeros((n, cheb.M))
+    X, W = cell_nodes(mesh, cheb.m + 1)
+    pts, _ = simplex_rule(d, cheb.m + 1)
+    lam = np.stack([1 - pts[:, 0], pts[:, 0]], 1) if d == 1 else \
+        np.stack([1 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1)
+    offs, pdata = mesh.patch_arrays()
+    cd = np.asarray(dofmap.vertex_to_dof)[np.asarray(mesh.cells)]
+    dofs = np.asarray(dofmap.dofs)
+    for nd in tree.leaves:
+        nds = tree.node_dofs(nd)
+        if not len(nds):
+            continue
+        cells = np.unique(np.concatenate([pdata[offs[dofs[i]]:offs[dofs[i] + 1]] for i in nds]))
+        Lb = cheb.eval_basis(nd, X[cells].reshape(-1, d)).reshape(len(cells), -1, cheb.M)
+        mom = np.einsum("cq,qa,cqm->cam", W[cells], lam, Lb, optimize=True)
+        gd = cd[cells]
+        ok = (gd >= 0) & (tree.leaf_of_dof[np.clip(gd, 0, None)] == nd)
+        np.add.at(out, gd[ok], mom[ok])
+    return out
+
+
+def compress(mesh, dofmap, kernel, tree, eta, m, params=None, device=None):
+    """The cluster-compressed stiffness operator (cluster.compress, cluster.py:667-712) with the
+    heavy parts on the GPU: far blocks built on the device from the Chebyshev points, the near
+    field by assemble_near_field (fl_assemble_near_field) with the dual-tree boundary flux V, the
+    matvec / strong form through ClusterOperatorDevice.  Host: Chebyshev data, basis coefficients,
+    the edge-tree boundary flux (as the reference)."""
+    from .assembly import Variant, assemble_near_field
+    from .adapt import cell_leaf_assignment, cell_nodes
+    variant = getattr(getattr(kernel, "variant", Variant.INTEGRAL), "value", "integral")
+    if variant == "symmetrized":
+        raise NotImplementedError("symmetrized kernels are assembled densely")
+    d = mesh.vertices.shape[1]
+    far, near = admissible_partition(tree, eta)
+    cheb = _Boxes(tree.center, tree.half, tree.parent, tree.topo_order, d, m)
+    seen, fp = set(), []
+    for a, b in far:
+        key = (min(a, b), max(a, b))
+        if key not in seen:
+            seen.add(key)
+            fp.append(key)
+    far_pairs = np.asarray(fp, np.int64).reshape(-1, 2)
+    basis_coef = _basis_coefficients(mesh, dofmap, tree, cheb)
+    ns = NearStructure(mesh, dofmap, tree, near)
+    cell_leaf = cell_leaf_assignment(mesh, dofmap, tree.leaf_of_dof)
+    X, _ = cell_nodes(mesh, 6 if d == 1 else 4)
+    V = boundary_flux_at_nodes(mesh, float(kernel.s), tree, cheb, eta, X, cell_leaf)
+    A_near = assemble_near_field(mesh, dofmap, kernel, ns, params, V_nodes=V, device=device)
+    shift = np.zeros((tree.num_nodes, d, m, m))
+    for nd in range(tree.num_nodes):
+        if cheb.shift[nd] is not None:
+            for j in range(d):
+                shift[nd, j] = cheb.shift[nd][j]
+    op = ClusterOperatorDevice.from_arrays(d, m, tree.parent, tree.topo_order, tree.ranges, tree.dof_perm, shift,
+                                           basis_coef, far_pairs, None, cheb.points, kernel.s, kernel.C_ds, A_near,
+                                           A_near.diagonal().copy(), device, tree.center, tree.half,
+                                           ns.near_leaf_map)
+    op.far_pairs, op.basis_coef, op.near, op.cheb, op.tree = far_pairs, basis_coef, A_near, cheb, tree
+    op.meta = {"near_leaf_map": ns.near_leaf_map, "eta": eta}
+    return op
