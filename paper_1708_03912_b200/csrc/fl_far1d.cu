@@ -52,19 +52,20 @@ struct Src1D {
   const double* cstat;          // per 32-cell chunk: CSTAT doubles (chunk_all_k2)
 };
 
-// Per chunk of 32 consecutive cells: x extent (lo, hi), max h, min / max |ln h|, ln(max h).
+// Per chunk of 32 consecutive cells: x extent (lo, hi), max h, min / max |ln h|, ln(max h), min h,
+// ln(min h).
 constexpr int CSTAT = 8;
 
 __global__ void build_src1d_kernel(DevMesh m, Rec1D* rec, double* x0, double* x1, double* lo, double* hi, double* h,
                                    double* lh, int* v0, int* v1, float* lnhf, float* lhf, double* cstat) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;   // blockDim a multiple of 32: warp = chunk
   {
-    double clo = 1e300, chi = -1e300, hmx = 0.0, lmn = 1e300, lmx = 0.0;
+    double clo = 1e300, chi = -1e300, hmx = 0.0, hmn = 1e300, lmn = 1e300, lmx = 0.0;
     if (c < m.nc) {
       const CellGeo& g = m.geo[c];
       clo = fmin(g.p[0][0], g.p[1][0]);
       chi = fmax(g.p[0][0], g.p[1][0]);
-      hmx = g.diam;
+      hmx = hmn = g.diam;
       lmn = lmx = g.ldiam;
     }
 #pragma unroll
@@ -72,12 +73,14 @@ __global__ void build_src1d_kernel(DevMesh m, Rec1D* rec, double* x0, double* x1
       clo = fmin(clo, __shfl_xor_sync(0xffffffffu, clo, o));
       chi = fmax(chi, __shfl_xor_sync(0xffffffffu, chi, o));
       hmx = fmax(hmx, __shfl_xor_sync(0xffffffffu, hmx, o));
+      hmn = fmin(hmn, __shfl_xor_sync(0xffffffffu, hmn, o));
       lmn = fmin(lmn, __shfl_xor_sync(0xffffffffu, lmn, o));
       lmx = fmax(lmx, __shfl_xor_sync(0xffffffffu, lmx, o));
     }
     if ((c & 31) == 0 && c < m.nc) {
       double* cs = cstat + (size_t)CSTAT * (c >> 5);
-      cs[0] = clo; cs[1] = chi; cs[2] = hmx; cs[3] = lmn; cs[4] = lmx; cs[5] = log(hmx); cs[6] = 0.0; cs[7] = 0.0;
+      cs[0] = clo; cs[1] = chi; cs[2] = hmx; cs[3] = lmn; cs[4] = lmx; cs[5] = log(hmx); cs[6] = hmn;
+      cs[7] = log(hmn);
     }
   }
   if (c >= m.nc) return;
@@ -125,6 +128,44 @@ __device__ __forceinline__ bool chunk_all_k2(const OrderConsts& oc, double alo, 
   const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * lD + oc.s * lhmx - oc.coff_tail;
   const double den = fmax(lD - lhmx, 0.0) + oc.ln_rho2;
   return (num > 0.0 ? num / den : 0.0) <= 2.0 - 1e-9;
+}
+
+// The tail order shared by every source of a 32-cell chunk, or 0.  Beside the upper bound of
+// chunk_all_k2, a lower bound of the first branch of the order formula (quadrature.py:159-168):
+// numerator down (|ln h_B| at its chunk maximum in the (s-1) term, ln(dist / h_B) with the farthest
+// gap and the smallest h_B), denominator up (the farthest gap); when ceil() of both bounds (1e-9
+// margins) agree — and so every order between them — the chunk's order is that value.
+__device__ __forceinline__ int chunk_order(const OrderConsts& oc, double alo, double ahi, double alh, double lah,
+                                           const double* __restrict__ cs) {
+  const double D = fmax(cs[0] - ahi, alo - cs[1]);
+  if (!(D > 0.0)) return 0;
+  const double lmn = fmin(alh, cs[3]), lmx = fmax(alh, cs[4]), lhmx = fmax(lah, cs[5]);
+  const double lD = log(D);
+  const double num_u = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * lD + oc.s * lhmx - oc.coff_tail;
+  const double den_l = fmax(lD - lhmx, 0.0) + oc.ln_rho2;
+  const double up = num_u > 0.0 ? num_u / den_l : 0.0;
+  if (up <= 2.0 - 1e-9) return 2;
+  const double Dmax = cs[0] > ahi ? cs[1] - ahi : alo - cs[0];         // farthest gap to the chunk
+  const double lDx = log(Dmax);
+  const double num_l = oc.lead_lnn + oc.sm1 * cs[4] + fmax(alh, cs[3]) - oc.s * lDx + oc.s * cs[7] - oc.coff_tail;
+  if (!(num_l > 0.0)) return 0;
+  const double lo = num_l / (fmax(lDx - lah, 0.0) + oc.ln_rho2);
+  const double kl = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
+  const double ku = fmin(fmax(ceil(up + 1e-9), 2.0), (double)oc.cap_disjoint);
+  return kl == ku ? (int)kl : 0;
+}
+
+// one source of uniform order k on a known side of the target: k nodes x 6 target nodes
+template <int E4, bool RIGHT>
+__device__ __forceinline__ void tail1d_source_side(const double* __restrict__ nd, int k, double ex,
+                                                   const double (&xq)[6], double (&acc)[6], double x0, double e,
+                                                   double J) {
+  for (int r = 0; r < k; ++r) {
+    const double y = x0 + __ldg(nd + r * NODE) * e;
+    const double jw = J * __ldg(nd + r * NODE + 2);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) acc[q] = fma(jw, kpow_pos<E4>(RIGHT ? y - xq[q] : xq[q] - y, ex), acc[q]);
+  }
 }
 
 template <int E4>
@@ -184,11 +225,12 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
   }
   const double* n2 = tab + (size_t)dir.rule(T_DISJ, 2).off * NODE;
   const double t0 = n2[0], w0 = n2[2], t1 = n2[NODE], w1 = n2[NODE + 2];
-  unsigned nodes[NT], umask[NT], rmask[NT];
+  unsigned nodes[NT], rmask[NT];
+  int ck[NT];                                   // per lane: the order of chunk (ci & ~31) + lane
   int qn[NT];                                   // warp-uniform queue lengths
   const int nchunks = (m.nc + 31) >> 5;
 #pragma unroll
-  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; umask[t] = 0; rmask[t] = 0; }
+  for (int t = 0; t < NT; ++t) { nodes[t] = 0; qn[t] = 0; ck[t] = 0; rmask[t] = 0; }
   const unsigned lt = (1u << lane) - 1u;
   const int4* R = reinterpret_cast<const int4*>(S.rec);
   int4 na = make_int4(0, 0, 0, 0), nb = na;     // prefetched record of the next source
@@ -208,15 +250,23 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
       const int cj = ci + lane;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        umask[t] = __ballot_sync(0xffffffffu, cj < nchunks &&
-                                                  chunk_all_k2(oc, alo[t], ahi[t], alh[t], alg[t],
-                                                               S.cstat + (size_t)CSTAT * cj));
+        ck[t] = cj < nchunks ? chunk_order(oc, alo[t], ahi[t], alh[t], alg[t], S.cstat + (size_t)CSTAT * cj) : 0;
         rmask[t] = __ballot_sync(0xffffffffu, cj < nchunks && S.cstat[(size_t)CSTAT * cj] > ahi[t]);
       }
     }
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      if ((umask[t] >> (ci & 31)) & 1u) {       // warp-uniform: the whole chunk is k = 2
+      const int kc = __shfl_sync(0xffffffffu, ck[t], ci & 31);   // warp-uniform chunk order (0: mixed)
+      if (kc > 2) {                             // the whole chunk has order kc: no per-source orders
+        if (s < m.nc) {
+          const double* nd = tab + (size_t)dir.rule(T_DISJ, kc).off * NODE;
+          if ((rmask[t] >> (ci & 31)) & 1u) tail1d_source_side<E4, true>(nd, kc, ex, xq[t], acc[t], sx0, e, J);
+          else tail1d_source_side<E4, false>(nd, kc, ex, xq[t], acc[t], sx0, e, J);
+          nodes[t] += kc;
+        }
+        continue;
+      }
+      if (kc == 2) {                            // warp-uniform: the whole chunk is k = 2
         // the chunk lies on one side of the target (gap > 0): the distance is y - x or x - y,
         // positive, so the kernel power needs no |.| (bitwise the same values)
         if (s < m.nc) {
