@@ -586,9 +586,35 @@ struct SurfConsts {
   const double* glw;
 };
 
+// Powers of the strong form, specialised for s in {1/4, 1/2, 3/4} (SQ = 4s; 0: general pow) with
+// the assembly's seed-corrected kernel powers: gradient term r^(2-d-2s) (1D: of r = |x - y|;
+// 2D: r2^(-s)), flux term |x-y|^(-d-2s) (1D: of r; 2D: r2^(-(1+s))).
+template <int D, int SQ>
+__device__ __forceinline__ double sf_grad(double rr, double p_grad) {
+  if constexpr (SQ == 0) {
+    return D == 1 ? pow(rr, p_grad) : pow(rr, 0.5 * p_grad);
+  } else if constexpr (D == 1) {
+    if constexpr (SQ == 1) return rr * rpow_half<1>(rr);        // r^(1/2)
+    else return rpow_half<1>(rr);                               // s = 3/4: r^(-1/2) (s = 1/2: log case)
+  } else {
+    if constexpr (SQ == 2) return rpow_half<1>(rr);             // r2^(-1/2)
+    else return rpow_quarter<SQ>(rr);                           // r2^(-1/4), r2^(-3/4)
+  }
+}
+template <int D, int SQ>
+__device__ __forceinline__ double sf_flux(double rr, double s) {
+  if constexpr (SQ == 0) {
+    return D == 1 ? pow(rr, -1.0 - 2.0 * s) : pow(rr, -(1.0 + s));
+  } else if constexpr (D == 1) {
+    return rpow_half<2 + SQ>(rr);          // r^(-(1 + 2s)) = r^(-(2 + SQ) / 2)
+  } else {
+    return kpow<8 + 2 * SQ>(rr, 0.0);      // r2^(-(1 + s)) = r2^(-(8 + 2 SQ) / 8)
+  }
+}
+
 // surface terms of cell c at point x: returns (gradient term, flux term) sums over the cell's edges
 // (1D: its two end points), the flux term WITHOUT the u factor when `flux_only` (own cell)
-template <int D>
+template <int D, int SQ>
 __device__ void surf_terms(const CellSurf& c, double x0, double x1, const SurfConsts& K, bool own, double& tg,
                            double& tf) {
   tg = 0.0;
@@ -599,8 +625,8 @@ __device__ void surf_terms(const CellSurf& c, double x0, double x1, const SurfCo
       const double pn = e == 0 ? -sg : sg;
       const double diff = x0 - c.P[e][0], r = fabs(diff);
       const double gp = c.g[0] * pn;
-      tg += K.log_case ? gp * log(1.0 / r) : gp * pow(r, K.p_grad);
-      const double fl = pn * diff * pow(r, -1.0 - 2.0 * K.s);
+      tg += K.log_case ? gp * log(1.0 / r) : gp * sf_grad<D, SQ>(r, K.p_grad);
+      const double fl = pn * diff * sf_flux<D, SQ>(r, K.s);
       tf += own ? fl : c.v[e] * fl;
     }
   } else {
@@ -619,9 +645,9 @@ __device__ void surf_terms(const CellSurf& c, double x0, double x1, const SurfCo
         const double yx = c.P[a][0] + t * tx, yy = c.P[a][1] + t * ty;
         const double dx = x0 - yx, dy = x1 - yy;
         const double r2 = dx * dx + dy * dy;
-        sg += w * (K.log_case ? -0.5 * log(r2) : pow(r2, 0.5 * K.p_grad));
+        sg += w * (K.log_case ? -0.5 * log(r2) : sf_grad<D, SQ>(r2, K.p_grad));
         const double uY = own ? 1.0 : c.v[a] * (1.0 - t) + c.v[b] * t;
-        sf += w * uY * (dx * nx + dy * ny) * pow(r2, K.ex_flux);
+        sf += w * uY * (dx * nx + dy * ny) * sf_flux<D, SQ>(r2, K.s);
       }
       tg += gn * sg * EL;
       tf += sf * EL;
@@ -631,7 +657,7 @@ __device__ void surf_terms(const CellSurf& c, double x0, double x1, const SurfCo
 
 // warp per point: near cells of the owning leaf (lanes; u restricted to the near DoFs, the point's
 // own cell excluded) + the own cell with the full u; out = far + C * contrib
-template <int D>
+template <int D, int SQ>
 __global__ void __launch_bounds__(256) strong_near_kernel(
     DevMesh m, int64_t npts, int q, const double* __restrict__ X, const int64_t* __restrict__ cell_leaf,
     const int64_t* __restrict__ near_off, const int64_t* __restrict__ near_val, const int64_t* __restrict__ ncell_off,
@@ -668,7 +694,7 @@ __global__ void __launch_bounds__(256) strong_near_kernel(
     }
     cell_grad<D>(cs);
     double tg, tf;
-    surf_terms<D>(cs, x0, x1, K, false, tg, tf);
+    surf_terms<D, SQ>(cs, x0, x1, K, false, tg, tf);
     acc += tg / K.cgrad_near - tf / (2.0 * K.s);
   }
   acc = warp_sum(acc);
@@ -683,7 +709,7 @@ __global__ void __launch_bounds__(256) strong_near_kernel(
     }
     cell_grad<D>(cs);
     double tg, tf;
-    surf_terms<D>(cs, x0, x1, K, true, tg, tf);
+    surf_terms<D, SQ>(cs, x0, x1, K, true, tg, tf);
     double ux;                                   // the affine u_c at x (_affine_on_cells, adapt.py:217-233)
     if (D == 1) {
       const double t = (x0 - cs.P[0][0]) / (cs.P[1][0] - cs.P[0][0]);
@@ -730,14 +756,23 @@ int32_t cluster_strong_form(fl_cluster* C, const DevMesh& m, double s, const dou
   K.ngl = ngl;
   K.glx = glx;
   K.glw = glw;
-  if (d == 1)
-    strong_near_kernel<1><<<grid_of(npts * 32), 256, 0, st>>>(m, npts, (int)q, X_dev, cell_leaf, near_off, near_val,
-                                                              ncell_off, ncell_val, C->leaf_of_dof.p, u_dev, K, C->C,
-                                                              far_dev, out_dev);
-  else
-    strong_near_kernel<2><<<grid_of(npts * 32), 256, 0, st>>>(m, npts, (int)q, X_dev, cell_leaf, near_off, near_val,
-                                                              ncell_off, ncell_val, C->leaf_of_dof.p, u_dev, K, C->C,
-                                                              far_dev, out_dev);
+  const int sq = (s == 0.25 || s == 0.5 || s == 0.75) ? (int)std::lround(4.0 * s) : 0;
+#define FL_SF_LAUNCH(DD, SS)                                                                                   \
+  strong_near_kernel<DD, SS><<<grid_of(npts * 32), 256, 0, st>>>(m, npts, (int)q, X_dev, cell_leaf, near_off,   \
+                                                                 near_val, ncell_off, ncell_val,              \
+                                                                 C->leaf_of_dof.p, u_dev, K, C->C, far_dev,   \
+                                                                 out_dev)
+  if (d == 1) {
+    if (sq == 1) FL_SF_LAUNCH(1, 1);
+    else if (sq == 3) FL_SF_LAUNCH(1, 3);
+    else FL_SF_LAUNCH(1, 0);                  // s = 1/2 is the log case in 1D
+  } else {
+    if (sq == 1) FL_SF_LAUNCH(2, 1);
+    else if (sq == 2) FL_SF_LAUNCH(2, 2);
+    else if (sq == 3) FL_SF_LAUNCH(2, 3);
+    else FL_SF_LAUNCH(2, 0);
+  }
+#undef FL_SF_LAUNCH
   note_launch();
   FL_CHECK_LAUNCH();
   return FL_OK;
