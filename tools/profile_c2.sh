@@ -14,7 +14,7 @@ $CMD0 > gpurun_out/plain_f_c2.log 2>&1 && {
       -o gpurun_out/prof_c2tail $CMD0 > gpurun_out/ncu_full_c2tail.log 2>&1
   ncu --set full --clock-control none --import-source on -k regex:"cross1d_tile" -c 1 \
       -o gpurun_out/prof_c2cross $CMD0 > gpurun_out/ncu_full_c2cross.log 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:"matvec_kernel" --launch-skip 1 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:"matvec" --launch-skip 1 -c 1 \
       -o gpurun_out/prof_c2mv $CMD0 > gpurun_out/ncu_full_c2mv.log 2>&1
 }
 ls gpurun_out/*.ncu-rep
