@@ -376,6 +376,40 @@ def main():
         near = {"ms": 1e3 * float(np.median(nts[1:])), "nnz": int(An.nnz), "leaf_cap": 8 if mesh.d == 1 else 16,
                 "eta": 1.0, "near_leaf_pairs": int(len(ns.nl_pairs)), "far_node_pairs": int(len(far_nodes)),
                 "host_tree_partition_s": host_s}
+        # the whole cluster path (compress -> H-matrix matvec -> residual strong form), m = choose_order
+        try:
+            from paper_1708_03912_b200 import adapt as AD
+
+            class _St:
+                pass
+            st_ = _St()
+            st_.h_min, st_.dim = float(mesh.cell_diameters().min()), mesh.d
+            mo = CL.choose_order(st_)
+            t0 = time.perf_counter()
+            cop = CL.compress(mesh, dm, ker, tree, 1.0, mo)
+            comp_s = time.perf_counter() - t0
+            xv = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
+            yv = torch.empty_like(xv)
+            cev = []
+            for i in range(23):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                _lib.check(lib.fl_cluster_matvec(cop.handle, C.c_void_p(xv.data_ptr()), C.c_void_p(yv.data_ptr()),
+                                                 None, 1))
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if i >= 3:
+                    cev.append(e0.elapsed_time(e1))
+            X4, _ = AD.cell_nodes(mesh, 4)
+            AD.strong_form_at(xv.cpu().numpy(), mesh, dm, cop, X=X4)
+            t0 = time.perf_counter()
+            AD.strong_form_at(xv.cpu().numpy(), mesh, dm, cop, X=X4)
+            near["cluster"] = {"cheb_order": mo, "far_pairs": int(len(cop.far_pairs)), "compress_s": comp_s,
+                               "matvec_us": 1e3 * float(np.median(cev)),
+                               "strong_form_ms": 1e3 * (time.perf_counter() - t0)}
+            cop.free()
+        except Exception as exc:     # reported, never fatal for the headline line
+            near["cluster"] = {"error": repr(exc)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
