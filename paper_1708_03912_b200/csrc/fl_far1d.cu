@@ -49,7 +49,7 @@ struct Src1D {
   const double *x0, *x1, *lo, *hi, *h, *lh;
   const int *v0, *v1;
   const float *lnhf, *lhf;      // __logf((float)h), (float)|ln h| for the fp32 order estimate
-  const double* cstat;          // per 32-cell chunk: CSTAT doubles (chunk_all_k2)
+  const double* cstat;          // per 32-cell chunk: CSTAT doubles (chunk_order)
 };
 
 // Per chunk of 32 consecutive cells: x extent (lo, hi), max h, min / max |ln h|, ln(max h), min h,
@@ -113,28 +113,15 @@ static __device__ __noinline__ int order_exact1d(const OrderConsts& oc, double c
 }
 
 // ------------------------------------------------------------------ tail
-// True when every source cell of a 32-cell chunk provably has tail order 2 for the target cell
-// (alo, ahi, h = ah, |ln h| = alh, ln h = lah): the gap D between the target and the chunk's x
-// extent bounds every pair distance from below, so the disjoint order formula with the tail's
-// C_offset - 4 (quadrature.py:159-168, assembly.py:997) is bounded above term by term (numerator
-// up, denominator down); 1e-9 of margin absorbs rounding, so the reference's ceil() clips to 2.
-// D > 0 also excludes K and every cell sharing a vertex with it (N(K), assembly.py:999-1009).
-__device__ __forceinline__ bool chunk_all_k2(const OrderConsts& oc, double alo, double ahi, double alh, double lah,
-                                             const double* __restrict__ cs) {
-  const double D = fmax(cs[0] - ahi, alo - cs[1]);
-  if (!(D > 0.0)) return false;
-  const double lmn = fmin(alh, cs[3]), lmx = fmax(alh, cs[4]), lhmx = fmax(lah, cs[5]);
-  const double lD = log(D);
-  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * lD + oc.s * lhmx - oc.coff_tail;
-  const double den = fmax(lD - lhmx, 0.0) + oc.ln_rho2;
-  return (num > 0.0 ? num / den : 0.0) <= 2.0 - 1e-9;
-}
-
-// The tail order shared by every source of a 32-cell chunk, or 0.  Beside the upper bound of
-// chunk_all_k2, a lower bound of the first branch of the order formula (quadrature.py:159-168):
-// numerator down (|ln h_B| at its chunk maximum in the (s-1) term, ln(dist / h_B) with the farthest
-// gap and the smallest h_B), denominator up (the farthest gap); when ceil() of both bounds (1e-9
-// margins) agree — and so every order between them — the chunk's order is that value.
+// The tail order shared by every source of a 32-cell chunk (target cell alo, ahi, |ln h| = alh,
+// ln h = lah), or 0.  Upper bound: the gap D between the target and the chunk's x extent bounds
+// every pair distance from below, so the disjoint order formula with the tail's C_offset - 4
+// (quadrature.py:159-168, assembly.py:997) is bounded above term by term (numerator up,
+// denominator down).  Lower bound of its first branch: numerator down (|ln h_B| at its chunk
+// maximum in the (s-1) term, ln(dist / h_B) with the farthest gap and the smallest h_B),
+// denominator up (the farthest gap).  When ceil() of both bounds (1e-9 margins) agree — and so
+// every order between them — the chunk's order is that value.  D > 0 also excludes K and every
+// cell sharing a vertex with it (N(K), assembly.py:999-1009).
 __device__ __forceinline__ int chunk_order(const OrderConsts& oc, double alo, double ahi, double alh, double lah,
                                            const double* __restrict__ cs) {
   const double D = fmax(cs[0] - ahi, alo - cs[1]);
