@@ -98,5 +98,35 @@ def launches(path):
         print("| %s | %d | %.1f | %.1f%% |" % (k, c, t, 100 * t / tot))
 
 
+def flops(path):
+    """Executed fp64 FLOPs from the per-instruction SASS counters (2*DFMA + DADD + DMUL, predicated-on
+    thread instructions) and the kernel duration: the ncu-executed figure of SURVEY.md §8(d)."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[1]
+    ip = hdr.index("Predicated-On Thread Instructions Executed")
+    isrc = hdr.index("Source")
+    cnt = collections.Counter()
+    for r in rows[2:]:
+        if len(r) <= ip or not r[ip].isdigit():
+            continue
+        t = r[isrc].split()
+        if not t:
+            continue
+        op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
+        if op in ("DFMA", "DADD", "DMUL"):
+            cnt[op] += int(r[ip])
+    h, u, rr = _raw(path)
+    d = dict(zip(h, rr[0]))
+    t = float(d["gpu__time_duration.sum"].replace(",", ""))
+    t *= {"ms": 1e-3, "msecond": 1e-3, "us": 1e-6, "usecond": 1e-6, "ns": 1e-9, "nsecond": 1e-9}.get(
+        dict(zip(h, u)).get("gpu__time_duration.sum", "ms"), 1e-3)
+    fl = 2 * cnt["DFMA"] + cnt["DADD"] + cnt["DMUL"]
+    name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "")
+    print("| %s | executed fp64 FLOPs (2*DFMA+DADD+DMUL thread instructions) | %.4g |" % (name, fl))
+    print("| %s | executed fp64 TFLOP/s (serialised ncu replay) | %.2f |" % (name, fl / t / 1e12))
+
+
 if __name__ == "__main__":
-    {"report": report, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"report": report, "launches": launches, "flops": flops}[sys.argv[1]](sys.argv[2])
