@@ -73,13 +73,17 @@ __global__ void item_keys_kernel(const BndPair* items, int64_t ni, int* k, int* 
   k[i] = items[i].cell;
   idx[i] = (int)i;
 }
-// offsets of a sorted key array: off[v] = #keys < v, v = 0..nk
+// offsets of a sorted key array: off[v] = #keys < v, v = 0..nk (one binary search per v: no
+// thread walks a long run of empty keys, e.g. the two boundary items of a 1D mesh over nc cells)
 __global__ void offsets_kernel(const int* keys, int m, int nk, int* off) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > m) return;
-  const int prev = (i == 0) ? -1 : keys[i - 1];
-  const int cur = (i == m) ? nk : keys[i];
-  for (int v = prev + 1; v <= cur; ++v) off[v] = i;
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > nk) return;
+  int a = 0, b = m;
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if (keys[mid] < v) a = mid + 1; else b = mid;
+  }
+  off[v] = a;
 }
 
 static void sort_by_key(const int* keys, const int* vals, int* keys_out, int* vals_out, int m, int maxkey,
@@ -103,9 +107,9 @@ void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs
     DBuf<int> k0(np), k1(np), idx(np), k1s(np);
     si.tp_second.alloc(np);
     pair_keys_kernel<<<(np + 255) / 256, 256, 0, st>>>(pairs, np, k0.p, k1.p, idx.p), ::fl::note_launch();
-    offsets_kernel<<<(np + 1 + 255) / 256, 256, 0, st>>>(k0.p, np, nc, si.tp_first_off.p), ::fl::note_launch();  // already sorted by c0
+    offsets_kernel<<<(nc + 1 + 255) / 256, 256, 0, st>>>(k0.p, np, nc, si.tp_first_off.p), ::fl::note_launch();  // already sorted by c0
     sort_by_key(k1.p, idx.p, k1s.p, si.tp_second.p, np, nc, st);                           // stable
-    offsets_kernel<<<(np + 1 + 255) / 256, 256, 0, st>>>(k1s.p, np, nc, si.tp_second_off.p), ::fl::note_launch();
+    offsets_kernel<<<(nc + 1 + 255) / 256, 256, 0, st>>>(k1s.p, np, nc, si.tp_second_off.p), ::fl::note_launch();
   } else {
     si.tp_second.alloc(1);
     FL_CUDA(cudaMemsetAsync(si.tp_first_off.p, 0, (nc + 1) * sizeof(int), st));
@@ -117,7 +121,7 @@ void build_sparse_index(const DevMesh& m, const TouchPair* pairs, int64_t npairs
     si.bp_idx.alloc(ni);
     item_keys_kernel<<<(ni + 255) / 256, 256, 0, st>>>(items, ni, k.p, idx.p), ::fl::note_launch();
     sort_by_key(k.p, idx.p, ks.p, si.bp_idx.p, ni, nc, st);
-    offsets_kernel<<<(ni + 1 + 255) / 256, 256, 0, st>>>(ks.p, ni, nc, si.bp_off.p), ::fl::note_launch();
+    offsets_kernel<<<(nc + 1 + 255) / 256, 256, 0, st>>>(ks.p, ni, nc, si.bp_off.p), ::fl::note_launch();
   } else {
     si.bp_idx.alloc(1);
     FL_CUDA(cudaMemsetAsync(si.bp_off.p, 0, (nc + 1) * sizeof(int), st));

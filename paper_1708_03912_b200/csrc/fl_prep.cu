@@ -97,12 +97,15 @@ __global__ void iota_kernel(int* a, int n) {
   if (i < n) a[i] = i;
 }
 __global__ void patch_offsets_kernel(const int* keys, int m, int nv, int* off) {
-  // off[v] = #entries with key < v: position i starts vertices prev+1 .. cur
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > m) return;
-  const int prev = (i == 0) ? -1 : keys[i - 1];
-  const int cur = (i == m) ? nv : keys[i];
-  for (int v = prev + 1; v <= cur; ++v) off[v] = i;
+  // off[v] = #entries with key < v (binary search per vertex)
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v > nv) return;
+  int a = 0, b = m;
+  while (a < b) {
+    const int mid = (a + b) >> 1;
+    if (keys[mid] < v) a = mid + 1; else b = mid;
+  }
+  off[v] = a;
 }
 __global__ void flat_to_cell_kernel(const int* flat, int m, int dp1, int* cellv) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,7 +138,7 @@ void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf
   FL_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, cells, keys_out.p, idx.p, idx_out.p, m, 0, bits, st));
   off.alloc(nv + 1);
   data.alloc(m);
-  patch_offsets_kernel<<<(m + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p), ::fl::note_launch();
+  patch_offsets_kernel<<<(nv + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p), ::fl::note_launch();
   flat_to_cell_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx_out.p, m, d + 1, data.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
