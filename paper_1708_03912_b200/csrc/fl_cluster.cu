@@ -12,6 +12,7 @@
 // results are deterministic; the near CSR product is a warp-per-row fixed-order reduction.
 // The far blocks B_p = |xi_a - xi_b|^(2 ex) at the Chebyshev points (compress, :683-694) are
 // either uploaded or built here (one thread per block entry).
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -837,6 +838,16 @@ int32_t fl_cluster_strong_form(fl_cluster* C, const fl_mesh* mesh, const fl_dofm
   const int64_t nv = mesh->nv, nc = mesh->nc, nn = C->nn;
   for (int64_t c = 0; c < nc; ++c)
     if (cell_leaf[c] < 0 || cell_leaf[c] >= nn) return fl::api_fail(FL_E_ARG, "cell leaf out of range");
+  if (near_off[0] != 0 || ncell_off[0] != 0) return fl::api_fail(FL_E_ARG, "near lists must start at 0");
+  for (int64_t k = 0; k < nn; ++k)
+    if (near_off[k + 1] < near_off[k] || ncell_off[k + 1] < ncell_off[k])
+      return fl::api_fail(FL_E_ARG, "near list offsets must be non-decreasing");
+  for (int64_t e = 0; e < near_off[nn]; ++e)
+    if (near_val[e] < 0 || near_val[e] >= nn || (e > 0 && near_val[e] < near_val[e - 1] &&
+                                                 !std::binary_search(near_off, near_off + nn + 1, e)))
+      return fl::api_fail(FL_E_ARG, "near leaves must be node ids, ascending per node");
+  for (int64_t e = 0; e < ncell_off[nn]; ++e)
+    if (ncell_val[e] < 0 || ncell_val[e] >= nc) return fl::api_fail(FL_E_ARG, "near cell out of range");
   FL_CUDA(cudaSetDevice(C->device));
   cudaStream_t st = C->stream;
   fl::StreamScope scope(st);
