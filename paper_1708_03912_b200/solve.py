@@ -59,9 +59,12 @@ def pcg(op, b, precond="jacobi", tol=1e-8, max_iter=None, x0=None, record_lanczo
     if isinstance(op, np.ndarray):
         with DenseDeviceOperator.from_host(op) as dev:      # Ad @ x of solve.py:31-32, on the GPU
             return pcg(dev, b, precond, tol, max_iter, x0)
+    from .cluster import ClusterOperatorDevice
+    if isinstance(op, ClusterOperatorDevice):
+        return _pcg_cluster(op, b, precond, tol, max_iter)
     if not isinstance(op, DenseDeviceOperator):
-        raise TypeError("pcg expects a DenseDeviceOperator (assemble_dense_device) or a dense "
-                        "ndarray; host operators are not on the device path")
+        raise TypeError("pcg expects a DenseDeviceOperator (assemble_dense_device), a "
+                        "ClusterOperatorDevice or a dense ndarray; host operators are not on the device path")
     if not op.full:
         raise ValueError("a row-block operator needs distributed.pcg_sharded")
     b = np.ascontiguousarray(b, dtype=np.float64)
@@ -84,3 +87,55 @@ def pcg(op, b, precond="jacobi", tol=1e-8, max_iter=None, x0=None, record_lanczo
                                   float(tol), int(max_iter), pc, x.ctypes.data, C.byref(rep)))
     return x, SolveReport(int(rep.iterations), float(rep.residual), time.perf_counter() - t0,
                           bool(rep.converged), true_residual=float(rep.true_residual))
+
+
+class _OneRank:
+    """torch.distributed stand-in for a single process (pcg_sharded's exchange steps are identities)."""
+
+    class ReduceOp:
+        MAX = SUM = None
+
+    @staticmethod
+    def get_rank(group=None):
+        return 0
+
+    @staticmethod
+    def get_world_size(group=None):
+        return 1
+
+    @staticmethod
+    def all_reduce(t, op=None, group=None):
+        return None
+
+    @staticmethod
+    def all_gather_into_tensor(out, inp, group=None):
+        out.copy_(inp)
+
+
+def _pcg_cluster(op, b, precond, tol, max_iter):
+    """The same Jacobi PCG (solve.py:52-109) on a ClusterOperatorDevice: device vectors, the fused
+    CG kernels of libfraclap_b200 and the H-matrix matvec (fl_cluster_matvec on device pointers)."""
+    import torch
+    from .distributed import TorchDeviceBackend, pcg_sharded
+
+    class _Backend(TorchDeviceBackend):
+        def __init__(self, cop):
+            super().__init__(None, torch.cuda.current_stream().cuda_stream)
+            self.cop = cop
+
+        def matvec(self, p_full, out_local):
+            torch.cuda.current_stream().synchronize()      # the operator runs on its own stream
+            _lib.check(self.lib.fl_cluster_matvec(self.cop.handle, C.c_void_p(p_full.data_ptr()),
+                                                  C.c_void_p(out_local.data_ptr()), None, 1))
+
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n = len(b)
+    if n != op.n:
+        raise ValueError("b has length %d, operator is %d x %d" % (n, op.n, op.n))
+    if precond not in ("jacobi", None, "none"):
+        raise ValueError("precond must be 'jacobi' or None on the device path")
+    t0 = time.perf_counter()
+    x, rep = pcg_sharded(_Backend(op), b, op.diag(), [(0, n)], n, _OneRank, tol=tol, max_iter=max_iter,
+                         precond="jacobi" if precond == "jacobi" else None)
+    return x.cpu().numpy(), SolveReport(int(rep["iterations"]), float(rep.get("residual", float("nan"))),
+                                        time.perf_counter() - t0, bool(rep["converged"]))
