@@ -404,9 +404,14 @@ def main():
             AD.strong_form_at(xv.cpu().numpy(), mesh, dm, cop, X=X4)
             t0 = time.perf_counter()
             AD.strong_form_at(xv.cpu().numpy(), mesh, dm, cop, X=X4)
+            sf_ms = 1e3 * (time.perf_counter() - t0)
+            bc = A.load_vector(mesh, dm, 1.0)
+            t0 = time.perf_counter()
+            _, crep = S.pcg(cop, bc, tol=1e-10, max_iter=10 ** 5)
+            cg_s = time.perf_counter() - t0
             near["cluster"] = {"cheb_order": mo, "far_pairs": int(len(cop.far_pairs)), "compress_s": comp_s,
-                               "matvec_us": 1e3 * float(np.median(cev)),
-                               "strong_form_ms": 1e3 * (time.perf_counter() - t0)}
+                               "matvec_us": 1e3 * float(np.median(cev)), "strong_form_ms": sf_ms,
+                               "cg_iterations": crep.iterations, "cg_ms_per_iteration": 1e3 * cg_s / max(crep.iterations, 1)}
             cop.free()
         except Exception as exc:     # reported, never fatal for the headline line
             near["cluster"] = {"error": repr(exc)[:200]}
