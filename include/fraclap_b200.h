@@ -249,6 +249,10 @@ int32_t fl_cluster_strong_form(fl_cluster* C, const fl_mesh* mesh, const fl_dofm
                                const int64_t* near_off, const int64_t* near_val, const int64_t* ncell_off,
                                const int64_t* ncell_val, const double* gl_x, const double* gl_w, int64_t ngl,
                                double* out, double* far_out);
+/* The far field of u at arbitrary points (ClusterOperator.evaluate_far_field_at_points,
+ * cluster.py:469-485): -C * sum L_alpha^owner(x) F[owner], owner = the leaf node of each point. */
+int32_t fl_cluster_far_at_points(fl_cluster* C, const double* u, int64_t npts, const double* points,
+                                 const int64_t* owner, double* out);
 /* the device far blocks (npairs, M, M) */
 int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out);
 void fl_cluster_free(fl_cluster* C);

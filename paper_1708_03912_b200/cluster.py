@@ -270,6 +270,37 @@ class ClusterOperatorDevice:
     def diag(self):
         return self._diag
 
+    def evaluate_far_field_at_points(self, u, points, owner_leaves):
+        """-C * int k(x, y) u_far(y) dy at points (cluster.py:469-485); owner_leaves = the leaf node
+        owning each point."""
+        from . import _lib
+        pts = np.ascontiguousarray(np.asarray(points, float).reshape(-1, self.d))
+        own = np.ascontiguousarray(owner_leaves, dtype=np.int64).reshape(-1)
+        if len(own) != len(pts):
+            raise ValueError("one owner leaf per point")
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.empty(len(pts))
+        _lib.check(_lib.load().fl_cluster_far_at_points(self.handle, u.ctypes.data, len(pts), pts.ctypes.data,
+                                                        own.ctypes.data, out.ctypes.data))
+        return out
+
+    def near_dof_leaves(self):
+        """Leaf node -> its near leaf nodes (ClusterOperator.near_dof_leaves, cluster.py:487-489)."""
+        if self.tree_info is None:
+            raise ValueError("built without tree information")
+        return self.tree_info["near_leaf_map"]
+
+    def to_dense(self):
+        """The operator as a dense (n, n) array (ClusterOperator.to_dense, cluster.py:460-467): the
+        device matvec of every unit vector."""
+        A = np.empty((self.n, self.n))
+        e = np.zeros(self.n)
+        for j in range(self.n):
+            e[j] = 1.0
+            A[:, j] = self.matvec(e)
+            e[j] = 0.0
+        return A
+
     def far_blocks(self, npairs):
         from . import _lib
         out = np.empty((int(npairs), self.M, self.M))

@@ -730,6 +730,20 @@ __global__ void __launch_bounds__(256) strong_near_kernel(
 
 }  // namespace
 
+// -C * L(x) . F[owner(x)] at arbitrary points (owner = the leaf node per point)
+void cluster_far_points(fl_cluster* C, const double* u_dev, int64_t npts, const double* X_dev,
+                        const int64_t* owner_dev, double* out_dev, cudaStream_t st) {
+  far_potentials(C, u_dev, st);
+  if (C->d == 1)
+    far_points_kernel<1><<<grid_of(npts), 256, 0, st>>>(npts, 1, X_dev, owner_dev, C->center.p, C->half.p, C->ref.p,
+                                                        C->m, C->M, C->F.p, -C->C, out_dev);
+  else
+    far_points_kernel<2><<<grid_of(npts), 256, 0, st>>>(npts, 1, X_dev, owner_dev, C->center.p, C->half.p, C->ref.p,
+                                                        C->m, C->M, C->F.p, -C->C, out_dev);
+  note_launch();
+  FL_CHECK_LAUNCH();
+}
+
 int32_t cluster_strong_form(fl_cluster* C, const DevMesh& m, double s, const double* u_dev, int64_t q,
                             const double* X_dev, const int64_t* cell_leaf, const int64_t* near_off,
                             const int64_t* near_val, const int64_t* ncell_off, const int64_t* ncell_val,
@@ -886,6 +900,30 @@ int32_t fl_cluster_strong_form(fl_cluster* C, const fl_mesh* mesh, const fl_dofm
                           (int)ngl, dout.p, dfar.p, st);
   FL_CUDA(cudaMemcpyAsync(out, dout.p, (size_t)nc * q * 8, cudaMemcpyDeviceToHost, st));
   if (far_out) FL_CUDA(cudaMemcpyAsync(far_out, dfar.p, (size_t)nc * q * 8, cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  return FL_OK;
+  FL_CATCH
+}
+
+int32_t fl_cluster_far_at_points(fl_cluster* C, const double* u, int64_t npts, const double* points,
+                                 const int64_t* owner, double* out) {
+  FL_TRY
+  if (!C || !u || (npts > 0 && (!points || !owner || !out))) return fl::api_fail(FL_E_ARG, "null argument");
+  if (!C->center.p || !C->ref.p) return fl::api_fail(FL_E_ARG, "cluster: the operator has no node boxes");
+  if (C->m > 16) return fl::api_fail(FL_E_ARG, "cluster: Chebyshev order above 16");
+  for (int64_t p = 0; p < npts; ++p)
+    if (owner[p] < 0 || owner[p] >= C->nn) return fl::api_fail(FL_E_ARG, "owner node out of range");
+  FL_CUDA(cudaSetDevice(C->device));
+  cudaStream_t st = C->stream;
+  fl::StreamScope scope(st);
+  if (npts == 0) return FL_OK;
+  fl::DBuf<double> du(std::max<int64_t>(C->n, 1)), dX((size_t)npts * C->d), dout(npts);
+  fl::DBuf<int64_t> down(npts);
+  if (C->n) FL_CUDA(cudaMemcpyAsync(du.p, u, C->n * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dX.p, points, (size_t)npts * C->d * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(down.p, owner, npts * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  fl::cluster_far_points(C, du.p, npts, dX.p, down.p, dout.p, st);
+  FL_CUDA(cudaMemcpyAsync(out, dout.p, npts * sizeof(double), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   return FL_OK;
   FL_CATCH

@@ -314,6 +314,8 @@ struct fl_cluster_desc;
 namespace fl {
 int32_t cluster_create(const ::fl_cluster_desc* D, int device, ::fl_cluster** out);
 int32_t cluster_matvec_dev(::fl_cluster* C, const double* x, double* y, double* yfar, cudaStream_t st);
+void cluster_far_points(::fl_cluster* C, const double* u_dev, int64_t npts, const double* X_dev,
+                        const int64_t* owner_dev, double* out_dev, cudaStream_t st);
 // sets fl_last_error() and returns code (fl_capi.cu)
 int32_t api_fail(int code, const char* msg);
 
