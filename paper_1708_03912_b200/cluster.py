@@ -284,6 +284,20 @@ class ClusterOperatorDevice:
                                                         own.ctypes.data, out.ctypes.data))
         return out
 
+    def memory_entries(self):
+        """Stored entries: near nnz + far block entries (cluster.py:402-403)."""
+        near = getattr(self, "near", None)
+        npairs = len(getattr(self, "far_pairs", ()))
+        return (near.nnz if near is not None else 0) + npairs * self.M * self.M
+
+    def block_stats(self):
+        """cluster.py:405-413."""
+        near = getattr(self, "near", None)
+        cheb = getattr(self, "cheb", None)
+        return {"n": self.n, "near_nnz": int(near.nnz) if near is not None else 0,
+                "far_blocks": int(len(getattr(self, "far_pairs", ()))), "block_size": int(self.M ** 2),
+                "memory_entries": int(self.memory_entries()), "cheb_order": int(cheb.m) if cheb is not None else 0}
+
     def near_dof_leaves(self):
         """Leaf node -> its near leaf nodes (ClusterOperator.near_dof_leaves, cluster.py:487-489)."""
         if self.tree_info is None:
@@ -629,3 +643,13 @@ def compress(mesh, dofmap, kernel, tree, eta, m, params=None, device=None):
     op.far_pairs, op.basis_coef, op.near, op.cheb, op.tree = far_pairs, basis_coef, A_near, cheb, tree
     op.meta = {"near_leaf_map": ns.near_leaf_map, "eta": eta}
     return op
+
+
+def matvec(op, x):
+    """cluster.py:814-815."""
+    return op.matvec(x)
+
+
+def evaluate_far_field_at_points(op, u, points, owner_leaves):
+    """cluster.py:818-819."""
+    return op.evaluate_far_field_at_points(u, points, owner_leaves)
