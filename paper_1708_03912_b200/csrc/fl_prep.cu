@@ -96,22 +96,6 @@ __global__ void iota_kernel(int* a, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
 }
-__global__ void patch_offsets_kernel(const int* keys, int m, int nv, int* off) {
-  // off[v] = #entries with key < v (binary search per vertex)
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v > nv) return;
-  int a = 0, b = m;
-  while (a < b) {
-    const int mid = (a + b) >> 1;
-    if (keys[mid] < v) a = mid + 1; else b = mid;
-  }
-  off[v] = a;
-}
-__global__ void flat_to_cell_kernel(const int* flat, int m, int dp1, int* cellv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) cellv[i] = flat[i] / dp1;
-}
-
 // mesh.py:114-125: argsort(cells.ravel(), kind="stable") -> per vertex, ascending cell ids.
 __global__ void max_valence_kernel(const int* off, int nv, int* mx) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -125,21 +109,47 @@ void launch_max_valence(const int* off, int nv, int* mx, cudaStream_t st) {
   FL_CHECK_LAUNCH();
 }
 
+// vertex -> cells CSR by counting (valences are small): counts, one scan, a fill by atomic slot
+// claims, then each vertex's few cells sorted ascending — the order of
+// argsort(cells.ravel(), kind="stable") (mesh.py:114-125) without a device-wide radix sort
+__global__ void patch_count_kernel(const int* __restrict__ cells, int m, int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) atomicAdd(&cnt[cells[i]], 1);
+}
+__global__ void patch_fill_kernel(const int* __restrict__ cells, int m, int dp1, const int* __restrict__ off,
+                                  int* __restrict__ cursor, int* __restrict__ data) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int v = cells[i];
+  data[off[v] + atomicAdd(&cursor[v], 1)] = i / dp1;
+}
+__global__ void patch_sort_kernel(const int* __restrict__ off, int nv, int* __restrict__ data) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int a = off[v], b = off[v + 1];
+  for (int i = a + 1; i < b; ++i) {
+    const int x = data[i];
+    int j = i - 1;
+    while (j >= a && data[j] > x) { data[j + 1] = data[j]; --j; }
+    data[j + 1] = x;
+  }
+}
+
 void build_patches(int nv, int nc, int d, const int* cells, DBuf<int>& off, DBuf<int>& data,
                    cudaStream_t st) {
   const int m = nc * (d + 1);
-  DBuf<int> idx(m), keys_out(m), idx_out(m);
-  iota_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx.p, m), ::fl::note_launch();
-  size_t tmp = 0;
-  int bits = 1;
-  while ((1 << bits) < nv + 1) ++bits;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, cells, keys_out.p, idx.p, idx_out.p, m, 0, bits, st);
-  DBuf<unsigned char> t(tmp);
-  FL_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, cells, keys_out.p, idx.p, idx_out.p, m, 0, bits, st));
+  DBuf<int> cnt(nv + 1), cursor(nv);
   off.alloc(nv + 1);
   data.alloc(m);
-  patch_offsets_kernel<<<(nv + 1 + 255) / 256, 256, 0, st>>>(keys_out.p, m, nv, off.p), ::fl::note_launch();
-  flat_to_cell_kernel<<<(m + 255) / 256, 256, 0, st>>>(idx_out.p, m, d + 1, data.p), ::fl::note_launch();
+  FL_CUDA(cudaMemsetAsync(cnt.p, 0, (nv + 1) * sizeof(int), st));
+  FL_CUDA(cudaMemsetAsync(cursor.p, 0, nv * sizeof(int), st));
+  patch_count_kernel<<<(m + 255) / 256, 256, 0, st>>>(cells, m, cnt.p), ::fl::note_launch();
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.p, off.p, nv + 1, st);
+  DBuf<unsigned char> t(tmp);
+  FL_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tmp, cnt.p, off.p, nv + 1, st));
+  patch_fill_kernel<<<(m + 255) / 256, 256, 0, st>>>(cells, m, d + 1, off.p, cursor.p, data.p), ::fl::note_launch();
+  patch_sort_kernel<<<(nv + 255) / 256, 256, 0, st>>>(off.p, nv, data.p), ::fl::note_launch();
   FL_CHECK_LAUNCH();
 }
 
