@@ -306,6 +306,26 @@ __global__ void flag_target_cells(DevMesh m, int r0, int r1, int* flags) {
   }
   flags[c] = f;
 }
+// every cell into the target list of each row band holding one of its vertex DoFs (cut: band starts)
+__global__ void band_targets_kernel(DevMesh m, const int* __restrict__ cut, int nbands, int* __restrict__ lists,
+                                    int* __restrict__ cnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m.nc) return;
+  int seen[3] = {-1, -1, -1};
+  for (int i = 0; i <= m.d; ++i) {
+    const int dof = m.v2d[m.cells[c * (m.d + 1) + i]];
+    if (dof < 0) continue;
+    int a = 0, b = nbands;                       // the band of dof: cut[band] <= dof < cut[band + 1]
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      if (cut[mid] <= dof) a = mid; else b = mid;
+    }
+    bool dup = false;
+    for (int j = 0; j < i; ++j) dup |= seen[j] == a;
+    seen[i] = a;
+    if (!dup) lists[(size_t)a * m.nc + atomicAdd(&cnt[a], 1)] = c;
+  }
+}
 __global__ void iota2(int* a, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
@@ -468,16 +488,16 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
                                      (int)row_end, st));
   // banded: the target cells of every band (cells with a vertex DoF in the band), counts read
   // back with the other sizes
-  std::vector<DBuf<int>> btgt(nbands);
-  DBuf<int> bcnt(std::max(nbands, 1));
-  for (int b = 0; b < nbands; ++b) {
-    btgt[b].alloc(m.nc);
-    flag_target_cells<<<(m.nc + 255) / 256, 256, 0, st>>>(m, cut[b], cut[b + 1], flags.p), ::fl::note_launch();
-    size_t tmp = 0;
-    cub::DeviceSelect::Flagged(nullptr, tmp, all.p, flags.p, btgt[b].p, bcnt.p + b, m.nc, st);
-    DBuf<unsigned char> tb(tmp);
-    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, all.p, flags.p, btgt[b].p, bcnt.p + b, m.nc, st));
+  // (one pass, atomic appends: the per-target results do not depend on the list order)
+  DBuf<int> btgt_all((size_t)std::max(nbands, 1) * m.nc), bcnt(std::max(nbands, 1)), dcut(nbands + 1);
+  std::vector<const int*> btgt(nbands);
+  if (nbands) {
+    FL_CUDA(cudaMemsetAsync(bcnt.p, 0, nbands * sizeof(int), st));
+    FL_CUDA(cudaMemcpyAsync(dcut.p, cut.data(), (nbands + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    band_targets_kernel<<<(m.nc + 255) / 256, 256, 0, st>>>(m, dcut.p, nbands, btgt_all.p, bcnt.p),
+        ::fl::note_launch();
     FL_CHECK_LAUNCH();
+    for (int b = 0; b < nbands; ++b) btgt[b] = btgt_all.p + (size_t)b * m.nc;
   }
   touching_count(m, tcounts, toffs, st);
   if (do_bnd) boundary_count(m, bcounts, boffs, st);
@@ -522,7 +542,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     FL_CUDA(cudaEventRecord(tstream.e[0], st));
     FL_CUDA(cudaStreamWaitEvent(tstream.s, tstream.e[0], 0));
     FL_CUDA(cudaEventRecord(tstream.e[1], tstream.s));
-    launch_tail1d(m, U.t, oc, ex, e4, P1.get(), btgt[0].p, bcnt.p, m.nc, psi.p, evc.p, tstream.s);
+    launch_tail1d(m, U.t, oc, ex, e4, P1.get(), btgt[0], bcnt.p, m.nc, psi.p, evc.p, tstream.s);
     FL_CUDA(cudaEventRecord(tstream.e[2], tstream.s));
   }
   if (early_tail) {
@@ -635,8 +655,8 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     for (int b = 0; b < nbands; ++b) {
       const int nt_b = hs[16 + b];
       if (b == 0) FL_CUDA(cudaStreamWaitEvent(st, tstream.e[2], 0));     // launched before the size sync
-      else launch_tail1d(m, U.t, oc, ex, e4, P1.get(), btgt[b].p, bcnt.p + b, nt_b, psi.p, evc.p, st);
-      launch_cell_local(m, U.t, C, s, integral && m.nb > 0, btgt[b].p, nt_b, ident.p, psi.p, win.p, Lc.p, st);
+      else launch_tail1d(m, U.t, oc, ex, e4, P1.get(), btgt[b], bcnt.p + b, nt_b, psi.p, evc.p, st);
+      launch_cell_local(m, U.t, C, s, integral && m.nb > 0, btgt[b], nt_b, ident.p, psi.p, win.p, Lc.p, st);
       launch_cross1d(m, U.t, oc, ex, e4, C, P1.get(), maxcells1d, targets.p, ntargets, row_vertex.p, D->A.p, D->lda,
                      evc.p + 1, st, cut[b], cut[b + 1]);
       if (b == 0) FL_CUDA(cudaStreamWaitEvent(st, ev_si, 0));
