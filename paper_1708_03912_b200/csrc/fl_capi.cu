@@ -473,7 +473,8 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   std::vector<int> cut;
   if (nbands) {
     const int T = cross1d_tile_dofs();
-    const int first = std::min<int>((int)n, 16 * T);
+    static const int first_tiles = [] { const char* v = getenv("FRACLAP_BAND0_TILES"); return v ? std::max(1, atoi(v)) : 16; }();
+    const int first = std::min<int>((int)n, first_tiles * T);
     const int rest = (int)((n - first + nbands - 2) / (nbands - 1));
     const int blk = std::max(T, (rest + T - 1) / T * T);
     cut.push_back(0);
