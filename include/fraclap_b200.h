@@ -256,6 +256,14 @@ int32_t fl_cluster_far_at_points(fl_cluster* C, const double* u, int64_t npts, c
 /* the device far blocks (npairs, M, M) */
 int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out);
 void fl_cluster_free(fl_cluster* C);
+/* Near part of the dual-tree boundary flux at the cell nodes (boundary_flux_at_nodes,
+ * cluster.py:586-592; 2D): out[p] = sum over the edges eid[eoff[g]:eoff[g+1]] of the point's group g
+ * (poff[g] <= p < poff[g+1]) of edge_flux_potential (assembly.py:303-333) with the rule (gl_x, gl_w)
+ * on [0, 1].  X: (npts, 2) grouped by DoF leaf; p0, p1, normals: (nb, 2) boundary edges. */
+int32_t fl_boundary_flux_near(int32_t device, double s, int64_t npts, const double* X, int64_t ngroups,
+                              const int64_t* poff, const int64_t* eoff, const int64_t* eid, int64_t nb,
+                              const double* p0, const double* p1, const double* normals, const double* gl_x,
+                              const double* gl_w, int64_t ngl, double* out);
 
 /* ------------------------------------------------------------- driver steps (host O(n) in the
  * reference), on the device

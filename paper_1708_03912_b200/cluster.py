@@ -11,6 +11,8 @@ NearStructure) is accepted by assemble_near_field (duck typing, like the referen
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 
@@ -111,17 +113,32 @@ def admissible_partition(tree: ClusterTree, eta: float):
     if eta <= 0:
         raise ValueError("eta must be positive")
     far, near = [], []
+    # scalar fast path: the gap is the reference's elementwise float64 arithmetic; only the norm
+    # may differ from np.linalg.norm in the last ulp, so near-ties re-check with tree.dist
+    cen = [tuple(float(v) for v in row) for row in np.asarray(tree.center).reshape(tree.num_nodes, -1)]
+    half = [float(v) for v in tree.half]
+    diam = [float(tree.diam(nd)) for nd in range(tree.num_nodes)]
     todo = [(0, 0)]
     while todo:
         a, b = todo.pop()
-        if a != b and eta * tree.dist(a, b) >= max(tree.diam(a), tree.diam(b)):
-            far.append((a, b))
-            continue
+        if a != b:
+            hab = half[a] + half[b]
+            d2 = 0.0
+            for ca, cb in zip(cen[a], cen[b]):
+                g = abs(ca - cb) - hab
+                if g > 0.0:
+                    d2 += g * g
+            lhs, rhs = eta * math.sqrt(d2), max(diam[a], diam[b])
+            if abs(lhs - rhs) <= 1e-12 * rhs:
+                lhs = eta * tree.dist(a, b)
+            if lhs >= rhs:
+                far.append((a, b))
+                continue
         ka, kb = tree.children[a], tree.children[b]
         if not ka and not kb:
             near.append((a, b))
             continue
-        ha, hb = tree.half[a], tree.half[b]
+        ha, hb = half[a], half[b]
         split_a = bool(ka) and (not kb or ha > hb * (1 + 1e-12) or (abs(ha - hb) <= 1e-12 * ha and a <= b))
         todo.extend([(c, b) for c in ka] if split_a else [(a, c) for c in kb])
     return far, near
@@ -190,7 +207,7 @@ class ClusterOperatorDevice:
         ClusterOperator.near_dof_leaves) enable adapt.strong_form_at on this operator."""
         import ctypes as C
         from scipy.sparse import csr_matrix
-        from . import _lib
+        from . import _lib  # noqa: F811
         i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)           # noqa: E731
         f64 = lambda a: np.ascontiguousarray(a, dtype=np.float64)         # noqa: E731
         near = csr_matrix(near)
@@ -248,7 +265,7 @@ class ClusterOperatorDevice:
 
     # ------------------------------------------------------------ contract
     def _apply(self, x, want_far=False):
-        from . import _lib
+        from . import _lib  # noqa: F811
         x = np.ascontiguousarray(x, dtype=np.float64)
         if x.shape != (self.n,):
             raise ValueError("dimension mismatch")
@@ -273,7 +290,7 @@ class ClusterOperatorDevice:
     def evaluate_far_field_at_points(self, u, points, owner_leaves):
         """-C * int k(x, y) u_far(y) dy at points (cluster.py:469-485); owner_leaves = the leaf node
         owning each point."""
-        from . import _lib
+        from . import _lib  # noqa: F811
         pts = np.ascontiguousarray(np.asarray(points, float).reshape(-1, self.d))
         own = np.ascontiguousarray(owner_leaves, dtype=np.int64).reshape(-1)
         if len(own) != len(pts):
@@ -316,7 +333,7 @@ class ClusterOperatorDevice:
         return A
 
     def far_blocks(self, npairs):
-        from . import _lib
+        from . import _lib  # noqa: F811
         out = np.empty((int(npairs), self.M, self.M))
         _lib.check(_lib.load().fl_cluster_far_blocks(self.handle, out.ctypes.data))
         return out
@@ -498,26 +515,11 @@ def dual_partition(tree, etree, eta):
     return far, near
 
 
-def _edge_flux(X, p0, p1, nrm, s, d, gl):
-    """edge_flux_potential (assembly.py:303-333) for a few edges, host numpy (near edges only)."""
-    ex = -(d / 2.0 + s)
-    Xf = X.reshape(-1, d)
-    if d == 1:
-        diff = Xf[:, None, :] - p0[None, :, :]
-        return np.sum(np.einsum("xed,ed->xe", diff, nrm) * np.sum(diff ** 2, axis=-1) ** ex, axis=1)
-    gl_x, gl_w = gl
-    Y = p0[:, None, :] + gl_x[None, :, None] * (p1 - p0)[:, None, :]
-    L = np.linalg.norm(p1 - p0, axis=1)
-    diff = Xf[:, None, None, :] - Y[None]
-    r2 = np.sum(diff ** 2, axis=-1)
-    nd = np.einsum("xeqd,ed->xeq", diff, nrm)
-    return np.einsum("xeq,q,e->x", nd * r2 ** ex, gl_w, L, optimize=True)
-
-
-def boundary_flux_at_nodes(mesh, s, tree, cheb, eta, X, cell_leaf):
+def boundary_flux_at_nodes(mesh, s, tree, cheb, eta, X, cell_leaf, device=None):
     """V(x) = int_dOmega n_out.(x-y)|x-y|^(-d-2s) dy at the cell nodes through the dual (DoF tree x
     edge tree) partition (cluster.py:525-593).  1D / <= 16 edges: None (the device computes V
-    directly with the same rule)."""
+    directly with the same rule).  The edge-tree moments and far pairs are host numpy; the direct
+    near-edge sums (:586-592) run on the device (fl_boundary_flux_near)."""
     from .quadrature import gauss_legendre
     d = mesh.vertices.shape[1]
     E = np.asarray(mesh.boundary_edges)
@@ -567,13 +569,33 @@ def boundary_flux_at_nodes(mesh, s, tree, cheb, eta, X, cell_leaf):
     by_leaf = {}
     for c in range(nc):
         by_leaf.setdefault(cell_leaf[c], []).append(c)
+    groups, poff, eoff, eid = [], [0], [0], []
     for nd, cs in by_leaf.items():
         cs = np.asarray(cs)
         V[cs] = (cheb.eval_basis(nd, X[cs].reshape(-1, d)) @ F[nd]).reshape(len(cs), q)
         if near_map.get(nd):
             eids = np.concatenate([etree.node_edges(b) for b in near_map[nd]])
             if len(eids):
-                V[cs] += _edge_flux(X[cs], p0[eids], p1[eids], nrm[eids], s, d, gl).reshape(len(cs), q)
+                groups.append(cs)
+                poff.append(poff[-1] + len(cs) * q)
+                eid.append(eids)
+                eoff.append(eoff[-1] + len(eids))
+    if groups:
+        # the near edges of every leaf in one device launch (fl_boundary_flux_near)
+        from . import _lib
+        from .assembly import _device_index
+        cells = np.concatenate(groups)
+        P = np.ascontiguousarray(X[cells].reshape(-1, d), dtype=np.float64)
+        poff, eoff = np.asarray(poff, np.int64), np.asarray(eoff, np.int64)
+        eid = np.ascontiguousarray(np.concatenate(eid), dtype=np.int64)
+        p0c, p1c, nrmc = (np.ascontiguousarray(a, dtype=np.float64) for a in (p0, p1, nrm))
+        gx, gw = (np.ascontiguousarray(a, dtype=np.float64) for a in gl)
+        out = np.empty(len(P))
+        _lib.check(_lib.load().fl_boundary_flux_near(
+            _device_index(device), float(s), len(P), P.ctypes.data, len(poff) - 1, poff.ctypes.data,
+            eoff.ctypes.data, eid.ctypes.data, len(E), p0c.ctypes.data, p1c.ctypes.data, nrmc.ctypes.data,
+            gx.ctypes.data, gw.ctypes.data, len(gx), out.ctypes.data))
+        V[cells] += out.reshape(len(cells), q)
     return V
 
 
@@ -629,7 +651,7 @@ def compress(mesh, dofmap, kernel, tree, eta, m, params=None, device=None):
     ns = NearStructure(mesh, dofmap, tree, near)
     cell_leaf = cell_leaf_assignment(mesh, dofmap, tree.leaf_of_dof)
     X, _ = cell_nodes(mesh, 6 if d == 1 else 4)
-    V = boundary_flux_at_nodes(mesh, float(kernel.s), tree, cheb, eta, X, cell_leaf)
+    V = boundary_flux_at_nodes(mesh, float(kernel.s), tree, cheb, eta, X, cell_leaf, device)
     A_near = assemble_near_field(mesh, dofmap, kernel, ns, params, V_nodes=V, device=device)
     shift = np.zeros((tree.num_nodes, d, m, m))
     for nd in range(tree.num_nodes):

@@ -13,6 +13,7 @@
 // The far blocks B_p = |xi_a - xi_b|^(2 ex) at the Chebyshev points (compress, :683-694) are
 // either uploaded or built here (one thread per block entry).
 #include <algorithm>
+#include <cmath>
 #include <memory>
 #include <vector>
 
@@ -796,6 +797,40 @@ int32_t cluster_strong_form(fl_cluster* C, const DevMesh& m, double s, const dou
 }  // namespace fl
 
 // ------------------------------------------------------------------ C ABI
+
+// near part of the dual-tree boundary flux (boundary_flux_at_nodes, cluster.py:586-592): every
+// point of a DoF leaf sums edge_flux_potential (assembly.py:303-333) over the edges of that leaf's
+// near edge-tree nodes, in the order given.  One thread per point; points are grouped by leaf so
+// a warp walks one edge list.
+__global__ void __launch_bounds__(128) near_edge_flux_kernel(int64_t npts, const double* __restrict__ X,
+                                                             int64_t ngroups, const int64_t* __restrict__ poff,
+                                                             const int64_t* __restrict__ eoff,
+                                                             const int* __restrict__ eid,
+                                                             const double* __restrict__ seg,
+                                                             const double* __restrict__ glx,
+                                                             const double* __restrict__ glw, int ngl, double ex,
+                                                             double* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npts) return;
+  int64_t a = 0, b = ngroups;                       // group g: poff[g] <= p < poff[g + 1]
+  while (b - a > 1) {
+    const int64_t mid = (a + b) >> 1;
+    if (poff[mid] <= p) a = mid; else b = mid;
+  }
+  const double x0 = X[2 * p], x1 = X[2 * p + 1];
+  double acc = 0.0;
+  for (int64_t k = eoff[a]; k < eoff[a + 1]; ++k) {
+    const double* e = seg + (size_t)7 * eid[k];     // p0x p0y ux uy nx ny |e|
+    double s = 0.0;
+    for (int g = 0; g < ngl; ++g) {
+      const double dx = x0 - (e[0] + glx[g] * e[2]), dy = x1 - (e[1] + glx[g] * e[3]);
+      s = fma(glw[g], fma(dy, e[5], dx * e[4]) * pow(fma(dy, dy, dx * dx), ex), s);
+    }
+    acc = fma(s, e[6], acc);
+  }
+  out[p] = acc;
+}
+
 #define FL_TRY try {
 #define FL_CATCH                                                                   \
   }                                                                                \
@@ -937,6 +972,57 @@ int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out) {
     FL_CUDA(cudaMemcpyAsync(blocks_out, C->blocks.p, (size_t)C->np * C->M * C->M * sizeof(double),
                             cudaMemcpyDeviceToHost, C->stream));
   FL_CUDA(cudaStreamSynchronize(C->stream));
+  return FL_OK;
+  FL_CATCH
+}
+
+int32_t fl_boundary_flux_near(int32_t device, double s, int64_t npts, const double* X, int64_t ngroups,
+                              const int64_t* poff, const int64_t* eoff, const int64_t* eid, int64_t nb,
+                              const double* p0, const double* p1, const double* normals, const double* gl_x,
+                              const double* gl_w, int64_t ngl, double* out) {
+  FL_TRY
+  if (npts < 0 || ngroups < 0 || nb < 0 || ngl <= 0 || ngl > 64 || !(s > 0.0 && s < 1.0))
+    return fl::api_fail(FL_E_ARG, "bad argument");
+  if (npts == 0) return FL_OK;
+  if (!X || !poff || !eoff || !out || !gl_x || !gl_w || ngroups == 0)
+    return fl::api_fail(FL_E_ARG, "null argument");
+  if (poff[0] != 0 || poff[ngroups] != npts || eoff[0] != 0) return fl::api_fail(FL_E_ARG, "bad group offsets");
+  for (int64_t g = 0; g < ngroups; ++g)
+    if (poff[g + 1] < poff[g] || eoff[g + 1] < eoff[g]) return fl::api_fail(FL_E_ARG, "bad group offsets");
+  const int64_t ne = eoff[ngroups];
+  if (ne > 0 && (!eid || !p0 || !p1 || !normals)) return fl::api_fail(FL_E_ARG, "null argument");
+  std::vector<int> ei((size_t)std::max<int64_t>(ne, 1));
+  for (int64_t k = 0; k < ne; ++k) {
+    if (eid[k] < 0 || eid[k] >= nb) return fl::api_fail(FL_E_ARG, "edge index out of range");
+    ei[k] = (int)eid[k];
+  }
+  std::vector<double> seg((size_t)std::max<int64_t>(7 * nb, 1));
+  for (int64_t e = 0; e < nb; ++e) {
+    const double ux = p1[2 * e] - p0[2 * e], uy = p1[2 * e + 1] - p0[2 * e + 1];
+    double* r = &seg[7 * e];
+    r[0] = p0[2 * e]; r[1] = p0[2 * e + 1]; r[2] = ux; r[3] = uy;
+    r[4] = normals[2 * e]; r[5] = normals[2 * e + 1]; r[6] = std::sqrt(ux * ux + uy * uy);
+  }
+  FL_CUDA(cudaSetDevice(device));
+  fl::OwnedStreamLease lease(device);
+  cudaStream_t st = lease.s;
+  fl::StreamScope scope(st);
+  fl::DBuf<double> dX((size_t)2 * npts), dseg(seg.size()), dgx(ngl), dgw(ngl), dout(npts);
+  fl::DBuf<int64_t> dpo(ngroups + 1), deo(ngroups + 1);
+  fl::DBuf<int> dei(ei.size());
+  FL_CUDA(cudaMemcpyAsync(dX.p, X, (size_t)2 * npts * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dseg.p, seg.data(), seg.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dgx.p, gl_x, ngl * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dgw.p, gl_w, ngl * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dpo.p, poff, (ngroups + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(deo.p, eoff, (ngroups + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyAsync(dei.p, ei.data(), ei.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  near_edge_flux_kernel<<<(unsigned)((npts + 127) / 128), 128, 0, st>>>(npts, dX.p, ngroups, dpo.p, deo.p, dei.p,
+                                                                         dseg.p, dgx.p, dgw.p, (int)ngl,
+                                                                         -(1.0 + s), dout.p);
+  FL_CUDA(cudaGetLastError());
+  FL_CUDA(cudaMemcpyAsync(out, dout.p, npts * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
   return FL_OK;
   FL_CATCH
 }
