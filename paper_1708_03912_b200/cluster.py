@@ -365,15 +365,23 @@ def cheb_points_1d(m):
 
 
 def lagrange_eval(ref_nodes, t):
-    """Lagrange basis at the Chebyshev nodes evaluated at t (..., ) -> (..., m) (cluster.py:276-287)."""
+    """Lagrange basis at the Chebyshev nodes evaluated at t (..., ) -> (..., m) (cluster.py:276-287):
+    prod_{b != a} (t - x_b) / (x_a - x_b), the numerator as prefix x suffix products."""
+    ref_nodes = np.asarray(ref_nodes, float)
     m = len(ref_nodes)
     t = np.asarray(t, float)
     diff = t[..., None] - ref_nodes
-    out = np.empty(t.shape + (m,))
-    for a in range(m):
-        keep = np.arange(m) != a
-        out[..., a] = np.prod(diff[..., keep], axis=-1) / np.prod(ref_nodes[a] - ref_nodes[keep])
-    return out
+    pre = np.ones(t.shape + (m,))
+    suf = np.ones(t.shape + (m,))
+    if m > 1:
+        pre[..., 1:] = np.cumprod(diff[..., :-1], axis=-1)
+        suf[..., :-1] = np.cumprod(diff[..., :0:-1], axis=-1)[..., ::-1]
+    return pre * suf / _lagrange_denominators(ref_nodes)
+
+
+def _lagrange_denominators(ref_nodes):
+    m = len(ref_nodes)
+    return np.array([np.prod(ref_nodes[a] - ref_nodes[np.arange(m) != a]) for a in range(m)])
 
 
 def choose_order(mesh_stats, tol=1e-6):
@@ -404,12 +412,13 @@ class _Boxes:
         self.parent = np.asarray(parent)
         self.order = list(order)
         self.shift = [None] * len(cen)
-        for nd in self.order:
-            par = self.parent[nd]
-            if par < 0:
-                continue
-            self.shift[nd] = [lagrange_eval(self.ref, (cen[nd, j] + half[nd] * self.ref - cen[par, j]) / half[par]).T
-                              for j in range(d)]
+        kids = np.asarray([nd for nd in self.order if self.parent[nd] >= 0], np.int64)
+        if len(kids):
+            par = self.parent[kids]
+            T = (cen[kids, :, None] + half[kids, None, None] * self.ref - cen[par, :, None]) / half[par, None, None]
+            L = np.swapaxes(lagrange_eval(self.ref, T), -1, -2)           # (kids, d, m, m)
+            for i, nd in enumerate(kids):
+                self.shift[nd] = [L[i, j] for j in range(d)]
 
     def eval_basis(self, nd, X):
         per = [lagrange_eval(self.ref, (X[..., j] - self.cen[nd][j]) / self.half[nd]) for j in range(self.d)]
@@ -570,9 +579,15 @@ def boundary_flux_at_nodes(mesh, s, tree, cheb, eta, X, cell_leaf, device=None):
     for c in range(nc):
         by_leaf.setdefault(cell_leaf[c], []).append(c)
     groups, poff, eoff, eid = [], [0], [0], []
+    cl = np.asarray(cell_leaf, np.int64)
+    for a in range(0, nc, 16384):                                          # far part, bounded temporaries
+        l = cl[a:a + 16384]
+        T = (X[a:a + 16384] - cheb.cen[l][:, None, :]) / cheb.half[l][:, None, None]
+        per = [lagrange_eval(cheb.ref, T[..., j]) for j in range(d)]
+        Lb = per[0] if d == 1 else per[0][..., cheb.multi[:, 0]] * per[1][..., cheb.multi[:, 1]]
+        V[a:a + 16384] = np.einsum("cqm,cm->cq", Lb, F[l])
     for nd, cs in by_leaf.items():
         cs = np.asarray(cs)
-        V[cs] = (cheb.eval_basis(nd, X[cs].reshape(-1, d)) @ F[nd]).reshape(len(cs), q)
         if near_map.get(nd):
             eids = np.concatenate([etree.node_edges(b) for b in near_map[nd]])
             if len(eids):
@@ -611,18 +626,28 @@ def _basis_coefficients(mesh, dofmap, tree, cheb):
     lam = np.stack([1 - pts[:, 0], pts[:, 0]], 1) if d == 1 else \
         np.stack([1 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]], 1)
     offs, pdata = mesh.patch_arrays()
+    offs, pdata = np.asarray(offs, np.int64), np.asarray(pdata, np.int64)
     cd = np.asarray(dofmap.vertex_to_dof)[np.asarray(mesh.cells)]
     dofs = np.asarray(dofmap.dofs)
-    for nd in tree.leaves:
-        nds = tree.node_dofs(nd)
-        if not len(nds):
-            continue
-        cells = np.unique(np.concatenate([pdata[offs[dofs[i]]:offs[dofs[i] + 1]] for i in nds]))
-        Lb = cheb.eval_basis(nd, X[cells].reshape(-1, d)).reshape(len(cells), -1, cheb.M)
-        mom = np.einsum("cq,qa,cqm->cam", W[cells], lam, Lb, optimize=True)
-        gd = cd[cells]
-        ok = (gd >= 0) & (tree.leaf_of_dof[np.clip(gd, 0, None)] == nd)
-        np.add.at(out, gd[ok], mom[ok])
+    lod = np.asarray(tree.leaf_of_dof, np.int64)
+    # (leaf, cell) pairs: every cell of the patch of every DoF of the leaf, unique and sorted
+    v = dofs[np.arange(n)]
+    cnt = offs[v + 1] - offs[v]
+    first = np.repeat(offs[v] - np.concatenate([[0], np.cumsum(cnt)[:-1]]), cnt)
+    pc = pdata[first + np.arange(cnt.sum())]
+    key = np.unique(np.repeat(lod, cnt) * np.int64(mesh.cells.shape[0]) + pc)
+    pl, pcell = key // mesh.cells.shape[0], key % mesh.cells.shape[0]
+    for a in range(0, len(key), 16384):                                    # bounded temporaries
+        l, c = pl[a:a + 16384], pcell[a:a + 16384]
+        T = (X[c] - cheb.cen[l][:, None, :]) / cheb.half[l][:, None, None]   # (pairs, q, d)
+        per = [lagrange_eval(cheb.ref, T[..., j]) for j in range(d)]
+        Lb = per[0] if d == 1 else per[0][..., cheb.multi[:, 0]] * per[1][..., cheb.multi[:, 1]]
+        mom = np.tensordot(W[c][:, :, None] * Lb, lam, axes=([1], [0]))     # (pairs, M, d+1)
+        gd = cd[c]
+        ok = (gd >= 0) & (lod[np.clip(gd, 0, None)] == l[:, None])
+        g, vals = gd[ok], mom.transpose(0, 2, 1)[ok]                         # (entries, M)
+        for k in range(cheb.M):
+            out[:, k] += np.bincount(g, weights=vals[:, k], minlength=n)
     return out
 
 
