@@ -38,6 +38,10 @@ struct fl_cluster {
   bool fused = false;
   int coop_blocks = 0;                                  // resident blocks of the cooperative far field
   int nleaves = 0;
+  // fused schedule: subtrees of <= S nodes, each finished by one block (moments, upward and
+  // downward passes, evaluation) with block barriers; the nodes above them ("top") by block 0
+  fl::DBuf<int> sub_info, grp_off, grp_nodes, sub_leaves;
+  int nsub = 0, top_g0 = 0, top_g1 = 0;
   cudaStream_t stream = nullptr;
   ~fl_cluster() {
     for (auto* b : {&data, &diag, &shift, &bc, &blocks, &mom, &F, &Fp, &x, &y, &yfar}) b->free();
@@ -185,41 +189,76 @@ __global__ void eval_kernel(int64_t n, const int* __restrict__ leaf_of_dof, cons
 // The whole far field in ONE cooperative launch (small / medium operators, e.g. 1D at c2: ~2k
 // nodes, M <= 12): the same phases and accumulation orders as the kernels above, separated by
 // grid-wide barriers instead of ~2 x depth + 4 launches.
+// one level group of the upward pass inside a block: mom[p] += S_c mom[c] over both children
+template <int D>
+__device__ __forceinline__ void up_group(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
+                                         const double* __restrict__ shift, int m, int M, double* __restrict__ mom,
+                                         bool internal_zero) {
+  for (int t = threadIdx.x; t < cnt * M; t += blockDim.x) {
+    const int p = nodes[t / M], a = t % M;
+    double acc = internal_zero ? 0.0 : mom[(int64_t)p * M + a];
+    for (int k = 1; k >= 0; --k) {
+      const int c = children[2 * p + k];
+      if (c >= 0) acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+    }
+    mom[(int64_t)p * M + a] = acc;
+  }
+}
+// one level group of the downward pass: F[c] += S_c^T F[p] for both children of every p
+template <int D>
+__device__ __forceinline__ void down_group(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
+                                           const double* __restrict__ shift, int m, int M, double* __restrict__ F) {
+  for (int t = threadIdx.x; t < cnt * 2 * M; t += blockDim.x) {
+    const int p = nodes[t / (2 * M)], k = (t / M) & 1, a = t % M;
+    const int c = children[2 * p + k];
+    if (c >= 0) F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)p * M, m, a, true);
+  }
+}
+
+// The whole far field in one cooperative launch with five grid barriers.  Per node the arithmetic
+// (and so the result) is that of the level-by-level passes (ChebData.push_up / push_down,
+// cluster.py:339-374): the schedule only changes which block runs a node, and when.
+//   sub_info[6j..]: group range [g0, g1) (deepest first), leaf range [l0, l1) of sub_leaves,
+//   dof range [r0, r1) of dof_perm;  groups: grp_nodes[grp_off[g] .. grp_off[g+1]) (parents only)
 template <int D>
 __global__ void __launch_bounds__(256) far_fused_kernel(
-    int nleaves, const int* __restrict__ leaf_nodes, const int* __restrict__ lo, const int* __restrict__ hi,
-    const int* __restrict__ perm, const double* __restrict__ x, const double* __restrict__ bc, int m, int M,
-    int64_t nn, const int* __restrict__ level_nodes, const int64_t* __restrict__ off_up, int nup,
-    const int64_t* __restrict__ off_down, int ndown, const int* __restrict__ children, const int* __restrict__ parent,
+    int nsub, const int* __restrict__ sub_info, const int* __restrict__ grp_off, const int* __restrict__ grp_nodes,
+    const int* __restrict__ sub_leaves, int top_g0, int top_g1, const int* __restrict__ leaf_nodes,
+    const int* __restrict__ lo, const int* __restrict__ hi, const int* __restrict__ perm, const double* __restrict__ x,
+    const double* __restrict__ bc, int m, int M, int64_t nn, const int* __restrict__ children,
     const double* __restrict__ shift, int64_t np, const int* __restrict__ pairs, const double* __restrict__ B,
     const int* __restrict__ poff, const int* __restrict__ plist, double* __restrict__ mom, double* __restrict__ Fp,
-    double* __restrict__ F, int64_t n, const int* __restrict__ leaf_of_dof, double negC, double* __restrict__ y,
+    double* __restrict__ F, const int* __restrict__ leaf_of_dof, double negC, double* __restrict__ y,
     double* __restrict__ yfar) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = tid; t < nn * M; t += nt) mom[t] = 0.0;
-  grid.sync();
-  for (int64_t t = tid; t < (int64_t)nleaves * M; t += nt) {
-    const int l = (int)(t / M), a = (int)(t % M);
-    double s = 0.0;
-    for (int r = lo[l]; r < hi[l]; ++r) s = fma(x[perm[r]], bc[(int64_t)perm[r] * M + a], s);
-    mom[(int64_t)leaf_nodes[l] * M + a] = s;
+  // 1. subtrees: leaf moments, then the upward pass to the subtree root
+  for (int j = blockIdx.x; j < nsub; j += gridDim.x) {
+    const int* I = sub_info + 6 * j;
+    for (int t = threadIdx.x; t < (I[3] - I[2]) * M; t += blockDim.x) {
+      const int l = sub_leaves[I[2] + t / M], a = t % M;
+      double s = 0.0;
+      for (int r = lo[l]; r < hi[l]; ++r) s = fma(x[perm[r]], bc[(int64_t)perm[r] * M + a], s);
+      mom[(int64_t)leaf_nodes[l] * M + a] = s;
+    }
+    for (int g = I[0]; g < I[1]; ++g) {
+      __syncthreads();
+      up_group<D>(grp_nodes + grp_off[g], grp_off[g + 1] - grp_off[g], children, shift, m, M, mom, true);
+    }
+    __syncthreads();
   }
   grid.sync();
-  for (int L = 0; L < nup; ++L) {
-    const int64_t a0 = off_up[L], cnt = off_up[L + 1] - a0;
-    for (int64_t t = tid; t < cnt * M; t += nt) {
-      const int p = level_nodes[a0 + t / M], a = (int)(t % M);
-      double acc = mom[(int64_t)p * M + a];
-      for (int k = 1; k >= 0; --k) {
-        const int c = children[2 * p + k];
-        if (c >= 0) acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+  // 2. the nodes above the subtrees, one block
+  if (top_g1 > top_g0) {
+    if (blockIdx.x == 0)
+      for (int g = top_g0; g < top_g1; ++g) {
+        up_group<D>(grp_nodes + grp_off[g], grp_off[g + 1] - grp_off[g], children, shift, m, M, mom, true);
+        __syncthreads();
       }
-      mom[(int64_t)p * M + a] = acc;
-    }
     grid.sync();
   }
+  // 3. far pairs
   for (int64_t t = tid; t < np * 2 * M; t += nt) {
     const int64_t p = t / (2 * M);
     const int r = (int)(t % (2 * M));
@@ -235,6 +274,7 @@ __global__ void __launch_bounds__(256) far_fused_kernel(
     Fp[t] = s;
   }
   grid.sync();
+  // 4. gather the pair contributions of every node
   for (int64_t t = tid; t < nn * M; t += nt) {
     const int64_t nd = t / M;
     const int a = (int)(t % M);
@@ -246,21 +286,32 @@ __global__ void __launch_bounds__(256) far_fused_kernel(
     F[t] = s;
   }
   grid.sync();
-  for (int L = 0; L < ndown; ++L) {
-    const int64_t a0 = off_down[L], cnt = off_down[L + 1] - a0;
-    for (int64_t t = tid; t < cnt * M; t += nt) {
-      const int c = level_nodes[a0 + t / M], a = (int)(t % M);
-      F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)parent[c] * M, m, a, true);
-    }
+  // 5. downward pass above the subtrees (down to the subtree roots), one block
+  if (top_g1 > top_g0) {
+    if (blockIdx.x == 0)
+      for (int g = top_g1 - 1; g >= top_g0; --g) {
+        down_group<D>(grp_nodes + grp_off[g], grp_off[g + 1] - grp_off[g], children, shift, m, M, F);
+        __syncthreads();
+      }
     grid.sync();
   }
-  for (int64_t i = tid; i < n; i += nt) {
-    const double* f = F + (int64_t)leaf_of_dof[i] * M;
-    double s = 0.0;
-    for (int a = 0; a < M; ++a) s = fma(bc[i * M + a], f[a], s);
-    const double v = negC * s;
-    yfar[i] = v;
-    y[i] += v;
+  // 6. subtrees: downward pass to the leaves, then y_far = -C basis_coef . F[leaf]
+  for (int j = blockIdx.x; j < nsub; j += gridDim.x) {
+    const int* I = sub_info + 6 * j;
+    for (int g = I[1] - 1; g >= I[0]; --g) {
+      down_group<D>(grp_nodes + grp_off[g], grp_off[g + 1] - grp_off[g], children, shift, m, M, F);
+      __syncthreads();
+    }
+    for (int r = I[4] + threadIdx.x; r < I[5]; r += blockDim.x) {
+      const int i = perm[r];
+      const double* f = F + (int64_t)leaf_of_dof[i] * M;
+      double s = 0.0;
+      for (int a = 0; a < M; ++a) s = fma(bc[(int64_t)i * M + a], f[a], s);
+      const double v = negC * s;
+      yfar[i] = v;
+      y[i] += v;
+    }
+    __syncthreads();
   }
 }
 
@@ -345,6 +396,54 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
     }
     off_down.push_back((int64_t)lvl_nodes.size());
   }
+  // fused schedule: subtree roots = maximal nodes of <= S nodes; their internal nodes grouped by
+  // depth (deepest first), then the nodes above them ("top") grouped the same way
+  const int S = getenv("FRACLAP_SUBTREE_NODES") ? std::max(1, atoi(getenv("FRACLAP_SUBTREE_NODES")))
+                                                 : (int)std::max<int64_t>(32, nn / 128);
+  std::vector<int64_t> tsize(nn, 1);
+  for (int64_t t = nn - 1; t >= 0; --t) {
+    const int64_t k = D.topo_order[t];
+    if (par[k] >= 0) tsize[par[k]] += tsize[k];
+  }
+  std::vector<int> leaf_index(nn, -1);
+  for (size_t l = 0; l < leaf_nodes.size(); ++l) leaf_index[leaf_nodes[l]] = (int)l;
+  std::vector<int> sub_info, grp_off{0}, grp_nodes, sub_leaves;
+  int64_t covered = 0;
+  for (int64_t t = 0; t < nn; ++t) {
+    const int64_t root = D.topo_order[t];
+    if (tsize[root] > S || (par[root] >= 0 && tsize[par[root]] <= S)) continue;
+    std::vector<int> bfs{(int)root};
+    for (size_t u = 0; u < bfs.size(); ++u)
+      for (int k = 0; k < 2; ++k)
+        if (children[2 * bfs[u] + k] >= 0) bfs.push_back(children[2 * bfs[u] + k]);
+    int dmax = depth[root];
+    for (int k : bfs) dmax = std::max(dmax, depth[k]);
+    sub_info.push_back((int)grp_off.size() - 1);
+    for (int L = dmax - 1; L >= depth[root]; --L) {
+      size_t before = grp_nodes.size();
+      for (int k : bfs)
+        if (depth[k] == L && children[2 * k] >= 0) grp_nodes.push_back(k);
+      if (grp_nodes.size() > before) grp_off.push_back((int)grp_nodes.size());
+    }
+    sub_info.push_back((int)grp_off.size() - 1);
+    sub_info.push_back((int)sub_leaves.size());
+    for (int k : bfs)
+      if (leaf_index[k] >= 0) sub_leaves.push_back(leaf_index[k]);
+    sub_info.push_back((int)sub_leaves.size());
+    sub_info.push_back((int)D.ranges[2 * root]);
+    sub_info.push_back((int)D.ranges[2 * root + 1]);
+    covered += D.ranges[2 * root + 1] - D.ranges[2 * root];
+  }
+  const int top_g0 = (int)grp_off.size() - 1;
+  for (int L = maxd - 1; L >= 0; --L) {
+    size_t before = grp_nodes.size();
+    for (int64_t t = 0; t < nn; ++t) {
+      const int64_t k = D.topo_order[t];
+      if (depth[k] == L && tsize[k] > S && children[2 * k] >= 0) grp_nodes.push_back((int)k);
+    }
+    if (grp_nodes.size() > before) grp_off.push_back((int)grp_nodes.size());
+  }
+  const int top_g1 = (int)grp_off.size() - 1;
   // pair lists per node: first-node roles in pair order, then second-node roles
   std::vector<int> prs(std::max<int64_t>(2 * np, 1)), cnt(nn + 1, 0);
   for (int64_t p = 0; p < np; ++p) {
@@ -384,6 +483,11 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
   up_i(C->leaf_nodes, leaf_nodes); up_i(C->leaf_lo, lo); up_i(C->leaf_hi, hi); up_i(C->dof_perm, perm);
   up_i(C->leaf_of_dof, lod); up_i(C->children, children); up_i(C->parent, par); up_i(C->pairs, prs);
   up_i(C->plist_off, cnt); up_i(C->plist, lst); up_i(C->level_nodes, lvl_nodes);
+  up_i(C->sub_info, sub_info); up_i(C->grp_off, grp_off); up_i(C->grp_nodes, grp_nodes);
+  up_i(C->sub_leaves, sub_leaves);
+  C->nsub = (int)(sub_info.size() / 6);
+  C->top_g0 = top_g0;
+  C->top_g1 = top_g1;
   up_d(C->shift, D.shift, (size_t)nn * d * m * m);
   up_d(C->bc, D.basis_coef, (size_t)n * M);
   if (D.center && D.half && D.ref) {
@@ -443,7 +547,7 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, d == 1 ? (const void*)far_fused_kernel<1>
                                                                : (const void*)far_fused_kernel<2>, 256, 0);
     C->coop_blocks = sms * std::min(per, getenv("FRACLAP_COOP_PER_SM") ? atoi(getenv("FRACLAP_COOP_PER_SM")) : 1);
-    C->fused = coop && C->coop_blocks > 0;
+    C->fused = coop && C->coop_blocks > 0 && covered == n && (int64_t)sub_leaves.size() == (int64_t)leaf_nodes.size();
   }
   C->mom.alloc((size_t)nn * M);
   C->F.alloc((size_t)nn * M);
@@ -464,15 +568,13 @@ int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yf
   if (n == 0) return FL_OK;
   csr_spmv_kernel<<<grid_of(n * 32), 256, 0, st>>>(n, C->indptr.p, C->indices.p, C->data.p, x, y), note_launch();
   if (C->fused) {
-    int nup = (int)C->level_off_up.size() - 1, ndown = (int)C->level_off_down.size() - 1;
-    int nl = C->nleaves;
     double negC = -C->C;
-    int64_t nn_ = nn, np_ = np, n_ = n;
+    int64_t nn_ = nn, np_ = np;
     int m_ = m, M_ = M;
-    void* args[] = {&nl, &C->leaf_nodes.p, &C->leaf_lo.p, &C->leaf_hi.p, &C->dof_perm.p, &x, &C->bc.p, &m_, &M_,
-                    &nn_, &C->level_nodes.p, &C->d_off_up.p, &nup, &C->d_off_down.p, &ndown, &C->children.p,
-                    &C->parent.p, &C->shift.p, &np_, &C->pairs.p, &C->blocks.p, &C->plist_off.p, &C->plist.p,
-                    &C->mom.p, &C->Fp.p, &C->F.p, &n_, &C->leaf_of_dof.p, &negC, &y, &yfar};
+    void* args[] = {&C->nsub, &C->sub_info.p, &C->grp_off.p, &C->grp_nodes.p, &C->sub_leaves.p, &C->top_g0,
+                    &C->top_g1, &C->leaf_nodes.p, &C->leaf_lo.p, &C->leaf_hi.p, &C->dof_perm.p, &x, &C->bc.p, &m_,
+                    &M_, &nn_, &C->children.p, &C->shift.p, &np_, &C->pairs.p, &C->blocks.p, &C->plist_off.p,
+                    &C->plist.p, &C->mom.p, &C->Fp.p, &C->F.p, &C->leaf_of_dof.p, &negC, &y, &yfar};
     const void* fn = C->d == 1 ? (const void*)far_fused_kernel<1> : (const void*)far_fused_kernel<2>;
     FL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(C->coop_blocks), dim3(256), args, 0, st));
     note_launch();
