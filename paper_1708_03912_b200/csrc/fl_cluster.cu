@@ -42,6 +42,8 @@ struct fl_cluster {
   // downward passes, evaluation) with block barriers; the nodes above them ("top") by block 0
   fl::DBuf<int> sub_info, grp_off, grp_nodes, sub_leaves;
   int nsub = 0, top_g0 = 0, top_g1 = 0;
+  fl::DBuf<int> early, late;                            // far pairs before / after the top levels
+  int64_t n_early = 0, n_late = 0;
   cudaStream_t stream = nullptr;
   ~fl_cluster() {
     for (auto* b : {&data, &diag, &shift, &bc, &blocks, &mom, &F, &Fp, &x, &y, &yfar}) b->free();
@@ -215,6 +217,26 @@ __device__ __forceinline__ void down_group(const int* __restrict__ nodes, int cn
   }
 }
 
+// Fp[p] = (B_p mom[b], B_p^T mom[a]) for the pairs listed  (_far_potentials, cluster.py:436-447)
+__device__ __forceinline__ void far_pair_items(int64_t cnt, const int* __restrict__ list, const int* __restrict__ pairs,
+                                               const double* __restrict__ B, int M, const double* __restrict__ mom,
+                                               double* __restrict__ Fp, int64_t tid, int64_t nt) {
+  for (int64_t t = tid; t < cnt * 2 * M; t += nt) {
+    const int64_t p = list[t / (2 * M)];
+    const int r = (int)(t % (2 * M));
+    const double* Bp = B + p * M * M;
+    double s = 0.0;
+    if (r < M) {
+      const double* mb = mom + (int64_t)pairs[2 * p + 1] * M;
+      for (int b = 0; b < M; ++b) s = fma(Bp[(int64_t)r * M + b], mb[b], s);
+    } else {
+      const double* ma = mom + (int64_t)pairs[2 * p] * M;
+      for (int a = 0; a < M; ++a) s = fma(Bp[(int64_t)a * M + (r - M)], ma[a], s);
+    }
+    Fp[p * 2 * M + r] = s;
+  }
+}
+
 // The whole far field in one cooperative launch with five grid barriers.  Per node the arithmetic
 // (and so the result) is that of the level-by-level passes (ChebData.push_up / push_down,
 // cluster.py:339-374): the schedule only changes which block runs a node, and when.
@@ -229,7 +251,9 @@ __global__ void __launch_bounds__(256) far_fused_kernel(
     const double* __restrict__ shift, int64_t np, const int* __restrict__ pairs, const double* __restrict__ B,
     const int* __restrict__ poff, const int* __restrict__ plist, double* __restrict__ mom, double* __restrict__ Fp,
     double* __restrict__ F, const int* __restrict__ leaf_of_dof, double negC, double* __restrict__ y,
-    double* __restrict__ yfar) {
+    double* __restrict__ yfar, int64_t n, const int64_t* __restrict__ indptr, const int* __restrict__ idx,
+    const double* __restrict__ val, int64_t n_early, const int* __restrict__ early, int64_t n_late,
+    const int* __restrict__ late) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
@@ -249,30 +273,31 @@ __global__ void __launch_bounds__(256) far_fused_kernel(
     __syncthreads();
   }
   grid.sync();
-  // 2. the nodes above the subtrees, one block
-  if (top_g1 > top_g0) {
-    if (blockIdx.x == 0)
-      for (int g = top_g0; g < top_g1; ++g) {
-        up_group<D>(grp_nodes + grp_off[g], grp_off[g + 1] - grp_off[g], children, shift, m, M, mom, true);
-        __syncthreads();
-      }
-    grid.sync();
-  }
-  // 3. far pairs
-  for (int64_t t = tid; t < np * 2 * M; t += nt) {
-    const int64_t p = t / (2 * M);
-    const int r = (int)(t % (2 * M));
-    const double* Bp = B + p * M * M;
-    double s = 0.0;
-    if (r < M) {
-      const double* mb = mom + (int64_t)pairs[2 * p + 1] * M;
-      for (int b = 0; b < M; ++b) s = fma(Bp[(int64_t)r * M + b], mb[b], s);
-    } else {
-      const double* ma = mom + (int64_t)pairs[2 * p] * M;
-      for (int a = 0; a < M; ++a) s = fma(Bp[(int64_t)a * M + (r - M)], ma[a], s);
+  // 2. block 0: the nodes above the subtrees; the other blocks meanwhile: the near CSR product
+  //    (warp per row, as csr_spmv_kernel) and the far pairs whose two nodes are final already
+  const bool has_top = top_g1 > top_g0, split = has_top && gridDim.x > 1;
+  if (has_top && blockIdx.x == 0) {
+    for (int g = top_g0; g < top_g1; ++g) {
+      up_group<D>(grp_nodes + grp_off[g], grp_off[g + 1] - grp_off[g], children, shift, m, M, mom, true);
+      __syncthreads();
     }
-    Fp[t] = s;
   }
+  if (!split || blockIdx.x != 0) {
+    const int64_t b0 = split ? 1 : 0;
+    const int64_t ltid = (int64_t)(blockIdx.x - b0) * blockDim.x + threadIdx.x;
+    const int64_t lnt = (int64_t)(gridDim.x - b0) * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = ltid >> 5; w < n; w += lnt >> 5) {
+      double s = 0.0;
+      for (int64_t e = indptr[w] + lane; e < indptr[w + 1]; e += 32) s = fma(val[e], x[idx[e]], s);
+      s = warp_sum(s);
+      if (lane == 0) y[w] = s;
+    }
+    far_pair_items(n_early, early, pairs, B, M, mom, Fp, ltid, lnt);
+  }
+  grid.sync();
+  // 3. the remaining far pairs
+  far_pair_items(n_late, late, pairs, B, M, mom, Fp, tid, nt);
   grid.sync();
   // 4. gather the pair contributions of every node
   for (int64_t t = tid; t < nn * M; t += nt) {
@@ -458,6 +483,10 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
   std::vector<int> lst(std::max<int64_t>(2 * np, 1)), fill(cnt.begin(), cnt.end() - 1);
   for (int role = 0; role < 2; ++role)
     for (int64_t p = 0; p < np; ++p) lst[fill[prs[2 * p + role]]++] = (int)(2 * p + role);
+  // far pairs whose nodes are both inside subtrees run while block 0 does the top levels
+  std::vector<int> early, late;
+  for (int64_t p = 0; p < np; ++p)
+    (tsize[prs[2 * p]] > S || tsize[prs[2 * p + 1]] > S ? late : early).push_back((int)p);
 
   FL_CUDA(cudaSetDevice(device));
   init_pool(device);
@@ -483,6 +512,9 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
   up_i(C->leaf_nodes, leaf_nodes); up_i(C->leaf_lo, lo); up_i(C->leaf_hi, hi); up_i(C->dof_perm, perm);
   up_i(C->leaf_of_dof, lod); up_i(C->children, children); up_i(C->parent, par); up_i(C->pairs, prs);
   up_i(C->plist_off, cnt); up_i(C->plist, lst); up_i(C->level_nodes, lvl_nodes);
+  up_i(C->early, early); up_i(C->late, late);
+  C->n_early = (int64_t)early.size();
+  C->n_late = (int64_t)late.size();
   up_i(C->sub_info, sub_info); up_i(C->grp_off, grp_off); up_i(C->grp_nodes, grp_nodes);
   up_i(C->sub_leaves, sub_leaves);
   C->nsub = (int)(sub_info.size() / 6);
@@ -566,21 +598,22 @@ int32_t cluster_matvec_dev(fl_cluster* C, const double* x, double* y, double* yf
   const int64_t n = C->n, nn = C->nn, np = C->np;
   const int M = C->M, m = C->m;
   if (n == 0) return FL_OK;
-  csr_spmv_kernel<<<grid_of(n * 32), 256, 0, st>>>(n, C->indptr.p, C->indices.p, C->data.p, x, y), note_launch();
-  if (C->fused) {
+  if (C->fused) {                                      // the near product runs inside the fused kernel
     double negC = -C->C;
-    int64_t nn_ = nn, np_ = np;
+    int64_t nn_ = nn, np_ = np, n_ = n;
     int m_ = m, M_ = M;
     void* args[] = {&C->nsub, &C->sub_info.p, &C->grp_off.p, &C->grp_nodes.p, &C->sub_leaves.p, &C->top_g0,
                     &C->top_g1, &C->leaf_nodes.p, &C->leaf_lo.p, &C->leaf_hi.p, &C->dof_perm.p, &x, &C->bc.p, &m_,
                     &M_, &nn_, &C->children.p, &C->shift.p, &np_, &C->pairs.p, &C->blocks.p, &C->plist_off.p,
-                    &C->plist.p, &C->mom.p, &C->Fp.p, &C->F.p, &C->leaf_of_dof.p, &negC, &y, &yfar};
+                    &C->plist.p, &C->mom.p, &C->Fp.p, &C->F.p, &C->leaf_of_dof.p, &negC, &y, &yfar, &n_, &C->indptr.p,
+                    &C->indices.p, &C->data.p, &C->n_early, &C->early.p, &C->n_late, &C->late.p};
     const void* fn = C->d == 1 ? (const void*)far_fused_kernel<1> : (const void*)far_fused_kernel<2>;
     FL_CUDA(cudaLaunchCooperativeKernel(fn, dim3(C->coop_blocks), dim3(256), args, 0, st));
     note_launch();
     FL_CHECK_LAUNCH();
     return FL_OK;
   }
+  csr_spmv_kernel<<<grid_of(n * 32), 256, 0, st>>>(n, C->indptr.p, C->indices.p, C->data.p, x, y), note_launch();
   far_potentials(C, x, st);
   eval_kernel<<<grid_of(n), 256, 0, st>>>(n, C->leaf_of_dof.p, C->bc.p, M, C->F.p, -C->C, y, yfar), note_launch();
   FL_CHECK_LAUNCH();
