@@ -191,6 +191,64 @@ __global__ void eval_kernel(int64_t n, const int* __restrict__ leaf_of_dof, cons
 // The whole far field in ONE cooperative launch (small / medium operators, e.g. 1D at c2: ~2k
 // nodes, M <= 12): the same phases and accumulation orders as the kernels above, separated by
 // grid-wide barriers instead of ~2 x depth + 4 launches.
+// 1D, m <= 16: the operands of one shift product (a row / column of S and the vector) loaded into
+// registers before the FMA chain, so a level costs one memory round trip instead of one per
+// unrolled chunk; the FMA order is shift_apply<1>'s
+struct Row16 {
+  double s[16], v[16];
+};
+__device__ __forceinline__ void load_row16(Row16& r, const double* __restrict__ S, const double* __restrict__ v, int m,
+                                           int a, bool transpose) {
+#pragma unroll
+  for (int b = 0; b < 16; ++b)
+    if (b < m) {
+      r.s[b] = transpose ? S[b * m + a] : S[a * m + b];
+      r.v[b] = v[b];
+    }
+}
+__device__ __forceinline__ double dot_row16(const Row16& r, int m) {
+  double s = 0.0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b)
+    if (b < m) s = fma(r.s[b], r.v[b], s);
+  return s;
+}
+
+// 2D, m <= 6: the same for S0 V S1^T (shift_apply<2>'s order)
+struct Mat6 {
+  double s0[6], s1[6], v[36];
+};
+__device__ __forceinline__ void load_mat6(Mat6& r, const double* __restrict__ S, const double* __restrict__ v, int m,
+                                          int a, bool transpose) {
+  const double* S0 = S;
+  const double* S1 = S + m * m;
+  const int a0 = a / m, a1 = a % m;
+#pragma unroll
+  for (int b = 0; b < 6; ++b)
+    if (b < m) {
+      r.s0[b] = transpose ? S0[b * m + a0] : S0[a0 * m + b];
+      r.s1[b] = transpose ? S1[b * m + a1] : S1[a1 * m + b];
+    }
+#pragma unroll
+  for (int b0 = 0; b0 < 6; ++b0)
+#pragma unroll
+    for (int b1 = 0; b1 < 6; ++b1)
+      if (b0 < m && b1 < m) r.v[b0 * 6 + b1] = v[b0 * m + b1];
+}
+__device__ __forceinline__ double dot_mat6(const Mat6& r, int m) {
+  double s = 0.0;
+#pragma unroll
+  for (int b1 = 0; b1 < 6; ++b1)
+    if (b1 < m) {
+      double t = 0.0;
+#pragma unroll
+      for (int b0 = 0; b0 < 6; ++b0)
+        if (b0 < m) t = fma(r.s0[b0], r.v[b0 * 6 + b1], t);
+      s = fma(t, r.s1[b1], s);
+    }
+  return s;
+}
+
 // one level group of the upward pass inside a block: mom[p] += S_c mom[c] over both children
 template <int D>
 __device__ __forceinline__ void up_group(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
@@ -199,9 +257,25 @@ __device__ __forceinline__ void up_group(const int* __restrict__ nodes, int cnt,
   for (int t = threadIdx.x; t < cnt * M; t += blockDim.x) {
     const int p = nodes[t / M], a = t % M;
     double acc = internal_zero ? 0.0 : mom[(int64_t)p * M + a];
-    for (int k = 1; k >= 0; --k) {
-      const int c = children[2 * p + k];
-      if (c >= 0) acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+    if (D == 1 && m <= 16) {
+      const int c1 = children[2 * p + 1], c0 = children[2 * p];
+      Row16 r1, r0;
+      if (c1 >= 0) load_row16(r1, shift + (int64_t)c1 * m * m, mom + (int64_t)c1 * M, m, a, false);
+      if (c0 >= 0) load_row16(r0, shift + (int64_t)c0 * m * m, mom + (int64_t)c0 * M, m, a, false);
+      if (c1 >= 0) acc += dot_row16(r1, m);
+      if (c0 >= 0) acc += dot_row16(r0, m);
+    } else if (D == 2 && m <= 6) {
+      const int c1 = children[2 * p + 1], c0 = children[2 * p];
+      Mat6 r1, r0;
+      if (c1 >= 0) load_mat6(r1, shift + (int64_t)c1 * 2 * m * m, mom + (int64_t)c1 * M, m, a, false);
+      if (c0 >= 0) load_mat6(r0, shift + (int64_t)c0 * 2 * m * m, mom + (int64_t)c0 * M, m, a, false);
+      if (c1 >= 0) acc += dot_mat6(r1, m);
+      if (c0 >= 0) acc += dot_mat6(r0, m);
+    } else {
+      for (int k = 1; k >= 0; --k) {
+        const int c = children[2 * p + k];
+        if (c >= 0) acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+      }
     }
     mom[(int64_t)p * M + a] = acc;
   }
@@ -213,7 +287,20 @@ __device__ __forceinline__ void down_group(const int* __restrict__ nodes, int cn
   for (int t = threadIdx.x; t < cnt * 2 * M; t += blockDim.x) {
     const int p = nodes[t / (2 * M)], k = (t / M) & 1, a = t % M;
     const int c = children[2 * p + k];
-    if (c >= 0) F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)p * M, m, a, true);
+    if (c < 0) continue;
+    if (D == 1 && m <= 16) {
+      Row16 r;
+      load_row16(r, shift + (int64_t)c * m * m, F + (int64_t)p * M, m, a, true);
+      const double f = F[(int64_t)c * M + a];
+      F[(int64_t)c * M + a] = f + dot_row16(r, m);
+    } else if (D == 2 && m <= 6) {
+      Mat6 r;
+      load_mat6(r, shift + (int64_t)c * 2 * m * m, F + (int64_t)p * M, m, a, true);
+      const double f = F[(int64_t)c * M + a];
+      F[(int64_t)c * M + a] = f + dot_mat6(r, m);
+    } else {
+      F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)p * M, m, a, true);
+    }
   }
 }
 
