@@ -658,7 +658,8 @@ int32_t cluster_create(const fl_cluster_desc* Dd, int device, fl_cluster** out) 
   up_l(C->d_off_up, off_up);
   up_l(C->d_off_down, off_down);
   // one block does the far field when it is small (work ~ far blocks + shifts), else level kernels
-  C->fused = (double)np * M * M + (double)nn * M * m * (d == 2 ? m : 1) <= 8.0e6;
+  C->fused = (double)np * M * M + (double)nn * M * m * (d == 2 ? m : 1) <=
+             (getenv("FRACLAP_FUSED_WORK") ? atof(getenv("FRACLAP_FUSED_WORK")) : 8.0e6);
   if (C->fused) {
     int sms = 148, per = 0, coop = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
