@@ -114,83 +114,6 @@ __device__ __forceinline__ double shift_apply(const double* __restrict__ S, cons
   }
 }
 
-// upward: one thread per (parent, alpha): children in reversed BFS order (second child first)
-template <int D>
-__global__ void up_kernel(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
-                          const double* __restrict__ shift, int m, int M, double* __restrict__ mom) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)cnt * M) return;
-  const int p = nodes[t / M], a = (int)(t % M);
-  double acc = mom[(int64_t)p * M + a];
-  for (int k = 1; k >= 0; --k) {
-    const int c = children[2 * p + k];
-    if (c < 0) continue;
-    acc += shift_apply<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
-  }
-  mom[(int64_t)p * M + a] = acc;
-}
-
-// far pairs: Fp[p] = (B mom[b], B^T mom[a])
-__global__ void far_pair_kernel(int64_t np, const int* __restrict__ pairs, const double* __restrict__ B, int M,
-                                const double* __restrict__ mom, double* __restrict__ Fp) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= np * 2 * M) return;
-  const int64_t p = t / (2 * M);
-  const int r = (int)(t % (2 * M));
-  const double* Bp = B + p * M * M;
-  double s = 0.0;
-  if (r < M) {
-    const double* mb = mom + (int64_t)pairs[2 * p + 1] * M;
-    for (int b = 0; b < M; ++b) s = fma(Bp[(int64_t)r * M + b], mb[b], s);
-  } else {
-    const int c = r - M;
-    const double* ma = mom + (int64_t)pairs[2 * p] * M;
-    for (int a = 0; a < M; ++a) s = fma(Bp[(int64_t)a * M + c], ma[a], s);
-  }
-  Fp[t] = s;
-}
-// F[node] = sum over its pair list (as first node, pair order, then as second node, pair order)
-__global__ void far_gather_kernel(int64_t nn, const int* __restrict__ off, const int* __restrict__ lst, int M,
-                                  const double* __restrict__ Fp, double* __restrict__ F) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nn * M) return;
-  const int64_t nd = t / M;
-  const int a = (int)(t % M);
-  double s = 0.0;
-  for (int k = off[nd]; k < off[nd + 1]; ++k) {
-    const int e = lst[k];                  // 2 p + role
-    s += Fp[(int64_t)(e >> 1) * 2 * M + (e & 1) * M + a];
-  }
-  F[t] = s;
-}
-
-// downward: one thread per (child, alpha): F[child] += S^T F[parent]
-template <int D>
-__global__ void down_kernel(const int* __restrict__ nodes, int cnt, const int* __restrict__ parent,
-                            const double* __restrict__ shift, int m, int M, double* __restrict__ F) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)cnt * M) return;
-  const int c = nodes[t / M], a = (int)(t % M);
-  F[(int64_t)c * M + a] += shift_apply<D>(shift + (int64_t)c * D * m * m, F + (int64_t)parent[c] * M, m, a, true);
-}
-
-// y[i] = y_near[i] - C * basis_coef[i, :] . F[leaf(i)]
-__global__ void eval_kernel(int64_t n, const int* __restrict__ leaf_of_dof, const double* __restrict__ bc, int M,
-                            const double* __restrict__ F, double negC, double* __restrict__ y,
-                            double* __restrict__ yfar) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double* f = F + (int64_t)leaf_of_dof[i] * M;
-  double s = 0.0;
-  for (int a = 0; a < M; ++a) s = fma(bc[i * M + a], f[a], s);
-  const double v = negC * s;
-  yfar[i] = v;
-  y[i] += v;
-}
-
-// The whole far field in ONE cooperative launch (small / medium operators, e.g. 1D at c2: ~2k
-// nodes, M <= 12): the same phases and accumulation orders as the kernels above, separated by
-// grid-wide barriers instead of ~2 x depth + 4 launches.
 // 1D, m <= 16: the operands of one shift product (a row / column of S and the vector) loaded into
 // registers before the FMA chain, so a level costs one memory round trip instead of one per
 // unrolled chunk; the FMA order is shift_apply<1>'s
@@ -249,6 +172,100 @@ __device__ __forceinline__ double dot_mat6(const Mat6& r, int m) {
   return s;
 }
 
+// shift_apply<D> with the operands in registers first where they fit (same FMA order)
+template <int D>
+__device__ __forceinline__ double shift_apply_fast(const double* __restrict__ S, const double* __restrict__ v, int m,
+                                                   int a, bool transpose) {
+  if (D == 1 && m <= 16) {
+    Row16 r;
+    load_row16(r, S, v, m, a, transpose);
+    return dot_row16(r, m);
+  }
+  if (D == 2 && m <= 6) {
+    Mat6 r;
+    load_mat6(r, S, v, m, a, transpose);
+    return dot_mat6(r, m);
+  }
+  return shift_apply<D>(S, v, m, a, transpose);
+}
+
+// upward: one thread per (parent, alpha): children in reversed BFS order (second child first)
+template <int D>
+__global__ void up_kernel(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
+                          const double* __restrict__ shift, int m, int M, double* __restrict__ mom) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)cnt * M) return;
+  const int p = nodes[t / M], a = (int)(t % M);
+  double acc = mom[(int64_t)p * M + a];
+  for (int k = 1; k >= 0; --k) {
+    const int c = children[2 * p + k];
+    if (c < 0) continue;
+    acc += shift_apply_fast<D>(shift + (int64_t)c * D * m * m, mom + (int64_t)c * M, m, a, false);
+  }
+  mom[(int64_t)p * M + a] = acc;
+}
+
+// far pairs: Fp[p] = (B mom[b], B^T mom[a])
+__global__ void far_pair_kernel(int64_t np, const int* __restrict__ pairs, const double* __restrict__ B, int M,
+                                const double* __restrict__ mom, double* __restrict__ Fp) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= np * 2 * M) return;
+  const int64_t p = t / (2 * M);
+  const int r = (int)(t % (2 * M));
+  const double* Bp = B + p * M * M;
+  double s = 0.0;
+  if (r < M) {
+    const double* mb = mom + (int64_t)pairs[2 * p + 1] * M;
+    for (int b = 0; b < M; ++b) s = fma(Bp[(int64_t)r * M + b], mb[b], s);
+  } else {
+    const int c = r - M;
+    const double* ma = mom + (int64_t)pairs[2 * p] * M;
+    for (int a = 0; a < M; ++a) s = fma(Bp[(int64_t)a * M + c], ma[a], s);
+  }
+  Fp[t] = s;
+}
+// F[node] = sum over its pair list (as first node, pair order, then as second node, pair order)
+__global__ void far_gather_kernel(int64_t nn, const int* __restrict__ off, const int* __restrict__ lst, int M,
+                                  const double* __restrict__ Fp, double* __restrict__ F) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nn * M) return;
+  const int64_t nd = t / M;
+  const int a = (int)(t % M);
+  double s = 0.0;
+  for (int k = off[nd]; k < off[nd + 1]; ++k) {
+    const int e = lst[k];                  // 2 p + role
+    s += Fp[(int64_t)(e >> 1) * 2 * M + (e & 1) * M + a];
+  }
+  F[t] = s;
+}
+
+// downward: one thread per (child, alpha): F[child] += S^T F[parent]
+template <int D>
+__global__ void down_kernel(const int* __restrict__ nodes, int cnt, const int* __restrict__ parent,
+                            const double* __restrict__ shift, int m, int M, double* __restrict__ F) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)cnt * M) return;
+  const int c = nodes[t / M], a = (int)(t % M);
+  F[(int64_t)c * M + a] += shift_apply_fast<D>(shift + (int64_t)c * D * m * m, F + (int64_t)parent[c] * M, m, a, true);
+}
+
+// y[i] = y_near[i] - C * basis_coef[i, :] . F[leaf(i)]
+__global__ void eval_kernel(int64_t n, const int* __restrict__ leaf_of_dof, const double* __restrict__ bc, int M,
+                            const double* __restrict__ F, double negC, double* __restrict__ y,
+                            double* __restrict__ yfar) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* f = F + (int64_t)leaf_of_dof[i] * M;
+  double s = 0.0;
+  for (int a = 0; a < M; ++a) s = fma(bc[i * M + a], f[a], s);
+  const double v = negC * s;
+  yfar[i] = v;
+  y[i] += v;
+}
+
+// The whole far field in ONE cooperative launch (small / medium operators, e.g. 1D at c2: ~2k
+// nodes, M <= 12): the same phases and accumulation orders as the kernels above, separated by
+// grid-wide barriers instead of ~2 x depth + 4 launches.
 // one level group of the upward pass inside a block: mom[p] += S_c mom[c] over both children
 template <int D>
 __device__ __forceinline__ void up_group(const int* __restrict__ nodes, int cnt, const int* __restrict__ children,
