@@ -255,6 +255,10 @@ int32_t fl_cluster_far_at_points(fl_cluster* C, const double* u, int64_t npts, c
                                  const int64_t* owner, double* out);
 /* the device far blocks (npairs, M, M) */
 int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out);
+/* y = A x on device pointers, enqueued on `stream` (NULL: the default stream) without a host
+ * synchronisation — the matvec inside the cluster Jacobi-PCG (solve.py:112-214 with the
+ * operator's matvec, cluster.py:417-456).  One matvec per operator at a time. */
+int32_t fl_cluster_matvec_async(fl_cluster* C, const double* x, double* y, void* stream);
 void fl_cluster_free(fl_cluster* C);
 /* Near part of the dual-tree boundary flux at the cell nodes (boundary_flux_at_nodes,
  * cluster.py:586-592; 2D): out[p] = sum over the edges eid[eoff[g]:eoff[g+1]] of the point's group g

@@ -20,7 +20,7 @@ EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_coun
            "fl_assemble_dense_host", "fl_finish_polygon_mesh", "fl_build_dofmap", "fl_cell_rule_nodes",
            "fl_load_vector", "fl_assemble_near_field", "fl_sparse_info", "fl_sparse_to_host", "fl_sparse_free",
            "fl_debug_ring_tail", "fl_cluster_create", "fl_cluster_matvec", "fl_cluster_far_blocks", "fl_cluster_free",
-           "fl_cluster_strong_form", "fl_cluster_far_at_points", "fl_boundary_flux_near",
+           "fl_cluster_strong_form", "fl_cluster_far_at_points", "fl_boundary_flux_near", "fl_cluster_matvec_async",
            "fl_dense_from_host",
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_rows", "fl_dense_diag", "fl_matvec",
@@ -122,6 +122,7 @@ def load():
         "fl_cluster_far_blocks": (C.c_int32, [vp, vp]),
         "fl_cluster_free": (None, [vp]),
         "fl_cluster_far_at_points": (C.c_int32, [vp, vp, C.c_int64, vp, vp, vp]),
+        "fl_cluster_matvec_async": (C.c_int32, [vp, vp, vp, vp]),
         "fl_boundary_flux_near": (C.c_int32, [C.c_int32, C.c_double, C.c_int64, vp, C.c_int64, vp, vp, vp,
                                               C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp]),
         "fl_cluster_strong_form": (C.c_int32, [vp, P(fl_mesh), P(fl_dofmap), C.c_double, vp, C.c_int64, vp, vp, vp,

@@ -1112,6 +1112,17 @@ int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_f
   FL_CATCH
 }
 
+int32_t fl_cluster_matvec_async(fl_cluster* C, const double* x, double* y, void* stream) {
+  FL_TRY
+  if (!C || !x || !y) return fl::api_fail(FL_E_ARG, "null argument");
+  FL_CUDA(cudaSetDevice(C->device));
+  cudaStream_t st = (cudaStream_t)stream;             // NULL: the legacy default stream
+  fl::StreamScope scope(st);
+  fl::cluster_matvec_dev(C, x, y, C->yfar.p, st);
+  return FL_OK;
+  FL_CATCH
+}
+
 int32_t fl_cluster_strong_form(fl_cluster* C, const fl_mesh* mesh, const fl_dofmap* dofmap, double s,
                                const double* u, int64_t q, const double* X, const int64_t* cell_leaf,
                                const int64_t* near_off, const int64_t* near_val, const int64_t* ncell_off,

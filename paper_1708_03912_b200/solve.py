@@ -124,9 +124,10 @@ def _pcg_cluster(op, b, precond, tol, max_iter):
             self.cop = cop
 
         def matvec(self, p_full, out_local):
-            torch.cuda.current_stream().synchronize()      # the operator runs on its own stream
-            _lib.check(self.lib.fl_cluster_matvec(self.cop.handle, C.c_void_p(p_full.data_ptr()),
-                                                  C.c_void_p(out_local.data_ptr()), None, 1))
+            # enqueued on torch's current stream, no host synchronisation
+            _lib.check(self.lib.fl_cluster_matvec_async(self.cop.handle, C.c_void_p(p_full.data_ptr()),
+                                                        C.c_void_p(out_local.data_ptr()),
+                                                        C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 
     b = np.ascontiguousarray(b, dtype=np.float64)
     n = len(b)
