@@ -2,17 +2,21 @@
 """Benchmark of the dense fractional-Laplacian hot path on B200.
 
 Metric (BASELINE.json): element-pair quadratures/s of the dense assembly, with the dense
-matvec GB/s (and the CG solve) reported beside it, against the FP64 / HBM rooflines.
+matvec GB/s and the Jacobi-PCG solve reported beside it, against the FP64 / HBM rooflines.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-A step = one full dense assembly (assembly.py:1059-1104) of the configuration: every
-element pair K x K~ (identical, touching, disjoint cross, ordered tail, boundary) on the
-device, timed with CUDA events on the launching stream.  N > 1: rows are sharded by
-contiguous DoF blocks (owner computes, no collective in the assembly); value = total pairs /
-max-over-ranks time (strong scaling: the mesh is fixed).  After the timed steps: 100
-matvecs with x ~ U(-1,1) (seed 0) and one Jacobi-PCG to 1e-10 (sharded CG with NCCL when
-N > 1).  `--impl reference` times the CPU oracle port of the reference (oracle/) on a bounded
+Workload: BASELINE configs[4] = c5 (2D unit square 256x256, s = 1/2, n = 65025, A = 33.8 GB),
+the largest configuration that fits one GPU (configs[1] = c2 is timed too, as `extra.c2`).
+A step = one full dense assembly (assembly.py:1059-1104) of the configuration: every element
+pair K x K~ (identical, touching, disjoint cross, ordered tail, boundary) on the device, inputs
+resident, timed with CUDA events on the launching stream.  N > 1 (`--gpus N` re-launches itself
+under torch.distributed.run when WORLD_SIZE is unset): rank g assembles the DoF row block
+shard_rows(n, N)[g] (owner computes, no collective); value = the whole matrix's pairs / max-over-
+ranks time (strong scaling: the mesh is fixed).  After the timed steps: 100 matvecs with
+x ~ U(-1,1) (seed 0), Jacobi-PCG to 1e-8 (c5) through the sharded solver (NCCL all-gathers when
+N > 1), and the end-to-end public-API path (host mesh in -> assemble -> load_vector -> pcg -> x
+to host).  `--impl reference` times the CPU oracle port of the reference (oracle/) on a bounded
 sample of the same workload on the host cores.
 """
 from __future__ import annotations
@@ -20,6 +24,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,13 +43,16 @@ CONFIG_TEXT = {
     "c3": "2D unit square 64x64 SW-NE, s=0.5 (n=3969)",
     "c4a": "2D unit square 128x128 SW-NE, s=0.25 (n=16641)",
     "c4b": "2D unit square 128x128 SW-NE, s=0.75 (n=16129)",
-    "c5": "2D unit square 256x256 SW-NE, s=0.5 (n=65025)",
+    "c5": "2D unit square 256x256 SW-NE, s=0.5 (n=65025, A = 33.8 GB fp64)",
 }
+CG_TOL = {"c1": 1e-10, "c2": 1e-10, "c3": 1e-10, "c4a": 1e-10, "c4b": 1e-10, "c5": 1e-8}   # BASELINE.json configs
 # per-evaluation algorithmic fp64 FLOPs excluding the power and the
 # executed FLOPs of the specialised power r2^ex (ncu-measured)
 ALG_FLOPS = {(1, "tail"): 4, (1, "cross"): 6, (2, "tail"): 7, (2, "cross"): 11}
 POW_FLOPS = {6: 11, 8: 8, 10: 11, 12: 9, 14: 12, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh (2D)
 POW_FLOPS_1D = {6: 9, 8: 9, 10: 10, 0: 60}                  # = kpow_abs_flops() (1D far field)
+KERNEL_NAME = {("tail", 1): "tail1d_kernel", ("tail", 2): "tail_kernel", ("cross", 1): "cross1d_tile_kernel",
+               ("cross", 2): "cross_tile_kernel"}
 
 
 def peaks():
@@ -69,7 +77,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -103,13 +111,17 @@ class ClockSampler:
 
 
 def committed_traffic(cfg, kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/r01/traffic.json,
-    dram__bytes_read.sum + dram__bytes_write.sum), or None when that kernel was not captured."""
-    try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")) as f:
-            return json.load(f).get(cfg, {}).get(kernel)
-    except (OSError, ValueError):
-        return None
+    """DRAM bytes per launch of `kernel` from the committed ncu captures (profiles/*/traffic.json,
+    dram__bytes_read.sum + dram__bytes_write.sum; the newest round that has it), or None."""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                v = json.load(f).get(cfg, {}).get(kernel)
+            if v is not None:
+                return {"bytes": v, "source": "profiles/%s/traffic.json" % rnd}
+        except (OSError, ValueError):
+            continue
+    return None
 
 
 def dist_env():
@@ -119,8 +131,32 @@ def dist_env():
     return world, rank, local
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(n):
+    """`--gpus N` without a torch.distributed launcher: re-run this script as N NCCL ranks."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # stderr shows nranks / NVLS for the record
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+# ----------------------------------------------------------------------------- CPU arm
 def _cpu_worker(job):
-    """One host process of the CPU baseline: the oracle port on its share of target cells."""
+    """One host process of the CPU baseline: the oracle port (numpy restatement of the reference's
+    assemble_dense, pinned to its outputs) on its share of target cells — for each cell K every
+    contribution the reference computes for K: identical pair, ordered tail pairs (Psi_K), the
+    boundary flux at K's nodes, the unordered disjoint cross pairs (K, K2 > K), the touching pairs
+    (K, K2 > K) and the singular (K, edge) pairs, all scattered into a dense row buffer with
+    np.add.at as the reference does (rows folded modulo 64 so the buffer is (64, n) instead of (n, n);
+    the scatter work is the reference's)."""
     cfg, budget_s, w, nw = job
     try:
         import threadpoolctl
@@ -132,24 +168,64 @@ def _cpu_worker(job):
     mesh, s = M.baseline_mesh(cfg)
     dm = M.DofMap(mesh, s)
     o = O.Oracle(mesh, dm, s)
+    g = o.g
     cells = np.random.default_rng(0).permutation(mesh.num_cells)[w::nw]
-    A = np.zeros((1, dm.n))
-    rowmap = np.full(dm.n, -1, np.int64)
+    R = 64
+    A = np.zeros((R, dm.n))
+    rowmap = np.arange(dm.n, dtype=np.int64) % R
+    bitems = {}
+    if len(g.be):
+        for e in range(len(g.be)):
+            for c in np.unique(np.concatenate([g.patch(v) for v in g.be[e]])):
+                bitems.setdefault(int(c), []).append(e)
+    extra = 0
     t0 = time.perf_counter()
     done = 0
     for K in cells:
-        o.psi(int(K))                                   # ordered tail pairs of K
-        o.add_cell(int(K), A, rowmap, symmetric=True)   # unordered cross pairs (K, K2 > K) + identical
+        K = int(K)
+        o.add_cell(K, A, rowmap, symmetric=True)            # identical + tail + flux + cross (K2 > K)
+        for K2 in g.neigh(K):                               # touching pairs (K, K2 > K), assembly.py:644-690
+            if K2 <= K:
+                continue
+            vA, vB = list(g.cells[K]), list(g.cells[K2])
+            com = sorted(set(vA) & set(vB))
+            vK = com + [v for v in vA if v not in com]
+            vK2 = com + [v for v in vB if v not in com]
+            topo = "cv" if (g.d == 1 or len(com) == 1) else "ce"
+            locs = vK + ([vK2[2]] if topo == "ce" else vK2[1:]) if g.d == 2 else [com[0], vK[1], vK2[1]]
+            k = int(O.order_touch(min(g.h[K], g.h[K2]), g.n, s, g.d, o.p))
+            T = O.touching_matrix(topo, g.V[vK], g.V[vK2], s, k)
+            dofs = g.v2d[locs]
+            ok = dofs >= 0
+            np.add.at(A, (rowmap[dofs[ok]][:, None], dofs[ok][None, :]), o.C * T[np.ix_(ok, ok)])
+            extra += 1
+        for e in bitems.get(K, ()):                          # singular (cell, edge) pairs, :784-857
+            ev = list(g.be[e])
+            cv = list(g.cells[K])
+            shared = sorted(set(ev) & set(cv))
+            if g.d == 1 or len(shared) == 2:
+                topo, order, pe = "eoc", (ev + [v for v in cv if v not in ev]) if g.d == 2 else \
+                    [ev[0]] + [v for v in cv if v != ev[0]], ev if g.d == 2 else [ev[0]]
+            else:
+                sv = shared[0]
+                topo, order, pe = "te", [sv] + [v for v in cv if v != sv], [sv] + [v for v in ev if v != sv]
+            kb = int(O.order_touch(g.h[K], g.n, s, g.d, o.p, boundary=True))
+            van = (0 if s < 0.5 else 2) if topo == "eoc" else 0
+            B = O.boundary_matrix(topo, g.V[order], g.V[pe], -g.bn[e], s, kb, van)
+            dofs = g.v2d[order]
+            ok = dofs >= 0
+            np.add.at(A, (rowmap[dofs[ok]][:, None], dofs[ok][None, :]), o.C / (2 * s) * B[np.ix_(ok, ok)])
+            extra += 1
+        extra += 1 + len(g.be)                               # identical pair + nb boundary-flux pairs
         done += 1
         if time.perf_counter() - t0 > budget_s:
             break
-    return o.stats["pairs"], time.perf_counter() - t0, done
+    return o.stats["pairs"] + extra, time.perf_counter() - t0, done
 
 
-def cpu_sample(cfg, budget_s=12.0, procs=None):
+def cpu_sample(cfg, budget_s=10.0, procs=None):
     """Oracle port on every host core (one process per core, BLAS pinned to one thread each):
-    owner-computes rows of random target cells of the same mesh for ~budget_s seconds; returns
-    the aggregate pairs/s and the description."""
+    rows of random target cells of the same mesh for ~budget_s seconds; aggregate pairs/s."""
     import multiprocessing as mp
     if procs is None:
         try:
@@ -168,10 +244,17 @@ def cpu_sample(cfg, budget_s=12.0, procs=None):
     return pairs / dt, dict(cells=sum(r[2] for r in res), seconds=dt, pairs=pairs, threads=procs)
 
 
+def cpu_sample_text(info, cfg):
+    return ("oracle port (numpy restatement of assemble_dense, pinned to the reference's outputs), %d host "
+            "processes, %d random target cells of %s: per cell its identical, ordered tail, boundary-flux, "
+            "unordered cross (K2 > K), touching and boundary-singular pairs with the dense np.add.at scatter; "
+            "%.1f s" % (info["threads"], info["cells"], cfg, info["seconds"]))
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
-        return
+        return 0
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
@@ -179,18 +262,58 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(v)
     v = float(np.median(vals))
-    sample = ("oracle port (numpy restatement of assemble_dense), %d host processes, on %d random target "
-              "cells of %s: their ordered tail pairs + unordered cross pairs, %.1f s per step"
-              % (info["threads"], info["cells"], args.config, info["seconds"]))
     line = {"metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": 0, "steps": args.steps,
             "ms_per_step": 1e3 * info["seconds"],
             "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "impl": "reference",
-            "dtype": "f64", "data": "synthetic", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE mesh, f=1)", "vs_baseline": None,
             "config": {"workload": args.config, "mesh": CONFIG_TEXT[args.config]},
             "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": info["threads"], "kind": "port",
-                             "sample": sample},
+                             "sample": cpu_sample_text(info, args.config)},
             "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def roofline_of(stats, d, s, fp64, kind):
+    e4 = int(round(4 * (d + 2 * s))) if s in (0.25, 0.5, 0.75) else 0
+    ms = stats["ms_tail"] if kind == "tail" else (stats["ms_cross_compute"] or stats["ms_cross"])
+    ev = stats["evals_tail"] if kind == "tail" else stats["evals_cross"]
+    fpe = ALG_FLOPS[(d, kind)] + (POW_FLOPS_1D if d == 1 else POW_FLOPS).get(e4, 60)
+    ach = ev * fpe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    return {"bound": "fp64", "kernel": KERNEL_NAME[(kind, d)], "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+            "frac": ach / fp64 if fp64 else None, "flops_per_eval": fpe, "evals_per_launch": ev,
+            "ms_per_launch": ms}
+
+
+def pair_count(stats):
+    return (stats["pairs_identical"] + stats["pairs_touching"] + stats["pairs_cross"] + stats["pairs_tail"]
+            + stats["pairs_boundary_singular"] + stats["pairs_boundary_flux"])
+
+
+def time_assembly(assemble, steps, warmup, stream, flush, world, dist):
+    import torch
+    for _ in range(warmup):
+        op = assemble()
+        op.free()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times, op = [], None
+    for i in range(steps):
+        if op is not None:
+            op.free()
+        flush.fill_(float(i))                       # L2 flush between timed steps (not timed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        op = assemble()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    return op, times
 
 
 def main():
@@ -198,22 +321,29 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIG_TEXT))
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIG_TEXT))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--matvecs", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-near", action="store_true", help="skip the near-field (cluster path) timing")
-    ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the c2 line and the cluster-path timings")
+    ap.add_argument("--ref-budget", type=float, default=6.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
 
+    import ctypes as C
     import torch
     import torch.distributed as dist
     from paper_1708_03912_b200 import _lib, mesh as M, assembly as A, solve as S, distributed as D
-
-    world, rank, local = dist_env()
+    if torch.cuda.device_count() <= local:
+        print(json.dumps({"error": "rank %d needs cuda:%d, %d visible" % (rank, local, torch.cuda.device_count())}))
+        return 1
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -229,200 +359,135 @@ def main():
     rows = D.shard_rows(n, world)
     r0, r1 = rows[rank]
 
+    def maxr(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     def assemble():
         return A.assemble_dense_device(mesh, dm, ker, rows=(r0, r1), device=local, stream=sptr)
 
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")   # > L2 (126 MB)
-    for _ in range(args.warmup):
-        op = assemble()
-        op.free()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    fp64c = C.c_double()
+    _lib.check(lib.fl_probe_fp64_peak(local, C.byref(fp64c)))
+    fp64 = fp64c.value
+
+    # ---------------------------------------------------------------- timed assembly steps
     launches0 = lib.fl_launch_count()
-    times, stats = [], None
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.fill_(float(i))                       # L2 flush between timed steps (not timed)
-            ev[i][0].record(stream)
-            op = assemble()
-            ev[i][1].record(stream)
-            torch.cuda.synchronize()
-            times.append(ev[i][0].elapsed_time(ev[i][1]))
-            stats = op.stats()
-            if i < args.steps - 1:
-                op.free()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    launches = (lib.fl_launch_count() - launches0) // max(args.steps, 1)
-    tot = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms_step = float(tot.item()) / args.steps
-    pairs = (stats["pairs_identical"] + stats["pairs_touching"] + stats["pairs_cross"] + stats["pairs_tail"]
-             + stats["pairs_boundary_singular"] + stats["pairs_boundary_flux"])
+        op, times = time_assembly(assemble, args.steps, args.warmup, stream, flush, world, dist)
+    launches = (lib.fl_launch_count() - launches0) // max(args.steps + args.warmup, 1)
+    stats = op.stats()
+    ms_step = maxr(sum(times)) / args.steps
+    # the whole matrix's element pairs (the classification is global, so every rank reports the
+    # job's counts; a row block is a share of that job)
+    pairs = pair_count(stats)
     value = pairs / (ms_step / 1e3)
+    roof_tail = roofline_of(stats, mesh.d, s, fp64, "tail")
+    roof_cross = roofline_of(stats, mesh.d, s, fp64, "cross")
+    roof = dict(max((roof_tail, roof_cross), key=lambda r: r["ms_per_launch"]))
+    roof["traffic"] = committed_traffic(args.config, roof["kernel"])
+    roof["peak_source"] = "fl_probe_fp64_peak (DFMA chains, this run, same GPU)"
+    other = roof_cross if roof["kernel"] == roof_tail["kernel"] else roof_tail
+    other["traffic"] = committed_traffic(args.config, other["kernel"])
 
-    # roofline of the dominant assembly kernel (fp64 pipe)
-    fp64 = C_double = None
-    import ctypes as C
-    C_double = C.c_double()
-    _lib.check(lib.fl_probe_fp64_peak(local, C.byref(C_double)))
-    fp64 = C_double.value
-    e4 = int(round(4 * (mesh.d + 2 * s))) if s in (0.25, 0.5, 0.75) else 0
-    kern = {"tail": (stats["ms_tail"], stats["evals_tail"]), "cross": (stats["ms_cross"], stats["evals_cross"])}
-    dom = max(kern, key=lambda k: kern[k][0])
-    ms_k, ev_k = kern[dom]
-    fl_per_eval = ALG_FLOPS[(mesh.d, dom)] + (POW_FLOPS_1D if mesh.d == 1 else POW_FLOPS).get(e4, 60)
-    achieved = ev_k * fl_per_eval / (ms_k * 1e-3) / 1e12 if ms_k > 0 else 0.0
-    kname = {("tail", 1): "tail1d_kernel", ("tail", 2): "tail_kernel", ("cross", 1): "cross1d_tile_kernel",
-             ("cross", 2): "cross_tile_kernel"}[(dom, mesh.d)]
-    roofline = {"bound": "fp64", "kernel": kname, "achieved": achieved, "peak": fp64,
-                "unit": "TFLOP/s", "frac": achieved / fp64 if fp64 else None,
-                "traffic": committed_traffic(args.config, kname),
-                "peak_source": "fl_probe_fp64_peak (DFMA chains, this run)",
-                "flops_per_eval": fl_per_eval, "evals_per_launch": ev_k, "ms_per_launch": ms_k}
-
-    # dense matvec GB/s (100 matvecs, x ~ U(-1,1) seed 0), A (> L2) read once per matvec
+    # ---------------------------------------------------------------- dense matvec GB/s
     pk, pk_src = peaks()
-    lda = ((n + 31) // 32) * 32
-    x = torch.zeros(lda, dtype=torch.float64, device="cuda")
-    x[:n] = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
+    blk = D.block_rows(n, world)
+    xg = torch.zeros(world * blk, dtype=torch.float64, device="cuda")
+    xg[:n] = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
     y = torch.zeros(max(r1 - r0, 1), dtype=torch.float64, device="cuda")
     mv = []
     for i in range(args.matvecs + 3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        op.matvec_device(x.data_ptr(), y.data_ptr(), sptr)
+        op.matvec_device(xg.data_ptr(), y.data_ptr(), sptr)
         e1.record(stream)
         torch.cuda.synchronize()
         if i >= 3:
             mv.append(e0.elapsed_time(e1))
-    mv_ms = float(np.median(mv))
-    mv_bytes = 8.0 * (r1 - r0) * n + 8.0 * n + 8.0 * (r1 - r0)
-    mvt = torch.tensor([mv_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(mvt, op=dist.ReduceOp.MAX)
-    mv_gbs = (8.0 * n * n + 16.0 * n) / (float(mvt.item()) * 1e-3) / 1e9
-    matvec = {"gbs": mv_gbs, "ms": float(mvt.item()), "bytes": 8.0 * n * n + 16.0 * n,
-              "traffic": committed_traffic(args.config, "matvec_kernel"),
-              "frac_of_measured_copy_peak": mv_gbs / (pk["hbm_gbs"] * world), "peak_source": pk_src}
+    mv_ms = maxr(float(np.median(mv)))
+    mv_bytes = 8.0 * n * n + 16.0 * n
+    mv_gbs = mv_bytes / (mv_ms * 1e-3) / 1e9
+    matvec = {"gbs": mv_gbs, "ms": mv_ms, "bytes": mv_bytes, "count": args.matvecs,
+              "x": "U(-1,1) seed 0", "traffic": committed_traffic(args.config, "mv_rows_kernel")
+              or committed_traffic(args.config, "matvec_kernel"),
+              "frac_of_measured_copy_peak": mv_gbs / (pk["hbm_gbs"] * world), "peak_gbs": pk["hbm_gbs"] * world,
+              "peak_source": pk_src}
 
-    # CG (Jacobi PCG to 1e-10, solve.py:52-109)
+    # ---------------------------------------------------------------- CG (solve.py:52-109)
     cg = None
+    b = A.load_vector(mesh, dm, 1.0)
+    tol = CG_TOL[args.config]
     if not args.no_cg:
-        b = A.load_vector(mesh, dm, lambda X: np.ones(len(X)))
+        cg = {"tol": tol, "stopping": "sqrt(r.z) <= tol sqrt(r0.z0) (solve.py:96)"}
+        be = D.TorchDeviceBackend(op)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
+        xs, rep = D.pcg_sharded(be, b[r0:r1], op.diag(), rows, n, dist if world > 1 else S._OneRank,
+                                tol=tol, max_iter=10 ** 5)
+        torch.cuda.synchronize()
+        sec = maxr(time.perf_counter() - t0)
+        cg.update({"path": "distributed.pcg_sharded (fl_cg_*, NCCL all-gathers)" if world > 1 else
+                   "distributed.pcg_sharded (fl_cg_*, one rank)", "iterations": rep["iterations"],
+                   "converged": rep["converged"], "seconds": sec,
+                   "ms_per_iteration": 1e3 * sec / max(rep["iterations"], 1)})
         if world == 1:
-            xs, rep = S.pcg(op, b, tol=1e-10, max_iter=10 ** 5)
-            cg = {"iterations": rep.iterations, "seconds": rep.seconds, "converged": rep.converged,
-                  "true_residual": rep.true_residual}
-        else:
-            be = D.TorchDeviceBackend(op, sptr)
-            xs, rep = D.pcg_sharded(be, b[r0:r1], op.diag(), rows, n, dist, tol=1e-10, max_iter=10 ** 5)
-            cg = {"iterations": rep["iterations"], "seconds": time.perf_counter() - t0,
-                  "converged": rep["converged"]}
-        cg["ms_per_iteration"] = 1e3 * cg["seconds"] / max(cg["iterations"], 1)
+            x1, rep1 = S.pcg(op, b, tol=tol, max_iter=10 ** 5)       # fl_pcg: CUDA-graph solver, same kernels
+            cg["fl_pcg"] = {"iterations": rep1.iterations, "seconds": rep1.seconds,
+                            "ms_per_iteration": 1e3 * rep1.seconds / max(rep1.iterations, 1),
+                            "true_residual": rep1.true_residual}
+            cg["sharded_equals_fl_pcg_bitwise"] = bool(np.array_equal(xs.cpu().numpy(), x1))
+    op.free()
 
-    # e2e through the public API with host buffers: assemble_dense -> (n, n) ndarray (N = 1), or
-    # each rank's row block assemble_dense_device(rows) -> to_host (N > 1); max over ranks
+    # ---------------------------------------------------------------- end to end, public API
     e2e = None
-    if 8.0 * (r1 - r0) * n <= 4e9:     # host copy of the rows must fit comfortably in pinned RAM
+    if not args.no_e2e:
         Mh = A._lib.Marshal(mesh, dm, ker, None)
         tdir, tdata, _ = A._tables(mesh, dm, s, None)
         h2d = (Mh.vertices.nbytes + Mh.cells.nbytes + Mh.bedges.nbytes + Mh.bnormals.nbytes + Mh.v2d.nbytes
                + tdir.nbytes + tdata.nbytes)
-        out = torch.empty((r1 - r0, n), dtype=torch.float64, pin_memory=True).numpy()
         et = []
-        for i in range(max(2, args.steps)):
+        for i in range(max(1, args.e2e_steps)):
             flush.fill_(float(i))
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
+            ope = A.assemble_dense_device(mesh, dm, ker, rows=(r0, r1), device=local)
+            bb = A.load_vector(mesh, dm, lambda X: np.ones(len(X)))          # f evaluated on the host
             if world == 1:
-                A.assemble_dense(mesh, dm, ker, n_limit=10 ** 7, out=out)
+                xe, repe = S.pcg(ope, bb, tol=tol, max_iter=10 ** 5)
             else:
-                ope = A.assemble_dense_device(mesh, dm, ker, rows=(r0, r1), device=local, stream=sptr)
-                ope.to_host(out)
-                ope.free()
-            tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            et.append(float(tt.item()))
-        e2e = {"value": pairs / float(np.median(et)), "unit": "pairs/s", "h2d_bytes_per_step": int(h2d * world),
-               "d2h_bytes_per_step": int(8 * n * n), "seconds_per_step": float(np.median(et))}
+                xl, repe = D.pcg_sharded(D.TorchDeviceBackend(ope), bb[r0:r1], ope.diag(), rows, n, dist, tol=tol,
+                                         max_iter=10 ** 5)
+                xe = xl.cpu().numpy()
+            torch.cuda.synchronize()
+            et.append(maxr(time.perf_counter() - t0))
+            ope.free()
+        sec = float(np.median(et))
+        q = 16 if mesh.d == 2 else 6
+        e2e = {"value": pairs / sec, "unit": "pairs/s", "seconds_per_step": sec, "steps": len(et),
+               "path": "host mesh -> assemble_dense_device -> load_vector -> pcg (tol %g) -> x on the host" % tol,
+               # H2D: mesh + dofmap + quadrature tables (assembly), the same + f at the rule nodes
+               # (load_vector), b and the diagonal (pcg); D2H: b (load_vector) and x
+               "h2d_bytes_per_step": int(world * (2 * h2d + 8 * mesh.num_cells * q + 8 * n + 8 * (r1 - r0))),
+               "d2h_bytes_per_step": int(world * 8 * n + 8 * n),
+               "copies_declared": True}
 
-    # near-field (cluster path) assembly of the same mesh, SPEC defaults (leaf cap 8 / 16, eta 1):
-    # assemble_near_field through the public API (host tree + partition excluded, CSR returned to
-    # the host included), median of 3 after one warm-up
-    near = None
-    if rank == 0 and world == 1 and not args.no_near:
-        from paper_1708_03912_b200 import cluster as CL
-        th = time.perf_counter()
-        tree = CL.build_tree(mesh, dm, 8 if mesh.d == 1 else 16)
-        far_nodes, near_nodes = CL.admissible_partition(tree, 1.0)
-        ns = CL.NearStructure(mesh, dm, tree, near_nodes)
-        host_s = time.perf_counter() - th
-        nts = []
-        for i in range(4):
-            t0 = time.perf_counter()
-            An = A.assemble_near_field(mesh, dm, ker, ns)
-            nts.append(time.perf_counter() - t0)
-        near = {"ms": 1e3 * float(np.median(nts[1:])), "nnz": int(An.nnz), "leaf_cap": 8 if mesh.d == 1 else 16,
-                "eta": 1.0, "near_leaf_pairs": int(len(ns.nl_pairs)), "far_node_pairs": int(len(far_nodes)),
-                "host_tree_partition_s": host_s}
-        # the whole cluster path (compress -> H-matrix matvec -> residual strong form), m = choose_order
-        try:
-            from paper_1708_03912_b200 import adapt as AD
-
-            class _St:
-                pass
-            st_ = _St()
-            st_.h_min, st_.dim = float(mesh.cell_diameters().min()), mesh.d
-            mo = CL.choose_order(st_)
-            t0 = time.perf_counter()
-            cop = CL.compress(mesh, dm, ker, tree, 1.0, mo)
-            comp_s = time.perf_counter() - t0
-            xv = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
-            yv = torch.empty_like(xv)
-            cev = []
-            for i in range(23):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                _lib.check(lib.fl_cluster_matvec(cop.handle, C.c_void_p(xv.data_ptr()), C.c_void_p(yv.data_ptr()),
-                                                 None, 1))
-                e1.record(stream)
-                torch.cuda.synchronize()
-                if i >= 3:
-                    cev.append(e0.elapsed_time(e1))
-            X4, _ = AD.cell_nodes(mesh, 4)
-            AD.strong_form_at(xv.cpu().numpy(), mesh, dm, cop, X=X4)
-            t0 = time.perf_counter()
-            AD.strong_form_at(xv.cpu().numpy(), mesh, dm, cop, X=X4)
-            sf_ms = 1e3 * (time.perf_counter() - t0)
-            bc = A.load_vector(mesh, dm, 1.0)
-            t0 = time.perf_counter()
-            _, crep = S.pcg(cop, bc, tol=1e-10, max_iter=10 ** 5)
-            cg_s = time.perf_counter() - t0
-            near["cluster"] = {"cheb_order": mo, "far_pairs": int(len(cop.far_pairs)), "compress_s": comp_s,
-                               "matvec_us": 1e3 * float(np.median(cev)), "strong_form_ms": sf_ms,
-                               "cg_iterations": crep.iterations, "cg_ms_per_iteration": 1e3 * cg_s / max(crep.iterations, 1)}
-            cop.free()
-        except Exception as exc:     # reported, never fatal for the headline line
-            near["cluster"] = {"error": repr(exc)[:200]}
+    # ---------------------------------------------------------------- extra lines (rank 0, N = 1)
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra and args.config != "c2":
+        extra["c2"] = extra_c2(lib, stream, flush, fp64)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, info = cpu_sample(args.config)
         cpu = {"value": v, "unit": "pairs/s", "cores": info["threads"], "kind": "port",
-               "sample": "oracle port, %d host processes, on %d random target cells of %s (their ordered "
-                         "tail + unordered cross pairs), %.1f s" % (info["threads"], info["cells"], args.config,
-                                                                   info["seconds"])}
+               "sample": cpu_sample_text(info, args.config)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
@@ -430,20 +495,41 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE mesh, f=1)",
                 "config": {"workload": args.config, "mesh": CONFIG_TEXT[args.config], "n": n,
                            "cells": mesh.num_cells, "pairs_per_step": pairs,
-                           "parallelism": "rows%d" % world, "l2": "flushed (256 MB write) between steps",
-                           "phases_ms": {k: stats[k] for k in ("ms_prep", "ms_singular", "ms_tail", "ms_flux",
-                                                               "ms_tiles", "ms_cross", "ms_discover", "ms_near",
-                                                               "ms_cross_compute", "ms_local", "ms_total")},
+                           "parallelism": "rows%d" % world, "row_block": [r0, r1],
+                           "l2": "flushed (256 MB write) between steps; A (%.1f GB) > L2" % (8e-9 * n * n),
+                           "phases_ms_rank0": {k: stats[k] for k in ("ms_prep", "ms_singular", "ms_tail", "ms_flux",
+                                                                     "ms_tiles", "ms_cross", "ms_discover", "ms_near",
+                                                                     "ms_cross_compute", "ms_local", "ms_total")},
                            "near_pairs": stats["near_pairs"], "evals_tail": stats["evals_tail"],
                            "evals_cross": stats["evals_cross"]},
-                "roofline": roofline, "matvec": matvec, "cg": cg, "e2e": e2e, "near_field": near,
-                "cpu_baseline": cpu,
+                "roofline": roof, "roofline_second": other, "matvec": matvec, "cg": cg, "e2e": e2e,
+                "cpu_baseline": cpu, "extra": extra or None,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
-    op.free()
     if world > 1:
         dist.destroy_process_group()
+    return 0
+
+
+def extra_c2(lib, stream, flush, fp64, steps=5):
+    """configs[1] (c2, 1D graded, s = 3/4): device-timed assembly + its roofline, matvec, CG."""
+    import torch
+    from paper_1708_03912_b200 import mesh as M, assembly as A, solve as S
+    mesh, s = M.baseline_mesh("c2")
+    dm = M.DofMap(mesh, s)
+    ker = A.FractionalKernel(1, s)
+    sptr = stream.cuda_stream
+    op, times = time_assembly(lambda: A.assemble_dense_device(mesh, dm, ker, stream=sptr), steps, 2, stream, flush,
+                              1, None)
+    st = op.stats()
+    ms = float(np.mean(times))
+    out = {"mesh": CONFIG_TEXT["c2"], "ms_per_step": ms, "value": pair_count(st) / (ms * 1e-3), "unit": "pairs/s",
+           "roofline": roofline_of(st, 1, s, fp64, "tail"), "roofline_cross": roofline_of(st, 1, s, fp64, "cross")}
+    x, rep = S.pcg(op, A.load_vector(mesh, dm, 1.0), tol=1e-10, max_iter=10 ** 5)
+    out["cg"] = {"iterations": rep.iterations, "ms_per_iteration": 1e3 * rep.seconds / max(rep.iterations, 1)}
+    op.free()
+    return out
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

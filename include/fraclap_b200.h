@@ -168,6 +168,10 @@ int32_t fl_assemble_dense_host(const fl_mesh* mesh, const fl_dofmap* dofmap,
 /* Wrap an existing dense host matrix (n x n, row-major) as a device operator — the
  * `Ad = np.asarray(A)` branch of LinearOperatorHandle.from_matrix (solve.py:31-32). */
 int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out);
+/* rows [row_begin, row_end) of an (n x n) host matrix (row-major, (row_end - row_begin) x n) as a
+ * row-block operator, e.g. one rank's block of a matrix assembled elsewhere */
+int32_t fl_dense_from_host_rows(const double* rows, int64_t n, int64_t row_begin, int64_t row_end,
+                                int32_t device, fl_dense** out);
 
 void fl_dense_free(fl_dense* A);
 int32_t fl_dense_info(const fl_dense* A, int64_t* n, int64_t* row_begin, int64_t* row_end,
@@ -257,7 +261,11 @@ int32_t fl_cluster_far_at_points(fl_cluster* C, const double* u, int64_t npts, c
 int32_t fl_cluster_far_blocks(const fl_cluster* C, double* blocks_out);
 /* y = A x on device pointers, enqueued on `stream` (NULL: the default stream) without a host
  * synchronisation — the matvec inside the cluster Jacobi-PCG (solve.py:112-214 with the
- * operator's matvec, cluster.py:417-456).  One matvec per operator at a time. */
+ * operator's matvec, cluster.py:417-456).  One matvec per operator at a time.  The call is
+ * ordered after all work pending on the operator's internal stream, and later synchronous calls
+ * and fl_cluster_free are ordered after it (event joins), so no host sync is needed around it.
+ * x and y must not alias (the fused kernel writes y while other blocks still read x).  The
+ * caller's current device is restored on return. */
 int32_t fl_cluster_matvec_async(fl_cluster* C, const double* x, double* y, void* stream);
 void fl_cluster_free(fl_cluster* C);
 /* Near part of the dual-tree boundary flux at the cell nodes (boundary_flux_at_nodes,
@@ -302,15 +310,46 @@ int32_t fl_matvec_async(const fl_dense* A, const double* x_dev, double* y_dev, v
 int32_t fl_pcg(const fl_dense* A, const double* b, const double* x0, double tol,
                int64_t max_iter, int32_t precond, double* x, fl_solve_report* report);
 
-/* Fused CG vector step on device pointers for the sharded solver (rows of one shard):
- *   x += alpha p; r -= alpha Ap; z = minv * r; partial[0] = r.z   (deterministic)    */
-int32_t fl_cg_update_async(int64_t m, double alpha, double* x, double* r, double* z,
-                           const double* p, const double* Ap, const double* minv,
-                           double* partial_dev, void* stream);
-/* partial_dev[0] = a.b over m entries (deterministic fixed-order reduction) */
-int32_t fl_dot_async(int64_t m, const double* a, const double* b, double* out_dev, void* stream);
-/* p = z + beta p */
-int32_t fl_xpby_async(int64_t m, const double* z, double beta, double* p, void* stream);
+/* Row-block sharded Jacobi-PCG (solve.py:52-109 over row blocks): the
+ * per-rank device state and steps; the exchanges between the steps (all-gather of the search
+ * direction and of the chunk sums) are the caller's (torch.distributed / NCCL).  Rank g owns
+ * rows [g*block_rows, min(n, (g+1)*block_rows)); block_rows is a multiple of 512.  Every
+ * reduction is over fixed global chunks of 512 entries and the gathered chunk sums are folded
+ * in global order, so the iterates are bitwise the same for any number of ranks and equal to
+ * fl_pcg's.  Scalars stay on the device; fl_cg_poll reads them (one host sync).  Vector
+ * arguments are device pointers of length >= block_rows (zero padded); p_full >= world*block_rows.
+ * One iteration:  [diag] gather(p) [rest] gather(parts) [alpha_update] gather(parts) [beta_xpby]. */
+typedef struct fl_cg fl_cg;
+typedef struct fl_cg_status {
+  int64_t iterations;
+  double rz, norm0;                 /* current r.z and sqrt|r0.z0| */
+  int32_t done, converged, error, pad_;   /* error 1: p^T A p <= 0 (solve.py:87-88) */
+} fl_cg_status;
+int32_t fl_cg_create(int64_t n, int64_t m_local, int64_t block_rows, int32_t world, int32_t rank, double tol,
+                     int64_t max_iter, int32_t device, void* stream, fl_cg** out);
+/* the rank's chunk sums (chunks_per_rank doubles) and the gathered ones (world * chunks_per_rank) */
+int32_t fl_cg_buffers(fl_cg* S, double** local_parts, double** all_parts, int64_t* chunks_per_rank);
+/* write this rank's chunk sums into a caller-owned device buffer (chunks_per_rank doubles, e.g. the
+ * input of the caller's all-gather) instead of the state's own; NULL restores the default */
+int32_t fl_cg_bind_parts(fl_cg* S, double* local_parts);
+/* z = minv r, p = z; local chunk sums of r.z (solve.py:75-77) */
+int32_t fl_cg_begin(fl_cg* S, const double* r, const double* minv, double* z, double* p, void* stream);
+/* rz, norm0 from the gathered chunk sums; done at once if b = 0 */
+int32_t fl_cg_init(fl_cg* S, const double* all_parts, void* stream);
+/* the diagonal block's chunks of A[rows, :] p from the rank's own slice of p (overlaps the all-gather) */
+int32_t fl_cg_matvec_diag(fl_cg* S, const fl_dense* A, const double* p_local, void* stream);
+/* Ap = A[rows, :] p_full (diagonal chunks from fl_cg_matvec_diag when world > 1); local chunk sums of p.Ap */
+int32_t fl_cg_matvec_rest(fl_cg* S, const fl_dense* A, const double* p_full, const double* p_local, double* Ap,
+                          void* stream);
+/* local chunk sums of a.b (for operators whose matvec is not an fl_dense, e.g. the cluster operator) */
+int32_t fl_cg_dot_parts(fl_cg* S, const double* a, const double* b, void* stream);
+/* alpha = rz / pAp (pAp folded from all_parts); x += alpha p; r -= alpha Ap; z = minv r; local sums of r.z */
+int32_t fl_cg_alpha_update(fl_cg* S, const double* all_parts, double* x, double* r, double* z, const double* p,
+                           const double* Ap, const double* minv, void* stream);
+/* rz_new folded from all_parts; stopping rule of solve.py:96; beta; p = z + beta p */
+int32_t fl_cg_beta_xpby(fl_cg* S, const double* all_parts, const double* z, double* p, void* stream);
+int32_t fl_cg_poll(fl_cg* S, fl_cg_status* status, void* stream);
+void fl_cg_free(fl_cg* S);
 
 /* ------------------------------------------------------------- parity / diagnostics
  * Per-pair Gauss orders exactly as select_order computes them (quadrature.py:138-179):

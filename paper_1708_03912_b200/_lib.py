@@ -21,10 +21,12 @@ EXPORTS = ["fl_abi_version", "fl_last_error", "fl_device_count", "fl_launch_coun
            "fl_load_vector", "fl_assemble_near_field", "fl_sparse_info", "fl_sparse_to_host", "fl_sparse_free",
            "fl_debug_ring_tail", "fl_cluster_create", "fl_cluster_matvec", "fl_cluster_far_blocks", "fl_cluster_free",
            "fl_cluster_strong_form", "fl_cluster_far_at_points", "fl_boundary_flux_near", "fl_cluster_matvec_async",
-           "fl_dense_from_host",
+           "fl_dense_from_host", "fl_dense_from_host_rows",
            "fl_dense_free",
            "fl_dense_info", "fl_dense_stats", "fl_dense_to_host", "fl_dense_rows", "fl_dense_diag", "fl_matvec",
-           "fl_matvec_async", "fl_pcg", "fl_cg_update_async", "fl_dot_async", "fl_xpby_async",
+           "fl_matvec_async", "fl_pcg", "fl_cg_create", "fl_cg_buffers", "fl_cg_bind_parts", "fl_cg_begin", "fl_cg_init",
+           "fl_cg_matvec_diag", "fl_cg_matvec_rest", "fl_cg_dot_parts", "fl_cg_alpha_update", "fl_cg_beta_xpby",
+           "fl_cg_poll", "fl_cg_free",
            "fl_debug_orders", "fl_debug_order_hist", "fl_debug_kpow", "fl_probe_fp64_peak", "fl_debug_touching"]
 
 
@@ -49,6 +51,11 @@ class fl_order_params(C.Structure):
 
 class fl_tables(C.Structure):
     _fields_ = [("dir", C.c_void_p), ("data", C.c_void_p), ("ndata", C.c_int64)]
+
+
+class fl_cg_status(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("rz", C.c_double), ("norm0", C.c_double), ("done", C.c_int32),
+                ("converged", C.c_int32), ("error", C.c_int32), ("pad_", C.c_int32)]
 
 
 class fl_near_structure(C.Structure):
@@ -130,6 +137,7 @@ def load():
         "fl_debug_ring_tail": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), P(fl_tables),
                                            vp, C.c_int32, vp, vp]),
         "fl_dense_from_host": (C.c_int32, [vp, C.c_int64, C.c_int32, P(vp)]),
+        "fl_dense_from_host_rows": (C.c_int32, [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P(vp)]),
         "fl_dense_free": (None, [vp]),
         "fl_dense_info": (C.c_int32, [vp, P(C.c_int64), P(C.c_int64), P(C.c_int64), P(vp)]),
         "fl_dense_stats": (C.c_int32, [vp, P(fl_assembly_stats)]),
@@ -139,9 +147,19 @@ def load():
         "fl_matvec": (C.c_int32, [vp, vp, vp, C.c_int32]),
         "fl_matvec_async": (C.c_int32, [vp, vp, vp, vp]),
         "fl_pcg": (C.c_int32, [vp, vp, vp, C.c_double, C.c_int64, C.c_int32, vp, P(fl_solve_report)]),
-        "fl_cg_update_async": (C.c_int32, [C.c_int64, C.c_double, vp, vp, vp, vp, vp, vp, vp, vp]),
-        "fl_dot_async": (C.c_int32, [C.c_int64, vp, vp, vp, vp]),
-        "fl_xpby_async": (C.c_int32, [C.c_int64, vp, C.c_double, vp, vp]),
+        "fl_cg_create": (C.c_int32, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_int64,
+                                     C.c_int32, vp, P(vp)]),
+        "fl_cg_buffers": (C.c_int32, [vp, P(vp), P(vp), P(C.c_int64)]),
+        "fl_cg_bind_parts": (C.c_int32, [vp, vp]),
+        "fl_cg_begin": (C.c_int32, [vp, vp, vp, vp, vp, vp]),
+        "fl_cg_init": (C.c_int32, [vp, vp, vp]),
+        "fl_cg_matvec_diag": (C.c_int32, [vp, vp, vp, vp]),
+        "fl_cg_matvec_rest": (C.c_int32, [vp, vp, vp, vp, vp, vp]),
+        "fl_cg_dot_parts": (C.c_int32, [vp, vp, vp, vp]),
+        "fl_cg_alpha_update": (C.c_int32, [vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "fl_cg_beta_xpby": (C.c_int32, [vp, vp, vp, vp, vp]),
+        "fl_cg_poll": (C.c_int32, [vp, P(fl_cg_status), vp]),
+        "fl_cg_free": (None, [vp]),
         "fl_debug_orders": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params), C.c_int32,
                                         vp, vp]),
         "fl_debug_order_hist": (C.c_int32, [P(fl_mesh), P(fl_dofmap), P(fl_kernel), P(fl_order_params),

@@ -190,8 +190,9 @@ class ClusterOperatorDevice:
     `from_operator(op)` wraps an operator built by the reference's `cluster.compress` (or any
     object with its attributes: tree, cheb, near, far_pairs, far_blocks, basis_coef, kernel)."""
 
-    def __init__(self, handle, n, diag, d, M, s=None, tree_info=None):
+    def __init__(self, handle, n, diag, d, M, s=None, tree_info=None, device=0):
         self._h = handle
+        self.device = int(device)
         self.n = int(n)
         self._diag = diag
         self.d, self.M = d, M
@@ -246,7 +247,8 @@ class ClusterOperatorDevice:
             info = {"num_nodes": nn, "node_dofs": lambda nd: perm[rng[nd, 0]:rng[nd, 1]],
                     "near_leaf_map": {int(k): np.asarray(v) for k, v in near_leaf_map.items()},
                     "leaf_of_dof": leaf_of_dof}
-        return cls(h, n, near.diagonal().copy() if diag is None else np.asarray(diag, float), d, M, float(s), info)
+        return cls(h, n, near.diagonal().copy() if diag is None else np.asarray(diag, float), d, M, float(s), info,
+                   device=_device_index(device))
 
     @classmethod
     def from_operator(cls, op, device=None, build_blocks_on_device=False):

@@ -430,6 +430,13 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   const int e4 = e4_of(d, s);
   const bool integral = kernel->variant == FL_VARIANT_INTEGRAL;
   const int64_t rows = row_end - row_begin;
+  if (rows == 0 && !host) {        // an empty row block (a rank past the last row): nothing to assemble
+    D->A.alloc(D->lda);
+    FL_CUDA(cudaMemsetAsync(D->A.p, 0, D->lda * sizeof(double), st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    *out = D.release();
+    return FL_OK;
+  }
 
   Timer tm(st);
   tm.h0 = t_enter;
@@ -1032,29 +1039,39 @@ void fl_sparse_free(fl_sparse* A) {
   delete A;
 }
 
-int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out) {
+int32_t fl_dense_from_host_rows(const double* rows_host, int64_t n, int64_t row_begin, int64_t row_end,
+                                int32_t device, fl_dense** out) {
   FL_API_BEGIN
-  if (!A || !out || n <= 0) return fail(FL_E_ARG, "bad argument");
+  if (!out) return fail(FL_E_ARG, "null output handle");
   *out = nullptr;
-  FL_CUDA(cudaSetDevice(device));
+  if (n <= 0 || row_begin < 0 || row_end < row_begin || row_end > n || (row_end > row_begin && !rows_host))
+    return fail(FL_E_ARG, "bad argument");
+  DeviceScope dev(device);
   std::unique_ptr<fl_dense> D(new fl_dense());
   D->device = device;
   D->n = n;
-  D->row0 = 0;
-  D->row1 = n;
+  D->row0 = row_begin;
+  D->row1 = row_end;
   D->lda = ((n + 31) / 32) * 32;
+  const int64_t rows = row_end - row_begin;
   init_pool(device);
   D->stream = acquire_stream(device);
   D->own_stream = true;
   StreamScope scope(D->stream);
-  D->A.alloc((size_t)n * D->lda);
-  FL_CUDA(cudaMemsetAsync(D->A.p, 0, (size_t)n * D->lda * sizeof(double), D->stream));
-  FL_CUDA(cudaMemcpy2DAsync(D->A.p, D->lda * sizeof(double), A, n * sizeof(double), n * sizeof(double), n,
-                            cudaMemcpyHostToDevice, D->stream));
+  D->A.alloc((size_t)std::max<int64_t>(rows, 1) * D->lda);
+  FL_CUDA(cudaMemsetAsync(D->A.p, 0, (size_t)std::max<int64_t>(rows, 1) * D->lda * sizeof(double), D->stream));
+  if (rows > 0)
+    FL_CUDA(cudaMemcpy2DAsync(D->A.p, D->lda * sizeof(double), rows_host, n * sizeof(double), n * sizeof(double),
+                              rows, cudaMemcpyHostToDevice, D->stream));
   FL_CUDA(cudaStreamSynchronize(D->stream));
   *out = D.release();
   return FL_OK;
   FL_API_END
+}
+
+int32_t fl_dense_from_host(const double* A, int64_t n, int32_t device, fl_dense** out) {
+  if (!A) return fail(FL_E_ARG, "bad argument");
+  return fl_dense_from_host_rows(A, n, 0, n, device, out);
 }
 
 void fl_dense_free(fl_dense* A) {
@@ -1208,30 +1225,89 @@ int32_t fl_pcg(const fl_dense* A, const double* b, const double* x0, double tol,
   FL_API_END
 }
 
-int32_t fl_cg_update_async(int64_t m, double alpha, double* x, double* r, double* z, const double* p,
-                           const double* Ap, const double* minv, double* partial_dev, void* stream) {
+int32_t fl_cg_create(int64_t n, int64_t m_local, int64_t block_rows, int32_t world, int32_t rank, double tol,
+                     int64_t max_iter, int32_t device, void* stream, fl_cg** out) {
   FL_API_BEGIN
-  DBuf<double> scratch(DOT_BLOCKS);
-  launch_cg_update(m, alpha, nullptr, x, r, z, p, Ap, minv, partial_dev, scratch.p, (cudaStream_t)stream);
-  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (!out) return fail(FL_E_ARG, "null argument");
+  *out = nullptr;
+  DeviceScope dev(device);
+  StreamScope scope((cudaStream_t)stream);
+  *out = cg_create(n, m_local, block_rows, world, rank, tol, (long long)max_iter, device);
   return FL_OK;
   FL_API_END
 }
 
-int32_t fl_dot_async(int64_t m, const double* a, const double* b, double* out_dev, void* stream) {
+int32_t fl_cg_buffers(fl_cg* S, double** local_parts, double** all_parts, int64_t* chunks_per_rank) {
   FL_API_BEGIN
-  DBuf<double> scratch(DOT_BLOCKS);
-  launch_dot(m, a, b, out_dev, scratch.p, (cudaStream_t)stream);
-  FL_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (!S) return fail(FL_E_ARG, "null argument");
+  if (local_parts) *local_parts = cg_local_parts(S);
+  if (all_parts) *all_parts = cg_all_parts(S);
+  if (chunks_per_rank) *chunks_per_rank = cg_chunks(S);
   return FL_OK;
   FL_API_END
 }
 
-int32_t fl_xpby_async(int64_t m, const double* z, double beta, double* p, void* stream) {
+int32_t fl_cg_bind_parts(fl_cg* S, double* local_parts) {
   FL_API_BEGIN
-  launch_xpby(m, z, beta, nullptr, p, (cudaStream_t)stream);
+  if (!S) return fail(FL_E_ARG, "null argument");
+  cg_bind_parts(S, local_parts);
   return FL_OK;
   FL_API_END
+}
+
+#define FL_CG_CALL(cond, body)                                          \
+  FL_API_BEGIN                                                         \
+  if (!S || !(cond)) return fail(FL_E_ARG, "null argument");           \
+  DeviceScope dev(cg_device(S));                                       \
+  cudaStream_t st = (cudaStream_t)stream;                              \
+  StreamScope scope(st);                                               \
+  body;                                                                \
+  return FL_OK;                                                        \
+  FL_API_END
+
+static void cg_check_rows(const fl_cg* S, const fl_dense* A) {
+  int dev;
+  int64_t n, row0, m;
+  cg_info(S, &dev, &n, &row0, &m);
+  if (A->device != dev || A->n != n || A->row0 != row0 || A->row1 - A->row0 != m)
+    throw Error(FL_E_ARG, "operator rows do not match the CG rank's row block");
+}
+
+int32_t fl_cg_begin(fl_cg* S, const double* r, const double* minv, double* z, double* p, void* stream) {
+  FL_CG_CALL(r && minv && z && p, cg_begin(S, r, minv, z, p, st))
+}
+int32_t fl_cg_init(fl_cg* S, const double* all_parts, void* stream) {
+  FL_CG_CALL(all_parts, cg_init(S, all_parts, st))
+}
+int32_t fl_cg_matvec_diag(fl_cg* S, const fl_dense* A, const double* p_local, void* stream) {
+  FL_CG_CALL(A && p_local, (cg_check_rows(S, A), cg_matvec_diag(S, A->A.p, A->lda, p_local, st)))
+}
+int32_t fl_cg_matvec_rest(fl_cg* S, const fl_dense* A, const double* p_full, const double* p_local, double* Ap,
+                          void* stream) {
+  FL_CG_CALL(A && p_full && p_local && Ap, (cg_check_rows(S, A), cg_matvec_rest(S, A->A.p, A->lda, p_full, p_local, Ap, st)))
+}
+int32_t fl_cg_dot_parts(fl_cg* S, const double* a, const double* b, void* stream) {
+  FL_CG_CALL(a && b, cg_dot_parts(S, a, b, st))
+}
+int32_t fl_cg_alpha_update(fl_cg* S, const double* all_parts, double* x, double* r, double* z, const double* p,
+                           const double* Ap, const double* minv, void* stream) {
+  FL_CG_CALL(all_parts && x && r && z && p && Ap && minv, cg_alpha_update(S, all_parts, x, r, z, p, Ap, minv, st))
+}
+int32_t fl_cg_beta_xpby(fl_cg* S, const double* all_parts, const double* z, double* p, void* stream) {
+  FL_CG_CALL(all_parts && z && p, cg_beta_xpby(S, all_parts, z, p, st))
+}
+int32_t fl_cg_poll(fl_cg* S, fl_cg_status* status, void* stream) {
+  FL_CG_CALL(status, cg_status(S, status, st))
+}
+#undef FL_CG_CALL
+
+void fl_cg_free(fl_cg* S) {
+  if (!S) return;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(cg_device(S));
+  cg_free(S);
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
 int32_t fl_debug_orders(const fl_mesh* mesh, const fl_dofmap* dofmap, const fl_kernel* kernel,

@@ -1094,7 +1094,7 @@ int32_t fl_cluster_create(const fl_cluster_desc* desc, int32_t device, fl_cluste
 int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_far, int32_t ptr_kind) {
   FL_TRY
   if (!C || !x || !y) return fl::api_fail(FL_E_ARG, "null argument");
-  FL_CUDA(cudaSetDevice(C->device));
+  fl::DeviceScope dev(C->device);
   cudaStream_t st = C->stream;
   fl::StreamScope scope(st);
   const int64_t n = C->n;
@@ -1115,10 +1115,26 @@ int32_t fl_cluster_matvec(fl_cluster* C, const double* x, double* y, double* y_f
 int32_t fl_cluster_matvec_async(fl_cluster* C, const double* x, double* y, void* stream) {
   FL_TRY
   if (!C || !x || !y) return fl::api_fail(FL_E_ARG, "null argument");
-  FL_CUDA(cudaSetDevice(C->device));
+  fl::DeviceScope dev(C->device);
   cudaStream_t st = (cudaStream_t)stream;             // NULL: the legacy default stream
   fl::StreamScope scope(st);
-  fl::cluster_matvec_dev(C, x, y, C->yfar.p, st);
+  // The operator's scratch (mom, F, Fp, yfar) is shared with the synchronous entry points and
+  // released on C->stream: order this matvec after everything pending on C->stream, and
+  // everything later on C->stream after this matvec.
+  if (st != C->stream) {
+    cudaEvent_t e0, e1;
+    FL_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    FL_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    FL_CUDA(cudaEventRecord(e0, C->stream));
+    FL_CUDA(cudaStreamWaitEvent(st, e0, 0));
+    fl::cluster_matvec_dev(C, x, y, C->yfar.p, st);
+    FL_CUDA(cudaEventRecord(e1, st));
+    FL_CUDA(cudaStreamWaitEvent(C->stream, e1, 0));
+    cudaEventDestroy(e0);   // (destruction is deferred by the runtime until the events complete)
+    cudaEventDestroy(e1);
+  } else {
+    fl::cluster_matvec_dev(C, x, y, C->yfar.p, st);
+  }
   return FL_OK;
   FL_CATCH
 }

@@ -49,6 +49,20 @@ struct OwnedStreamLease {
   OwnedStreamLease& operator=(const OwnedStreamLease&) = delete;
 };
 
+// Makes `device` current for the scope of an API call and restores the caller's device on exit.
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    FL_CUDA(cudaSetDevice(device));
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 struct StreamScope {
   cudaStream_t prev;
   explicit StreamScope(cudaStream_t s) : prev(cur_stream()) { cur_stream() = s; }
@@ -310,6 +324,8 @@ void near_field_cross(const DevMesh& m, const DevTables& t, const OrderConsts& o
 // fl_cluster.cu: the cluster (H-matrix) operator
 }  // namespace fl
 struct fl_cluster;
+struct fl_cg;
+struct fl_cg_status;
 struct fl_cluster_desc;
 namespace fl {
 int32_t cluster_create(const ::fl_cluster_desc* D, int device, ::fl_cluster** out);
@@ -320,18 +336,10 @@ void cluster_far_points(::fl_cluster* C, const double* u_dev, int64_t npts, cons
 int32_t api_fail(int code, const char* msg);
 
 // fl_solve.cu
+constexpr int VCH = 512;   // fixed global vector chunk of every solve reduction; row blocks are multiples of it
 void launch_matvec(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
                    cudaStream_t st);
 void launch_diag(const double* A, int64_t rows, int64_t row0, int64_t lda, double* d, cudaStream_t st);
-void launch_dot(int64_t m, const double* a, const double* b, double* out, double* scratch,
-                cudaStream_t st);
-void launch_cg_update(int64_t m, double alpha, const double* alpha_dev, double* x, double* r,
-                      double* z, const double* p, const double* Ap, const double* minv,
-                      double* out, double* scratch, cudaStream_t st);
-void launch_xpby(int64_t m, const double* z, double beta, const double* beta_dev, double* p,
-                 cudaStream_t st);
-void launch_matvec_flag(const double* A, int64_t rows, int64_t n, int64_t lda, const double* x, double* y,
-                        const int* done, cudaStream_t st);
 struct PcgResult {
   long long it;
   double rz, norm0;
@@ -339,6 +347,24 @@ struct PcgResult {
 };
 PcgResult run_pcg(const double* A, int64_t n, int64_t lda, const double* minv, double* x, double* r, double* z,
                   double* p, double* Ap, double tol, long long max_iter, bool have_x0, cudaStream_t st);
+fl_cg* cg_create(int64_t n, int64_t m, int64_t blk, int world, int rank, double tol, long long max_iter, int device);
+void cg_begin(fl_cg* S, const double* r, const double* minv, double* z, double* p, cudaStream_t st);
+void cg_init(fl_cg* S, const double* parts, cudaStream_t st);
+void cg_matvec_diag(fl_cg* S, const double* A, int64_t lda, const double* x_local, cudaStream_t st);
+void cg_matvec_rest(fl_cg* S, const double* A, int64_t lda, const double* x_full, const double* p_local,
+                    double* Ap, cudaStream_t st);
+void cg_dot_parts(fl_cg* S, const double* a, const double* b, cudaStream_t st);
+void cg_alpha_update(fl_cg* S, const double* parts, double* x, double* r, double* z, const double* p,
+                     const double* Ap, const double* minv, cudaStream_t st);
+void cg_beta_xpby(fl_cg* S, const double* parts, const double* z, double* p, cudaStream_t st);
+void cg_status(fl_cg* S, fl_cg_status* out, cudaStream_t st);
+double* cg_local_parts(fl_cg* S);
+void cg_bind_parts(fl_cg* S, double* ext);
+double* cg_all_parts(fl_cg* S);
+int64_t cg_chunks(fl_cg* S);
+void cg_free(fl_cg* S);
+int cg_device(const fl_cg* S);
+void cg_info(const fl_cg* S, int* device, int64_t* n, int64_t* row0, int64_t* m);
 constexpr int DOT_BLOCKS = 296;   // 2 x 148 SMs; fixed => deterministic reduction tree
 
 }  // namespace fl

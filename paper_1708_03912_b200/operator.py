@@ -31,6 +31,15 @@ class DenseDeviceOperator:
         _lib.check(_lib.load().fl_dense_from_host(A.ctypes.data, A.shape[0], int(device), C.byref(h)))
         return cls(h, A.shape[0], 0, A.shape[0])
 
+    @classmethod
+    def from_host_rows(cls, rows, n, row_begin, device=0):
+        """Rows [row_begin, row_begin + len(rows)) of an (n, n) host matrix as a row-block operator."""
+        rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, int(n))
+        h = C.c_void_p()
+        _lib.check(_lib.load().fl_dense_from_host_rows(rows.ctypes.data, int(n), int(row_begin),
+                                                       int(row_begin) + len(rows), int(device), C.byref(h)))
+        return cls(h, n, row_begin, row_begin + len(rows))
+
     # ------------------------------------------------------------ lifetime
     def free(self):
         if self._h is not None and self._h.value:

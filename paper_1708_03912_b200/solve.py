@@ -61,7 +61,7 @@ def pcg(op, b, precond="jacobi", tol=1e-8, max_iter=None, x0=None, record_lanczo
             return pcg(dev, b, precond, tol, max_iter, x0)
     from .cluster import ClusterOperatorDevice
     if isinstance(op, ClusterOperatorDevice):
-        return _pcg_cluster(op, b, precond, tol, max_iter)
+        return _pcg_cluster(op, b, precond, tol, max_iter, x0)
     if not isinstance(op, DenseDeviceOperator):
         raise TypeError("pcg expects a DenseDeviceOperator (assemble_dense_device), a "
                         "ClusterOperatorDevice or a dense ndarray; host operators are not on the device path")
@@ -108,26 +108,29 @@ class _OneRank:
         return None
 
     @staticmethod
-    def all_gather_into_tensor(out, inp, group=None):
+    def all_gather_into_tensor(out, inp, group=None, async_op=False):
         out.copy_(inp)
 
 
-def _pcg_cluster(op, b, precond, tol, max_iter):
-    """The same Jacobi PCG (solve.py:52-109) on a ClusterOperatorDevice: device vectors, the fused
-    CG kernels of libfraclap_b200 and the H-matrix matvec (fl_cluster_matvec on device pointers)."""
+def _pcg_cluster(op, b, precond, tol, max_iter, x0=None):
+    """The same Jacobi PCG (solve.py:52-109) on a ClusterOperatorDevice: device vectors, the
+    device-scalar CG steps of libfraclap_b200 (fl_cg_*) and the H-matrix matvec
+    (fl_cluster_matvec_async on torch's stream), run on the operator's own device."""
     import torch
     from .distributed import TorchDeviceBackend, pcg_sharded
 
     class _Backend(TorchDeviceBackend):
         def __init__(self, cop):
-            super().__init__(None, torch.cuda.current_stream().cuda_stream)
+            super().__init__(None)
             self.cop = cop
 
-        def matvec(self, p_full, out_local):
+        def matvec_diag(self, p_local):
+            pass                                  # one rank: nothing to overlap
+
+        def matvec_rest(self, p_full, p_local, Ap):
             # enqueued on torch's current stream, no host synchronisation
-            _lib.check(self.lib.fl_cluster_matvec_async(self.cop.handle, C.c_void_p(p_full.data_ptr()),
-                                                        C.c_void_p(out_local.data_ptr()),
-                                                        C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            _lib.check(self.lib.fl_cluster_matvec_async(self.cop.handle, self._p(p_full), self._p(Ap), self.stream))
+            _lib.check(self.lib.fl_cg_dot_parts(self.S, self._p(p_local), self._p(Ap), self.stream))
 
     b = np.ascontiguousarray(b, dtype=np.float64)
     n = len(b)
@@ -135,8 +138,12 @@ def _pcg_cluster(op, b, precond, tol, max_iter):
         raise ValueError("b has length %d, operator is %d x %d" % (n, op.n, op.n))
     if precond not in ("jacobi", None, "none"):
         raise ValueError("precond must be 'jacobi' or None on the device path")
+    if x0 is not None and np.shape(x0) != (n,):
+        raise ValueError("x0 must have shape (%d,)" % n)
     t0 = time.perf_counter()
-    x, rep = pcg_sharded(_Backend(op), b, op.diag(), [(0, n)], n, _OneRank, tol=tol, max_iter=max_iter,
-                         precond="jacobi" if precond == "jacobi" else None)
-    return x.cpu().numpy(), SolveReport(int(rep["iterations"]), float(rep.get("residual", float("nan"))),
-                                        time.perf_counter() - t0, bool(rep["converged"]))
+    with torch.cuda.device(op.device):
+        x, rep = pcg_sharded(_Backend(op), b, op.diag(), [(0, n)], n, _OneRank, tol=tol, max_iter=max_iter,
+                             precond="jacobi" if precond == "jacobi" else None, x0_local=x0)
+        x = x.cpu().numpy()
+    return x, SolveReport(int(rep["iterations"]), float(rep.get("residual", float("nan"))),
+                          time.perf_counter() - t0, bool(rep["converged"]))

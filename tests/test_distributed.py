@@ -15,32 +15,102 @@ from conftest import GOLDEN
 
 
 class HostBackend:
-    def __init__(self, A_rows):
+    """The device steps of fl_cg_* (csrc/fl_solve.cu) restated on CPU tensors: chunk sums over
+    fixed global chunks of 512 entries, gathered and folded in global order on every rank."""
+    VCH = 512
+
+    def __init__(self, A_rows, r0):
         self.A = torch.as_tensor(A_rows)
+        self.r0 = r0
 
     def zeros(self, m):
         return torch.zeros(m, dtype=torch.float64)
 
-    def from_numpy(self, a):
-        return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64).clone()
+    def from_numpy(self, a, length=None):
+        a = np.asarray(a, dtype=np.float64)
+        t = self.zeros(len(a) if length is None else length)
+        t[:len(a)] = torch.from_numpy(a)
+        return t
 
-    def matvec(self, p_full, out):
-        out.copy_(self.A @ p_full[: self.A.shape[1]])
-
-    def dot(self, a, b):
-        return torch.dot(a, b).reshape(1)
-
-    def update(self, alpha, x, r, z, p, Ap, minv):
-        x.add_(alpha * p)
-        r.sub_(alpha * Ap)
-        z.copy_(minv * r)
-        return torch.dot(r, z).reshape(1)
-
-    def xpby(self, z, beta, p):
-        p.mul_(beta).add_(z)
+    def scalar(self, v):
+        return torch.tensor([float(v)], dtype=torch.float64)
 
     def item(self, t):
         return float(t.item())
+
+    def setup(self, n, m, blk, world, rank, tol, max_iter):
+        self.n, self.m, self.blk, self.world, self.tol, self.max_iter = n, m, blk, world, tol, max_iter
+        self.L = blk // self.VCH
+        self.local = self.zeros(self.L)
+        self.all = self.local if world == 1 else self.zeros(self.L * world)
+        self.sc = dict(it=0, done=False, converged=False, error=0, rz=0.0, norm0=0.0, alpha=0.0, beta=0.0)
+        return self.local, self.all
+
+    def _parts(self, v):
+        self.local.zero_()
+        for c in range(-(-self.m // self.VCH)):
+            self.local[c] = float(v[c * self.VCH:min(self.m, (c + 1) * self.VCH)].sum())
+
+    def _fold(self, allp):
+        t = 0.0
+        for g in range(self.world):
+            rows = max(0, min(self.n, (g + 1) * self.blk) - g * self.blk)
+            for c in range(-(-rows // self.VCH)):
+                t += float(allp[g * self.L + c])
+        return t
+
+    def begin(self, r, minv, z, p):
+        m = self.m
+        z[:m] = minv[:m] * r[:m]
+        p[:m] = z[:m]
+        self._parts(r[:m] * z[:m])
+
+    def init(self, allp):
+        rz = self._fold(allp)
+        self.sc.update(rz=rz, norm0=float(np.sqrt(abs(rz))))
+        if self.sc["norm0"] == 0:
+            self.sc.update(done=True, converged=True)
+
+    def matvec_diag(self, p_local):
+        pass
+
+    def matvec_rest(self, p_full, p_local, Ap):
+        if self.sc["done"]:
+            return
+        Ap[:self.m] = self.A @ p_full[:self.A.shape[1]]
+        self._parts(p_local[:self.m] * Ap[:self.m])
+
+    def alpha_update(self, allp, x, r, z, p, Ap, minv):
+        if self.sc["done"]:
+            return
+        pAp = self._fold(allp)
+        if not pAp > 0:
+            self.sc.update(error=1, done=True)
+            return
+        a = self.sc["rz"] / pAp
+        m = self.m
+        x[:m] += a * p[:m]
+        r[:m] -= a * Ap[:m]
+        z[:m] = minv[:m] * r[:m]
+        self._parts(r[:m] * z[:m])
+
+    def beta_xpby(self, allp, z, p):
+        if self.sc["done"]:
+            return
+        rzn = self._fold(allp)
+        self.sc["it"] += 1
+        if np.sqrt(abs(rzn)) <= self.tol * self.sc["norm0"]:
+            self.sc.update(converged=True, done=True, rz=rzn)
+            return
+        beta = rzn / self.sc["rz"]
+        self.sc["rz"] = rzn
+        if self.sc["it"] >= self.max_iter:
+            self.sc["done"] = True
+        p[:self.m] = z[:self.m] + beta * p[:self.m]
+
+    def poll(self):
+        return dict(iterations=self.sc["it"], rz=self.sc["rz"], norm0=self.sc["norm0"], done=self.sc["done"],
+                    converged=self.sc["converged"], error=self.sc["error"])
 
 
 def _free_port():
@@ -60,7 +130,7 @@ def _worker(rank, world, port, path, out):
     n = len(b)
     rows = D.shard_rows(n, world)
     r0, r1 = rows[rank]
-    be = HostBackend(A[r0:r1])
+    be = HostBackend(A[r0:r1], r0)
     x, rep = D.pcg_sharded(be, b[r0:r1], np.diag(A)[r0:r1], rows, n, dist, tol=1e-10, max_iter=10 ** 5)
     parts = [None] * world
     dist.all_gather_object(parts, (r0, x.numpy(), rep["iterations"]))
@@ -72,13 +142,15 @@ def _worker(rank, world, port, path, out):
     dist.destroy_process_group()
 
 
-def test_sharded_pcg_gloo_world2(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_pcg_gloo(tmp_path, world):
+    """world 3 at n = 513 leaves the last rank without rows (blocks of 512 rows)."""
     from oracle import fraclap_oracle as O
     path = os.path.join(GOLDEN, "c1.npz")
     if not os.path.exists(path):
         pytest.skip("c1 golden missing")
     out = str(tmp_path / "x.npy")
-    mp.spawn(_worker, args=(2, _free_port(), path, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), path, out), nprocs=world, join=True)
     res = np.load(out)
     it, x = int(res[0]), res[1:]
     G = np.load(path)
@@ -89,8 +161,12 @@ def test_sharded_pcg_gloo_world2(tmp_path):
 
 
 def test_shard_rows():
-    from paper_1708_03912_b200.distributed import shard_rows
-    assert shard_rows(10, 3) == [(0, 3), (3, 7), (7, 10)]
-    r = shard_rows(100, 4, weights=np.r_[np.ones(50), 3 * np.ones(50)])
-    assert r[0][0] == 0 and r[-1][1] == 100 and all(a[1] == b[0] for a, b in zip(r, r[1:]))
-    assert r[0][1] == 50 and r[1][1] == 67
+    from paper_1708_03912_b200.distributed import shard_rows, block_rows
+    assert shard_rows(10, 3, align=1) == [(0, 4), (4, 8), (8, 10)]
+    assert shard_rows(65025, 8) == [(g * 8192, min(65025, (g + 1) * 8192)) for g in range(8)]
+    assert block_rows(8191, 2) == 4096 and shard_rows(8191, 2) == [(0, 4096), (4096, 8191)]
+    assert shard_rows(513, 1) == [(0, 513)]
+    for n, w in [(1, 4), (513, 3), (16641, 8), (3969, 2)]:
+        r = shard_rows(n, w)
+        assert r[0][0] == 0 and r[-1][1] == n and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+        assert all(a % 512 == 0 for a, _ in r if a < n)
