@@ -137,6 +137,11 @@ typedef struct fl_assembly_stats {
   /* cross term split: discovery pass (orders only), near blocks, compute pass; near pair count */
   double ms_discover, ms_near, ms_cross_compute;
   int64_t near_pairs;
+  /* pairs whose pre-ceil Gauss order lay within 1e-12 of an integer (recomputed with a
+   * correctly rounded log; SURVEY.md §8(d) k-flip guard) */
+  int64_t order_ties;
+  /* 2D cross term: contributions accumulated as integers of 2^-cross_scale_exp (exact, order-free) */
+  int32_t cross_scale_exp, pad2_;
 } fl_assembly_stats;
 
 /* ---------------------------------------------------------------- library */

@@ -445,7 +445,10 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   upload(mesh, dofmap, tables, U, st);
   DevMesh& m = U.m;
   const int ncolors = 0;   // (the cross tiles no longer need a cell colouring)
-  const OrderConsts oc = make_order_consts(*params, d, s, n);
+  OrderConsts oc = make_order_consts(*params, d, s, n);
+  DBuf<unsigned long long> ties(1);          // k-flip guard counter (fl_device.cuh order_near_tie)
+  FL_CUDA(cudaMemsetAsync(ties.p, 0, sizeof(unsigned long long), st));
+  oc.ties = ties.p;
 
   // target cells: cells with a vertex DoF in the owned rows
   DBuf<int> flags(m.nc), all(m.nc), targets(m.nc), nsel(1);
@@ -683,6 +686,20 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     done1d = launch_cross1d(m, U.t, oc, ex, e4, C, P1.get(), maxcells1d, targets.p, ntargets, row_vertex.p, D->A.p,
                             D->lda, evc.p + 1, st);
   }
+  static const bool cross2d_tiles = [] {      // FRACLAP_CROSS2D=tiles: the round-1 DoF-tile kernel
+    const char* v = getenv("FRACLAP_CROSS2D");
+    return v && std::string(v) == "tiles";
+  }();
+  Cross2DInfo x2{};
+  if (!done1d && d == 2 && !cross2d_tiles) {
+    cudaEventCreate(&xev[0]);
+    cudaEventCreate(&xev[1]);
+    tm.mark();  // 5
+    assemble_cross2d(m, U.t, oc, ex, e4, C, (int)row_begin, (int)row_end, D->A.p, D->lda, evc.p + 1, near, x2,
+                     xev[0], xev[1], st);
+    ntiles = -1;
+    done1d = true;
+  }
   if (!done1d) {
     cudaEventCreate(&xev[0]);
     cudaEventCreate(&xev[1]);
@@ -735,6 +752,8 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   unsigned long long* hev = reinterpret_cast<unsigned long long*>(hs + 8);
   FL_CUDA(cudaMemcpyAsync(hev, evc.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[4], m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  unsigned long long hties = 0;
+  FL_CUDA(cudaMemcpyAsync(&hties, ties.p, sizeof(hties), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   if (nbands) {
     FL_CUDA(cudaStreamSynchronize(cps.s));
@@ -753,6 +772,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   S.pairs_boundary_singular = nitems;
   S.pairs_boundary_flux = integral ? nc * m.nb : 0;
   S.evals_tail = (double)hev[0];
+  S.order_ties = (int64_t)hties;
   S.evals_cross = (double)hev[1];
   S.ms_prep = tm.ms(0, 1);
   S.ms_singular = early_tail ? tm.ms(2, 3) : tm.ms(1, 2);   // 1D: tail (1 -> 2) runs before the singular kernels
@@ -780,7 +800,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   }
   S.cross_tile_pairs = ntp;
   S.near_pairs = near.n;
-  if (ntiles > 0) {
+  if (ntiles > 0 || ntiles == -1) {
     float a = 0, b = 0, c = 0;
     cudaEventElapsedTime(&a, tm.e[5], xev[0]);
     cudaEventElapsedTime(&b, xev[0], xev[1]);
@@ -791,6 +811,11 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     if (e) cudaEventDestroy(e);
   S.ncolors = ncolors;
   S.ntiles = ntiles;
+  if (ntiles == -1) {
+    S.cross_tile_pairs = x2.block_pairs;
+    S.ntiles = 0;
+    S.cross_scale_exp = x2.scale_exp;
+  }
   *out = D.release();
   return FL_OK;
   FL_API_END

@@ -1,0 +1,756 @@
+// 2D disjoint cross term (cross_matrices, assembly.py:172-229, scattered by _cross_triplets
+// :693-725) by CELL-BLOCK PAIRS with exact fixed-point accumulation.
+//
+// Layout.  The cells are sorted along a Morton curve of their centroids and cut into blocks of
+// CB = 32 cells; every block keeps the sorted list of the DoFs of its cells (<= BRMAX) and each
+// cell the local slot of its vertices in that list.  A CTA owns one unordered block pair
+// {P, Q} (P <= Q) at a time (persistent queue, heaviest pairs first):
+//   (A) the Gauss order of its <= 1024 cell pairs (select_order, quadrature.py:138-179; the
+//       fast fp32 path with the exact fp64 fallback, or one order for the whole block pair
+//       when rigorous bounds of the order formula agree), touching pairs skipped;
+//   (B) every disjoint pair evaluated ONCE: k = 2, 3, 4 one thread per pair with the mapped
+//       nodes of both cells staged in shared memory (heaviest orders first), k >= 5 (rare,
+//       near pairs) looked up from the near-block table computed by fl_near.cu;
+//   (C) -C * M^{K,L} added into an int64 tile of the block pair's DoF rectangle in shared
+//       memory, and the tile (plus its transpose for P != Q) added into A with 64-bit integer
+//       atomics.
+// Determinism.  Every contribution is converted to a fixed-point integer with a global scale
+// 2^S chosen from a rigorous bound of the largest entry (S leaves ~2^8 headroom); integer
+// addition is associative, so every entry is the exact sum of its rounded contributions in
+// ANY order: bitwise reproducible run to run, and identical for any split of the rows over
+// GPUs (a rank processes the block pairs touching its rows and keeps only its rows).  The
+// resolution is ~2^-54 of the bound — finer than an fp64 ulp of the largest entries.  No cell
+// pair is evaluated twice (the DoF-tile kernel of round 1 recomputed ~1.5x at the halo).
+#include <cstring>
+
+#include <cub/cub.cuh>
+
+#include "fl_internal.h"
+
+namespace fl {
+
+namespace {
+
+constexpr int CB = 32;            // cells per block
+constexpr int BRMAX = 64;         // DoFs per block (more: the mesh is refused by this path)
+constexpr int TCAP = 48 * 48;     // int64 tile capacity; larger rectangles go straight to HBM
+constexpr int X2T = 256;          // threads per CTA
+constexpr int NPRE2 = 29;         // mapped nodes per cell: k = 2, 3, 4 (4 + 9 + 16)
+__host__ __device__ constexpr int poff(int k) { return k == 2 ? 0 : (k == 3 ? 4 : 13); }
+
+struct XRec {                     // per staged cell: order inputs
+  double cx, cy, rad, J;
+  float lnh, lh;
+  int id, pad;
+};
+
+struct XShared {
+  double2 nd[2 * CB][NPRE2];      // mapped nodes (absolute coordinates, as _map_points)
+  unsigned long long tile[TCAP];
+  XRec r[2 * CB];
+  double wl[NPRE2][3];            // w * lambda_a of the rules k = 2, 3, 4
+  int dofP[BRMAX], dofQ[BRMAX];
+  signed char sl[2 * CB][3];      // local DoF slot of each staged cell's vertices
+  unsigned short plist[CB * CB];
+  unsigned char pk[CB * CB];
+  int hist[8], cursor[8];
+  short chs[CB * CB / 4 + 8];       // chunks of same-order pairs: start in plist, count, order
+  unsigned char chn[CB * CB / 4 + 8], chk[CB * CB / 4 + 8];
+  int nchunk;
+  int bp, nP, nQ, q;
+  unsigned long long evals;
+};
+
+// ---------------------------------------------------------------- preparation
+__device__ __forceinline__ uint32_t spread16b(uint32_t x) {
+  x &= 0xFFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+__global__ void cell_morton_kernel(DevMesh m, double x0, double y0, double sx, double sy, uint32_t* keys,
+                                   int* vals) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= m.nc) return;
+  const CellGeo& g = m.geo[c];
+  const uint32_t qx = (uint32_t)fmin(fmax((g.cx - x0) * sx, 0.0), 65535.0);
+  const uint32_t qy = (uint32_t)fmin(fmax((g.cy - y0) * sy, 0.0), 65535.0);
+  keys[c] = spread16b(qx) | (spread16b(qy) << 1);
+  vals[c] = c;
+}
+
+// one CTA (128 threads) per block: cells, sorted DoF list, vertex slots, block statistics
+__global__ void __launch_bounds__(128) block_build_kernel(DevMesh m, const int* __restrict__ sorted, int nb,
+                                                          int r0, int r1, int* __restrict__ bcells,
+                                                          int* __restrict__ bdofs, int* __restrict__ bndof,
+                                                          signed char* __restrict__ slot, double* __restrict__ bstat,
+                                                          int* __restrict__ rowflag, int* __restrict__ err) {
+  const int b = blockIdx.x, t = threadIdx.x;
+  __shared__ int key[128];
+  __shared__ int list[128];
+  __shared__ int nu, cells[CB];
+  if (t < CB) {
+    const int i = b * CB + t;
+    cells[t] = i < m.nc ? sorted[i] : -1;
+    bcells[b * CB + t] = cells[t];
+  }
+  __syncthreads();
+  key[t] = 0x7fffffff;
+  if (t < 3 * CB) {
+    const int c = cells[t / 3];
+    if (c >= 0) {
+      const int dof = m.geo[c].dof[t % 3];
+      if (dof >= 0) key[t] = dof;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= 128; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int ixj = t ^ j;
+      if (ixj > t) {
+        const bool up = (t & k) == 0;
+        const int a = key[t], c = key[ixj];
+        if ((a > c) == up) { key[t] = c; key[ixj] = a; }
+      }
+      __syncthreads();
+    }
+  if (t == 0) {
+    int u = 0;
+    for (int i = 0; i < 128 && key[i] != 0x7fffffff; ++i)
+      if (i == 0 || key[i] != key[i - 1]) list[u++] = key[i];
+    nu = u;
+    if (u > BRMAX) atomicAdd(err, 1);
+    bndof[b] = min(u, BRMAX);
+  }
+  __syncthreads();
+  const int n = min(nu, BRMAX);
+  if (t < BRMAX) bdofs[b * BRMAX + t] = t < n ? list[t] : -1;
+  if (t < 3 * CB) {
+    const int c = cells[t / 3];
+    if (c >= 0) {
+      const int dof = m.geo[c].dof[t % 3];
+      int s = -1;
+      for (int i = 0; i < n; ++i)
+        if (list[i] == dof) s = i;
+      slot[c * 3 + t % 3] = (signed char)(dof >= 0 ? s : -1);
+    }
+  }
+  if (t == 0) {
+    int fl = 0;
+    for (int i = 0; i < n; ++i) fl |= (list[i] >= r0 && list[i] < r1);
+    rowflag[b] = fl;
+    double cx = 0, cy = 0;
+    int cnt = 0;
+    for (int i = 0; i < CB; ++i)
+      if (cells[i] >= 0) { cx += m.geo[cells[i]].cx; cy += m.geo[cells[i]].cy; ++cnt; }
+    cx /= max(cnt, 1);
+    cy /= max(cnt, 1);
+    double R = 0, hmn = 1e300, hmx = 0, lmn = 1e300, lmx = 0;
+    for (int i = 0; i < CB; ++i) {
+      if (cells[i] < 0) continue;
+      const CellGeo& g = m.geo[cells[i]];
+      const double dx = g.cx - cx, dy = g.cy - cy;
+      R = fmax(R, sqrt(dx * dx + dy * dy) * (1.0 + 1e-12) + g.rad);
+      hmn = fmin(hmn, g.diam); hmx = fmax(hmx, g.diam);
+      lmn = fmin(lmn, g.ldiam); lmx = fmax(lmx, g.ldiam);
+    }
+    double* st = bstat + 8 * b;
+    st[0] = cx; st[1] = cy; st[2] = R * (1.0 + 1e-12); st[3] = hmn; st[4] = hmx; st[5] = lmn; st[6] = lmx; st[7] = 0;
+  }
+}
+
+// mapped nodes of the rules k = 2, 3, 4 for every cell: X = P0 + (u0 (P1 - P0) + u1 (P2 - P0))
+__global__ void cell_nodes2_kernel(DevMesh m, const double* __restrict__ tab, RuleRef r2, RuleRef r3, RuleRef r4,
+                                   double2* __restrict__ nodes) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)m.nc * NPRE2) return;
+  const int c = (int)(i / NPRE2), x = (int)(i % NPRE2);
+  const RuleRef rr = x < 4 ? r2 : (x < 13 ? r3 : r4);
+  const int xl = x < 4 ? x : (x < 13 ? x - 4 : x - 13);
+  const double* nd = tab + (size_t)(rr.off + xl) * NODE;
+  const CellGeo& g = m.geo[c];
+  const double X0 = g.p[0][0] + (nd[0] * (g.p[1][0] - g.p[0][0]) + nd[1] * (g.p[2][0] - g.p[0][0]));
+  const double X1 = g.p[0][1] + (nd[0] * (g.p[1][1] - g.p[0][1]) + nd[1] * (g.p[2][1] - g.p[0][1]));
+  nodes[i] = make_double2(X0, X1);
+}
+
+// Bound of the largest cross entry: the closest disjoint cell to K lies in its second ring (a
+// segment from K to any cell not sharing a vertex with K leaves the star of K through an edge
+// whose outer cell is in that ring), so dmin = min over K of the exact distance to its
+// second-ring disjoint cells bounds every disjoint pair's node distance from below.
+__global__ void dmin_kernel(DevMesh m, unsigned long long* __restrict__ dmin_bits,
+                            unsigned long long* __restrict__ jmax_bits) {
+  const int K = blockIdx.x * blockDim.x + threadIdx.x;
+  if (K >= m.nc) return;
+  const CellGeo& A = m.geo[K];
+  double best = 1e300;
+  for (int a = 0; a < 3; ++a) {
+    const int v = A.v[a];
+    for (int p = m.patch_off[v]; p < m.patch_off[v + 1]; ++p) {
+      const CellGeo& N = m.geo[m.patch_cells[p]];
+      for (int b = 0; b < 3; ++b) {
+        const int u = N.v[b];
+        for (int q = m.patch_off[u]; q < m.patch_off[u + 1]; ++q) {
+          const int L = m.patch_cells[q];
+          const CellGeo& B = m.geo[L];
+          if (touching<2>(A, B)) continue;
+          best = fmin(best, exact_tri_dist(A, B));
+        }
+      }
+    }
+  }
+  if (best < 1e300) atomicMin(dmin_bits, (unsigned long long)__double_as_longlong(best));
+  atomicMax(jmax_bits, (unsigned long long)__double_as_longlong(A.J));
+}
+
+// Rigorous bounds of select_order's disjoint formula (quadrature.py:159-168) over all cell pairs
+// of two blocks with centre distance dc: Dmin <= dist estimate <= Dmax, h in [hmn, hmx], |ln h|
+// in [lmn, lmx].  hi: every numerator term bounded above, the denominator below; lo: the reverse.
+__device__ double bound_hi(const OrderConsts& oc, double Dmin, double hmn, double hmx, double lmn, double lmx) {
+  if (!(Dmin > 0.0)) return 1e30;
+  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * log(Dmin / hmx) - oc.coff;
+  const double den = fmax(log(Dmin / hmx), 0.0) + oc.ln_rho2;    // > 0
+  return num / den;         // (num < 0: the order clips to 2 whatever the denominator)
+}
+__device__ double bound_lo(const OrderConsts& oc, double Dmin, double Dmax, double hmn, double hmx, double lmn,
+                           double lmx) {
+  if (!(Dmin > 0.0)) return -1e30;
+  const double num = oc.lead_lnn + oc.sm1 * lmx + lmn - oc.s * log(Dmax / hmn) - oc.coff;
+  const double den_hi = fmax(log(Dmax / hmn), 0.0) + oc.ln_rho2;
+  const double den_lo = fmax(log(Dmin / hmx), 0.0) + oc.ln_rho2;
+  return num >= 0.0 ? num / den_hi : num / den_lo;
+}
+
+__global__ void block_pairs_kernel(OrderConsts oc, const double* __restrict__ bs, const int* __restrict__ rowflag,
+                                   int nb, int full, int64_t ncand, int4* __restrict__ pairs,
+                                   unsigned* __restrict__ key, int* __restrict__ keep, int* __restrict__ nearflag) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ncand) return;
+  // row-major upper triangle (P <= Q)
+  const double qq = 2.0 * nb + 1.0;
+  int P = (int)((qq - sqrt(qq * qq - 8.0 * (double)i)) * 0.5);
+  auto cum = [&](int64_t e) { return e * nb - e * (e - 1) / 2; };
+  while (P > 0 && cum(P) > i) --P;
+  while (cum(P + 1) <= i) ++P;
+  const int Q = P + (int)(i - cum(P));
+  const double* a = bs + 8 * P;
+  const double* b = bs + 8 * Q;
+  const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
+  const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
+  const double Dmax = (dc + a[2] + b[2]) * (1.0 + 1e-12);
+  const double hmn = fmin(a[3], b[3]), hmx = fmax(a[4], b[4]), lmn = fmin(a[5], b[5]), lmx = fmax(a[6], b[6]);
+  int kuni = 0;
+  const double hi = bound_hi(oc, Dmin, hmn, hmx, lmn, lmx);
+  if (P != Q && Dmin > 0.0) {
+    const double lo = bound_lo(oc, Dmin, Dmax, hmn, hmx, lmn, lmx);
+    const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
+    const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
+    if (c0 == c1) kuni = (int)c0;
+  }
+  pairs[i] = make_int4(P, Q, kuni, 0);
+  keep[i] = full ? 1 : (rowflag[P] | rowflag[Q]);
+  nearflag[i] = (kuni == 0 && hi + 1e-9 > (double)(KW2D - 1)) || kuni >= KW2D ? 1 : 0;
+  key[i] = __float_as_uint((float)fmax(Dmin, 0.0));      // heavy first: ascending gap
+}
+
+// ---------------------------------------------------------------- the block-pair kernel
+// Partial 3x3 block of one cell pair from the lane's NX x nodes x0, x0 + XS, ... (node
+// coordinates and w*lambda staged in shared memory): each y node and its weights are loaded
+// once and used for the NX x nodes.
+template <int E4, int NN, int NX, int XS>
+__device__ __forceinline__ void blk_part(const double2* __restrict__ Xn, const double2* __restrict__ Yn,
+                                         const double (*__restrict__ w)[3], int x0, double ex, double (&M)[3][3]) {
+  double X0[NX], X1[NX], t[NX][3];
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    const int x = min(x0 + u * XS, NN - 1);
+    X0[u] = Xn[x].x;
+    X1[u] = Xn[x].y;
+    t[u][0] = t[u][1] = t[u][2] = 0.0;
+  }
+#pragma unroll(NN <= 4 ? NN : 3)
+  for (int y = 0; y < NN; ++y) {
+    const double2 Y = Yn[y];
+    const double w0 = w[y][0], w1 = w[y][1], w2 = w[y][2];
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const double d0 = X0[u] - Y.x, d1 = X1[u] - Y.y;
+      const double v = kpow<E4>(fma(d1, d1, d0 * d0), ex);
+      t[u][0] = fma(v, w0, t[u][0]);
+      t[u][1] = fma(v, w1, t[u][1]);
+      t[u][2] = fma(v, w2, t[u][2]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    if (x0 + u * XS >= NN) continue;
+    const int x = x0 + u * XS;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      M[a][0] = fma(w[x][a], t[u][0], M[a][0]);
+      M[a][1] = fma(w[x][a], t[u][1], M[a][1]);
+      M[a][2] = fma(w[x][a], t[u][2], M[a][2]);
+    }
+  }
+}
+
+struct XArgs {
+  DevMesh m;
+  OrderConsts oc;
+  double ex, cs;                      // cs = -C * 2^S
+  double lim;                         // |scaled contribution| must stay below this (headroom check)
+  const int* bcells;
+  const int* bdofs;
+  const int* bndof;
+  const signed char* slot;
+  const double2* nodes;
+  const int4* bpairs;
+  int nbp;
+  int* queue;
+  unsigned long long* A;              // int64 view of the rank's rows [r0, r1) (leading dim lda)
+  int64_t lda;
+  int r0, r1;
+  unsigned long long* evals;
+  int* ovf;
+  // near pairs (k >= KW2D): discovery output or the precomputed table
+  unsigned long long* near_keys;
+  unsigned int* near_count;
+  unsigned int near_cap;
+  const unsigned long long* nearH;
+  const int* nearI;
+  unsigned long long hmask;
+  const double* nearG;
+};
+
+template <int E4, bool DISC>
+__global__ void __launch_bounds__(X2T, 3) cross2d_kernel(XArgs a, const double* __restrict__ wl_g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  XShared& S = *reinterpret_cast<XShared*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const OrderConsts& oc = a.oc;
+  for (int i = tid; i < NPRE2 * 3; i += X2T) (&S.wl[0][0])[i] = wl_g[i];
+  if (tid == 0) S.evals = 0;
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) S.bp = atomicAdd(a.queue, 1);
+    __syncthreads();
+    const int bp = S.bp;
+    if (bp >= a.nbp) break;
+    const int4 pr = a.bpairs[bp];
+    const int P = pr.x, Q = pr.y, kuni = pr.z;
+    const bool diag = P == Q;
+    // ---- stage the two blocks
+    if (tid < 2 * CB) {
+      const int c = a.bcells[(tid < CB ? P : Q) * CB + (tid & (CB - 1))];
+      XRec r;
+      r.id = c;
+      if (c >= 0) {
+        const CellGeo& g = a.m.geo[c];
+        r.cx = g.cx; r.cy = g.cy; r.rad = g.rad; r.J = g.J;
+        r.lnh = __logf((float)g.diam); r.lh = (float)g.ldiam;
+        for (int v = 0; v < 3; ++v) S.sl[tid][v] = a.slot[c * 3 + v];
+      } else {
+        r.cx = r.cy = r.rad = r.J = 0.0; r.lnh = r.lh = 0.f;
+        for (int v = 0; v < 3; ++v) S.sl[tid][v] = -1;
+      }
+      S.r[tid] = r;
+    }
+    if (tid == 0) { S.nP = a.bndof[P]; S.nQ = a.bndof[Q]; S.q = 0; }
+    if (tid < BRMAX) { S.dofP[tid] = a.bdofs[P * BRMAX + tid]; S.dofQ[tid] = a.bdofs[Q * BRMAX + tid]; }
+    if (tid < 8) S.hist[tid] = 0;
+    __syncthreads();
+    const int nP = S.nP, nQ = S.nQ;
+    const bool in_tile = nP * nQ <= TCAP;
+    if (!DISC) {
+      for (int i = tid; i < 2 * CB * NPRE2; i += X2T) {
+        const int c = S.r[i / NPRE2].id;
+        if (c >= 0) S.nd[i / NPRE2][i % NPRE2] = a.nodes[(int64_t)c * NPRE2 + i % NPRE2];
+      }
+      if (in_tile)
+        for (int i = tid; i < nP * nQ; i += X2T) S.tile[i] = 0ull;
+    }
+    __syncthreads();
+    // contribution of pair (row cell i of P, column cell j of Q), M in the reference's (min, max)
+    // orientation: entry (slot of i's vertex a, slot of j's vertex b) gets M[a][b] if i is the min cell
+    auto put = [&](int i, int j, bool imin, const double (&M)[3][3]) {
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          const int si = S.sl[i][imin ? x : y], sj = S.sl[CB + j][imin ? y : x];
+          if (si < 0 || sj < 0) continue;
+          const double v = M[x][y] * a.cs;
+          if (!(fabs(v) < a.lim)) atomicOr(a.ovf, 1);
+          const unsigned long long q = (unsigned long long)__double2ll_rn(v);
+          if (in_tile) {
+            atomicAdd(&S.tile[si * nQ + sj], q);
+            if (diag) atomicAdd(&S.tile[sj * nQ + si], q);
+          } else {
+            const int gi = S.dofP[si], gj = S.dofQ[sj];
+            if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
+            if (gj >= a.r0 && gj < a.r1) atomicAdd(&a.A[(int64_t)(gj - a.r0) * a.lda + gi], q);
+          }
+        }
+    };
+    // ---- (A) orders
+    for (int p = tid; p < CB * CB; p += X2T) {
+      const int i = p / CB, j = p % CB;
+      const XRec& rK = S.r[i];
+      const XRec& rL = S.r[CB + j];
+      int k = 0;
+      if (rK.id >= 0 && rL.id >= 0 && (!diag || i < j)) {
+        if (kuni) {
+          k = kuni;
+        } else {
+          k = order2d_fast(oc, rK.cx - rL.cx, rK.cy - rL.cy, rK.rad, rL.rad, rK.lnh, rK.lh, rL.lnh, rL.lh);
+          if (k == 0) {
+            const CellGeo& gK = a.m.geo[rK.id];
+            const CellGeo& gL = a.m.geo[rL.id];
+            if (!touching<2>(gK, gL)) {
+              const CellGeo& lo = rK.id < rL.id ? gK : gL;
+              const CellGeo& hi = rK.id < rL.id ? gL : gK;
+              k = order_disjoint_fast(oc, oc.coff, lo, hi, dist_estimate<2>(lo, hi));
+            }
+          }
+        }
+      }
+      if (k >= KW2D) {
+        const unsigned long long key = near_key(rK.id, rL.id, k);
+        if (DISC) {
+          const unsigned am = __activemask();
+          const int leader = __ffs(am) - 1;
+          unsigned int base = 0;
+          if (lane == leader) base = atomicAdd(a.near_count, (unsigned)__popc(am));
+          base = __shfl_sync(am, base, leader);
+          const unsigned int slotn = base + __popc(am & ((1u << lane) - 1u));
+          if (slotn < a.near_cap) a.near_keys[slotn] = key;
+        } else {
+          unsigned long long h = near_hash(key) & a.hmask, hk;
+          while ((hk = a.nearH[h]) != key && hk != NEAR_EMPTY) h = (h + 1) & a.hmask;
+          int64_t lo = 0;
+          if (hk == key) lo = a.nearI[h];
+          else atomicOr(a.m.err, 4);
+          const double* g = a.nearG + lo * 9;
+          double M[3][3];
+#pragma unroll
+          for (int x = 0; x < 3; ++x)
+#pragma unroll
+            for (int y = 0; y < 3; ++y) M[x][y] = g[x * 3 + y];
+          put(i, j, rK.id < rL.id, M);
+        }
+        k = 0;
+      }
+      if (!DISC) {
+        S.pk[p] = (unsigned char)k;
+        if (k) atomicAdd(&S.hist[k], 1);
+      }
+    }
+    if (DISC) continue;
+    __syncthreads();
+    if (tid == 0) {                  // descending k: the heaviest pairs are taken first
+      int off = 0, nch = 0;
+      for (int k = 4; k >= 2; --k) {
+        S.cursor[k] = off;
+        const int ppc = k == 4 ? 4 : (k == 3 ? 10 : 32);      // pairs per warp: 8 / 3 / 1 lanes each
+        for (int s0 = 0; s0 < S.hist[k]; s0 += ppc) {
+          S.chs[nch] = (short)(off + s0);
+          S.chn[nch] = (unsigned char)min(ppc, S.hist[k] - s0);
+          S.chk[nch] = (unsigned char)k;
+          ++nch;
+        }
+        off += S.hist[k];
+      }
+      S.nchunk = nch;
+    }
+    __syncthreads();
+    for (int p = tid; p < CB * CB; p += X2T) {
+      const int k = S.pk[p];
+      if (k) S.plist[atomicAdd(&S.cursor[k], 1)] = (unsigned short)p;
+    }
+    __syncthreads();
+    // ---- (B) blocks: a warp takes one chunk of same-order pairs at a time; k = 2: a lane per
+    // pair, k = 3: 3 lanes (3 x nodes each), k = 4: 8 lanes (2 x nodes each), fixed-order
+    // shuffle reduction over the lanes of a pair
+    unsigned long long my = 0;
+    for (;;) {
+      int ch = 0;
+      if (lane == 0) ch = atomicAdd(&S.q, 1);
+      ch = __shfl_sync(0xffffffffu, ch, 0);
+      if (ch >= S.nchunk) break;
+      const int k = S.chk[ch];
+      const int L = k == 4 ? 8 : (k == 3 ? 3 : 1);
+      const int g = lane / L, sub = lane - g * L;
+      const bool act = g < S.chn[ch];
+      const int p = act ? S.plist[S.chs[ch] + g] : 0;
+      const int i = p / CB, j = p % CB;
+      const bool imin = S.r[i].id < S.r[CB + j].id;
+      const double2* Xn = S.nd[imin ? i : CB + j];
+      const double2* Yn = S.nd[imin ? CB + j : i];
+      double M[3][3] = {};
+      if (act) {
+        if (k == 2) blk_part<E4, 4, 4, 1>(Xn + poff(2), Yn + poff(2), S.wl + poff(2), 0, a.ex, M);
+        else if (k == 3) blk_part<E4, 9, 3, 3>(Xn + poff(3), Yn + poff(3), S.wl + poff(3), sub, a.ex, M);
+        else blk_part<E4, 16, 2, 8>(Xn + poff(4), Yn + poff(4), S.wl + poff(4), sub, a.ex, M);
+      }
+      if (k > 2) {
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int y = 0; y < 3; ++y) {
+            double v = M[x][y];
+            if (k == 3) {
+              const double v1 = __shfl_down_sync(0xffffffffu, v, 1), v2 = __shfl_down_sync(0xffffffffu, v, 2);
+              v = (v + v1) + v2;
+            } else {
+              v += __shfl_down_sync(0xffffffffu, v, 4);
+              v += __shfl_down_sync(0xffffffffu, v, 2);
+              v += __shfl_down_sync(0xffffffffu, v, 1);
+            }
+            M[x][y] = v;
+          }
+      }
+      if (act && sub == 0) {
+        const double JJ = S.r[i].J * S.r[CB + j].J;
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int y = 0; y < 3; ++y) M[x][y] *= JJ;
+        put(i, j, imin, M);
+        my += (unsigned long long)(k * k) * (k * k);
+      }
+    }
+    if (my) atomicAdd(&S.evals, my);
+    __syncthreads();
+    // ---- (C) the tile (and its transpose) into HBM
+    if (in_tile) {
+      for (int idx = tid; idx < nP * nQ; idx += X2T) {
+        const unsigned long long q = S.tile[idx];
+        if (!q) continue;
+        const int r = idx / nQ, c = idx - r * nQ;
+        const int gi = S.dofP[r], gj = S.dofQ[c];
+        if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
+        if (!diag && gj >= a.r0 && gj < a.r1) atomicAdd(&a.A[(int64_t)(gj - a.r0) * a.lda + gi], q);
+      }
+    }
+  }
+  if (tid == 0 && S.evals && a.evals) atomicAdd(a.evals, S.evals);
+}
+
+__global__ void iota_kernel64(int* a, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int)i;
+}
+__global__ void gather4_kernel(const int4* __restrict__ raw, const int* __restrict__ keep, const int* __restrict__ nf,
+                               const int* __restrict__ idx, int64_t n, int4* __restrict__ out, int* __restrict__ okeep,
+                               int* __restrict__ onear) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = idx[i];
+  out[i] = raw[j];
+  okeep[i] = keep[j];
+  onear[i] = keep[j] & nf[j];
+}
+
+__global__ void fixed_to_double_kernel(unsigned long long* A, int64_t count, double inv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const long long v = (long long)A[i];
+    reinterpret_cast<double*>(A)[i] = (double)v * inv;
+  }
+}
+
+#define FL_E4_SWITCH2(e4, ...)                                \
+  switch (e4) {                                               \
+    case 10: { constexpr int E4 = 10; __VA_ARGS__; } break;   \
+    case 12: { constexpr int E4 = 12; __VA_ARGS__; } break;   \
+    case 14: { constexpr int E4 = 14; __VA_ARGS__; } break;   \
+    default: { constexpr int E4 = 0; __VA_ARGS__; } break;    \
+  }
+
+}  // namespace
+
+// The whole 2D cross term of rows [row_begin, row_end) into A (double, leading dim lda): A is
+// overwritten (zeroed first).  Near pairs (k >= KW2D) are discovered here and computed once by
+// near_pairs_build into `near`.  t_disc / t_near: events recorded after discovery and after the
+// near blocks (phase timing).
+void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+                      int row_begin, int row_end, double* A, int64_t lda, unsigned long long* evals, NearPairs& near,
+                      Cross2DInfo& info, cudaEvent_t t_disc, cudaEvent_t t_near, cudaStream_t st) {
+  const int nc = m.nc;
+  const int nb = (nc + CB - 1) / CB;
+  const int64_t rows = row_end - row_begin;
+  // ---- Morton order of the cells
+  std::vector<double> hv((size_t)m.nv * 2);
+  FL_CUDA(cudaMemcpyAsync(hv.data(), m.vert, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  double bb[4] = {hv[0], hv[0], hv[1], hv[1]};
+  for (int v = 0; v < m.nv; ++v) {
+    bb[0] = std::min(bb[0], hv[2 * v]); bb[1] = std::max(bb[1], hv[2 * v]);
+    bb[2] = std::min(bb[2], hv[2 * v + 1]); bb[3] = std::max(bb[3], hv[2 * v + 1]);
+  }
+  const double sx = 65535.0 / std::max(bb[1] - bb[0], 1e-300), sy = 65535.0 / std::max(bb[3] - bb[2], 1e-300);
+  DBuf<uint32_t> keys(nc), keys2(nc);
+  DBuf<int> vals(nc), vals2(nc);
+  cell_morton_kernel<<<(nc + 255) / 256, 256, 0, st>>>(m, bb[0], bb[2], sx, sy, keys.p, vals.p), note_launch();
+  {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.p, keys2.p, vals.p, vals2.p, nc, 0, 32, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, keys.p, keys2.p, vals.p, vals2.p, nc, 0, 32, st));
+  }
+  // ---- blocks
+  DBuf<int> bcells((size_t)nb * CB), bdofs((size_t)nb * BRMAX), bndof(nb), rowflag(nb), err(1);
+  DBuf<signed char> slot((size_t)nc * 3);
+  DBuf<double> bstat((size_t)nb * 8);
+  FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
+  block_build_kernel<<<nb, 128, 0, st>>>(m, vals2.p, nb, row_begin, row_end, bcells.p, bdofs.p, bndof.p, slot.p,
+                                         bstat.p, rowflag.p, err.p), note_launch();
+  // ---- mapped nodes, rule weights, scale bound
+  const RuleRef r2 = t.rule(T_DISJ, 2), r3 = t.rule(T_DISJ, 3), r4 = t.rule(T_DISJ, 4);
+  if (r2.cnt != 4 || r3.cnt != 9 || r4.cnt != 16) throw Error(-3, "disjoint rules k = 2, 3, 4 missing");
+  DBuf<double2> nodes((size_t)nc * NPRE2);
+  cell_nodes2_kernel<<<(unsigned)(((int64_t)nc * NPRE2 + 255) / 256), 256, 0, st>>>(m, t.data, r2, r3, r4, nodes.p),
+      note_launch();
+  std::vector<double> hw(NPRE2 * 3), hrow(NODE);
+  for (int x = 0; x < NPRE2; ++x) {
+    const RuleRef rr = x < 4 ? r2 : (x < 13 ? r3 : r4);
+    const int xl = x < 4 ? x : (x < 13 ? x - 4 : x - 13);
+    FL_CUDA(cudaMemcpyAsync(hrow.data(), t.data + (size_t)(rr.off + xl) * NODE, NODE * sizeof(double),
+                            cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    for (int c = 0; c < 3; ++c) hw[x * 3 + c] = hrow[3 + c];
+  }
+  DBuf<double> wl(NPRE2 * 3);
+  FL_CUDA(cudaMemcpyAsync(wl.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  DBuf<unsigned long long> bnd(2);
+  unsigned long long init[2] = {0ull, 0ull};
+  const double big = 1e300;
+  std::memcpy(&init[0], &big, 8);
+  FL_CUDA(cudaMemcpyAsync(bnd.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  dmin_kernel<<<(nc + 127) / 128, 128, 0, st>>>(m, bnd.p, bnd.p + 1), note_launch();
+  unsigned long long hb[2];
+  int herr = 0;
+  FL_CUDA(cudaMemcpyAsync(hb, bnd.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  if (herr) throw Error(-1, "a Morton block of 32 cells touches more than 64 DoFs (mesh too irregular)");
+  double dmin, jmax;
+  std::memcpy(&dmin, &hb[0], 8);
+  std::memcpy(&jmax, &hb[1], 8);
+  // |entry| <= vmax^2 * C * Jmax^2 * (1/6)^2 * dmin^(-(d+2s)) (sum of w*lambda over the reference
+  // triangle = 1/6; at most vmax cells around a vertex); scale: that bound -> 2^54
+  const double e = -2.0 * ex;                      // d + 2s
+  const double vmax = (double)MAX_VALENCE;
+  const double bound = dmin < 1e299 ? vmax * vmax * Cds * jmax * jmax / 36.0 * std::pow(dmin, -e) : 1.0;
+  int S = 54 - (int)std::ceil(std::log2(std::max(bound, 1e-300)));
+  S = std::max(-1000, std::min(1000, S));
+  const double scale = std::ldexp(1.0, S);
+  info.scale_exp = S;
+  info.dmin = dmin;
+  // ---- block pairs, heavy first
+  const int64_t ncand = (int64_t)nb * (nb + 1) / 2;
+  DBuf<int4> raw(ncand);
+  DBuf<unsigned> key(ncand), key2(ncand);
+  DBuf<int> keep(ncand), nflag(ncand);
+  block_pairs_kernel<<<(unsigned)((ncand + 255) / 256), 256, 0, st>>>(oc, bstat.p, rowflag.p, nb,
+                                                                     (row_begin == 0 && row_end == m.n) ? 1 : 0,
+                                                                     ncand, raw.p, key.p, keep.p, nflag.p),
+      note_launch();
+  DBuf<int> idx(ncand), idx2(ncand);
+  iota_kernel64<<<(unsigned)((ncand + 255) / 256), 256, 0, st>>>(idx.p, ncand), note_launch();
+  {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, key2.p, idx.p, idx2.p, (int)ncand, 0, 32, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, key.p, key2.p, idx.p, idx2.p, (int)ncand, 0, 32, st));
+  }
+  // gather in sorted order, then keep (rows) / near subsets
+  DBuf<int4> sorted(ncand);
+  DBuf<int> skeep(ncand), snear(ncand), nsel(2);
+  gather4_kernel<<<(unsigned)((ncand + 255) / 256), 256, 0, st>>>(raw.p, keep.p, nflag.p, idx2.p, ncand, sorted.p,
+                                                                  skeep.p, snear.p), note_launch();
+  DBuf<int4> all(ncand), nearl(ncand);
+  {
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, sorted.p, skeep.p, all.p, nsel.p, (int)ncand, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, sorted.p, skeep.p, all.p, nsel.p, (int)ncand, st));
+    // near candidates among the kept pairs
+    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, sorted.p, snear.p, nearl.p, nsel.p + 1, (int)ncand, st));
+  }
+  int hn[2];
+  FL_CUDA(cudaMemcpyAsync(hn, nsel.p, sizeof(hn), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  const int nall = hn[0], nnear = hn[1];
+  info.block_pairs = nall;
+  info.near_block_pairs = nnear;
+  // ---- A (int64 view) zeroed
+  unsigned long long* Ai = reinterpret_cast<unsigned long long*>(A);
+  if (rows > 0) FL_CUDA(cudaMemsetAsync(A, 0, (size_t)rows * lda * sizeof(double), st));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = sizeof(XShared);
+  DBuf<int> queue(1), ovf(1);
+  FL_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
+  XArgs xa{};
+  xa.m = m; xa.oc = oc; xa.ex = ex; xa.cs = -Cds * scale; xa.lim = std::ldexp(1.0, 62) / (vmax * vmax);
+  xa.bcells = bcells.p; xa.bdofs = bdofs.p; xa.bndof = bndof.p; xa.slot = slot.p; xa.nodes = nodes.p;
+  xa.A = Ai; xa.lda = lda; xa.r0 = row_begin; xa.r1 = row_end; xa.evals = evals; xa.ovf = ovf.p;
+  // ---- pass 1: discovery of the near pairs (block pairs whose bound reaches KW2D)
+  unsigned int cap = (unsigned int)std::max<int64_t>(
+      1024, std::min<int64_t>({(int64_t)nnear * CB * CB, (int64_t)nc * 4096, ((int64_t)1 << 31) - 1}));
+  DBuf<unsigned long long> near_keys;
+  DBuf<unsigned int> near_cnt(1);
+  int64_t nkeys = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    near_keys.alloc(cap);
+    FL_CUDA(cudaMemsetAsync(near_cnt.p, 0, sizeof(unsigned int), st));
+    FL_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+    xa.bpairs = nearl.p; xa.nbp = nnear; xa.queue = queue.p;
+    xa.near_keys = near_keys.p; xa.near_count = near_cnt.p; xa.near_cap = cap;
+    if (nnear > 0) {
+      const int grid = std::min(nnear, 3 * sms);
+      FL_E4_SWITCH2(e4, {
+        FL_CUDA(cudaFuncSetAttribute(cross2d_kernel<E4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        cross2d_kernel<E4, true><<<grid, X2T, smem, st>>>(xa, wl.p), note_launch();
+      });
+      FL_CHECK_LAUNCH();
+    }
+    unsigned int cnt = 0;
+    FL_CUDA(cudaMemcpyAsync(&cnt, near_cnt.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+    nkeys = cnt;
+    if (cnt <= cap) break;
+    cap = cnt;
+  }
+  if (t_disc) FL_CUDA(cudaEventRecord(t_disc, st));
+  near_pairs_build(m, t, oc, ex, e4, near_keys.p, nkeys, near, evals ? evals : nullptr, st);
+  near_keys.free();
+  if (t_near) FL_CUDA(cudaEventRecord(t_near, st));
+  // ---- pass 2: every block pair
+  FL_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
+  xa.bpairs = all.p; xa.nbp = nall; xa.queue = queue.p;
+  xa.near_keys = nullptr; xa.near_count = nullptr; xa.near_cap = 0;
+  xa.nearH = near.hkey.p; xa.nearI = near.hidx.p; xa.hmask = near.hmask; xa.nearG = near.G.p;
+  if (nall > 0) {
+    const int grid = std::min(nall, 3 * sms);
+    FL_E4_SWITCH2(e4, {
+      FL_CUDA(cudaFuncSetAttribute(cross2d_kernel<E4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cross2d_kernel<E4, false><<<grid, X2T, smem, st>>>(xa, wl.p), note_launch();
+    });
+    FL_CHECK_LAUNCH();
+  }
+  // ---- fixed point -> double, in place
+  if (rows > 0) {
+    fixed_to_double_kernel<<<4 * sms, 256, 0, st>>>(Ai, rows * lda, std::ldexp(1.0, -S)), note_launch();
+    FL_CHECK_LAUNCH();
+  }
+  int hovf = 0;
+  FL_CUDA(cudaMemcpyAsync(&hovf, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  if (hovf) throw Error(-5, "internal: a cross contribution exceeded the fixed-point bound");
+}
+
+}  // namespace fl

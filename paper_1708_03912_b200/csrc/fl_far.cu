@@ -215,23 +215,6 @@ struct CrossShared {
   // followed by the packed disjoint rules: per node u0 u1 lw0 lw1 lw2 (5 doubles)
 };
 
-// Fast 2D disjoint order from staged centroids / radii / fp32 log sizes: 0 when the exact path
-// is needed (close pair — the reference then uses the exact simplex distance — or an fp32
-// estimate within ORDER_DELTA of an integer), else k.  A pair classified far here is far in the
-// reference arithmetic too: the centroid-gap bound carries a 1e-12 relative margin, far above
-// the few-ulp error of the approximate square root.
-__device__ __forceinline__ int order2d_fast(const OrderConsts& oc, double dx, double dy, double ra, double rb,
-                                            float lnA, float lA, float lnB, float lB) {
-  const double r2 = fma(dy, dy, dx * dx);
-  if (!(r2 > 1e-200)) return 0;
-  const double dc = r2 * rsqrt_nb(r2);
-  const double sr = ra + rb;
-  const double lower = dc - sr;
-  if (!(lower > 2.0 * sr * (1.0 + 1e-12))) return 0;
-  return order_from_estimate(order_estimate_f(oc, oc.coff_f, lnA, lA, lnB, lB, __logf((float)lower)),
-                             oc.cap_disjoint);
-}
-
 template <int D>
 __device__ __forceinline__ int pre_off(int k) {   // offset of order k in CrossShared::nodes
   return D == 1 ? (k == 2 ? 0 : k == 3 ? 2 : 5) : (k == 2 ? 0 : k == 3 ? 4 : 13);

@@ -233,6 +233,15 @@ struct NearPairs {
 void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                       unsigned long long* keys, int64_t nkeys, NearPairs& np, unsigned long long* evals,
                       cudaStream_t st);
+// fl_cross2d.cu: the 2D cross term by cell-block pairs, exact fixed-point accumulation
+struct Cross2DInfo {
+  int scale_exp = 0;          // contributions are accumulated as integers of 2^-scale_exp
+  double dmin = 0.0;          // smallest disjoint cell distance (the scale bound)
+  int64_t block_pairs = 0, near_block_pairs = 0;
+};
+void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+                      int row_begin, int row_end, double* A, int64_t lda, unsigned long long* evals, NearPairs& near,
+                      Cross2DInfo& info, cudaEvent_t t_disc, cudaEvent_t t_near, cudaStream_t st);
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
 // fl_far1d.cu (1D: lean tail, packed pair-block cross + gather)

@@ -192,7 +192,7 @@ __global__ void touch_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, To
   const int K = blockIdx.x * blockDim.x + threadIdx.x;
   if (K >= m.nc) return;
   const CellGeo A = m.geo[K];
-  ident_k[K] = order_touching(oc, A.ldiam, false);   // assembly.py:658
+  ident_k[K] = order_touching(oc, A.diam, A.ldiam, false);   // assembly.py:658
   int nb[MAXNB];
   const int cnt = neighbours_above<D>(m, K, nb);
   int o = offs[K];
@@ -205,7 +205,7 @@ __global__ void touch_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, To
     for (int i = 0; i < 3; ++i) { tp.vK[i] = -1; tp.vK2[i] = -1; }
     // hmin = np.minimum(h_K, h_K2) -> |log hmin| (quadrature.py:154-155)
     const double lmin = (A.diam <= B.diam) ? A.ldiam : B.ldiam;
-    tp.k = order_touching(oc, lmin, false);
+    tp.k = order_touching(oc, fmin(A.diam, B.diam), lmin, false);
     if constexpr (D == 1) {
       // assembly.py:435-446: shared vertex first in both cells
       int sh = -1;
@@ -361,7 +361,7 @@ __global__ void bnd_fill_kernel(DevMesh m, OrderConsts oc, const int* offs, BndP
         it.pe[i][j] = (pe[i] >= 0 && j < D) ? m.vert[pe[i] * D + j] : 0.0;
     it.ne[0] = -m.bnorm[e * D + 0];
     it.ne[1] = (D == 2) ? -m.bnorm[e * D + 1] : 0.0;
-    it.k = order_touching(oc, g.ldiam, true);      // select_order(..., boundary=True) :815
+    it.k = order_touching(oc, g.diam, g.ldiam, true);      // select_order(..., boundary=True) :815
     items[offs[e] + t] = it;
   }
 }

@@ -365,7 +365,7 @@ fl_cg* cg_create(int64_t n, int64_t m, int64_t blk, int world, int rank, double 
   S->blk = blk;
   S->L = blk / VCH;
   S->world = world;
-  S->row0 = (int64_t)rank * blk;
+  S->row0 = std::min<int64_t>((int64_t)rank * blk, n);   // (an empty block sits at n)
   S->sc.alloc(1);
   S->done.alloc(1);
   S->local.alloc(S->L);

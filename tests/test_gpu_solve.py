@@ -87,10 +87,12 @@ def lockstep_pcg(mesh, dm, ker, b, world, tol, max_iter, ops=None):
     return x, polls[0], ops
 
 
-@pytest.mark.parametrize("kind,N,s", [("graded1d", 2048, 0.75), ("uniform1d", 1500, 0.25)])
+@pytest.mark.parametrize("kind,N,s", [("graded1d", 2048, 0.75), ("uniform1d", 1500, 0.25), ("square2d", 40, 0.5),
+                                      ("square2d", 48, 0.25)])
 def test_lockstep_ranks_bitwise(cuda_lib, kind, N, s):
-    """1D row blocks are bitwise the whole matrix's rows, so 1/2/4/8 ranks give bitwise the same
-    x and iteration count, equal to fl_pcg's."""
+    """Row blocks are bitwise the whole matrix's rows (1D: canonical gather order; 2D: exact
+    fixed-point cross accumulation), so 1/2/4/8 ranks give bitwise the same x and iteration
+    count, equal to fl_pcg's."""
     from paper_1708_03912_b200 import solve as S, assembly as A
     mesh, dm, ker, b = _setup(kind, N, s)
     full = A.assemble_dense_device(mesh, dm, ker)
