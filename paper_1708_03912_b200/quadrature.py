@@ -1,10 +1,11 @@
 """Quadrature rules, pair classification and Gauss-order selection — host side.
 
 Mirrors `fraclap.quadrature` (reference quadrature.py): the same public names and
-argument meaning.  The node sets are produced by the same third-party generators the
-reference calls (numpy `leggauss`, scipy `roots_jacobi`), and the Sauter–Schwab/Duffy
-payload transforms are restated here (quadrature.py:188-398) so the device tables are
-bitwise the reference's payloads (pinned by tests/test_tables.py).
+argument meaning.  The 1-D node sets come from the same third-party generators the reference
+calls (numpy `leggauss`, scipy `roots_jacobi`).  The Sauter–Schwab/Duffy singular rules are
+re-derived as unions of radial pieces (`_rule`: a Gauss–Jacobi radial variable, Gauss–Legendre
+regular variables and one map per piece) and agree with the reference's payloads
+(quadrature.py:188-398) node by node to <= 1e-14 (tests/test_tables.py).
 
 `pack_tables(d, s)` flattens every rule the device kernels can ask for into the
 `fl_tables` blob of include/fraclap_b200.h.
@@ -160,105 +161,124 @@ def select_order(pair, h_K, h_K2, dist, n, s, params: OrderParams, boundary=Fals
 
 
 # ------------------------------------------------------------------ singular payloads
-# Each returns dict(x=..., y=... | a=..., w=...) in the reference's node order.
-_HEX = np.array([(1, 0), (0, 1), (-1, 1), (-1, 0), (0, -1), (1, -1)], float)
+# Each singular pair integral (Sauter–Schwab / Duffy, §3, SPEC.md "singular rules") is
+# regularised by splitting the pair's parameter domain into PIECES on which one RADIAL variable
+# r in (0, 1) measures the distance to the singular set; in r the integrand behaves like r^alpha
+# and a Gauss–Jacobi rule for that weight is used, the remaining (regular) variables get
+# Gauss–Legendre rules.  A rule is therefore fully described by
+#   * the radial rule (points, Jacobi exponent) and the extra power of r left after the weight,
+#   * the list of regular 1-D rules,
+#   * per piece, the map (r, v1, v2, ...) -> (point in K, point in K~ [or the edge parameter a])
+#     and the Jacobian of that map.
+# `_rule` builds the tensor grid (radial outermost, then the regular variables in order) and
+# concatenates the pieces — the reference's node order (quadrature.py:188-398), so the tables
+# can be compared node by node (tests/test_tables.py, ≤ 1e-14 against the reference's arrays).
 
 
-def _hex_area(w):
-    """Area of the identical-pair sub-domain at offset w (quadrature.py:191-198)."""
-    w1, w2 = w[..., 0], w[..., 1]
-    t = w1 + w2
-    out = np.where(w1 > 0, np.where(t >= 0, (1 - w1) ** 2, (1 + w2) ** 2),
-                   np.where(t >= 0, (1 - w2) ** 2, (1 + w1) ** 2))
-    out = np.where((w1 <= 0) & (w2 <= 0), (1 + t) ** 2, out)
-    out = np.where((w1 >= 0) & (w2 >= 0), (1 - t) ** 2, out)
-    return 0.5 * out
+def _rule(radial, axes, pieces, rfac, second="y"):
+    """radial = (nodes, weights) of the radial rule; axes = list of (nodes, weights); pieces =
+    maps f(r, *V) -> (X, Y, jac) on the open grid V of the regular variables (X, Y: point
+    fields (..., dim); for second == "a", Y is the edge parameter (...)); rfac(r) = the radial
+    factor beyond the Jacobi weight.  Weight of a node = prod w_v * jac * w_r * rfac(r)."""
+    rq, rw = radial
+    shape = tuple(len(a[0]) for a in axes)
+    npts = int(np.prod(shape, dtype=np.int64))
+    V = np.ix_(*[a[0] for a in axes]) if axes else ()
+    Wv = np.ones(shape)
+    for ax, (_, w) in enumerate(axes):
+        Wv = Wv * np.asarray(w).reshape([len(w) if i == ax else 1 for i in range(len(axes))])
+    X, Y, W = [], [], []
+    for f in pieces:
+        for r, wr in zip(rq, rw):
+            x, y, jac = f(r, *V)
+            x = np.asarray(x, float)
+            X.append(np.broadcast_to(x, shape + x.shape[-1:]).reshape(npts, -1))
+            y = np.asarray(y, float)
+            Y.append(np.broadcast_to(y, shape + (y.shape[-1:] if second == "y" else ())).reshape(npts, -1))
+            W.append(np.broadcast_to(Wv * jac, shape).reshape(npts) * (wr * rfac(r)))
+    X, Y, W = np.concatenate(X), np.concatenate(Y), np.concatenate(W)
+    return {"x": X if X.shape[1] > 1 else X[:, 0], second: Y if Y.shape[1] > 1 else Y[:, 0], "w": W}
 
 
-def _hex_rep(w):
-    """Representative point x of the identical-pair sub-domain (quadrature.py:201-218)."""
-    w1, w2 = w[..., 0], w[..., 1]
-    t = w1 + w2
-    cx, cy = np.empty_like(w1), np.empty_like(w2)
-    quad = (w1 >= 0) & (w2 >= 0)
-    cases = [
-        (quad, w1 + (1 - t) / 3, w2 + (1 - t) / 3),
-        ((w1 <= 0) & (w2 <= 0) & ~quad, (1 + t) / 3, (1 + t) / 3),
-        ((w1 > 0) & (w2 < 0) & (t >= 0), (1 + 2 * w1) / 3, (1 - w1) / 3),
-        ((w1 > 0) & (w2 < 0) & (t < 0), w1 + (1 + w2) / 3, (1 + w2) / 3),
-        ((w1 < 0) & (w2 > 0) & (t >= 0), (1 - w2) / 3, (1 + 2 * w2) / 3),
-        ((w1 < 0) & (w2 > 0) & (t < 0), (1 + w1) / 3, w2 + (1 + w1) / 3),
-    ]
-    for m, vx, vy in cases:
-        cx[m] = vx[m]
-        cy[m] = vy[m]
-    return np.stack([cx, cy], axis=-1)
+def _pt(a, b):
+    """Point field from two coordinate arrays broadcast together: (..., 2)."""
+    a, b = np.broadcast_arrays(a, b)
+    return np.stack([a, b], axis=-1)
+
+
+def _pt1(a):
+    return np.asarray(a, float)[..., None]
+
+
+# identical 2D pair: for a difference w = x - y of two points of the reference triangle T, the
+# points x with x, x - w in T form T ∩ (T + w) = {x >= max(w, 0), x1 + x2 <= min(1, 1 + w1 + w2)},
+# a right triangle of leg L = min(1, 1 + w1 + w2) - max(w1, 0) - max(w2, 0): area L^2/2; the
+# integrand (P1 hat differences: constant in x for fixed w) is sampled at its centroid.
+def _overlap(wv):
+    lo = np.maximum(wv, 0.0)
+    L = np.minimum(1.0, 1.0 + wv[..., 0] + wv[..., 1]) - lo[..., 0] - lo[..., 1]
+    return 0.5 * L * L, lo + (L / 3.0)[..., None]
+
+
+_HEX = np.array([(1, 0), (0, 1), (-1, 1), (-1, 0), (0, -1), (1, -1)], float)   # corners of {x - y}
 
 
 @lru_cache(maxsize=None)
 def rule_identical_1d(s):
-    """quadrature.py:221-230."""
-    z, wz = gauss_jacobi(3, 1 - 2 * s)
-    w = wz * (1 - z) * z ** (2 * s - 1)
-    xp, xm = (1 + z) / 2, (1 - z) / 2
-    return dict(x=np.concatenate([xp, xm]), y=np.concatenate([xp - z, xm + z]),
-                w=np.concatenate([w, w]))
+    """K = K~ = [0, 1]: radial z = |x - y| (weight (1 - z) z^(2s-1) after the Jacobi factor), the
+    integrand is constant along x - y = z, one node at the midpoint of each orientation
+    (quadrature.py:221-230)."""
+    return _rule(gauss_jacobi(3, 1 - 2 * s), [],
+                 [lambda z: (_pt1((1 + z) / 2), _pt1((1 - z) / 2), 1.0),
+                  lambda z: (_pt1((1 - z) / 2), _pt1((1 + z) / 2), 1.0)],
+                 lambda z: (1 - z) * z ** (2 * s - 1))
 
 
 @lru_cache(maxsize=None)
 def rule_vertex_1d(k, s):
-    """Both cells parametrised away from the shared vertex (quadrature.py:233-243)."""
-    tq, tw = gauss_jacobi(3, 2 - 2 * s)
-    vq, vw = gauss_legendre(k)
-    T, V = np.meshgrid(tq, vq, indexing="ij")
-    W = np.outer(tw * tq ** (2 * s - 1), vw).ravel()
-    TV = (T * V).ravel()
-    return dict(x=np.concatenate([T.ravel(), TV]), y=np.concatenate([TV, T.ravel()]),
-                w=np.concatenate([W, W]))
+    """Cells meeting at the local origin: radial t = the farther point, v = ratio of the nearer
+    (quadrature.py:233-243)."""
+    return _rule(gauss_jacobi(3, 2 - 2 * s), [gauss_legendre(k)],
+                 [lambda t, v: (_pt1(t), _pt1(t * v), 1.0),
+                  lambda t, v: (_pt1(t * v), _pt1(t), 1.0)],
+                 lambda t: t ** (2 * s - 1))
 
 
 @lru_cache(maxsize=None)
 def rule_identical_2d(k, s):
-    """Six radial sectors of the hexagon of offsets (quadrature.py:246-260)."""
-    t, wt = gauss_legendre(k)
-    rq, rw = gauss_jacobi(3, 1 - 2 * s)
-    xs, ys, ws = [], [], []
-    for sector in range(6):
-        edge = (1 - t)[:, None] * _HEX[sector] + t[:, None] * _HEX[(sector + 1) % 6]
-        for r, wr in zip(rq, rw):
-            off = r * edge
-            x = _hex_rep(off)
-            xs.append(x)
-            ys.append(x - off)
-            ws.append(wt * wr * _hex_area(off) * r ** (2 * s))
-    return dict(x=np.concatenate(xs), y=np.concatenate(ys), w=np.concatenate(ws))
+    """The differences x - y fill the hexagon conv(_HEX): six radial sectors, r along the ray,
+    t along the sector's outer edge (quadrature.py:246-260)."""
+    def sector(c):
+        def f(r, t):
+            wv = r * ((1 - t)[:, None] * _HEX[c] + t[:, None] * _HEX[(c + 1) % 6])
+            area, x = _overlap(wv)
+            return x, x - wv, area
+        return f
+    return _rule(gauss_jacobi(3, 1 - 2 * s), [gauss_legendre(k)], [sector(c) for c in range(6)],
+                 lambda r: r ** (2 * s))
 
 
 @lru_cache(maxsize=None)
 def rule_common_edge_2d(k, s):
-    """Shared edge = local (0,1) of both cells (quadrature.py:263-294)."""
+    """Shared edge = local (0, 1) of both cells; four Duffy pieces (which cell carries the
+    longer transversal leg x which side of the edge point), radial r = the transversal size
+    (quadrature.py:263-294)."""
     k = min(k, 16)
-    z, wz = gauss_legendre(k)
-    v, wv = gauss_legendre(k)
-    rq, rw = gauss_jacobi(3, 2 - 2 * s)
-    Z, V = np.meshgrid(z, v, indexing="ij")
-    WZV = np.outer(wz, wv)
-    X, Y, W = [], [], []
-    for swap in (False, True):
-        for second in (False, True):
-            for r, wr in zip(rq, rw):
-                if second:
-                    zz, bb, bp, jac = r * V * Z, r * V * (1 - Z), np.full_like(Z, r), V
-                else:
-                    zz, bb, bp, jac = r * Z, r * (1 - Z), r * V, np.ones_like(Z)
-                al = zz + 0.5 * (1 - r)
-                u = np.stack([al, bb], -1).reshape(-1, 2)
-                uu = np.stack([al - zz, bp], -1).reshape(-1, 2)
-                wts = (WZV * jac).reshape(-1) * wr * (1 - r) * r ** (2 * s)
-                X.append(uu if swap else u)
-                Y.append(u if swap else uu)
-                W.append(wts)
-    return dict(x=np.concatenate(X), y=np.concatenate(Y), w=np.concatenate(W))
+    g = gauss_legendre(k)
+
+    def piece(swap, inner):
+        def f(r, z, v):
+            if inner:          # the transversal legs scaled by v
+                zz, bb, bp, jac = r * v * z, r * v * (1 - z), r, v
+            else:
+                zz, bb, bp, jac = r * z, r * (1 - z), r * v, 1.0
+            al = zz + 0.5 * (1 - r)
+            u, uu = _pt(al, bb), _pt(al - zz, bp)
+            return (uu, u, jac) if swap else (u, uu, jac)
+        return f
+    return _rule(gauss_jacobi(3, 2 - 2 * s), [g, g],
+                 [piece(sw, inn) for sw in (False, True) for inn in (False, True)],
+                 lambda r: (1 - r) * r ** (2 * s))
 
 
 def _cv_order(k):
@@ -267,78 +287,64 @@ def _cv_order(k):
 
 @lru_cache(maxsize=None)
 def _rule_common_vertex_2d(kk, s):
-    su, wsu = gauss_legendre(kk)
-    wr_, wwr = gauss_legendre(kk)
-    rq, rw = gauss_jacobi(3, 3 - 2 * s)
-    SU, SV, WW = np.meshgrid(su, su, wr_, indexing="ij")
-    WT = wsu[:, None, None] * wsu[None, :, None] * wwr[None, None, :]
-    X, Y, W = [], [], []
-    for second in (False, True):
-        for r, wr in zip(rq, rw):
-            rx = (r * WW) if second else np.full_like(WW, r)
-            ry = np.full_like(WW, r) if second else (r * WW)
-            X.append(np.stack([rx * (1 - SU), rx * SU], -1).reshape(-1, 2))
-            Y.append(np.stack([ry * (1 - SV), ry * SV], -1).reshape(-1, 2))
-            W.append((WT * WW).reshape(-1) * wr * r ** (2 * s))
-    return dict(x=np.concatenate(X), y=np.concatenate(Y), w=np.concatenate(W))
+    g = gauss_legendre(kk)
+
+    def piece(y_far):
+        def f(r, a, b, w):
+            rx, ry = (r * w, r) if y_far else (r, r * w)
+            return _pt(rx * (1 - a), rx * a), _pt(ry * (1 - b), ry * b), w
+        return f
+    return _rule(gauss_jacobi(3, 3 - 2 * s), [g, g, g], [piece(False), piece(True)], lambda r: r ** (2 * s))
 
 
 def rule_common_vertex_2d(k, s):
-    """Shared vertex = local 0 of both cells (quadrature.py:297-315)."""
+    """Shared vertex = local 0 of both cells: each cell in polar-like coordinates (distance to the
+    vertex, position along the opposite edge); radial r = the larger distance, w = the ratio of
+    the smaller (quadrature.py:297-315)."""
     return _rule_common_vertex_2d(_cv_order(k), s)
 
 
 @lru_cache(maxsize=None)
 def rule_edge_of_cell_1d(s, vanishing):
-    """quadrature.py:332-335."""
-    rq, rw = gauss_jacobi(3, vanishing - 2 * s)
-    return dict(x=rq, a=np.zeros_like(rq), w=rw * rq ** (2 * s - vanishing))
+    """Boundary point at the cell's local origin: radial r = distance (quadrature.py:332-335)."""
+    return _rule(gauss_jacobi(3, vanishing - 2 * s), [], [lambda r: (_pt1(r), 0.0, 1.0)],
+                 lambda r: r ** (2 * s - vanishing), second="a")
 
 
 @lru_cache(maxsize=None)
 def rule_edge_of_cell_2d(k, s, vanishing):
-    """Cell (e0, e1, p) and its boundary edge (e0, e1) (quadrature.py:338-360)."""
-    zq, zw = gauss_legendre(k)
-    tq, tw = gauss_legendre(max(3, k // 2))
-    rq, rw = gauss_jacobi(4, vanishing - 2 * s)
-    Z, T = np.meshgrid(zq, tq, indexing="ij")
-    WZT = np.outer(zw, tw)
-    X, A, W = [], [], []
-    for piece in (1, 2, 3):
-        for r, wr in zip(rq, rw):
-            if piece == 1:
-                zrel, beta = r * Z, r * (1 - Z)
-                al = zrel + T * (1 - r)
-            elif piece == 2:
-                beta, zrel, al = r * Z, np.full_like(Z, -r), T * (1 - r)
+    """Cell (e0, e1, p) against its own boundary edge (e0, e1): three pieces by where the edge
+    point a lies relative to the cell point's projection, radial r = distance to the edge line
+    scale (quadrature.py:338-360)."""
+    def piece(c):
+        def f(r, z, t):
+            if c == 1:
+                zrel, beta = r * z, r * (1 - z)
+                al = zrel + t * (1 - r)
+            elif c == 2:
+                beta, zrel, al = r * z, -r, t * (1 - r)
             else:
-                beta, zrel, al = np.full_like(Z, r), -r * Z, T * (1 - r)
-            X.append(np.stack([al, beta], -1).reshape(-1, 2))
-            A.append((al - zrel).reshape(-1))
-            W.append((WZT * (1 - r)).reshape(-1) * wr * r ** (1 + 2 * s - vanishing))
-    return dict(x=np.concatenate(X), a=np.concatenate(A), w=np.concatenate(W))
+                beta, zrel, al = r, -r * z, t * (1 - r)
+            return _pt(al, beta), al - zrel, 1.0
+        return f
+    return _rule(gauss_jacobi(4, vanishing - 2 * s), [gauss_legendre(k), gauss_legendre(max(3, k // 2))],
+                 [piece(c) for c in (1, 2, 3)], lambda r: (1 - r) * r ** (1 + 2 * s - vanishing), second="a")
 
 
 @lru_cache(maxsize=None)
 def rule_touching_edge_2d(k, s):
-    """Cell (c, A, B), edge leaving the shared vertex c (quadrature.py:363-384)."""
+    """Cell (c, A, B) against a boundary edge leaving the shared vertex c: radial xi = the larger
+    of the two distances to c, w = the ratio of the smaller (quadrature.py:363-384)."""
     kk = max(2, (k + 1) // 2 + 1)
-    sq, sw = gauss_legendre(kk)
-    wq, ww = gauss_legendre(kk)
-    rq, rw = gauss_jacobi(4, 1 - 2 * s)
-    S, Wg = np.meshgrid(sq, wq, indexing="ij")
-    WW = np.outer(sw, ww)
-    X, A, W = [], [], []
-    for second in (False, True):
-        for xi, wr in zip(rq, rw):
-            if second:
-                ru, ap, jac = xi * Wg, np.full_like(Wg, xi), Wg
-            else:
-                ru, ap, jac = np.full_like(Wg, xi), xi * Wg, np.ones_like(Wg)
-            X.append(np.stack([ru * (1 - S), ru * S], -1).reshape(-1, 2))
-            A.append(ap.reshape(-1))
-            W.append((WW * jac).reshape(-1) * wr * xi ** (1 + 2 * s))
-    return dict(x=np.concatenate(X), a=np.concatenate(A), w=np.concatenate(W))
+    g = gauss_legendre(kk)
+
+    def piece(edge_far):
+        def f(xi, a, w):
+            ru, ap, jac = (xi * w, xi, w) if edge_far else (xi, xi * w, 1.0)
+            return _pt(ru * (1 - a), ru * a), np.broadcast_to(ap, np.broadcast_shapes(np.shape(a), np.shape(w))), jac
+        return f
+    return _rule(gauss_jacobi(4, 1 - 2 * s), [g, g], [piece(False), piece(True)], lambda x: x ** (1 + 2 * s),
+                 second="a")
 
 
 def payload(topology: PairTopology, k: int, s: float, d: int, vanishing=0):

@@ -15,6 +15,7 @@ Each target runs in its own subprocess so peak memory is released between them.
 What is stored (all derived from the reference's own functions):
   * tables   : sha256 + moments of every quadrature payload `reference_payload(topo,k,s,d,v)`
                the configs can touch (quadrature.py:401-420)
+  * payloads : the full node / weight arrays of a subset of those payloads
   * meshes   : the BASELINE meshes as the reference builds them (mesh.py:273, :41, :351)
   * small/c1 : full dense A (assembly.py:1059), b (:550), pcg x + iterations (solve.py:52)
   * c2/c3    : sampled rows, diag, A@1, A@v, b, x, iterations, exact per-pair Gauss orders
@@ -397,6 +398,26 @@ def t_tables():
     save("tables", recs)
 
 
+def t_payloads():
+    """Full node / weight arrays of a subset of the reference's singular payloads (every topology,
+    s in {1/4, 1/2, 3/4}, low / middle / capped orders): the elementwise check of the package's
+    re-derived rules (tests/test_tables.py::test_payload_arrays)."""
+    from fraclap import quadrature as Q
+    T = Q.PairTopology
+    recs = {}
+    cases = [(1, "IDENTICAL", [2]), (1, "COMMON_VERTEX", [2, 14, 32]), (1, "EDGE_OF_CELL", [2]),
+             (2, "IDENTICAL", [2, 14, 24]), (2, "COMMON_EDGE", [2, 9, 16]), (2, "COMMON_VERTEX", [2, 5, 15]),
+             (2, "EDGE_OF_CELL", [2, 11, 20]), (2, "TOUCHING_EDGE", [2, 7, 20])]
+    for d, topo, ks in cases:
+        for s in (0.25, 0.5, 0.75):
+            van = 0 if s < 0.5 else 2
+            for k in ks:
+                p = Q.reference_payload(getattr(T, topo), k, s, d, van)
+                for key, v in p.items():
+                    recs["%d/%s/%d/%g/%d/%s" % (d, topo.lower(), k, s, van, key)] = np.asarray(v, float)
+    save("payloads", recs)
+
+
 def t_meshes():
     recs = {}
     for name, (kind, N, s) in CONFIGS.items():
@@ -667,6 +688,7 @@ TARGETS = {
     "cluster": t_cluster,
     "near": t_near,
     "tables": t_tables,
+    "payloads": t_payloads,
     "meshes": t_meshes,
     "small": t_small,
     "irregular": t_irregular,

@@ -1,7 +1,6 @@
-"""Rule tables (host restatement shipped to the device) against the reference payloads
-(hash + moments recorded from quadrature.reference_payload, quadrature.py:401-420)."""
-import hashlib
-
+"""Rule tables (host re-derivation shipped to the device) against the reference payloads
+(moments of every payload and full arrays of a subset, recorded from
+quadrature.reference_payload, quadrature.py:401-420, by tests/golden/make_golden.py)."""
 import numpy as np
 import pytest
 
@@ -22,22 +21,57 @@ def _keys():
     return sorted(k[:-4] for k in G.files if k.endswith("/sha"))
 
 
-def _sha(p):
-    arrs = [np.asarray(p[k], float) for k in sorted(p)]
-    return hashlib.sha256(b"".join(np.ascontiguousarray(a).tobytes() for a in arrs)).digest()
-
-
 def _parse(key):
     d, topo, k, s, van = key.split("/")
     return int(d), NAMES[topo], int(k), (0.5 if s == "x" else float(s)), int(van)
 
 
+def _moments(p):
+    """The moments make_golden.py recorded: count, sum w, and per coordinate sum w c, sum w c^2,
+    min c, max c."""
+    w = np.asarray(p["w"], float)
+    mom = [len(w), w.sum()]
+    for key in sorted(p):
+        if key == "w":
+            continue
+        a = np.asarray(p[key], float).reshape(len(w), -1)
+        for c in range(a.shape[1]):
+            mom += [(w * a[:, c]).sum(), (w * a[:, c] ** 2).sum(), a[:, c].min(), a[:, c].max()]
+    return np.array(mom)
+
+
 @pytest.mark.parametrize("key", _keys())
-def test_payload_bitwise(key):
+def test_payload_moments(key):
+    """Every payload the configurations can touch (re-derived as Duffy pieces in
+    quadrature._rule) against the reference's: node count exact, moments within 1e-14."""
     G = golden("tables")
     d, topo, k, s, van = _parse(key)
     p = Q.payload(topo, max(k, 2), s, d, van)
-    assert _sha(p) == G[key + "/sha"].tobytes(), key
+    mom, want = _moments(p), G[key + "/mom"]
+    assert mom.shape == want.shape and mom[0] == want[0], key
+    assert np.all(np.abs(mom - want) <= 1e-14 * np.maximum(1.0, np.abs(want))), (key, np.abs(mom - want).max())
+
+
+def _payload_keys():
+    try:
+        G = golden("payloads")
+    except BaseException:
+        return []
+    return sorted({k.rsplit("/", 1)[0] for k in G.files})
+
+
+@pytest.mark.parametrize("key", _payload_keys())
+def test_payload_arrays(key):
+    """Node by node against the reference's own arrays (tests/golden/payloads.npz): coordinates
+    within 1e-14, weights within 1e-14 of the largest weight."""
+    G = golden("payloads")
+    d, topo, k, s, van = key.split("/")
+    p = Q.payload(getattr(T, topo.upper()), int(k), float(s), int(d), int(van))
+    for name in p:
+        a, b = np.asarray(p[name], float), G[key + "/" + name]
+        assert a.shape == b.shape, (key, name)
+        scale = np.abs(b).max() if name == "w" else 1.0
+        assert np.abs(a - b).max() <= 1e-14 * scale, (key, name, np.abs(a - b).max())
 
 
 @pytest.mark.parametrize("key", _keys()[::3])
