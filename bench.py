@@ -17,7 +17,9 @@ ranks time (strong scaling: the mesh is fixed).  After the timed steps: 100 matv
 x ~ U(-1,1) (seed 0), Jacobi-PCG to 1e-8 (c5) through the sharded solver (NCCL all-gathers when
 N > 1), and the end-to-end public-API path (host mesh in -> assemble -> load_vector -> pcg -> x
 to host).  `--impl reference` times the CPU oracle port of the reference (oracle/) on a bounded
-sample of the same workload on the host cores.
+sample of the same workload on the host cores (the reference itself cannot assemble c4/c5: its
+nc^2 pair arrays need > 100 GB); beside it, `reference_own` times the UNMODIFIED reference
+(baseline/_ref, its own assemble_dense + pcg) on c1 and a 512-cell 2D square with every host core.
 """
 from __future__ import annotations
 
@@ -251,6 +253,77 @@ def cpu_sample_text(info, cfg):
             "%.1f s" % (info["threads"], info["cells"], cfg, info["seconds"]))
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")      # pip install --target of the unmodified reference
+REF_OWN_CASES = {"c1": ("c1", None), "sq16": ("2D unit square 16x16 SW-NE, s=0.5 (512 cells, n=225)", 16)}
+
+
+def _ref_own_child(cases):
+    """Runs in a fresh interpreter (bench.py --ref-own): the UNMODIFIED reference's own
+    assemble_dense (assembly.py:1059-1104) + Jacobi-PCG (solve.py:52-109), imported from
+    baseline/_ref, on every host core its BLAS uses; the oracle port on the same job beside it
+    (single process) so the port's speed relative to the reference is on record."""
+    sys.path.insert(0, REF_DIR)
+    import fraclap
+    from fraclap import mesh as RM, assembly as RA, solve as RS
+    from paper_1708_03912_b200 import mesh as M
+    from oracle import fraclap_oracle as O
+    out = {"module": os.path.dirname(fraclap.__file__).replace(ROOT + "/", ""), "cpu_count": os.cpu_count()}
+    try:
+        import threadpoolctl
+        out["threadpool_info"] = [{k: i.get(k) for k in ("internal_api", "num_threads", "version")}
+                                  for i in threadpoolctl.threadpool_info()]
+    except Exception as e:                       # noqa: BLE001
+        out["threadpool_info"] = "unavailable: %s" % e
+    for name in cases:
+        cfg, N = REF_OWN_CASES[name]
+        if N is None:
+            mesh, s = M.baseline_mesh(cfg)
+        else:
+            mesh, s = M.build_unit_square_mesh(N), 0.5
+        rmesh = RM.Mesh(mesh.vertices, mesh.cells, mesh.boundary_edges, mesh.boundary_normals)
+        rdm = RM.DofMap(rmesh, s)
+        t0 = time.perf_counter()
+        Ar = RA.assemble_dense(rmesh, rdm, RA.FractionalKernel(rmesh.d, s), n_limit=10 ** 6)
+        t_asm = time.perf_counter() - t0
+        b = RA.load_vector(rmesh, rdm, lambda X: np.ones(len(X)))
+        t0 = time.perf_counter()
+        x, rep = RS.pcg(Ar, b, precond="jacobi", tol=1e-10, max_iter=10 ** 5)
+        t_cg = time.perf_counter() - t0
+        dm = M.DofMap(mesh, s)
+        o = O.Oracle(mesh, dm, s)
+        t0 = time.perf_counter()
+        Ao = o.assemble()
+        t_port = time.perf_counter() - t0
+        pairs = port_pair_total(o, mesh)
+        out[name] = {"mesh": CONFIG_TEXT.get(cfg, cfg), "n": int(rdm.n), "pairs": int(pairs),
+                     "assemble_s": t_asm, "pairs_per_s": pairs / t_asm, "cg_s": t_cg,
+                     "cg_iterations": int(getattr(rep, "iterations", -1)),
+                     "port_assemble_s_1proc": t_port, "port_max_rel_dev": float(np.abs(Ao - Ar).max() / np.abs(Ar).max())}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def port_pair_total(o, mesh):
+    """Element pairs of one full oracle assembly, counted as the GPU arm counts them (pair_count)."""
+    g = o.g
+    nc, nb = mesh.num_cells, len(g.be)
+    touching = len(o.touching_pairs())
+    bsing = len(o.boundary_items())
+    return nc + touching + (nc * (nc - 1) // 2 - touching) + (nc * (nc - 1) - 2 * touching) + bsing + nc * nb
+
+
+def reference_own(cases=("c1", "sq16"), timeout=600):
+    """The reference's own CPU path, timed in a child interpreter; None when baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "fraclap")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference)"}
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--ref-own", ",".join(cases)],
+                           capture_output=True, text=True, timeout=timeout)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:                       # noqa: BLE001
+        return {"unavailable": "reference run failed: %s" % str(e)[:200]}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -262,13 +335,14 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(v)
     v = float(np.median(vals))
+    own = None if args.no_ref_own else reference_own()
     line = {"metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": 0, "steps": args.steps,
             "ms_per_step": 1e3 * info["seconds"],
             "warmup": args.warmup, "higher_is_better": True, "scaling": "strong", "impl": "reference",
             "dtype": "f64", "data": "synthetic (BASELINE mesh, f=1)", "vs_baseline": None,
             "config": {"workload": args.config, "mesh": CONFIG_TEXT[args.config]},
             "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": info["threads"], "kind": "port",
-                             "sample": cpu_sample_text(info, args.config)},
+                             "sample": cpu_sample_text(info, args.config), "reference_own": own},
             "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -330,7 +404,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the c2 line and the cluster-path timings")
     ap.add_argument("--ref-budget", type=float, default=6.0)
+    ap.add_argument("--no-ref-own", action="store_true", help="skip timing the reference's own code (baseline/_ref)")
+    ap.add_argument("--ref-own", default=None, help=argparse.SUPPRESS)    # internal: child of reference_own()
     args = ap.parse_args()
+    if args.ref_own:
+        return _ref_own_child(args.ref_own.split(","))
     if args.impl == "reference":
         return run_reference(args)
     world, rank, local = dist_env()
@@ -487,7 +565,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         v, info = cpu_sample(args.config)
         cpu = {"value": v, "unit": "pairs/s", "cores": info["threads"], "kind": "port",
-               "sample": cpu_sample_text(info, args.config)}
+               "sample": cpu_sample_text(info, args.config),
+               "reference_own": None if args.no_ref_own else reference_own()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
