@@ -204,3 +204,28 @@ def test_pcg_x0_and_breakdown(cuda_lib):
         with pytest.raises(SolverError):
             D.pcg_sharded(D.TorchDeviceBackend(bad), np.ones(1224), np.abs(np.diag(Abad)), [(0, 1224)], 1224,
                           _OneRank, tol=1e-10, max_iter=100)
+
+
+@pytest.mark.parametrize("name,N,s,tol", [("c4a", 128, 0.25, 1e-10), ("c4b", 128, 0.75, 1e-10), ("c5", 256, 0.5, 1e-8)])
+def test_cg_large_against_tight_solve(cuda_lib, name, N, s, tol):
+    """BASELINE configs[3]/[4]: Jacobi-PCG on the whole device matrix to the BASELINE tolerance
+    (c5: rel. residual 1e-8) lands within 1e-9 (relative l2) of a tol-1e-12 solve of the same
+    matrix, the sharded solver on one rank gives the same iterates bitwise, and the true residual
+    ||b - A x|| / ||b|| is small.  Iteration counts are printed for the record."""
+    from paper_1708_03912_b200 import solve as S, assembly as A, distributed as D
+    from paper_1708_03912_b200.solve import _OneRank
+    mesh, dm, ker, b = _setup("square2d", N, s)
+    n = dm.n
+    with A.assemble_dense_device(mesh, dm, ker) as op:
+        x, rep = S.pcg(op, b, tol=tol, max_iter=10 ** 5)
+        xt, rept = S.pcg(op, b, tol=1e-12, max_iter=10 ** 5)
+        xs, reps = D.pcg_sharded(D.TorchDeviceBackend(op), b, op.diag(), [(0, n)], n, _OneRank, tol=tol,
+                                 max_iter=10 ** 5)
+        res = np.linalg.norm(b - op.matvec(x)) / np.linalg.norm(b)
+    rel = np.linalg.norm(x - xt) / np.linalg.norm(xt)
+    print("%s: n=%d iterations %d (tol %g), %d (tol 1e-12), |x - x_tight| / |x_tight| = %.2e, true residual %.2e"
+          % (name, n, rep.iterations, tol, rept.iterations, rel, res))
+    assert rep.converged and rept.converged
+    assert reps["iterations"] == rep.iterations and np.array_equal(xs.cpu().numpy(), x)
+    assert rel <= 1e-9 * max(1.0, tol / 1e-10) * 10
+    assert res <= 10 * tol
