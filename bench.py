@@ -53,8 +53,10 @@ CG_TOL = {"c1": 1e-10, "c2": 1e-10, "c3": 1e-10, "c4a": 1e-10, "c4b": 1e-10, "c5
 ALG_FLOPS = {(1, "tail"): 4, (1, "cross"): 6, (2, "tail"): 7, (2, "cross"): 11}
 POW_FLOPS = {6: 11, 8: 8, 10: 11, 12: 9, 14: 12, 0: 60}   # = kpow_flops() in csrc/fl_device.cuh (2D)
 POW_FLOPS_1D = {6: 9, 8: 9, 10: 10, 0: 60}                  # = kpow_abs_flops() (1D far field)
-KERNEL_NAME = {("tail", 1): "tail1d_kernel", ("tail", 2): "tail_kernel", ("cross", 1): "cross1d_tile_kernel",
-               ("cross", 2): "cross2d_kernel"}
+KERNEL_NAME = {("tail", 1): "tail1d_kernel", ("tail", 2): "tail2d_block_kernel + tail_kernel",
+               ("cross", 1): "cross1d_tile_kernel", ("cross", 2): "cross2d_kernel + near_block_kernel",
+               ("tail_block", 2): "tail2d_block_kernel", ("tail_pairs", 2): "tail_kernel",
+               ("cross_far", 2): "cross2d_kernel", ("near", 2): "near_block_kernel"}
 
 
 def peaks():
@@ -350,10 +352,26 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 def roofline_of(stats, d, s, fp64, kind):
+    """Algorithmic FP64 rate of one assembly kernel: its evaluations (device-counted) x FLOPs per
+    evaluation / its device ms (CUDA events on the assembly stream).  kind: tail / cross (1D or
+    the whole 2D phase), tail_block (2D block-pair tail kernel), tail_pairs (2D warp-per-target
+    tail on the remaining source blocks), cross_far (2D cross2d_kernel compute pass), near (2D
+    near blocks, k >= 5)."""
     e4 = int(round(4 * (d + 2 * s))) if s in (0.25, 0.5, 0.75) else 0
-    ms = stats["ms_tail"] if kind == "tail" else (stats["ms_cross_compute"] or stats["ms_cross"])
-    ev = stats["evals_tail"] if kind == "tail" else stats["evals_cross"]
-    fpe = ALG_FLOPS[(d, kind)] + (POW_FLOPS_1D if d == 1 else POW_FLOPS).get(e4, 60)
+    base = "tail" if kind.startswith("tail") else "cross"
+    if kind == "tail":
+        ms, ev = stats["ms_tail"], stats["evals_tail"]
+    elif kind == "tail_block":
+        ms, ev = stats["ms_tail_block"], stats["evals_tail_block"]
+    elif kind == "tail_pairs":
+        ms, ev = stats["ms_tail"] - stats["ms_tail_block"], stats["evals_tail"] - stats["evals_tail_block"]
+    elif kind == "cross":
+        ms, ev = (stats["ms_cross_compute"] or stats["ms_cross"]), stats["evals_cross"]
+    elif kind == "cross_far":
+        ms, ev = stats["ms_cross_compute"], stats["evals_cross"] - stats["evals_near"]
+    else:   # near
+        ms, ev = stats["ms_near"], stats["evals_near"]
+    fpe = ALG_FLOPS[(d, base)] + (POW_FLOPS_1D if d == 1 else POW_FLOPS).get(e4, 60)
     ach = ev * fpe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
     return {"bound": "fp64", "kernel": KERNEL_NAME[(kind, d)], "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
             "frac": ach / fp64 if fp64 else None, "flops_per_eval": fpe, "evals_per_launch": ev,
@@ -462,13 +480,14 @@ def main():
     # job's counts; a row block is a share of that job)
     pairs = pair_count(stats)
     value = pairs / (ms_step / 1e3)
-    roof_tail = roofline_of(stats, mesh.d, s, fp64, "tail")
-    roof_cross = roofline_of(stats, mesh.d, s, fp64, "cross")
-    roof = dict(max((roof_tail, roof_cross), key=lambda r: r["ms_per_launch"]))
+    kinds = ("tail", "cross") if mesh.d == 1 or stats["ms_tail_block"] <= 0 else \
+        ("tail_block", "tail_pairs", "cross_far", "near")
+    roofs = [roofline_of(stats, mesh.d, s, fp64, k) for k in kinds]
+    for r in roofs:
+        r["traffic"] = committed_traffic(args.config, r["kernel"])
+    roof = dict(max(roofs, key=lambda r: r["ms_per_launch"]))
     roof["traffic"] = committed_traffic(args.config, roof["kernel"])
     roof["peak_source"] = "fl_probe_fp64_peak (DFMA chains, this run, same GPU)"
-    other = roof_cross if roof["kernel"] == roof_tail["kernel"] else roof_tail
-    other["traffic"] = committed_traffic(args.config, other["kernel"])
 
     # ---------------------------------------------------------------- dense matvec GB/s
     pk, pk_src = peaks()
@@ -581,7 +600,7 @@ def main():
                                                                      "ms_cross_compute", "ms_local", "ms_total")},
                            "near_pairs": stats["near_pairs"], "evals_tail": stats["evals_tail"],
                            "evals_cross": stats["evals_cross"]},
-                "roofline": roof, "roofline_second": other, "matvec": matvec, "cg": cg, "e2e": e2e,
+                "roofline": roof, "roofline_kernels": roofs, "matvec": matvec, "cg": cg, "e2e": e2e,
                 "cpu_baseline": cpu, "extra": extra or None,
                 "clocks": clk.summary(), "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)

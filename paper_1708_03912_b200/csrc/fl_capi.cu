@@ -523,8 +523,9 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   if (nbands) FL_CUDA(cudaMemcpyAsync(&hs[16], bcnt.p, nbands * sizeof(int), cudaMemcpyDeviceToHost, st));
   cudaEvent_t ev_sizes = tm.e[11];                 // (the last timing event doubles as the size fence)
   FL_CUDA(cudaEventRecord(ev_sizes, st));
-  DBuf<unsigned long long> evc(2);
-  FL_CUDA(cudaMemsetAsync(evc.p, 0, 2 * sizeof(unsigned long long), st));
+  // evaluation counters: tail (all), cross (all), tail by the block-pair kernel, cross near blocks
+  DBuf<unsigned long long> evc(4);
+  FL_CUDA(cudaMemsetAsync(evc.p, 0, 4 * sizeof(unsigned long long), st));
   DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
   FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
   // 1D: the tail runs on its own stream, so the cross tiles (issued on `st` once the sizes are
@@ -613,10 +614,31 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   launch_singular_identical(m, U.t, ex, e4, ident_k.p, ident.p, st);
   launch_singular_touching(m, U.t, ex, e4, tpairs.p, npairs, tloc.p, st);
   if (do_bnd) launch_singular_boundary(m, U.t, ex, e4, bitems.p, nitems, bloc.p, st);
+  // 2D: the Morton cell blocks shared by the tail and the cross term
+  static const bool tail2d_warp = [] {        // FRACLAP_TAIL2D=warp: round-1 warp-per-target tail only
+    const char* v = getenv("FRACLAP_TAIL2D");
+    return v && std::string(v) == "warp";
+  }();
+  Blocks2D blocks;
+  struct EvPair {                      // events around the 2D block-pair tail kernel
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    cudaEvent_t& operator[](int i) { return e[i]; }
+    ~EvPair() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } tbev;
+  if (d == 2) build_blocks2d(m, (int)row_begin, (int)row_end, blocks, st);
   if (!early_tail) {
     tm.mark();  // 2
     // tail at the nodes of the target cells (banded 1D: per band, below)
-    if (d == 2) launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+    if (d == 2 && tail2d_warp) launch_tail(m, U.t, oc, ex, e4, targets.p, ntargets, psi.p, evc.p, st);
+    else if (d == 2) {
+      cudaEventCreate(&tbev[0]);
+      cudaEventCreate(&tbev[1]);
+      launch_tail2d_blocks(m, U.t, oc, ex, e4, blocks, targets.p, ntargets, psi.p, evc.p, st, evc.p + 2, tbev[0],
+                           tbev[1]);
+    }
     else if (!nbands) launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, st);
   }
   tm.mark();  // 3
@@ -695,8 +717,8 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     cudaEventCreate(&xev[0]);
     cudaEventCreate(&xev[1]);
     tm.mark();  // 5
-    assemble_cross2d(m, U.t, oc, ex, e4, C, (int)row_begin, (int)row_end, D->A.p, D->lda, evc.p + 1, near, x2,
-                     xev[0], xev[1], st);
+    assemble_cross2d(m, U.t, oc, ex, e4, C, blocks, (int)row_begin, (int)row_end, D->A.p, D->lda, evc.p + 1, near, x2,
+                     xev[0], xev[1], st, evc.p + 3);
     ntiles = -1;
     done1d = true;
   }
@@ -750,7 +772,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   }
   tm.mark();  // 7
   unsigned long long* hev = reinterpret_cast<unsigned long long*>(hs + 8);
-  FL_CUDA(cudaMemcpyAsync(hev, evc.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaMemcpyAsync(hev, evc.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[4], m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   unsigned long long hties = 0;
   FL_CUDA(cudaMemcpyAsync(&hties, ties.p, sizeof(hties), cudaMemcpyDeviceToHost, st));
@@ -771,9 +793,17 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   S.pairs_tail = nc * (nc - 1) - 2 * npairs;
   S.pairs_boundary_singular = nitems;
   S.pairs_boundary_flux = integral ? nc * m.nb : 0;
-  S.evals_tail = (double)hev[0];
+  S.evals_tail = (double)hev[0] + (double)hev[2];     // warp-per-target pairs + block-pair kernel
   S.order_ties = (int64_t)hties;
-  S.evals_cross = (double)hev[1];
+  S.evals_cross = (double)hev[1] + (double)hev[3];    // far blocks + near blocks
+  S.evals_tail_block = (double)hev[2];
+  S.evals_near = (double)hev[3];
+  S.ms_tail_block = 0.0;
+  if (tbev[1]) {
+    float a = 0.f;
+    cudaEventElapsedTime(&a, tbev[0], tbev[1]);
+    S.ms_tail_block = a;
+  }
   S.ms_prep = tm.ms(0, 1);
   S.ms_singular = early_tail ? tm.ms(2, 3) : tm.ms(1, 2);   // 1D: tail (1 -> 2) runs before the singular kernels
   S.ms_tail = early_tail ? tm.ms(1, 2) : tm.ms(2, 3);

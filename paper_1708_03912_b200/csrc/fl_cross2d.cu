@@ -31,7 +31,7 @@ namespace fl {
 
 namespace {
 
-constexpr int CB = 32;            // cells per block
+constexpr int CB = CB2D;          // cells per block
 constexpr int BRMAX = 64;         // DoFs per block (more: the mesh is refused by this path)
 constexpr int TCAP = 48 * 48;     // int64 tile capacity; larger rectangles go straight to HBM
 constexpr int X2T = 256;          // threads per CTA
@@ -161,6 +161,11 @@ __global__ void __launch_bounds__(128) block_build_kernel(DevMesh m, const int* 
   }
 }
 
+__global__ void block_of_kernel(const int* __restrict__ sorted, int nc, int* __restrict__ blk_of) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nc) blk_of[sorted[i]] = i / CB;
+}
+
 // mapped nodes of the rules k = 2, 3, 4 for every cell: X = P0 + (u0 (P1 - P0) + u1 (P2 - P0))
 __global__ void cell_nodes2_kernel(DevMesh m, const double* __restrict__ tab, RuleRef r2, RuleRef r3, RuleRef r4,
                                    double2* __restrict__ nodes) {
@@ -205,22 +210,13 @@ __global__ void dmin_kernel(DevMesh m, unsigned long long* __restrict__ dmin_bit
   atomicMax(jmax_bits, (unsigned long long)__double_as_longlong(A.J));
 }
 
-// Rigorous bounds of select_order's disjoint formula (quadrature.py:159-168) over all cell pairs
-// of two blocks with centre distance dc: Dmin <= dist estimate <= Dmax, h in [hmn, hmx], |ln h|
-// in [lmn, lmx].  hi: every numerator term bounded above, the denominator below; lo: the reverse.
-__device__ double bound_hi(const OrderConsts& oc, double Dmin, double hmn, double hmx, double lmn, double lmx) {
-  if (!(Dmin > 0.0)) return 1e30;
-  const double num = oc.lead_lnn + oc.sm1 * lmn + lmx - oc.s * log(Dmin / hmx) - oc.coff;
-  const double den = fmax(log(Dmin / hmx), 0.0) + oc.ln_rho2;    // > 0
-  return num / den;         // (num < 0: the order clips to 2 whatever the denominator)
+__device__ __forceinline__ double bound_hi(const OrderConsts& oc, double Dmin, double hmn, double hmx, double lmn,
+                                           double lmx) {
+  return order_bound_hi(oc, oc.coff, Dmin, hmn, hmx, lmn, lmx);
 }
-__device__ double bound_lo(const OrderConsts& oc, double Dmin, double Dmax, double hmn, double hmx, double lmn,
-                           double lmx) {
-  if (!(Dmin > 0.0)) return -1e30;
-  const double num = oc.lead_lnn + oc.sm1 * lmx + lmn - oc.s * log(Dmax / hmn) - oc.coff;
-  const double den_hi = fmax(log(Dmax / hmn), 0.0) + oc.ln_rho2;
-  const double den_lo = fmax(log(Dmin / hmx), 0.0) + oc.ln_rho2;
-  return num >= 0.0 ? num / den_hi : num / den_lo;
+__device__ __forceinline__ double bound_lo(const OrderConsts& oc, double Dmin, double Dmax, double hmn, double hmx,
+                                           double lmn, double lmx) {
+  return order_bound_lo(oc, oc.coff, Dmin, Dmax, hmn, hmx, lmn, lmx);
 }
 
 __global__ void block_pairs_kernel(OrderConsts oc, const double* __restrict__ bs, const int* __restrict__ rowflag,
@@ -324,8 +320,11 @@ struct XArgs {
   const double* nearG;
 };
 
+#ifndef FL_X2_MINB
+#define FL_X2_MINB 3
+#endif
 template <int E4, bool DISC>
-__global__ void __launch_bounds__(X2T, 3) cross2d_kernel(XArgs a, const double* __restrict__ wl_g) {
+__global__ void __launch_bounds__(X2T, FL_X2_MINB) cross2d_kernel(XArgs a, const double* __restrict__ wl_g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   XShared& S = *reinterpret_cast<XShared*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
@@ -394,6 +393,52 @@ __global__ void __launch_bounds__(X2T, 3) cross2d_kernel(XArgs a, const double* 
           }
         }
     };
+    if (!DISC && kuni >= 2 && kuni < KW2D) {
+      // ---- one order for the whole block pair (disjoint blocks): no per-pair orders, no sort.
+      // A warp takes one row cell i and the 32 column cells j (lane), so the row cell's nodes
+      // are broadcast loads; each lane computes its whole pair in registers (the row cell's x
+      // nodes NX at a time against the column cell's y nodes).
+      const int k = kuni;
+      unsigned long long my = 0;
+      const int wid = tid >> 5;
+#pragma unroll 1
+      for (int i = wid; i < CB; i += X2T / 32) {
+        const int j = lane;
+        if (S.r[i].id < 0 || S.r[CB + j].id < 0) continue;
+        const double2* Xn = S.nd[i];
+        const double2* Yn = S.nd[CB + j];
+        double M[3][3] = {};
+        if (k == 2) {
+          blk_part<E4, 4, 4, 1>(Xn + poff(2), Yn + poff(2), S.wl + poff(2), 0, a.ex, M);
+        } else if (k == 3) {
+#pragma unroll 1
+          for (int xs = 0; xs < 3; ++xs) blk_part<E4, 9, 3, 3>(Xn + poff(3), Yn + poff(3), S.wl + poff(3), xs, a.ex, M);
+        } else {
+#pragma unroll 1
+          for (int xs = 0; xs < 4; ++xs) blk_part<E4, 16, 4, 4>(Xn + poff(4), Yn + poff(4), S.wl + poff(4), xs, a.ex, M);
+        }
+        const double JJ = S.r[i].J * S.r[CB + j].J;
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int y = 0; y < 3; ++y) M[x][y] *= JJ;
+        put(i, j, true, M);
+        my += (unsigned long long)(k * k) * (k * k);
+      }
+      if (my) atomicAdd(&S.evals, my);
+      __syncthreads();
+      if (in_tile) {
+        for (int idx = tid; idx < nP * nQ; idx += X2T) {
+          const unsigned long long q = S.tile[idx];
+          if (!q) continue;
+          const int r = idx / nQ, c = idx - r * nQ;
+          const int gi = S.dofP[r], gj = S.dofQ[c];
+          if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
+          if (gj >= a.r0 && gj < a.r1) atomicAdd(&a.A[(int64_t)(gj - a.r0) * a.lda + gi], q);
+        }
+      }
+      continue;
+    }
     // ---- (A) orders
     for (int p = tid; p < CB * CB; p += X2T) {
       const int i = p / CB, j = p % CB;
@@ -574,12 +619,10 @@ __global__ void fixed_to_double_kernel(unsigned long long* A, int64_t count, dou
 // overwritten (zeroed first).  Near pairs (k >= KW2D) are discovered here and computed once by
 // near_pairs_build into `near`.  t_disc / t_near: events recorded after discovery and after the
 // near blocks (phase timing).
-void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
-                      int row_begin, int row_end, double* A, int64_t lda, unsigned long long* evals, NearPairs& near,
-                      Cross2DInfo& info, cudaEvent_t t_disc, cudaEvent_t t_near, cudaStream_t st) {
+void build_blocks2d(const DevMesh& m, int row_begin, int row_end, Blocks2D& B, cudaStream_t st) {
   const int nc = m.nc;
   const int nb = (nc + CB - 1) / CB;
-  const int64_t rows = row_end - row_begin;
+  B.nb = nb;
   // ---- Morton order of the cells
   std::vector<double> hv((size_t)m.nv * 2);
   FL_CUDA(cudaMemcpyAsync(hv.data(), m.vert, hv.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -600,12 +643,29 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
     FL_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, keys.p, keys2.p, vals.p, vals2.p, nc, 0, 32, st));
   }
   // ---- blocks
-  DBuf<int> bcells((size_t)nb * CB), bdofs((size_t)nb * BRMAX), bndof(nb), rowflag(nb), err(1);
-  DBuf<signed char> slot((size_t)nc * 3);
-  DBuf<double> bstat((size_t)nb * 8);
-  FL_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), st));
-  block_build_kernel<<<nb, 128, 0, st>>>(m, vals2.p, nb, row_begin, row_end, bcells.p, bdofs.p, bndof.p, slot.p,
-                                         bstat.p, rowflag.p, err.p), note_launch();
+  B.bcells.alloc((size_t)nb * CB); B.bdofs.alloc((size_t)nb * BRMAX); B.bndof.alloc(nb); B.rowflag.alloc(nb);
+  B.err.alloc(1); B.slot.alloc((size_t)nc * 3); B.bstat.alloc((size_t)nb * 8); B.blk_of.alloc(nc);
+  FL_CUDA(cudaMemsetAsync(B.err.p, 0, sizeof(int), st));
+  block_build_kernel<<<nb, 128, 0, st>>>(m, vals2.p, nb, row_begin, row_end, B.bcells.p, B.bdofs.p, B.bndof.p,
+                                         B.slot.p, B.bstat.p, B.rowflag.p, B.err.p), note_launch();
+  block_of_kernel<<<(nc + 255) / 256, 256, 0, st>>>(vals2.p, nc, B.blk_of.p), note_launch();
+  FL_CHECK_LAUNCH();
+}
+
+void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
+                      const Blocks2D& B, int row_begin, int row_end, double* A, int64_t lda,
+                      unsigned long long* evals, NearPairs& near, Cross2DInfo& info, cudaEvent_t t_disc,
+                      cudaEvent_t t_near, cudaStream_t st, unsigned long long* evals_near) {
+  const int nc = m.nc;
+  const int nb = B.nb;
+  const int64_t rows = row_end - row_begin;
+  const DBuf<int>& bcells = B.bcells;
+  const DBuf<int>& bdofs = B.bdofs;
+  const DBuf<int>& bndof = B.bndof;
+  const DBuf<int>& rowflag = B.rowflag;
+  const DBuf<int>& err = B.err;
+  const DBuf<signed char>& slot = B.slot;
+  const DBuf<double>& bstat = B.bstat;
   // ---- mapped nodes, rule weights, scale bound
   const RuleRef r2 = t.rule(T_DISJ, 2), r3 = t.rule(T_DISJ, 3), r4 = t.rule(T_DISJ, 4);
   if (r2.cnt != 4 || r3.cnt != 9 || r4.cnt != 16) throw Error(-3, "disjoint rules k = 2, 3, 4 missing");
@@ -711,7 +771,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
     xa.bpairs = nearl.p; xa.nbp = nnear; xa.queue = queue.p;
     xa.near_keys = near_keys.p; xa.near_count = near_cnt.p; xa.near_cap = cap;
     if (nnear > 0) {
-      const int grid = std::min(nnear, 3 * sms);
+      const int grid = std::min(nnear, FL_X2_MINB * sms);
       FL_E4_SWITCH2(e4, {
         FL_CUDA(cudaFuncSetAttribute(cross2d_kernel<E4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         cross2d_kernel<E4, true><<<grid, X2T, smem, st>>>(xa, wl.p), note_launch();
@@ -726,7 +786,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
     cap = cnt;
   }
   if (t_disc) FL_CUDA(cudaEventRecord(t_disc, st));
-  near_pairs_build(m, t, oc, ex, e4, near_keys.p, nkeys, near, evals ? evals : nullptr, st);
+  near_pairs_build(m, t, oc, ex, e4, near_keys.p, nkeys, near, evals_near ? evals_near : evals, st);
   near_keys.free();
   if (t_near) FL_CUDA(cudaEventRecord(t_near, st));
   // ---- pass 2: every block pair
@@ -735,7 +795,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   xa.near_keys = nullptr; xa.near_count = nullptr; xa.near_cap = 0;
   xa.nearH = near.hkey.p; xa.nearI = near.hidx.p; xa.hmask = near.hmask; xa.nearG = near.G.p;
   if (nall > 0) {
-    const int grid = std::min(nall, 3 * sms);
+    const int grid = std::min(nall, FL_X2_MINB * sms);
     FL_E4_SWITCH2(e4, {
       FL_CUDA(cudaFuncSetAttribute(cross2d_kernel<E4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       cross2d_kernel<E4, false><<<grid, X2T, smem, st>>>(xa, wl.p), note_launch();

@@ -37,7 +37,10 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
                                                                   DevTables dir, OrderConsts oc, double ex,
                                                                   const int* __restrict__ targets, int ntargets,
                                                                   double* __restrict__ psi,
-                                                                  unsigned long long* __restrict__ evals) {
+                                                                  unsigned long long* __restrict__ evals,
+                                                                  const int8_t* __restrict__ kuni,
+                                                                  const int* __restrict__ blk_of,
+                                                                  const int* __restrict__ bcells, int nb) {
   constexpr int Q = (D == 1) ? 6 : 16;     // cell quadrature nodes (XQ_ORDER)
   constexpr int L = Q / TAIL_T;            // lanes per group (8 in 2D, 3 in 1D)
   constexpr int G = 32 / L;                // groups sweeping disjoint source nodes (4 / 10)
@@ -66,10 +69,32 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
   }
   double acc[TAIL_T][2] = {};
   unsigned long long nodes = 0;
-  for (int s0 = 0; s0 < m.nc; s0 += 32) {
-    const int src = s0 + lane;
+  // sources: every cell in chunks of 32, or (kuni) only the Morton source blocks of K's block
+  // whose orders the block bounds did not fix (kuni == 0; the others were evaluated by
+  // tail2d_block_kernel, whose psi this kernel then adds to)
+  const int8_t* krow = kuni ? kuni + (size_t)blk_of[K] * nb : nullptr;
+  const int nchunk = kuni ? nb : (m.nc + 31) / 32;
+  unsigned pend = 0;
+  int cbase = -32;
+  for (;;) {
+    int ci;
+    if (kuni) {
+      while (!pend) {
+        cbase += 32;
+        if (cbase >= nchunk) break;
+        pend = __ballot_sync(0xffffffffu, cbase + lane < nchunk && krow[cbase + lane] == 0);
+      }
+      if (!pend) break;
+      ci = cbase + __ffs(pend) - 1;
+      pend &= pend - 1;
+    } else {
+      cbase += 32;
+      if (cbase >= m.nc) break;
+      ci = cbase >> 5;
+    }
+    const int src = kuni ? bcells[ci * 32 + lane] : ci * 32 + lane;
     int k = 0, nn = 0;
-    if (src < m.nc && src != K) {
+    if (src >= 0 && src < m.nc && src != K) {
       const CellGeo& B = m.geo[src];
       if (!touching<D>(A, B)) {
         const double dist = dist_estimate<D>(A, B);            // (target, source) orientation
@@ -161,7 +186,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
     double tot = a;
 #pragma unroll
     for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, a, (lane + gg * L) & 31);
-    if (lane < L) psi[(size_t)K * Q + j + t * L] = tot;
+    if (lane < L) psi[(size_t)K * Q + j + t * L] = kuni ? psi[(size_t)K * Q + j + t * L] + tot : tot;
   }
   if (lane == 0 && evals) atomicAdd(evals, nodes * Q);
 }
@@ -907,13 +932,14 @@ __global__ void orders_kernel(DevMesh m, OrderConsts oc, int8_t* cross_k, int8_t
   }
 
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
-                 const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st) {
+                 const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st,
+                 const int8_t* kuni, const int* blk_of, const int* bcells, int nb) {
   if (ntargets <= 0) return;
   const int grid = (ntargets + TAIL_WARPS - 1) / TAIL_WARPS;
   if (m.d == 1) {
-    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, nullptr, nullptr, nullptr, 0), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }

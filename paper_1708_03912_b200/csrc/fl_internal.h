@@ -196,7 +196,8 @@ void launch_singular_boundary(const DevMesh& m, const DevTables& t, double ex, i
 // fl_far.cu
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                  const int* targets, int ntargets, double* psi /*nc*q*/, unsigned long long* evals,
-                 cudaStream_t st);
+                 cudaStream_t st, const int8_t* kuni = nullptr, const int* blk_of = nullptr,
+                 const int* bcells = nullptr, int nb = 0);
 void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const int* targets,
                  int ntargets, double* win /*nc*q*/, cudaStream_t st);
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,
@@ -239,9 +240,30 @@ struct Cross2DInfo {
   double dmin = 0.0;          // smallest disjoint cell distance (the scale bound)
   int64_t block_pairs = 0, near_block_pairs = 0;
 };
+// Morton blocks of CB2D cells (sorted along the Morton curve of the centroids): per block its
+// cells, the sorted DoFs of its cells (<= 64) with each cell vertex's slot, a bounding circle and
+// h / |ln h| ranges (bstat: cx cy R hmin hmax lmin lmax), whether it holds a DoF of the row range;
+// blk_of: the block of every cell.  Shared by the cross term and the tail.
+constexpr int CB2D = 32;
+struct Blocks2D {
+  int nb = 0;
+  DBuf<int> bcells, bdofs, bndof, rowflag, err, blk_of;
+  DBuf<signed char> slot;
+  DBuf<double> bstat;
+};
+void build_blocks2d(const DevMesh& m, int row_begin, int row_end, Blocks2D& B, cudaStream_t st);
 void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
-                      int row_begin, int row_end, double* A, int64_t lda, unsigned long long* evals, NearPairs& near,
-                      Cross2DInfo& info, cudaEvent_t t_disc, cudaEvent_t t_near, cudaStream_t st);
+                      const Blocks2D& B, int row_begin, int row_end, double* A, int64_t lda,
+                      unsigned long long* evals, NearPairs& near, Cross2DInfo& info, cudaEvent_t t_disc,
+                      cudaEvent_t t_near, cudaStream_t st, unsigned long long* evals_near = nullptr);
+// fl_tail2d.cu: the 2D tail by Morton block pairs.  Per ordered (target block, source block) the
+// rigorous bounds of the boosted order formula either prove one order for all 32 x 32 cell pairs
+// (kuni, the source block's nodes are evaluated against all 512 target nodes of the block) or
+// not (0: the warp-per-target tail_kernel evaluates those source blocks pair by pair and adds).
+void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                          const Blocks2D& B, const int* targets, int ntargets, double* psi,
+                          unsigned long long* evals, cudaStream_t st, unsigned long long* evals_block = nullptr,
+                          cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr);
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
 // fl_far1d.cu (1D: lean tail, packed pair-block cross + gather)

@@ -1,0 +1,266 @@
+// 2D kernel tail Psi_K(x_q) (direct_tail_potential, assembly.py:985-1025) by Morton block pairs.
+//
+// Psi_K(x_q) = sum over the cells L not touching K of J_L sum_y w_y |x_q - y|^(-d-2s), y the
+// Gauss nodes of L's order k(K, L) (select_order with C_offset - 4, :997).  The cells are cut
+// into the Morton blocks of the cross term (Blocks2D, 32 cells).  For an ordered pair of blocks
+// (P targets, Q sources) rigorous bounds of the order formula over all 32 x 32 cell pairs
+// (tail_kuni_kernel) either prove one order kuni for every pair — the blocks are then disjoint,
+// so no pair touches — or not (kuni = 0).
+//
+// tail2d_block_kernel: one CTA per target block P, 256 threads holding the 512 target nodes
+// (32 cells x 16 XQ nodes, 2 per thread) in registers.  It walks the uniform source blocks Q in
+// ascending order: the next block's geometry is loaded into registers while the current one is
+// evaluated, its k^2 mapped nodes per cell (absolute coordinates, as _map_points) and J*w are
+// staged in shared memory, and every thread sweeps them against its two targets, 4 sources per
+// step — a pure FP64 stream, every shared load a broadcast.  The remaining source blocks of P
+// (kuni = 0: nearby blocks, P itself, blocks straddling an order boundary) are evaluated cell
+// pair by cell pair by fl_far.cu's warp-per-target tail_kernel, which adds its sums to these.
+// Deterministic: every target node sums its sources in a fixed order (Q ascending, then the
+// block's nodes), independent of how the rows are split over GPUs.
+#include "fl_internal.h"
+
+namespace fl {
+
+namespace {
+
+constexpr int TB = CB2D;           // cells per block
+constexpr int TQN = 16;            // target nodes per cell (XQ_ORDER 4 in 2D, assembly.py:635)
+constexpr int TT = 256;            // threads per CTA: 2 target nodes each
+constexpr int TWIN = 1024;         // source nodes per shared-memory window
+constexpr int TU = 4;              // source nodes per thread per step
+constexpr int KC = 9;              // 2D disjoint order cap (quadrature.py:171-175)
+constexpr int RULE_NODES = 284;    // sum_{k=2}^{9} k^2
+__host__ __device__ constexpr int roff(int k) { return (k - 1) * k * (2 * k - 1) / 6 - 1; }   // sum_{j=2}^{k-1} j^2
+
+__global__ void tail_flag_kernel(const int* __restrict__ targets, int ntargets, const int* __restrict__ blk_of,
+                                 int* __restrict__ tflag, int* __restrict__ tcell) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ntargets) {
+    tflag[blk_of[targets[i]]] = 1;
+    tcell[targets[i]] = 1;
+  }
+}
+
+// kuni[P * nb + Q] for the target blocks P: one order for every (target in P, source in Q) pair
+// when the bounds of the boosted order formula agree, else 0
+__global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, const int* __restrict__ tflag, int nb,
+                                 int8_t* __restrict__ kuni) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * nb) return;
+  const int P = (int)(i / nb), Q = (int)(i - (int64_t)P * nb);
+  int k = 0;
+  if (tflag[P] && P != Q) {
+    const double* a = bs + 8 * P;
+    const double* b = bs + 8 * Q;
+    const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
+    const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
+    const double Dmax = (dc + a[2] + b[2]) * (1.0 + 1e-12);
+    if (Dmin > 0.0) {               // disjoint bounding circles: no pair touches
+      const double hmn = fmin(a[3], b[3]), hmx = fmax(a[4], b[4]), lmn = fmin(a[5], b[5]), lmx = fmax(a[6], b[6]);
+      const double hi = order_bound_hi(oc, oc.coff_tail, Dmin, hmn, hmx, lmn, lmx);
+      const double lo = order_bound_lo(oc, oc.coff_tail, Dmin, Dmax, hmn, hmx, lmn, lmx);
+      const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
+      const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
+      if (c0 == c1) k = (int)c0;
+    }
+  }
+  kuni[i] = (int8_t)k;
+}
+
+// geometry field f of cell slot c of block Q: P0x P0y (P1-P0)x (P1-P0)y (P2-P0)x (P2-P0)y J valid
+__device__ __forceinline__ double geo_field(const DevMesh& m, const int* __restrict__ bcells, int Q, int t) {
+  const int c = bcells[Q * TB + (t >> 3)], f = t & 7;
+  if (c < 0) return 0.0;
+  const CellGeo& g = m.geo[c];
+  switch (f) {
+    case 0: return g.p[0][0];
+    case 1: return g.p[0][1];
+    case 2: return g.p[1][0] - g.p[0][0];
+    case 3: return g.p[1][1] - g.p[0][1];
+    case 4: return g.p[2][0] - g.p[0][0];
+    case 5: return g.p[2][1] - g.p[0][1];
+    case 6: return g.J;
+    default: return 1.0;
+  }
+}
+
+template <int E4>
+__global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
+                                                            double ex, const int8_t* __restrict__ kuni,
+                                                            const int* __restrict__ tflag,
+                                                            const int* __restrict__ tcell,
+                                                            const int* __restrict__ bcells, int nb,
+                                                            double* __restrict__ psi,
+                                                            unsigned long long* __restrict__ evals) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* sY = reinterpret_cast<double2*>(smem_raw);          // TWIN mapped source nodes
+  double* sW = reinterpret_cast<double*>(sY + TWIN);           // TWIN J * w
+  double* sR = sW + TWIN;                                      // RULE_NODES x (u0, u1, w)
+  double* sG = sR + 3 * RULE_NODES;                            // TB x 8 geometry fields
+  int* sL = reinterpret_cast<int*>(sG + 8 * TB);               // uniform source blocks: Q | k << 24
+  __shared__ int s_wsum[TT / 32];
+  __shared__ int s_nq;
+  const int P = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (!tflag[P]) return;
+  // ---- the disjoint rules k = 2..9 (reference nodes and weights)
+  for (int i = tid; i < RULE_NODES; i += TT) {
+    int k = 2;
+    while (roff(k + 1) <= i) ++k;
+    const RuleRef rr = dir.rule(T_DISJ, k);
+    const int r = i - roff(k);
+    if (rr.cnt == k * k) {
+      const double* nd = tab + (size_t)(rr.off + r) * NODE;
+      sR[3 * i] = nd[0]; sR[3 * i + 1] = nd[1]; sR[3 * i + 2] = nd[2];
+    } else {
+      sR[3 * i] = sR[3 * i + 1] = sR[3 * i + 2] = 0.0;
+    }
+  }
+  // ---- the uniform source blocks of P in ascending order (block-wide ordered compaction)
+  const int8_t* krow = kuni + (size_t)P * nb;
+  if (tid == 0) s_nq = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += TT) {
+    const int Q = base + tid;
+    const int k = Q < nb ? (int)krow[Q] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, k != 0);
+    if (lane == 0) s_wsum[wid] = __popc(bal);
+    __syncthreads();
+    int off = s_nq;
+    for (int w = 0; w < wid; ++w) off += s_wsum[w];
+    if (k) sL[off + __popc(bal & ((1u << lane) - 1u))] = Q | (k << 24);
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < TT / 32; ++w) tot += s_wsum[w];
+      s_nq += tot;
+    }
+    __syncthreads();
+  }
+  const int nq = s_nq;
+  // ---- the thread's two target nodes
+  double x0[2], x1[2];
+  int Kc[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int i = tid + t * TT, c = i / TQN, q = i % TQN;
+    Kc[t] = bcells[P * TB + c];
+    if (Kc[t] >= 0 && !tcell[Kc[t]]) Kc[t] = -1;      // a cell of the block that is not a target
+    x0[t] = Kc[t] >= 0 ? m.X[((size_t)Kc[t] * TQN + q) * 2 + 0] : 1e100;
+    x1[t] = Kc[t] >= 0 ? m.X[((size_t)Kc[t] * TQN + q) * 2 + 1] : 1e100;
+  }
+  int ntv = 0;                       // target cells of the block (evaluation count)
+  if (tid == 0)
+    for (int c = 0; c < TB; ++c) {
+      const int K = bcells[P * TB + c];
+      ntv += K >= 0 && tcell[K];
+    }
+  double acc[2][2] = {};
+  unsigned long long nev = 0;
+  double gpre = nq > 0 ? geo_field(m, bcells, sL[0] & 0xffffff, tid) : 0.0;
+  bool missing = false;
+  for (int qi = 0; qi < nq; ++qi) {
+    const int k = sL[qi] >> 24, kk = k * k;
+    __syncthreads();                 // the previous block's windows are consumed
+    sG[tid] = gpre;
+    __syncthreads();
+    if (qi + 1 < nq) gpre = geo_field(m, bcells, sL[qi + 1] & 0xffffff, tid);   // in flight meanwhile
+    if (tid == 0 && dir.rule(T_DISJ, k).cnt != kk) missing = true;
+    const double* R = sR + 3 * roff(k);
+    const int cpw = TWIN / kk;       // cells per window (>= 12)
+    for (int c0 = 0; c0 < TB; c0 += cpw) {
+      const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + TU - 1) / TU * TU;
+      if (c0 > 0) __syncthreads();
+      for (int idx = tid; idx < nwp; idx += TT) {
+        double2 y = make_double2(1e100, 1e100);
+        double w = 0.0;
+        if (idx < nw) {
+          const int c = c0 + idx / kk, r = idx - (idx / kk) * kk;
+          const double* g = sG + 8 * c;
+          if (g[7] != 0.0) {
+            const double u0 = R[3 * r], u1 = R[3 * r + 1];
+            y.x = g[0] + (u0 * g[2] + u1 * g[4]);
+            y.y = g[1] + (u0 * g[3] + u1 * g[5]);
+            w = g[6] * R[3 * r + 2];
+          }
+        }
+        sY[idx] = y;
+        sW[idx] = w;
+      }
+      if (tid == 0) {
+        int nvs = 0;
+        for (int c = c0; c < c1; ++c) nvs += sG[8 * c + 7] != 0.0;
+        nev += (unsigned long long)nvs * kk * ntv * TQN;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int p = 0; p < nwp; p += TU) {
+        double2 y[TU];
+        double w[TU];
+#pragma unroll
+        for (int u = 0; u < TU; ++u) {
+          y[u] = sY[p + u];
+          w[u] = sW[p + u];
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int u = 0; u < TU; ++u) {
+            const double d0 = x0[t] - y[u].x, d1 = x1[t] - y[u].y;
+            acc[t][u & 1] = fma(w[u], kpow<E4>(fma(d1, d1, d0 * d0), ex), acc[t][u & 1]);
+          }
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int i = tid + t * TT;
+    if (Kc[t] >= 0) psi[(size_t)Kc[t] * TQN + i % TQN] = acc[t][0] + acc[t][1];
+  }
+  if (tid == 0) {
+    if (missing) atomicOr(m.err, 1);
+    if (evals && nev) atomicAdd(evals, nev);
+  }
+}
+
+#define FL_E4_SWITCH_T(e4, ...)                               \
+  switch (e4) {                                               \
+    case 10: { constexpr int E4 = 10; __VA_ARGS__; } break;   \
+    case 12: { constexpr int E4 = 12; __VA_ARGS__; } break;   \
+    case 14: { constexpr int E4 = 14; __VA_ARGS__; } break;   \
+    default: { constexpr int E4 = 0; __VA_ARGS__; } break;    \
+  }
+
+}  // namespace
+
+void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
+                          const Blocks2D& B, const int* targets, int ntargets, double* psi,
+                          unsigned long long* evals, cudaStream_t st, unsigned long long* evals_block,
+                          cudaEvent_t e0, cudaEvent_t e1) {
+  if (ntargets <= 0) return;
+  const int nb = B.nb;
+  const size_t smem = (size_t)TWIN * 24 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
+  if (m.d != 2 || m.q != TQN || smem > 200 * 1024) {      // out of this path's shape: pair by pair
+    launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st);
+    return;
+  }
+  DBuf<int> tflag(nb), tcell(m.nc);
+  FL_CUDA(cudaMemsetAsync(tflag.p, 0, (size_t)nb * sizeof(int), st));
+  FL_CUDA(cudaMemsetAsync(tcell.p, 0, (size_t)m.nc * sizeof(int), st));
+  tail_flag_kernel<<<(ntargets + 255) / 256, 256, 0, st>>>(targets, ntargets, B.blk_of.p, tflag.p, tcell.p),
+      note_launch();
+  DBuf<int8_t> kuni((size_t)nb * nb);
+  const int64_t nn = (int64_t)nb * nb;
+  tail_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, B.bstat.p, tflag.p, nb, kuni.p), note_launch();
+  if (e0) FL_CUDA(cudaEventRecord(e0, st));
+  FL_E4_SWITCH_T(e4, {
+    FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, ex, kuni.p, tflag.p, tcell.p, B.bcells.p, nb, psi,
+                                                  evals_block ? evals_block : evals),
+        note_launch();
+  });
+  FL_CHECK_LAUNCH();
+  if (e1) FL_CUDA(cudaEventRecord(e1, st));
+  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb);
+}
+
+}  // namespace fl
