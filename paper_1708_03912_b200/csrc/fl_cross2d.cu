@@ -583,6 +583,244 @@ __global__ void __launch_bounds__(X2T, FL_X2_MINB) cross2d_kernel(XArgs a, const
   if (tid == 0 && S.evals && a.evals) atomicAdd(a.evals, S.evals);
 }
 
+// ---------------------------------------------------------------- uniform-order block pairs
+// Block pairs whose bounds fix one order k in {2, 3, 4} for all 32 x 32 cell pairs (disjoint
+// blocks) are the bulk of the work; cross2d_uni_kernel streams them.  Everything a block pair
+// needs is stored block-ordered (UData) so the next pair's data is copied into the second half
+// of a double buffer with cp.async while the current pair is computed: the mapped nodes of the
+// order k of both blocks (node-major: node r of cell c at [r][c], so the 32 lanes of a warp —
+// one column cell each — read consecutive 16-byte words), J per cell, the vertex slots and the
+// DoF lists.  Pairs are dealt round-robin over the CTAs (heaviest first), a warp takes one row
+// cell i against the 32 column cells, each lane its whole pair; contributions go to the int64
+// tile as in cross2d_kernel (fixed point, order-free), flushed to A once per pair.
+constexpr int UNODES = 928;                // per block: k = 2, 3, 4 segments of 32 k^2 nodes
+__host__ __device__ constexpr int useg(int k) { return k == 2 ? 0 : (k == 3 ? 128 : 416); }
+
+__global__ void block_unodes_kernel(const int* __restrict__ bcells, const double2* __restrict__ nodes, int nb,
+                                    const DevMesh m, const signed char* __restrict__ slot,
+                                    double2* __restrict__ un, double* __restrict__ uj, int* __restrict__ us) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * UNODES) return;
+  const int b = (int)(i / UNODES), x = (int)(i % UNODES);
+  const int k = x < 128 ? 2 : (x < 416 ? 3 : 4);
+  const int loc = x - useg(k), r = loc / CB, c = loc % CB;
+  const int cell = bcells[b * CB + c];
+  un[i] = cell >= 0 ? nodes[(int64_t)cell * NPRE2 + poff(k) + r] : make_double2(0.0, 0.0);
+  if (x < CB) {
+    const int cc = bcells[b * CB + x];
+    uj[b * CB + x] = cc >= 0 ? m.geo[cc].J : 0.0;
+    int pk = 0xffffff;                         // three slot bytes (0xff: not a DoF of the block)
+    if (cc >= 0)
+      for (int v = 0; v < 3; ++v) pk = (pk & ~(0xff << (8 * v))) | ((int)(unsigned char)slot[cc * 3 + v] << (8 * v));
+    us[b * CB + x] = pk;
+  }
+}
+
+struct UArgs {
+  const int4* bpairs;                 // (P, Q, k, nP | nQ << 16)
+  int nbp;
+  const double2* un;
+  const double* uj;
+  const int* us;
+  const int* bdofs;
+  double ex, cs, lim;
+  unsigned long long* A;
+  int64_t lda;
+  int r0, r1;
+  unsigned long long* evals;
+  int* ovf;
+};
+
+struct UBuf {
+  double2 nd[2][16 * CB];             // [block][node r * 32 + cell]
+  double J[2][CB];
+  int sl[2][CB];
+  int dof[2][BRMAX];
+};
+struct UShared {
+  UBuf b[2];
+  unsigned long long tile[TCAP];
+  double wl[NPRE2][3];
+  unsigned long long evals;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// issue the copies of block pair `pr` into buffer B (every thread its share of 16-byte chunks)
+__device__ __forceinline__ void u_stage(const UArgs& a, UBuf& B, int4 pr, int tid) {
+  const int k = pr.z, nn = CB * k * k;           // nodes per block (16-byte chunks)
+  const int tot = 2 * nn + 2 * 16 + 2 * 8 + 2 * 16;
+  for (int c = tid; c < tot; c += X2T) {
+    int x = c;
+    if (x < 2 * nn) {
+      const int side = x >= nn, r = x - side * nn;
+      cp_async16(&B.nd[side][r], a.un + (int64_t)(side ? pr.y : pr.x) * UNODES + useg(k) + r);
+      continue;
+    }
+    x -= 2 * nn;
+    if (x < 32) {
+      const int side = x >= 16, r = x - side * 16;
+      cp_async16(&B.J[side][2 * r], a.uj + (int64_t)(side ? pr.y : pr.x) * CB + 2 * r);
+      continue;
+    }
+    x -= 32;
+    if (x < 16) {
+      const int side = x >= 8, r = x - side * 8;
+      cp_async16(&B.sl[side][4 * r], a.us + (int64_t)(side ? pr.y : pr.x) * CB + 4 * r);
+      continue;
+    }
+    x -= 16;
+    const int side = x >= 16, r = x - side * 16;
+    cp_async16(&B.dof[side][4 * r], a.bdofs + (int64_t)(side ? pr.y : pr.x) * BRMAX + 4 * r);
+  }
+}
+
+// partial 3x3 block from the NX x nodes x0, x0 + XS, ... of row cell i against all NN y nodes of
+// column cell j (node-major staging: node r of cell c at [r * 32 + c])
+template <int E4, int NN, int NX, int XS>
+__device__ __forceinline__ void blk_part_nm(const double2* __restrict__ Xb, const double2* __restrict__ Yb, int i,
+                                            int j, const double (*__restrict__ w)[3], int x0, double ex,
+                                            double (&M)[3][3]) {
+  double X0[NX], X1[NX], t[NX][3];
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    const double2 X = Xb[(x0 + u * XS) * CB + i];
+    X0[u] = X.x;
+    X1[u] = X.y;
+    t[u][0] = t[u][1] = t[u][2] = 0.0;
+  }
+#pragma unroll(NN <= 4 ? NN : 3)
+  for (int y = 0; y < NN; ++y) {
+    const double2 Y = Yb[y * CB + j];
+    const double w0 = w[y][0], w1 = w[y][1], w2 = w[y][2];
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const double d0 = X0[u] - Y.x, d1 = X1[u] - Y.y;
+      const double v = kpow<E4>(fma(d1, d1, d0 * d0), ex);
+      t[u][0] = fma(v, w0, t[u][0]);
+      t[u][1] = fma(v, w1, t[u][1]);
+      t[u][2] = fma(v, w2, t[u][2]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    const int x = x0 + u * XS;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      M[a][0] = fma(w[x][a], t[u][0], M[a][0]);
+      M[a][1] = fma(w[x][a], t[u][1], M[a][1]);
+      M[a][2] = fma(w[x][a], t[u][2], M[a][2]);
+    }
+  }
+}
+
+#ifndef FL_XU_MINB
+#define FL_XU_MINB 2
+#endif
+template <int E4>
+__global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, const double* __restrict__ wl_g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  UShared& S = *reinterpret_cast<UShared*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < NPRE2 * 3; i += X2T) (&S.wl[0][0])[i] = wl_g[i];
+  for (int i = tid; i < TCAP; i += X2T) S.tile[i] = 0ull;
+  if (tid == 0) S.evals = 0;
+  int it = blockIdx.x;
+  if (it >= a.nbp) return;
+  int4 cur = a.bpairs[it];
+  u_stage(a, S.b[0], cur, tid);
+  cp_async_commit();
+  int4 nxt = it + (int)gridDim.x < a.nbp ? a.bpairs[it + gridDim.x] : make_int4(0, 0, 0, 0);
+  unsigned long long my = 0;
+  int bsel = 0;
+  for (; it < a.nbp; it += gridDim.x) {
+    cp_async_wait_all();
+    __syncthreads();                             // buffer bsel holds `cur`; the tile is flushed
+    const bool more = it + (int)gridDim.x < a.nbp;
+    if (more) u_stage(a, S.b[bsel ^ 1], nxt, tid);
+    cp_async_commit();
+    const int4 pr = cur;
+    cur = nxt;
+    if (it + 2 * (int)gridDim.x < a.nbp) nxt = a.bpairs[it + 2 * gridDim.x];   // record two ahead
+    const UBuf& B = S.b[bsel];
+    const int k = pr.z, nP = pr.w & 0xffff, nQ = pr.w >> 16;
+    const bool in_tile = nP * nQ <= TCAP;
+#pragma unroll 1
+    for (int i = wid; i < CB; i += X2T / 32) {
+      const int j = lane;
+      const double JJ = B.J[0][i] * B.J[1][j];
+      if (JJ == 0.0) continue;                   // an empty slot of a partial block
+      double M[3][3] = {};
+      if (k == 2) {
+        blk_part_nm<E4, 4, 4, 1>(B.nd[0], B.nd[1], i, j, S.wl + poff(2), 0, a.ex, M);
+      } else if (k == 3) {
+#pragma unroll 1
+        for (int xs = 0; xs < 3; ++xs) blk_part_nm<E4, 9, 3, 3>(B.nd[0], B.nd[1], i, j, S.wl + poff(3), xs, a.ex, M);
+      } else {
+#pragma unroll 1
+        for (int xs = 0; xs < 4; ++xs)
+          blk_part_nm<E4, 16, 4, 4>(B.nd[0], B.nd[1], i, j, S.wl + poff(4), xs, a.ex, M);
+      }
+      const int spk = B.sl[0][i], tpk = B.sl[1][j];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        const int si = (spk >> (8 * x)) & 0xff;
+        if (si == 0xff) continue;
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          const int sj = (tpk >> (8 * y)) & 0xff;
+          if (sj == 0xff) continue;
+          const double v = (M[x][y] * JJ) * a.cs;
+          if (!(fabs(v) < a.lim)) atomicOr(a.ovf, 1);
+          const unsigned long long q = (unsigned long long)__double2ll_rn(v);
+          if (in_tile) {
+            atomicAdd(&S.tile[si * nQ + sj], q);
+          } else {
+            const int gi = B.dof[0][si], gj = B.dof[1][sj];
+            if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
+            if (gj >= a.r0 && gj < a.r1) atomicAdd(&a.A[(int64_t)(gj - a.r0) * a.lda + gi], q);
+          }
+        }
+      }
+      my += (unsigned long long)(k * k) * (k * k);
+    }
+    __syncthreads();
+    if (in_tile) {
+      for (int idx = tid; idx < nP * nQ; idx += X2T) {
+        const unsigned long long q = S.tile[idx];
+        if (!q) continue;
+        S.tile[idx] = 0ull;
+        const int r = idx / nQ, c = idx - r * nQ;
+        const int gi = B.dof[0][r], gj = B.dof[1][c];
+        if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
+        if (gj >= a.r0 && gj < a.r1) atomicAdd(&a.A[(int64_t)(gj - a.r0) * a.lda + gi], q);
+      }
+    }
+    bsel ^= 1;
+  }
+  cp_async_wait_all();
+  if (my) atomicAdd(&S.evals, my);
+  __syncthreads();
+  if (tid == 0 && S.evals && a.evals) atomicAdd(a.evals, S.evals);
+}
+
+__global__ void uni_flag_kernel(const int4* __restrict__ all, int n, const int* __restrict__ bndof,
+                                int4* __restrict__ allw, int* __restrict__ uf, int* __restrict__ rf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 p = all[i];
+  p.w = bndof[p.x] | (bndof[p.y] << 16);
+  allw[i] = p;
+  const int u = p.z >= 2 && p.z < KW2D;
+  uf[i] = u;
+  rf[i] = !u;
+}
+
 __global__ void iota_kernel64(int* a, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = (int)i;
@@ -743,6 +981,35 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   FL_CUDA(cudaMemcpyAsync(hn, nsel.p, sizeof(hn), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   const int nall = hn[0], nnear = hn[1];
+  // uniform-order block pairs (k = 2..4) for the streaming kernel, the rest for cross2d_kernel
+  static const bool uni_off = [] {             // FRACLAP_CROSS2D_UNI=0: every pair through cross2d_kernel
+    const char* v = getenv("FRACLAP_CROSS2D_UNI");
+    return v && std::string(v) == "0";
+  }();
+  DBuf<int4> allw(std::max(nall, 1)), ulist(std::max(nall, 1)), rlist(std::max(nall, 1));
+  DBuf<int> uf(std::max(nall, 1)), rf(std::max(nall, 1)), nsel2(2);
+  int hu[2] = {0, nall};
+  if (nall > 0 && !uni_off) {
+    uni_flag_kernel<<<(nall + 255) / 256, 256, 0, st>>>(all.p, nall, bndof.p, allw.p, uf.p, rf.p), note_launch();
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, allw.p, uf.p, ulist.p, nsel2.p, nall, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, allw.p, uf.p, ulist.p, nsel2.p, nall, st));
+    FL_CUDA(cub::DeviceSelect::Flagged(tb.p, tmp, allw.p, rf.p, rlist.p, nsel2.p + 1, nall, st));
+    FL_CUDA(cudaMemcpyAsync(hu, nsel2.p, sizeof(hu), cudaMemcpyDeviceToHost, st));
+    FL_CUDA(cudaStreamSynchronize(st));
+  }
+  const int nuni = hu[0], nrest = hu[1];
+  const int4* rest = (nall > 0 && !uni_off) ? rlist.p : all.p;
+  DBuf<double2> un;
+  DBuf<double> uj;
+  DBuf<int> us;
+  if (nuni > 0) {
+    un.alloc((size_t)nb * UNODES); uj.alloc((size_t)nb * CB); us.alloc((size_t)nb * CB);
+    block_unodes_kernel<<<(unsigned)(((int64_t)nb * UNODES + 255) / 256), 256, 0, st>>>(bcells.p, nodes.p, nb, m,
+                                                                                      slot.p, un.p, uj.p, us.p),
+        note_launch();
+  }
   info.block_pairs = nall;
   info.near_block_pairs = nnear;
   // ---- A (int64 view) zeroed
@@ -791,11 +1058,24 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   if (t_near) FL_CUDA(cudaEventRecord(t_near, st));
   // ---- pass 2: every block pair
   FL_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
-  xa.bpairs = all.p; xa.nbp = nall; xa.queue = queue.p;
+  xa.bpairs = rest; xa.nbp = nrest; xa.queue = queue.p;
   xa.near_keys = nullptr; xa.near_count = nullptr; xa.near_cap = 0;
   xa.nearH = near.hkey.p; xa.nearI = near.hidx.p; xa.hmask = near.hmask; xa.nearG = near.G.p;
-  if (nall > 0) {
-    const int grid = std::min(nall, FL_X2_MINB * sms);
+  if (nuni > 0) {
+    UArgs ua{};
+    ua.bpairs = ulist.p; ua.nbp = nuni; ua.un = un.p; ua.uj = uj.p; ua.us = us.p; ua.bdofs = bdofs.p;
+    ua.ex = ex; ua.cs = xa.cs; ua.lim = xa.lim; ua.A = Ai; ua.lda = lda; ua.r0 = row_begin; ua.r1 = row_end;
+    ua.evals = evals; ua.ovf = ovf.p;
+    const size_t usm = sizeof(UShared);
+    const int grid = std::min(nuni, FL_XU_MINB * sms);
+    FL_E4_SWITCH2(e4, {
+      FL_CUDA(cudaFuncSetAttribute(cross2d_uni_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+      cross2d_uni_kernel<E4><<<grid, X2T, usm, st>>>(ua, wl.p), note_launch();
+    });
+    FL_CHECK_LAUNCH();
+  }
+  if (nrest > 0) {
+    const int grid = std::min(nrest, FL_X2_MINB * sms);
     FL_E4_SWITCH2(e4, {
       FL_CUDA(cudaFuncSetAttribute(cross2d_kernel<E4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       cross2d_kernel<E4, false><<<grid, X2T, smem, st>>>(xa, wl.p), note_launch();
