@@ -251,6 +251,18 @@ __global__ void block_pairs_kernel(OrderConsts oc, const double* __restrict__ bs
   key[i] = __float_as_uint((float)fmax(Dmin, 0.0));      // heavy first: ascending gap
 }
 
+// 64-bit fixed-point add into a shared-memory tile word with two native 32-bit shared atomics
+// (a 64-bit shared atomicAdd compiles to a compare-and-swap loop): the low words add modulo 2^32
+// and the carry read from the returned old value goes into the high word, so once every add has
+// landed the word holds the exact 64-bit sum, whatever the order.
+__device__ __forceinline__ void tile_add(unsigned long long* w, unsigned long long q) {
+  unsigned* p = reinterpret_cast<unsigned*>(w);
+  const unsigned ql = (unsigned)q, qh = (unsigned)(q >> 32);
+  const unsigned old = atomicAdd(p, ql);
+  const unsigned hi = qh + ((unsigned)(old + ql) < old ? 1u : 0u);
+  if (hi) atomicAdd(p + 1, hi);
+}
+
 // ---------------------------------------------------------------- the block-pair kernel
 // Partial 3x3 block of one cell pair from the lane's NX x nodes x0, x0 + XS, ... (node
 // coordinates and w*lambda staged in shared memory): each y node and its weights are loaded
@@ -384,8 +396,8 @@ __global__ void __launch_bounds__(X2T, FL_X2_MINB) cross2d_kernel(XArgs a, const
           if (!(fabs(v) < a.lim)) atomicOr(a.ovf, 1);
           const unsigned long long q = (unsigned long long)__double2ll_rn(v);
           if (in_tile) {
-            atomicAdd(&S.tile[si * nQ + sj], q);
-            if (diag) atomicAdd(&S.tile[sj * nQ + si], q);
+            tile_add(&S.tile[si * nQ + sj], q);
+            if (diag) tile_add(&S.tile[sj * nQ + si], q);
           } else {
             const int gi = S.dofP[si], gj = S.dofQ[sj];
             if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
@@ -624,6 +636,7 @@ struct UArgs {
   const int* us;
   const int* bdofs;
   double ex, cs, lim;
+  long long limq;                     // lim as an integer: |scaled contribution| < limq
   unsigned long long* A;
   int64_t lda;
   int r0, r1;
@@ -767,6 +780,8 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
           blk_part_nm<E4, 16, 4, 4>(B.nd[0], B.nd[1], i, j, S.wl + poff(4), xs, a.ex, M);
       }
       const int spk = B.sl[0][i], tpk = B.sl[1][j];
+      const double sc = JJ * a.cs;
+      bool bad = false;
 #pragma unroll
       for (int x = 0; x < 3; ++x) {
         const int si = (spk >> (8 * x)) & 0xff;
@@ -775,11 +790,11 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
         for (int y = 0; y < 3; ++y) {
           const int sj = (tpk >> (8 * y)) & 0xff;
           if (sj == 0xff) continue;
-          const double v = (M[x][y] * JJ) * a.cs;
-          if (!(fabs(v) < a.lim)) atomicOr(a.ovf, 1);
-          const unsigned long long q = (unsigned long long)__double2ll_rn(v);
+          const long long qs = __double2ll_rn(M[x][y] * sc);
+          bad |= (unsigned long long)(qs + a.limq) > 2ull * (unsigned long long)a.limq;   // |q| >= limq, NaN
+          const unsigned long long q = (unsigned long long)qs;
           if (in_tile) {
-            atomicAdd(&S.tile[si * nQ + sj], q);
+            tile_add(&S.tile[si * nQ + sj], q);
           } else {
             const int gi = B.dof[0][si], gj = B.dof[1][sj];
             if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
@@ -787,6 +802,7 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
           }
         }
       }
+      if (bad) atomicOr(a.ovf, 1);
       my += (unsigned long long)(k * k) * (k * k);
     }
     __syncthreads();
@@ -1064,7 +1080,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   if (nuni > 0) {
     UArgs ua{};
     ua.bpairs = ulist.p; ua.nbp = nuni; ua.un = un.p; ua.uj = uj.p; ua.us = us.p; ua.bdofs = bdofs.p;
-    ua.ex = ex; ua.cs = xa.cs; ua.lim = xa.lim; ua.A = Ai; ua.lda = lda; ua.r0 = row_begin; ua.r1 = row_end;
+    ua.ex = ex; ua.cs = xa.cs; ua.lim = xa.lim; ua.limq = (long long)xa.lim; ua.A = Ai; ua.lda = lda; ua.r0 = row_begin; ua.r1 = row_end;
     ua.evals = evals; ua.ovf = ovf.p;
     const size_t usm = sizeof(UShared);
     const int grid = std::min(nuni, FL_XU_MINB * sms);
