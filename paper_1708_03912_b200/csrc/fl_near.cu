@@ -21,8 +21,8 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
                                                              const int* __restrict__ KK, int64_t n,
                                                              double* __restrict__ G,
                                                              unsigned long long* __restrict__ evals) {
-  __shared__ double2 sy[NW][NMAXN];
-  __shared__ double slw[NW][NMAXN][3];
+  __shared__ double4 syw[NW][NMAXN];   // y node (x, y) and w*lambda_0, w*lambda_1
+  __shared__ double sw2[NW][NMAXN];    // w*lambda_2
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long my = 0;
   for (int64_t pi = (int64_t)blockIdx.x * NW + w; pi < n; pi += (int64_t)gridDim.x * NW) {
@@ -41,10 +41,8 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
         Y0 = B.p[0][0] + (nd[0] * (B.p[1][0] - B.p[0][0]) + nd[1] * (B.p[2][0] - B.p[0][0]));
         Y1 = B.p[0][1] + (nd[0] * (B.p[1][1] - B.p[0][1]) + nd[1] * (B.p[2][1] - B.p[0][1]));
       }
-      sy[w][y] = make_double2(Y0, Y1);
-      slw[w][y][0] = nd[3];
-      slw[w][y][1] = nd[4];
-      slw[w][y][2] = nd[5];
+      syw[w][y] = make_double4(Y0, Y1, nd[3], nd[4]);
+      sw2[w][y] = nd[5];
     }
     __syncwarp();
     // work items (x node, y chunk): split the y range so that k^d * S fills the warp well
@@ -69,11 +67,12 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
         X0 = A.p[0][0] + (nx[0] * (A.p[1][0] - A.p[0][0]) + nx[1] * (A.p[2][0] - A.p[0][0]));
         X1 = A.p[0][1] + (nx[0] * (A.p[1][1] - A.p[0][1]) + nx[1] * (A.p[2][1] - A.p[0][1]));
       }
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      // two independent accumulator sets (even / odd y), summed in a fixed order
+      double ta0 = 0.0, ta1 = 0.0, ta2 = 0.0, tb0 = 0.0, tb1 = 0.0, tb2 = 0.0;
       const int y1 = min(nn, (c + 1) * chunk);
-#pragma unroll 2
-      for (int y = c * chunk; y < y1; ++y) {
-        const double2 Y = sy[w][y];
+      int y = c * chunk;
+      auto eval = [&](int yy, double& t0, double& t1, double& t2) {
+        const double4 Y = syw[w][yy];
         const double d0 = X0 - Y.x;
         double r2;
         if (D == 1) {
@@ -83,10 +82,17 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
           r2 = fma(d1, d1, d0 * d0);
         }
         const double v = kpow<E4>(r2, ex);
-        t0 = fma(v, slw[w][y][0], t0);
-        t1 = fma(v, slw[w][y][1], t1);
-        if (D == 2) t2 = fma(v, slw[w][y][2], t2);
+        t0 = fma(v, Y.z, t0);
+        t1 = fma(v, Y.w, t1);
+        if (D == 2) t2 = fma(v, sw2[w][yy], t2);
+      };
+#pragma unroll 2
+      for (; y + 1 < y1; y += 2) {
+        eval(y, ta0, ta1, ta2);
+        eval(y + 1, tb0, tb1, tb2);
       }
+      if (y < y1) eval(y, ta0, ta1, ta2);
+      const double t0 = ta0 + tb0, t1 = ta1 + tb1, t2 = ta2 + tb2;
 #pragma unroll
       for (int a = 0; a <= D; ++a) {
         const double lx = nx[3 + a];

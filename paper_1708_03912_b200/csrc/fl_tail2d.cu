@@ -42,7 +42,8 @@ __global__ void tail_flag_kernel(const int* __restrict__ targets, int ntargets, 
 }
 
 // kuni[P * nb + Q] for the target blocks P: one order for every (target in P, source in Q) pair
-// when the bounds of the boosted order formula agree, else 0
+// when the bounds of the boosted order formula agree; -1 when the blocks are disjoint but the
+// orders are not uniform (then decided per target cell, cell_block_korder); 0 otherwise
 __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, const int* __restrict__ tflag, int nb,
                                  int8_t* __restrict__ kuni) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -61,7 +62,7 @@ __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, 
       const double lo = order_bound_lo(oc, oc.coff_tail, Dmin, Dmax, hmn, hmx, lmn, lmx);
       const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
       const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
-      if (c0 == c1) k = (int)c0;
+      k = c0 == c1 ? (int)c0 : -1;  // -1: per target cell (cell_block_korder)
     }
   }
   kuni[i] = (int8_t)k;
@@ -84,12 +85,39 @@ __device__ __forceinline__ double geo_field(const DevMesh& m, const int* __restr
   }
 }
 
+// the thread's two targets against the nwp staged source nodes, TU per step (MASK: weights times
+// wsel, 0 for a thread whose cell takes another order from this block)
+template <int E4, bool MASK>
+__device__ __forceinline__ void sweep(const double2* __restrict__ sY, const double* __restrict__ sW, int nwp,
+                                      const double (&x0)[2], const double (&x1)[2], double wsel, double ex,
+                                      double (&acc)[2][2]) {
+#pragma unroll 1
+  for (int p = 0; p < nwp; p += TU) {
+    double2 y[TU];
+    double w[TU];
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      y[u] = sY[p + u];
+      w[u] = MASK ? sW[p + u] * wsel : sW[p + u];
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        const double d0 = x0[t] - y[u].x, d1 = x1[t] - y[u].y;
+        acc[t][u & 1] = fma(w[u], kpow<E4>(fma(d1, d1, d0 * d0), ex), acc[t][u & 1]);
+      }
+  }
+}
+
 template <int E4>
 __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
-                                                            double ex, const int8_t* __restrict__ kuni,
+                                                            OrderConsts oc, double ex,
+                                                            const int8_t* __restrict__ kuni,
                                                             const int* __restrict__ tflag,
                                                             const int* __restrict__ tcell,
-                                                            const int* __restrict__ bcells, int nb,
+                                                            const int* __restrict__ bcells,
+                                                            const double* __restrict__ bstat, int nb,
                                                             double* __restrict__ psi,
                                                             unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -97,9 +125,10 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   double* sW = reinterpret_cast<double*>(sY + TWIN);           // TWIN J * w
   double* sR = sW + TWIN;                                      // RULE_NODES x (u0, u1, w)
   double* sG = sR + 3 * RULE_NODES;                            // TB x 8 geometry fields
-  int* sL = reinterpret_cast<int*>(sG + 8 * TB);               // uniform source blocks: Q | k << 24
+  int* sL = reinterpret_cast<int*>(sG + 8 * TB);               // source blocks: Q | (k & 0xff) << 24
   __shared__ int s_wsum[TT / 32];
   __shared__ int s_nq;
+  __shared__ int s_kc[TB];                                     // per target cell order (mixed blocks)
   const int P = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (!tflag[P]) return;
   // ---- the disjoint rules k = 2..9 (reference nodes and weights)
@@ -115,7 +144,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
       sR[3 * i] = sR[3 * i + 1] = sR[3 * i + 2] = 0.0;
     }
   }
-  // ---- the uniform source blocks of P in ascending order (block-wide ordered compaction)
+  // ---- the source blocks of P handled here (uniform or mixed), ascending (ordered compaction)
   const int8_t* krow = kuni + (size_t)P * nb;
   if (tid == 0) s_nq = 0;
   __syncthreads();
@@ -127,7 +156,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     __syncthreads();
     int off = s_nq;
     for (int w = 0; w < wid; ++w) off += s_wsum[w];
-    if (k) sL[off + __popc(bal & ((1u << lane) - 1u))] = Q | (k << 24);
+    if (k) sL[off + __popc(bal & ((1u << lane) - 1u))] = Q | ((k & 0xff) << 24);
     __syncthreads();
     if (tid == 0) {
       int tot = 0;
@@ -137,16 +166,15 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     __syncthreads();
   }
   const int nq = s_nq;
-  // ---- the thread's two target nodes
+  // ---- the thread's two target nodes: cell tid / 8, nodes tid % 8 and tid % 8 + 8
+  const int cme = tid >> 3, q0 = tid & 7;
+  int Kc = bcells[P * TB + cme];
+  if (Kc >= 0 && !tcell[Kc]) Kc = -1;                // a cell of the block that is not a target
   double x0[2], x1[2];
-  int Kc[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    const int i = tid + t * TT, c = i / TQN, q = i % TQN;
-    Kc[t] = bcells[P * TB + c];
-    if (Kc[t] >= 0 && !tcell[Kc[t]]) Kc[t] = -1;      // a cell of the block that is not a target
-    x0[t] = Kc[t] >= 0 ? m.X[((size_t)Kc[t] * TQN + q) * 2 + 0] : 1e100;
-    x1[t] = Kc[t] >= 0 ? m.X[((size_t)Kc[t] * TQN + q) * 2 + 1] : 1e100;
+    x0[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 0] : 1e100;
+    x1[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 1] : 1e100;
   }
   int ntv = 0;                       // target cells of the block (evaluation count)
   if (tid == 0)
@@ -154,67 +182,77 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
       const int K = bcells[P * TB + c];
       ntv += K >= 0 && tcell[K];
     }
+  const int Kw = tid < TB ? bcells[P * TB + tid] : -1;     // thread c < 32: target cell c (orders)
+  const bool Kw_t = Kw >= 0 && tcell[Kw];
   double acc[2][2] = {};
   unsigned long long nev = 0;
   double gpre = nq > 0 ? geo_field(m, bcells, sL[0] & 0xffffff, tid) : 0.0;
   bool missing = false;
   for (int qi = 0; qi < nq; ++qi) {
-    const int k = sL[qi] >> 24, kk = k * k;
+    const int Q = sL[qi] & 0xffffff;
+    const int kq = (int)(int8_t)(sL[qi] >> 24);   // > 0: uniform, -1: per target cell
     __syncthreads();                 // the previous block's windows are consumed
     sG[tid] = gpre;
+    if (kq < 0 && tid < TB) s_kc[tid] = Kw_t ? cell_block_korder(oc, oc.coff_tail, m.geo[Kw], bstat + 8 * Q) : 0;
     __syncthreads();
     if (qi + 1 < nq) gpre = geo_field(m, bcells, sL[qi + 1] & 0xffffff, tid);   // in flight meanwhile
-    if (tid == 0 && dir.rule(T_DISJ, k).cnt != kk) missing = true;
-    const double* R = sR + 3 * roff(k);
-    const int cpw = TWIN / kk;       // cells per window (>= 12)
-    for (int c0 = 0; c0 < TB; c0 += cpw) {
-      const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + TU - 1) / TU * TU;
-      if (c0 > 0) __syncthreads();
-      for (int idx = tid; idx < nwp; idx += TT) {
-        double2 y = make_double2(1e100, 1e100);
-        double w = 0.0;
-        if (idx < nw) {
-          const int c = c0 + idx / kk, r = idx - (idx / kk) * kk;
-          const double* g = sG + 8 * c;
-          if (g[7] != 0.0) {
-            const double u0 = R[3 * r], u1 = R[3 * r + 1];
-            y.x = g[0] + (u0 * g[2] + u1 * g[4]);
-            y.y = g[1] + (u0 * g[3] + u1 * g[5]);
-            w = g[6] * R[3 * r + 2];
-          }
-        }
-        sY[idx] = y;
-        sW[idx] = w;
+    unsigned kset;                   // bit k: some target cell takes order k from this block here
+    if (kq > 0) {
+      kset = 1u << kq;
+    } else {
+      kset = 0;
+      for (int c = 0; c < TB; ++c) kset |= (1u << s_kc[c]);
+      kset &= ~1u;                   // order 0: that cell leaves the block to the warp tail
+    }
+    const int kmine = kq > 0 ? kq : s_kc[cme];
+    for (unsigned ks = kset; ks; ks &= ks - 1) {
+      const int k = __ffs(ks) - 1, kk = k * k;
+      if (tid == 0 && dir.rule(T_DISJ, k).cnt != kk) missing = true;
+      int ntk = ntv;                 // target cells evaluated at order k
+      if (kq < 0 && tid == 0) {
+        ntk = 0;
+        for (int c = 0; c < TB; ++c) ntk += s_kc[c] == k;
       }
-      if (tid == 0) {
-        int nvs = 0;
-        for (int c = c0; c < c1; ++c) nvs += sG[8 * c + 7] != 0.0;
-        nev += (unsigned long long)nvs * kk * ntv * TQN;
-      }
-      __syncthreads();
-#pragma unroll 1
-      for (int p = 0; p < nwp; p += TU) {
-        double2 y[TU];
-        double w[TU];
-#pragma unroll
-        for (int u = 0; u < TU; ++u) {
-          y[u] = sY[p + u];
-          w[u] = sW[p + u];
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int u = 0; u < TU; ++u) {
-            const double d0 = x0[t] - y[u].x, d1 = x1[t] - y[u].y;
-            acc[t][u & 1] = fma(w[u], kpow<E4>(fma(d1, d1, d0 * d0), ex), acc[t][u & 1]);
+      // warps with none of their 4 cells at order k skip the sweep; a thread of such a warp
+      // whose own cell is at another order adds exact zeros (weight 0)
+      const bool wact = __any_sync(0xffffffffu, kmine == k);
+      const double wsel = kmine == k ? 1.0 : 0.0;
+      const double* R = sR + 3 * roff(k);
+      const int cpw = TWIN / kk;     // cells per window (>= 12)
+      for (int c0 = 0; c0 < TB; c0 += cpw) {
+        const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + TU - 1) / TU * TU;
+        if (c0 > 0 || ks != kset) __syncthreads();
+        for (int idx = tid; idx < nwp; idx += TT) {
+          double2 y = make_double2(1e100, 1e100);
+          double w = 0.0;
+          if (idx < nw) {
+            const int c = c0 + idx / kk, r = idx - (idx / kk) * kk;
+            const double* g = sG + 8 * c;
+            if (g[7] != 0.0) {
+              const double u0 = R[3 * r], u1 = R[3 * r + 1];
+              y.x = g[0] + (u0 * g[2] + u1 * g[4]);
+              y.y = g[1] + (u0 * g[3] + u1 * g[5]);
+              w = g[6] * R[3 * r + 2];
+            }
           }
+          sY[idx] = y;
+          sW[idx] = w;
+        }
+        if (tid == 0) {
+          int nvs = 0;
+          for (int c = c0; c < c1; ++c) nvs += sG[8 * c + 7] != 0.0;
+          nev += (unsigned long long)nvs * kk * ntk * TQN;
+        }
+        __syncthreads();
+        if (!wact) continue;
+        if (kq > 0) sweep<E4, false>(sY, sW, nwp, x0, x1, 1.0, ex, acc);
+        else sweep<E4, true>(sY, sW, nwp, x0, x1, wsel, ex, acc);
       }
     }
   }
+  if (Kc >= 0) {
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int i = tid + t * TT;
-    if (Kc[t] >= 0) psi[(size_t)Kc[t] * TQN + i % TQN] = acc[t][0] + acc[t][1];
+    for (int t = 0; t < 2; ++t) psi[(size_t)Kc * TQN + q0 + 8 * t] = acc[t][0] + acc[t][1];
   }
   if (tid == 0) {
     if (missing) atomicOr(m.err, 1);
@@ -254,13 +292,14 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
   if (e0) FL_CUDA(cudaEventRecord(e0, st));
   FL_E4_SWITCH_T(e4, {
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, ex, kuni.p, tflag.p, tcell.p, B.bcells.p, nb, psi,
+    tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, tcell.p, B.bcells.p,
+                                                  B.bstat.p, nb, psi,
                                                   evals_block ? evals_block : evals),
         note_launch();
   });
   FL_CHECK_LAUNCH();
   if (e1) FL_CUDA(cudaEventRecord(e1, st));
-  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb);
+  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb, B.bstat.p);
 }
 
 }  // namespace fl
