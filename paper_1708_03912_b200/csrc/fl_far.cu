@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
                                                                   const int8_t* __restrict__ kuni,
                                                                   const int* __restrict__ blk_of,
                                                                   const int* __restrict__ bcells, int nb,
-                                                                  const double* __restrict__ bstat) {
+                                                                  const int8_t* __restrict__ kcell) {
   constexpr int Q = (D == 1) ? 6 : 16;     // cell quadrature nodes (XQ_ORDER)
   constexpr int L = Q / TAIL_T;            // lanes per group (8 in 2D, 3 in 1D)
   constexpr int G = 32 / L;                // groups sweeping disjoint source nodes (4 / 10)
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
         const int kq = cbase + lane < nchunk ? (int)krow[cbase + lane] : 1;
         // 0: the whole source block is ours; -1: ours unless K alone has one order for it
         // (then tail2d_block_kernel took it, by the same bitwise decision)
-        const bool mine = kq == 0 || (kq < 0 && cell_block_korder(oc, oc.coff_tail, A, bstat + 8 * (cbase + lane)) == 0);
+        const bool mine = kq == 0 || (kq < 0 && kcell[(size_t)K * nb + cbase + lane] == 0);
         pend = __ballot_sync(0xffffffffu, mine);
       }
       if (!pend) break;
@@ -938,13 +938,13 @@ __global__ void orders_kernel(DevMesh m, OrderConsts oc, int8_t* cross_k, int8_t
 
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                  const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st,
-                 const int8_t* kuni, const int* blk_of, const int* bcells, int nb, const double* bstat) {
+                 const int8_t* kuni, const int* blk_of, const int* bcells, int nb, const int8_t* kcell) {
   if (ntargets <= 0) return;
   const int grid = (ntargets + TAIL_WARPS - 1) / TAIL_WARPS;
   if (m.d == 1) {
     FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, nullptr, nullptr, nullptr, 0, nullptr), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, bstat), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, kcell), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }

@@ -14,6 +14,76 @@ namespace fl {
 constexpr int NW = 8;          // warps per CTA
 constexpr int NMAXN = 81;      // max k^d nodes (2D cap 9; 1D k <= 32)
 
+// One pair's 3x3 block: lane l takes the x nodes l, l + 32, l + 64 (NX of them) and sweeps all y
+// nodes, which every lane reads at the same address (broadcast shared loads); NX = 1 keeps two
+// accumulator sets (even / odd y) for independent chains.  Fixed summation order.
+template <int D, int E4, int NX>
+__device__ __forceinline__ void near_pair(const CellGeo& A, const double* __restrict__ tab, RuleRef rr, int nn,
+                                          const double4* __restrict__ syw, const double* __restrict__ sw2, int lane,
+                                          double ex, double (&Gm)[3][3]) {
+  double X0[NX], X1[NX], t[NX][2][3];
+  bool ok[NX];
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    const int x = lane + 32 * u;
+    ok[u] = x < nn;
+    const double* nx = tab + (size_t)(rr.off + (ok[u] ? x : 0)) * NODE;
+    if (D == 1) {
+      X0[u] = A.p[0][0] + nx[0] * (A.p[1][0] - A.p[0][0]);
+      X1[u] = 0.0;
+    } else {
+      X0[u] = A.p[0][0] + (nx[0] * (A.p[1][0] - A.p[0][0]) + nx[1] * (A.p[2][0] - A.p[0][0]));
+      X1[u] = A.p[0][1] + (nx[0] * (A.p[1][1] - A.p[0][1]) + nx[1] * (A.p[2][1] - A.p[0][1]));
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) t[u][h][0] = t[u][h][1] = t[u][h][2] = 0.0;
+  }
+  auto eval = [&](int y, int h) {
+    const double4 Y = syw[y];
+    const double w2 = D == 2 ? sw2[y] : 0.0;
+#pragma unroll
+    for (int u = 0; u < NX; ++u) {
+      const double d0 = X0[u] - Y.x;
+      double r2;
+      if (D == 1) {
+        r2 = d0 * d0;
+      } else {
+        const double d1 = X1[u] - Y.y;
+        r2 = fma(d1, d1, d0 * d0);
+      }
+      const double v = kpow<E4>(r2, ex);
+      t[u][h][0] = fma(v, Y.z, t[u][h][0]);
+      t[u][h][1] = fma(v, Y.w, t[u][h][1]);
+      if (D == 2) t[u][h][2] = fma(v, w2, t[u][h][2]);
+    }
+  };
+  int y = 0;
+  if (NX == 1) {
+#pragma unroll 2
+    for (; y + 1 < nn; y += 2) {
+      eval(y, 0);
+      eval(y + 1, 1);
+    }
+    if (y < nn) eval(y, 0);
+  } else {
+#pragma unroll 2
+    for (; y < nn; ++y) eval(y, 0);
+  }
+#pragma unroll
+  for (int u = 0; u < NX; ++u) {
+    if (!ok[u]) continue;
+    const double* nx = tab + (size_t)(rr.off + lane + 32 * u) * NODE;
+    const double t0 = t[u][0][0] + t[u][1][0], t1 = t[u][0][1] + t[u][1][1], t2 = t[u][0][2] + t[u][1][2];
+#pragma unroll
+    for (int a = 0; a <= D; ++a) {
+      const double lx = nx[3 + a];
+      Gm[a][0] = fma(lx, t0, Gm[a][0]);
+      Gm[a][1] = fma(lx, t1, Gm[a][1]);
+      if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
+    }
+  }
+}
+
 template <int D, int E4>
 __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const double* __restrict__ tab,
                                                              DevTables dir, OrderConsts oc, double ex,
@@ -45,62 +115,10 @@ __global__ void __launch_bounds__(NW * 32) near_block_kernel(DevMesh m, const do
       sw2[w][y] = nd[5];
     }
     __syncwarp();
-    // work items (x node, y chunk): split the y range so that k^d * S fills the warp well
-    int S = 1;
-    {
-      float best = 0.f;
-      for (int s = 1; s <= 4; ++s) {
-        const int items = nn * s;
-        const float u = (float)items / (32.f * (float)((items + 31) / 32));
-        if (u > best + 1e-3f) { best = u; S = s; }
-      }
-    }
-    const int chunk = (nn + S - 1) / S;
     double Gm[3][3] = {};
-    for (int it = lane; it < nn * S; it += 32) {
-      const int x = it / S, c = it % S;
-      const double* nx = tab + (size_t)(rr.off + x) * NODE;
-      double X0, X1 = 0.0;
-      if (D == 1) {
-        X0 = A.p[0][0] + nx[0] * (A.p[1][0] - A.p[0][0]);
-      } else {
-        X0 = A.p[0][0] + (nx[0] * (A.p[1][0] - A.p[0][0]) + nx[1] * (A.p[2][0] - A.p[0][0]));
-        X1 = A.p[0][1] + (nx[0] * (A.p[1][1] - A.p[0][1]) + nx[1] * (A.p[2][1] - A.p[0][1]));
-      }
-      // two independent accumulator sets (even / odd y), summed in a fixed order
-      double ta0 = 0.0, ta1 = 0.0, ta2 = 0.0, tb0 = 0.0, tb1 = 0.0, tb2 = 0.0;
-      const int y1 = min(nn, (c + 1) * chunk);
-      int y = c * chunk;
-      auto eval = [&](int yy, double& t0, double& t1, double& t2) {
-        const double4 Y = syw[w][yy];
-        const double d0 = X0 - Y.x;
-        double r2;
-        if (D == 1) {
-          r2 = d0 * d0;
-        } else {
-          const double d1 = X1 - Y.y;
-          r2 = fma(d1, d1, d0 * d0);
-        }
-        const double v = kpow<E4>(r2, ex);
-        t0 = fma(v, Y.z, t0);
-        t1 = fma(v, Y.w, t1);
-        if (D == 2) t2 = fma(v, sw2[w][yy], t2);
-      };
-#pragma unroll 2
-      for (; y + 1 < y1; y += 2) {
-        eval(y, ta0, ta1, ta2);
-        eval(y + 1, tb0, tb1, tb2);
-      }
-      if (y < y1) eval(y, ta0, ta1, ta2);
-      const double t0 = ta0 + tb0, t1 = ta1 + tb1, t2 = ta2 + tb2;
-#pragma unroll
-      for (int a = 0; a <= D; ++a) {
-        const double lx = nx[3 + a];
-        Gm[a][0] = fma(lx, t0, Gm[a][0]);
-        Gm[a][1] = fma(lx, t1, Gm[a][1]);
-        if (D == 2) Gm[a][2] = fma(lx, t2, Gm[a][2]);
-      }
-    }
+    if (nn <= 32) near_pair<D, E4, 1>(A, tab, rr, nn, syw[w], sw2[w], lane, ex, Gm);
+    else if (nn <= 64) near_pair<D, E4, 2>(A, tab, rr, nn, syw[w], sw2[w], lane, ex, Gm);
+    else near_pair<D, E4, 3>(A, tab, rr, nn, syw[w], sw2[w], lane, ex, Gm);
     const double JJ = A.J * B.J;
 #pragma unroll
     for (int a = 0; a < 3; ++a)

@@ -45,7 +45,7 @@ __global__ void tail_flag_kernel(const int* __restrict__ targets, int ntargets, 
 // when the bounds of the boosted order formula agree; -1 when the blocks are disjoint but the
 // orders are not uniform (then decided per target cell, cell_block_korder); 0 otherwise
 __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, const int* __restrict__ tflag, int nb,
-                                 int8_t* __restrict__ kuni) {
+                                 int mixed, int8_t* __restrict__ kuni) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)nb * nb) return;
   const int P = (int)(i / nb), Q = (int)(i - (int64_t)P * nb);
@@ -62,10 +62,22 @@ __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, 
       const double lo = order_bound_lo(oc, oc.coff_tail, Dmin, Dmax, hmn, hmx, lmn, lmx);
       const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
       const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
-      k = c0 == c1 ? (int)c0 : -1;  // -1: per target cell (cell_block_korder)
+      k = c0 == c1 ? (int)c0 : (mixed ? -1 : 0);  // -1: per target cell (cell_block_korder)
     }
   }
   kuni[i] = (int8_t)k;
+}
+
+// per target cell K and mixed source block Q (kuni == -1): K's own order for the block, or 0
+__global__ void tail_kcell_kernel(OrderConsts oc, DevMesh m, const int* __restrict__ targets, int ntargets,
+                                  const int* __restrict__ blk_of, const int8_t* __restrict__ kuni,
+                                  const double* __restrict__ bs, int nb, int8_t* __restrict__ kcell) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)ntargets * nb) return;
+  const int t = (int)(i / nb), Q = (int)(i - (int64_t)t * nb);
+  const int K = targets[t];
+  if (kuni[(size_t)blk_of[K] * nb + Q] != -1) return;
+  kcell[(size_t)K * nb + Q] = (int8_t)cell_block_korder(oc, oc.coff_tail, m.geo[K], bs + 8 * Q);
 }
 
 // geometry field f of cell slot c of block Q: P0x P0y (P1-P0)x (P1-P0)y (P2-P0)x (P2-P0)y J valid
@@ -117,7 +129,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
                                                             const int* __restrict__ tflag,
                                                             const int* __restrict__ tcell,
                                                             const int* __restrict__ bcells,
-                                                            const double* __restrict__ bstat, int nb,
+                                                            const int8_t* __restrict__ kcell, int nb,
                                                             double* __restrict__ psi,
                                                             unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     const int kq = (int)(int8_t)(sL[qi] >> 24);   // > 0: uniform, -1: per target cell
     __syncthreads();                 // the previous block's windows are consumed
     sG[tid] = gpre;
-    if (kq < 0 && tid < TB) s_kc[tid] = Kw_t ? cell_block_korder(oc, oc.coff_tail, m.geo[Kw], bstat + 8 * Q) : 0;
+    if (kq < 0 && tid < TB) s_kc[tid] = Kw_t ? (int)kcell[(size_t)Kw * nb + Q] : 0;
     __syncthreads();
     if (qi + 1 < nq) gpre = geo_field(m, bcells, sL[qi + 1] & 0xffffff, tid);   // in flight meanwhile
     unsigned kset;                   // bit k: some target cell takes order k from this block here
@@ -288,18 +300,33 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
       note_launch();
   DBuf<int8_t> kuni((size_t)nb * nb);
   const int64_t nn = (int64_t)nb * nb;
-  tail_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, B.bstat.p, tflag.p, nb, kuni.p), note_launch();
+  // FRACLAP_TAIL2D_MIXED=1: disjoint non-uniform block pairs split per target cell (measured slower
+  // at c5: the masked two-order sweeps cost what the warp tail does)
+  static const bool mixed = [] {
+    const char* v = getenv("FRACLAP_TAIL2D_MIXED");
+    return v && std::string(v) == "1";
+  }();
+  tail_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, B.bstat.p, tflag.p, nb, mixed ? 1 : 0, kuni.p),
+      note_launch();
+  // per target cell orders of the mixed block pairs (read by both tail kernels: one decision)
+  DBuf<int8_t> kcell(mixed ? (size_t)m.nc * nb : 1);
+  if (mixed) {
+    const int64_t nt = (int64_t)ntargets * nb;
+    tail_kcell_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(oc, m, targets, ntargets, B.blk_of.p, kuni.p,
+                                                                    B.bstat.p, nb, kcell.p),
+        note_launch();
+  }
   if (e0) FL_CUDA(cudaEventRecord(e0, st));
   FL_E4_SWITCH_T(e4, {
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, tcell.p, B.bcells.p,
-                                                  B.bstat.p, nb, psi,
+                                                  kcell.p, nb, psi,
                                                   evals_block ? evals_block : evals),
         note_launch();
   });
   FL_CHECK_LAUNCH();
   if (e1) FL_CUDA(cudaEventRecord(e1, st));
-  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb, B.bstat.p);
+  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb, kcell.p);
 }
 
 }  // namespace fl

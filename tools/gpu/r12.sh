@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r12_t_all.log 2>&1
+echo "all rc=$?" >> gpurun_out/r12_t_all.log
+timeout 300 python tools/assemble_once.py c5 --reps 2 > gpurun_out/r12_c5.log 2>&1
+timeout 1200 python bench.py > gpurun_out/r12_bench.log 2>&1
+echo "bench rc=$?" >> gpurun_out/r12_bench.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r12_bench_ref.log 2>&1
+echo "ref rc=$?" >> gpurun_out/r12_bench_ref.log
