@@ -56,7 +56,9 @@ __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, 
     const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
     const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
     const double Dmax = (dc + a[2] + b[2]) * (1.0 + 1e-12);
-    if (Dmin > 0.0) {               // disjoint bounding circles: no pair touches
+    // disjoint bounding circles (no pair touches), at least the target block's radius apart: the
+    // centred r2 expansion of the block kernel then loses at most a factor 9 of relative accuracy
+    if (Dmin > 0.0 && Dmin >= a[2]) {
       const double hmn = fmin(a[3], b[3]), hmx = fmax(a[4], b[4]), lmn = fmin(a[5], b[5]), lmx = fmax(a[6], b[6]);
       const double hi = order_bound_hi(oc, oc.coff_tail, Dmin, hmn, hmx, lmn, lmx);
       const double lo = order_bound_lo(oc, oc.coff_tail, Dmin, Dmax, hmn, hmx, lmn, lmx);
@@ -98,26 +100,30 @@ __device__ __forceinline__ double geo_field(const DevMesh& m, const int* __restr
 }
 
 // the thread's two targets against the nwp staged source nodes, TU per step (MASK: weights times
-// wsel, 0 for a thread whose cell takes another order from this block)
+// wsel, 0 for a thread whose cell takes another order from this block).  Coordinates are relative
+// to the target block's centre c and r2 = |x'|^2 + |y'|^2 - 2 x'.y' = fma(x0', -2y0', fma(x1', -2y1',
+// |x'|^2 + |y'|^2)): 3 FP64 instructions instead of 4.  The cancellation factor (|x'| + |y'|)^2 / r2
+// stays below ~3 for a uniform source block (its distance exceeds the target block's radius), so r2
+// keeps a few-ulp relative accuracy.
 template <int E4, bool MASK>
-__device__ __forceinline__ void sweep(const double2* __restrict__ sY, const double* __restrict__ sW, int nwp,
-                                      const double (&x0)[2], const double (&x1)[2], double wsel, double ex,
-                                      double (&acc)[2][2]) {
+__device__ __forceinline__ void sweep(const double2* __restrict__ sM, const double2* __restrict__ sQ, int nwp,
+                                      const double (&x0)[2], const double (&x1)[2], const double (&xx)[2],
+                                      double wsel, double ex, double (&acc)[2][2]) {
 #pragma unroll 1
   for (int p = 0; p < nwp; p += TU) {
-    double2 y[TU];
-    double w[TU];
+    double2 my[TU], qw[TU];
 #pragma unroll
     for (int u = 0; u < TU; ++u) {
-      y[u] = sY[p + u];
-      w[u] = MASK ? sW[p + u] * wsel : sW[p + u];
+      my[u] = sM[p + u];             // (-2 y0', -2 y1')
+      qw[u] = sQ[p + u];             // (|y'|^2, J w)
+      if (MASK) qw[u].y *= wsel;
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t)
 #pragma unroll
       for (int u = 0; u < TU; ++u) {
-        const double d0 = x0[t] - y[u].x, d1 = x1[t] - y[u].y;
-        acc[t][u & 1] = fma(w[u], kpow<E4>(fma(d1, d1, d0 * d0), ex), acc[t][u & 1]);
+        const double r2 = fma(x0[t], my[u].x, fma(x1[t], my[u].y, xx[t] + qw[u].x));
+        acc[t][u & 1] = fma(qw[u].y, kpow<E4>(r2, ex), acc[t][u & 1]);
       }
   }
 }
@@ -129,13 +135,14 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
                                                             const int* __restrict__ tflag,
                                                             const int* __restrict__ tcell,
                                                             const int* __restrict__ bcells,
-                                                            const int8_t* __restrict__ kcell, int nb,
+                                                            const int8_t* __restrict__ kcell,
+                                                            const double* __restrict__ bstat, int nb,
                                                             double* __restrict__ psi,
                                                             unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* sY = reinterpret_cast<double2*>(smem_raw);          // TWIN mapped source nodes
-  double* sW = reinterpret_cast<double*>(sY + TWIN);           // TWIN J * w
-  double* sR = sW + TWIN;                                      // RULE_NODES x (u0, u1, w)
+  double2* sM = reinterpret_cast<double2*>(smem_raw);          // TWIN source nodes: -2 y' (centred)
+  double2* sQ = sM + TWIN;                                     // TWIN: |y'|^2, J * w
+  double* sR = reinterpret_cast<double*>(sQ + TWIN);           // RULE_NODES x (u0, u1, w)
   double* sG = sR + 3 * RULE_NODES;                            // TB x 8 geometry fields
   int* sL = reinterpret_cast<int*>(sG + 8 * TB);               // source blocks: Q | (k & 0xff) << 24
   __shared__ int s_wsum[TT / 32];
@@ -182,11 +189,13 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   const int cme = tid >> 3, q0 = tid & 7;
   int Kc = bcells[P * TB + cme];
   if (Kc >= 0 && !tcell[Kc]) Kc = -1;                // a cell of the block that is not a target
-  double x0[2], x1[2];
+  const double ccx = bstat[8 * P], ccy = bstat[8 * P + 1];   // the target block's centre
+  double x0[2], x1[2], xx[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    x0[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 0] : 1e100;
-    x1[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 1] : 1e100;
+    x0[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 0] - ccx : -1e100;
+    x1[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 1] - ccy : -1e100;
+    xx[t] = fma(x1[t], x1[t], x0[t] * x0[t]);
   }
   int ntv = 0;                       // target cells of the block (evaluation count)
   if (tid == 0)
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
         const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + TU - 1) / TU * TU;
         if (c0 > 0 || ks != kset) __syncthreads();
         for (int idx = tid; idx < nwp; idx += TT) {
-          double2 y = make_double2(1e100, 1e100);
+          double2 y = make_double2(1e100, 1e100);   // padding: far away, weight 0
           double w = 0.0;
           if (idx < nw) {
             const int c = c0 + idx / kk, r = idx - (idx / kk) * kk;
@@ -247,8 +256,9 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
               w = g[6] * R[3 * r + 2];
             }
           }
-          sY[idx] = y;
-          sW[idx] = w;
+          const double yx = y.x - ccx, yy = y.y - ccy;
+          sM[idx] = make_double2(-2.0 * yx, -2.0 * yy);
+          sQ[idx] = make_double2(fma(yy, yy, yx * yx), w);
         }
         if (tid == 0) {
           int nvs = 0;
@@ -257,8 +267,8 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
         }
         __syncthreads();
         if (!wact) continue;
-        if (kq > 0) sweep<E4, false>(sY, sW, nwp, x0, x1, 1.0, ex, acc);
-        else sweep<E4, true>(sY, sW, nwp, x0, x1, wsel, ex, acc);
+        if (kq > 0) sweep<E4, false>(sM, sQ, nwp, x0, x1, xx, 1.0, ex, acc);
+        else sweep<E4, true>(sM, sQ, nwp, x0, x1, xx, wsel, ex, acc);
       }
     }
   }
@@ -288,7 +298,7 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
                           cudaEvent_t e0, cudaEvent_t e1) {
   if (ntargets <= 0) return;
   const int nb = B.nb;
-  const size_t smem = (size_t)TWIN * 24 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
+  const size_t smem = (size_t)TWIN * 32 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
   if (m.d != 2 || m.q != TQN || smem > 200 * 1024) {      // out of this path's shape: pair by pair
     launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st);
     return;
@@ -320,7 +330,7 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
   FL_E4_SWITCH_T(e4, {
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, tcell.p, B.bcells.p,
-                                                  kcell.p, nb, psi,
+                                                  kcell.p, B.bstat.p, nb, psi,
                                                   evals_block ? evals_block : evals),
         note_launch();
   });

@@ -13,9 +13,14 @@ def main():
     ap.add_argument("config", default="c5", nargs="?")
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--hist", action="store_true", help="also print the cross / tail order histograms")
+    ap.add_argument("--square", type=int, default=0, help="unit square N x N (SW-NE) instead of a config")
+    ap.add_argument("--s", type=float, default=0.5)
     a = ap.parse_args()
     from paper_1708_03912_b200 import mesh as M, assembly as A, _lib
-    mesh, s = M.baseline_mesh(a.config)
+    if a.square:
+        mesh, s = M.build_unit_square_mesh(a.square), a.s
+    else:
+        mesh, s = M.baseline_mesh(a.config)
     dm = M.DofMap(mesh, s)
     ker = A.FractionalKernel(mesh.d, s)
     st = None
