@@ -628,7 +628,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
         if (x) cudaEventDestroy(x);
     }
   } tbev;
-  if (d == 2) build_blocks2d(m, (int)row_begin, (int)row_end, blocks, st);
+  if (d == 2) build_blocks2d(m, U.t, (int)row_begin, (int)row_end, blocks, st);
   if (!early_tail) {
     tm.mark();  // 2
     // tail at the nodes of the target cells (banded 1D: per band, below)

@@ -825,6 +825,19 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
   if (tid == 0 && S.evals && a.evals) atomicAdd(a.evals, S.evals);
 }
 
+__global__ void pair_morton_kernel(const int4* __restrict__ pr, int n, unsigned* __restrict__ key,
+                                   int* __restrict__ idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = spread16b((uint32_t)pr[i].x) | (spread16b((uint32_t)pr[i].y) << 1);
+  idx[i] = i;
+}
+__global__ void gather_int4_kernel(const int4* __restrict__ src, const int* __restrict__ idx, int n,
+                                   int4* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
 __global__ void uni_flag_kernel(const int4* __restrict__ all, int n, const int* __restrict__ bndof,
                                 int4* __restrict__ allw, int* __restrict__ uf, int* __restrict__ rf) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -873,7 +886,8 @@ __global__ void fixed_to_double_kernel(unsigned long long* A, int64_t count, dou
 // overwritten (zeroed first).  Near pairs (k >= KW2D) are discovered here and computed once by
 // near_pairs_build into `near`.  t_disc / t_near: events recorded after discovery and after the
 // near blocks (phase timing).
-void build_blocks2d(const DevMesh& m, int row_begin, int row_end, Blocks2D& B, cudaStream_t st) {
+void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row_end, Blocks2D& B,
+                    cudaStream_t st) {
   const int nc = m.nc;
   const int nb = (nc + CB - 1) / CB;
   B.nb = nb;
@@ -903,6 +917,17 @@ void build_blocks2d(const DevMesh& m, int row_begin, int row_end, Blocks2D& B, c
   block_build_kernel<<<nb, 128, 0, st>>>(m, vals2.p, nb, row_begin, row_end, B.bcells.p, B.bdofs.p, B.bndof.p,
                                          B.slot.p, B.bstat.p, B.rowflag.p, B.err.p), note_launch();
   block_of_kernel<<<(nc + 255) / 256, 256, 0, st>>>(vals2.p, nc, B.blk_of.p), note_launch();
+  // mapped nodes of the orders 2, 3, 4: per cell (cross2d_kernel) and block-ordered node-major with
+  // J and the vertex slots (cross2d_uni_kernel, tail2d_block_kernel)
+  const RuleRef r2 = t.rule(T_DISJ, 2), r3 = t.rule(T_DISJ, 3), r4 = t.rule(T_DISJ, 4);
+  if (r2.cnt != 4 || r3.cnt != 9 || r4.cnt != 16) throw Error(-3, "disjoint rules k = 2, 3, 4 missing");
+  B.nodes.alloc((size_t)nc * NPRE2);
+  cell_nodes2_kernel<<<(unsigned)(((int64_t)nc * NPRE2 + 255) / 256), 256, 0, st>>>(m, t.data, r2, r3, r4, B.nodes.p),
+      note_launch();
+  B.un.alloc((size_t)nb * UNODES); B.uj.alloc((size_t)nb * CB); B.us.alloc((size_t)nb * CB);
+  block_unodes_kernel<<<(unsigned)(((int64_t)nb * UNODES + 255) / 256), 256, 0, st>>>(B.bcells.p, B.nodes.p, nb, m,
+                                                                                    B.slot.p, B.un.p, B.uj.p, B.us.p),
+      note_launch();
   FL_CHECK_LAUNCH();
 }
 
@@ -922,10 +947,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   const DBuf<double>& bstat = B.bstat;
   // ---- mapped nodes, rule weights, scale bound
   const RuleRef r2 = t.rule(T_DISJ, 2), r3 = t.rule(T_DISJ, 3), r4 = t.rule(T_DISJ, 4);
-  if (r2.cnt != 4 || r3.cnt != 9 || r4.cnt != 16) throw Error(-3, "disjoint rules k = 2, 3, 4 missing");
-  DBuf<double2> nodes((size_t)nc * NPRE2);
-  cell_nodes2_kernel<<<(unsigned)(((int64_t)nc * NPRE2 + 255) / 256), 256, 0, st>>>(m, t.data, r2, r3, r4, nodes.p),
-      note_launch();
+  const DBuf<double2>& nodes = B.nodes;
   std::vector<double> hw(NPRE2 * 3), hrow(NODE);
   for (int x = 0; x < NPRE2; ++x) {
     const RuleRef rr = x < 4 ? r2 : (x < 13 ? r3 : r4);
@@ -1017,15 +1039,29 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   }
   const int nuni = hu[0], nrest = hu[1];
   const int4* rest = (nall > 0 && !uni_off) ? rlist.p : all.p;
-  DBuf<double2> un;
-  DBuf<double> uj;
-  DBuf<int> us;
-  if (nuni > 0) {
-    un.alloc((size_t)nb * UNODES); uj.alloc((size_t)nb * CB); us.alloc((size_t)nb * CB);
-    block_unodes_kernel<<<(unsigned)(((int64_t)nb * UNODES + 255) / 256), 256, 0, st>>>(bcells.p, nodes.p, nb, m,
-                                                                                      slot.p, un.p, uj.p, us.p),
-        note_launch();
+  // the uniform pairs in 2D Morton order of (P, Q): CTAs working at the same time touch a compact
+  // region of A, so the integer atomics of neighbouring block pairs meet in L2 instead of DRAM
+  static const bool uni_heavy = [] {          // FRACLAP_CROSS2D_UNI_ORDER=heavy: keep the heavy-first order
+    const char* v = getenv("FRACLAP_CROSS2D_UNI_ORDER");
+    return v && std::string(v) == "heavy";
+  }();
+  DBuf<int4> ulist2;
+  const int4* uorder = ulist.p;
+  if (nuni > 1 && !uni_heavy) {
+    DBuf<unsigned> mk(nuni), mk2(nuni);
+    DBuf<int> mi(nuni), mi2(nuni);
+    pair_morton_kernel<<<(nuni + 255) / 256, 256, 0, st>>>(ulist.p, nuni, mk.p, mi.p), note_launch();
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, mk.p, mk2.p, mi.p, mi2.p, nuni, 0, 32, st);
+    DBuf<unsigned char> tb(tmp);
+    FL_CUDA(cub::DeviceRadixSort::SortPairs(tb.p, tmp, mk.p, mk2.p, mi.p, mi2.p, nuni, 0, 32, st));
+    ulist2.alloc(nuni);
+    gather_int4_kernel<<<(nuni + 255) / 256, 256, 0, st>>>(ulist.p, mi2.p, nuni, ulist2.p), note_launch();
+    uorder = ulist2.p;
   }
+  const DBuf<double2>& un = B.un;
+  const DBuf<double>& uj = B.uj;
+  const DBuf<int>& us = B.us;
   info.block_pairs = nall;
   info.near_block_pairs = nnear;
   // ---- A (int64 view) zeroed
@@ -1079,7 +1115,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   xa.nearH = near.hkey.p; xa.nearI = near.hidx.p; xa.hmask = near.hmask; xa.nearG = near.G.p;
   if (nuni > 0) {
     UArgs ua{};
-    ua.bpairs = ulist.p; ua.nbp = nuni; ua.un = un.p; ua.uj = uj.p; ua.us = us.p; ua.bdofs = bdofs.p;
+    ua.bpairs = uorder; ua.nbp = nuni; ua.un = un.p; ua.uj = uj.p; ua.us = us.p; ua.bdofs = bdofs.p;
     ua.ex = ex; ua.cs = xa.cs; ua.lim = xa.lim; ua.limq = (long long)xa.lim; ua.A = Ai; ua.lda = lda; ua.r0 = row_begin; ua.r1 = row_end;
     ua.evals = evals; ua.ovf = ovf.p;
     const size_t usm = sizeof(UShared);

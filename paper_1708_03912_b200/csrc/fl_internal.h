@@ -250,8 +250,14 @@ struct Blocks2D {
   DBuf<int> bcells, bdofs, bndof, rowflag, err, blk_of;
   DBuf<signed char> slot;
   DBuf<double> bstat;
+  // mapped nodes of the orders 2, 3, 4: per cell (29 each), and per block node-major
+  // (un[b][seg(k) + r * 32 + c], seg = 0 / 128 / 416, 928 per block) with J and packed vertex slots
+  DBuf<double2> nodes, un;
+  DBuf<double> uj;
+  DBuf<int> us;
 };
-void build_blocks2d(const DevMesh& m, int row_begin, int row_end, Blocks2D& B, cudaStream_t st);
+constexpr int UNODES2D = 928;
+void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row_end, Blocks2D& B, cudaStream_t st);
 void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                       const Blocks2D& B, int row_begin, int row_end, double* A, int64_t lda,
                       unsigned long long* evals, NearPairs& near, Cross2DInfo& info, cudaEvent_t t_disc,

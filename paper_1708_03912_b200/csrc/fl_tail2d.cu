@@ -28,8 +28,8 @@ constexpr int TQN = 16;            // target nodes per cell (XQ_ORDER 4 in 2D, a
 constexpr int TT = 256;            // threads per CTA: 2 target nodes each
 constexpr int TWIN = 1024;         // source nodes per shared-memory window
 constexpr int TU = 4;              // source nodes per thread per step
-constexpr int KC = 9;              // 2D disjoint order cap (quadrature.py:171-175)
 constexpr int RULE_NODES = 284;    // sum_{k=2}^{9} k^2
+__host__ __device__ constexpr int useg(int k) { return k == 2 ? 0 : (k == 3 ? 128 : 416); }   // Blocks2D::un
 __host__ __device__ constexpr int roff(int k) { return (k - 1) * k * (2 * k - 1) / 6 - 1; }   // sum_{j=2}^{k-1} j^2
 
 __global__ void tail_flag_kernel(const int* __restrict__ targets, int ntargets, const int* __restrict__ blk_of,
@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
                                                             const int* __restrict__ tcell,
                                                             const int* __restrict__ bcells,
                                                             const int8_t* __restrict__ kcell,
-                                                            const double* __restrict__ bstat, int nb,
+                                                            const double* __restrict__ bstat,
+                                                            const double2* __restrict__ un,
+                                                            const double* __restrict__ uj, int nb,
                                                             double* __restrict__ psi,
                                                             unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -207,16 +209,70 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   const bool Kw_t = Kw >= 0 && tcell[Kw];
   double acc[2][2] = {};
   unsigned long long nev = 0;
-  double gpre = nq > 0 ? geo_field(m, bcells, sL[0] & 0xffffff, tid) : 0.0;
   bool missing = false;
+  // fast path: uniform order k <= 4, the whole block's 32 k^2 nodes in one half of the window
+  // (node-major from the block-ordered staging array un / uj), software-pipelined: the next fast
+  // block's nodes are loaded into registers before the sweep of the current one and written to the
+  // other half after it — one barrier per source block
+  auto kof = [&](int qi) { return (int)(int8_t)(sL[qi] >> 24); };
+  auto is_fast = [&](int qi) { return qi < nq && kof(qi) >= 2 && kof(qi) <= 4; };
+  double2 py[2];
+  double pj[2];
+  auto prefetch = [&](int qi) {
+    const int Q = sL[qi] & 0xffffff, k = kof(qi), nn = TB * k * k;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int idx = tid + TT * t;
+      if (idx < nn) {
+        py[t] = un[(size_t)Q * UNODES2D + useg(k) + idx];
+        pj[t] = uj[(size_t)Q * TB + (idx & (TB - 1))];
+      }
+    }
+  };
+  auto put_nodes = [&](int qi, int half) {
+    const int k = kof(qi), kk = k * k, nn = TB * kk;
+    const double* R = sR + 3 * roff(k);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int idx = tid + TT * t;
+      if (idx < nn) {
+        const bool ok = pj[t] != 0.0;            // an empty slot of a partial block: far, weight 0
+        const double yx = (ok ? py[t].x : 1e100) - ccx, yy = (ok ? py[t].y : 1e100) - ccy;
+        sM[half * (TWIN / 2) + idx] = make_double2(-2.0 * yx, -2.0 * yy);
+        sQ[half * (TWIN / 2) + idx] = make_double2(fma(yy, yy, yx * yx), pj[t] * R[3 * (idx >> 5) + 2]);
+      }
+    }
+    if (wid == 0) {                              // evaluation count: valid source cells (lanes = row 0)
+      const int nvs = __popc(__ballot_sync(0xffffffffu, pj[0] != 0.0));
+      if (lane == 0) nev += (unsigned long long)nvs * kk * ntv * TQN;
+    }
+    if (tid == 0 && dir.rule(T_DISJ, k).cnt != kk) missing = true;
+  };
+  int half = 0;
+  bool staged = false;
   for (int qi = 0; qi < nq; ++qi) {
     const int Q = sL[qi] & 0xffffff;
-    const int kq = (int)(int8_t)(sL[qi] >> 24);   // > 0: uniform, -1: per target cell
-    __syncthreads();                 // the previous block's windows are consumed
-    sG[tid] = gpre;
+    const int kq = kof(qi);          // > 0: uniform, -1: per target cell
+    if (is_fast(qi)) {
+      if (!staged) {
+        prefetch(qi);
+        put_nodes(qi, half);
+        __syncthreads();
+      }
+      const bool nf = is_fast(qi + 1);
+      if (nf) prefetch(qi + 1);      // in flight during the sweep
+      sweep<E4, false>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * kq * kq, x0, x1, xx, 1.0, ex, acc);
+      if (nf) put_nodes(qi + 1, half ^ 1);
+      __syncthreads();
+      staged = nf;
+      if (nf) half ^= 1;
+      continue;
+    }
+    staged = false;
+    // general path: order >= 5 (windows) or per-target-cell orders; geometry through sG
+    sG[tid] = geo_field(m, bcells, Q, tid);
     if (kq < 0 && tid < TB) s_kc[tid] = Kw_t ? (int)kcell[(size_t)Kw * nb + Q] : 0;
     __syncthreads();
-    if (qi + 1 < nq) gpre = geo_field(m, bcells, sL[qi + 1] & 0xffffff, tid);   // in flight meanwhile
     unsigned kset;                   // bit k: some target cell takes order k from this block here
     if (kq > 0) {
       kset = 1u << kq;
@@ -271,6 +327,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
         else sweep<E4, true>(sM, sQ, nwp, x0, x1, xx, wsel, ex, acc);
       }
     }
+    __syncthreads();                 // the window is consumed before the next block reuses it
   }
   if (Kc >= 0) {
 #pragma unroll
@@ -330,7 +387,7 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
   FL_E4_SWITCH_T(e4, {
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, tcell.p, B.bcells.p,
-                                                  kcell.p, B.bstat.p, nb, psi,
+                                                  kcell.p, B.bstat.p, B.un.p, B.uj.p, nb, psi,
                                                   evals_block ? evals_block : evals),
         note_launch();
   });
