@@ -547,7 +547,19 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     const char* v = getenv("FRACLAP_TAIL_CONCURRENT");
     return !v || atoi(v) != 0;
   }();
-  TailStream tstream(device, (early_tail && tail_concurrent) || nbands > 0);
+  static const bool tail2d_warp = [] {        // FRACLAP_TAIL2D=warp: round-1 warp-per-target tail only
+    const char* v = getenv("FRACLAP_TAIL2D");
+    return v && std::string(v) == "warp";
+  }();
+  // 1D: the tail on its own stream beside the cross tiles.  2D: FRACLAP_TAIL2D_STREAM=1 puts the
+  // block-pair tail beside the cross term (measured: no gain at c5 — the block scheduler drains the
+  // tail's CTAs first — and the phase timings then overlap), default off
+  static const bool tail2d_stream = [] {
+    const char* v = getenv("FRACLAP_TAIL2D_STREAM");
+    return v && atoi(v) != 0;
+  }();
+  TailStream tstream(device, ((early_tail || (d == 2 && !tail2d_warp && tail2d_stream)) && tail_concurrent) ||
+                                 nbands > 0);
   if (nbands) {
     // banded: the first band's tail runs while the host waits for the sizes (the band's copy
     // cannot start before it); the other bands' tails follow in the band loop
@@ -615,10 +627,6 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   launch_singular_touching(m, U.t, ex, e4, tpairs.p, npairs, tloc.p, st);
   if (do_bnd) launch_singular_boundary(m, U.t, ex, e4, bitems.p, nitems, bloc.p, st);
   // 2D: the Morton cell blocks shared by the tail and the cross term
-  static const bool tail2d_warp = [] {        // FRACLAP_TAIL2D=warp: round-1 warp-per-target tail only
-    const char* v = getenv("FRACLAP_TAIL2D");
-    return v && std::string(v) == "warp";
-  }();
   Blocks2D blocks;
   struct EvPair {                      // events around the 2D block-pair tail kernel
     cudaEvent_t e[2] = {nullptr, nullptr};
@@ -636,8 +644,19 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     else if (d == 2) {
       cudaEventCreate(&tbev[0]);
       cudaEventCreate(&tbev[1]);
-      launch_tail2d_blocks(m, U.t, oc, ex, e4, blocks, targets.p, ntargets, psi.p, evc.p, st, evc.p + 2, tbev[0],
-                           tbev[1]);
+      cudaStream_t ts = st;
+      if (tstream.s) {                  // joined before the cell-local matrices (psi complete)
+        FL_CUDA(cudaEventRecord(tstream.e[0], st));
+        FL_CUDA(cudaStreamWaitEvent(tstream.s, tstream.e[0], 0));
+        FL_CUDA(cudaEventRecord(tstream.e[1], tstream.s));
+        ts = tstream.s;
+      }
+      {
+        StreamScope sc(ts);             // the tail's temporaries are freed in its own stream order
+        launch_tail2d_blocks(m, U.t, oc, ex, e4, blocks, targets.p, ntargets, psi.p, evc.p, ts, evc.p + 2, tbev[0],
+                             tbev[1]);
+      }
+      if (tstream.s) FL_CUDA(cudaEventRecord(tstream.e[2], tstream.s));
     }
     else if (!nbands) launch_tail1d(m, U.t, oc, ex, e4, P1.get(), targets.p, nsel.p, m.nc, psi.p, evc.p, st);
   }

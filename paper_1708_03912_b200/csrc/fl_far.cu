@@ -41,7 +41,9 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
                                                                   const int8_t* __restrict__ kuni,
                                                                   const int* __restrict__ blk_of,
                                                                   const int* __restrict__ bcells, int nb,
-                                                                  const int8_t* __restrict__ kcell) {
+                                                                  const int8_t* __restrict__ kcell,
+                                                                  const unsigned long long* __restrict__ psifx,
+                                                                  double fxinv) {
   constexpr int Q = (D == 1) ? 6 : 16;     // cell quadrature nodes (XQ_ORDER)
   constexpr int L = Q / TAIL_T;            // lanes per group (8 in 2D, 3 in 1D)
   constexpr int G = 32 / L;                // groups sweeping disjoint source nodes (4 / 10)
@@ -191,7 +193,11 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
     double tot = a;
 #pragma unroll
     for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, a, (lane + gg * L) & 31);
-    if (lane < L) psi[(size_t)K * Q + j + t * L] = kuni ? psi[(size_t)K * Q + j + t * L] + tot : tot;
+    // kuni: the block kernel's sums (double part, then the sym4 fixed-point part) plus ours
+    if (lane < L)
+      psi[(size_t)K * Q + j + t * L] =
+          kuni ? (psi[(size_t)K * Q + j + t * L] + (psifx ? (double)(long long)psifx[(size_t)K * Q + j + t * L] * fxinv : 0.0)) + tot
+               : tot;
   }
   if (lane == 0 && evals) atomicAdd(evals, nodes * Q);
 }
@@ -938,13 +944,14 @@ __global__ void orders_kernel(DevMesh m, OrderConsts oc, int8_t* cross_k, int8_t
 
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                  const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st,
-                 const int8_t* kuni, const int* blk_of, const int* bcells, int nb, const int8_t* kcell) {
+                 const int8_t* kuni, const int* blk_of, const int* bcells, int nb, const int8_t* kcell,
+                 const unsigned long long* psifx, double fxinv) {
   if (ntargets <= 0) return;
   const int grid = (ntargets + TAIL_WARPS - 1) / TAIL_WARPS;
   if (m.d == 1) {
-    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, nullptr, nullptr, nullptr, 0, nullptr), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, kcell), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, kcell, psifx, fxinv), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }

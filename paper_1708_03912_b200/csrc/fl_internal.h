@@ -197,7 +197,8 @@ void launch_singular_boundary(const DevMesh& m, const DevTables& t, double ex, i
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                  const int* targets, int ntargets, double* psi /*nc*q*/, unsigned long long* evals,
                  cudaStream_t st, const int8_t* kuni = nullptr, const int* blk_of = nullptr,
-                 const int* bcells = nullptr, int nb = 0, const int8_t* kcell = nullptr);
+                 const int* bcells = nullptr, int nb = 0, const int8_t* kcell = nullptr,
+                 const unsigned long long* psifx = nullptr, double fxinv = 0.0);
 void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const int* targets,
                  int ntargets, double* win /*nc*q*/, cudaStream_t st);
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,

@@ -17,6 +17,8 @@
 // pair by cell pair by fl_far.cu's warp-per-target tail_kernel, which adds its sums to these.
 // Deterministic: every target node sums its sources in a fixed order (Q ascending, then the
 // block's nodes), independent of how the rows are split over GPUs.
+#include <cstring>
+
 #include "fl_internal.h"
 
 namespace fl {
@@ -45,29 +47,51 @@ __global__ void tail_flag_kernel(const int* __restrict__ targets, int ntargets, 
 // when the bounds of the boosted order formula agree; -1 when the blocks are disjoint but the
 // orders are not uniform (then decided per target cell, cell_block_korder); 0 otherwise
 __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, const int* __restrict__ tflag, int nb,
-                                 int mixed, int8_t* __restrict__ kuni) {
+                                 int mixed, int8_t* __restrict__ kuni, unsigned long long* __restrict__ dmin4,
+                                 int* __restrict__ run) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)nb * nb) return;
   const int P = (int)(i / nb), Q = (int)(i - (int64_t)P * nb);
   int k = 0;
-  if (tflag[P] && P != Q) {
+  // every row (not only the target blocks'): the sym4 split must not depend on the row range
+  if (P != Q) {
     const double* a = bs + 8 * P;
     const double* b = bs + 8 * Q;
     const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
     const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
     const double Dmax = (dc + a[2] + b[2]) * (1.0 + 1e-12);
-    // disjoint bounding circles (no pair touches), at least the target block's radius apart: the
-    // centred r2 expansion of the block kernel then loses at most a factor 9 of relative accuracy
-    if (Dmin > 0.0 && Dmin >= a[2]) {
+    // disjoint bounding circles (no pair touches), at least either block's radius apart: the
+    // centred r2 expansion of the block kernel then loses at most a factor 9 of relative accuracy;
+    // every operation is symmetric in (P, Q), so kuni[P][Q] == kuni[Q][P] bitwise
+    if (Dmin > 0.0 && Dmin >= fmax(a[2], b[2])) {
       const double hmn = fmin(a[3], b[3]), hmx = fmax(a[4], b[4]), lmn = fmin(a[5], b[5]), lmx = fmax(a[6], b[6]);
       const double hi = order_bound_hi(oc, oc.coff_tail, Dmin, hmn, hmx, lmn, lmx);
       const double lo = order_bound_lo(oc, oc.coff_tail, Dmin, Dmax, hmn, hmx, lmn, lmx);
       const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
       const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
       k = c0 == c1 ? (int)c0 : (mixed ? -1 : 0);  // -1: per target cell (cell_block_korder)
+      if (k == 4) {
+        atomicMin(dmin4, (unsigned long long)__double_as_longlong(Dmin));
+        if (Q > P && tflag[Q]) run[P] = 1;   // P's CTA evaluates (P, Q) for target block Q
+      }
     }
   }
   kuni[i] = (int8_t)k;
+}
+
+__global__ void jmax_kernel(DevMesh m, unsigned long long* __restrict__ jmax) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < m.nc) atomicMax(jmax, (unsigned long long)__double_as_longlong(m.geo[c].J));
+}
+
+// sym4: an order-4 uniform block pair (P, Q) is evaluated once, by the CTA of min(P, Q); its
+// kernel values serve both directions, because the order-4 source rule is the 16-node target rule
+// itself (simplex_rule(2, 4) == XQ, assembly.py:635, :1012).  The split depends on the mesh only,
+// not on the row range, so row blocks stay bitwise the whole matrix's rows: a block that holds no
+// target still runs (as a helper) when it is the smaller block of an order-4 pair with a target block.
+__device__ __forceinline__ int sym4_mode(int T, int S, int k) {
+  if (k != 4) return 0;                // 0: ordinary source block
+  return S > T ? 1 : -1;               // 1: this CTA takes both directions; -1: S's CTA does
 }
 
 // per target cell K and mixed source block Q (kuni == -1): K's own order for the block, or 0
@@ -128,17 +152,60 @@ __device__ __forceinline__ void sweep(const double2* __restrict__ sM, const doub
   }
 }
 
+// sym4 sweep: also the column sums sum_t w_t v(t, y) of every source node y over the warp's 64
+// targets (two per lane), reduced across the warp with a 4-value butterfly (lanes 0/8/16/24 end up
+// with the four columns of a step) and stored per warp in colw[y]
+template <int E4>
+__device__ __forceinline__ void sweep_sym(const double2* __restrict__ sM, const double2* __restrict__ sQ, int nwp,
+                                          const double (&x0)[2], const double (&x1)[2], const double (&xx)[2],
+                                          const double (&wt)[2], double ex, double (&acc)[2][2],
+                                          double* __restrict__ colw, int lane) {
+#pragma unroll 1
+  for (int p = 0; p < nwp; p += TU) {
+    double2 my[TU], qw[TU];
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      my[u] = sM[p + u];
+      qw[u] = sQ[p + u];
+    }
+    double c[TU];
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      double cu = 0.0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const double v = kpow<E4>(fma(x0[t], my[u].x, fma(x1[t], my[u].y, xx[t] + qw[u].x)), ex);
+        acc[t][u & 1] = fma(qw[u].y, v, acc[t][u & 1]);
+        cu = fma(wt[t], v, cu);
+      }
+      c[u] = cu;
+    }
+    const bool h16 = lane & 16, h8 = lane & 8;
+    double k0 = h16 ? c[2] : c[0], k1 = h16 ? c[3] : c[1];
+    k0 += __shfl_xor_sync(0xffffffffu, h16 ? c[0] : c[2], 16);
+    k1 += __shfl_xor_sync(0xffffffffu, h16 ? c[1] : c[3], 16);
+    double kk = h8 ? k1 : k0;
+    kk += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 4);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 2);
+    kk += __shfl_xor_sync(0xffffffffu, kk, 1);
+    if ((lane & 7) == 0) colw[p + (lane >> 3)] = kk;   // lane 0: column p, 8: p + 1, 16: p + 2, 24: p + 3
+  }
+}
+
 template <int E4>
 __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
                                                             OrderConsts oc, double ex,
                                                             const int8_t* __restrict__ kuni,
                                                             const int* __restrict__ tflag,
+                                                            const int* __restrict__ run,
                                                             const int* __restrict__ tcell,
                                                             const int* __restrict__ bcells,
                                                             const int8_t* __restrict__ kcell,
                                                             const double* __restrict__ bstat,
                                                             const double2* __restrict__ un,
                                                             const double* __restrict__ uj, int nb,
+                                                            unsigned long long* __restrict__ psifx, double fxscale,
                                                             double* __restrict__ psi,
                                                             unsigned long long* __restrict__ evals) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -146,12 +213,14 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   double2* sQ = sM + TWIN;                                     // TWIN: |y'|^2, J * w
   double* sR = reinterpret_cast<double*>(sQ + TWIN);           // RULE_NODES x (u0, u1, w)
   double* sG = sR + 3 * RULE_NODES;                            // TB x 8 geometry fields
-  int* sL = reinterpret_cast<int*>(sG + 8 * TB);               // source blocks: Q | (k & 0xff) << 24
+  double* colbuf = sG + 8 * TB;                                // [8 warps][512] sym4 column partials
+  int* sL = reinterpret_cast<int*>(colbuf + (TT / 32) * (TWIN / 2));   // source blocks: Q | (k & 0xff) << 24
   __shared__ int s_wsum[TT / 32];
   __shared__ int s_nq;
   __shared__ int s_kc[TB];                                     // per target cell order (mixed blocks)
   const int P = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (!tflag[P]) return;
+  if (!run[P]) return;
+  const bool helper = !tflag[P];       // no target here: only the order-4 pairs with target blocks
   // ---- the disjoint rules k = 2..9 (reference nodes and weights)
   for (int i = tid; i < RULE_NODES; i += TT) {
     int k = 2;
@@ -171,7 +240,9 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   __syncthreads();
   for (int base = 0; base < nb; base += TT) {
     const int Q = base + tid;
-    const int k = Q < nb ? (int)krow[Q] : 0;
+    int k = Q < nb ? (int)krow[Q] : 0;
+    if (k && sym4_mode(P, Q, k) < 0) k = 0;          // (Q, P) evaluated by Q's CTA for both
+    if (k && helper && !(sym4_mode(P, Q, k) > 0 && tflag[Q])) k = 0;
     const unsigned bal = __ballot_sync(0xffffffffu, k != 0);
     if (lane == 0) s_wsum[wid] = __popc(bal);
     __syncthreads();
@@ -189,21 +260,26 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   const int nq = s_nq;
   // ---- the thread's two target nodes: cell tid / 8, nodes tid % 8 and tid % 8 + 8
   const int cme = tid >> 3, q0 = tid & 7;
-  int Kc = bcells[P * TB + cme];
-  if (Kc >= 0 && !tcell[Kc]) Kc = -1;                // a cell of the block that is not a target
+  const int Kv = bcells[P * TB + cme];               // the cell (-1: an empty slot of a partial block)
+  const int Kc = Kv >= 0 && tcell[Kv] ? Kv : -1;     // ... if its psi is wanted (a target)
   const double ccx = bstat[8 * P], ccy = bstat[8 * P + 1];   // the target block's centre
   double x0[2], x1[2], xx[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    x0[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 0] - ccx : -1e100;
-    x1[t] = Kc >= 0 ? m.X[((size_t)Kc * TQN + q0 + 8 * t) * 2 + 1] - ccy : -1e100;
+    // every cell's nodes, targets or not: they are also the sources of the sym4 column sums
+    x0[t] = Kv >= 0 ? m.X[((size_t)Kv * TQN + q0 + 8 * t) * 2 + 0] - ccx : -1e100;
+    x1[t] = Kv >= 0 ? m.X[((size_t)Kv * TQN + q0 + 8 * t) * 2 + 1] - ccy : -1e100;
     xx[t] = fma(x1[t], x1[t], x0[t] * x0[t]);
   }
-  int ntv = 0;                       // target cells of the block (evaluation count)
+  double wt[2];                      // J_K w_q of the thread's targets (sym4 column sums; 0: no target)
+#pragma unroll
+  for (int t = 0; t < 2; ++t) wt[t] = Kv >= 0 ? m.geo[Kv].J * sR[3 * (roff(4) + q0 + 8 * t) + 2] : 0.0;
+  int ntv = 0, nvp = 0;              // target cells / cells of the block (evaluation counts)
   if (tid == 0)
     for (int c = 0; c < TB; ++c) {
       const int K = bcells[P * TB + c];
       ntv += K >= 0 && tcell[K];
+      nvp += K >= 0;
     }
   const int Kw = tid < TB ? bcells[P * TB + tid] : -1;     // thread c < 32: target cell c (orders)
   const bool Kw_t = Kw >= 0 && tcell[Kw];
@@ -244,7 +320,9 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     }
     if (wid == 0) {                              // evaluation count: valid source cells (lanes = row 0)
       const int nvs = __popc(__ballot_sync(0xffffffffu, pj[0] != 0.0));
-      if (lane == 0) nev += (unsigned long long)nvs * kk * ntv * TQN;
+      // sym4: every cell of the block is swept (its nodes are the sources of the column sums)
+      const int ntt = sym4_mode(P, sL[qi] & 0xffffff, k) > 0 ? nvp : ntv;
+      if (lane == 0) nev += (unsigned long long)nvs * kk * ntt * TQN;
     }
     if (tid == 0 && dir.rule(T_DISJ, k).cnt != kk) missing = true;
   };
@@ -261,9 +339,28 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
       }
       const bool nf = is_fast(qi + 1);
       if (nf) prefetch(qi + 1);      // in flight during the sweep
-      sweep<E4, false>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * kq * kq, x0, x1, xx, 1.0, ex, acc);
+      const bool sym = sym4_mode(P, Q, kq) > 0;
+      if (sym)
+        sweep_sym<E4>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * 16, x0, x1, xx, wt, ex, acc,
+                      colbuf + wid * (TWIN / 2), lane);
+      else
+        sweep<E4, false>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * kq * kq, x0, x1, xx, 1.0, ex, acc);
       if (nf) put_nodes(qi + 1, half ^ 1);
       __syncthreads();
+      if (sym) {
+        // Q's target nodes: node r of cell c (node-major idx = 32 r + c) is Q's XQ node r; the 8
+        // warps' partials summed in a fixed order, added to Q's psi in exact fixed point
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int idx = tid + TT * t, c = idx & (TB - 1), r = idx >> 5;
+          double v = 0.0;
+#pragma unroll
+          for (int w = 0; w < TT / 32; ++w) v += colbuf[w * (TWIN / 2) + idx];
+          const int Kq = bcells[Q * TB + c];
+          if (Kq >= 0) atomicAdd(psifx + (size_t)Kq * TQN + r, (unsigned long long)__double2ll_rn(v * fxscale));
+        }
+        __syncthreads();               // colbuf consumed
+      }
       staged = nf;
       if (nf) half ^= 1;
       continue;
@@ -355,7 +452,7 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
                           cudaEvent_t e0, cudaEvent_t e1) {
   if (ntargets <= 0) return;
   const int nb = B.nb;
-  const size_t smem = (size_t)TWIN * 32 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
+  const size_t smem = (size_t)TWIN * 32 + (size_t)(TT / 32) * (TWIN / 2) * 8 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
   if (m.d != 2 || m.q != TQN || smem > 200 * 1024) {      // out of this path's shape: pair by pair
     launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st);
     return;
@@ -365,6 +462,8 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
   FL_CUDA(cudaMemsetAsync(tcell.p, 0, (size_t)m.nc * sizeof(int), st));
   tail_flag_kernel<<<(ntargets + 255) / 256, 256, 0, st>>>(targets, ntargets, B.blk_of.p, tflag.p, tcell.p),
       note_launch();
+  DBuf<int> run(nb);                   // CTAs that run: target blocks and sym4 helpers
+  FL_CUDA(cudaMemcpyAsync(run.p, tflag.p, (size_t)nb * sizeof(int), cudaMemcpyDeviceToDevice, st));
   DBuf<int8_t> kuni((size_t)nb * nb);
   const int64_t nn = (int64_t)nb * nb;
   // FRACLAP_TAIL2D_MIXED=1: disjoint non-uniform block pairs split per target cell (measured slower
@@ -373,8 +472,35 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
     const char* v = getenv("FRACLAP_TAIL2D_MIXED");
     return v && std::string(v) == "1";
   }();
-  tail_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, B.bstat.p, tflag.p, nb, mixed ? 1 : 0, kuni.p),
+  // smallest block distance of the order-4 uniform pairs and the largest Jacobian: the bound of the
+  // sym4 column sums that sets the fixed-point scale of psifx
+  DBuf<unsigned long long> red(2);
+  {
+    const double big = 1e300;
+    unsigned long long init[2] = {0ull, 0ull};
+    std::memcpy(&init[0], &big, 8);
+    FL_CUDA(cudaMemcpyAsync(red.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  }
+  tail_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, B.bstat.p, tflag.p, nb, mixed ? 1 : 0, kuni.p,
+                                                                 red.p, run.p),
       note_launch();
+  jmax_kernel<<<(m.nc + 255) / 256, 256, 0, st>>>(m, red.p + 1), note_launch();
+  unsigned long long hred[2];
+  FL_CUDA(cudaMemcpyAsync(hred, red.p, sizeof(hred), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  double dmin4, jmax;
+  std::memcpy(&dmin4, &hred[0], 8);
+  std::memcpy(&jmax, &hred[1], 8);
+  // |column sum| <= sum_K J_K / 2 * dmin4^(2 ex) <= nc * jmax / 2 * dmin4^(2 ex); scale: that -> 2^60
+  double fxscale = 1.0;
+  if (dmin4 < 1e299 && jmax > 0.0) {
+    const double bound = (double)m.nc * jmax * 0.5 * std::pow(dmin4, 2.0 * ex);
+    int S = 60 - (int)std::ceil(std::log2(std::max(bound, 1e-300)));
+    S = std::max(-1000, std::min(1000, S));
+    fxscale = std::ldexp(1.0, S);
+  }
+  DBuf<unsigned long long> psifx((size_t)m.nc * TQN);
+  FL_CUDA(cudaMemsetAsync(psifx.p, 0, (size_t)m.nc * TQN * sizeof(unsigned long long), st));
   // per target cell orders of the mixed block pairs (read by both tail kernels: one decision)
   DBuf<int8_t> kcell(mixed ? (size_t)m.nc * nb : 1);
   if (mixed) {
@@ -386,14 +512,15 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
   if (e0) FL_CUDA(cudaEventRecord(e0, st));
   FL_E4_SWITCH_T(e4, {
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, tcell.p, B.bcells.p,
-                                                  kcell.p, B.bstat.p, B.un.p, B.uj.p, nb, psi,
+    tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, run.p, tcell.p, B.bcells.p,
+                                                  kcell.p, B.bstat.p, B.un.p, B.uj.p, nb, psifx.p, fxscale, psi,
                                                   evals_block ? evals_block : evals),
         note_launch();
   });
   FL_CHECK_LAUNCH();
   if (e1) FL_CUDA(cudaEventRecord(e1, st));
-  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb, kcell.p);
+  launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb, kcell.p,
+              psifx.p, 1.0 / fxscale);
 }
 
 }  // namespace fl
