@@ -372,10 +372,20 @@ def roofline_of(stats, d, s, fp64, kind):
     else:   # near
         ms, ev = stats["ms_near"], stats["evals_near"]
     fpe = ALG_FLOPS[(d, base)] + (POW_FLOPS_1D if d == 1 else POW_FLOPS).get(e4, 60)
-    ach = ev * fpe / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-    return {"bound": "fp64", "kernel": KERNEL_NAME[(kind, d)], "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
-            "frac": ach / fp64 if fp64 else None, "flops_per_eval": fpe, "evals_per_launch": ev,
-            "ms_per_launch": ms}
+    flops = ev * fpe
+    extra = {}
+    if kind in ("tail_block", "tail") and stats.get("evals_tail_sym", 0) > 0:
+        # an order-4 block pair swept once for both directions: each of those evaluations also
+        # accumulates into the partner cell's psi (one more FMA); it stands for two of the reference's
+        sym = stats["evals_tail_sym"]
+        flops += 2 * sym
+        extra = {"evals_sym_both_directions": sym, "reference_equivalent_evals": ev + sym}
+    ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    out = {"bound": "fp64", "kernel": KERNEL_NAME[(kind, d)], "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+           "frac": ach / fp64 if fp64 else None, "flops_per_eval": fpe, "evals_per_launch": ev,
+           "ms_per_launch": ms}
+    out.update(extra)
+    return out
 
 
 def pair_count(stats):

@@ -145,6 +145,9 @@ typedef struct fl_assembly_stats {
   /* 2D: the part of evals_tail done by the block-pair tail kernel and its device ms; the part of
    * evals_cross done by the near blocks (k >= 5, ms_near) */
   double evals_tail_block, ms_tail_block, evals_near;
+  /* 2D: the part of evals_tail_block swept for an order-4 block pair once for both directions
+   * (each such evaluation also adds to the partner cell's psi: 2 more FLOPs) */
+  double evals_tail_sym;
 } fl_assembly_stats;
 
 /* ---------------------------------------------------------------- library */

@@ -524,8 +524,8 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   cudaEvent_t ev_sizes = tm.e[11];                 // (the last timing event doubles as the size fence)
   FL_CUDA(cudaEventRecord(ev_sizes, st));
   // evaluation counters: tail (all), cross (all), tail by the block-pair kernel, cross near blocks
-  DBuf<unsigned long long> evc(4);
-  FL_CUDA(cudaMemsetAsync(evc.p, 0, 4 * sizeof(unsigned long long), st));
+  DBuf<unsigned long long> evc(5);      // [4]: the sym4 part of [2]
+  FL_CUDA(cudaMemsetAsync(evc.p, 0, 5 * sizeof(unsigned long long), st));
   DBuf<double> psi((size_t)m.nc * m.q), win((size_t)m.nc * m.q);
   FL_CUDA(cudaMemsetAsync(win.p, 0, win.n * sizeof(double), st));
   // 1D: the tail runs on its own stream, so the cross tiles (issued on `st` once the sizes are
@@ -654,7 +654,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
       {
         StreamScope sc(ts);             // the tail's temporaries are freed in its own stream order
         launch_tail2d_blocks(m, U.t, oc, ex, e4, blocks, targets.p, ntargets, psi.p, evc.p, ts, evc.p + 2, tbev[0],
-                             tbev[1]);
+                             tbev[1], evc.p + 4);
       }
       if (tstream.s) FL_CUDA(cudaEventRecord(tstream.e[2], tstream.s));
     }
@@ -790,8 +790,8 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
                        (int)row_begin, (int)row_end, D->A.p, D->lda, st);
   }
   tm.mark();  // 7
-  unsigned long long* hev = reinterpret_cast<unsigned long long*>(hs + 8);
-  FL_CUDA(cudaMemcpyAsync(hev, evc.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  unsigned long long* hev = reinterpret_cast<unsigned long long*>(hs + 32);
+  FL_CUDA(cudaMemcpyAsync(hev, evc.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&hs[4], m.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   unsigned long long hties = 0;
   FL_CUDA(cudaMemcpyAsync(&hties, ties.p, sizeof(hties), cudaMemcpyDeviceToHost, st));
@@ -817,6 +817,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
   S.evals_cross = (double)hev[1] + (double)hev[3];    // far blocks + near blocks
   S.evals_tail_block = (double)hev[2];
   S.evals_near = (double)hev[3];
+  S.evals_tail_sym = (double)hev[4];
   S.ms_tail_block = 0.0;
   if (tbev[1]) {
     float a = 0.f;

@@ -270,7 +270,8 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
 void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                           const Blocks2D& B, const int* targets, int ntargets, double* psi,
                           unsigned long long* evals, cudaStream_t st, unsigned long long* evals_block = nullptr,
-                          cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr);
+                          cudaEvent_t e0 = nullptr, cudaEvent_t e1 = nullptr,
+                          unsigned long long* evals_sym = nullptr);
 void launch_debug_orders(const DevMesh& m, const OrderConsts& oc, int8_t* cross_k, int8_t* tail_k,
                          cudaStream_t st);
 // fl_far1d.cu (1D: lean tail, packed pair-block cross + gather)

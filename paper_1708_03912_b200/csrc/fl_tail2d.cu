@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
                                                             const double* __restrict__ uj, int nb,
                                                             unsigned long long* __restrict__ psifx, double fxscale,
                                                             double* __restrict__ psi,
-                                                            unsigned long long* __restrict__ evals) {
+                                                            unsigned long long* __restrict__ evals,
+                                                            unsigned long long* __restrict__ evals_sym) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sM = reinterpret_cast<double2*>(smem_raw);          // TWIN source nodes: -2 y' (centred)
   double2* sQ = sM + TWIN;                                     // TWIN: |y'|^2, J * w
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   const int Kw = tid < TB ? bcells[P * TB + tid] : -1;     // thread c < 32: target cell c (orders)
   const bool Kw_t = Kw >= 0 && tcell[Kw];
   double acc[2][2] = {};
-  unsigned long long nev = 0;
+  unsigned long long nev = 0, nsy = 0;
   bool missing = false;
   // fast path: uniform order k <= 4, the whole block's 32 k^2 nodes in one half of the window
   // (node-major from the block-ordered staging array un / uj), software-pipelined: the next fast
@@ -321,8 +322,11 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     if (wid == 0) {                              // evaluation count: valid source cells (lanes = row 0)
       const int nvs = __popc(__ballot_sync(0xffffffffu, pj[0] != 0.0));
       // sym4: every cell of the block is swept (its nodes are the sources of the column sums)
-      const int ntt = sym4_mode(P, sL[qi] & 0xffffff, k) > 0 ? nvp : ntv;
-      if (lane == 0) nev += (unsigned long long)nvs * kk * ntt * TQN;
+      const bool sy = sym4_mode(P, sL[qi] & 0xffffff, k) > 0;
+      if (lane == 0) {
+        nev += (unsigned long long)nvs * kk * (sy ? nvp : ntv) * TQN;
+        if (sy) nsy += (unsigned long long)nvs * kk * nvp * TQN;
+      }
     }
     if (tid == 0 && dir.rule(T_DISJ, k).cnt != kk) missing = true;
   };
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   if (tid == 0) {
     if (missing) atomicOr(m.err, 1);
     if (evals && nev) atomicAdd(evals, nev);
+    if (evals_sym && nsy) atomicAdd(evals_sym, nsy);
   }
 }
 
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
 void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                           const Blocks2D& B, const int* targets, int ntargets, double* psi,
                           unsigned long long* evals, cudaStream_t st, unsigned long long* evals_block,
-                          cudaEvent_t e0, cudaEvent_t e1) {
+                          cudaEvent_t e0, cudaEvent_t e1, unsigned long long* evals_sym) {
   if (ntargets <= 0) return;
   const int nb = B.nb;
   const size_t smem = (size_t)TWIN * 32 + (size_t)(TT / 32) * (TWIN / 2) * 8 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
@@ -514,7 +519,7 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, run.p, tcell.p, B.bcells.p,
                                                   kcell.p, B.bstat.p, B.un.p, B.uj.p, nb, psifx.p, fxscale, psi,
-                                                  evals_block ? evals_block : evals),
+                                                  evals_block ? evals_block : evals, evals_sym),
         note_launch();
   });
   FL_CHECK_LAUNCH();
