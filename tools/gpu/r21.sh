@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+timeout 300 python tools/assemble_once.py c5 --reps 2 > gpurun_out/r21_c5.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r21_t_all.log 2>&1
+echo "all rc=$?" >> gpurun_out/r21_t_all.log
+timeout 1200 python bench.py > gpurun_out/r21_bench.log 2>&1
+echo "bench rc=$?" >> gpurun_out/r21_bench.log
