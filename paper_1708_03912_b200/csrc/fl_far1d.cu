@@ -183,9 +183,7 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
                                                      const int* __restrict__ targets,
                                                      const int* __restrict__ d_ntargets,
                                                      double* __restrict__ psi,
-                                                     unsigned long long* __restrict__ evals,
-                                                     const int8_t* __restrict__ kuni, int nch,
-                                                     const double* __restrict__ part, int nsplit) {
+                                                     unsigned long long* __restrict__ evals) {
   constexpr int Q = 6;
   __shared__ int qs[4][NT][64], qk[4][NT][64];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -224,57 +222,27 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
   const int4* R = reinterpret_cast<const int4*>(S.rec);
   int4 na = make_int4(0, 0, 0, 0), nb = na;     // prefetched record of the next source
   if (lane < m.nc) { na = __ldg(R + 2 * lane); nb = __ldg(R + 2 * lane + 1); }
-  // per-lane chunk orders / sides of the 32 chunks starting at cb
-  auto chunk_flags = [&](int cb) {
-    const int cj = cb + lane;
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      ck[t] = cj < nchunks ? chunk_order(oc, alo[t], ahi[t], alh[t], alg[t], S.cstat + (size_t)CSTAT * cj) : 0;
-      rmask[t] = __ballot_sync(0xffffffffu, cj < nchunks && S.cstat[(size_t)CSTAT * cj] > ahi[t]);
-    }
-  };
-  // kuni (one target per warp): only the source chunks the chunk-pair bounds left open, taken from
-  // a ballot of the target chunk's kuni row; the others were done by tail1d_block_kernel
-  const bool listed = kuni != nullptr && NT == 1;
-  const int8_t* krow = listed ? kuni + (size_t)(K[0] >> 5) * nch : nullptr;
-  unsigned pend = 0;
-  int cbase = -32;
-  for (int s0 = 0;;) {
-    int ci;
-    int4 ra, rb;
-    if (listed) {
-      while (!pend) {
-        cbase += 32;
-        if (cbase >= nchunks) break;
-        pend = __ballot_sync(0xffffffffu, cbase + lane < nchunks && krow[cbase + lane] == 0);
-        if (pend) chunk_flags(cbase);
-      }
-      if (!pend) break;
-      ci = cbase + __ffs(pend) - 1;
-      pend &= pend - 1;
-      s0 = ci << 5;
-      ra = rb = make_int4(0, 0, 0, 0);
-      if (s0 + lane < m.nc) { ra = __ldg(R + 2 * (s0 + lane)); rb = __ldg(R + 2 * (s0 + lane) + 1); }
-    } else {
-      if (s0 >= m.nc) break;
-      ci = s0 >> 5;
-      ra = na;
-      rb = nb;
-      if (s0 + lane + 32 < m.nc) { na = __ldg(R + 2 * (s0 + lane + 32)); nb = __ldg(R + 2 * (s0 + lane + 32) + 1); }
-      if ((ci & 31) == 0) chunk_flags(ci);   // order-2 flags of the next 32 chunks, one per lane
-    }
+  for (int s0 = 0; s0 < m.nc; s0 += 32) {
     const int s = s0 + lane;
-    if (!listed) s0 += 32;
+    const int4 ra = na, rb = nb;
+    if (s + 32 < m.nc) { na = __ldg(R + 2 * (s + 32)); nb = __ldg(R + 2 * (s + 32) + 1); }
     const double sx0 = __hiloint2double(ra.y, ra.x), sx1 = __hiloint2double(ra.w, ra.z);
     const int bv0 = rb.x, bv1 = rb.y;
     const double blo = fmin(sx0, sx1), bhi = fmax(sx0, sx1);
     const double e = sx1 - sx0, J = fabs(e);
     const double y0 = sx0 + t0 * e, y1 = sx0 + t1 * e;
     const double j0 = J * w0, j1 = J * w1;
+    const int ci = s0 >> 5;
+    if ((ci & 31) == 0) {                       // order-2 flags of the next 32 chunks, one per lane
+      const int cj = ci + lane;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        ck[t] = cj < nchunks ? chunk_order(oc, alo[t], ahi[t], alh[t], alg[t], S.cstat + (size_t)CSTAT * cj) : 0;
+        rmask[t] = __ballot_sync(0xffffffffu, cj < nchunks && S.cstat[(size_t)CSTAT * cj] > ahi[t]);
+      }
+    }
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
-      // kuni with several targets per warp: skip per target
-      if (kuni && !listed && kuni[(size_t)(K[t] >> 5) * nch + ci] != 0) continue;
       const int kc = __shfl_sync(0xffffffffu, ck[t], ci & 31);   // warp-uniform chunk order (0: mixed)
       if (kc > 2) {                             // the whole chunk has order kc: no per-source orders
         if (s < m.nc) {
@@ -370,11 +338,7 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const double v = warp_sum(acc[t][q]);
-      if (lane == 0 && valid[t]) {
-        double b = 0.0;                          // the block kernel's partial sums, in split order
-        for (int g = 0; kuni && g < nsplit; ++g) b += part[(size_t)g * m.nc * Q + (size_t)K[t] * Q + q];
-        psi[(size_t)K[t] * Q + q] = kuni ? b + v : v;
-      }
+      if (lane == 0 && valid[t]) psi[(size_t)K[t] * Q + q] = v;
     }
     if (evals && valid[t]) {
       unsigned long long nd = nodes[t];
@@ -382,182 +346,6 @@ __global__ void __launch_bounds__(128, FL_TAIL1D_MINB) tail1d_kernel(DevMesh m, 
       for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(0xffffffffu, nd, o);
       if (lane == 0) atomicAdd(evals, nd * Q);
     }
-  }
-}
-
-// ------------------------------------------------------------------ tail by chunk pairs
-// The 1D counterpart of fl_tail2d.cu (opt-in: FRACLAP_TAIL1D=block, see launch_tail1d): chunks of
-// 32 consecutive cells (cstat extents); for an
-// ordered (target chunk P, source chunk Q) pair the bounds of the boosted order formula over the
-// chunks' gap, farthest distance and h / |ln h| ranges either fix one order for all 32 x 32 cell
-// pairs (the extents are then disjoint: no pair touches) or not.  tail1d_block_kernel: a CTA per
-// target chunk, the 192 target nodes (32 cells x 6) in registers, two per thread; the uniform
-// source chunks are packed into windows of up to 1024 mapped nodes (any mix of orders: every
-// target shares the node list) and swept with broadcast shared loads.  tail1d_kernel then does
-// the other chunks pair by pair and adds.  Deterministic: fixed source order per target.
-constexpr int T1D_TT = 96;
-constexpr int T1D_WIN = 1024;
-constexpr int T1D_RN = 527;                      // sum_{k=2}^{32} k
-__host__ __device__ constexpr int roff1(int k) { return (k - 2) * (k + 1) / 2; }
-
-__global__ void tail1d_flag_kernel(const int* __restrict__ targets, const int* __restrict__ d_nt,
-                                   int* __restrict__ cflag, int* __restrict__ tcell) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < *d_nt) {
-    const int c = targets[i];
-    cflag[c >> 5] = 1;
-    tcell[c] = 1;
-  }
-}
-
-__global__ void tail1d_kuni_kernel(OrderConsts oc, const double* __restrict__ cs, const int* __restrict__ cflag,
-                                   int nch, int8_t* __restrict__ kuni) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nch * nch) return;
-  const int P = (int)(i / nch), Q = (int)(i - (int64_t)P * nch);
-  int k = 0;
-  if (cflag[P] && P != Q) {
-    const double* a = cs + (size_t)CSTAT * P;
-    const double* b = cs + (size_t)CSTAT * Q;
-    const double D = fmax(b[0] - a[1], a[0] - b[1]) * (1.0 - 1e-12);   // gap of the extents
-    if (D > 0.0) {
-      const double Dmax = fmax(b[1] - a[0], a[1] - b[0]) * (1.0 + 1e-12);
-      const double hmn = fmin(a[6], b[6]), hmx = fmax(a[2], b[2]), lmn = fmin(a[3], b[3]), lmx = fmax(a[4], b[4]);
-      const double hi = order_bound_hi(oc, oc.coff_tail, D, hmn, hmx, lmn, lmx);
-      const double lo = order_bound_lo(oc, oc.coff_tail, D, Dmax, hmn, hmx, lmn, lmx);
-      const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
-      const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
-      if (c0 == c1) k = (int)c0;
-    }
-  }
-  kuni[i] = (int8_t)k;
-}
-
-template <int E4>
-__global__ void __launch_bounds__(T1D_TT) tail1d_block_kernel(DevMesh m, const double* __restrict__ tab, DevTables dir,
-                                                              double ex, Src1D S, const int8_t* __restrict__ kuni,
-                                                              const int* __restrict__ cflag,
-                                                              const int* __restrict__ tcell, int nch, int nsplit,
-                                                              double* __restrict__ part,
-                                                              unsigned long long* __restrict__ evals) {
-  extern __shared__ __align__(16) unsigned char smem1t[];
-  double* sY = reinterpret_cast<double*>(smem1t);        // T1D_WIN mapped source nodes
-  double* sW = sY + T1D_WIN;                             // T1D_WIN J * w
-  double* sR = sW + T1D_WIN;                             // T1D_RN x (t, w)
-  int* sL = reinterpret_cast<int*>(sR + 2 * T1D_RN);     // uniform source chunks: Q | k << 24
-  __shared__ int s_wsum[T1D_TT / 32], s_nq, s_wn;
-  __shared__ int s_woff[33], s_wq[32], s_wk[32];
-  constexpr int Q6 = 6;
-  // CTA (P, g): target chunk P against the g-th of nsplit consecutive parts of its uniform source
-  // chunks (partial sums to part[g], added in g order by tail1d_kernel)
-  const int P = blockIdx.x / nsplit, g = blockIdx.x - P * nsplit;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (!cflag[P]) return;
-  for (int i = tid; i < T1D_RN; i += T1D_TT) {
-    int k = 2;
-    while (roff1(k + 1) <= i) ++k;
-    const RuleRef rr = dir.rule(T_DISJ, k);
-    const int r = i - roff1(k);
-    if (rr.cnt == k) {
-      const double* nd = tab + (size_t)(rr.off + r) * NODE;
-      sR[2 * i] = nd[0];
-      sR[2 * i + 1] = nd[2];
-    } else {
-      sR[2 * i] = sR[2 * i + 1] = 0.0;
-    }
-  }
-  const int8_t* krow = kuni + (size_t)P * nch;
-  if (tid == 0) s_nq = 0;
-  __syncthreads();
-  for (int base = 0; base < nch; base += T1D_TT) {
-    const int Q = base + tid;
-    const int k = Q < nch ? (int)krow[Q] : 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, k != 0);
-    if (lane == 0) s_wsum[wid] = __popc(bal);
-    __syncthreads();
-    int off = s_nq;
-    for (int w = 0; w < wid; ++w) off += s_wsum[w];
-    if (k) sL[off + __popc(bal & ((1u << lane) - 1u))] = Q | (k << 24);
-    __syncthreads();
-    if (tid == 0) s_nq += s_wsum[0] + s_wsum[1] + s_wsum[2];
-    __syncthreads();
-  }
-  const int q_begin = (int)((int64_t)s_nq * g / nsplit), q_end = (int)((int64_t)s_nq * (g + 1) / nsplit);
-  // the thread's two target nodes (cell P * 32 + idx / 6, node idx % 6)
-  double xq[2];
-  int Kc[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int idx = tid + T1D_TT * t, c = P * 32 + idx / Q6;
-    Kc[t] = c < m.nc && tcell[c] ? c : -1;
-    xq[t] = c < m.nc ? m.X[(size_t)c * Q6 + idx % Q6] : -1e300;
-  }
-  int ntv = 0;
-  if (tid == 0)
-    for (int c = P * 32; c < min(m.nc, P * 32 + 32); ++c) ntv += tcell[c];
-  double acc[2][2] = {};
-  unsigned long long nev = 0;
-  bool missing = false;
-  for (int qi = q_begin; qi < q_end;) {
-    if (tid == 0) {                              // a window: consecutive chunks while they fit
-      int n = 0, tot = 0;
-      while (qi + n < q_end && n < 32) {
-        const int k = sL[qi + n] >> 24;
-        if (tot + 32 * k > T1D_WIN) break;
-        s_wq[n] = sL[qi + n] & 0xffffff;
-        s_wk[n] = k;
-        s_woff[n] = tot;
-        tot += 32 * k;
-        const int nvs = min(32, m.nc - s_wq[n] * 32);
-        nev += (unsigned long long)nvs * k * ntv * Q6;
-        if (dir.rule(T_DISJ, k).cnt != k) missing = true;
-        ++n;
-      }
-      s_woff[n] = tot;
-      s_wn = n;
-    }
-    __syncthreads();
-    const int n = s_wn, tot = s_woff[n], totp = (tot + 3) & ~3;
-    for (int idx = tid; idx < totp; idx += T1D_TT) {
-      double y = 1e300, w = 0.0;                 // padding: far away, weight 0
-      if (idx < tot) {
-        int j = 0;
-        while (j + 1 < n && s_woff[j + 1] <= idx) ++j;
-        const int k = s_wk[j], loc = idx - s_woff[j], c = s_wq[j] * 32 + loc / k, r = loc % k;
-        if (c < m.nc) {
-          const double x0 = S.x0[c], e = S.x1[c] - x0;
-          y = x0 + sR[2 * (roff1(k) + r)] * e;
-          w = S.h[c] * sR[2 * (roff1(k) + r) + 1];
-        }
-      }
-      sY[idx] = y;
-      sW[idx] = w;
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int p = 0; p < totp; p += 4) {
-      double y[4], w[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        y[u] = sY[p + u];
-        w[u] = sW[p + u];
-      }
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) acc[t][u & 1] = fma(w[u], kpow_abs<E4>(xq[t] - y[u], ex), acc[t][u & 1]);
-    }
-    __syncthreads();
-    qi += n;
-  }
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int idx = tid + T1D_TT * t;
-    if (Kc[t] >= 0) part[(size_t)g * m.nc * Q6 + (size_t)Kc[t] * Q6 + idx % Q6] = acc[t][0] + acc[t][1];
-  }
-  if (tid == 0) {
-    if (missing) atomicOr(m.err, 1);
-    if (evals && nev) atomicAdd(evals, nev);
   }
 }
 
@@ -1383,46 +1171,8 @@ void launch_tail1d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, 
   const Src1D S = P->B.view();
   constexpr int NT = FL_TAIL1D_NT;
   const int grid = (ntargets_ub + 4 * NT - 1) / (4 * NT);
-  // FRACLAP_TAIL1D=block: uniform chunk pairs through tail1d_block_kernel.  Off by default: at c2
-  // the warp kernel's own per-target chunk bounds already make the far chunks cheap, and the
-  // chunk-pair split measured 1.09 ms against 0.85 ms for the warp kernel alone
-  static const bool warp_only = [] {
-    const char* v = getenv("FRACLAP_TAIL1D");
-    return !(v && std::string(v) == "block");
-  }();
-  const int nch = (m.nc + 31) / 32;
-  const size_t smem = (size_t)2 * T1D_WIN * 8 + (size_t)2 * T1D_RN * 8 + (size_t)nch * 4;
-  if (warp_only || m.q != 6 || smem > 200 * 1024) {
-    FL_E4_SWITCH1(e4, (tail1d_kernel<E4, NT><<<grid, 128, 0, st>>>(m, t.data, t, oc, ex, S, targets, d_ntargets, psi,
-                                                                   evals, nullptr, 0, nullptr, 0),
-                       ::fl::note_launch()));
-    FL_CHECK_LAUNCH();
-    return;
-  }
-  StreamScope sc(st);                             // temporaries in the tail's stream order
-  DBuf<int> cflag(nch), tcell(m.nc);
-  DBuf<int8_t> kuni((size_t)nch * nch);
-  FL_CUDA(cudaMemsetAsync(cflag.p, 0, (size_t)nch * sizeof(int), st));
-  FL_CUDA(cudaMemsetAsync(tcell.p, 0, (size_t)m.nc * sizeof(int), st));
-  tail1d_flag_kernel<<<(ntargets_ub + 255) / 256, 256, 0, st>>>(targets, d_ntargets, cflag.p, tcell.p),
-      ::fl::note_launch();
-  const int64_t nn = (int64_t)nch * nch;
-  tail1d_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, S.cstat, cflag.p, nch, kuni.p),
-      ::fl::note_launch();
-  // enough CTAs to fill the GPU: each target chunk's uniform sources in nsplit parts
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int nsplit = std::max(1, std::min(16, (12 * sms + nch - 1) / nch));
-  DBuf<double> part((size_t)nsplit * m.nc * 6);
-  FL_E4_SWITCH1(e4, {
-    FL_CUDA(cudaFuncSetAttribute(tail1d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tail1d_block_kernel<E4><<<nch * nsplit, T1D_TT, smem, st>>>(m, t.data, t, ex, S, kuni.p, cflag.p, tcell.p, nch,
-                                                                nsplit, part.p, evals);
-    ::fl::note_launch();
-  });
   FL_E4_SWITCH1(e4, (tail1d_kernel<E4, NT><<<grid, 128, 0, st>>>(m, t.data, t, oc, ex, S, targets, d_ntargets, psi,
-                                                                 evals, kuni.p, nch, part.p, nsplit),
+                                                                 evals),
                      ::fl::note_launch()));
   FL_CHECK_LAUNCH();
 }
