@@ -7,7 +7,8 @@ matvec GB/s and the Jacobi-PCG solve reported beside it, against the FP64 / HBM 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 Workload: BASELINE configs[4] = c5 (2D unit square 256x256, s = 1/2, n = 65025, A = 33.8 GB),
-the largest configuration that fits one GPU (configs[1] = c2 is timed too, as `extra.c2`).
+the largest configuration that fits one GPU (configs[1] = c2 and configs[3] = c4a / c4b with their
+100-matvec bandwidth runs are timed too, as `extra`).
 A step = one full dense assembly (assembly.py:1059-1104) of the configuration: every element
 pair K x K~ (identical, touching, disjoint cross, ordered tail, boundary) on the device, inputs
 resident, timed with CUDA events on the launching stream.  N > 1 (`--gpus N` re-launches itself
@@ -589,6 +590,8 @@ def main():
     extra = {}
     if rank == 0 and world == 1 and not args.no_extra and args.config != "c2":
         extra["c2"] = extra_c2(lib, stream, flush, fp64)
+        for c4 in ("c4a", "c4b"):
+            extra[c4] = extra_c4(c4, lib, stream, flush, fp64)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -634,6 +637,43 @@ def extra_c2(lib, stream, flush, fp64, steps=5):
     out = {"mesh": CONFIG_TEXT["c2"], "ms_per_step": ms, "value": pair_count(st) / (ms * 1e-3), "unit": "pairs/s",
            "roofline": roofline_of(st, 1, s, fp64, "tail"), "roofline_cross": roofline_of(st, 1, s, fp64, "cross")}
     x, rep = S.pcg(op, A.load_vector(mesh, dm, 1.0), tol=1e-10, max_iter=10 ** 5)
+    out["cg"] = {"iterations": rep.iterations, "ms_per_iteration": 1e3 * rep.seconds / max(rep.iterations, 1)}
+    op.free()
+    return out
+
+
+def extra_c4(name, lib, stream, flush, fp64, steps=3, matvecs=100):
+    """configs[3] (c4a / c4b: 2D 128x128, s = 1/4 / 3/4): device-timed assembly with its kernel
+    rooflines, 100 matvecs with x ~ U(-1,1) (seed 0) for the bandwidth, and Jacobi-PCG to 1e-10."""
+    import torch
+    from paper_1708_03912_b200 import mesh as M, assembly as A, solve as S
+    mesh, s = M.baseline_mesh(name)
+    dm = M.DofMap(mesh, s)
+    ker = A.FractionalKernel(2, s)
+    sptr = stream.cuda_stream
+    op, times = time_assembly(lambda: A.assemble_dense_device(mesh, dm, ker, stream=sptr), steps, 2, stream, flush,
+                              1, None)
+    st = op.stats()
+    ms = float(np.mean(times))
+    kinds = ("tail_block", "tail_pairs", "cross_far", "near") if st["ms_tail_block"] > 0 else ("tail", "cross")
+    out = {"mesh": CONFIG_TEXT[name], "ms_per_step": ms, "value": pair_count(st) / (ms * 1e-3), "unit": "pairs/s",
+           "roofline_kernels": [roofline_of(st, 2, s, fp64, k) for k in kinds]}
+    n = dm.n
+    x = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, n)).cuda()
+    y = torch.zeros(n, dtype=torch.float64, device="cuda")
+    mv = []
+    for i in range(matvecs + 3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        op.matvec_device(x.data_ptr(), y.data_ptr(), sptr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= 3:
+            mv.append(e0.elapsed_time(e1))
+    mv_ms = float(np.median(mv))
+    out["matvec"] = {"gbs": (8.0 * n * n + 16.0 * n) / (mv_ms * 1e-3) / 1e9, "ms": mv_ms, "count": matvecs,
+                     "x": "U(-1,1) seed 0"}
+    xs, rep = S.pcg(op, A.load_vector(mesh, dm, 1.0), tol=1e-10, max_iter=10 ** 5)
     out["cg"] = {"iterations": rep.iterations, "ms_per_iteration": 1e3 * rep.seconds / max(rep.iterations, 1)}
     op.free()
     return out

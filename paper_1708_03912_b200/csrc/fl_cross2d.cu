@@ -186,10 +186,11 @@ __global__ void cell_nodes2_kernel(DevMesh m, const double* __restrict__ tab, Ru
 // whose outer cell is in that ring), so dmin = min over K of the exact distance to its
 // second-ring disjoint cells bounds every disjoint pair's node distance from below.
 __global__ void dmin_kernel(DevMesh m, unsigned long long* __restrict__ dmin_bits,
-                            unsigned long long* __restrict__ jmax_bits) {
+                            unsigned long long* __restrict__ jmax_bits, unsigned long long* __restrict__ rmax_bits) {
   const int K = blockIdx.x * blockDim.x + threadIdx.x;
   if (K >= m.nc) return;
   const CellGeo& A = m.geo[K];
+  atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(A.rad));
   double best = 1e300;
   for (int a = 0; a < 3; ++a) {
     const int v = A.v[a];
@@ -928,6 +929,19 @@ void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row
   block_unodes_kernel<<<(unsigned)(((int64_t)nb * UNODES + 255) / 256), 256, 0, st>>>(B.bcells.p, B.nodes.p, nb, m,
                                                                                     B.slot.p, B.un.p, B.uj.p, B.us.p),
       note_launch();
+  // smallest distance of two disjoint cells (second-ring scan), largest Jacobian and cell radius
+  DBuf<unsigned long long> bnd(3);
+  unsigned long long init[3] = {0ull, 0ull, 0ull};
+  const double big = 1e300;
+  std::memcpy(&init[0], &big, 8);
+  FL_CUDA(cudaMemcpyAsync(bnd.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  dmin_kernel<<<(nc + 127) / 128, 128, 0, st>>>(m, bnd.p, bnd.p + 1, bnd.p + 2), note_launch();
+  unsigned long long hb[3];
+  FL_CUDA(cudaMemcpyAsync(hb, bnd.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  FL_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(&B.dmin, &hb[0], 8);
+  std::memcpy(&B.jmax, &hb[1], 8);
+  std::memcpy(&B.radmax, &hb[2], 8);
   FL_CHECK_LAUNCH();
 }
 
@@ -959,21 +973,11 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   }
   DBuf<double> wl(NPRE2 * 3);
   FL_CUDA(cudaMemcpyAsync(wl.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-  DBuf<unsigned long long> bnd(2);
-  unsigned long long init[2] = {0ull, 0ull};
-  const double big = 1e300;
-  std::memcpy(&init[0], &big, 8);
-  FL_CUDA(cudaMemcpyAsync(bnd.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  dmin_kernel<<<(nc + 127) / 128, 128, 0, st>>>(m, bnd.p, bnd.p + 1), note_launch();
-  unsigned long long hb[2];
   int herr = 0;
-  FL_CUDA(cudaMemcpyAsync(hb, bnd.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   if (herr) throw Error(-1, "a Morton block of 32 cells touches more than 64 DoFs (mesh too irregular)");
-  double dmin, jmax;
-  std::memcpy(&dmin, &hb[0], 8);
-  std::memcpy(&jmax, &hb[1], 8);
+  const double dmin = B.dmin, jmax = B.jmax;
   // |entry| <= vmax^2 * C * Jmax^2 * (1/6)^2 * dmin^(-(d+2s)) (sum of w*lambda over the reference
   // triangle = 1/6; at most vmax cells around a vertex); scale: that bound -> 2^54
   const double e = -2.0 * ex;                      // d + 2s

@@ -256,6 +256,9 @@ struct Blocks2D {
   DBuf<double2> nodes, un;
   DBuf<double> uj;
   DBuf<int> us;
+  double dmin = 1e300;    // smallest distance of two cells sharing no vertex (second-ring scan)
+  double jmax = 0.0;      // largest Jacobian
+  double radmax = 0.0;    // largest cell radius (vertex - centroid)
 };
 constexpr int UNODES2D = 928;
 void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row_end, Blocks2D& B, cudaStream_t st);

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 300 python tools/assemble_once.py c5 --reps 2 > gpurun_out/r27_c5.log 2>&1
+timeout 300 python tools/assemble_once.py c3 --reps 3 > gpurun_out/r27_c3.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r27_t_all.log 2>&1
+echo "all rc=$?" >> gpurun_out/r27_t_all.log
