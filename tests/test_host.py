@@ -65,3 +65,46 @@ def test_no_oracle_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def test_assembly_stats_layout_matches_header():
+    """The ctypes mirror of fl_assembly_stats has the header's fields, types and order."""
+    from paper_1708_03912_b200 import _lib
+    src = open(os.path.join(ROOT, "include", "fraclap_b200.h")).read()
+    body = re.search(r"typedef struct fl_assembly_stats \{(.*?)\} fl_assembly_stats;", src, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        ctype, names = decl.split(None, 1)
+        fields += [(n.strip(), ctype) for n in names.split(",")]
+    cmap = {"int64_t": ctypes.c_int64, "int32_t": ctypes.c_int32, "double": ctypes.c_double}
+    st = [c for c in vars(_lib).values() if isinstance(c, type) and issubclass(c, ctypes.Structure)
+          and [f[0] for f in c._fields_][:2] == ["pairs_identical", "pairs_touching"]]
+    assert len(st) == 1
+    got = [(n, t) for n, t in st[0]._fields_]
+    assert [n for n, _ in got] == [n for n, _ in fields]
+    assert all(t == cmap[c] for (_, t), (_, c) in zip(got, fields))
+
+
+def test_bench_rooflines_and_pair_count():
+    """bench.py's pure pieces: the element-pair count and the per-kernel rooflines (the order-4
+    evaluations serving both directions add their partner accumulation)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    B = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(B)
+    st = dict(pairs_identical=1, pairs_touching=2, pairs_cross=3, pairs_tail=4, pairs_boundary_singular=5,
+              pairs_boundary_flux=6, ms_tail=2.0, evals_tail=3e9, ms_tail_block=1.0, evals_tail_block=2e9,
+              evals_tail_sym=1e9, ms_cross=1.0, ms_cross_compute=0.5, evals_cross=1e9, evals_near=2e8, ms_near=0.1)
+    assert B.pair_count(st) == 21
+    r = B.roofline_of(st, 2, 0.5, 30.0, "tail_block")
+    assert r["kernel"] == "tail2d_block_kernel" and r["flops_per_eval"] == 16
+    assert abs(r["achieved"] - (2e9 * 16 + 2 * 1e9) / 1e-3 / 1e12) < 1e-9
+    assert r["reference_equivalent_evals"] == 3e9
+    rp = B.roofline_of(st, 2, 0.5, 30.0, "tail_pairs")
+    assert rp["evals_per_launch"] == 1e9 and rp["ms_per_launch"] == 1.0
+    rc = B.roofline_of(st, 2, 0.5, 30.0, "cross_far")
+    assert rc["evals_per_launch"] == 8e8 and rc["flops_per_eval"] == 20
