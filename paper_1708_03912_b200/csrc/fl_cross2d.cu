@@ -252,6 +252,29 @@ __global__ void block_pairs_kernel(OrderConsts oc, const double* __restrict__ bs
   key[i] = __float_as_uint((float)fmax(Dmin, 0.0));      // heavy first: ascending gap
 }
 
+// The disjoint block pairs the circle bounds left open (kuni == 0) get a second try with the exact
+// range of their 32 x 32 pairs' distance estimates (block_pair_dist_range): a warp per pair.
+__global__ void cross_refine_kernel(OrderConsts oc, DevMesh m, const int* __restrict__ bcells,
+                                    const double* __restrict__ bs, int64_t ncand, int4* __restrict__ pairs,
+                                    int* __restrict__ nearflag) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ncand) return;
+  const int4 p = pairs[w];
+  if (p.z != 0 || p.x == p.y) return;
+  const double* a = bs + 8 * p.x;
+  const double* b = bs + 8 * p.y;
+  const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
+  const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
+  if (!(Dmin > 0.0)) return;
+  double lo, hi;
+  block_pair_dist_range(m, bcells, p.x, p.y, lane, lo, hi);
+  const int k = block_uniform_order(oc, oc.coff, lo * (1.0 - 1e-12) - 1e-300, hi * (1.0 + 1e-12), a, b);
+  if (k == 0 || lane) return;
+  pairs[w].z = k;
+  nearflag[w] = k >= KW2D ? 1 : 0;
+}
+
 // 64-bit fixed-point add into a shared-memory tile word with two native 32-bit shared atomics
 // (a 64-bit shared atomicAdd compiles to a compare-and-swap loop): the low words add modulo 2^32
 // and the carry read from the returned old value goes into the high word, so once every add has
@@ -997,6 +1020,15 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
                                                                      (row_begin == 0 && row_end == m.n) ? 1 : 0,
                                                                      ncand, raw.p, key.p, keep.p, nflag.p),
       note_launch();
+  // FRACLAP_EXACT_RANGE=0: circle bounds only
+  static const bool exact_range = [] {
+    const char* v = getenv("FRACLAP_EXACT_RANGE");
+    return !(v && std::string(v) == "0");
+  }();
+  if (exact_range)
+    cross_refine_kernel<<<(unsigned)((ncand * 32 + 255) / 256), 256, 0, st>>>(oc, m, bcells.p, bstat.p, ncand, raw.p,
+                                                                            nflag.p),
+        note_launch();
   DBuf<int> idx(ncand), idx2(ncand);
   iota_kernel64<<<(unsigned)((ncand + 255) / 256), 256, 0, st>>>(idx.p, ncand), note_launch();
   {

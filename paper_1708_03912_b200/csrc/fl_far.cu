@@ -1053,7 +1053,7 @@ void launch_order_hist(const DevMesh& m, const OrderConsts& oc, unsigned long lo
   FL_CHECK_LAUNCH();
 }
 
-// FP64 peak probe: 8 independent DFMA chains per thread, 148*8 CTAs of 256 threads.
+// FP64 peak probe: 8 independent DFMA chains per thread, 148*8 CTAs of 256 threads, best of 5.
 __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int iters, double a, double b) {
   double x[8];
 #pragma unroll
@@ -1073,7 +1073,8 @@ double probe_fp64_tflops(cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = sms * 8, iters = 4096;
+  // ~5 ms per launch: long enough that launch and ramp are < 1 % (a 0.6 ms probe read ~8 % low)
+  const int grid = sms * 8, iters = 32768;
   dfma_probe_kernel<<<grid, 256, 0, st>>>(out.p, 64, 0.999999, 1e-7), ::fl::note_launch();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);

@@ -261,6 +261,55 @@ struct Blocks2D {
   double radmax = 0.0;    // largest cell radius (vertex - centroid)
 };
 constexpr int UNODES2D = 928;
+
+// Exact range, over the 32 x 32 cell pairs of Morton blocks P and Q, of the distance estimate that
+// select_order is fed (assembly.py:764-781): every pair's estimate lies in [lo, hi] with
+// lo = min (|cK - cL| - (rK + rL)) (the estimate of a close pair is the exact triangle distance,
+// >= that) and hi = max of the same value, or |cK - cL| for a close pair (the triangles hold their
+// centroids, so their distance is <= it).  The block bounding circles give only
+// dc -+ (R_P + R_Q); these exact values let the order bounds prove one order for more block pairs.
+// Warp-cooperative (every lane returns the result); empty slots of partial blocks are skipped.
+// Symmetric in (P, Q) bitwise: (-d)^2 == d^2 and rK + rL == rL + rK.
+__device__ __forceinline__ void block_pair_dist_range(const DevMesh& m, const int* __restrict__ bcells, int P, int Q,
+                                                      int lane, double& lo, double& hi) {
+  const int cp = bcells[P * CB2D + lane], cq = bcells[Q * CB2D + lane];
+  double px = 0.0, py = 0.0, pr = 0.0, qx = 0.0, qy = 0.0, qr = 0.0;
+  if (cp >= 0) { const CellGeo& g = m.geo[cp]; px = g.cx; py = g.cy; pr = g.rad; }
+  if (cq >= 0) { const CellGeo& g = m.geo[cq]; qx = g.cx; qy = g.cy; qr = g.rad; }
+  const unsigned qvalid = __ballot_sync(0xffffffffu, cq >= 0);
+  double l = 1e300, h = -1e300;
+  for (int j = 0; j < CB2D; ++j) {
+    const double x = __shfl_sync(0xffffffffu, qx, j), y = __shfl_sync(0xffffffffu, qy, j);
+    const double r = __shfl_sync(0xffffffffu, qr, j);
+    if (cp < 0 || !((qvalid >> j) & 1u)) continue;
+    const double dx = __dsub_rn(px, x), dy = __dsub_rn(py, y);
+    const double dc = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    const double rr = __dadd_rn(pr, r);
+    const double low = __dsub_rn(dc, rr);
+    l = fmin(l, low);
+    h = fmax(h, low < 2.0 * rr ? dc : low);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    l = fmin(l, __shfl_xor_sync(0xffffffffu, l, o));
+    h = fmax(h, __shfl_xor_sync(0xffffffffu, h, o));
+  }
+  lo = l;
+  hi = h;
+}
+// One order for every cell pair of blocks a, b (bstat records: cx cy R hmin hmax |ln h|min
+// |ln h|max) whose distance estimates lie in [Dmin, Dmax], or 0: the rigorous bounds of the order
+// formula (coff = C_offset or C_offset - 4) with 1e-9 margins around the ceil.
+__device__ __forceinline__ int block_uniform_order(const OrderConsts& oc, double coff, double Dmin, double Dmax,
+                                                   const double* a, const double* b) {
+  if (!(Dmin > 0.0)) return 0;
+  const double hmn = fmin(a[3], b[3]), hmx = fmax(a[4], b[4]), lmn = fmin(a[5], b[5]), lmx = fmax(a[6], b[6]);
+  const double hi = order_bound_hi(oc, coff, Dmin, hmn, hmx, lmn, lmx);
+  const double lo = order_bound_lo(oc, coff, Dmin, Dmax, hmn, hmx, lmn, lmx);
+  const double c0 = fmin(fmax(ceil(lo - 1e-9), 2.0), (double)oc.cap_disjoint);
+  const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
+  return c0 == c1 ? (int)c0 : 0;
+}
 void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row_end, Blocks2D& B, cudaStream_t st);
 void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                       const Blocks2D& B, int row_begin, int row_end, double* A, int64_t lda,

@@ -79,6 +79,36 @@ __global__ void tail_kuni_kernel(OrderConsts oc, const double* __restrict__ bs, 
   kuni[i] = (int8_t)k;
 }
 
+// The block pairs the circle bounds left open (kuni == 0, disjoint, at least a block radius
+// apart) get a second try with the exact range of the 32 x 32 pairs' distance estimates
+// (block_pair_dist_range): a warp per unordered pair P < Q, both entries written with the same
+// order, so kuni stays symmetric; the order-4 bookkeeping as in tail_kuni_kernel.
+__global__ void tail_refine_kernel(OrderConsts oc, DevMesh m, const int* __restrict__ bcells,
+                                   const double* __restrict__ bs, const int* __restrict__ tflag, int nb,
+                                   int8_t* __restrict__ kuni, unsigned long long* __restrict__ dmin4,
+                                   int* __restrict__ run) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)nb * nb) return;
+  const int P = (int)(w / nb), Q = (int)(w - (int64_t)P * nb);
+  if (P >= Q || kuni[w] != 0) return;
+  const double* a = bs + 8 * P;
+  const double* b = bs + 8 * Q;
+  const double dc = sqrt((a[0] - b[0]) * (a[0] - b[0]) + (a[1] - b[1]) * (a[1] - b[1]));
+  const double Dmin = (dc - a[2] - b[2]) * (1.0 - 1e-12) - 1e-300;
+  if (!(Dmin > 0.0 && Dmin >= fmax(a[2], b[2]))) return;
+  double lo, hi;
+  block_pair_dist_range(m, bcells, P, Q, lane, lo, hi);
+  const int k = block_uniform_order(oc, oc.coff_tail, lo * (1.0 - 1e-12) - 1e-300, hi * (1.0 + 1e-12), a, b);
+  if (k == 0 || lane) return;
+  kuni[w] = (int8_t)k;
+  kuni[(size_t)Q * nb + P] = (int8_t)k;
+  if (k == 4) {
+    atomicMin(dmin4, (unsigned long long)__double_as_longlong(Dmin));
+    if (tflag[Q]) run[P] = 1;
+  }
+}
+
 __global__ void jmax_kernel(DevMesh m, unsigned long long* __restrict__ jmax) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < m.nc) atomicMax(jmax, (unsigned long long)__double_as_longlong(m.geo[c].J));
@@ -489,6 +519,15 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
   tail_kuni_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(oc, B.bstat.p, tflag.p, nb, mixed ? 1 : 0, kuni.p,
                                                                  red.p, run.p),
       note_launch();
+  // FRACLAP_EXACT_RANGE=0: circle bounds only (round-2 behaviour before the exact ranges)
+  static const bool exact_range = [] {
+    const char* v = getenv("FRACLAP_EXACT_RANGE");
+    return !(v && std::string(v) == "0");
+  }();
+  if (exact_range && !mixed)
+    tail_refine_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, st>>>(oc, m, B.bcells.p, B.bstat.p, tflag.p, nb,
+                                                                          kuni.p, red.p, run.p),
+        note_launch();
   jmax_kernel<<<(m.nc + 255) / 256, 256, 0, st>>>(m, red.p + 1), note_launch();
   unsigned long long hred[2];
   FL_CUDA(cudaMemcpyAsync(hred, red.p, sizeof(hred), cudaMemcpyDeviceToHost, st));
