@@ -32,7 +32,22 @@ constexpr int TAIL_WIN = 256;
 constexpr int TAIL_U = FL_TAIL_U;   // source nodes per lane per step
 constexpr int TAIL_T = 2;           // target nodes per lane
 
-template <int D, int E4>
+// Block-ordered, node-major staging arrays of the mapped disjoint-rule nodes (node r of slot c of
+// block Q at [r * 32 + c] of the order's segment): orders 2-4 in Blocks2D::un (shared with the cross
+// term), orders 5-9 in the tail's own array uhi (fl_tail2d.cu, hi_nodes_kernel)
+__device__ __forceinline__ const double2* staged_nodes(const double2* __restrict__ un, const double2* __restrict__ uhi,
+                                                       int Q, int k) {
+  return k <= 4 ? un + (size_t)Q * UNODES2D + (k == 2 ? 0 : (k == 3 ? 128 : 416))
+                : uhi + (size_t)Q * UHI2D + uhi_seg(k);
+}
+
+// FOLD (2D, behind the block kernel): the source weight J w is folded into the staged coordinates —
+// s_jw = sc = (J w)^(1/(2 ex)) (cell factor ujh per block slot, rule factor wh per node), s_y =
+// -sc (y - c_K) with c_K the target cell's centroid, targets held as x - c_K — so that
+// d' = fma(x', sc, s_y) = sc (x - y), r2' = |d'|^2 = (J w)^(1/ex) r2 and (J w) r2^ex = r2'^ex is added
+// by kpow_acc: 10 FP64 instructions per evaluation instead of 11.  Centring on the target cell keeps
+// the cancellation factor |y - c_K| / |x - y| of a non-touching pair to a few units.
+template <int D, int E4, bool FOLD>
 __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(DevMesh m, const double* __restrict__ tab,
                                                                   DevTables dir, OrderConsts oc, double ex,
                                                                   const int* __restrict__ targets, int ntargets,
@@ -43,7 +58,11 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
                                                                   const int* __restrict__ bcells, int nb,
                                                                   const int8_t* __restrict__ kcell,
                                                                   const unsigned long long* __restrict__ psifx,
-                                                                  double fxinv) {
+                                                                  double fxinv,
+                                                                  const double* __restrict__ ujh,
+                                                                  const double* __restrict__ wh,
+                                                                  const double2* __restrict__ un,
+                                                                  const double2* __restrict__ uhi) {
   constexpr int Q = (D == 1) ? 6 : 16;     // cell quadrature nodes (XQ_ORDER)
   constexpr int L = Q / TAIL_T;            // lanes per group (8 in 2D, 3 in 1D)
   constexpr int G = 32 / L;                // groups sweeping disjoint source nodes (4 / 10)
@@ -69,6 +88,10 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
     const int q = j + t * L;
     x0[t] = active ? m.X[((size_t)K * Q + q) * D + 0] : 0.0;
     x1[t] = (active && D == 2) ? m.X[((size_t)K * Q + q) * D + 1] : 0.0;
+    if (FOLD) {
+      x0[t] -= A.cx;
+      x1[t] -= A.cy;
+    }
   }
   double acc[TAIL_T][2] = {};
   unsigned long long nodes = 0;
@@ -113,7 +136,72 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
         s_src[w][3][lane] = B.p[1][1] - B.p[0][1];
         s_src[w][4][lane] = B.p[2][0] - B.p[0][0];
         s_src[w][5][lane] = B.p[2][1] - B.p[0][1];
-        s_src[w][6][lane] = B.J;
+        s_src[w][6][lane] = FOLD ? ujh[ci * 32 + lane] : B.J;
+      }
+    }
+    // the warp's evaluation of one staged window: G groups of L lanes sweep disjoint nodes
+    auto eval_window = [&](int cntp) {
+      if (!active) return;
+#pragma unroll 1
+      for (int p = g; p < cntp; p += STEP) {
+        double2 y[TAIL_U];
+        double jw[TAIL_U];
+#pragma unroll
+        for (int u = 0; u < TAIL_U; ++u) {
+          y[u] = s_y[w][p + u * G];
+          jw[u] = s_jw[w][p + u * G];
+        }
+#pragma unroll
+        for (int t = 0; t < TAIL_T; ++t) {
+#pragma unroll
+          for (int u = 0; u < TAIL_U; ++u) {
+            if (FOLD) {
+              const double e0 = fma(x0[t], jw[u], y[u].x), e1 = fma(x1[t], jw[u], y[u].y);
+              acc[t][u & 1] = kpow_acc<E4>(fma(e1, e1, e0 * e0), ex, acc[t][u & 1]);
+              continue;
+            }
+            const double d0 = x0[t] - y[u].x;
+            double r2;
+            if (D == 1) {
+              r2 = d0 * d0;
+            } else {
+              const double d1 = x1[t] - y[u].y;
+              r2 = fma(d1, d1, d0 * d0);
+            }
+            acc[t][u & 1] = fma(jw[u], kpow<E4>(r2, ex), acc[t][u & 1]);
+          }
+        }
+      }
+    };
+    if (FOLD) {
+      // one order for every cell of the source block (and none touching K): the block's mapped
+      // nodes lie node-major in the staging arrays, so the lanes copy them coalesced, 8 nodes of
+      // every cell per window, each lane its own slot's weight factor
+      const bool slot_ok = src >= 0;
+      const unsigned act = __ballot_sync(0xffffffffu, nn > 0);
+      const int k0 = __shfl_sync(0xffffffffu, k, act ? __ffs(act) - 1 : 0);
+      if (act && __all_sync(0xffffffffu, slot_ok ? (nn > 0 && k == k0) : true)) {
+        const int kk = k0 * k0;
+        const double Jh = slot_ok ? s_src[w][6][lane] : 0.0;
+        const double2* __restrict__ ub = staged_nodes(un, uhi, ci, k0) + lane;
+        const double* __restrict__ whk = wh + disj_roff(k0);
+        nodes += (unsigned long long)__popc(act) * kk;
+        __syncwarp();
+        for (int rb = 0; rb < kk; rb += TAIL_WIN / 32) {
+          const int nr = min(TAIL_WIN / 32, kk - rb);
+#pragma unroll 4
+          for (int r = 0; r < nr; ++r) {
+            const double2 yv = ub[(rb + r) * 32];
+            const double sc = Jh * __ldg(whk + rb + r);
+            s_y[w][r * 32 + lane] = slot_ok ? make_double2(-sc * (yv.x - A.cx), -sc * (yv.y - A.cy))
+                                            : make_double2(1e150, 1e150);
+            s_jw[w][r * 32 + lane] = slot_ok ? sc : 1.0;
+          }
+          __syncwarp();
+          eval_window(nr * 32);
+          __syncwarp();
+        }
+        continue;
       }
     }
     int incl = nn;
@@ -137,52 +225,37 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
           const double p0x = s_src[w][0][lane], p0y = s_src[w][1][lane];
           const double e00 = s_src[w][2][lane], e01 = s_src[w][3][lane];
           const double e10 = s_src[w][4][lane], e11 = s_src[w][5][lane], J = s_src[w][6][lane];
-          for (int r = r0; r < r1; ++r) {
-            const double* nd = tab + (size_t)(rr.off + r) * NODE;
-            double y0, y1 = 0.0;
-            if (D == 1) {
-              y0 = p0x + nd[0] * e00;
-            } else {
-              y0 = p0x + (nd[0] * e00 + nd[1] * e10);
-              y1 = p0y + (nd[0] * e01 + nd[1] * e11);
+          if (FOLD) {                           // mapped nodes from the staging arrays
+            const double2* __restrict__ ub = staged_nodes(un, uhi, ci, k) + lane;
+            const double* __restrict__ whk = wh + disj_roff(k);
+            for (int r = r0; r < r1; ++r) {
+              const double2 yv = ub[r * 32];
+              const double sc = J * __ldg(whk + r);
+              s_y[w][my0 + r] = make_double2(-sc * (yv.x - A.cx), -sc * (yv.y - A.cy));
+              s_jw[w][my0 + r] = sc;
             }
-            s_y[w][my0 + r] = make_double2(y0, y1);
-            s_jw[w][my0 + r] = J * nd[2];
+          } else {
+            for (int r = r0; r < r1; ++r) {
+              const double* nd = tab + (size_t)(rr.off + r) * NODE;
+              double y0, y1 = 0.0;
+              if (D == 1) {
+                y0 = p0x + nd[0] * e00;
+              } else {
+                y0 = p0x + (nd[0] * e00 + nd[1] * e10);
+                y1 = p0y + (nd[0] * e01 + nd[1] * e11);
+              }
+              s_y[w][my0 + r] = make_double2(y0, y1);
+              s_jw[w][my0 + r] = J * nd[2];
+            }
           }
         }
       }
       for (int idx = cnt + lane; idx < cntp; idx += 32) {      // padding: far away, zero weight
-        s_y[w][idx] = make_double2(1e100, 1e100);
-        s_jw[w][idx] = 0.0;
+        s_y[w][idx] = FOLD ? make_double2(1e150, 1e150) : make_double2(1e100, 1e100);   // folded: sc = 1
+        s_jw[w][idx] = FOLD ? 1.0 : 0.0;
       }
       __syncwarp();
-      if (active) {
-#pragma unroll 1
-        for (int p = g; p < cntp; p += STEP) {
-          double2 y[TAIL_U];
-          double jw[TAIL_U];
-#pragma unroll
-          for (int u = 0; u < TAIL_U; ++u) {
-            y[u] = s_y[w][p + u * G];
-            jw[u] = s_jw[w][p + u * G];
-          }
-#pragma unroll
-          for (int t = 0; t < TAIL_T; ++t) {
-#pragma unroll
-            for (int u = 0; u < TAIL_U; ++u) {
-              const double d0 = x0[t] - y[u].x;
-              double r2;
-              if (D == 1) {
-                r2 = d0 * d0;
-              } else {
-                const double d1 = x1[t] - y[u].y;
-                r2 = fma(d1, d1, d0 * d0);
-              }
-              acc[t][u & 1] = fma(jw[u], kpow<E4>(r2, ex), acc[t][u & 1]);
-            }
-          }
-        }
-      }
+      eval_window(cntp);
       __syncwarp();
     }
   }
@@ -942,16 +1015,28 @@ __global__ void orders_kernel(DevMesh m, OrderConsts oc, int8_t* cross_k, int8_t
     default: { constexpr int E4 = 0; __VA_ARGS__; } break;    \
   }
 
+// FRACLAP_TAIL_FOLD_WARP=0: the warp tail behind the block kernel keeps plain weights (A/B switch)
+static bool tail_fold_warp() {
+  static const bool on = [] {
+    const char* v = getenv("FRACLAP_TAIL_FOLD_WARP");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4,
                  const int* targets, int ntargets, double* psi, unsigned long long* evals, cudaStream_t st,
                  const int8_t* kuni, const int* blk_of, const int* bcells, int nb, const int8_t* kcell,
-                 const unsigned long long* psifx, double fxinv) {
+                 const unsigned long long* psifx, double fxinv, const double* ujh, const double* wh,
+                 const double2* un, const double2* uhi) {
   if (ntargets <= 0) return;
   const int grid = (ntargets + TAIL_WARPS - 1) / TAIL_WARPS;
   if (m.d == 1) {
-    FL_E4_SWITCH(e4, (tail_kernel<1, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<1, E4, false><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr), ::fl::note_launch()));
+  } else if (kuni && ujh && wh && un && uhi && oc.cap_disjoint <= 9 && tail_fold_warp()) {
+    FL_E4_SWITCH(e4, (tail_kernel<2, E4, true><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, kcell, psifx, fxinv, ujh, wh, un, uhi), ::fl::note_launch()));
   } else {
-    FL_E4_SWITCH(e4, (tail_kernel<2, E4><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, kcell, psifx, fxinv), ::fl::note_launch()));
+    FL_E4_SWITCH(e4, (tail_kernel<2, E4, false><<<grid, TAIL_WARPS * 32, 0, st>>>(m, t.data, t, oc, ex, targets, ntargets, psi, evals, kuni, blk_of, bcells, nb, kcell, psifx, fxinv, nullptr, nullptr, nullptr, nullptr), ::fl::note_launch()));
   }
   FL_CHECK_LAUNCH();
 }

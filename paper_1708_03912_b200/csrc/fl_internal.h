@@ -198,7 +198,9 @@ void launch_tail(const DevMesh& m, const DevTables& t, const OrderConsts& oc, do
                  const int* targets, int ntargets, double* psi /*nc*q*/, unsigned long long* evals,
                  cudaStream_t st, const int8_t* kuni = nullptr, const int* blk_of = nullptr,
                  const int* bcells = nullptr, int nb = 0, const int8_t* kcell = nullptr,
-                 const unsigned long long* psifx = nullptr, double fxinv = 0.0);
+                 const unsigned long long* psifx = nullptr, double fxinv = 0.0,
+                 const double* ujh = nullptr, const double* wh = nullptr, const double2* un = nullptr,
+                 const double2* uhi = nullptr);
 void launch_flux(const DevMesh& m, const DevTables& t, double ex, int e4, const int* targets,
                  int ntargets, double* win /*nc*q*/, cudaStream_t st);
 void launch_cross_tiles(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex,
@@ -261,6 +263,11 @@ struct Blocks2D {
   double radmax = 0.0;    // largest cell radius (vertex - centroid)
 };
 constexpr int UNODES2D = 928;
+// the 2D tail's staging array of the orders 5-9: per block 32 * (25 + 36 + 49 + 64 + 81) nodes
+constexpr int UHI2D = 8160;
+__host__ __device__ constexpr int uhi_seg(int k) {
+  return k == 5 ? 0 : (k == 6 ? 800 : (k == 7 ? 1952 : (k == 8 ? 3520 : 5568)));
+}
 
 // Exact range, over the 32 x 32 cell pairs of Morton blocks P and Q, of the distance estimate that
 // select_order is fed (assembly.py:764-781): every pair's estimate lies in [lo, hi] with

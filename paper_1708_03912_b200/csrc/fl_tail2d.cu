@@ -30,9 +30,10 @@ constexpr int TQN = 16;            // target nodes per cell (XQ_ORDER 4 in 2D, a
 constexpr int TT = 256;            // threads per CTA: 2 target nodes each
 constexpr int TWIN = 1024;         // source nodes per shared-memory window
 constexpr int TU = 4;              // source nodes per thread per step
-constexpr int RULE_NODES = 284;    // sum_{k=2}^{9} k^2
+constexpr int RULE_NODES = DISJ_RULE_NODES;   // sum_{k=2}^{9} k^2
+constexpr int RS = 4;              // doubles per staged rule node: u0, u1, w, w^(1/(2 ex))
 __host__ __device__ constexpr int useg(int k) { return k == 2 ? 0 : (k == 3 ? 128 : 416); }   // Blocks2D::un
-__host__ __device__ constexpr int roff(int k) { return (k - 1) * k * (2 * k - 1) / 6 - 1; }   // sum_{j=2}^{k-1} j^2
+__host__ __device__ constexpr int roff(int k) { return disj_roff(k); }   // sum_{j=2}^{k-1} j^2
 
 __global__ void tail_flag_kernel(const int* __restrict__ targets, int ntargets, const int* __restrict__ blk_of,
                                  int* __restrict__ tflag, int* __restrict__ tcell) {
@@ -109,6 +110,49 @@ __global__ void tail_refine_kernel(OrderConsts oc, DevMesh m, const int* __restr
   }
 }
 
+// per block slot J^(1/(2 ex)) (0 for an empty slot): the cell factor of the folded source weights
+// c = (J w)^(1/ex) = (J^(1/(2 ex)) w^(1/(2 ex)))^2 of sweep_fold and of the warp tail's folded path
+__global__ void fold_slots_kernel(DevMesh m, const int* __restrict__ bcells, int nslots, double hex,
+                                  double* __restrict__ ujh) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nslots) return;
+  const int c = bcells[i];
+  ujh[i] = c >= 0 ? pow(m.geo[c].J, hex) : 0.0;
+}
+
+// per node of the disjoint rules k = 2..9: w^(1/(2 ex)) (0 when the rule is missing)
+__global__ void fold_rules_kernel(const double* __restrict__ tab, DevTables dir, double hex, double* __restrict__ wh) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= RULE_NODES) return;
+  int k = 2;
+  while (roff(k + 1) <= i) ++k;
+  const RuleRef rr = dir.rule(T_DISJ, k);
+  wh[i] = rr.cnt == k * k ? pow(tab[(size_t)(rr.off + i - roff(k)) * NODE + 2], hex) : 0.0;
+}
+
+// mapped nodes of the disjoint rules k = 5..9 for every block slot, node-major per order (the warp
+// tail copies them instead of mapping them per (target, source) pair); the mapping is _map_points'
+// y = P0 + u0 (P1 - P0) + u1 (P2 - P0) in the warp tail's own operation order
+__global__ void hi_nodes_kernel(DevMesh m, const int* __restrict__ bcells, int nb, const double* __restrict__ tab,
+                                DevTables dir, double2* __restrict__ uhi) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nb * UHI2D) return;
+  const int b = (int)(i / UHI2D), x = (int)(i % UHI2D);
+  int k = 5;
+  while (k < 9 && uhi_seg(k + 1) <= x) ++k;
+  const int loc = x - uhi_seg(k), r = loc / TB, c = loc % TB;
+  const int cell = bcells[b * TB + c];
+  const RuleRef rr = dir.rule(T_DISJ, k);
+  double2 y = make_double2(0.0, 0.0);
+  if (cell >= 0 && rr.cnt == k * k) {
+    const CellGeo& g = m.geo[cell];
+    const double* nd = tab + (size_t)(rr.off + r) * NODE;
+    y.x = g.p[0][0] + (nd[0] * (g.p[1][0] - g.p[0][0]) + nd[1] * (g.p[2][0] - g.p[0][0]));
+    y.y = g.p[0][1] + (nd[0] * (g.p[1][1] - g.p[0][1]) + nd[1] * (g.p[2][1] - g.p[0][1]));
+  }
+  uhi[i] = y;
+}
+
 __global__ void jmax_kernel(DevMesh m, unsigned long long* __restrict__ jmax) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < m.nc) atomicMax(jmax, (unsigned long long)__double_as_longlong(m.geo[c].J));
@@ -137,7 +181,9 @@ __global__ void tail_kcell_kernel(OrderConsts oc, DevMesh m, const int* __restri
 }
 
 // geometry field f of cell slot c of block Q: P0x P0y (P1-P0)x (P1-P0)y (P2-P0)x (P2-P0)y J valid
-__device__ __forceinline__ double geo_field(const DevMesh& m, const int* __restrict__ bcells, int Q, int t) {
+// (the last field is J^(1/(2 ex)) of the folded weights, nonzero exactly for a valid slot)
+__device__ __forceinline__ double geo_field(const DevMesh& m, const int* __restrict__ bcells,
+                                            const double* __restrict__ ujh, int Q, int t) {
   const int c = bcells[Q * TB + (t >> 3)], f = t & 7;
   if (c < 0) return 0.0;
   const CellGeo& g = m.geo[c];
@@ -149,7 +195,7 @@ __device__ __forceinline__ double geo_field(const DevMesh& m, const int* __restr
     case 4: return g.p[2][0] - g.p[0][0];
     case 5: return g.p[2][1] - g.p[0][1];
     case 6: return g.J;
-    default: return 1.0;
+    default: return ujh[Q * TB + (t >> 3)];
   }
 }
 
@@ -178,6 +224,32 @@ __device__ __forceinline__ void sweep(const double2* __restrict__ sM, const doub
       for (int u = 0; u < TU; ++u) {
         const double r2 = fma(x0[t], my[u].x, fma(x1[t], my[u].y, xx[t] + qw[u].x));
         acc[t][u & 1] = fma(qw[u].y, kpow<E4>(r2, ex), acc[t][u & 1]);
+      }
+  }
+}
+
+// The same sweep with the source weight folded into the staged coordinates (kpow_acc): sM = -2 c y',
+// sQ = (c |y'|^2, c), c = (J w)^(1/ex), so r2' = c r2 = fma(x0', sM.x, fma(x1', sM.y, fma(|x'|^2, c,
+// sQ.x))) and (J w) r2^ex = r2'^ex is added with the fused correction: 9 FP64 instructions per
+// evaluation instead of 10.  Padding nodes sit at 1e150 with c = 1: their term underflows to an exact 0.
+template <int E4>
+__device__ __forceinline__ void sweep_fold(const double2* __restrict__ sM, const double2* __restrict__ sQ, int nwp,
+                                           const double (&x0)[2], const double (&x1)[2], const double (&xx)[2],
+                                           double ex, double (&acc)[2][2]) {
+#pragma unroll 1
+  for (int p = 0; p < nwp; p += TU) {
+    double2 my[TU], qw[TU];
+#pragma unroll
+    for (int u = 0; u < TU; ++u) {
+      my[u] = sM[p + u];             // (-2 c y0', -2 c y1')
+      qw[u] = sQ[p + u];             // (c |y'|^2, c)
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        const double r2 = fma(x0[t], my[u].x, fma(x1[t], my[u].y, fma(xx[t], qw[u].y, qw[u].x)));
+        acc[t][u & 1] = kpow_acc<E4>(r2, ex, acc[t][u & 1]);
       }
   }
 }
@@ -234,7 +306,9 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
                                                             const int8_t* __restrict__ kcell,
                                                             const double* __restrict__ bstat,
                                                             const double2* __restrict__ un,
-                                                            const double* __restrict__ uj, int nb,
+                                                            const double* __restrict__ uj,
+                                                            const double* __restrict__ ujh,
+                                                            const double* __restrict__ wh, int nb,
                                                             unsigned long long* __restrict__ psifx, double fxscale,
                                                             double* __restrict__ psi,
                                                             unsigned long long* __restrict__ evals,
@@ -242,8 +316,8 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* sM = reinterpret_cast<double2*>(smem_raw);          // TWIN source nodes: -2 y' (centred)
   double2* sQ = sM + TWIN;                                     // TWIN: |y'|^2, J * w
-  double* sR = reinterpret_cast<double*>(sQ + TWIN);           // RULE_NODES x (u0, u1, w)
-  double* sG = sR + 3 * RULE_NODES;                            // TB x 8 geometry fields
+  double* sR = reinterpret_cast<double*>(sQ + TWIN);           // RULE_NODES x (u0, u1, w, w^(1/(2 ex)))
+  double* sG = sR + RS * RULE_NODES;                           // TB x 8 geometry fields
   double* colbuf = sG + 8 * TB;                                // [8 warps][512] sym4 column partials
   int* sL = reinterpret_cast<int*>(colbuf + (TT / 32) * (TWIN / 2));   // source blocks: Q | (k & 0xff) << 24
   __shared__ int s_wsum[TT / 32];
@@ -260,9 +334,10 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     const int r = i - roff(k);
     if (rr.cnt == k * k) {
       const double* nd = tab + (size_t)(rr.off + r) * NODE;
-      sR[3 * i] = nd[0]; sR[3 * i + 1] = nd[1]; sR[3 * i + 2] = nd[2];
+      sR[RS * i] = nd[0]; sR[RS * i + 1] = nd[1]; sR[RS * i + 2] = nd[2];
+      sR[RS * i + 3] = wh[i];
     } else {
-      sR[3 * i] = sR[3 * i + 1] = sR[3 * i + 2] = 0.0;
+      sR[RS * i] = sR[RS * i + 1] = sR[RS * i + 2] = sR[RS * i + 3] = 0.0;
     }
   }
   // ---- the source blocks of P handled here (uniform or mixed), ascending (ordered compaction)
@@ -304,7 +379,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   }
   double wt[2];                      // J_K w_q of the thread's targets (sym4 column sums; 0: no target)
 #pragma unroll
-  for (int t = 0; t < 2; ++t) wt[t] = Kv >= 0 ? m.geo[Kv].J * sR[3 * (roff(4) + q0 + 8 * t) + 2] : 0.0;
+  for (int t = 0; t < 2; ++t) wt[t] = Kv >= 0 ? m.geo[Kv].J * sR[RS * (roff(4) + q0 + 8 * t) + 2] : 0.0;
   int ntv = 0, nvp = 0;              // target cells / cells of the block (evaluation counts)
   if (tid == 0)
     for (int c = 0; c < TB; ++c) {
@@ -325,28 +400,39 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
   auto is_fast = [&](int qi) { return qi < nq && kof(qi) >= 2 && kof(qi) <= 4; };
   double2 py[2];
   double pj[2];
+  // a sym4 pair keeps plain weights J w (its kernel values also feed the column sums); every
+  // other block is staged with the weight folded into the coordinates (sweep_fold)
   auto prefetch = [&](int qi) {
     const int Q = sL[qi] & 0xffffff, k = kof(qi), nn = TB * k * k;
+    const double* __restrict__ jsrc = sym4_mode(P, Q, k) > 0 ? uj : ujh;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const int idx = tid + TT * t;
       if (idx < nn) {
         py[t] = un[(size_t)Q * UNODES2D + useg(k) + idx];
-        pj[t] = uj[(size_t)Q * TB + (idx & (TB - 1))];
+        pj[t] = jsrc[(size_t)Q * TB + (idx & (TB - 1))];
       }
     }
   };
   auto put_nodes = [&](int qi, int half) {
     const int k = kof(qi), kk = k * k, nn = TB * kk;
-    const double* R = sR + 3 * roff(k);
+    const double* R = sR + RS * roff(k);
+    const bool sy4 = sym4_mode(P, sL[qi] & 0xffffff, k) > 0;
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const int idx = tid + TT * t;
       if (idx < nn) {
         const bool ok = pj[t] != 0.0;            // an empty slot of a partial block: far, weight 0
-        const double yx = (ok ? py[t].x : 1e100) - ccx, yy = (ok ? py[t].y : 1e100) - ccy;
-        sM[half * (TWIN / 2) + idx] = make_double2(-2.0 * yx, -2.0 * yy);
-        sQ[half * (TWIN / 2) + idx] = make_double2(fma(yy, yy, yx * yx), pj[t] * R[3 * (idx >> 5) + 2]);
+        if (sy4) {
+          const double yx = (ok ? py[t].x : 1e100) - ccx, yy = (ok ? py[t].y : 1e100) - ccy;
+          sM[half * (TWIN / 2) + idx] = make_double2(-2.0 * yx, -2.0 * yy);
+          sQ[half * (TWIN / 2) + idx] = make_double2(fma(yy, yy, yx * yx), pj[t] * R[RS * (idx >> 5) + 2]);
+        } else {
+          const double yx = (ok ? py[t].x : 1e150) - ccx, yy = (ok ? py[t].y : 1e150) - ccy;
+          const double sc = pj[t] * R[RS * (idx >> 5) + 3], c = ok ? sc * sc : 1.0;
+          sM[half * (TWIN / 2) + idx] = make_double2(-2.0 * c * yx, -2.0 * c * yy);
+          sQ[half * (TWIN / 2) + idx] = make_double2(c * fma(yy, yy, yx * yx), c);
+        }
       }
     }
     if (wid == 0) {                              // evaluation count: valid source cells (lanes = row 0)
@@ -378,7 +464,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
         sweep_sym<E4>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * 16, x0, x1, xx, wt, ex, acc,
                       colbuf + wid * (TWIN / 2), lane);
       else
-        sweep<E4, false>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * kq * kq, x0, x1, xx, 1.0, ex, acc);
+        sweep_fold<E4>(sM + half * (TWIN / 2), sQ + half * (TWIN / 2), TB * kq * kq, x0, x1, xx, ex, acc);
       if (nf) put_nodes(qi + 1, half ^ 1);
       __syncthreads();
       if (sym) {
@@ -401,7 +487,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
     }
     staged = false;
     // general path: order >= 5 (windows) or per-target-cell orders; geometry through sG
-    sG[tid] = geo_field(m, bcells, Q, tid);
+    sG[tid] = geo_field(m, bcells, ujh, Q, tid);
     if (kq < 0 && tid < TB) s_kc[tid] = Kw_t ? (int)kcell[(size_t)Kw * nb + Q] : 0;
     __syncthreads();
     unsigned kset;                   // bit k: some target cell takes order k from this block here
@@ -425,27 +511,34 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
       // whose own cell is at another order adds exact zeros (weight 0)
       const bool wact = __any_sync(0xffffffffu, kmine == k);
       const double wsel = kmine == k ? 1.0 : 0.0;
-      const double* R = sR + 3 * roff(k);
+      const double* R = sR + RS * roff(k);
       const int cpw = TWIN / kk;     // cells per window (>= 12)
       for (int c0 = 0; c0 < TB; c0 += cpw) {
         const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + TU - 1) / TU * TU;
         if (c0 > 0 || ks != kset) __syncthreads();
+        const double far = kq > 0 ? 1e150 : 1e100;
         for (int idx = tid; idx < nwp; idx += TT) {
-          double2 y = make_double2(1e100, 1e100);   // padding: far away, weight 0
-          double w = 0.0;
+          double2 y = make_double2(far, far);       // padding: far away, weight 0 (folded: c = 1)
+          double w = kq > 0 ? 1.0 : 0.0;
           if (idx < nw) {
             const int c = c0 + idx / kk, r = idx - (idx / kk) * kk;
             const double* g = sG + 8 * c;
             if (g[7] != 0.0) {
-              const double u0 = R[3 * r], u1 = R[3 * r + 1];
+              const double u0 = R[RS * r], u1 = R[RS * r + 1];
               y.x = g[0] + (u0 * g[2] + u1 * g[4]);
               y.y = g[1] + (u0 * g[3] + u1 * g[5]);
-              w = g[6] * R[3 * r + 2];
+              const double sc = g[7] * R[RS * r + 3];
+              w = kq > 0 ? sc * sc : g[6] * R[RS * r + 2];
             }
           }
           const double yx = y.x - ccx, yy = y.y - ccy;
-          sM[idx] = make_double2(-2.0 * yx, -2.0 * yy);
-          sQ[idx] = make_double2(fma(yy, yy, yx * yx), w);
+          if (kq > 0) {                             // uniform order: weight folded (sweep_fold)
+            sM[idx] = make_double2(-2.0 * w * yx, -2.0 * w * yy);
+            sQ[idx] = make_double2(w * fma(yy, yy, yx * yx), w);
+          } else {
+            sM[idx] = make_double2(-2.0 * yx, -2.0 * yy);
+            sQ[idx] = make_double2(fma(yy, yy, yx * yx), w);
+          }
         }
         if (tid == 0) {
           int nvs = 0;
@@ -454,7 +547,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
         }
         __syncthreads();
         if (!wact) continue;
-        if (kq > 0) sweep<E4, false>(sM, sQ, nwp, x0, x1, xx, 1.0, ex, acc);
+        if (kq > 0) sweep_fold<E4>(sM, sQ, nwp, x0, x1, xx, ex, acc);
         else sweep<E4, true>(sM, sQ, nwp, x0, x1, xx, wsel, ex, acc);
       }
     }
@@ -487,7 +580,7 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
                           cudaEvent_t e0, cudaEvent_t e1, unsigned long long* evals_sym) {
   if (ntargets <= 0) return;
   const int nb = B.nb;
-  const size_t smem = (size_t)TWIN * 32 + (size_t)(TT / 32) * (TWIN / 2) * 8 + (size_t)3 * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
+  const size_t smem = (size_t)TWIN * 32 + (size_t)(TT / 32) * (TWIN / 2) * 8 + (size_t)RS * RULE_NODES * 8 + (size_t)8 * TB * 8 + (size_t)nb * 4;
   if (m.d != 2 || m.q != TQN || smem > 200 * 1024) {      // out of this path's shape: pair by pair
     launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st);
     return;
@@ -553,18 +646,30 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
                                                                     B.bstat.p, nb, kcell.p),
         note_launch();
   }
+  const double hex = 0.5 / ex;         // exponent of the folded weight factors
+  DBuf<double> ujh((size_t)nb * TB);
+  DBuf<double> wh(RULE_NODES);
+  fold_slots_kernel<<<(nb * TB + 255) / 256, 256, 0, st>>>(m, B.bcells.p, nb * TB, hex, ujh.p), note_launch();
+  fold_rules_kernel<<<(RULE_NODES + 255) / 256, 256, 0, st>>>(t.data, t, hex, wh.p), note_launch();
+  // orders 5-9 staged for the warp tail (130 KB per block; skipped beyond 8 GB: it then maps per pair)
+  DBuf<double2> uhi;
+  if ((size_t)nb * UHI2D * sizeof(double2) <= ((size_t)8 << 30) && oc.cap_disjoint <= 9) {
+    uhi.alloc((size_t)nb * UHI2D);
+    hi_nodes_kernel<<<(unsigned)(((int64_t)nb * UHI2D + 255) / 256), 256, 0, st>>>(m, B.bcells.p, nb, t.data, t, uhi.p),
+        note_launch();
+  }
   if (e0) FL_CUDA(cudaEventRecord(e0, st));
   FL_E4_SWITCH_T(e4, {
     FL_CUDA(cudaFuncSetAttribute(tail2d_block_kernel<E4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tail2d_block_kernel<E4><<<nb, TT, smem, st>>>(m, t.data, t, oc, ex, kuni.p, tflag.p, run.p, tcell.p, B.bcells.p,
-                                                  kcell.p, B.bstat.p, B.un.p, B.uj.p, nb, psifx.p, fxscale, psi,
+                                                  kcell.p, B.bstat.p, B.un.p, B.uj.p, ujh.p, wh.p, nb, psifx.p, fxscale, psi,
                                                   evals_block ? evals_block : evals, evals_sym),
         note_launch();
   });
   FL_CHECK_LAUNCH();
   if (e1) FL_CUDA(cudaEventRecord(e1, st));
   launch_tail(m, t, oc, ex, e4, targets, ntargets, psi, evals, st, kuni.p, B.blk_of.p, B.bcells.p, nb, kcell.p,
-              psifx.p, 1.0 / fxscale);
+              psifx.p, 1.0 / fxscale, ujh.p, wh.p, B.un.p, uhi.p);
 }
 
 }  // namespace fl
