@@ -203,6 +203,43 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
         }
         continue;
       }
+      // mixed orders (or touching cells in the block): rounds of up to 8 nodes per cell, the
+      // nodes of a round packed node-major (ballot ranks), so every lane stages in every round
+      // and a window never exceeds 256 nodes
+      const int nmax = __reduce_max_sync(0xffffffffu, nn);
+      const double Jh = nn > 0 ? s_src[w][6][lane] : 0.0;
+      const int ks = nn > 0 ? k : 2;
+      const double2* __restrict__ ub = staged_nodes(un, uhi, ci, ks) + lane;
+      const double* __restrict__ whk = wh + disj_roff(ks);
+      const unsigned lt = (1u << lane) - 1u;
+      __syncwarp();
+      for (int rb = 0; rb < nmax; rb += TAIL_WIN / 32) {
+        const int c = min(TAIL_WIN / 32, nn - rb), cm = min(TAIL_WIN / 32, nmax - rb);
+        int tot = 0;
+#pragma unroll 4
+        for (int r = 0; r < cm; ++r) {
+          const bool on = r < c;
+          const unsigned bal = __ballot_sync(0xffffffffu, on);
+          if (on) {
+            const double2 yv = ub[(rb + r) * 32];
+            const double sc = Jh * __ldg(whk + rb + r);
+            const int pos = tot + __popc(bal & lt);
+            s_y[w][pos] = make_double2(-sc * (yv.x - A.cx), -sc * (yv.y - A.cy));
+            s_jw[w][pos] = sc;
+          }
+          tot += __popc(bal);
+        }
+        nodes += (unsigned long long)tot;
+        const int cntp = (tot + STEP - 1) / STEP * STEP;
+        for (int idx = tot + lane; idx < cntp; idx += 32) {      // padding: far away, sc = 1
+          s_y[w][idx] = make_double2(1e150, 1e150);
+          s_jw[w][idx] = 1.0;
+        }
+        __syncwarp();
+        eval_window(cntp);
+        __syncwarp();
+      }
+      continue;
     }
     int incl = nn;
 #pragma unroll
@@ -225,16 +262,7 @@ __global__ void __launch_bounds__(TAIL_WARPS * 32, FL_TAIL_MINB) tail_kernel(Dev
           const double p0x = s_src[w][0][lane], p0y = s_src[w][1][lane];
           const double e00 = s_src[w][2][lane], e01 = s_src[w][3][lane];
           const double e10 = s_src[w][4][lane], e11 = s_src[w][5][lane], J = s_src[w][6][lane];
-          if (FOLD) {                           // mapped nodes from the staging arrays
-            const double2* __restrict__ ub = staged_nodes(un, uhi, ci, k) + lane;
-            const double* __restrict__ whk = wh + disj_roff(k);
-            for (int r = r0; r < r1; ++r) {
-              const double2 yv = ub[r * 32];
-              const double sc = J * __ldg(whk + r);
-              s_y[w][my0 + r] = make_double2(-sc * (yv.x - A.cx), -sc * (yv.y - A.cy));
-              s_jw[w][my0 + r] = sc;
-            }
-          } else {
+          {
             for (int r = r0; r < r1; ++r) {
               const double* nd = tab + (size_t)(rr.off + r) * NODE;
               double y0, y1 = 0.0;
