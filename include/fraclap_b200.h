@@ -377,7 +377,8 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
 /* The device's specialised kernel power on n host values (parity of the building block every
  * quadrature uses): d = 2: x = r2, out = r2^(-(1+s)); d = 1: x = |x - y| (the 1D far field
  * works on the distance itself), out = |x - y|^(-(1+2s)); d = 11: x = r2 with the 1D exponent,
- * out = r2^(-(1/2+s)) (the 1D singular rules). */
+ * out = r2^(-(1/2+s)) (the 1D singular rules); d = 12: the 2D power through the fused
+ * accumulate form of the tail kernels (0 + r2^(-(1+s)), kpow_acc). */
 int32_t fl_debug_kpow(int32_t d, double s, const double* x, int64_t n, double* out, int32_t device);
 /* Measured FP64 FMA peak of the device (TFLOP/s), the roofline denominator of assembly. */
 int32_t fl_probe_fp64_peak(int32_t device, double* tflops);

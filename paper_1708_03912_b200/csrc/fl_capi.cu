@@ -1453,14 +1453,14 @@ int32_t fl_debug_order_hist(const fl_mesh* mesh, const fl_dofmap* dofmap, const 
 
 int32_t fl_debug_kpow(int32_t d, double s, const double* r2, int64_t n, double* out, int32_t device) {
   FL_API_BEGIN
-  if (!r2 || !out || n < 0 || (d != 1 && d != 2 && d != 11)) return fail(FL_E_ARG, "bad argument");
+  if (!r2 || !out || n < 0 || (d != 1 && d != 2 && d != 11 && d != 12)) return fail(FL_E_ARG, "bad argument");
   FL_CUDA(cudaSetDevice(device));
   OwnedStream os_;
   cudaStream_t st = os_.s;
   StreamScope scope(st);
   DBuf<double> a(std::max<int64_t>(n, 1)), b(std::max<int64_t>(n, 1));
   FL_CUDA(cudaMemcpyAsync(a.p, r2, n * sizeof(double), cudaMemcpyHostToDevice, st));
-  const int dd = d == 11 ? 1 : d;
+  const int dd = d == 11 ? 1 : (d == 12 ? 2 : d);
   launch_kpow_probe(d, e4_of(dd, s), a.p, n, -(dd / 2.0 + s), b.p, st);
   FL_CUDA(cudaMemcpyAsync(out, b.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));

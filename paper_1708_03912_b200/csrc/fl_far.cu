@@ -1215,7 +1215,7 @@ namespace fl {
 template <int E4>
 __global__ void kpow_probe_kernel(int d, const double* x, int64_t n, double ex, double* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = d == 1 ? kpow_abs<E4>(x[i], ex) : kpow<E4>(x[i], ex);
+  if (i < n) out[i] = d == 1 ? kpow_abs<E4>(x[i], ex) : (d == 12 ? kpow_acc<E4>(x[i], ex, 0.0) : kpow<E4>(x[i], ex));
 }
 void launch_kpow_probe(int d, int e4, const double* x, int64_t n, double ex, double* out, cudaStream_t st) {
   const int grid = (int)((n + 255) / 256);
