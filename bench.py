@@ -611,7 +611,8 @@ def main():
                            "phases_ms_rank0": {k: stats[k] for k in ("ms_prep", "ms_singular", "ms_tail", "ms_flux",
                                                                      "ms_tiles", "ms_cross", "ms_discover", "ms_near",
                                                                      "ms_cross_compute", "ms_local", "ms_total")},
-                           "near_pairs": stats["near_pairs"], "evals_tail": stats["evals_tail"],
+                           "near_pairs": stats["near_pairs"], "order_ties": stats["order_ties"],
+                           "evals_tail": stats["evals_tail"],
                            "evals_cross": stats["evals_cross"]},
                 "roofline": roof, "roofline_kernels": roofs, "matvec": matvec, "cg": cg, "e2e": e2e,
                 "cpu_baseline": cpu, "extra": extra or None,
