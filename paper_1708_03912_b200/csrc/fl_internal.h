@@ -268,6 +268,10 @@ constexpr int UHI2D = 8160;
 __host__ __device__ constexpr int uhi_seg(int k) {
   return k == 5 ? 0 : (k == 6 ? 800 : (k == 7 ? 1952 : (k == 8 ? 3520 : 5568)));
 }
+static_assert(uhi_seg(6) == 32 * 25 && uhi_seg(7) == uhi_seg(6) + 32 * 36 && uhi_seg(8) == uhi_seg(7) + 32 * 49 &&
+                  uhi_seg(9) == uhi_seg(8) + 32 * 64 && UHI2D == uhi_seg(9) + 32 * 81,
+              "uhi segments: 32 k^2 nodes per order");
+static_assert(disj_roff(2) == 0 && disj_roff(3) == 4 && disj_roff(10) == DISJ_RULE_NODES, "disjoint rule offsets");
 
 // Exact range, over the 32 x 32 cell pairs of Morton blocks P and Q, of the distance estimate that
 // select_order is fed (assembly.py:764-781): every pair's estimate lies in [lo, hi] with
