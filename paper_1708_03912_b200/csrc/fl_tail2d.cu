@@ -30,6 +30,10 @@ constexpr int TQN = 16;            // target nodes per cell (XQ_ORDER 4 in 2D, a
 constexpr int TT = 256;            // threads per CTA: 2 target nodes each
 constexpr int TWIN = 1024;         // source nodes per shared-memory window
 constexpr int TU = 4;              // source nodes per thread per step
+#ifndef FL_TUF
+#define FL_TUF 8
+#endif
+constexpr int TUF = FL_TUF;        // ... of the folded sweep (window sizes are multiples of 8)
 constexpr int RULE_NODES = DISJ_RULE_NODES;   // sum_{k=2}^{9} k^2
 constexpr int RS = 4;              // doubles per staged rule node: u0, u1, w, w^(1/(2 ex))
 __host__ __device__ constexpr int useg(int k) { return k == 2 ? 0 : (k == 3 ? 128 : 416); }   // Blocks2D::un
@@ -237,17 +241,17 @@ __device__ __forceinline__ void sweep_fold(const double2* __restrict__ sM, const
                                            const double (&x0)[2], const double (&x1)[2], const double (&xx)[2],
                                            double ex, double (&acc)[2][2]) {
 #pragma unroll 1
-  for (int p = 0; p < nwp; p += TU) {
-    double2 my[TU], qw[TU];
+  for (int p = 0; p < nwp; p += TUF) {
+    double2 my[TUF], qw[TUF];
 #pragma unroll
-    for (int u = 0; u < TU; ++u) {
+    for (int u = 0; u < TUF; ++u) {
       my[u] = sM[p + u];             // (-2 c y0', -2 c y1')
       qw[u] = sQ[p + u];             // (c |y'|^2, c)
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t)
 #pragma unroll
-      for (int u = 0; u < TU; ++u) {
+      for (int u = 0; u < TUF; ++u) {
         const double r2 = fma(x0[t], my[u].x, fma(x1[t], my[u].y, fma(xx[t], qw[u].y, qw[u].x)));
         acc[t][u & 1] = kpow_acc<E4>(r2, ex, acc[t][u & 1]);
       }
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(TT, 2) tail2d_block_kernel(DevMesh m, const do
       const double* R = sR + RS * roff(k);
       const int cpw = TWIN / kk;     // cells per window (>= 12)
       for (int c0 = 0; c0 < TB; c0 += cpw) {
-        const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + TU - 1) / TU * TU;
+        const int c1 = min(TB, c0 + cpw), nw = (c1 - c0) * kk, nwp = (nw + 7) / 8 * 8;
         if (c0 > 0 || ks != kset) __syncthreads();
         const double far = kq > 0 ? 1e150 : 1e100;
         for (int idx = tid; idx < nwp; idx += TT) {

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python tools/assemble_once.py c5 --reps 2 > gpurun_out/r43_base.log 2>&1
+for v in tuf8 tailu8; do
+FRACLAP_B200_LIB=paper_1708_03912_b200/lib/var/$v.so timeout 300 python tools/assemble_once.py c5 --reps 2 > gpurun_out/r43_$v.log 2>&1
+done
