@@ -30,6 +30,16 @@ def make_mesh(kind, N):
         return M.build_graded_interval_mesh(N)
     if kind == "square2d":
         return M.build_unit_square_mesh(N)
+    if kind == "jitter2d":
+        # the unit square with its interior vertices moved by up to 0.3 h and the cells relabelled
+        # at random (seeded): non-uniform diameters, mixed orders, a partial last Morton block
+        base = M.build_unit_square_mesh(N)
+        rng = np.random.default_rng(1000 + N)
+        V = np.array(base.vertices, dtype=np.float64)
+        inner = (V[:, 0] > 1e-12) & (V[:, 0] < 1 - 1e-12) & (V[:, 1] > 1e-12) & (V[:, 1] < 1 - 1e-12)
+        V[inner] += rng.uniform(-0.3 / N, 0.3 / N, size=(int(inner.sum()), 2))
+        cells = np.array(base.cells)[rng.permutation(len(base.cells))]
+        return M.finish_polygon_mesh(V, [tuple(int(v) for v in c) for c in cells])
     raise ValueError(kind)
 
 
