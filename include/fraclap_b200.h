@@ -141,7 +141,7 @@ typedef struct fl_assembly_stats {
    * correctly rounded log; SURVEY.md §8(d) k-flip guard) */
   int64_t order_ties;
   /* 2D cross term: contributions accumulated as integers of 2^-cross_scale_exp (exact, order-free) */
-  int32_t cross_scale_exp, pad2_;
+  int32_t cross_scale_exp, cross_fallback; /* cross_fallback = 1: the 2D fixed-point cross accumulation was too coarse for this mesh, the DoF-tile kernel assembled the cross term */
   /* 2D: the part of evals_tail done by the block-pair tail kernel and its device ms; the part of
    * evals_cross done by the near blocks (k >= 5, ms_near) */
   double evals_tail_block, ms_tail_block, evals_near;

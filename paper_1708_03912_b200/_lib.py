@@ -86,7 +86,7 @@ class fl_assembly_stats(C.Structure):
                 ("ms_local", C.c_double), ("ms_total", C.c_double), ("cross_tile_pairs", C.c_int64),
                 ("ncolors", C.c_int32), ("ntiles", C.c_int32), ("ms_discover", C.c_double),
                 ("ms_near", C.c_double), ("ms_cross_compute", C.c_double), ("near_pairs", C.c_int64),
-                ("order_ties", C.c_int64), ("cross_scale_exp", C.c_int32), ("pad2_", C.c_int32),
+                ("order_ties", C.c_int64), ("cross_scale_exp", C.c_int32), ("cross_fallback", C.c_int32),
                 ("evals_tail_block", C.c_double), ("ms_tail_block", C.c_double), ("evals_near", C.c_double),
                 ("evals_tail_sym", C.c_double)]
 

@@ -636,7 +636,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
         if (x) cudaEventDestroy(x);
     }
   } tbev;
-  if (d == 2) build_blocks2d(m, U.t, (int)row_begin, (int)row_end, blocks, st);
+  if (d == 2) build_blocks2d(m, U.t, -2.0 * ex, (int)row_begin, (int)row_end, blocks, st);
   if (!early_tail) {
     tm.mark();  // 2
     // tail at the nodes of the target cells (banded 1D: per band, below)
@@ -740,6 +740,15 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
                      xev[0], xev[1], st, evc.p + 3);
     ntiles = -1;
     done1d = true;
+    if (x2.fallback) {
+      // the mesh is too irregular for the fixed-point accumulation (Cross2DInfo::fallback): nothing
+      // was added to A; the DoF-tile kernel below assembles the cross term (its own near pairs)
+      done1d = false;
+      cudaEventDestroy(xev[0]);
+      cudaEventDestroy(xev[1]);
+      FL_CUDA(cudaMemsetAsync(evc.p + 1, 0, sizeof(unsigned long long), st));
+      FL_CUDA(cudaMemsetAsync(evc.p + 3, 0, sizeof(unsigned long long), st));
+    }
   }
   if (!done1d) {
     cudaEventCreate(&xev[0]);
@@ -751,7 +760,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     TilePairs tps;
     build_tile_pairs(m, oc, trow, full ? trow : tcol, full, d == 1 ? KW1D : KW2D, tps, st);
     ntp = tps.nall;
-    if (d != 1) tm.mark();  // 5 (1D fallback: already marked)
+    if (d != 1 && !x2.fallback) tm.mark();  // 5 (1D fallback / 2D fixed-point fallback: already marked)
     // pass 1 (discovery): orders of the pairs of the tile pairs that can hold near pairs (order
     // >= KW, by the tile bound); near pairs are recorded.  Near-key list (with halo duplicates):
     // generous, bounded by a quarter of the free memory
@@ -866,6 +875,7 @@ static int32_t assemble_impl(const fl_mesh* mesh, const fl_dofmap* dofmap, const
     S.ntiles = 0;
     S.cross_scale_exp = x2.scale_exp;
   }
+  S.cross_fallback = x2.fallback;
   *out = D.release();
   return FL_OK;
   FL_API_END

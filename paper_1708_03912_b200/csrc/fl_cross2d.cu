@@ -23,6 +23,8 @@
 // pair is evaluated twice (the DoF-tile kernel of round 1 recomputed ~1.5x at the halo).
 #include <cstring>
 
+#include <chrono>
+#include <cstdio>
 #include <cub/cub.cuh>
 
 #include "fl_internal.h"
@@ -186,7 +188,8 @@ __global__ void cell_nodes2_kernel(DevMesh m, const double* __restrict__ tab, Ru
 // whose outer cell is in that ring), so dmin = min over K of the exact distance to its
 // second-ring disjoint cells bounds every disjoint pair's node distance from below.
 __global__ void dmin_kernel(DevMesh m, unsigned long long* __restrict__ dmin_bits,
-                            unsigned long long* __restrict__ jmax_bits, unsigned long long* __restrict__ rmax_bits) {
+                            unsigned long long* __restrict__ jmax_bits, unsigned long long* __restrict__ rmax_bits,
+                            double e, unsigned long long* __restrict__ beta_bits) {
   const int K = blockIdx.x * blockDim.x + threadIdx.x;
   if (K >= m.nc) return;
   const CellGeo& A = m.geo[K];
@@ -207,7 +210,14 @@ __global__ void dmin_kernel(DevMesh m, unsigned long long* __restrict__ dmin_bit
       }
     }
   }
-  if (best < 1e300) atomicMin(dmin_bits, (unsigned long long)__double_as_longlong(best));
+  // beta = max over the cells of J_K^2 d_K^(-(d+2s)), d_K = best: a disjoint pair (K, L) lies at least
+  // max(d_K, d_L) apart (the segment between them leaves the star of either cell through its second
+  // ring), so J_K J_L dist^(-e) <= sqrt(J_K^2 d_K^(-e) J_L^2 d_L^(-e)) <= beta — tighter than
+  // Jmax^2 dmin^(-e) on graded meshes
+  if (best < 1e300) {
+    atomicMin(dmin_bits, (unsigned long long)__double_as_longlong(best));
+    atomicMax(beta_bits, (unsigned long long)__double_as_longlong(A.J * A.J * pow(best, -e)));
+  }
   atomicMax(jmax_bits, (unsigned long long)__double_as_longlong(A.J));
 }
 
@@ -273,6 +283,13 @@ __global__ void cross_refine_kernel(OrderConsts oc, DevMesh m, const int* __rest
   if (k == 0 || lane) return;
   pairs[w].z = k;
   nearflag[w] = k >= KW2D ? 1 : 0;
+}
+
+__global__ void clear_kuni_kernel(int4* __restrict__ pairs, int* __restrict__ nearflag, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  pairs[i].z = 0;
+  nearflag[i] = 1;          // any pair may hold near pairs: the discovery pass looks at all of them
 }
 
 // 64-bit fixed-point add into a shared-memory tile word with two native 32-bit shared atomics
@@ -365,6 +382,7 @@ __global__ void __launch_bounds__(X2T, FL_X2_MINB) cross2d_kernel(XArgs a, const
   XShared& S = *reinterpret_cast<XShared*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31;
   const OrderConsts& oc = a.oc;
+  if (!DISC && (*a.ovf & 2)) return;             // fixed-point unit too coarse for this mesh (coarse_flag_kernel)
   for (int i = tid; i < NPRE2 * 3; i += X2T) (&S.wl[0][0])[i] = wl_g[i];
   if (tid == 0) S.evals = 0;
   for (;;) {
@@ -768,7 +786,7 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
   for (int i = tid; i < TCAP; i += X2T) S.tile[i] = 0ull;
   if (tid == 0) S.evals = 0;
   int it = blockIdx.x;
-  if (it >= a.nbp) return;
+  if (it >= a.nbp || (*a.ovf & 2)) return;       // (bit 1: unit too coarse, coarse_flag_kernel)
   int4 cur = a.bpairs[it];
   u_stage(a, S.b[0], cur, tid);
   cp_async_commit();
@@ -910,7 +928,7 @@ __global__ void fixed_to_double_kernel(unsigned long long* A, int64_t count, dou
 // overwritten (zeroed first).  Near pairs (k >= KW2D) are discovered here and computed once by
 // near_pairs_build into `near`.  t_disc / t_near: events recorded after discovery and after the
 // near blocks (phase timing).
-void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row_end, Blocks2D& B,
+void build_blocks2d(const DevMesh& m, const DevTables& t, double e, int row_begin, int row_end, Blocks2D& B,
                     cudaStream_t st) {
   const int nc = m.nc;
   const int nb = (nc + CB - 1) / CB;
@@ -953,19 +971,38 @@ void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row
                                                                                     B.slot.p, B.un.p, B.uj.p, B.us.p),
       note_launch();
   // smallest distance of two disjoint cells (second-ring scan), largest Jacobian and cell radius
-  DBuf<unsigned long long> bnd(3);
-  unsigned long long init[3] = {0ull, 0ull, 0ull};
+  DBuf<unsigned long long> bnd(4);
+  unsigned long long init[4] = {0ull, 0ull, 0ull, 0ull};
   const double big = 1e300;
   std::memcpy(&init[0], &big, 8);
   FL_CUDA(cudaMemcpyAsync(bnd.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
-  dmin_kernel<<<(nc + 127) / 128, 128, 0, st>>>(m, bnd.p, bnd.p + 1, bnd.p + 2), note_launch();
-  unsigned long long hb[3];
+  dmin_kernel<<<(nc + 127) / 128, 128, 0, st>>>(m, bnd.p, bnd.p + 1, bnd.p + 2, e, bnd.p + 3), note_launch();
+  unsigned long long hb[4];
   FL_CUDA(cudaMemcpyAsync(hb, bnd.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   std::memcpy(&B.dmin, &hb[0], 8);
   std::memcpy(&B.jmax, &hb[1], 8);
   std::memcpy(&B.radmax, &hb[2], 8);
+  std::memcpy(&B.beta, &hb[3], 8);
   FL_CHECK_LAUNCH();
+}
+
+// largest |entry| of the near blocks (already scaled by J_K J_L)
+__global__ void absmax_kernel(const double* __restrict__ G, int64_t n, unsigned long long* __restrict__ out) {
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v = fmax(v, fabs(G[i]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(v));
+}
+
+// sets bit 1 of *flag when an entry's worst rounding error (err_units of 2^-S) could reach 1e-12 of
+// the largest near block entry times C (ref_scale * gmax): pass 2 then adds nothing
+__global__ void coarse_flag_kernel(const unsigned long long* __restrict__ gmax_bits, double err, double ref_scale,
+                                   int force, int* __restrict__ flag) {
+  const double gmax = __longlong_as_double((long long)*gmax_bits);
+  if (force || err > ref_scale * gmax) atomicOr(flag, 2);
 }
 
 void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
@@ -1000,13 +1037,16 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
   if (herr) throw Error(-1, "a Morton block of 32 cells touches more than 64 DoFs (mesh too irregular)");
-  const double dmin = B.dmin, jmax = B.jmax;
-  // |entry| <= vmax^2 * C * Jmax^2 * (1/6)^2 * dmin^(-(d+2s)) (sum of w*lambda over the reference
-  // triangle = 1/6; at most vmax cells around a vertex); scale: that bound -> 2^54
+  const double dmin = B.dmin;
+  // one pair's |contribution| <= C * (1/6)^2 * J_K J_L dist^(-(d+2s)) <= C beta / 36 (sum of
+  // w*lambda over the reference triangle = 1/6; beta_kernel); an entry sums at most vmax^2 pairs
+  // (vmax cells around a vertex).  Scale: vmax^2 * that -> 2^61, so every contribution stays below
+  // lim = 2^62 / vmax^2 (checked in the kernels) and every sum below 2^62.
   const double e = -2.0 * ex;                      // d + 2s
   const double vmax = (double)MAX_VALENCE;
-  const double bound = dmin < 1e299 ? vmax * vmax * Cds * jmax * jmax / 36.0 * std::pow(dmin, -e) : 1.0;
-  int S = 54 - (int)std::ceil(std::log2(std::max(bound, 1e-300)));
+  const double beta = B.beta;
+  const double bound = beta > 0.0 ? vmax * vmax * Cds * beta / 36.0 : 1.0;
+  int S = 61 - (int)std::ceil(std::log2(std::max(bound, 1e-300)));
   S = std::max(-1000, std::min(1000, S));
   const double scale = std::ldexp(1.0, S);
   info.scale_exp = S;
@@ -1025,7 +1065,13 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
     const char* v = getenv("FRACLAP_EXACT_RANGE");
     return !(v && std::string(v) == "0");
   }();
-  if (exact_range)
+  // FRACLAP_CROSS2D_KUNI=0 (diagnostic): no block-uniform orders, every pair gets its own order
+  static const bool kuni_off = [] {
+    const char* v = getenv("FRACLAP_CROSS2D_KUNI");
+    return v && std::string(v) == "0";
+  }();
+  if (kuni_off) clear_kuni_kernel<<<(unsigned)((ncand + 255) / 256), 256, 0, st>>>(raw.p, nflag.p, ncand), note_launch();
+  if (exact_range && !kuni_off)
     cross_refine_kernel<<<(unsigned)((ncand * 32 + 255) / 256), 256, 0, st>>>(oc, m, bcells.p, bstat.p, ncand, raw.p,
                                                                             nflag.p),
         note_launch();
@@ -1144,6 +1190,24 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   near_pairs_build(m, t, oc, ex, e4, near_keys.p, nkeys, near, evals_near ? evals_near : evals, st);
   near_keys.free();
   if (t_near) FL_CUDA(cudaEventRecord(t_near, st));
+  // ---- is the fixed-point unit fine enough?  An entry's rounding error is at most vmax^2 / 2
+  // units of 2^-S; the largest near block entry (times C) is of the size of A's significant
+  // off-diagonal entries.  When the units could reach 1e-12 of it (cells sharing no vertex that
+  // almost touch: the bound above is then far above every real contribution) pass 2 adds nothing
+  // (bit 1 of ovf) and the caller assembles the cross term with the DoF-tile kernel (exact double
+  // sums, any mesh).
+  if (near.n > 0) {
+    static const bool force_fb = [] {              // FRACLAP_CROSS2D_FALLBACK=1: take the fallback (test switch)
+      const char* v = getenv("FRACLAP_CROSS2D_FALLBACK");
+      return v && std::string(v) == "1";
+    }();
+    DBuf<unsigned long long> gmax(1);
+    FL_CUDA(cudaMemsetAsync(gmax.p, 0, sizeof(unsigned long long), st));
+    absmax_kernel<<<4 * sms, 256, 0, st>>>(near.G.p, (int64_t)near.n * 9, gmax.p), note_launch();
+    // decided on the device (no host synchronisation here): pass 2 returns at once when the flag is set
+    coarse_flag_kernel<<<1, 1, 0, st>>>(gmax.p, 0.5 * vmax * vmax * std::ldexp(1.0, -S), 1e-12 * Cds, force_fb ? 1 : 0,
+                                        ovf.p), note_launch();
+  }
   // ---- pass 2: every block pair
   FL_CUDA(cudaMemsetAsync(queue.p, 0, sizeof(int), st));
   xa.bpairs = rest; xa.nbp = nrest; xa.queue = queue.p;
@@ -1178,6 +1242,10 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   int hovf = 0;
   FL_CUDA(cudaMemcpyAsync(&hovf, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
+  if (hovf & 2) {
+    info.fallback = 1;
+    return;
+  }
   if (hovf) throw Error(-5, "internal: a cross contribution exceeded the fixed-point bound");
 }
 

@@ -240,8 +240,10 @@ void near_pairs_build(const DevMesh& m, const DevTables& t, const OrderConsts& o
 // fl_cross2d.cu: the 2D cross term by cell-block pairs, exact fixed-point accumulation
 struct Cross2DInfo {
   int scale_exp = 0;          // contributions are accumulated as integers of 2^-scale_exp
-  double dmin = 0.0;          // smallest disjoint cell distance (the scale bound)
+  double dmin = 0.0;          // smallest disjoint cell distance
   int64_t block_pairs = 0, near_block_pairs = 0;
+  int fallback = 0;           // 1: the fixed-point unit is too coarse for this mesh, nothing was added to A
+                              // (the caller runs the DoF-tile cross kernel instead)
 };
 // Morton blocks of CB2D cells (sorted along the Morton curve of the centroids): per block its
 // cells, the sorted DoFs of its cells (<= 64) with each cell vertex's slot, a bounding circle and
@@ -261,6 +263,7 @@ struct Blocks2D {
   double dmin = 1e300;    // smallest distance of two cells sharing no vertex (second-ring scan)
   double jmax = 0.0;      // largest Jacobian
   double radmax = 0.0;    // largest cell radius (vertex - centroid)
+  double beta = 0.0;      // max_K J_K^2 d_K^(-(d+2s)), d_K the smallest distance from K to a cell sharing no vertex
 };
 constexpr int UNODES2D = 928;
 // the 2D tail's staging array of the orders 5-9: per block 32 * (25 + 36 + 49 + 64 + 81) nodes
@@ -321,7 +324,8 @@ __device__ __forceinline__ int block_uniform_order(const OrderConsts& oc, double
   const double c1 = fmin(fmax(ceil(hi + 1e-9), 2.0), (double)oc.cap_disjoint);
   return c0 == c1 ? (int)c0 : 0;
 }
-void build_blocks2d(const DevMesh& m, const DevTables& t, int row_begin, int row_end, Blocks2D& B, cudaStream_t st);
+void build_blocks2d(const DevMesh& m, const DevTables& t, double e /* d + 2s */, int row_begin, int row_end,
+                    Blocks2D& B, cudaStream_t st);
 void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& oc, double ex, int e4, double Cds,
                       const Blocks2D& B, int row_begin, int row_end, double* A, int64_t lda,
                       unsigned long long* evals, NearPairs& near, Cross2DInfo& info, cudaEvent_t t_disc,
