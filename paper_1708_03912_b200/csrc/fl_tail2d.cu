@@ -157,9 +157,13 @@ __global__ void hi_nodes_kernel(DevMesh m, const int* __restrict__ bcells, int n
   uhi[i] = y;
 }
 
-__global__ void jmax_kernel(DevMesh m, unsigned long long* __restrict__ jmax) {
+// sum of the Jacobians in units of jmax / 2^30 (an integer sum: the same whatever the order)
+__global__ void jsum_kernel(DevMesh m, double units, unsigned long long* __restrict__ jsum) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < m.nc) atomicMax(jmax, (unsigned long long)__double_as_longlong(m.geo[c].J));
+  unsigned long long v = c < m.nc ? (unsigned long long)__double2ll_ru(m.geo[c].J * units) : 0ull;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(jsum, v);
 }
 
 // sym4: an order-4 uniform block pair (P, Q) is evaluated once, by the CTA of min(P, Q); its
@@ -625,17 +629,21 @@ void launch_tail2d_blocks(const DevMesh& m, const DevTables& t, const OrderConst
     tail_refine_kernel<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, st>>>(oc, m, B.bcells.p, B.bstat.p, tflag.p, nb,
                                                                           kuni.p, red.p, run.p),
         note_launch();
-  jmax_kernel<<<(m.nc + 255) / 256, 256, 0, st>>>(m, red.p + 1), note_launch();
+  const double jmax = B.jmax;
+  jsum_kernel<<<(m.nc + 255) / 256, 256, 0, st>>>(m, jmax > 0.0 ? std::ldexp(1.0, 30) / jmax : 0.0, red.p + 1),
+      note_launch();
   unsigned long long hred[2];
   FL_CUDA(cudaMemcpyAsync(hred, red.p, sizeof(hred), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));
-  double dmin4, jmax;
+  double dmin4;
   std::memcpy(&dmin4, &hred[0], 8);
-  std::memcpy(&jmax, &hred[1], 8);
-  // |column sum| <= sum_K J_K / 2 * dmin4^(2 ex) <= nc * jmax / 2 * dmin4^(2 ex); scale: that -> 2^60
+  // |column sum| <= sum_K J_K / 2 * dmin4^(2 ex) (every target cell at most once per source node, at
+  // least dmin4 away; sum_K J_K / 2 = the area of the mesh, summed in integer units rounded up);
+  // scale: that -> 2^60
   double fxscale = 1.0;
   if (dmin4 < 1e299 && jmax > 0.0) {
-    const double bound = (double)m.nc * jmax * 0.5 * std::pow(dmin4, 2.0 * ex);
+    const double jsum = (double)hred[1] * jmax * std::ldexp(1.0, -30) * (1.0 + 1e-9);
+    const double bound = jsum * 0.5 * std::pow(dmin4, 2.0 * ex);
     int S = 60 - (int)std::ceil(std::log2(std::max(bound, 1e-300)));
     S = std::max(-1000, std::min(1000, S));
     fxscale = std::ldexp(1.0, S);

@@ -40,6 +40,12 @@ def make_mesh(kind, N):
         V[inner] += rng.uniform(-0.3 / N, 0.3 / N, size=(int(inner.sum()), 2))
         cells = np.array(base.cells)[rng.permutation(len(base.cells))]
         return M.finish_polygon_mesh(V, [tuple(int(v) for v in c) for c in cells])
+    if kind == "graded2d":
+        # the unit square graded toward the origin (vertex (x, y) -> (x^1.7, y^1.7)): cell diameters
+        # spread over ~1.5 decades, anisotropic cells along the axes
+        base = M.build_unit_square_mesh(N)
+        V = np.array(base.vertices, dtype=np.float64) ** 1.7
+        return M.finish_polygon_mesh(V, [tuple(int(v) for v in c) for c in base.cells])
     raise ValueError(kind)
 
 
