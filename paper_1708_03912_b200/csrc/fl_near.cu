@@ -15,13 +15,14 @@ constexpr int NW = 8;          // warps per CTA
 constexpr int NMAXN = 81;      // max k^d nodes (2D cap 9; 1D k <= 32)
 
 // One pair's 3x3 block: lane l takes the x nodes l, l + 32, l + 64 (NX of them) and sweeps all y
-// nodes, which every lane reads at the same address (broadcast shared loads); NX = 1 keeps two
-// accumulator sets (even / odd y) for independent chains.  Fixed summation order.
+// nodes, which every lane reads at the same address (broadcast shared loads); NX = 1 keeps four
+// accumulator sets (y mod 4) for independent chains.  Fixed summation order.
 template <int D, int E4, int NX>
 __device__ __forceinline__ void near_pair(const CellGeo& A, const double* __restrict__ tab, RuleRef rr, int nn,
                                           const double4* __restrict__ syw, const double* __restrict__ sw2, int lane,
                                           double ex, double (&Gm)[3][3]) {
-  double X0[NX], X1[NX], t[NX][2][3];
+  constexpr int HS = NX == 1 ? 4 : 1;          // accumulator sets (independent chains when a lane has one x)
+  double X0[NX], X1[NX], t[NX][HS][3];
   bool ok[NX];
 #pragma unroll
   for (int u = 0; u < NX; ++u) {
@@ -36,7 +37,7 @@ __device__ __forceinline__ void near_pair(const CellGeo& A, const double* __rest
       X1[u] = A.p[0][1] + (nx[0] * (A.p[1][1] - A.p[0][1]) + nx[1] * (A.p[2][1] - A.p[0][1]));
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) t[u][h][0] = t[u][h][1] = t[u][h][2] = 0.0;
+    for (int h = 0; h < HS; ++h) t[u][h][0] = t[u][h][1] = t[u][h][2] = 0.0;
   }
   auto eval = [&](int y, int h) {
     const double4 Y = syw[y];
@@ -59,12 +60,14 @@ __device__ __forceinline__ void near_pair(const CellGeo& A, const double* __rest
   };
   int y = 0;
   if (NX == 1) {
-#pragma unroll 2
-    for (; y + 1 < nn; y += 2) {
+#pragma unroll 1
+    for (; y + 3 < nn; y += 4) {
       eval(y, 0);
-      eval(y + 1, 1);
+      eval(y + 1, HS > 1 ? 1 : 0);
+      eval(y + 2, HS > 2 ? 2 : 0);
+      eval(y + 3, HS > 3 ? 3 : 0);
     }
-    if (y < nn) eval(y, 0);
+    for (; y < nn; ++y) eval(y, 0);
   } else {
 #pragma unroll 2
     for (; y < nn; ++y) eval(y, 0);
@@ -73,7 +76,9 @@ __device__ __forceinline__ void near_pair(const CellGeo& A, const double* __rest
   for (int u = 0; u < NX; ++u) {
     if (!ok[u]) continue;
     const double* nx = tab + (size_t)(rr.off + lane + 32 * u) * NODE;
-    const double t0 = t[u][0][0] + t[u][1][0], t1 = t[u][0][1] + t[u][1][1], t2 = t[u][0][2] + t[u][1][2];
+    double t0 = t[u][0][0], t1 = t[u][0][1], t2 = t[u][0][2];
+#pragma unroll
+    for (int h = 1; h < HS; ++h) { t0 += t[u][h][0]; t1 += t[u][h][1]; t2 += t[u][h][2]; }
 #pragma unroll
     for (int a = 0; a <= D; ++a) {
       const double lx = nx[3 + a];
