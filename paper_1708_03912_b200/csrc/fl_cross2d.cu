@@ -735,6 +735,11 @@ __device__ __forceinline__ void u_stage(const UArgs& a, UBuf& B, int4 pr, int ti
   }
 }
 
+#ifndef FL_XU_YUNROLL
+#define FL_XU_YUNROLL 3
+#endif
+constexpr int XU_YUNROLL = FL_XU_YUNROLL;      // y-loop unroll of the k = 3, 4 blocks
+
 // partial 3x3 block from the NX x nodes x0, x0 + XS, ... of row cell i against all NN y nodes of
 // column cell j (node-major staging: node r of cell c at [r * 32 + c])
 template <int E4, int NN, int NX, int XS>
@@ -749,7 +754,7 @@ __device__ __forceinline__ void blk_part_nm(const double2* __restrict__ Xb, cons
     X1[u] = X.y;
     t[u][0] = t[u][1] = t[u][2] = 0.0;
   }
-#pragma unroll(NN <= 4 ? NN : 3)
+#pragma unroll(NN <= 4 ? NN : XU_YUNROLL)
   for (int y = 0; y < NN; ++y) {
     const double2 Y = Yb[y * CB + j];
     const double w0 = w[y][0], w1 = w[y][1], w2 = w[y][2];
