@@ -779,8 +779,45 @@ __device__ __forceinline__ void blk_part_nm(const double2* __restrict__ Xb, cons
   }
 }
 
+// w * lambda_a of the rules k = 2, 3, 4 (the same numbers for every assembly: reference-element
+// rules) in constant memory: the FP64 instructions of blk_regy read them as constant-bank operands
+__constant__ double c_wl[NPRE2 * 3];
+
+// Whole 3x3 block of (row cell i, the lane's column cell) for k = 2, 3: the column cell's NN mapped
+// nodes stay in registers for every row cell of the block pair (Yr, loaded once per pair), the row
+// cell's nodes are broadcast one at a time, the rule weights come from constant memory — no shared
+// load inside the y sweep.  Two accumulator sets (even / odd y) shorten the FMA chains.
+template <int E4, int NN>
+__device__ __forceinline__ void blk_regy(const double2* __restrict__ Xb, const double2 (&Yr)[9], int i, int wo,
+                                         double ex, double (&M)[3][3]) {
+#pragma unroll 1
+  for (int x = 0; x < NN; ++x) {
+    const double2 X = Xb[x * CB + i];
+    double t[2][3] = {};
+#pragma unroll
+    for (int y = 0; y < NN; ++y) {
+      const double d0 = X.x - Yr[y].x, d1 = X.y - Yr[y].y;
+      const double v = kpow<E4>(fma(d1, d1, d0 * d0), ex);
+      t[y & 1][0] = fma(v, c_wl[(wo + y) * 3 + 0], t[y & 1][0]);
+      t[y & 1][1] = fma(v, c_wl[(wo + y) * 3 + 1], t[y & 1][1]);
+      t[y & 1][2] = fma(v, c_wl[(wo + y) * 3 + 2], t[y & 1][2]);
+    }
+    const double t0 = t[0][0] + t[1][0], t1 = t[0][1] + t[1][1], t2 = t[0][2] + t[1][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double wa = c_wl[(wo + x) * 3 + a];
+      M[a][0] = fma(wa, t0, M[a][0]);
+      M[a][1] = fma(wa, t1, M[a][1]);
+      M[a][2] = fma(wa, t2, M[a][2]);
+    }
+  }
+}
+
 #ifndef FL_XU_MINB
 #define FL_XU_MINB 2
+#endif
+#ifndef FL_XU_REGY
+#define FL_XU_REGY 0
 #endif
 template <int E4>
 __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, const double* __restrict__ wl_g) {
@@ -810,13 +847,23 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
     const UBuf& B = S.b[bsel];
     const int k = pr.z, nP = pr.w & 0xffff, nQ = pr.w >> 16;
     const bool in_tile = nP * nQ <= TCAP;
+    double2 Yr[9];                               // the lane's column cell nodes (k = 2, 3)
+    if (FL_XU_REGY && k <= 3) {
+#pragma unroll
+      for (int y = 0; y < 9; ++y)
+        if (y < k * k) Yr[y] = B.nd[1][y * CB + lane];
+    }
 #pragma unroll 1
     for (int i = wid; i < CB; i += X2T / 32) {
       const int j = lane;
       const double JJ = B.J[0][i] * B.J[1][j];
       if (JJ == 0.0) continue;                   // an empty slot of a partial block
       double M[3][3] = {};
-      if (k == 2) {
+      if (FL_XU_REGY && k == 2) {
+        blk_regy<E4, 4>(B.nd[0], Yr, i, poff(2), a.ex, M);
+      } else if (FL_XU_REGY && k == 3) {
+        blk_regy<E4, 9>(B.nd[0], Yr, i, poff(3), a.ex, M);
+      } else if (k == 2) {
         blk_part_nm<E4, 4, 4, 1>(B.nd[0], B.nd[1], i, j, S.wl + poff(2), 0, a.ex, M);
       } else if (k == 3) {
 #pragma unroll 1
@@ -1038,6 +1085,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   }
   DBuf<double> wl(NPRE2 * 3);
   FL_CUDA(cudaMemcpyAsync(wl.p, hw.data(), hw.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  FL_CUDA(cudaMemcpyToSymbolAsync(c_wl, hw.data(), hw.size() * sizeof(double), 0, cudaMemcpyHostToDevice, st));
   int herr = 0;
   FL_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   FL_CUDA(cudaStreamSynchronize(st));

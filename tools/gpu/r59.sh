@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python tools/assemble_once.py c5 --reps 3 > gpurun_out/r59_c5.log 2>&1
+timeout 300 python tools/assemble_once.py c4a --reps 2 > gpurun_out/r59_c4a.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "2d or block or large or row_block or c3 or sampled or c5 or jitter or irregular" > gpurun_out/r59_t.log 2>&1
+echo "rc=$?" >> gpurun_out/r59_t.log
