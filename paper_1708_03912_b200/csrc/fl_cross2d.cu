@@ -670,6 +670,29 @@ __global__ void block_unodes_kernel(const int* __restrict__ bcells, const double
   }
 }
 
+// Column-DoF lists of every block: for DoF slot c of block b the (cell slot j, vertex v) pairs with
+// slot(j, v) == c, ascending, packed in 16 bytes: byte 0 = count (<= 15), then j * 3 + v.
+__global__ void block_colmap_kernel(const int* __restrict__ us, int nb, uint4* __restrict__ ucol, int* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb * BRMAX) return;
+  const int b = i / BRMAX, c = i % BRMAX;
+  unsigned char e[16] = {};
+  int n = 0;
+  for (int j = 0; j < CB; ++j) {
+    const int pk = us[b * CB + j];
+    for (int v = 0; v < 3; ++v)
+      if (((pk >> (8 * v)) & 0xff) == c) {
+        if (n < 15) e[1 + n] = (unsigned char)(j * 3 + v);
+        ++n;
+      }
+  }
+  if (n > 15) atomicAdd(err, 1);
+  e[0] = (unsigned char)min(n, 15);
+  uint4 o;
+  memcpy(&o, e, 16);
+  ucol[i] = o;
+}
+
 struct UArgs {
   const int4* bpairs;                 // (P, Q, k, nP | nQ << 16)
   int nbp;
@@ -677,6 +700,7 @@ struct UArgs {
   const double* uj;
   const int* us;
   const int* bdofs;
+  const uint4* ucol;                  // per block and DoF slot: count + (cell * 3 + vertex) entries (block_colmap_kernel)
   double ex, cs, lim;
   long long limq;                     // lim as an integer: |scaled contribution| < limq
   unsigned long long* A;
@@ -691,9 +715,11 @@ struct UBuf {
   double J[2][CB];
   int sl[2][CB];
   int dof[2][BRMAX];
+  uint4 col[BRMAX];                   // the column block's DoF -> (cell, vertex) lists
 };
 struct UShared {
   UBuf b[2];
+  double mx[X2T / 32][9][CB];         // per warp: the 32 lanes' scaled 3x3 blocks (column-DoF exchange)
   unsigned long long tile[TCAP];
   double wl[NPRE2][3];
   unsigned long long evals;
@@ -709,7 +735,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // issue the copies of block pair `pr` into buffer B (every thread its share of 16-byte chunks)
 __device__ __forceinline__ void u_stage(const UArgs& a, UBuf& B, int4 pr, int tid) {
   const int k = pr.z, nn = CB * k * k;           // nodes per block (16-byte chunks)
-  const int tot = 2 * nn + 2 * 16 + 2 * 8 + 2 * 16;
+  const int tot = 2 * nn + 2 * 16 + 2 * 8 + 2 * 16 + BRMAX;
   for (int c = tid; c < tot; c += X2T) {
     int x = c;
     if (x < 2 * nn) {
@@ -730,8 +756,13 @@ __device__ __forceinline__ void u_stage(const UArgs& a, UBuf& B, int4 pr, int ti
       continue;
     }
     x -= 16;
-    const int side = x >= 16, r = x - side * 16;
-    cp_async16(&B.dof[side][4 * r], a.bdofs + (int64_t)(side ? pr.y : pr.x) * BRMAX + 4 * r);
+    if (x < 32) {
+      const int side = x >= 16, r = x - side * 16;
+      cp_async16(&B.dof[side][4 * r], a.bdofs + (int64_t)(side ? pr.y : pr.x) * BRMAX + 4 * r);
+      continue;
+    }
+    x -= 32;
+    cp_async16(&B.col[x], a.ucol + (int64_t)pr.y * BRMAX + x);
   }
 }
 
@@ -819,6 +850,9 @@ __device__ __forceinline__ void blk_regy(const double2* __restrict__ Xb, const d
 #ifndef FL_XU_REGY
 #define FL_XU_REGY 0
 #endif
+#ifndef FL_XU_COLDOF
+#define FL_XU_COLDOF 0
+#endif
 template <int E4>
 __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, const double* __restrict__ wl_g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -857,8 +891,15 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
     for (int i = wid; i < CB; i += X2T / 32) {
       const int j = lane;
       const double JJ = B.J[0][i] * B.J[1][j];
+#if FL_XU_COLDOF
+      if (B.J[0][i] == 0.0) continue;            // an empty row slot (warp-uniform)
+      double M[3][3] = {};
+      if (JJ == 0.0) {                           // an empty column slot: zeros into the exchange
+      } else
+#else
       if (JJ == 0.0) continue;                   // an empty slot of a partial block
       double M[3][3] = {};
+#endif
       if (FL_XU_REGY && k == 2) {
         blk_regy<E4, 4>(B.nd[0], Yr, i, poff(2), a.ex, M);
       } else if (FL_XU_REGY && k == 3) {
@@ -873,6 +914,57 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
         for (int xs = 0; xs < 4; ++xs)
           blk_part_nm<E4, 16, 4, 4>(B.nd[0], B.nd[1], i, j, S.wl + poff(4), xs, a.ex, M);
       }
+#if FL_XU_COLDOF
+      // column-DoF exchange: the lanes' scaled blocks go to shared memory, then lane c sums the
+      // (cell, vertex) entries of column DoF c in their fixed list order — one rounding and three
+      // tile adds per (row cell, column DoF) instead of nine per cell pair, no address conflicts
+      // inside the warp
+      const int spk = B.sl[0][i];
+      {
+        const double sc = JJ * a.cs;
+        double(*mx)[CB] = S.mx[wid];
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int y = 0; y < 3; ++y) mx[x * 3 + y][lane] = M[x][y] * sc;
+      }
+      __syncwarp();
+      bool bad = false;
+      for (int c = lane; c < nQ; c += 32) {
+        const uint4 cm = B.col[c];
+        const unsigned char* e = reinterpret_cast<const unsigned char*>(&cm);
+        const int n = e[0];
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int m = 0; m < n; ++m) {
+          const int jv = e[1 + m], jj = jv / 3, v = jv - jj * 3;
+          s0 += S.mx[wid][v][jj];
+          s1 += S.mx[wid][3 + v][jj];
+          s2 += S.mx[wid][6 + v][jj];
+        }
+        const double sv[3] = {s0, s1, s2};
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          const int si = (spk >> (8 * x)) & 0xff;
+          if (si == 0xff) continue;
+          const long long qs = __double2ll_rn(sv[x]);
+          // at most 15 contributions, each below limq
+          bad |= (unsigned long long)(qs + 16 * a.limq) > 32ull * (unsigned long long)a.limq;
+          const unsigned long long q = (unsigned long long)qs;
+          if (!q) continue;
+          if (in_tile) {
+            tile_add(&S.tile[si * nQ + c], q);
+          } else {
+            const int gi = B.dof[0][si], gj = B.dof[1][c];
+            if (gi >= a.r0 && gi < a.r1) atomicAdd(&a.A[(int64_t)(gi - a.r0) * a.lda + gj], q);
+            if (gj >= a.r0 && gj < a.r1) atomicAdd(&a.A[(int64_t)(gj - a.r0) * a.lda + gi], q);
+          }
+        }
+      }
+      __syncwarp();                              // mx is rewritten for the next row cell
+      if (bad) atomicOr(a.ovf, 1);
+      if (JJ != 0.0) my += (unsigned long long)(k * k) * (k * k);
+      continue;
+#else
       const int spk = B.sl[0][i], tpk = B.sl[1][j];
       const double sc = JJ * a.cs;
       bool bad = false;
@@ -896,6 +988,7 @@ __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, c
           }
         }
       }
+#endif
       if (bad) atomicOr(a.ovf, 1);
       my += (unsigned long long)(k * k) * (k * k);
     }
@@ -1022,6 +1115,8 @@ void build_blocks2d(const DevMesh& m, const DevTables& t, double e, int row_begi
   block_unodes_kernel<<<(unsigned)(((int64_t)nb * UNODES + 255) / 256), 256, 0, st>>>(B.bcells.p, B.nodes.p, nb, m,
                                                                                     B.slot.p, B.un.p, B.uj.p, B.us.p),
       note_launch();
+  B.ucol.alloc((size_t)nb * BRMAX);
+  block_colmap_kernel<<<(nb * BRMAX + 255) / 256, 256, 0, st>>>(B.us.p, nb, B.ucol.p, B.err.p), note_launch();
   // smallest distance of two disjoint cells (second-ring scan), largest Jacobian and cell radius
   DBuf<unsigned long long> bnd(4);
   unsigned long long init[4] = {0ull, 0ull, 0ull, 0ull};
@@ -1275,7 +1370,7 @@ void assemble_cross2d(const DevMesh& m, const DevTables& t, const OrderConsts& o
   xa.nearH = near.hkey.p; xa.nearI = near.hidx.p; xa.hmask = near.hmask; xa.nearG = near.G.p;
   if (nuni > 0) {
     UArgs ua{};
-    ua.bpairs = uorder; ua.nbp = nuni; ua.un = un.p; ua.uj = uj.p; ua.us = us.p; ua.bdofs = bdofs.p;
+    ua.bpairs = uorder; ua.nbp = nuni; ua.un = un.p; ua.uj = uj.p; ua.us = us.p; ua.bdofs = bdofs.p; ua.ucol = B.ucol.p;
     ua.ex = ex; ua.cs = xa.cs; ua.lim = xa.lim; ua.limq = (long long)xa.lim; ua.A = Ai; ua.lda = lda; ua.r0 = row_begin; ua.r1 = row_end;
     ua.evals = evals; ua.ovf = ovf.p;
     const size_t usm = sizeof(UShared);

@@ -260,6 +260,7 @@ struct Blocks2D {
   DBuf<double2> nodes, un;
   DBuf<double> uj;
   DBuf<int> us;
+  DBuf<uint4> ucol;       // per block and DoF slot: count + (cell slot * 3 + vertex) entries, 16 bytes
   double dmin = 1e300;    // smallest distance of two cells sharing no vertex (second-ring scan)
   double jmax = 0.0;      // largest Jacobian
   double radmax = 0.0;    // largest cell radius (vertex - centroid)
