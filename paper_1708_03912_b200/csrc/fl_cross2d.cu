@@ -670,6 +670,9 @@ __global__ void block_unodes_kernel(const int* __restrict__ bcells, const double
   }
 }
 
+#ifndef FL_XU_COLDOF
+#define FL_XU_COLDOF 0      // 1: column-DoF exchange epilogue in cross2d_uni_kernel (measured neutral)
+#endif
 // Column-DoF lists of every block: for DoF slot c of block b the (cell slot j, vertex v) pairs with
 // slot(j, v) == c, ascending, packed in 16 bytes: byte 0 = count (<= 15), then j * 3 + v.
 __global__ void block_colmap_kernel(const int* __restrict__ us, int nb, uint4* __restrict__ ucol, int* __restrict__ err) {
@@ -715,11 +718,15 @@ struct UBuf {
   double J[2][CB];
   int sl[2][CB];
   int dof[2][BRMAX];
+#if FL_XU_COLDOF
   uint4 col[BRMAX];                   // the column block's DoF -> (cell, vertex) lists
+#endif
 };
 struct UShared {
   UBuf b[2];
+#if FL_XU_COLDOF
   double mx[X2T / 32][9][CB];         // per warp: the 32 lanes' scaled 3x3 blocks (column-DoF exchange)
+#endif
   unsigned long long tile[TCAP];
   double wl[NPRE2][3];
   unsigned long long evals;
@@ -735,7 +742,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // issue the copies of block pair `pr` into buffer B (every thread its share of 16-byte chunks)
 __device__ __forceinline__ void u_stage(const UArgs& a, UBuf& B, int4 pr, int tid) {
   const int k = pr.z, nn = CB * k * k;           // nodes per block (16-byte chunks)
-  const int tot = 2 * nn + 2 * 16 + 2 * 8 + 2 * 16 + BRMAX;
+  const int tot = 2 * nn + 2 * 16 + 2 * 8 + 2 * 16 + (FL_XU_COLDOF ? BRMAX : 0);
   for (int c = tid; c < tot; c += X2T) {
     int x = c;
     if (x < 2 * nn) {
@@ -761,8 +768,10 @@ __device__ __forceinline__ void u_stage(const UArgs& a, UBuf& B, int4 pr, int ti
       cp_async16(&B.dof[side][4 * r], a.bdofs + (int64_t)(side ? pr.y : pr.x) * BRMAX + 4 * r);
       continue;
     }
+#if FL_XU_COLDOF
     x -= 32;
     cp_async16(&B.col[x], a.ucol + (int64_t)pr.y * BRMAX + x);
+#endif
   }
 }
 
@@ -850,9 +859,7 @@ __device__ __forceinline__ void blk_regy(const double2* __restrict__ Xb, const d
 #ifndef FL_XU_REGY
 #define FL_XU_REGY 0
 #endif
-#ifndef FL_XU_COLDOF
-#define FL_XU_COLDOF 0
-#endif
+
 template <int E4>
 __global__ void __launch_bounds__(X2T, FL_XU_MINB) cross2d_uni_kernel(UArgs a, const double* __restrict__ wl_g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1115,8 +1122,10 @@ void build_blocks2d(const DevMesh& m, const DevTables& t, double e, int row_begi
   block_unodes_kernel<<<(unsigned)(((int64_t)nb * UNODES + 255) / 256), 256, 0, st>>>(B.bcells.p, B.nodes.p, nb, m,
                                                                                     B.slot.p, B.un.p, B.uj.p, B.us.p),
       note_launch();
+#if FL_XU_COLDOF
   B.ucol.alloc((size_t)nb * BRMAX);
   block_colmap_kernel<<<(nb * BRMAX + 255) / 256, 256, 0, st>>>(B.us.p, nb, B.ucol.p, B.err.p), note_launch();
+#endif
   // smallest distance of two disjoint cells (second-ring scan), largest Jacobian and cell radius
   DBuf<unsigned long long> bnd(4);
   unsigned long long init[4] = {0ull, 0ull, 0ull, 0ull};
