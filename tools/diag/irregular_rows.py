@@ -6,8 +6,11 @@ sys.path.insert(0, ROOT); sys.path.insert(0, ROOT + "/tests")
 from conftest import make_mesh
 from paper_1708_03912_b200 import mesh as M, assembly as A
 from oracle import fraclap_oracle as O
-for kind, N, s in (("jitter2d", 32, 0.5), ("jitter2d", 40, 0.75), ("graded2d", 32, 0.5), ("graded2d", 40, 0.25),
-                   ("graded2d", 48, 0.75), ("square2d", 40, 0.5)):
+CASES = (("jitter2d", 32, 0.5), ("jitter2d", 40, 0.75), ("graded2d", 32, 0.5), ("graded2d", 40, 0.25),
+         ("graded2d", 48, 0.75), ("square2d", 40, 0.5))
+if len(sys.argv) > 1:          # kind:N:s ...
+    CASES = tuple((a.split(":")[0], int(a.split(":")[1]), float(a.split(":")[2])) for a in sys.argv[1:])
+for kind, N, s in CASES:
     mesh = make_mesh(kind, N)
     dm = M.DofMap(mesh, s)
     rows = [0, 3, dm.n // 3, dm.n // 2 + 1, dm.n - 2]
